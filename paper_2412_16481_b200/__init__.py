@@ -1,0 +1,19 @@
+"""B200-native Flash3D hot path: PSH bucketing, bucket-swin attention,
+in-bucket pooling, and the row scatter/gather around them.
+
+Drop-in for the reference package ``bucketswin`` (same module names,
+signatures, defaults and exception classes) — ``import
+paper_2412_16481_b200 as bucketswin``.  Compute runs in hand-written sm_100a
+CUDA (libf3d.so, include/f3d.h); there is no CPU fallback.
+"""
+
+from .bucketing import (BucketAssignment, ProbeSchedule, assign_buckets,
+                        assign_buckets_two_stage, compute_bucket_base,
+                        default_probe_schedule, gather, scatter)
+from .errors import (ConfigError, EmptyInputError, IntegrityError, NumericError,
+                     ParseError, RangeError)
+from .geometry import PointCloud, VoxelGrid, synth_cloud, voxelize
+from .hashing import (HASH_KINDS, HashConfig, hash_bucket, morton_encode,
+                      remap_nonnegative)
+
+__version__ = "0.1.0"

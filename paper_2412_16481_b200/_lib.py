@@ -1,0 +1,119 @@
+"""ctypes binding of libf3d.so (include/f3d.h) and device-array plumbing.
+
+The library is built in-tree by ``make -C paper_2412_16481_b200/csrc`` (or
+``__graft_entry__.build()``).  There is no CPU fallback: if the shared
+library or a CUDA device is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from .errors import (ConfigError, EmptyInputError, IntegrityError, NumericError,
+                     RangeError)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libf3d.so")
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_INT = ctypes.c_int
+_F64 = ctypes.c_double
+_SZ = ctypes.c_size_t
+
+# name -> (restype, argtypes); mirrors include/f3d.h
+SIGNATURES = {
+    "f3d_abi_version": (_INT, []),
+    "f3d_last_error": (ctypes.c_char_p, []),
+    "f3d_voxelize": (_INT, [_P, _I64, _P, _F64, _P, _P]),
+    "f3d_remap_nonnegative": (_INT, [_P, _P, _I64, _I32, _P, _P, _P]),
+    "f3d_hash_bucket": (_INT, [_P, _I64, _INT, _I32, _I64, _INT, _P, _P, _P, _P]),
+    "f3d_morton_encode": (_INT, [_P, _I64, _INT, _P, _P, _P]),
+    "f3d_voxel_hash": (_INT, [_P, _P, _I64, _I32, _P, _F64, _INT, _I32, _I64, _INT, _P, _P, _P,
+                              _P, _P]),
+    "f3d_psh_workspace_size": (_SZ, [_I64, _I32, _I32]),
+    "f3d_psh_assign": (_INT, [_P, _P, _P, _I64, _I32, _I32, _I32, _INT, _I64, _INT, _INT, _P,
+                              _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "f3d_validate_workspace_size": (_SZ, [_I64, _I64]),
+    "f3d_validate_assignment": (_INT, [_P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P]),
+    "f3d_scatter_rows": (_INT, [_P, _P, _I64, _I64, _P, _P]),
+    "f3d_gather_rows": (_INT, [_P, _P, _I64, _I64, _P, _P]),
+}
+
+_lib = None
+
+
+def load():
+    """Load libf3d.so and bind every declared symbol (raises if absent)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `make -C {os.path.join(_HERE, 'csrc')}` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+_ERRS = {1: ConfigError, 2: RangeError, 3: IntegrityError, 5: EmptyInputError, 6: NumericError}
+
+
+def call(name, *args):
+    """Invoke an f3d_* entry point and map a non-zero status to the
+    reference exception classes (bw/errors.py)."""
+    st = getattr(load(), name)(*args)
+    if st != 0:
+        msg = load().f3d_last_error().decode(errors="replace")
+        if st == 4:
+            raise RuntimeError(f"{name}: {msg}")
+        raise _ERRS.get(st, RuntimeError)(f"{name} failed (status {st}) {msg}".strip())
+    return st
+
+
+# ------------------------------------------------------------ device plumbing
+
+def device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2412_16481_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream():
+    return _P(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return None if t is None else _P(t.data_ptr())
+
+
+def is_host(x) -> bool:
+    """True when the caller passed host data (numpy / lists / CPU tensors):
+    results are then handed back as numpy, like the reference."""
+    return not (isinstance(x, torch.Tensor) and x.is_cuda)
+
+
+def to_dev(x, dtype) -> torch.Tensor:
+    """Any array-like -> contiguous CUDA tensor of dtype."""
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device(), dtype=dtype).contiguous()
+    arr = np.asarray(x)
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(device=device(), dtype=dtype)
+
+
+def out(t: torch.Tensor, host: bool):
+    return t.cpu().numpy() if host else t
+
+
+def empty(shape, dtype):
+    return torch.empty(shape, dtype=dtype, device=device())

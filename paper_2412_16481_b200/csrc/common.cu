@@ -1,0 +1,29 @@
+// Library-wide state: error text, device properties.
+#include <cstdio>
+#include <cstring>
+
+#include "f3d_common.cuh"
+
+static thread_local char g_last_error[512] = "";
+
+void f3d_set_last_cuda_error(cudaError_t e) {
+    snprintf(g_last_error, sizeof(g_last_error), "CUDA error %d: %s", (int)e,
+             cudaGetErrorString(e));
+}
+
+int f3d_num_sms() {
+    static int sms[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (sms[dev] == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        sms[dev] = v > 0 ? v : 148;
+    }
+    return sms[dev];
+}
+
+extern "C" int f3d_abi_version(void) { return 1; }
+
+extern "C" const char* f3d_last_error(void) { return g_last_error; }

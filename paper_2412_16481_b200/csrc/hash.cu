@@ -1,0 +1,278 @@
+// Voxelize, per-batch remap, range statistics and bucket hash (HBM-bound).
+//
+// bw/geometry.py:69-72   voxelize: floor((c - origin) / size), IEEE f64 ops
+// bw/hashing.py:128-149  remap_nonnegative: subtract the per-batch axis minimum
+// bw/hashing.py:60-125   _check_range + morton_encode + hash_bucket
+#include <climits>
+
+#include "f3d_common.cuh"
+
+namespace f3d {
+namespace hashk {
+
+constexpr int kThreads = 256;
+
+struct Origin {
+    double o[3];
+};
+
+// floor((c - o) / vs) with no contraction: __dsub_rn then __ddiv_rn.
+__device__ __forceinline__ long long vox1(double c, double o, double vs) {
+    return (long long)floor(__ddiv_rn(__dsub_rn(c, o), vs));
+}
+
+__device__ __forceinline__ void warp_min_max_atomic(long long v, long long* mn, long long* mx) {
+    long long a = v, b = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (mn) atomicMin(mn, a);
+        if (mx) atomicMax(mx, b);
+    }
+}
+
+__global__ void init_stats_kernel(int64_t* stats, int64_t* ws_min, int nmin) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (stats && i < 7) stats[i] = (i < 3) ? LLONG_MAX : LLONG_MIN;
+    if (ws_min && i < nmin) ws_min[i] = LLONG_MAX;
+}
+
+__global__ void voxelize_kernel(const double* __restrict__ coords, int64_t n, Origin org,
+                                double vs, int64_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t tot = 3 * n;
+    if (i < tot) out[i] = vox1(coords[i], org.o[i % 3], vs);
+}
+
+// per-(batch, axis) minimum; batch == null means one batch.
+__global__ void batch_min_kernel(const int64_t* __restrict__ vox, const int32_t* __restrict__ batch,
+                                 int64_t n, int nbatch, int64_t* ws_min) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = i < n;
+    long long v[3];
+    int b = 0;
+    if (ok) {
+        v[0] = vox[3 * i];
+        v[1] = vox[3 * i + 1];
+        v[2] = vox[3 * i + 2];
+        if (batch) b = batch[i];
+    } else {
+        v[0] = v[1] = v[2] = LLONG_MAX;
+    }
+    if (!batch || nbatch == 1) {
+        for (int a = 0; a < 3; ++a)
+            warp_min_max_atomic(v[a], (long long*)ws_min + a, nullptr);
+    } else if (ok && b >= 0 && b < nbatch) {
+        for (int a = 0; a < 3; ++a) atomicMin((long long*)ws_min + 3 * b + a, v[a]);
+    }
+}
+
+__global__ void remap_kernel(const int64_t* __restrict__ vox, const int32_t* __restrict__ batch,
+                             int64_t n, int nbatch, const int64_t* __restrict__ ws_min,
+                             int64_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * n) return;
+    const int64_t pt = i / 3;
+    const int a = (int)(i - 3 * pt);
+    int b = (batch && nbatch > 1) ? batch[pt] : 0;
+    if (b < 0 || b >= nbatch) b = 0;
+    out[i] = vox[i] - ws_min[3 * b + a];
+}
+
+struct HashArgs {
+    HashParams hp;
+    int want_quot;
+};
+
+__device__ __forceinline__ void hash_point(long long x, long long y, long long z, int64_t i,
+                                           const HashArgs& ha, int32_t* home, int32_t* vox32,
+                                           int64_t* stats, bool valid) {
+    const long long lim = 1ll << ha.hp.bits;
+    const bool in = x >= 0 && y >= 0 && z >= 0 && x < lim && y < lim && z < lim;
+    long long q = LLONG_MIN;
+    if (valid) {
+        int h = 0;
+        if (in) {
+            int64_t key;
+            if (ha.hp.kind <= XOR_DIV) key = x ^ y ^ z;
+            else key = morton3(x, y, z);
+            if (ha.hp.kind == XOR_DIV || ha.hp.kind == ZORDER_DIV) {
+                key = key / ha.hp.S_div;
+                q = key;
+            }
+            h = (int)(key % ha.hp.K);
+        }
+        home[i] = h;
+        if (vox32) {
+            vox32[3 * i] = (int)x;
+            vox32[3 * i + 1] = (int)y;
+            vox32[3 * i + 2] = (int)z;
+        }
+    }
+    if (stats) {
+        const long long BIGP = LLONG_MAX, BIGN = LLONG_MIN;
+        warp_min_max_atomic(valid ? x : BIGP, (long long*)stats + 0, nullptr);
+        warp_min_max_atomic(valid ? y : BIGP, (long long*)stats + 1, nullptr);
+        warp_min_max_atomic(valid ? z : BIGP, (long long*)stats + 2, nullptr);
+        warp_min_max_atomic(valid ? x : BIGN, nullptr, (long long*)stats + 3);
+        warp_min_max_atomic(valid ? y : BIGN, nullptr, (long long*)stats + 4);
+        warp_min_max_atomic(valid ? z : BIGN, nullptr, (long long*)stats + 5);
+        if (ha.want_quot) warp_min_max_atomic(valid ? q : BIGN, nullptr, (long long*)stats + 6);
+    }
+}
+
+__global__ void hash_kernel(const int64_t* __restrict__ vox, int64_t n, HashArgs ha,
+                            int32_t* __restrict__ home, int32_t* __restrict__ vox32,
+                            int64_t* stats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    long long x = 0, y = 0, z = 0;
+    if (valid) {
+        x = vox[3 * i];
+        y = vox[3 * i + 1];
+        z = vox[3 * i + 2];
+    }
+    hash_point(x, y, z, i, ha, home, vox32, stats, valid);
+}
+
+__global__ void morton_kernel(const int64_t* __restrict__ vox, int64_t n, int bits,
+                              int64_t* __restrict__ codes, int64_t* stats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    long long x = 0, y = 0, z = 0;
+    if (valid) {
+        x = vox[3 * i];
+        y = vox[3 * i + 1];
+        z = vox[3 * i + 2];
+        const uint64_t m = (1ull << bits) - 1;
+        codes[i] = morton3((int64_t)(x & m), (int64_t)(y & m), (int64_t)(z & m));
+    }
+    const long long BIGP = LLONG_MAX, BIGN = LLONG_MIN;
+    warp_min_max_atomic(valid ? x : BIGP, (long long*)stats + 0, nullptr);
+    warp_min_max_atomic(valid ? y : BIGP, (long long*)stats + 1, nullptr);
+    warp_min_max_atomic(valid ? z : BIGP, (long long*)stats + 2, nullptr);
+    warp_min_max_atomic(valid ? x : BIGN, nullptr, (long long*)stats + 3);
+    warp_min_max_atomic(valid ? y : BIGN, nullptr, (long long*)stats + 4);
+    warp_min_max_atomic(valid ? z : BIGN, nullptr, (long long*)stats + 5);
+}
+
+// Fused pass 1: voxelize + per-batch axis minimum (voxels are not stored).
+__global__ void fused_min_kernel(const double* __restrict__ coords,
+                                 const int32_t* __restrict__ batch, int64_t n, int nbatch,
+                                 Origin org, double vs, int64_t* ws_min) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = i < n;
+    long long v[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+    int b = 0;
+    if (ok) {
+        for (int a = 0; a < 3; ++a) v[a] = vox1(coords[3 * i + a], org.o[a], vs);
+        if (batch) b = batch[i];
+    }
+    if (!batch || nbatch == 1) {
+        for (int a = 0; a < 3; ++a) warp_min_max_atomic(v[a], (long long*)ws_min + a, nullptr);
+    } else if (ok && b >= 0 && b < nbatch) {
+        for (int a = 0; a < 3; ++a) atomicMin((long long*)ws_min + 3 * b + a, v[a]);
+    }
+}
+
+// Fused pass 2: re-voxelize, remap by the batch minimum, range stats, hash.
+__global__ void fused_hash_kernel(const double* __restrict__ coords,
+                                  const int32_t* __restrict__ batch, int64_t n, int nbatch,
+                                  Origin org, double vs, const int64_t* __restrict__ ws_min,
+                                  HashArgs ha, int32_t* __restrict__ home,
+                                  int32_t* __restrict__ vox32, int64_t* stats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    long long v[3] = {0, 0, 0};
+    if (valid) {
+        int b = (batch && nbatch > 1) ? batch[i] : 0;
+        if (b < 0 || b >= nbatch) b = 0;
+        for (int a = 0; a < 3; ++a)
+            v[a] = vox1(coords[3 * i + a], org.o[a], vs) - ws_min[3 * b + a];
+    }
+    hash_point(v[0], v[1], v[2], i, ha, home, vox32, stats, valid);
+}
+
+}  // namespace hashk
+}  // namespace f3d
+
+using namespace f3d;
+using namespace f3d::hashk;
+
+static inline int nblk(int64_t work) { return (int)((work + kThreads - 1) / kThreads); }
+
+extern "C" int f3d_voxelize(const double* coords, int64_t n, const double* origin3_host,
+                            double voxel_size, int64_t* vox_out, void* stream) {
+    if (n < 0 || !(voxel_size > 0)) return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    Origin o{{origin3_host[0], origin3_host[1], origin3_host[2]}};
+    voxelize_kernel<<<nblk(3 * n), kThreads, 0, (cudaStream_t)stream>>>(coords, n, o, voxel_size,
+                                                                       vox_out);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_remap_nonnegative(const int64_t* vox, const int32_t* batch, int64_t n,
+                                     int32_t nbatch, int64_t* vox_out, int64_t* ws,
+                                     void* stream) {
+    if (n < 0 || nbatch < 1) return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    init_stats_kernel<<<nblk(3 * nbatch + 7), kThreads, 0, st>>>(nullptr, ws, 3 * nbatch);
+    batch_min_kernel<<<nblk(n), kThreads, 0, st>>>(vox, batch, n, nbatch, ws);
+    remap_kernel<<<nblk(3 * n), kThreads, 0, st>>>(vox, batch, n, nbatch, ws, vox_out);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+static bool bad_hash_cfg(int kind, int32_t K, int64_t S_div, int bits) {
+    return kind < 0 || kind > 3 || K < 1 || S_div < 1 || bits < 1 || bits > 21;
+}
+
+extern "C" int f3d_hash_bucket(const int64_t* vox, int64_t n, int kind, int32_t K,
+                               int64_t S_div, int bits, int32_t* home_out, int32_t* vox32_out,
+                               int64_t* stats_out, void* stream) {
+    if (n < 0 || bad_hash_cfg(kind, K, S_div, bits)) return F3D_ERR_CONFIG;
+    cudaStream_t st = (cudaStream_t)stream;
+    init_stats_kernel<<<1, 32, 0, st>>>(stats_out, nullptr, 0);
+    if (n > 0) {
+        HashArgs ha{HashParams{kind, K, S_div, bits, 0}, 1};
+        hash_kernel<<<nblk(n), kThreads, 0, st>>>(vox, n, ha, home_out, vox32_out, stats_out);
+    }
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_morton_encode(const int64_t* vox, int64_t n, int bits, int64_t* codes_out,
+                                 int64_t* stats_out, void* stream) {
+    if (n < 0 || bits < 1 || bits > 21) return F3D_ERR_CONFIG;
+    cudaStream_t st = (cudaStream_t)stream;
+    init_stats_kernel<<<1, 32, 0, st>>>(stats_out, nullptr, 0);
+    if (n > 0) morton_kernel<<<nblk(n), kThreads, 0, st>>>(vox, n, bits, codes_out, stats_out);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_voxel_hash(const double* coords, const int32_t* batch, int64_t n,
+                              int32_t nbatch, const double* origin3_host, double voxel_size,
+                              int kind, int32_t K, int64_t S_div, int bits, int32_t* vox32_out,
+                              int32_t* home_out, int64_t* stats_out, int64_t* ws,
+                              void* stream) {
+    if (n < 0 || nbatch < 1 || !(voxel_size > 0) || bad_hash_cfg(kind, K, S_div, bits))
+        return F3D_ERR_CONFIG;
+    cudaStream_t st = (cudaStream_t)stream;
+    Origin o{{origin3_host[0], origin3_host[1], origin3_host[2]}};
+    init_stats_kernel<<<nblk(3 * nbatch + 7), kThreads, 0, st>>>(stats_out, ws, 3 * nbatch);
+    if (n > 0) {
+        fused_min_kernel<<<nblk(n), kThreads, 0, st>>>(coords, batch, n, nbatch, o, voxel_size,
+                                                        ws);
+        HashArgs ha{HashParams{kind, K, S_div, bits, 0}, 1};
+        fused_hash_kernel<<<nblk(n), kThreads, 0, st>>>(coords, batch, n, nbatch, o, voxel_size,
+                                                         ws, ha, home_out, vox32_out, stats_out);
+    }
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}

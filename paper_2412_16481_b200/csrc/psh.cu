@@ -1,0 +1,672 @@
+// PSH bucket assignment: exact parallel fill-time fixed point.
+//
+// Reference semantics (bw/_kernels.py:41-90, bw/bucketing.py:275-320): per
+// batch, points are visited in index order; a point takes its home bucket if
+// fewer than S earlier points hold it, else the first of P clamped probe
+// buckets with room (strict-div probes that hash to -1 are skipped), else the
+// unbounded recycle bucket K; its offset is its pre-increment count.
+//
+// Parallel restatement: let T[c] be the (sorted-domain) position of the point
+// holding slot S-1 of bucket c (INT_MAX if c never fills).  Point p has room in
+// c  <=>  fewer than S earlier takers  <=>  T[c] >= p.  Iterate
+//     D <- home;  repeat { T <- S-th taker of each bucket under D;
+//                          D' <- first candidate c with T[c] >= p, else K }
+// until D' == D.  By induction on p every fixed point equals the sequential
+// result, and prefix p is correct after p+1 sweeps, so it terminates.
+//
+// One cooperative launch runs everything: an optional stable batch sort, the
+// sweeps (decide + per-tile histograms, column scans over tiles, in-tile
+// stable ranks via __match_any_sync), and the final base/dest pass.  Points
+// live in tiles of 2048 (8 warps x 8 rounds x 32 lanes); per-warp u16
+// histograms of the K+1 local buckets sit in shared memory.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "f3d_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace f3d {
+namespace psh {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kPerLane = 8;
+constexpr int kWarpSpan = 32 * kPerLane;      // 256 points per warp
+constexpr int kTile = kWarps * kWarpSpan;     // 2048 points per tile
+constexpr int kMaxBins = 12288;               // smem histogram limit (8 * 12288 * 2 B)
+constexpr int kMaxProbes = 128;
+constexpr int kScanU = 4;
+
+enum { INFO_SWEEPS = 0, INFO_FALLBACK = 1, INFO_BATCH_ERR = 2 };
+
+struct Params {
+    const int32_t* vox;    // (n,3) original order
+    const int32_t* home;   // (n)
+    const int32_t* batch;  // (n) or null
+    int n, nbatch, K, S, P, max_sweeps;
+    HashParams hp;
+    int vmax;
+    int8_t probe[kMaxProbes * 3];
+    int32_t *bucket_id, *bucket_offset, *counts, *base, *dest, *info;
+    // workspace
+    int4* pk;          // sorted domain: x, y, z, home
+    int32_t* D;        // sorted domain decision (local bucket id)
+    int32_t* off;      // sorted domain offset
+    int32_t* orig;     // sorted -> original index (multi-batch)
+    int32_t* T0;       // nslots
+    int32_t* T1;       // nslots
+    int32_t* hist;     // max_tiles * max(K+1, nbatch)
+    int32_t* tile_p0;  // sorted-domain tile start (multi), max_tiles + 1
+    int32_t* tile_b;   // tile -> batch (multi)
+    int32_t* btile;    // batch -> first tile (multi), nbatch + 1
+    int32_t* bstart;   // batch -> first sorted position, nbatch + 1
+    int32_t* flags;    // max_sweeps + 2 "changed" words
+    int max_tiles;
+};
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ void zero_hist(uint16_t* h, int words32) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(h);
+    for (int i = threadIdx.x; i < words32; i += kThreads) w[i] = 0u;
+}
+
+// Count this warp's keys into its private u16 row (keys < 0 ignored).
+__device__ __forceinline__ void warp_count(const int (&key)[kPerLane], uint16_t* row) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < kPerLane; ++j) {
+        const int k = key[j];
+        const unsigned m = __match_any_sync(0xffffffffu, k);
+        if (k >= 0 && lane == __ffs(m) - 1) row[k] = (uint16_t)(row[k] + __popc(m));
+        __syncwarp();
+    }
+}
+
+// Stable rank of each key within the tile, given row = exclusive prefix of
+// this warp's keys over earlier warps of the tile.
+__device__ __forceinline__ void warp_rank(const int (&key)[kPerLane], uint16_t* row,
+                                          int (&rank)[kPerLane]) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < kPerLane; ++j) {
+        const int k = key[j];
+        const unsigned m = __match_any_sync(0xffffffffu, k);
+        const int b = (k >= 0) ? (int)row[k] : 0;
+        rank[j] = b + __popc(m & lt);
+        __syncwarp();
+        if (k >= 0 && lane == __ffs(m) - 1) row[k] = (uint16_t)(b + __popc(m));
+        __syncwarp();
+    }
+}
+
+// Sum the per-warp rows into hist_row (global), one int per bin.
+__device__ __forceinline__ void store_tile_hist(const uint16_t* h, int stride, int nbins,
+                                                int32_t* hist_row) {
+    for (int c = threadIdx.x; c < nbins; c += kThreads) {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s += h[w * stride + c];
+        hist_row[c] = s;
+    }
+}
+
+// Exclusive prefix across the warps, in place (values stay < 2048).
+__device__ __forceinline__ void warp_prefix_rows(uint16_t* h, int stride, int nbins) {
+    for (int c = threadIdx.x; c < nbins; c += kThreads) {
+        int run = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const int t = h[w * stride + c];
+            h[w * stride + c] = (uint16_t)run;
+            run += t;
+        }
+    }
+}
+
+// One warp: exclusive scan of hist[t*stride + col] over tiles [t0, t1) in
+// place; returns the column total.
+__device__ int column_scan(int32_t* hist, int stride, int col, int t0, int t1) {
+    const int lane = threadIdx.x & 31;
+    int carry = 0;
+    for (int base = t0; base < t1; base += 32 * kScanU) {
+        int v[kScanU];
+        int s = 0;
+#pragma unroll
+        for (int u = 0; u < kScanU; ++u) {
+            const int t = base + lane * kScanU + u;
+            v[u] = (t < t1) ? __ldcg(hist + (int64_t)t * stride + col) : 0;
+            s += v[u];
+        }
+        const int incl = warp_incl_scan(s);
+        int e = carry + incl - s;
+#pragma unroll
+        for (int u = 0; u < kScanU; ++u) {
+            const int t = base + lane * kScanU + u;
+            if (t < t1) hist[(int64_t)t * stride + col] = e;
+            e += v[u];
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    return carry;
+}
+
+// First candidate bucket with room for point p (T[c] >= p), else K.
+__device__ __forceinline__ int decide(const int4 q, int p, const int32_t* __restrict__ T,
+                                      const Params& P_, const int8_t* probe) {
+    if (__ldcg(T + q.w) >= p) return q.w;
+    constexpr int kChunk = 8;
+    for (int p0 = 0; p0 < P_.P; p0 += kChunk) {
+        int cand[kChunk];
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            const int pi = p0 + u;
+            cand[u] = -1;
+            if (pi < P_.P) {
+                const int x = min(max(q.x + (int)probe[3 * pi + 0], 0), P_.vmax);
+                const int y = min(max(q.y + (int)probe[3 * pi + 1], 0), P_.vmax);
+                const int z = min(max(q.z + (int)probe[3 * pi + 2], 0), P_.vmax);
+                cand[u] = hash_bucket1(x, y, z, P_.hp);
+            }
+        }
+        int tv[kChunk];
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) tv[u] = cand[u] >= 0 ? __ldcg(T + cand[u]) : -1;
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u)
+            if (cand[u] >= 0 && tv[u] >= p) return cand[u];
+    }
+    return P_.K;
+}
+
+struct TileInfo {
+    int p0, p1, b;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const Params& P_, bool multi, int t) {
+    TileInfo ti;
+    if (multi) {
+        ti.p0 = __ldcg(P_.tile_p0 + t);
+        ti.b = __ldcg(P_.tile_b + t);
+        ti.p1 = min(ti.p0 + kTile, __ldcg(P_.bstart + ti.b + 1));
+    } else {
+        ti.p0 = t * kTile;
+        ti.p1 = min(ti.p0 + kTile, P_.n);
+        ti.b = 0;
+    }
+    return ti;
+}
+
+// Sequential exact path (the reference loop) for one batch, counters in smem.
+__device__ void sequential_batch(const Params& P_, int b, int pb0, int pb1, int32_t* ctr,
+                                 const int8_t* probe) {
+    const int W = P_.K + 1;
+    for (int c = 0; c < W; ++c) ctr[c] = 0;
+    for (int p = pb0; p < pb1; ++p) {
+        const int4 q = __ldcg(P_.pk + p);
+        int got = -1;
+        if (ctr[q.w] < P_.S) {
+            got = q.w;
+        } else {
+            for (int pi = 0; pi < P_.P && got < 0; ++pi) {
+                const int x = min(max(q.x + (int)probe[3 * pi + 0], 0), P_.vmax);
+                const int y = min(max(q.y + (int)probe[3 * pi + 1], 0), P_.vmax);
+                const int z = min(max(q.z + (int)probe[3 * pi + 2], 0), P_.vmax);
+                const int c = hash_bucket1(x, y, z, P_.hp);
+                if (c >= 0 && ctr[c] < P_.S) got = c;
+            }
+            if (got < 0) got = P_.K;
+        }
+        P_.D[p] = got;
+        P_.off[p] = ctr[got]++;
+    }
+    for (int c = 0; c < W; ++c) P_.counts[(int64_t)b * W + c] = ctr[c];
+}
+
+// --------------------------------------------------------------- the kernel
+
+__global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) uint16_t sh[];
+    __shared__ int8_t probe[kMaxProbes * 3];
+    __shared__ int s_flag;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const bool multi = P_.nbatch > 1;
+    const int K = P_.K;
+    const int W = K + 1;
+    const int nbins = multi ? max(W, P_.nbatch) : W;
+    const int stride = (nbins + 1) & ~1;  // u16 row stride, even
+    uint16_t* myrow = sh + warp * stride;
+    const int hwords = kWarps * stride / 2;
+
+    for (int i = tid; i < P_.P * 3; i += kThreads) probe[i] = P_.probe[i];
+    if (blockIdx.x == 0)
+        for (int i = tid; i < P_.max_sweeps + 2; i += kThreads) P_.flags[i] = 0;
+
+    const int gwarp = blockIdx.x * kWarps + warp;
+    const int nwarps = gridDim.x * kWarps;
+
+    int ntiles;
+    // ------------------------------------------------ stable batch sort
+    if (multi) {
+        const int B = P_.nbatch;
+        const int nto = cdiv_dev(P_.n, kTile);
+        for (int t = blockIdx.x; t < nto; t += gridDim.x) {
+            zero_hist(sh, hwords);
+            __syncthreads();
+            int key[kPerLane];
+#pragma unroll
+            for (int j = 0; j < kPerLane; ++j) {
+                const int i = t * kTile + warp * kWarpSpan + j * 32 + lane;
+                int b = -1;
+                if (i < P_.n) {
+                    b = P_.batch[i];
+                    if (b < 0 || b >= B) {
+                        atomicOr(P_.info + INFO_BATCH_ERR, 1);
+                        b = -1;
+                    }
+                }
+                key[j] = b;
+            }
+            warp_count(key, myrow);
+            __syncthreads();
+            store_tile_hist(sh, stride, B, P_.hist + (int64_t)t * B);
+            __syncthreads();
+        }
+        grid.sync();
+        for (int b = gwarp; b < B; b += nwarps) {
+            const int tot = column_scan(P_.hist, B, b, 0, nto);
+            if (lane == 0) P_.counts[b] = tot;  // temp: batch sizes
+        }
+        grid.sync();
+        if (blockIdx.x == 0 && tid == 0) {
+            int pos = 0, tl = 0;
+            for (int b = 0; b < B; ++b) {
+                const int cb = __ldcg(P_.counts + b);
+                if (cb == 0) P_.info[INFO_BATCH_ERR] |= 2;  // non-contiguous ids
+                P_.bstart[b] = pos;
+                P_.btile[b] = tl;
+                for (int q = 0; q < cb; q += kTile) {
+                    P_.tile_p0[tl] = pos + q;
+                    P_.tile_b[tl] = b;
+                    ++tl;
+                }
+                pos += cb;
+            }
+            P_.bstart[B] = pos;
+            P_.btile[B] = tl;
+        }
+        grid.sync();
+        for (int t = blockIdx.x; t < nto; t += gridDim.x) {
+            zero_hist(sh, hwords);
+            __syncthreads();
+            int key[kPerLane];
+#pragma unroll
+            for (int j = 0; j < kPerLane; ++j) {
+                const int i = t * kTile + warp * kWarpSpan + j * 32 + lane;
+                int b = (i < P_.n) ? P_.batch[i] : -1;
+                key[j] = (b >= 0 && b < B) ? b : -1;
+            }
+            warp_count(key, myrow);
+            __syncthreads();
+            warp_prefix_rows(sh, stride, B);
+            __syncthreads();
+            int rank[kPerLane];
+            warp_rank(key, myrow, rank);
+#pragma unroll
+            for (int j = 0; j < kPerLane; ++j) {
+                const int i = t * kTile + warp * kWarpSpan + j * 32 + lane;
+                if (key[j] >= 0) {
+                    const int b = key[j];
+                    const int pos = __ldcg(P_.bstart + b) + __ldcg(P_.hist + (int64_t)t * B + b) + rank[j];
+                    P_.orig[pos] = i;
+                    P_.pk[pos] = make_int4(P_.vox[3 * (int64_t)i], P_.vox[3 * (int64_t)i + 1],
+                                           P_.vox[3 * (int64_t)i + 2], P_.home[i]);
+                }
+            }
+            __syncthreads();
+        }
+        grid.sync();
+        ntiles = __ldcg(P_.btile + B);
+    } else {
+        ntiles = cdiv_dev(P_.n, kTile);
+    }
+
+    // ------------------------------------------------------------ sweeps
+    int32_t* Tc = P_.T0;
+    int32_t* Tn = P_.T1;
+    int sweep = 0;
+    bool fallback = false;
+    for (;;) {
+        // Phase A: decide + per-tile histogram
+        int changed = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const TileInfo ti = tile_info(P_, multi, t);
+            zero_hist(sh, hwords);
+            __syncthreads();
+            int key[kPerLane];
+            const int32_t* Tb = Tc + (int64_t)ti.b * W;
+#pragma unroll
+            for (int j = 0; j < kPerLane; ++j) {
+                const int p = ti.p0 + warp * kWarpSpan + j * 32 + lane;
+                int k = -1;
+                if (p < ti.p1) {
+                    if (sweep == 0) {
+                        int4 q;
+                        if (multi) {
+                            q = __ldcg(P_.pk + p);
+                        } else {
+                            q = make_int4(P_.vox[3 * (int64_t)p], P_.vox[3 * (int64_t)p + 1],
+                                          P_.vox[3 * (int64_t)p + 2], P_.home[p]);
+                            P_.pk[p] = q;
+                        }
+                        k = q.w;
+                        if (k < 0 || k >= K) {  // precondition: home in [0, K)
+                            atomicOr(P_.info + INFO_BATCH_ERR, 4);
+                            k = K;
+                        }
+                    } else {
+                        const int4 q = __ldcg(P_.pk + p);
+                        k = decide(q, p, Tb, P_, probe);
+                        changed |= (k != P_.D[p]);
+                    }
+                    P_.D[p] = k;
+                }
+                key[j] = k;
+            }
+            warp_count(key, myrow);
+            __syncthreads();
+            store_tile_hist(sh, stride, W, P_.hist + (int64_t)t * W);
+            __syncthreads();
+        }
+        if (sweep > 0) {
+            const int any = __syncthreads_or(changed);
+            if (tid == 0 && any) atomicOr(P_.flags + sweep, 1);
+        }
+        grid.sync();
+        if (sweep > 0) {
+            if (tid == 0) s_flag = *((volatile int32_t*)(P_.flags + sweep));
+            __syncthreads();
+            if (s_flag == 0) break;  // D unchanged: previous offsets are final
+        }
+        if (sweep >= P_.max_sweeps) {
+            fallback = true;
+            break;
+        }
+        // Phase B: column scans over each batch's tiles; counts; T reset
+        {
+            const int ncols = P_.nbatch * W;
+            for (int col = gwarp; col < ncols; col += nwarps) {
+                const int b = col / W;
+                const int c = col - b * W;
+                const int t0 = multi ? __ldcg(P_.btile + b) : 0;
+                const int t1 = multi ? __ldcg(P_.btile + b + 1) : ntiles;
+                const int tot = column_scan(P_.hist, W, c, t0, t1);
+                if (lane == 0) {
+                    P_.counts[col] = tot;
+                    if (c < K && tot < P_.S) Tn[col] = INT_MAX;
+                }
+            }
+        }
+        grid.sync();
+        // Phase C: in-tile stable ranks -> offsets; S-th taker -> T
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const TileInfo ti = tile_info(P_, multi, t);
+            zero_hist(sh, hwords);
+            __syncthreads();
+            int key[kPerLane];
+#pragma unroll
+            for (int j = 0; j < kPerLane; ++j) {
+                const int p = ti.p0 + warp * kWarpSpan + j * 32 + lane;
+                key[j] = (p < ti.p1) ? P_.D[p] : -1;
+            }
+            warp_count(key, myrow);
+            __syncthreads();
+            warp_prefix_rows(sh, stride, W);
+            __syncthreads();
+            int rank[kPerLane];
+            warp_rank(key, myrow, rank);
+            const int32_t* hrow = P_.hist + (int64_t)t * W;
+#pragma unroll
+            for (int j = 0; j < kPerLane; ++j) {
+                const int p = ti.p0 + warp * kWarpSpan + j * 32 + lane;
+                if (key[j] >= 0) {
+                    const int o = __ldcg(hrow + key[j]) + rank[j];
+                    P_.off[p] = o;
+                    if (key[j] < K && o == P_.S - 1) Tn[(int64_t)ti.b * W + key[j]] = p;
+                }
+            }
+            __syncthreads();
+        }
+        grid.sync();
+        int32_t* tmp = Tc;
+        Tc = Tn;
+        Tn = tmp;
+        ++sweep;
+    }
+
+    if (fallback) {
+        // Exact sequential path: one thread per batch, counters in smem.
+        if (blockIdx.x == 0 && tid == 0) {
+            int32_t* ctr = reinterpret_cast<int32_t*>(sh);
+            for (int b = 0; b < P_.nbatch; ++b) {
+                const int pb0 = multi ? __ldcg(P_.bstart + b) : 0;
+                const int pb1 = multi ? __ldcg(P_.bstart + b + 1) : P_.n;
+                sequential_batch(P_, b, pb0, pb1, ctr, probe);
+            }
+        }
+        grid.sync();
+    }
+
+    // ------------------------------------------- final: base scan, dest
+    if (blockIdx.x == 0) {
+        const int nslots = P_.nbatch * W;
+        __shared__ int s_part[kThreads];
+        const int per = (nslots + kThreads - 1) / kThreads;
+        const int a0 = min(tid * per, nslots), a1 = min(a0 + per, nslots);
+        int s = 0;
+        for (int i = a0; i < a1; ++i) s += __ldcg(P_.counts + i);
+        s_part[tid] = s;
+        __syncthreads();
+        if (tid < 32) {
+            int acc = 0;
+            for (int w = 0; w < kThreads / 32; ++w) {
+                const int v = s_part[w * 32 + lane];
+                const int incl = warp_incl_scan(v);
+                s_part[w * 32 + lane] = acc + incl - v;
+                acc += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncthreads();
+        int run = s_part[tid];
+        for (int i = a0; i < a1; ++i) {
+            P_.base[i] = run;
+            run += __ldcg(P_.counts + i);
+        }
+        if (tid == 0) {
+            P_.info[INFO_SWEEPS] = sweep + 1;
+            P_.info[INFO_FALLBACK] = fallback ? 1 : 0;
+        }
+    }
+    grid.sync();
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TileInfo ti = tile_info(P_, multi, t);
+        const int32_t* bb = P_.base + (int64_t)ti.b * W;
+        for (int p = ti.p0 + tid; p < ti.p1; p += kThreads) {
+            const int i = multi ? __ldcg(P_.orig + p) : p;
+            const int d = __ldcg(P_.D + p);
+            const int o = __ldcg(P_.off + p);
+            P_.bucket_id[i] = d;
+            P_.bucket_offset[i] = o;
+            P_.dest[i] = __ldcg(bb + d) + o;
+        }
+    }
+}
+
+struct WsLayout {
+    size_t pk, D, off, orig, T0, T1, hist, tile_p0, tile_b, btile, bstart, flags, total;
+};
+
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static WsLayout layout(int64_t n, int32_t nbatch, int32_t K, int max_sweeps) {
+    WsLayout L;
+    const int64_t max_tiles = n / kTile + nbatch + 1;
+    const int64_t nslots = (int64_t)nbatch * (K + 1);
+    const int64_t nbins = nbatch > 1 ? std::max<int64_t>(K + 1, nbatch) : (K + 1);
+    size_t o = 0;
+    L.pk = o;      o = align256(o + sizeof(int4) * n);
+    L.D = o;       o = align256(o + 4 * n);
+    L.off = o;     o = align256(o + 4 * n);
+    L.orig = o;    o = align256(o + (nbatch > 1 ? 4 * n : 4));
+    L.T0 = o;      o = align256(o + 4 * nslots);
+    L.T1 = o;      o = align256(o + 4 * nslots);
+    L.hist = o;    o = align256(o + 4 * max_tiles * nbins);
+    L.tile_p0 = o; o = align256(o + 4 * (max_tiles + 1));
+    L.tile_b = o;  o = align256(o + 4 * (max_tiles + 1));
+    L.btile = o;   o = align256(o + 4 * (nbatch + 1));
+    L.bstart = o;  o = align256(o + 4 * (nbatch + 1));
+    L.flags = o;   o = align256(o + 4 * (max_sweeps + 2));
+    L.total = o;
+    return L;
+}
+
+constexpr int kMaxSweepsCap = 4096;
+
+}  // namespace psh
+}  // namespace f3d
+
+using namespace f3d;
+
+extern "C" size_t f3d_psh_workspace_size(int64_t n, int32_t nbatch, int32_t K) {
+    return psh::layout(n, nbatch, K, psh::kMaxSweepsCap).total;
+}
+
+// Fully sequential single-thread kernel for bucket counts beyond the smem
+// histogram limit: the reference loop verbatim, counters in global memory.
+__global__ void psh_sequential_kernel(psh::Params P_) {
+    const int W = P_.K + 1;
+    for (int s = 0; s < P_.nbatch * W; ++s) P_.counts[s] = 0;
+    for (int i = 0; i < P_.n; ++i) {
+        const int b = P_.batch ? P_.batch[i] : 0;
+        int32_t* ctr = P_.counts + (int64_t)b * W;
+        const int x = P_.vox[3 * (int64_t)i], y = P_.vox[3 * (int64_t)i + 1],
+                  z = P_.vox[3 * (int64_t)i + 2];
+        int got = -1;
+        const int h = P_.home[i];
+        if (ctr[h] < P_.S) {
+            got = h;
+        } else {
+            for (int pi = 0; pi < P_.P && got < 0; ++pi) {
+                const int xx = min(max(x + (int)P_.probe[3 * pi + 0], 0), P_.vmax);
+                const int yy = min(max(y + (int)P_.probe[3 * pi + 1], 0), P_.vmax);
+                const int zz = min(max(z + (int)P_.probe[3 * pi + 2], 0), P_.vmax);
+                const int c = hash_bucket1(xx, yy, zz, P_.hp);
+                if (c >= 0 && ctr[c] < P_.S) got = c;
+            }
+            if (got < 0) got = P_.K;
+        }
+        P_.bucket_id[i] = got;
+        P_.bucket_offset[i] = ctr[got]++;
+    }
+    int run = 0;
+    for (int s = 0; s < P_.nbatch * W; ++s) {
+        P_.base[s] = run;
+        run += P_.counts[s];
+    }
+    for (int i = 0; i < P_.n; ++i) {
+        const int b = P_.batch ? P_.batch[i] : 0;
+        P_.dest[i] = P_.base[(int64_t)b * W + P_.bucket_id[i]] + P_.bucket_offset[i];
+    }
+    P_.info[0] = 0;
+    P_.info[1] = 2;
+}
+
+extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const int32_t* batch,
+                              int64_t n, int32_t nbatch, int32_t K, int32_t S, int kind,
+                              int64_t S_div, int bits, int strict,
+                              const int8_t* probe_offsets_host, int32_t P, int32_t max_sweeps,
+                              int32_t* bucket_id, int32_t* bucket_offset, int32_t* counts,
+                              int32_t* base, int32_t* dest, int32_t* info_out, void* ws,
+                              size_t ws_bytes, void* stream) {
+    if (n <= 0) return F3D_ERR_EMPTY;
+    if (n >= INT_MAX / 2 || K < 1 || S < 1 || nbatch < 1 || P < 0 || P > psh::kMaxProbes ||
+        bits < 1 || bits > 21 || S_div < 1 || kind < 0 || kind > 3)
+        return F3D_ERR_CONFIG;
+    if (max_sweeps < 1) max_sweeps = 1;
+    if (max_sweeps > psh::kMaxSweepsCap) max_sweeps = psh::kMaxSweepsCap;
+    const psh::WsLayout L = psh::layout(n, nbatch, K, max_sweeps);
+    if (ws_bytes < L.total) return F3D_ERR_CONFIG;
+    cudaStream_t st = (cudaStream_t)stream;
+    char* w = (char*)ws;
+
+    psh::Params p{};
+    p.vox = vox32;
+    p.home = home;
+    p.batch = nbatch > 1 ? batch : nullptr;
+    p.n = (int)n;
+    p.nbatch = nbatch;
+    p.K = K;
+    p.S = S;
+    p.P = P;
+    p.max_sweeps = max_sweeps;
+    p.hp = HashParams{kind, K, S_div, bits, strict};
+    p.vmax = (1 << bits) - 1;
+    for (int i = 0; i < 3 * P; ++i) p.probe[i] = probe_offsets_host[i];
+    p.bucket_id = bucket_id;
+    p.bucket_offset = bucket_offset;
+    p.counts = counts;
+    p.base = base;
+    p.dest = dest;
+    p.info = info_out;
+    p.pk = (int4*)(w + L.pk);
+    p.D = (int32_t*)(w + L.D);
+    p.off = (int32_t*)(w + L.off);
+    p.orig = (int32_t*)(w + L.orig);
+    p.T0 = (int32_t*)(w + L.T0);
+    p.T1 = (int32_t*)(w + L.T1);
+    p.hist = (int32_t*)(w + L.hist);
+    p.tile_p0 = (int32_t*)(w + L.tile_p0);
+    p.tile_b = (int32_t*)(w + L.tile_b);
+    p.btile = (int32_t*)(w + L.btile);
+    p.bstart = (int32_t*)(w + L.bstart);
+    p.flags = (int32_t*)(w + L.flags);
+    p.max_tiles = (int)(n / psh::kTile + nbatch + 1);
+
+    F3D_CUDA_TRY(cudaMemsetAsync(info_out, 0, 4 * sizeof(int32_t), st));
+    const int nbins = nbatch > 1 ? std::max(K + 1, nbatch) : K + 1;
+    if (nbins > psh::kMaxBins) {
+        psh_sequential_kernel<<<1, 1, 0, st>>>(p);
+        F3D_LAUNCH_CHECK();
+        return F3D_OK;
+    }
+    const int stride = (nbins + 1) & ~1;
+    const size_t smem = (size_t)psh::kWarps * stride * sizeof(uint16_t);
+    static int attr_smem = 0;
+    if ((int)smem > 48 * 1024 && (int)smem > attr_smem) {
+        F3D_CUDA_TRY(cudaFuncSetAttribute(psh::psh_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_smem = (int)smem;
+    }
+    int per_sm = 0;
+    F3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, psh::psh_kernel,
+                                                               psh::kThreads, smem));
+    if (per_sm < 1) return F3D_ERR_CONFIG;
+    const int max_tiles = p.max_tiles;
+    int grid = std::min(per_sm * f3d_num_sms(), max_tiles);
+    // Phase B needs nbatch*(K+1) column-warps; more CTAs than tiles only help it.
+    const int col_ctas = cdiv((int64_t)nbatch * (K + 1), psh::kWarps * 2);
+    grid = std::max(grid, std::min(col_ctas, per_sm * f3d_num_sms()));
+    grid = std::max(grid, 1);
+    void* args[] = {(void*)&p};
+    F3D_CUDA_TRY(cudaLaunchCooperativeKernel((void*)psh::psh_kernel, dim3(grid),
+                                             dim3(psh::kThreads), args, smem, st));
+    return F3D_OK;
+}
