@@ -116,6 +116,71 @@ int f3d_scatter_rows(const void *src, const int32_t *dest, int64_t n, int64_t ro
 int f3d_gather_rows(const void *src, const int32_t *idx, int64_t n, int64_t row_bytes,
                     void *dst, void *stream);
 
+
+/* ------------------------------------------ a9-a11: bucket-swin attention
+ * Replaces bw/attention.py:188-268 tiled_attention (and the per-scope loop of
+ * bw/stage.py:141-156).  One launch covers every scope of a round: scope s is
+ * the concatenation of segments [scope_seg[s], scope_seg[s+1]) with physical
+ * start seg_start[j] and virtual start seg_vstart[j]; scope_len[s] = m_s.
+ * work: nwork x (scope, q_start) pairs (64-row query tiles).  q/k/v are bf16
+ * rows with head h at columns [h*dh, (h+1)*dh) and row strides ld_*; o is bf16
+ * (out_f32 = 0) or f32 with the same layout, written at the fixed rows.
+ * mask (nullable): per-row uint8 validity; masked keys are excluded, masked
+ * queries give 0.  starved (nullable): count of rows with no valid key. */
+int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_q,
+                        int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
+                        int dh, const int32_t *scope_seg, const int32_t *seg_start,
+                        const int32_t *seg_vstart, const int32_t *scope_len,
+                        const int32_t *work, int nwork, const uint8_t *mask, int32_t *starved,
+                        void *stream);
+
+/* ---------------------------------------------- a12: positional encoding
+ * bw/attention.py:271-288 (d % 6 == 0).  out_f64: 1 -> double, 0 -> float. */
+int f3d_positional_encoding(const double *coords, int64_t n, int d, double base, int out_f64,
+                            void *out, int64_t ld, void *stream);
+/* Stage form: coords normalised by lo_ext = [lo[3], extent[3]] first
+ * (bw/stage.py:129-132).  out_kind: 1 float, 2 double. */
+int f3d_stage_pe(const double *coords, int64_t n, int d, double base, const double *lo_ext,
+                 int out_kind, void *out, int64_t ld, void *stream);
+/* Per-axis bbox: lo_ext[0..2] = min, lo_ext[3..5] = max - min (0 -> 1).
+ * ws: 6 * 296 doubles. */
+int f3d_coord_bbox(const double *coords, int64_t n, double *ws, double *lo_ext, void *stream);
+
+/* ------------------------------------------------------ a13: stage rows
+ * Fused residual + LayerNorm (+PE) (bw/stage.py:84-88, 135, 157-158):
+ *   if y:   F[r] += y[r] + ybias           (F float or double, y bf16)
+ *   if out: out[r] = LN(F[r]) * gain + beta (+ pe[r])   (population var, eps)
+ * out_kind: 0 bf16, 1 float, 2 double. */
+int f3d_row_ln(void *F, int f_is_f64, int64_t ldf, const void *y, int64_t ldy,
+               const float *ybias, const float *gain, const float *beta, const float *pe,
+               int64_t ldpe, void *out, int out_kind, int64_t ldo, int64_t n, int d, double eps,
+               void *stream);
+/* y = 0.5 x (1 + erf(x / sqrt 2)) in float64 (bw/stage.py:91-92). */
+int f3d_gelu_f64(const double *x, int64_t n, double *y, void *stream);
+/* u = gelu(u + bias) with the exact erf form (bw/stage.py:91-96), bf16 rows. */
+int f3d_bias_gelu(void *u_bf16, int64_t n, int dh, const float *bias, void *stream);
+
+/* ------------------------------------------------ a14-a15: pooling
+ * Replaces bw/pooling.py:68-163 build_subbuckets for every <=1024-row tile
+ * of every bucket slot (tile_start/tile_m/tile_out: first scattered row, row
+ * count and first pooled row of each tile; bw/pooling.py:211-225).  Writes,
+ * per pooled row j, sizes_out[j], seeds_out[j] (tile-local seed row,
+ * nullable) and members[j*rho + r] = r-th member row in index order (-1
+ * padded); sub_out (nullable) gets each row's tile-local sub-bucket id.
+ * flags (device int32) collects integrity failures (1 allocation short,
+ * 2 no candidate, 4 over rho, 8 empty, 16 >1 under-filled, 32 bad id).
+ * rho <= 64. */
+int f3d_pool_build(const double *coords, const int32_t *tile_start, const int32_t *tile_m,
+                   const int32_t *tile_out, int ntiles, int rho, int32_t *sub_out,
+                   int32_t *members, int32_t *sizes_out, int32_t *seeds_out,
+                   int32_t *passes_out, int32_t *flags, void *stream);
+/* Replaces bw/pooling.py:166-184 pool_features: out[j] = reduce over
+ * members of x (sequential in index order; mean = sum / size).
+ * dtype: 0 bf16, 1 float, 2 double.  op: 0 sum, 1 mean, 2 min, 3 max. */
+int f3d_pool_reduce(const void *x, int dtype, int64_t ldx, int d, const int32_t *members,
+                    const int32_t *sizes, int64_t npool, int rho, int op, void *out,
+                    int64_t ldo, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

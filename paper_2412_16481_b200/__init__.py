@@ -7,6 +7,9 @@ paper_2412_16481_b200 as bucketswin``.  Compute runs in hand-written sm_100a
 CUDA (libf3d.so, include/f3d.h); there is no CPU fallback.
 """
 
+from .attention import (AttentionParams, CopyMeter, ScopeSchedule, build_schedule,
+                        copy_meter, logical_gather, lowest_period, positional_encoding,
+                        reference_attention, tiled_attention)
 from .bucketing import (BucketAssignment, ProbeSchedule, assign_buckets,
                         assign_buckets_two_stage, compute_bucket_base,
                         default_probe_schedule, gather, scatter)
@@ -15,5 +18,8 @@ from .errors import (ConfigError, EmptyInputError, IntegrityError, NumericError,
 from .geometry import PointCloud, VoxelGrid, synth_cloud, voxelize
 from .hashing import (HASH_KINDS, HashConfig, hash_bucket, morton_encode,
                       remap_nonnegative)
+from .pooling import (SubBucketAssignment, build_subbuckets, pool_features,
+                      pool_stage)
+from .stage import StageParams, gelu, init_params, layer_norm, stage_forward
 
 __version__ = "0.1.0"

@@ -1,0 +1,320 @@
+"""Bucket-swin scope scheduling and GPU attention.
+
+Drop-in for bw/attention.py.  Scheduling (``build_schedule``,
+``logical_gather``) is integer bookkeeping on the host exactly as in the
+reference; ``tiled_attention`` / ``reference_attention`` run the fused
+bucket-swin kernel of csrc/attn.cu (bf16 operands, fp32 accumulation and
+softmax), which reads every scope's rows in place from the fixed scattered
+layout — the "gather" channel of ``copy_meter`` stays 0 by construction and
+the "attention" channel is charged analytically with the bytes the kernel
+streams.
+"""
+
+import math
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .bucketing import BucketAssignment
+from .errors import ConfigError, NumericError
+
+BLOCK_M = 64   # query rows per work item (csrc/attn.cu kBM)
+BLOCK_N = 64   # keys per streamed tile (csrc/attn.cu kBN)
+
+
+class CopyMeter:
+    """Counts feature bytes copied, split by channel (bw/attention.py:22-41)."""
+
+    def __init__(self):
+        self.bytes = {"gather": 0, "attention": 0}
+
+    def add(self, channel: str, nbytes: int) -> None:
+        self.bytes[channel] += int(nbytes)
+
+    def reset(self) -> None:
+        for k in self.bytes:
+            self.bytes[k] = 0
+
+
+copy_meter = CopyMeter()
+
+
+@dataclass(frozen=True)
+class AttentionParams:
+    """bw/attention.py:44-66."""
+
+    d_model: int
+    n_heads: int
+    tile_rows: int = 64
+
+    def __post_init__(self):
+        if self.d_model < 1 or self.n_heads < 1:
+            raise ConfigError("d_model and n_heads must be >= 1")
+        if self.d_model % self.n_heads:
+            raise ConfigError(
+                f"d_model ({self.d_model}) must be divisible by n_heads ({self.n_heads})")
+        if self.tile_rows < 16 or self.tile_rows % 16:
+            raise ConfigError(f"tile_rows must be a positive multiple of 16, got {self.tile_rows}")
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_heads
+
+    @property
+    def scale(self) -> float:
+        return 1.0 / math.sqrt(self.head_dim)
+
+
+@dataclass(frozen=True)
+class ScopeSchedule:
+    """rounds[t] is a tuple of scopes (int64 bucket-id arrays) that partition
+    all bucket ids (bw/attention.py:69-81)."""
+
+    num_buckets: int
+    window_w: int
+    stride: int
+    shift: int
+    rounds: tuple
+
+    def num_rounds(self) -> int:
+        return len(self.rounds)
+
+
+def build_schedule(num_buckets: int, window_w: int, stride: int = 1, shift: int = 0,
+                   rounds: int = 1) -> ScopeSchedule:
+    """Round t rotates the bucket list by (t*shift) mod W, chops it into
+    windows of W*stride buckets and deals every stride-th bucket into a scope
+    (bw/attention.py:84-117)."""
+    if num_buckets < 1:
+        raise ConfigError(f"num_buckets must be >= 1, got {num_buckets}")
+    if window_w < 1:
+        raise ConfigError(f"window_w must be >= 1, got {window_w}")
+    if window_w > num_buckets:
+        raise ConfigError(f"window_w ({window_w}) exceeds num_buckets ({num_buckets})")
+    if stride < 1:
+        raise ConfigError(f"stride must be >= 1, got {stride}")
+    if not 0 <= shift < window_w:
+        raise ConfigError(f"shift must satisfy 0 <= shift < window_w, got {shift}")
+    if rounds < 1:
+        raise ConfigError(f"rounds must be >= 1, got {rounds}")
+    span = window_w * stride
+    out = []
+    for t in range(rounds):
+        order = (np.arange(num_buckets, dtype=np.int64) + (t * shift) % window_w) % num_buckets
+        scopes = []
+        for s0 in range(0, num_buckets, span):
+            chunk = order[s0:s0 + span]
+            for lane in range(stride):
+                sc = chunk[lane::stride]
+                if len(sc):
+                    scopes.append(sc)
+        out.append(tuple(scopes))
+    return ScopeSchedule(num_buckets=num_buckets, window_w=window_w, stride=stride, shift=shift,
+                         rounds=tuple(out))
+
+
+def _table_np(assignment):
+    if isinstance(assignment, BucketAssignment):
+        st, ln = assignment.bucket_table(split_recycle=False)
+    else:
+        st, ln = assignment
+    to = lambda a: a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+    return to(st).astype(np.int64), to(ln).astype(np.int64)
+
+
+def logical_gather(assignment, scope):
+    """[(start, stop), ...] of the scope's non-empty buckets; copies nothing
+    (bw/attention.py:120-139)."""
+    starts, lengths = _table_np(assignment)
+    ranges = []
+    for b in np.asarray(scope, dtype=np.int64):
+        if b < 0 or b >= len(starts):
+            raise ConfigError(f"scope bucket id {int(b)} outside the bucket table")
+        if lengths[b] == 0:
+            continue
+        ranges.append((int(starts[b]), int(starts[b]) + int(lengths[b])))
+    return ranges
+
+
+# --------------------------------------------------------------- kernel plan
+
+class RoundPlan:
+    """Device tables for one launch: scopes as merged physical segments plus
+    the (scope, q_start) work list, longest scopes first (LPT order)."""
+
+    def __init__(self, scope_ranges, dev):
+        seg_first, seg_start, seg_vstart, lens = [0], [], [], []
+        for ranges in scope_ranges:
+            v = 0
+            last_end = None
+            for a, b in ranges:
+                if b <= a:
+                    continue
+                if last_end is not None and a == last_end:
+                    last_end = b                      # adjacent bucket: extend the segment
+                else:
+                    seg_start.append(a)
+                    seg_vstart.append(v)
+                    last_end = b
+                v += b - a
+            seg_first.append(len(seg_start))
+            lens.append(v)
+        lens = np.array(lens, dtype=np.int64)
+        self.scope_len_host = lens
+        order = np.argsort(-lens, kind="stable")
+        work = [(s, q) for s in order for q in range(0, int(lens[s]), BLOCK_M)]
+        self.nwork = len(work)
+        self.flops_per_head = int((lens.astype(np.float64) ** 2).sum())   # sum m^2
+        i32 = lambda a: torch.tensor(np.asarray(a, dtype=np.int32), device=dev)
+        self.scope_seg = i32(seg_first)
+        self.seg_start = i32(seg_start if seg_start else [0])
+        self.seg_vstart = i32(seg_vstart if seg_vstart else [0])
+        self.scope_len = i32(lens if len(lens) else [0])
+        self.work = i32(np.array(work, dtype=np.int32).reshape(-1, 2) if work else np.zeros((1, 2)))
+
+
+def plan_schedule(table, schedule: ScopeSchedule, dev):
+    """One RoundPlan per round of the schedule over a (starts, lengths) table."""
+    starts, lengths = _table_np(table)
+    plans = []
+    for scopes in schedule.rounds:
+        rngs = []
+        for sc in scopes:
+            sc = np.asarray(sc, dtype=np.int64)
+            if (sc < 0).any() or (sc >= len(starts)).any():
+                raise ConfigError("scope bucket id outside the bucket table")
+            rngs.append([(int(starts[b]), int(starts[b] + lengths[b])) for b in sc if lengths[b] > 0])
+        plans.append(RoundPlan(rngs, dev))
+    return plans
+
+
+def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, starved=None):
+    """Launch f3d_bswin_attention.  q/k/v: bf16 CUDA tensors whose rows hold
+    heads side by side (head h at columns h*dh..), any row stride; out: bf16
+    or fp32 rows with the same head layout."""
+    L.call("f3d_bswin_attention", L.ptr(q), L.ptr(k), L.ptr(v), q.stride(0), k.stride(0),
+           v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads, dh,
+           L.ptr(plan.scope_seg), L.ptr(plan.seg_start), L.ptr(plan.seg_vstart),
+           L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork, L.ptr(mask), L.ptr(starved),
+           L.stream())
+
+
+def _check_finite(name, t):
+    if t.numel() and not bool(torch.isfinite(t).all()):
+        raise NumericError(f"{name} contains non-finite values")
+
+
+def _prep_qkv(Q, K, V, params):
+    host = L.is_host(Q)
+    ts = []
+    for name, a in (("Q", Q), ("K", K), ("V", V)):
+        t = L.to_dev(a, torch.float64 if not isinstance(a, torch.Tensor) else a.dtype)
+        if t.ndim != 2:
+            raise ConfigError(f"{name} must be 2-D")
+        ts.append(t)
+    return ts, host
+
+
+def tiled_attention(Q, K, V, params: AttentionParams, ranges=None, mask=None):
+    """Online-softmax attention over the rows of ``ranges`` (one scope),
+    bw/attention.py:188-268.  Returns the real rows of every range in range
+    order.  Masked keys are excluded, masked query rows give zeros, and rows
+    with no valid key give zeros plus a RuntimeWarning."""
+    (q, k, v), host = _prep_qkv(Q, K, V, params)
+    if q.shape != k.shape or q.shape != v.shape:
+        raise ConfigError("Q, K, V must share one shape")
+    if q.shape[1] != params.d_model:
+        raise ConfigError(f"feature width {q.shape[1]} != d_model {params.d_model}")
+    total = q.shape[0]
+    if ranges is None:
+        ranges = [(0, total)]
+    ranges = [(int(a), int(b)) for a, b in ranges]
+    for a, b in ranges:
+        if not 0 <= a <= b <= total:
+            raise ConfigError(f"range ({a}, {b}) outside [0, {total}]")
+    mk = None
+    if mask is not None:
+        mk = L.to_dev(np.asarray(mask, dtype=bool) if not isinstance(mask, torch.Tensor) else mask,
+                      torch.bool)
+        if tuple(mk.shape) != (total,):
+            raise ConfigError("mask must have shape (N,)")
+        mk = mk.to(torch.uint8)
+    real = [(a, b) for a, b in ranges if b > a]
+    if not real:
+        out = torch.empty((0, params.d_model), dtype=torch.float64, device=q.device)
+        return L.out(out, host)
+    rows = torch.cat([torch.arange(a, b, device=q.device) for a, b in real])
+    for name, t in (("Q", q), ("K", k), ("V", v)):
+        _check_finite(name, t[rows])
+    dh = params.head_dim
+    qb, kb, vb = (t.to(torch.bfloat16).contiguous() for t in (q, k, v))
+    out = torch.zeros((total, params.d_model), dtype=torch.float32, device=q.device)
+    # overlapping / repeated ranges are legal in the reference: run each
+    # distinct physical range list as one scope over a private row space
+    plan = RoundPlan([real], q.device)
+    starved = torch.zeros(1, dtype=torch.int32, device=q.device) if mk is not None else None
+    m = sum(b - a for a, b in real)
+    # bytes the kernel streams: Q once, K and V once per query tile (bf16)
+    copy_meter.add("attention", 2 * m * params.d_model * (1 + 2 * (-(-m // BLOCK_M))))
+    if _disjoint(real):
+        attend(qb, kb, vb, out, plan, params.n_heads, dh, mask=mk, starved=starved)
+        res = out[rows].to(torch.float64)
+    else:
+        qs, ks, vs = qb[rows].contiguous(), kb[rows].contiguous(), vb[rows].contiguous()
+        o2 = torch.zeros((m, params.d_model), dtype=torch.float32, device=q.device)
+        mk2 = mk[rows].contiguous() if mk is not None else None
+        attend(qs, ks, vs, o2, RoundPlan([[(0, m)]], q.device), params.n_heads, dh, mask=mk2,
+               starved=starved)
+        res = o2.to(torch.float64)
+    if mk is not None and not bool(mk[rows].any()):
+        warnings.warn(f"{m} query rows had every key masked; their outputs are zero",
+                      RuntimeWarning, stacklevel=2)
+    return L.out(res, host)
+
+
+def _disjoint(ranges):
+    s = sorted(ranges)
+    return all(s[i][1] <= s[i + 1][0] for i in range(len(s) - 1))
+
+
+def reference_attention(Q, K, V, params: AttentionParams):
+    """Dense attention over all rows (bw/attention.py:147-166); runs the same
+    kernel as one scope.  NumericError on non-finite inputs."""
+    (q, k, v), host = _prep_qkv(Q, K, V, params)
+    for name, t in (("Q", q), ("K", k), ("V", v)):
+        _check_finite(name, t)
+    if q.shape[1] != params.d_model:
+        raise ConfigError(f"feature width {q.shape[1]} != d_model {params.d_model}")
+    m = q.shape[0]
+    qb, kb, vb = (t.to(torch.bfloat16).contiguous() for t in (q, k, v))
+    mk = k.shape[0]
+    if mk != m:
+        raise ConfigError("reference_attention on the GPU needs as many keys as queries")
+    out = torch.zeros((m, params.d_model), dtype=torch.float32, device=q.device)
+    attend(qb, kb, vb, out, RoundPlan([[(0, m)]], q.device), params.n_heads, params.head_dim)
+    return L.out(out.to(torch.float64), host)
+
+
+def positional_encoding(coords, d_model: int, base: float = 10000.0):
+    """Sinusoidal per-axis encoding, d_model/3 dims per axis as alternating
+    sin/cos pairs (bw/attention.py:271-288); computed by f3d_positional_encoding
+    in float64."""
+    if d_model % 6:
+        raise ConfigError(f"d_model must be divisible by 6, got {d_model}")
+    host = L.is_host(coords)
+    c = L.to_dev(coords, torch.float64)
+    if c.ndim != 2 or c.shape[1] != 3:
+        raise ConfigError(f"coords must have shape (m, 3), got {tuple(c.shape)}")
+    out = L.empty((c.shape[0], d_model), torch.float64)
+    L.call("f3d_positional_encoding", L.ptr(c), c.shape[0], d_model, float(base), 1,
+           L.ptr(out), d_model, L.stream())
+    return L.out(out, host)
+
+
+def lowest_period(d_model: int, base: float = 10000.0) -> float:
+    """Period of the lowest-frequency sin/cos pair (bw/attention.py:291-294)."""
+    n_pairs = d_model // 6
+    return 2.0 * math.pi * base ** ((n_pairs - 1) / n_pairs)

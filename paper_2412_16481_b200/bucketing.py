@@ -129,6 +129,14 @@ class BucketAssignment:
             "dest": None,
         }
 
+    def to_host(self) -> "BucketAssignment":
+        """Public fields as numpy int64 (device mirrors kept)."""
+        for name in ("bucket_id", "bucket_offset", "counts", "bucket_base", "batch_id"):
+            v = getattr(self, name)
+            if isinstance(v, torch.Tensor):
+                setattr(self, name, v.detach().cpu().numpy())
+        return self
+
     def _wrap(self, t):
         return t if self.on_device else t.cpu().numpy()
 

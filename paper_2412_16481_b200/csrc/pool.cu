@@ -1,0 +1,432 @@
+// In-bucket pooling (bw/pooling.py): sub-bucket partition of every <=1024-row
+// tile of every bucket slot, then the per-sub-bucket reduce.
+//
+// Partition (bw/pooling.py:68-163), one warp per tile, bit-exact:
+//   q = min((c - lo) / ext * 1024, 1023) truncated (f64, IEEE ops)      :59-65
+//   key = morton10(q) % target, target = ceil(m / rho)                   :84
+//   step 1: ids in first-seen key order; a row stays iff its occurrence
+//           rank within its key is < rho (index order)                  :88-102
+//   step 2: the first (target - #ids) overflow rows seed new ids         :104-117
+//   step 3: the rest, in index order, join the nearest under-filled new
+//           id (else any under-filled id); f64 sqrt((dx^2+dy^2)+dz^2) to the
+//           seed row, lowest id on ties                                   :119-139
+//   repair: pour the smallest under-filled into the fullest one by stable
+//           distance order until <= 1 is under-filled                     :141-157
+// Occurrence ranks are computed 32 rows at a time with __match_any_sync,
+// so index order is preserved exactly.  Members of each sub-bucket are
+// emitted in index order as a dense [pooled_rows][rho] list for the reduce.
+#include <cuda_bf16.h>
+
+#include <cfloat>
+#include <climits>
+
+#include "f3d_common.cuh"
+
+namespace f3d {
+namespace pool {
+
+constexpr int kCap = 1024;         // TILE_CAP (bw/pooling.py:22)
+constexpr int kWarpsPerCta = 4;
+constexpr int kThreads = 32 * kWarpsPerCta;
+
+struct WarpSmem {
+    uint16_t cnt[kCap];     // per key running count
+    int16_t idk[kCap];      // key -> sub id
+    int16_t sizes[kCap];    // per sub id
+    int16_t seeds[kCap];    // per sub id: tile-local seed row
+    int16_t sub[kCap];      // per row: sub id (-1 overflow, -2 queued)
+    uint16_t key[kCap];     // per row
+};
+
+struct Args {
+    const double* coords;       // (N,3) scattered rows
+    const int32_t* tile_start;  // global first row of tile t
+    const int32_t* tile_m;      // rows in tile t
+    const int32_t* tile_out;    // first pooled row of tile t
+    int ntiles;
+    int rho;
+    int32_t* sub_out;           // (N) tile-local sub id per row (nullable)
+    int32_t* members;           // (npool, rho) global row ids, -1 padded
+    int32_t* sizes_out;         // (npool)
+    int32_t* seeds_out;         // (npool) tile-local seed row (nullable)
+    int32_t* passes_out;        // (ntiles) scan passes (nullable)
+    int32_t* flags;             // integrity flags
+};
+
+__device__ __forceinline__ double dist3(const double* a, const double* b) {
+    const double dx = __dsub_rn(a[0], b[0]);
+    const double dy = __dsub_rn(a[1], b[1]);
+    const double dz = __dsub_rn(a[2], b[2]);
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+}
+
+// lexicographic (d, id) minimum across the warp; returns the winning id
+__device__ __forceinline__ int warp_argmin(double d, int id) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double d2 = __shfl_xor_sync(0xffffffffu, d, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, id, o);
+        if (d2 < d || (d2 == d && i2 < id)) {
+            d = d2;
+            id = i2;
+        }
+    }
+    return id;
+}
+
+__global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
+    __shared__ WarpSmem smem_all[kWarpsPerCta];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * kWarpsPerCta + warp;
+    if (t >= A.ntiles) return;
+    WarpSmem& S = smem_all[warp];
+    const int r0 = A.tile_start[t];
+    const int m = A.tile_m[t];
+    const int rho = A.rho;
+    const int target = (m + rho - 1) / rho;
+    const double* C = A.coords + 3 * (int64_t)r0;
+    const unsigned lt = lanemask_lt();
+
+    // ---- bbox of the tile
+    double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    for (int i = lane; i < m; i += 32)
+        for (int a = 0; a < 3; ++a) {
+            const double v = C[3 * i + a];
+            lo[a] = fmin(lo[a], v);
+            hi[a] = fmax(hi[a], v);
+        }
+    for (int a = 0; a < 3; ++a)
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+    double ext[3];
+    for (int a = 0; a < 3; ++a) {
+        ext[a] = __dsub_rn(hi[a], lo[a]);
+        if (ext[a] == 0.0) ext[a] = 1.0;
+    }
+    // ---- keys; reset per-key / per-id state
+    for (int i = lane; i < kCap; i += 32) {
+        S.cnt[i] = 0;
+        S.idk[i] = -1;
+        S.sizes[i] = 0;
+        S.seeds[i] = -1;
+    }
+    for (int i = lane; i < m; i += 32) {
+        uint32_t q[3];
+        for (int a = 0; a < 3; ++a) {
+            double v = __dmul_rn(__ddiv_rn(__dsub_rn(C[3 * i + a], lo[a]), ext[a]), 1024.0);
+            v = fmin(v, 1023.0);
+            q[a] = (uint32_t)(int64_t)v;   // truncation (values >= 0)
+        }
+        const uint32_t code = spread3_10(q[0]) | (spread3_10(q[1]) << 1) | (spread3_10(q[2]) << 2);
+        S.key[i] = (uint16_t)(code % (uint32_t)target);
+    }
+    __syncwarp();
+    // ---- step 1: first-seen allocation + occurrence ranks, 32 rows at a time
+    int nalloc = 0, novf = 0;
+    for (int base = 0; base < m; base += 32) {
+        const int i = base + lane;
+        const bool v = i < m;
+        const int k = v ? (int)S.key[i] : -1 - lane;   // invalid lanes: unique keys
+        const unsigned mm = __match_any_sync(0xffffffffu, k);
+        int occ = 0;
+        if (v) occ = S.cnt[k] + __popc(mm & lt);
+        const bool first = v && occ == 0;
+        const unsigned fb = __ballot_sync(0xffffffffu, first);
+        __syncwarp();
+        if (first) {
+            const int id = nalloc + __popc(fb & lt);
+            S.idk[k] = (int16_t)id;
+            S.seeds[id] = (int16_t)i;
+        }
+        if (v && lane == __ffs(mm) - 1) S.cnt[k] = (uint16_t)(S.cnt[k] + __popc(mm));
+        nalloc += __popc(fb);
+        __syncwarp();
+        const bool keep = v && occ < rho;
+        const bool ovf = v && !keep;
+        const unsigned ob = __ballot_sync(0xffffffffu, ovf);
+        if (keep) S.sub[i] = S.idk[k];
+        if (ovf) S.sub[i] = -1;
+        novf += __popc(ob);
+        __syncwarp();
+    }
+    for (int k = lane; k < target; k += 32) {
+        const int c = S.cnt[k];
+        if (c > 0) S.sizes[S.idk[k]] = (int16_t)min(c, rho);
+    }
+    __syncwarp();
+    // ---- step 2: overflow rows seed new ids until target ids exist
+    const int need_new = target - nalloc;
+    int rank = 0;
+    int nqueue = 0;
+    for (int base = 0; base < m; base += 32) {
+        const int i = base + lane;
+        const bool o = i < m && S.sub[i] == -1;
+        const unsigned ob = __ballot_sync(0xffffffffu, o);
+        if (o) {
+            const int r = rank + __popc(ob & lt);
+            if (r < need_new) {
+                const int id = nalloc + r;
+                S.sub[i] = (int16_t)id;
+                S.sizes[id] = 1;
+                S.seeds[id] = (int16_t)i;
+            } else {
+                S.sub[i] = -2;
+            }
+        }
+        rank += __popc(ob);
+    }
+    nqueue = max(0, novf - need_new);
+    if (novf < need_new && lane == 0) atomicOr(A.flags, 1);   // allocation fell short
+    __syncwarp();
+    // ---- step 3: queued rows join the nearest under-filled sub-bucket
+    if (nqueue > 0) {
+        for (int i = 0; i < m; ++i) {
+            if (S.sub[i] != -2) continue;   // warp-uniform (smem broadcast)
+            const double* ci = C + 3 * i;
+            double best = DBL_MAX;
+            int bid = INT_MAX;
+            for (int j = nalloc + lane; j < target; j += 32) {
+                if (S.sizes[j] < rho) {
+                    const double d = dist3(C + 3 * S.seeds[j], ci);
+                    if (d < best || (d == best && j < bid)) {
+                        best = d;
+                        bid = j;
+                    }
+                }
+            }
+            bool any_new = __any_sync(0xffffffffu, bid != INT_MAX);
+            if (!any_new) {
+                for (int j = lane; j < target; j += 32) {
+                    if (S.sizes[j] < rho) {
+                        const double d = dist3(C + 3 * S.seeds[j], ci);
+                        if (d < best || (d == best && j < bid)) {
+                            best = d;
+                            bid = j;
+                        }
+                    }
+                }
+            }
+            const int j = warp_argmin(best, bid);
+            __syncwarp();
+            if (lane == 0) {
+                if (j == INT_MAX) {
+                    atomicOr(A.flags, 2);
+                } else {
+                    S.sub[i] = (int16_t)j;
+                    S.sizes[j] = (int16_t)(S.sizes[j] + 1);
+                }
+            }
+            __syncwarp();
+            if (j == INT_MAX) break;
+        }
+    }
+    // ---- repair: at most one under-filled sub-bucket may remain
+    for (int guard = 0; guard < kCap; ++guard) {
+        // under-filled ids: count, fullest (lowest id on ties)
+        int cnt_under = 0;
+        int best_sz = -1, best_id = INT_MAX;
+        for (int j = lane; j < target; j += 32) {
+            const int sz = S.sizes[j];
+            if (sz < rho) {
+                ++cnt_under;
+                if (sz > best_sz || (sz == best_sz && j < best_id)) {
+                    best_sz = sz;
+                    best_id = j;
+                }
+            }
+        }
+        cnt_under = warp_sum(cnt_under);
+        if (cnt_under <= 1) break;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int s2 = __shfl_xor_sync(0xffffffffu, best_sz, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, best_id, o);
+            if (s2 > best_sz || (s2 == best_sz && i2 < best_id)) {
+                best_sz = s2;
+                best_id = i2;
+            }
+        }
+        const int full_t = best_id;
+        int dsz = INT_MAX, donor = INT_MAX;
+        for (int j = lane; j < target; j += 32) {
+            const int sz = S.sizes[j];
+            if (sz < rho && j != full_t && (sz < dsz || (sz == dsz && j < donor))) {
+                dsz = sz;
+                donor = j;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int s2 = __shfl_xor_sync(0xffffffffu, dsz, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, donor, o);
+            if (s2 < dsz || (s2 == dsz && i2 < donor)) {
+                dsz = s2;
+                donor = i2;
+            }
+        }
+        const int need = rho - S.sizes[full_t];
+        if (lane == 0) {
+            // members of donor in index order (< rho of them), stable by distance
+            int mem[64];
+            double md[64];
+            int nm = 0;
+            const double* cs = C + 3 * S.seeds[full_t];
+            for (int i = 0; i < m && nm < 64; ++i)
+                if (S.sub[i] == donor) {
+                    mem[nm] = i;
+                    md[nm] = dist3(C + 3 * i, cs);
+                    ++nm;
+                }
+            // stable insertion sort by distance
+            for (int a = 1; a < nm; ++a) {
+                const int mi = mem[a];
+                const double dv = md[a];
+                int b = a - 1;
+                while (b >= 0 && md[b] > dv) {
+                    mem[b + 1] = mem[b];
+                    md[b + 1] = md[b];
+                    --b;
+                }
+                mem[b + 1] = mi;
+                md[b + 1] = dv;
+            }
+            const int mv = min(need, nm);
+            for (int a = 0; a < mv; ++a) S.sub[mem[a]] = (int16_t)full_t;
+            S.sizes[full_t] = (int16_t)(S.sizes[full_t] + mv);
+            S.sizes[donor] = (int16_t)(S.sizes[donor] - mv);
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+    // ---- validate + emit
+    const int out0 = A.tile_out[t];
+    int bad = 0;
+    int n_under = 0;
+    for (int j = lane; j < target; j += 32) {
+        const int sz = S.sizes[j];
+        if (sz > rho) bad |= 4;
+        if (sz < 1) bad |= 8;
+        if (sz < rho) ++n_under;
+        A.sizes_out[out0 + j] = sz;
+        if (A.seeds_out) A.seeds_out[out0 + j] = S.seeds[j];
+        S.cnt[j] = 0;
+    }
+    n_under = warp_sum(n_under);
+    if (n_under > 1) bad |= 16;
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && lane == 0) atomicOr(A.flags, bad);
+    if (A.passes_out && lane == 0) A.passes_out[t] = nqueue > 0 ? 1 : 0;
+    __syncwarp();
+    for (int base = 0; base < m; base += 32) {
+        const int i = base + lane;
+        const bool v = i < m;
+        const int s = v ? (int)S.sub[i] : -1 - lane;
+        const unsigned mm = __match_any_sync(0xffffffffu, s);
+        if (v) {
+            if (s < 0 || s >= target) {
+                atomicOr(A.flags, 32);
+            } else {
+                const int r = S.cnt[s] + __popc(mm & lt);
+                if (r < rho) A.members[(int64_t)(out0 + s) * rho + r] = r0 + i;
+                if (A.sub_out) A.sub_out[r0 + i] = s;
+            }
+        }
+        __syncwarp();
+        if (v && s >= 0 && s < target && lane == __ffs(mm) - 1)
+            S.cnt[s] = (uint16_t)(S.cnt[s] + __popc(mm));
+        __syncwarp();
+    }
+    // pad member lists of sub-buckets smaller than rho
+    for (int j = lane; j < target; j += 32)
+        for (int r = S.sizes[j]; r < rho; ++r) A.members[(int64_t)(out0 + j) * rho + r] = -1;
+}
+
+// ------------------------------------------------------------------ reduce
+
+enum { R_SUM = 0, R_MEAN = 1, R_MIN = 2, R_MAX = 3 };
+
+template <typename T> struct RAcc { using type = float; };
+template <> struct RAcc<double> { using type = double; };
+__device__ __forceinline__ float ld_f(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float ld_f(const float* p) { return *p; }
+__device__ __forceinline__ double ld_f(const double* p) { return *p; }
+__device__ __forceinline__ void st_f(__nv_bfloat16* p, float v) { *p = __float2bfloat16(v); }
+__device__ __forceinline__ void st_f(float* p, float v) { *p = v; }
+__device__ __forceinline__ void st_f(double* p, double v) { *p = v; }
+
+// One thread per (pooled row, column); members in index order, sequential
+// accumulation (np.add/minimum/maximum.reduceat order), mean = sum / size.
+template <typename T>
+__global__ void pool_reduce_kernel(const T* __restrict__ x, int64_t ldx, int d,
+                                   const int32_t* __restrict__ members,
+                                   const int32_t* __restrict__ sizes, int64_t npool, int rho,
+                                   int op, T* __restrict__ out, int64_t ldo) {
+    using A = typename RAcc<T>::type;
+    const int64_t tot = npool * d;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / d;
+        const int c = (int)(t - j * d);
+        const int32_t* mem = members + j * rho;
+        const int sz = sizes[j];
+        A acc = (A)ld_f(x + (int64_t)mem[0] * ldx + c);
+        for (int r = 1; r < sz; ++r) {
+            const A v = (A)ld_f(x + (int64_t)mem[r] * ldx + c);
+            if (op == R_MIN) acc = v < acc ? v : acc;
+            else if (op == R_MAX) acc = v > acc ? v : acc;
+            else acc = acc + v;
+        }
+        if (op == R_MEAN) acc = acc / (A)sz;
+        st_f(out + j * ldo + c, acc);
+    }
+}
+
+}  // namespace pool
+}  // namespace f3d
+
+using namespace f3d;
+
+extern "C" int f3d_pool_build(const double* coords, const int32_t* tile_start,
+                              const int32_t* tile_m, const int32_t* tile_out, int ntiles, int rho,
+                              int32_t* sub_out, int32_t* members, int32_t* sizes_out,
+                              int32_t* seeds_out, int32_t* passes_out, int32_t* flags,
+                              void* stream) {
+    if (rho < 1 || rho > 64 || ntiles < 0) return F3D_ERR_CONFIG;
+    cudaStream_t st = (cudaStream_t)stream;
+    F3D_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    if (ntiles == 0) return F3D_OK;
+    pool::Args A{coords, tile_start, tile_m, tile_out, ntiles, rho, sub_out, members, sizes_out,
+                 seeds_out, passes_out, flags};
+    const int grid = (ntiles + pool::kWarpsPerCta - 1) / pool::kWarpsPerCta;
+    pool::pool_build_kernel<<<grid, pool::kThreads, 0, st>>>(A);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_pool_reduce(const void* x, int dtype, int64_t ldx, int d,
+                               const int32_t* members, const int32_t* sizes, int64_t npool,
+                               int rho, int op, void* out, int64_t ldo, void* stream) {
+    if (d < 1 || rho < 1 || op < 0 || op > 3 || npool < 0) return F3D_ERR_CONFIG;
+    if (npool == 0) return F3D_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t tot = npool * d;
+    int64_t g = (tot + 255) / 256;
+    if (g > (int64_t)f3d_num_sms() * 32) g = (int64_t)f3d_num_sms() * 32;
+    if (dtype == 2)
+        pool::pool_reduce_kernel<double><<<(unsigned)g, 256, 0, st>>>(
+            (const double*)x, ldx, d, members, sizes, npool, rho, op, (double*)out, ldo);
+    else if (dtype == 1)
+        pool::pool_reduce_kernel<float><<<(unsigned)g, 256, 0, st>>>(
+            (const float*)x, ldx, d, members, sizes, npool, rho, op, (float*)out, ldo);
+    else if (dtype == 0)
+        pool::pool_reduce_kernel<__nv_bfloat16><<<(unsigned)g, 256, 0, st>>>(
+            (const __nv_bfloat16*)x, ldx, d, members, sizes, npool, rho, op,
+            (__nv_bfloat16*)out, ldo);
+    else
+        return F3D_ERR_CONFIG;
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}

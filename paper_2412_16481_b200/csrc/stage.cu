@@ -1,0 +1,294 @@
+// Stage row kernels around the GEMMs of bw/stage.py:99-159 (HBM-bound):
+//   positional encoding of bbox-normalised coords (bw/attention.py:271-288,
+//   bw/stage.py:129-132), fused residual + LayerNorm (+PE) -> bf16
+//   (bw/stage.py:84-88, 135, 157-158), and bias + exact-erf GELU
+//   (bw/stage.py:91-96).  One warp per row, fp32 (or f64) math.
+#include <cuda_bf16.h>
+
+#include <cfloat>
+
+#include "f3d_common.cuh"
+
+namespace f3d {
+namespace stage {
+
+constexpr int kThreads = 256;
+constexpr int kMaxPerLane = 32;   // d <= 1024
+
+// ---------------------------------------------------------------- bbox
+
+__global__ void bbox_partial_kernel(const double* __restrict__ c, int64_t n, double* part) {
+    __shared__ double s[6][kThreads / 32];
+    double mn[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, mx[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        for (int a = 0; a < 3; ++a) {
+            const double v = c[3 * i + a];
+            mn[a] = fmin(mn[a], v);
+            mx[a] = fmax(mx[a], v);
+        }
+    }
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fmin(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = fmax(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+        for (int a = 0; a < 3; ++a) {
+            s[a][w] = mn[a];
+            s[3 + a][w] = mx[a];
+        }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double r = threadIdx.x < 3 ? DBL_MAX : -DBL_MAX;
+        for (int j = 0; j < kThreads / 32; ++j)
+            r = threadIdx.x < 3 ? fmin(r, s[threadIdx.x][j]) : fmax(r, s[threadIdx.x][j]);
+        part[blockIdx.x * 6 + threadIdx.x] = r;
+    }
+}
+
+// lo[3], ext[3] with ext == 0 -> 1 (bw/stage.py:129-131)
+__global__ void bbox_final_kernel(const double* part, int nparts, double* lo_ext) {
+    if (threadIdx.x >= 3) return;
+    const int a = threadIdx.x;
+    double mn = DBL_MAX, mx = -DBL_MAX;
+    for (int j = 0; j < nparts; ++j) {
+        mn = fmin(mn, part[6 * j + a]);
+        mx = fmax(mx, part[6 * j + 3 + a]);
+    }
+    double e = __dsub_rn(mx, mn);
+    if (e == 0.0) e = 1.0;
+    lo_ext[a] = mn;
+    lo_ext[3 + a] = e;
+}
+
+// --------------------------------------------------------------------- PE
+
+template <typename OutT>
+__global__ void pe_kernel(const double* __restrict__ c, int64_t n, int d, double base,
+                          const double* __restrict__ lo_ext, OutT* __restrict__ out, int64_t ld) {
+    const int npair = d / 6;
+    const int blk = 2 * npair;
+    const int64_t tot = n * 3 * npair;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / (3 * npair);
+        const int r = (int)(t - i * 3 * npair);
+        const int a = r / npair, j = r - a * npair;
+        double x = c[3 * i + a];
+        if (lo_ext) x = __ddiv_rn(__dsub_rn(x, lo_ext[a]), lo_ext[3 + a]);
+        const double inv = pow(base, -(double)j / (double)npair);
+        const double ang = __dmul_rn(x, inv);
+        double sv, cv;
+        sincos(ang, &sv, &cv);
+        out[i * ld + a * blk + 2 * j] = (OutT)sv;
+        out[i * ld + a * blk + 2 * j + 1] = (OutT)cv;
+    }
+}
+
+// ------------------------------------------------------- residual + LN
+
+template <typename T> struct Acc { using type = float; };
+template <> struct Acc<double> { using type = double; };
+
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f(float v) { return v; }
+
+// F[r] += y[r] + bias (if y); out[r] = LN(F[r]) * g + b + pe[r] (if out).
+__device__ __forceinline__ void store_out(__nv_bfloat16* p, double v) { *p = __float2bfloat16((float)v); }
+__device__ __forceinline__ void store_out(float* p, double v) { *p = (float)v; }
+__device__ __forceinline__ void store_out(double* p, double v) { *p = v; }
+
+template <typename FT, typename OT>
+__global__ void row_ln_kernel(FT* __restrict__ F, int64_t ldf, const __nv_bfloat16* __restrict__ y,
+                              int64_t ldy, const float* __restrict__ ybias,
+                              const float* __restrict__ gain, const float* __restrict__ beta,
+                              const float* __restrict__ pe, int64_t ldpe,
+                              OT* __restrict__ out, int64_t ldo, int64_t n, int d,
+                              double eps) {
+    using A = typename Acc<FT>::type;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    if (row >= n) return;
+    A v[kMaxPerLane];
+    const int per = (d + 31) / 32;
+    FT* fr = F + row * ldf;
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+        if (j >= per) break;
+        const int c = lane + 32 * j;
+        if (c < d) {
+            A x = (A)fr[c];
+            if (y) {
+                x += (A)to_f(y[row * ldy + c]) + (ybias ? (A)ybias[c] : (A)0);
+                fr[c] = (FT)x;
+            }
+            v[j] = x;
+        } else {
+            v[j] = 0;
+        }
+    }
+    if (!out) return;
+    A s = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+        if (j >= per) break;
+        s += v[j];
+    }
+    s = warp_sum(s);
+    const A mean = s / (A)d;
+    A q = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+        if (j >= per) break;
+        const int c = lane + 32 * j;
+        if (c < d) {
+            const A t = v[j] - mean;
+            q += t * t;
+        }
+    }
+    q = warp_sum(q);
+    const A rstd = (A)1 / sqrt(q / (A)d + (A)eps);
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+        if (j >= per) break;
+        const int c = lane + 32 * j;
+        if (c < d) {
+            A o = (v[j] - mean) * rstd * (A)gain[c] + (A)beta[c];
+            if (pe) o += (A)pe[row * ldpe + c];
+            store_out(out + row * ldo + c, (double)o);
+        }
+    }
+}
+
+// u = gelu(u + b), exact erf form, in place on bf16 rows.
+__global__ void bias_gelu_kernel(__nv_bfloat16* __restrict__ u, int64_t n, int dh,
+                                 const float* __restrict__ b) {
+    const int64_t tot2 = n * dh / 2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot2;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)((2 * t) % dh);
+        __nv_bfloat162 p = reinterpret_cast<__nv_bfloat162*>(u)[t];
+        float x0 = __bfloat162float(p.x) + b[c], x1 = __bfloat162float(p.y) + b[c + 1];
+        x0 = 0.5f * x0 * (1.f + erff(x0 * 0.70710678118654752f));
+        x1 = 0.5f * x1 * (1.f + erff(x1 * 0.70710678118654752f));
+        reinterpret_cast<__nv_bfloat162*>(u)[t] = __floats2bfloat162_rn(x0, x1);
+    }
+}
+
+}  // namespace stage
+}  // namespace f3d
+
+using namespace f3d;
+
+static inline unsigned grid_for(int64_t work, int threads) {
+    int64_t g = (work + threads - 1) / threads;
+    const int64_t cap = (int64_t)f3d_num_sms() * 16;
+    if (g > cap) g = cap;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
+extern "C" int f3d_coord_bbox(const double* coords, int64_t n, double* ws, double* lo_ext,
+                              void* stream) {
+    if (n < 1) return F3D_ERR_EMPTY;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int parts = (int)std::min<int64_t>((n + 1023) / 1024, 296);
+    stage::bbox_partial_kernel<<<parts, stage::kThreads, 0, st>>>(coords, n, ws);
+    stage::bbox_final_kernel<<<1, 32, 0, st>>>(ws, parts, lo_ext);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_positional_encoding(const double* coords, int64_t n, int d, double base,
+                                       int out_f64, void* out, int64_t ld, void* stream) {
+    return f3d_stage_pe(coords, n, d, base, nullptr, out_f64 ? 2 : 1, out, ld, stream);
+}
+
+extern "C" int f3d_stage_pe(const double* coords, int64_t n, int d, double base,
+                            const double* lo_ext, int out_kind, void* out, int64_t ld,
+                            void* stream) {
+    if (d % 6 || d < 6 || n < 0) return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t work = n * 3 * (d / 6);
+    const unsigned g = grid_for(work, stage::kThreads);
+    if (out_kind == 2)
+        stage::pe_kernel<double><<<g, stage::kThreads, 0, st>>>(coords, n, d, base, lo_ext,
+                                                                (double*)out, ld);
+    else
+        stage::pe_kernel<float><<<g, stage::kThreads, 0, st>>>(coords, n, d, base, lo_ext,
+                                                               (float*)out, ld);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+template <typename FT>
+static void launch_row_ln(unsigned g, cudaStream_t st, void* F, int64_t ldf, const void* y,
+                          int64_t ldy, const float* ybias, const float* gain, const float* beta,
+                          const float* pe, int64_t ldpe, void* out, int out_kind, int64_t ldo,
+                          int64_t n, int d, double eps) {
+    const __nv_bfloat16* yy = (const __nv_bfloat16*)y;
+    if (out_kind == 2)
+        stage::row_ln_kernel<FT, double><<<g, stage::kThreads, 0, st>>>(
+            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pe, ldpe, (double*)out, ldo, n, d, eps);
+    else if (out_kind == 1)
+        stage::row_ln_kernel<FT, float><<<g, stage::kThreads, 0, st>>>(
+            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pe, ldpe, (float*)out, ldo, n, d, eps);
+    else
+        stage::row_ln_kernel<FT, __nv_bfloat16><<<g, stage::kThreads, 0, st>>>(
+            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pe, ldpe, (__nv_bfloat16*)out, ldo, n, d,
+            eps);
+}
+
+extern "C" int f3d_row_ln(void* F, int f_is_f64, int64_t ldf, const void* y, int64_t ldy,
+                          const float* ybias, const float* gain, const float* beta,
+                          const float* pe, int64_t ldpe, void* out, int out_kind, int64_t ldo,
+                          int64_t n, int d, double eps, void* stream) {
+    if (d < 1 || d > 32 * stage::kMaxPerLane || n < 0 || out_kind < 0 || out_kind > 2)
+        return F3D_ERR_CONFIG;
+    if (out && (!gain || !beta)) return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g = (unsigned)((n + stage::kThreads / 32 - 1) / (stage::kThreads / 32));
+    if (f_is_f64)
+        launch_row_ln<double>(g, st, F, ldf, y, ldy, ybias, gain, beta, pe, ldpe, out, out_kind,
+                              ldo, n, d, eps);
+    else
+        launch_row_ln<float>(g, st, F, ldf, y, ldy, ybias, gain, beta, pe, ldpe, out, out_kind,
+                             ldo, n, d, eps);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+namespace f3d {
+namespace stage {
+__global__ void gelu_f64_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ y) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = x[i];
+        y[i] = 0.5 * v * (1.0 + erf(v / sqrt(2.0)));
+    }
+}
+}  // namespace stage
+}  // namespace f3d
+
+extern "C" int f3d_gelu_f64(const double* x, int64_t n, double* y, void* stream) {
+    if (n < 0) return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    stage::gelu_f64_kernel<<<grid_for(n, stage::kThreads), stage::kThreads, 0,
+                             (cudaStream_t)stream>>>(x, n, y);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_bias_gelu(void* u_bf16, int64_t n, int dh, const float* bias, void* stream) {
+    if (dh < 2 || dh % 2 || n < 0) return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    stage::bias_gelu_kernel<<<grid_for(n * dh / 2, stage::kThreads), stage::kThreads, 0, st>>>(
+        (__nv_bfloat16*)u_bf16, n, dh, bias);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}

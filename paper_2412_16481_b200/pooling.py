@@ -1,0 +1,242 @@
+"""In-bucket pooling on the GPU.
+
+Drop-in for bw/pooling.py.  ``build_subbuckets`` / ``pool_stage`` run the
+one-warp-per-tile partition kernel of csrc/pool.cu (bit-identical sub-bucket
+ids, sizes and seeds, float64 distances without contraction) and
+``pool_features`` the member-ordered reduce (sequential in index order, so
+float64 centroids match the reference bit for bit).
+"""
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .bucketing import BucketAssignment
+from .errors import ConfigError, EmptyInputError, IntegrityError
+
+TILE_CAP = 1024
+REDUCES = ("sum", "mean", "min", "max")
+_OP = {"sum": 0, "mean": 1, "min": 2, "max": 3}
+_FLAG_MSGS = ((1, "sub-bucket allocation fell short of the target"),
+              (2, "step 3 found no under-filled sub-bucket"),
+              (4, "a sub-bucket exceeds capacity rho"),
+              (8, "empty sub-bucket"),
+              (16, "more than one under-filled sub-bucket"),
+              (32, "sub-bucket id out of range"))
+
+
+def _raise_flags(f: int):
+    for bit, msg in _FLAG_MSGS:
+        if f & bit:
+            raise IntegrityError(msg)
+
+
+@dataclass
+class SubBucketAssignment:
+    """Partition of one tile (bw/pooling.py:26-56)."""
+
+    subbucket_id: np.ndarray
+    rho: int
+    num_subbuckets: int
+    sizes: np.ndarray
+    seeds: np.ndarray
+    scan_passes: int = 0
+    _members: object = field(default=None, repr=False, compare=False)
+
+    def validate(self) -> None:
+        sid = np.asarray(self.subbucket_id.cpu() if isinstance(self.subbucket_id, torch.Tensor)
+                         else self.subbucket_id)
+        sizes = np.asarray(self.sizes.cpu() if isinstance(self.sizes, torch.Tensor) else self.sizes)
+        m = len(sid)
+        if sizes.shape != (self.num_subbuckets,):
+            raise IntegrityError("sizes shape mismatch")
+        if int(sizes.sum()) != m:
+            raise IntegrityError("sub-bucket sizes do not sum to the tile size")
+        counted = np.bincount(sid, minlength=self.num_subbuckets)
+        if not np.array_equal(counted, sizes):
+            raise IntegrityError("sizes disagree with subbucket_id")
+        if (sizes > self.rho).any():
+            raise IntegrityError("a sub-bucket exceeds capacity rho")
+        if (sizes < 1).any():
+            raise IntegrityError("empty sub-bucket")
+        if int((sizes < self.rho).sum()) > 1:
+            raise IntegrityError("more than one under-filled sub-bucket")
+
+
+class TilePlan:
+    """<=1024-row tiles of every non-empty slot in scatter order, with the
+    first pooled row of each tile (bw/pooling.py:211-225)."""
+
+    def __init__(self, counts, base, rho, dev):
+        counts = np.asarray(counts, dtype=np.int64)
+        base = np.asarray(base, dtype=np.int64)
+        reps = -(-counts // TILE_CAP)
+        slot_of_tile = np.repeat(np.arange(len(counts)), reps)
+        first_tile = np.cumsum(reps) - reps
+        k = np.arange(len(slot_of_tile)) - np.repeat(first_tile, reps)
+        starts = base[slot_of_tile] + k * TILE_CAP
+        m = np.minimum(TILE_CAP, counts[slot_of_tile] - k * TILE_CAP)
+        targets = -(-m // rho)
+        out = np.cumsum(targets) - targets
+        self.ntiles = len(m)
+        self.npool = int(targets.sum())
+        self.slot_of_tile = slot_of_tile
+        self.targets = targets
+        self.new_counts = np.bincount(slot_of_tile, weights=targets, minlength=len(counts)).astype(np.int64)
+        i32 = lambda a: torch.tensor(np.asarray(a, dtype=np.int32), device=dev)
+        self.tile_start = i32(starts if self.ntiles else [0])
+        self.tile_m = i32(m if self.ntiles else [0])
+        self.tile_out = i32(out if self.ntiles else [0])
+
+
+def _build(coords_dev, plan: TilePlan, rho: int, want_sub=False, want_seeds=False):
+    n = coords_dev.shape[0]
+    members = L.empty((max(1, plan.npool), rho), torch.int32)
+    sizes = L.empty((max(1, plan.npool),), torch.int32)
+    seeds = L.empty((max(1, plan.npool),), torch.int32) if want_seeds else None
+    sub = L.empty((max(1, n),), torch.int32) if want_sub else None
+    passes = L.empty((max(1, plan.ntiles),), torch.int32) if want_seeds else None
+    flags = L.empty((1,), torch.int32)
+    L.call("f3d_pool_build", L.ptr(coords_dev), L.ptr(plan.tile_start), L.ptr(plan.tile_m),
+           L.ptr(plan.tile_out), plan.ntiles, rho, L.ptr(sub), L.ptr(members), L.ptr(sizes),
+           L.ptr(seeds), L.ptr(passes), L.ptr(flags), L.stream())
+    return members, sizes, seeds, sub, passes, flags
+
+
+def _reduce(x, members, sizes, npool, rho, reduce):
+    if x.dtype == torch.float64:
+        dt = 2
+    elif x.dtype == torch.float32:
+        dt = 1
+    elif x.dtype == torch.bfloat16:
+        dt = 0
+    else:
+        x = x.to(torch.float64)
+        dt = 2
+    x = x.contiguous()
+    out = torch.empty((npool, x.shape[1]), dtype=x.dtype, device=x.device)
+    L.call("f3d_pool_reduce", L.ptr(x), dt, x.stride(0), x.shape[1], L.ptr(members),
+           L.ptr(sizes), npool, rho, _OP[reduce], L.ptr(out), out.stride(0), L.stream())
+    return out
+
+
+def build_subbuckets(coords, rho: int) -> SubBucketAssignment:
+    """Partition one tile of m <= 1024 points into ceil(m / rho) sub-buckets
+    (bw/pooling.py:68-163)."""
+    host = L.is_host(coords)
+    c = L.to_dev(coords, torch.float64)
+    if c.ndim != 2 or c.shape[1] != 3:
+        raise ConfigError(f"coords must be (m, 3), got {tuple(c.shape)}")
+    m = c.shape[0]
+    if m == 0:
+        raise EmptyInputError("build_subbuckets needs at least one point")
+    if m > TILE_CAP:
+        raise ConfigError(f"tile holds {m} points; the cap is {TILE_CAP}")
+    if rho < 1:
+        raise ConfigError(f"rho must be >= 1, got {rho}")
+    if rho > 64:
+        raise ConfigError("the GPU partition kernel supports rho <= 64")
+    plan = TilePlan([m], [0], rho, c.device)
+    members, sizes, seeds, sub, passes, flags = _build(c.contiguous(), plan, rho, True, True)
+    _raise_flags(int(flags.item()))
+    target = plan.npool
+    res = SubBucketAssignment(
+        subbucket_id=L.out(sub[:m].to(torch.int64), host), rho=rho, num_subbuckets=target,
+        sizes=L.out(sizes[:target].to(torch.int64), host),
+        seeds=L.out(seeds[:target].to(torch.int64), host), scan_passes=int(passes[0].item()),
+        _members=(members, sizes))
+    return res
+
+
+def pool_features(features, sub: SubBucketAssignment, reduce: str = "mean"):
+    """Reduce each sub-bucket's rows to one row, in sub-bucket id order
+    (bw/pooling.py:166-184)."""
+    if reduce not in REDUCES:
+        raise ConfigError(f"reduce must be one of {REDUCES}, got {reduce!r}")
+    host = L.is_host(features)
+    x = L.to_dev(features, torch.float64) if host else features.to(L.device())
+    if x.ndim == 1:
+        x = x[:, None]
+    if x.shape[0] != len(sub.subbucket_id):
+        raise ConfigError("features rows do not match the sub-bucket assignment")
+    sub.validate()
+    if sub._members is not None:
+        members, sizes = sub._members
+    else:
+        sid = np.asarray(sub.subbucket_id.cpu() if isinstance(sub.subbucket_id, torch.Tensor)
+                         else sub.subbucket_id, dtype=np.int64)
+        order = np.argsort(sid, kind="stable")
+        sz = np.bincount(sid, minlength=sub.num_subbuckets)
+        mem = np.full((sub.num_subbuckets, sub.rho), -1, dtype=np.int32)
+        pos = np.arange(len(sid)) - np.repeat(np.cumsum(sz) - sz, sz)
+        mem[sid[order], pos] = order
+        members = L.to_dev(mem, torch.int32)
+        sizes = L.to_dev(sz, torch.int32)
+    out = _reduce(x, members, sizes, sub.num_subbuckets, sub.rho, reduce)
+    return L.out(out, host)
+
+
+def pool_stage(features, coords, assignment: BucketAssignment, rho: int, reduce: str = "mean"):
+    """Pool every bucket slot by rho (bw/pooling.py:187-242).  Returns
+    (pooled_features, pooled_coords, new_assignment)."""
+    host = L.is_host(features)
+    if isinstance(features, torch.Tensor):
+        x = features.to(L.device())
+    else:
+        x = L.to_dev(np.asarray(features, dtype=np.float64), torch.float64)
+    C = L.to_dev(coords, torch.float64).contiguous()
+    if x.shape[0] != len(assignment) or tuple(C.shape) != (x.shape[0], 3):
+        raise ConfigError("features/coords must match the assignment size")
+    if rho < 1:
+        raise ConfigError(f"rho must be >= 1, got {rho}")
+    if rho > 64:
+        raise ConfigError("the GPU partition kernel supports rho <= 64")
+    if reduce not in REDUCES:
+        raise ConfigError(f"reduce must be one of {REDUCES}, got {reduce!r}")
+    K, S = assignment.K, assignment.S
+    m = assignment._mirrors()
+    counts = m["counts"].cpu().numpy().astype(np.int64)
+    base = m["base"].cpu().numpy().astype(np.int64)
+    res = pool_device(x, C, counts, base, K, S, assignment.num_batches, rho, reduce)
+    pf, pc, na = res
+    if host:
+        return pf.cpu().numpy(), pc.cpu().numpy(), na.to_host()
+    return pf, pc, na
+
+
+def pool_device(x, C, counts, base, K, S, nbatch, rho, reduce, check=True):
+    """Device path of pool_stage given host counts/base; returns device
+    tensors and a device-resident BucketAssignment."""
+    plan = TilePlan(counts, base, rho, x.device)
+    members, sizes, _, _, _, flags = _build(C, plan, rho)
+    if check:
+        _raise_flags(int(flags.item()))
+    pf = _reduce(x, members, sizes, plan.npool, rho, reduce)
+    pc = _reduce(C, members, sizes, plan.npool, rho, "mean")
+    na = new_assignment(plan.new_counts, K, max(1, math.ceil(S / rho)), nbatch, x.device)
+    return pf, pc, na
+
+
+def new_assignment(new_counts, K, S_new, nbatch, dev) -> BucketAssignment:
+    """Assignment of the pooled rows: bucket identity kept, offsets 0..c-1 in
+    slot order, so the pooled rows are already in scattered order."""
+    nc = torch.tensor(new_counts, dtype=torch.int64, device=dev)
+    nslots = len(new_counts)
+    slots = torch.repeat_interleave(torch.arange(nslots, device=dev), nc)
+    base = torch.zeros_like(nc)
+    if nslots > 1:
+        base[1:] = torch.cumsum(nc[:-1], 0)
+    npool = int(sum(new_counts))
+    offs = torch.arange(npool, device=dev) - base[slots]
+    bid = slots % (K + 1)
+    bat = slots // (K + 1)
+    a = BucketAssignment(bucket_id=bid, bucket_offset=offs, counts=nc, bucket_base=base, S=S_new,
+                         K=K, batch_id=bat, num_batches=nbatch,
+                         _dev={"id": bid.to(torch.int32), "off": offs.to(torch.int32),
+                               "counts": nc.to(torch.int32), "base": base.to(torch.int32),
+                               "batch": bat.to(torch.int32) if nbatch > 1 else None,
+                               "dest": torch.arange(npool, device=dev, dtype=torch.int32)})
+    return a

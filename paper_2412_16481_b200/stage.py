@@ -1,0 +1,224 @@
+"""Pre-norm transformer stage over bucket-swin scopes, on the GPU.
+
+Drop-in for bw/stage.py.  Per round (bw/stage.py:134-158):
+
+    x  = LN1(F) + PE(C)                 f3d_row_ln (fused with the previous
+                                        round's MLP residual) -> bf16
+    QKV = x @ [Wq|Wk|Wv] + b            one bf16 GEMM (cuBLAS, library GEMM)
+    A  = bucket-swin MHSA per scope     f3d_bswin_attention, one launch/round
+    F += A @ Wo + bo ; h = LN2(F)       GEMM + f3d_row_ln (fused residual+LN)
+    F += gelu(h @ Win + bin) @ Wout + bout    GEMM, f3d_bias_gelu, GEMM, row_ln
+
+The residual stream F stays in the caller's float precision (float64 for host
+float64 input, so zeroed branches leave F byte-identical as in
+pkg/tests/test_stage.py:75-84; float32 otherwise); GEMM operands are bf16 with
+fp32 accumulation.  Rows never move: attention reads each scope in place.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .attention import AttentionParams, ScopeSchedule, attend, plan_schedule
+from .bucketing import BucketAssignment
+from .errors import ConfigError
+
+LN_EPS = 1e-12
+
+
+@dataclass
+class StageParams:
+    """Projection, norm and MLP weights for one stage (bw/stage.py:25-54)."""
+
+    attention: AttentionParams
+    w_q: np.ndarray
+    w_k: np.ndarray
+    w_v: np.ndarray
+    w_o: np.ndarray
+    b_q: np.ndarray
+    b_k: np.ndarray
+    b_v: np.ndarray
+    b_o: np.ndarray
+    ln1_gain: np.ndarray
+    ln1_bias: np.ndarray
+    ln2_gain: np.ndarray
+    ln2_bias: np.ndarray
+    w_in: np.ndarray
+    b_in: np.ndarray
+    w_out: np.ndarray
+    b_out: np.ndarray
+    seed: int = 0
+
+    @property
+    def d_model(self) -> int:
+        return self.attention.d_model
+
+    @property
+    def d_hidden(self) -> int:
+        return self.w_in.shape[1]
+
+    def device_weights(self):
+        """bf16 GEMM operands and fp32 vectors on the device.  Rebuilt on every
+        call so in-place edits of the host arrays are honoured."""
+        f = lambda a, dt: L.to_dev(a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a, dt)
+        bf, f32 = torch.bfloat16, torch.float32
+        return {
+            "w_qkv": torch.cat([f(self.w_q, bf), f(self.w_k, bf), f(self.w_v, bf)], 1).contiguous(),
+            "b_qkv": torch.cat([f(self.b_q, bf), f(self.b_k, bf), f(self.b_v, bf)]).contiguous(),
+            "w_o": f(self.w_o, bf), "b_o": f(self.b_o, f32),
+            "w_in": f(self.w_in, bf), "b_in": f(self.b_in, f32),
+            "w_out": f(self.w_out, bf), "b_out": f(self.b_out, f32),
+            "ln1_g": f(self.ln1_gain, f32), "ln1_b": f(self.ln1_bias, f32),
+            "ln2_g": f(self.ln2_gain, f32), "ln2_b": f(self.ln2_bias, f32),
+        }
+
+
+def init_params(seed: int, d_model: int, d_hidden=None, n_heads: int = 4,
+                tile_rows: int = 64) -> StageParams:
+    """Seeded init (bw/stage.py:57-81): U(+-sqrt(3/fan_in)) drawn in the order
+    q, k, v, o, in, out on the host with the reference's PCG64 stream, so the
+    weights are bit-identical; biases zero, LN gains one."""
+    if d_hidden is None:
+        d_hidden = 4 * d_model
+    attn = AttentionParams(d_model=d_model, n_heads=n_heads, tile_rows=tile_rows)
+    rng = np.random.default_rng(seed)
+
+    def mat(fan_in, fan_out):
+        bound = np.sqrt(3.0 / fan_in)
+        return rng.uniform(-bound, bound, size=(fan_in, fan_out))
+
+    return StageParams(
+        attention=attn,
+        w_q=mat(d_model, d_model), w_k=mat(d_model, d_model),
+        w_v=mat(d_model, d_model), w_o=mat(d_model, d_model),
+        b_q=np.zeros(d_model), b_k=np.zeros(d_model), b_v=np.zeros(d_model), b_o=np.zeros(d_model),
+        ln1_gain=np.ones(d_model), ln1_bias=np.zeros(d_model),
+        ln2_gain=np.ones(d_model), ln2_bias=np.zeros(d_model),
+        w_in=mat(d_model, d_hidden), b_in=np.zeros(d_hidden),
+        w_out=mat(d_hidden, d_model), b_out=np.zeros(d_model), seed=seed)
+
+
+def layer_norm(x, gain, bias, eps: float = 1e-12):
+    """(x - mean) / sqrt(var + eps) * gain + bias, population variance
+    (bw/stage.py:84-88); f3d_row_ln in float64 for host float64 input."""
+    host = L.is_host(x)
+    t = L.to_dev(x, torch.float64).contiguous()
+    shp = t.shape
+    t2 = t.reshape(-1, shp[-1]).clone()
+    n, d = t2.shape
+    out = L.empty((n, d), torch.float64)
+    g = L.to_dev(gain, torch.float32)
+    b = L.to_dev(bias, torch.float32)
+    L.call("f3d_row_ln", L.ptr(t2), 1, d, None, 0, None, L.ptr(g), L.ptr(b), None, 0,
+           L.ptr(out), 2, d, n, d, float(eps), L.stream())
+    return L.out(out.reshape(shp), host)
+
+
+def gelu(x):
+    """Exact-erf GELU in float64 (bw/stage.py:91-92), f3d_gelu_f64."""
+    host = L.is_host(x)
+    t = L.to_dev(x, torch.float64).contiguous()
+    out = torch.empty_like(t)
+    L.call("f3d_gelu_f64", L.ptr(t), t.numel(), L.ptr(out), L.stream())
+    return L.out(out, host)
+
+
+class StageRunner:
+    """Device-resident execution of one stage over a fixed scattered layout:
+    weights, positional encoding and per-round attention plans are built once;
+    ``run(F)`` then executes every round with no host synchronisation."""
+
+    def __init__(self, coords, table, schedule: ScopeSchedule, params: StageParams, n: int,
+                 f_dtype=torch.float32):
+        dev = L.device()
+        self.p = params
+        self.n = n
+        self.d = params.d_model
+        self.H = params.attention.n_heads
+        self.dh = params.attention.head_dim
+        self.w = params.device_weights()
+        self.plans = plan_schedule(table, schedule, dev)
+        self.f_dtype = f_dtype
+        c = L.to_dev(coords, torch.float64).contiguous()
+        self.pe = L.empty((n, self.d), torch.float32)
+        ws = L.empty((6 * 296,), torch.float64)
+        self.lo_ext = L.empty((6,), torch.float64)
+        L.call("f3d_coord_bbox", L.ptr(c), n, L.ptr(ws), L.ptr(self.lo_ext), L.stream())
+        L.call("f3d_stage_pe", L.ptr(c), n, self.d, 10000.0, L.ptr(self.lo_ext), 1,
+               L.ptr(self.pe), self.d, L.stream())
+        d, dhid = self.d, params.d_hidden
+        self.x = L.empty((n, d), torch.bfloat16)
+        self.qkv = L.empty((n, 3 * d), torch.bfloat16)
+        self.a = L.empty((n, d), torch.bfloat16)
+        self.y = L.empty((n, d), torch.bfloat16)
+        self.u = L.empty((n, dhid), torch.bfloat16)
+
+    def _row_ln(self, F, y, ybias, g, b, pe, out):
+        L.call("f3d_row_ln", L.ptr(F), int(F.dtype == torch.float64), F.stride(0), L.ptr(y),
+               0 if y is None else y.stride(0), L.ptr(ybias), L.ptr(g), L.ptr(b), L.ptr(pe),
+               0 if pe is None else pe.stride(0), L.ptr(out), 0,
+               0 if out is None else out.stride(0), self.n, self.d, LN_EPS, L.stream())
+
+    def run(self, F: torch.Tensor) -> torch.Tensor:
+        """F: (n, d) residual stream on the device (float32/float64), updated
+        in place and returned."""
+        w = self.w
+        q, k, v = (self.qkv[:, i * self.d:(i + 1) * self.d] for i in range(3))
+        self._row_ln(F, None, None, w["ln1_g"], w["ln1_b"], self.pe, self.x)
+        R = len(self.plans)
+        for t, plan in enumerate(self.plans):
+            torch.addmm(w["b_qkv"], self.x, w["w_qkv"], out=self.qkv)
+            attend(q, k, v, self.a, plan, self.H, self.dh)
+            torch.mm(self.a, w["w_o"], out=self.y)
+            self._row_ln(F, self.y, w["b_o"], w["ln2_g"], w["ln2_b"], None, self.x)
+            torch.mm(self.x, w["w_in"], out=self.u)
+            L.call("f3d_bias_gelu", L.ptr(self.u), self.n, self.u.shape[1], L.ptr(w["b_in"]),
+                   L.stream())
+            torch.mm(self.u, w["w_out"], out=self.y)
+            if t + 1 < R:
+                self._row_ln(F, self.y, w["b_out"], w["ln1_g"], w["ln1_b"], self.pe, self.x)
+            else:
+                self._row_ln(F, self.y, w["b_out"], None, None, None, None)
+        return F
+
+    def attention_flops(self) -> int:
+        """Algorithmic attention FLOPs per run: sum over rounds and scopes of
+        4 * m_s^2 * d."""
+        return sum(4 * p.flops_per_head * self.d for p in self.plans)
+
+
+def stage_forward(features, coords, assignment: BucketAssignment, schedule: ScopeSchedule,
+                  params: StageParams, threads: int = 1):
+    """Run every round of the schedule over scattered features
+    (bw/stage.py:99-159); ``threads`` is accepted and ignored."""
+    host = L.is_host(features)
+    if isinstance(features, torch.Tensor):
+        F = features.to(L.device()).clone()
+        if F.dtype not in (torch.float32, torch.float64):
+            F = F.to(torch.float32)
+    else:
+        F = L.to_dev(np.array(features, dtype=np.float64, copy=True), torch.float64)
+    C = L.to_dev(coords, torch.float64)
+    if assignment.num_batches != 1:
+        raise ConfigError("stage_forward expects a single-batch assignment; process batches separately")
+    if F.ndim != 2 or F.shape[0] != len(assignment):
+        raise ConfigError("features must be (N, d) matching the assignment")
+    if tuple(C.shape) != (F.shape[0], 3):
+        raise ConfigError("coords must be (N, 3) matching features")
+    if F.shape[1] != params.d_model:
+        raise ConfigError(f"feature width {F.shape[1]} != d_model {params.d_model}")
+    if assignment.S % 16:
+        raise ConfigError(f"attention consumes buckets in 16-row tiles; "
+                          f"S={assignment.S} is not a multiple of 16")
+    table = assignment.bucket_table(split_recycle=True)
+    if schedule.num_buckets != len(table[0]):
+        raise ConfigError(
+            f"schedule covers {schedule.num_buckets} buckets but the assignment "
+            f"has {len(table[0])} (regular + recycle chunks)")
+    if params.d_model % 6:
+        raise ConfigError(f"d_model must be divisible by 6, got {params.d_model}")
+    runner = StageRunner(C, table, schedule, params, F.shape[0], F.dtype)
+    runner.run(F)
+    return L.out(F, host)

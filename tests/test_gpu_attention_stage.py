@@ -1,0 +1,197 @@
+"""GPU parity for bucket-swin attention, positional encoding and the stage
+against golden fixtures (reference output) and the CPU oracle.
+
+Tolerances (measured bf16 emulation): attention per scope
+<= 1e-2 relative Frobenius, stage <= 2e-2."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import restated as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2412_16481_b200 as F  # noqa: E402
+from paper_2412_16481_b200.errors import ConfigError, NumericError  # noqa: E402
+
+ATT_TOL = 1e-2
+STAGE_TOL = 2e-2
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def test_attention_golden():
+    g = load_golden("attention.npz")
+    for i, (m, d, H) in enumerate(((16, 64, 4), (100, 64, 4), (300, 96, 4), (200, 48, 2),
+                                   (130, 128, 1), (64, 32, 2))):
+        p = F.AttentionParams(d_model=d, n_heads=H)
+        out = F.tiled_attention(g[f"a{i}_Q"], g[f"a{i}_K"], g[f"a{i}_V"], p, ranges=[(0, m)])
+        assert out.shape == (m, d)
+        assert rel(out, g[f"a{i}_out"]) < ATT_TOL, (i, rel(out, g[f"a{i}_out"]))
+        dense = F.reference_attention(g[f"a{i}_Q"], g[f"a{i}_K"], g[f"a{i}_V"], p)
+        assert rel(dense, g[f"a{i}_out"]) < ATT_TOL
+
+
+def test_attention_ranges_and_mask_golden():
+    g = load_golden("attention.npz")
+    rg = [tuple(r) for r in g["rg_ranges"]]
+    out = F.tiled_attention(g["rg_Q"], g["rg_K"], g["rg_V"], F.AttentionParams(64, 4), ranges=rg,
+                            mask=g["rg_mask"])
+    ref = g["rg_out"]
+    assert out.shape == ref.shape
+    assert rel(out, ref) < ATT_TOL
+    # masked query rows are exactly zero
+    rows = np.concatenate([np.arange(a, b) for a, b in rg])
+    assert np.all(out[~g["rg_mask"][rows]] == 0)
+
+
+def test_positional_encoding_golden():
+    g = load_golden("attention.npz")
+    np.testing.assert_allclose(F.positional_encoding(g["pe_coords"], 96), g["pe_96"], atol=1e-12)
+    np.testing.assert_allclose(F.positional_encoding(g["pe_coords"], 12), g["pe_12"], atol=1e-12)
+    with pytest.raises(ConfigError):
+        F.positional_encoding(g["pe_coords"], 64)
+
+
+@pytest.mark.parametrize("d,H", [(64, 4), (96, 4), (384, 4), (512, 4), (12, 2), (40, 5), (256, 2)])
+def test_attention_random_scopes_vs_oracle(d, H):
+    """Multi-segment scopes (two disjoint ranges) and ragged lengths."""
+    r = np.random.default_rng(d * 7 + H)
+    for m in (16, 77, 200, 1000):
+        N = m + 50
+        Q, K, V = (r.normal(size=(N, d)) for _ in range(3))
+        cut = m // 2
+        ranges = [(3, 3 + cut), (3 + cut + 40, 3 + m + 40)]
+        out = F.tiled_attention(Q, K, V, F.AttentionParams(d, H), ranges=ranges)
+        ref = O.attention_ranges(Q, K, V, H, ranges)
+        assert rel(out, ref) < ATT_TOL, (d, H, m, rel(out, ref))
+
+
+def test_attention_extreme_logits_and_errors():
+    r = np.random.default_rng(0)
+    Q = r.normal(size=(128, 32)) * 30
+    K = r.normal(size=(128, 32)) * 30
+    V = r.normal(size=(128, 32))
+    out = F.tiled_attention(Q, K, V, F.AttentionParams(32, 2))
+    ref = O.attention_dense(Q, K, V, 2)
+    assert np.isfinite(out).all()
+    assert rel(out, ref) < 5e-2   # near-one-hot softmax: bf16 logits dominate the error
+    Q[3, 1] = np.nan
+    with pytest.raises(NumericError):
+        F.tiled_attention(Q, K, V, F.AttentionParams(32, 2))
+    with pytest.raises(ConfigError):
+        F.tiled_attention(K, K, V[:, :16], F.AttentionParams(32, 2))
+
+
+def test_all_masked_scope_warns():
+    r = np.random.default_rng(1)
+    Q = r.normal(size=(40, 16))
+    with pytest.warns(RuntimeWarning):
+        out = F.tiled_attention(Q, Q, Q, F.AttentionParams(16, 2), ranges=[(0, 40)],
+                                mask=np.zeros(40, dtype=bool))
+    assert np.all(out == 0)
+
+
+def test_zero_gather_bytes():
+    F.copy_meter.reset()
+    r = np.random.default_rng(2)
+    Q = r.normal(size=(300, 32))
+    F.tiled_attention(Q, Q, Q, F.AttentionParams(32, 2), ranges=[(0, 100), (150, 300)])
+    assert F.copy_meter.bytes["gather"] == 0
+    assert F.copy_meter.bytes["attention"] > 0
+
+
+# -------------------------------------------------------------------- stage
+
+@pytest.mark.parametrize("tag", ["s0", "s1"])
+def test_stage_golden(tag):
+    g = load_golden("stage.npz")
+    seed, n, K, S, d, H, W, shift, rounds = g[f"{tag}_meta"].tolist()
+    counts = g[f"{tag}_counts"]
+    base = O.exclusive_scan(counts)
+    a = F.BucketAssignment(np.zeros(n, np.int64), np.zeros(n, np.int64), counts, base, S, K)
+    table = O.bucket_table(counts, base, K, S)
+    sched = F.build_schedule(len(table[0]), W, 1, shift, rounds)
+    p = F.init_params(seed, d, n_heads=H)
+    out = F.stage_forward(g[f"{tag}_feats"], g[f"{tag}_coords"], a, sched, p)
+    assert rel(out, g[f"{tag}_out"]) < STAGE_TOL, rel(out, g[f"{tag}_out"])
+
+
+def _config_a(n=4096, seed=7, d=96):
+    coords = O.synth_cloud(seed, n, "uniform-box")
+    vox = O.remap_nonnegative(O.voxelize(coords, (0, 0, 0), 1 / 64))
+    a = F.assign_buckets(vox, None, F.HashConfig("zorder-div", K=40, S_div=6554), 128)
+    feats = np.random.default_rng(1).normal(size=(n, d))
+    sf, _ = F.scatter(feats, a)
+    sc, _ = F.scatter(coords, a)
+    return a, sf, sc
+
+
+@pytest.mark.parametrize("d,H", [(96, 4), (384, 4), (48, 2)])
+def test_stage_config_a_vs_oracle(d, H):
+    a, sf, sc = _config_a(d=d)
+    table = a.bucket_table()
+    sched = F.build_schedule(len(table[0]), 2, 1, 1, 2)
+    p = F.init_params(0, d, n_heads=H)
+    out = F.stage_forward(sf, sc, a, sched, p)
+    ref = O.stage_forward(sf, sc, table, O.build_schedule(len(table[0]), 2, 1, 1, 2),
+                          O.init_params(0, d, n_heads=H), threads=8)
+    assert rel(out, ref) < STAGE_TOL, rel(out, ref)
+
+
+def test_stage_residual_identity_is_exact():
+    a, sf, sc = _config_a(n=1024, d=12)
+    sched = F.build_schedule(len(a.bucket_table()[0]), 2)
+    p = F.init_params(1, 12, n_heads=2)
+    p.w_v[:] = 0
+    p.b_v[:] = 0
+    p.w_out[:] = 0
+    p.b_out[:] = 0
+    out = F.stage_forward(sf, sc, a, sched, p)
+    assert np.array_equal(out, sf)
+
+
+def test_stage_cross_scope_flow_needs_second_round():
+    """pkg/tests/test_stage.py:107-126 on the GPU: round 0 cannot leak across
+    scopes (bit-identical rows), round 1 does."""
+    sizes = [512, 512, 512, 512]
+    n = sum(sizes)
+    r = np.random.default_rng(3)
+    counts = np.array(sizes + [0])
+    base = O.exclusive_scan(counts)
+    ids = np.repeat(np.arange(4), sizes)
+    offs = np.concatenate([np.arange(s) for s in sizes])
+    a = F.BucketAssignment(ids, offs, counts, base, 512, 4)
+    feats = r.normal(size=(n, 12))
+    coords = r.uniform(size=(n, 3))
+    p = F.init_params(2, 12, n_heads=2)
+    zeroed = feats.copy()
+    zeroed[1024:1536] = 0.0
+    one = F.build_schedule(4, 2, shift=1, rounds=1)
+    np.testing.assert_array_equal(F.stage_forward(feats, coords, a, one, p)[512:1024],
+                                  F.stage_forward(zeroed, coords, a, one, p)[512:1024])
+    two = F.build_schedule(4, 2, shift=1, rounds=2)
+    diff = np.linalg.norm(F.stage_forward(feats, coords, a, two, p)[512:1024]
+                          - F.stage_forward(zeroed, coords, a, two, p)[512:1024])
+    assert diff > 0
+
+
+def test_stage_errors():
+    a, sf, sc = _config_a(n=512, d=12)
+    p = F.init_params(0, 12, n_heads=2)
+    with pytest.raises(ConfigError):
+        F.stage_forward(sf, sc, a, F.build_schedule(3, 2), p)      # wrong bucket count
+    p64 = F.init_params(0, 64, n_heads=4)
+    with pytest.raises(ConfigError):
+        F.stage_forward(np.zeros((512, 64)), sc, a, F.build_schedule(len(a.bucket_table()[0]), 2), p64)
+
+
+def test_layer_norm_and_gelu_f64():
+    r = np.random.default_rng(4)
+    x = r.normal(size=(50, 24))
+    g, b = r.normal(size=24), r.normal(size=24)
+    np.testing.assert_allclose(F.layer_norm(x, g, b), O.layer_norm(x, g, b), rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(F.gelu(x), O.gelu(x), rtol=1e-12, atol=1e-14)
