@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Flash3D forward points/sec on B200 (BASELINE.json metric).
+
+Default workload = BASELINE.json configs[1] / SURVEY.md §8(d) config B: a
+ScanNet-sized synthetic scene (synth_cloud seed 7+rank, 100K points,
+uniform-box) through the full 2-stage backbone forward (PSH -> scatter ->
+2-round bucket-swin stage C=96 H=4 -> pool rho=2 -> PSH on the pooled
+centroids -> stage), bf16 GEMM/attention operands, fp32 residual stream.
+One step = one backbone forward of one scene per GPU (weak scaling: every
+rank owns its own scene, no data-path collective; timing is max over ranks).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+``--impl reference`` times the reference's CPU implementation of the path
+(the oracle port in oracle/, numpy float64 + the C claim loop, all host
+threads) on rank 0 on a bounded sample of the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Flash3D forward points/sec at 1/2/4/8 B200; bucket-swin attn TFLOPS vs peak"
+N_POINTS = 100_000
+D_MODEL = 96
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            j = json.load(fh)
+        return j["hbm_gbs"], j["bf16_tflops"], "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def workload(rank):
+    from oracle.restated import synth_cloud   # input generation only (same PCG64 draws)
+    coords = synth_cloud(7 + rank, N_POINTS, "uniform-box")
+    feats = np.random.default_rng(1 + rank).normal(size=(N_POINTS, D_MODEL))
+    return coords, feats
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- CPU legs
+
+def cpu_forward_sample(coords, feats, threads, per_thread=2):
+    """One oracle backbone forward; attention sampled to per_thread*threads
+    scopes per round and extrapolated linearly in the scope count.  Returns
+    (seconds, scopes run, scopes total)."""
+    from oracle import restated as O
+    from paper_2412_16481_b200.backbone import scannet_backbone
+    tm = []
+    O.backbone_forward(coords, feats, scannet_backbone(), threads=threads,
+                       scope_limit=per_thread * threads, timings=tm)
+    total = sum(t["psh_scatter"] + t["stage_extrapolated"] + t["pool"] for t in tm)
+    ran = sum(t["scopes_run"] for t in tm)
+    scopes = sum(t["scopes"] for t in tm)
+    return total, ran, scopes
+
+
+def cpu_baseline(coords, feats):
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    sec, ran, scopes = cpu_forward_sample(coords, feats, threads)
+    wall = time.perf_counter() - t0
+    return {"value": N_POINTS / sec, "unit": "points/s", "cores": threads, "kind": "port",
+            "sample": (f"oracle backbone forward on the same 100K scene; PSH/scatter/pool and all "
+                       f"projections/LN/MLP at full size, attention on {ran} of {scopes} scopes "
+                       f"extrapolated linearly ({wall:.1f}s of CPU work)")}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    coords, feats = workload(0)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_forward_sample(coords, feats, threads, 1)
+    times = []
+    for _ in range(args.steps):
+        sec, ran, scopes = cpu_forward_sample(coords, feats, threads, 1)
+        times.append(sec)
+    ms = 1e3 * sum(times) / len(times)
+    value = N_POINTS / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (synth_cloud uniform-box, seed 7; features default_rng(1).normal)",
+            "impl": "reference",
+            "config": {"workload": "config B: 100K-point scene, 2-stage backbone forward "
+                                   "(K=256/128, S=512, W=2, 2 rounds, C=96, H=4, pool rho=2)",
+                       "l2": "n/a (CPU)"},
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
+                             "sample": f"attention {ran}/{scopes} scopes per step, extrapolated"},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU leg
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    args.warmup = max(3, args.warmup)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2412_16481_b200 as F
+    from paper_2412_16481_b200 import _lib as L
+    from paper_2412_16481_b200.backbone import Backbone
+
+    coords, feats = workload(rank)
+    dev = torch.device("cuda", local)
+    C_d = torch.tensor(coords, device=dev)
+    X_d = torch.tensor(feats, dtype=torch.float32, device=dev)
+    C_h = torch.tensor(coords).pin_memory()
+    X_h = torch.tensor(feats, dtype=torch.float32).pin_memory()
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.int32, device=dev)   # 256 MiB > 126 MB L2
+    bb = Backbone()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        bb.forward(C_d, X_d)
+    bb.forward(C_d, X_d, keep_trace=True)
+    trace = bb.last_trace
+
+    # ---- device-resident throughput (value): per-step events, L2 flushed between steps
+    barrier()
+    step_ms = []
+    probe_tot = {}
+    launches = 0
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            with L.Probe(events=True) as pr:
+                s0.record()
+                bb.forward(C_d, X_d)
+                s1.record()
+            torch.cuda.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            for k, v in pr.totals_ms().items():
+                probe_tot[k] = probe_tot.get(k, 0.0) + v
+            launches += pr.launches
+    barrier()
+    ms = sum(step_ms) / len(step_ms)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # ---- end to end through the public API with host buffers (e2e)
+    out_rows = []
+    barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cd = C_h.to(dev, non_blocking=True)
+        xd = X_h.to(dev, non_blocking=True)
+        f, c = bb.forward(cd, xd)
+        res = f.to("cpu", non_blocking=False)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        out_rows.append(res.shape[0])
+    te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms_max = float(te.item())
+
+    if rank == 0:
+        hbm, tflops, src = peaks()
+        steps = args.steps
+        attn_ms = probe_tot.get("f3d_bswin_attention", 0.0) / steps
+        attn_flops = sum(s.attention_flops for s in trace)
+        attn_tf = attn_flops / (attn_ms * 1e-3) / 1e12 if attn_ms else 0.0
+        psh_ms = (probe_tot.get("f3d_voxel_hash", 0.0) + probe_tot.get("f3d_psh_assign", 0.0)) / steps
+        n_tot = sum(s.n for s in trace)
+        psh_gbs = 36.0 * n_tot / (psh_ms * 1e-3) / 1e9 if psh_ms else 0.0
+        sc_ms = probe_tot.get("f3d_scatter_rows", 0.0) / steps
+        sc_gbs = sum((2 * 4 * D_MODEL + 48) * s.n for s in trace) / (sc_ms * 1e-3) / 1e9 if sc_ms else 0.0
+        pool_ms = (probe_tot.get("f3d_pool_build", 0.0) + probe_tot.get("f3d_pool_reduce", 0.0)) / steps
+        n_pool = trace[0].n
+        pool_gbs = (4 * D_MODEL + 24) * n_pool * 1.5 / (pool_ms * 1e-3) / 1e9 if pool_ms else 0.0
+        breakdown = {k: round(v / steps, 4) for k, v in sorted(probe_tot.items(), key=lambda kv: -kv[1])}
+        mine_ms = sum(probe_tot.values()) / steps
+        total_pts = N_POINTS * world
+        line = {
+            "metric": METRIC,
+            "value": total_pts / (ms_max / 1e3),
+            "unit": "points/s",
+            "n_gpus": world,
+            "steps": steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (synth_cloud uniform-box seed 7+rank; features default_rng(1+rank).normal; "
+                    "random-init weights from init_params)",
+            "config": {"workload": "config B: 100K-point ScanNet-sized scene per GPU, full 2-stage "
+                                   "backbone forward (PSH K=256 S=512 -> 2-round bucket-swin stage "
+                                   "C=96 H=4 W=2 -> pool rho=2 -> PSH K=128 -> stage)",
+                       "points_per_gpu": N_POINTS, "parallelism": f"scene-sharded x{world}",
+                       "l2": "flushed (256 MiB write) between timed steps"},
+            "roofline": {"kernel": "f3d_bswin_attention", "bound": "tensor",
+                         "achieved": round(attn_tf, 2), "peak": tflops, "unit": "TFLOP/s",
+                         "frac": round(attn_tf / tflops, 4), "traffic": None,
+                         "peak_source": src,
+                         "flops_per_step": attn_flops, "ms_per_step": round(attn_ms, 4),
+                         "note": "dh=24 (padded 32): exp/MUFU-bound, see DESIGN.md"},
+            "rooflines": {
+                "psh (f3d_voxel_hash+f3d_psh_assign)": {"bound": "hbm", "achieved": round(psh_gbs, 1),
+                                                        "peak": hbm, "unit": "GB/s",
+                                                        "frac": round(psh_gbs / hbm, 4),
+                                                        "ms_per_step": round(psh_ms, 4),
+                                                        "bytes_per_point": 36},
+                "scatter (f3d_scatter_rows)": {"bound": "hbm", "achieved": round(sc_gbs, 1), "peak": hbm,
+                                               "unit": "GB/s", "frac": round(sc_gbs / hbm, 4),
+                                               "ms_per_step": round(sc_ms, 4)},
+                "pool (f3d_pool_build+f3d_pool_reduce)": {"bound": "hbm", "achieved": round(pool_gbs, 1),
+                                                          "peak": hbm, "unit": "GB/s",
+                                                          "frac": round(pool_gbs / hbm, 4),
+                                                          "ms_per_step": round(pool_ms, 4)},
+            },
+            "kernel_ms_per_step": breakdown,
+            "own_kernels_ms_per_step": round(mine_ms, 4),
+            "psh_sweeps": [s.sweeps for s in trace],
+            "gpu_launches": launches // steps,
+            "e2e": {"value": total_pts / (e2e_ms_max / 1e3), "unit": "points/s",
+                    "h2d_bytes_per_step": int(C_h.numel() * 8 + X_h.numel() * 4),
+                    "d2h_bytes_per_step": int(out_rows[-1] * D_MODEL * 4),
+                    "ms_per_step": e2e_ms_max},
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(coords, feats)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -337,7 +337,7 @@ def init_params(seed, d, d_hidden=None, n_heads=4):
     return p
 
 
-def stage_forward(F, C, table, rounds, p, threads=1, scope_limit=None):
+def stage_forward(F, C, table, rounds, p, threads=1, scope_limit=None, timings=None):
     """stage.py:99-159 — pre-norm block per round over scattered rows.
 
     ``scope_limit`` (bench sampling only) runs attention on the first
@@ -351,7 +351,9 @@ def stage_forward(F, C, table, rounds, p, threads=1, scope_limit=None):
     ext = C.max(axis=0) - lo
     ext[ext == 0] = 1.0
     pe = positional_encoding((C - lo) / ext, d)
+    import time
     for scopes in rounds:
+        t0 = time.perf_counter()
         x = layer_norm(F, p["ln1_gain"], p["ln1_bias"]) + pe
         Q = x @ p["w_q"] + p["b_q"]
         K = x @ p["w_k"] + p["b_k"]
@@ -366,15 +368,20 @@ def stage_forward(F, C, table, rounds, p, threads=1, scope_limit=None):
             rows = np.concatenate([np.arange(a, b) for a, b in rg])
             att[rows] = attention_dense(Q[rows], K[rows], V[rows], H)
 
+        t1 = time.perf_counter()
         if threads > 1:
             with ThreadPoolExecutor(max_workers=threads) as ex:
                 list(ex.map(one, todo))
         else:
             for sc in todo:
                 one(sc)
+        t2 = time.perf_counter()
         F = F + att @ p["w_o"] + p["b_o"]
         h = layer_norm(F, p["ln2_gain"], p["ln2_bias"])
         F = F + gelu(h @ p["w_in"] + p["b_in"]) @ p["w_out"] + p["b_out"]
+        if timings is not None:
+            timings.append({"attn": t2 - t1, "rest": time.perf_counter() - t2 + (t1 - t0),
+                            "ran": len(todo), "scopes": len(scopes)})
     return F
 
 
@@ -487,3 +494,47 @@ def pool_stage(F, C, counts, base, K, S, nbatch, rho, reduce="mean"):
             oc.append(pool_reduce(C[lo:hi], sub, sizes, "mean"))
             new_counts[slot] += len(sizes)
     return (np.vstack(of), np.vstack(oc), new_counts, max(1, -(-S // rho)), sub_all)
+
+
+# ------------------------------------------------------------------ backbone
+
+def backbone_forward(coords, feats, stages, threads=1, scope_limit=None, timings=None):
+    """Composition of the restated ops in the order of
+    paper_2412_16481_b200/backbone.py (voxelize -> remap -> PSH -> scatter ->
+    stage_forward -> pool_stage, per stage).  ``stages`` is a sequence of
+    objects with the StageConfig fields.  Returns (features, coords)."""
+    import time
+    C = np.asarray(coords, dtype=np.float64)
+    X = np.asarray(feats, dtype=np.float64)
+    for cfg in stages:
+        t0 = time.perf_counter()
+        vox = remap_nonnegative(voxelize(C, (0.0, 0.0, 0.0), cfg.voxel))
+        ids, offs, counts, base = psh_assign(vox, None, cfg.kind, cfg.K, cfg.S, cfg.S_div)
+        dest = dest_index(ids, offs, base, cfg.K)
+        Xs = np.empty_like(X)
+        Xs[dest] = X
+        Cs = np.empty_like(C)
+        Cs[dest] = C
+        t1 = time.perf_counter()
+        table = bucket_table(counts, base, cfg.K, cfg.S)
+        rounds = build_schedule(len(table[0]), cfg.W, cfg.stride, cfg.shift, cfg.rounds)
+        p = init_params(cfg.seed, cfg.d_model, n_heads=cfg.n_heads)
+        st_t = []
+        Xs = stage_forward(Xs, Cs, table, rounds, p, threads=threads, scope_limit=scope_limit,
+                           timings=st_t)
+        t2 = time.perf_counter()
+        if cfg.pool_rho:
+            X, C, _, _, _ = pool_stage(Xs, Cs, counts, base, cfg.K, cfg.S, 1, cfg.pool_rho, "mean")
+        else:
+            X, C = Xs, Cs
+        t3 = time.perf_counter()
+        if timings is not None:
+            nsc = sum(len(r) for r in rounds)
+            # attention time extrapolated linearly in the scope count when sampled
+            attn_x = sum(r["attn"] * r["scopes"] / max(1, r["ran"]) for r in st_t)
+            rest = sum(r["rest"] for r in st_t)
+            timings.append({"psh_scatter": t1 - t0, "stage": t2 - t1, "pool": t3 - t2,
+                            "stage_extrapolated": attn_x + rest,
+                            "scopes": nsc, "scopes_run": sum(r["ran"] for r in st_t),
+                            "n": len(vox)})
+    return X, C

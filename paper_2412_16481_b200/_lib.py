@@ -79,10 +79,56 @@ def load():
 _ERRS = {1: ConfigError, 2: RangeError, 3: IntegrityError, 5: EmptyInputError, 6: NumericError}
 
 
+# kernels each entry point launches (for the bench's gpu_launches count)
+KERNELS_PER_CALL = {
+    "f3d_voxelize": 1, "f3d_remap_nonnegative": 3, "f3d_hash_bucket": 2, "f3d_morton_encode": 2,
+    "f3d_voxel_hash": 3, "f3d_psh_assign": 1, "f3d_validate_assignment": 3,
+    "f3d_scatter_rows": 1, "f3d_gather_rows": 1, "f3d_bswin_attention": 1,
+    "f3d_positional_encoding": 1, "f3d_stage_pe": 1, "f3d_coord_bbox": 2, "f3d_row_ln": 1,
+    "f3d_gelu_f64": 1, "f3d_bias_gelu": 1, "f3d_pool_build": 1, "f3d_pool_reduce": 1,
+}
+
+
+class Probe:
+    """Optional instrumentation used by bench.py: counts launches and records
+    CUDA events around every entry point on the launching stream."""
+
+    active = None
+
+    def __init__(self, events: bool = True):
+        self.launches = 0
+        self.events = events
+        self.records = []   # (name, start_event, end_event)
+
+    def __enter__(self):
+        Probe.active = self
+        return self
+
+    def __exit__(self, *exc):
+        Probe.active = None
+
+    def totals_ms(self):
+        torch.cuda.synchronize()
+        out = {}
+        for name, a, b in self.records:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
+
+
 def call(name, *args):
     """Invoke an f3d_* entry point and map a non-zero status to the
     reference exception classes (bw/errors.py)."""
+    pr = Probe.active
+    if pr is not None:
+        pr.launches += KERNELS_PER_CALL.get(name, 0)
+        if pr.events:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
     st = getattr(load(), name)(*args)
+    if pr is not None and pr.events:
+        e1.record()
+        pr.records.append((name, e0, e1))
     if st != 0:
         msg = load().f3d_last_error().decode(errors="replace")
         if st == 4:

@@ -357,8 +357,11 @@ __device__ __forceinline__ void st_f(__nv_bfloat16* p, float v) { *p = __float2b
 __device__ __forceinline__ void st_f(float* p, float v) { *p = v; }
 __device__ __forceinline__ void st_f(double* p, double v) { *p = v; }
 
-// One thread per (pooled row, column); members in index order, sequential
-// accumulation (np.add/minimum/maximum.reduceat order), mean = sum / size.
+// One thread per (pooled row, column), members in index order.  Sums follow
+// numpy's add.reduceat exactly: out = x[m0] + pairwise(x[m1..]), where the
+// pairwise rest is a plain loop from 0.0 below 8 terms and eight strided
+// accumulators combined ((0+1)+(2+3))+((4+5)+(6+7)) up to 128 terms
+// (rho <= 64 keeps us below the recursive split).  mean = sum / size.
 template <typename T>
 __global__ void pool_reduce_kernel(const T* __restrict__ x, int64_t ldx, int d,
                                    const int32_t* __restrict__ members,
@@ -372,12 +375,32 @@ __global__ void pool_reduce_kernel(const T* __restrict__ x, int64_t ldx, int d,
         const int c = (int)(t - j * d);
         const int32_t* mem = members + j * rho;
         const int sz = sizes[j];
-        A acc = (A)ld_f(x + (int64_t)mem[0] * ldx + c);
-        for (int r = 1; r < sz; ++r) {
-            const A v = (A)ld_f(x + (int64_t)mem[r] * ldx + c);
-            if (op == R_MIN) acc = v < acc ? v : acc;
-            else if (op == R_MAX) acc = v > acc ? v : acc;
-            else acc = acc + v;
+        auto X = [&](int r) -> A { return (A)ld_f(x + (int64_t)mem[r] * ldx + c); };
+        A acc = X(0);
+        if (op == R_MIN || op == R_MAX) {
+            for (int r = 1; r < sz; ++r) {
+                const A v = X(r);
+                if (op == R_MIN) acc = v < acc ? v : acc;
+                else acc = v > acc ? v : acc;
+            }
+        } else if (sz > 1) {
+            const int nr = sz - 1;
+            A res;
+            if (nr < 8) {
+                res = (A)0;
+                for (int r = 1; r <= nr; ++r) res = res + X(r);
+            } else {
+                A a8[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) a8[q] = X(1 + q);
+                const int full = nr - nr % 8;
+                for (int i = 8; i < full; i += 8)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) a8[q] = a8[q] + X(1 + i + q);
+                res = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+                for (int i = full; i < nr; ++i) res = res + X(1 + i);
+            }
+            acc = acc + res;
         }
         if (op == R_MEAN) acc = acc / (A)sz;
         st_f(out + j * ldo + c, acc);

@@ -131,14 +131,14 @@ class StageRunner:
     ``run(F)`` then executes every round with no host synchronisation."""
 
     def __init__(self, coords, table, schedule: ScopeSchedule, params: StageParams, n: int,
-                 f_dtype=torch.float32):
+                 f_dtype=torch.float32, weights=None):
         dev = L.device()
         self.p = params
         self.n = n
         self.d = params.d_model
         self.H = params.attention.n_heads
         self.dh = params.attention.head_dim
-        self.w = params.device_weights()
+        self.w = weights if weights is not None else params.device_weights()
         self.plans = plan_schedule(table, schedule, dev)
         self.f_dtype = f_dtype
         c = L.to_dev(coords, torch.float64).contiguous()
