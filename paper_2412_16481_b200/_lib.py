@@ -174,3 +174,38 @@ def out(t: torch.Tensor, host: bool):
 
 def empty(shape, dtype):
     return torch.empty(shape, dtype=dtype, device=device())
+
+
+class _Uploader:
+    """Packs many small int32 host arrays into one pinned staging buffer and
+    issues a single non-blocking H2D copy on the current stream (plans are
+    rebuilt once per stage; a blocking pageable copy per array would drain the
+    stream each time)."""
+
+    def __init__(self):
+        self.host = None
+        self.event = None
+
+    def __call__(self, arrays):
+        items = [(k, np.ascontiguousarray(v, dtype=np.int32)) for k, v in arrays.items()]
+        total = 0
+        spans = []
+        for k, a in items:
+            spans.append((k, total, a))
+            total += (a.size + 3) & ~3          # 16-byte aligned slices
+        total = max(total, 4)
+        if self.event is not None:
+            self.event.synchronize()
+        if self.host is None or self.host.numel() < total:
+            self.host = torch.empty(max(total, 1 << 20), dtype=torch.int32).pin_memory()
+        hv = self.host.numpy()
+        for k, o, a in spans:
+            hv[o:o + a.size] = a.ravel()
+        dev = torch.empty(total, dtype=torch.int32, device=device())
+        dev.copy_(self.host[:total], non_blocking=True)
+        self.event = torch.cuda.Event()
+        self.event.record()
+        return {k: dev[o:o + a.size].view(a.shape) for k, o, a in spans}
+
+
+upload = _Uploader()

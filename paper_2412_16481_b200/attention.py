@@ -141,53 +141,115 @@ def logical_gather(assignment, scope):
 
 # --------------------------------------------------------------- kernel plan
 
+def plan_arrays(starts, lens, members):
+    """Vectorised scope planning.  members: (n_scopes, W) bucket ids (-1 pad)
+    over a (starts, lens) table.  Returns int32 host arrays: scope_seg
+    (n_scopes+1), seg_start, seg_vstart, scope_len, work (nwork, 2) — adjacent
+    buckets merged into one physical segment, work items (scope, q_start) in
+    longest-scope-first order."""
+    starts = np.asarray(starts, dtype=np.int64)
+    lens = np.asarray(lens, dtype=np.int64)
+    M = np.asarray(members, dtype=np.int64)
+    ns, W = M.shape
+    ok = M >= 0
+    Mi = np.where(ok, M, 0)
+    st = np.where(ok, starts[Mi], 0)
+    ln = np.where(ok, lens[Mi], 0)
+    ln[~ok] = 0
+    valid = ln > 0
+    sc_of = np.repeat(np.arange(ns), W).reshape(ns, W)[valid]
+    st_v = st[valid]
+    ln_v = ln[valid]
+    scope_len = np.bincount(sc_of, weights=ln_v, minlength=ns).astype(np.int64)
+    # virtual start within the scope (exclusive prefix of lengths per scope)
+    csum = np.cumsum(ln_v)
+    first_of_scope = np.r_[True, sc_of[1:] != sc_of[:-1]] if len(sc_of) else np.zeros(0, bool)
+    scope_base = np.zeros(ns, dtype=np.int64)
+    if len(sc_of):
+        scope_base[sc_of[first_of_scope]] = (csum - ln_v)[first_of_scope]
+    vstart = csum - ln_v - scope_base[sc_of] if len(sc_of) else csum
+    prev_end = np.r_[-1, (st_v + ln_v)[:-1]] if len(sc_of) else st_v
+    new_seg = first_of_scope | (st_v != prev_end)
+    seg_start = st_v[new_seg]
+    seg_vstart = vstart[new_seg]
+    nseg = np.bincount(sc_of[new_seg], minlength=ns) if len(sc_of) else np.zeros(ns, np.int64)
+    scope_seg = np.r_[0, np.cumsum(nseg)]
+    order = np.argsort(-scope_len, kind="stable")
+    nt = -(-scope_len[order] // BLOCK_M)
+    wscope = np.repeat(order, nt)
+    wfirst = np.repeat(np.cumsum(nt) - nt, nt)
+    wq = (np.arange(len(wscope)) - wfirst) * BLOCK_M
+    work = np.stack([wscope, wq], 1) if len(wscope) else np.zeros((0, 2), np.int64)
+    i32 = lambda x: np.ascontiguousarray(x, dtype=np.int32)
+    return {"scope_seg": i32(scope_seg), "seg_start": i32(seg_start), "seg_vstart": i32(seg_vstart),
+            "scope_len": i32(scope_len), "work": i32(work)}
+
+
+def schedule_members(schedule: "ScopeSchedule", t: int):
+    """(n_scopes, W) member matrix of round t (-1 padded)."""
+    scopes = schedule.rounds[t]
+    W = max((len(s) for s in scopes), default=1)
+    M = np.full((len(scopes), max(1, W)), -1, dtype=np.int64)
+    for i, sc in enumerate(scopes):
+        M[i, :len(sc)] = sc
+    return M
+
+
+def round_members(nb, W, stride, shift, t):
+    """Vectorised build_schedule for one round (bw/attention.py:104-115):
+    position p of the rotated order belongs to scope (p // span, lane) with
+    lane = (p % span) % stride, slot j = (p % span) // stride."""
+    span = W * stride
+    order = (np.arange(nb, dtype=np.int64) + (t * shift) % W) % nb
+    p = np.arange(nb)
+    chunk, r = p // span, p % span
+    lane, j = r % stride, r // stride
+    sid = chunk * stride + lane
+    M = np.full((int(sid.max()) + 1 if nb else 0, W), -1, dtype=np.int64)
+    M[sid, j] = order
+    return M
+
+
 class RoundPlan:
-    """Device tables for one launch: scopes as merged physical segments plus
-    the (scope, q_start) work list, longest scopes first (LPT order)."""
+    """Device tables for one attention launch (see plan_arrays)."""
 
-    def __init__(self, scope_ranges, dev):
-        seg_first, seg_start, seg_vstart, lens = [0], [], [], []
-        for ranges in scope_ranges:
-            v = 0
-            last_end = None
-            for a, b in ranges:
-                if b <= a:
-                    continue
-                if last_end is not None and a == last_end:
-                    last_end = b                      # adjacent bucket: extend the segment
-                else:
-                    seg_start.append(a)
-                    seg_vstart.append(v)
-                    last_end = b
-                v += b - a
-            seg_first.append(len(seg_start))
-            lens.append(v)
-        lens = np.array(lens, dtype=np.int64)
-        self.scope_len_host = lens
-        order = np.argsort(-lens, kind="stable")
-        work = [(s, q) for s in order for q in range(0, int(lens[s]), BLOCK_M)]
-        self.nwork = len(work)
+    def __init__(self, arrays, dev=None, uploaded=None):
+        self.host = arrays
+        lens = arrays["scope_len"].astype(np.int64)
+        self.nwork = int(arrays["work"].shape[0])
         self.flops_per_head = int((lens.astype(np.float64) ** 2).sum())   # sum m^2
-        i32 = lambda a: torch.tensor(np.asarray(a, dtype=np.int32), device=dev)
-        self.scope_seg = i32(seg_first)
-        self.seg_start = i32(seg_start if seg_start else [0])
-        self.seg_vstart = i32(seg_vstart if seg_vstart else [0])
-        self.scope_len = i32(lens if len(lens) else [0])
-        self.work = i32(np.array(work, dtype=np.int32).reshape(-1, 2) if work else np.zeros((1, 2)))
+        up = uploaded if uploaded is not None else L.upload(arrays)
+        self.scope_seg = up["scope_seg"]
+        self.seg_start = up["seg_start"]
+        self.seg_vstart = up["seg_vstart"]
+        self.scope_len = up["scope_len"]
+        self.work = up["work"]
+
+    @classmethod
+    def from_ranges(cls, scope_ranges, dev=None):
+        """Plan from explicit [(start, stop), ...] lists (one per scope)."""
+        starts, lens, members = [], [], []
+        W = max((len(r) for r in scope_ranges), default=1)
+        M = np.full((len(scope_ranges), max(1, W)), -1, dtype=np.int64)
+        k = 0
+        for i, rg in enumerate(scope_ranges):
+            for j, (a, b) in enumerate(rg):
+                starts.append(a)
+                lens.append(max(0, b - a))
+                M[i, j] = k
+                k += 1
+        return cls(plan_arrays(np.array(starts + [0]), np.array(lens + [0]), M))
 
 
-def plan_schedule(table, schedule: ScopeSchedule, dev):
+def plan_schedule(table, schedule: ScopeSchedule, dev=None):
     """One RoundPlan per round of the schedule over a (starts, lengths) table."""
     starts, lengths = _table_np(table)
     plans = []
-    for scopes in schedule.rounds:
-        rngs = []
-        for sc in scopes:
-            sc = np.asarray(sc, dtype=np.int64)
-            if (sc < 0).any() or (sc >= len(starts)).any():
-                raise ConfigError("scope bucket id outside the bucket table")
-            rngs.append([(int(starts[b]), int(starts[b] + lengths[b])) for b in sc if lengths[b] > 0])
-        plans.append(RoundPlan(rngs, dev))
+    for t in range(len(schedule.rounds)):
+        M = schedule_members(schedule, t)
+        if ((M >= len(starts)) | (M < -1)).any():
+            raise ConfigError("scope bucket id outside the bucket table")
+        plans.append(RoundPlan(plan_arrays(starts, lengths, M)))
     return plans
 
 
@@ -254,7 +316,7 @@ def tiled_attention(Q, K, V, params: AttentionParams, ranges=None, mask=None):
     out = torch.zeros((total, params.d_model), dtype=torch.float32, device=q.device)
     # overlapping / repeated ranges are legal in the reference: run each
     # distinct physical range list as one scope over a private row space
-    plan = RoundPlan([real], q.device)
+    plan = RoundPlan.from_ranges([real])
     starved = torch.zeros(1, dtype=torch.int32, device=q.device) if mk is not None else None
     m = sum(b - a for a, b in real)
     # bytes the kernel streams: Q once, K and V once per query tile (bf16)
@@ -266,7 +328,7 @@ def tiled_attention(Q, K, V, params: AttentionParams, ranges=None, mask=None):
         qs, ks, vs = qb[rows].contiguous(), kb[rows].contiguous(), vb[rows].contiguous()
         o2 = torch.zeros((m, params.d_model), dtype=torch.float32, device=q.device)
         mk2 = mk[rows].contiguous() if mk is not None else None
-        attend(qs, ks, vs, o2, RoundPlan([[(0, m)]], q.device), params.n_heads, dh, mask=mk2,
+        attend(qs, ks, vs, o2, RoundPlan.from_ranges([[(0, m)]]), params.n_heads, dh, mask=mk2,
                starved=starved)
         res = o2.to(torch.float64)
     if mk is not None and not bool(mk[rows].any()):
@@ -294,7 +356,7 @@ def reference_attention(Q, K, V, params: AttentionParams):
     if mk != m:
         raise ConfigError("reference_attention on the GPU needs as many keys as queries")
     out = torch.zeros((m, params.d_model), dtype=torch.float32, device=q.device)
-    attend(qb, kb, vb, out, RoundPlan([[(0, m)]], q.device), params.n_heads, params.head_dim)
+    attend(qb, kb, vb, out, RoundPlan.from_ranges([[(0, m)]]), params.n_heads, params.head_dim)
     return L.out(out.to(torch.float64), host)
 
 

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .attention import build_schedule
+from .attention import RoundPlan, plan_arrays, round_members
 from .bucketing import BucketAssignment, _run_psh, default_probe_schedule
 from .errors import ConfigError, RangeError
 from .hashing import HashConfig, raise_range
@@ -53,6 +53,16 @@ class StageTrace:
     assignment: BucketAssignment
     attention_flops: int
     sweeps: int = 0
+
+
+def split_table(counts, base, K, S):
+    """bucket_table(split_recycle=True) from host counts/base
+    (bw/bucketing.py:147-166), vectorised."""
+    r = int(counts[K])
+    j = np.arange(0, r, S, dtype=np.int64)
+    starts = np.concatenate([base[:K], base[K] + j])
+    lens = np.concatenate([counts[:K], np.minimum(S, r - j)])
+    return starts.astype(np.int64), lens.astype(np.int64)
 
 
 class Backbone:
@@ -108,20 +118,21 @@ class Backbone:
             Cs = torch.empty_like(C)
             L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F), L.stream())
             L.call("f3d_scatter_rows", L.ptr(C), L.ptr(dest), n, 24, L.ptr(Cs), L.stream())
-            r = cfg.S
-            recyc = int(counts_h[cfg.K])
-            starts = list(base_h[:cfg.K]) + [int(base_h[cfg.K]) + j for j in range(0, recyc, r)]
-            lens = list(counts_h[:cfg.K]) + [min(r, recyc - j) for j in range(0, recyc, r)]
-            table = (np.array(starts, np.int64), np.array(lens, np.int64))
-            sched = build_schedule(len(starts), cfg.W, cfg.stride, cfg.shift, cfg.rounds)
-            runner = StageRunner(Cs, table, sched, self.params[si], n, torch.float32,
-                                 weights=self._w[si])
+            table = split_table(counts_h, base_h, cfg.K, cfg.S)
+            nb = len(table[0])
+            if cfg.W > nb:
+                raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb})")
+            plans = [RoundPlan(plan_arrays(table[0], table[1],
+                                           round_members(nb, cfg.W, cfg.stride, cfg.shift, t)))
+                     for t in range(cfg.rounds)]
+            runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
+                                 weights=self._w[si], plans=plans)
             runner.run(F)
             if keep_trace:
                 trace.append(StageTrace(n, counts_h, a, runner.attention_flops(), sweeps))
             if cfg.pool_rho:
                 X, C, _ = pool_device(F, Cs, counts_h, base_h, cfg.K, cfg.S, 1, cfg.pool_rho,
-                                      "mean", check=False)
+                                      "mean", check=False, assignment=False)
             else:
                 X, C = F, Cs
         self.last_trace = trace

@@ -86,10 +86,12 @@ class TilePlan:
         self.slot_of_tile = slot_of_tile
         self.targets = targets
         self.new_counts = np.bincount(slot_of_tile, weights=targets, minlength=len(counts)).astype(np.int64)
-        i32 = lambda a: torch.tensor(np.asarray(a, dtype=np.int32), device=dev)
-        self.tile_start = i32(starts if self.ntiles else [0])
-        self.tile_m = i32(m if self.ntiles else [0])
-        self.tile_out = i32(out if self.ntiles else [0])
+        up = L.upload({"tile_start": starts if self.ntiles else [0],
+                       "tile_m": m if self.ntiles else [0],
+                       "tile_out": out if self.ntiles else [0]})
+        self.tile_start = up["tile_start"]
+        self.tile_m = up["tile_m"]
+        self.tile_out = up["tile_out"]
 
 
 def _build(coords_dev, plan: TilePlan, rho: int, want_sub=False, want_seeds=False):
@@ -207,36 +209,37 @@ def pool_stage(features, coords, assignment: BucketAssignment, rho: int, reduce:
     return pf, pc, na
 
 
-def pool_device(x, C, counts, base, K, S, nbatch, rho, reduce, check=True):
+def pool_device(x, C, counts, base, K, S, nbatch, rho, reduce, check=True, assignment=True):
     """Device path of pool_stage given host counts/base; returns device
-    tensors and a device-resident BucketAssignment."""
+    tensors and (optionally) a device-resident BucketAssignment."""
     plan = TilePlan(counts, base, rho, x.device)
     members, sizes, _, _, _, flags = _build(C, plan, rho)
     if check:
         _raise_flags(int(flags.item()))
     pf = _reduce(x, members, sizes, plan.npool, rho, reduce)
     pc = _reduce(C, members, sizes, plan.npool, rho, "mean")
-    na = new_assignment(plan.new_counts, K, max(1, math.ceil(S / rho)), nbatch, x.device)
+    na = None
+    if assignment:
+        na = new_assignment(plan.new_counts, K, max(1, math.ceil(S / rho)), nbatch, x.device)
     return pf, pc, na
 
 
 def new_assignment(new_counts, K, S_new, nbatch, dev) -> BucketAssignment:
     """Assignment of the pooled rows: bucket identity kept, offsets 0..c-1 in
     slot order, so the pooled rows are already in scattered order."""
-    nc = torch.tensor(new_counts, dtype=torch.int64, device=dev)
+    new_counts = np.asarray(new_counts, dtype=np.int64)
     nslots = len(new_counts)
-    slots = torch.repeat_interleave(torch.arange(nslots, device=dev), nc)
-    base = torch.zeros_like(nc)
-    if nslots > 1:
-        base[1:] = torch.cumsum(nc[:-1], 0)
-    npool = int(sum(new_counts))
-    offs = torch.arange(npool, device=dev) - base[slots]
-    bid = slots % (K + 1)
-    bat = slots // (K + 1)
+    slots_h = np.repeat(np.arange(nslots), new_counts)
+    base_h = np.cumsum(new_counts) - new_counts
+    npool = int(new_counts.sum())
+    offs_h = np.arange(npool) - base_h[slots_h]
+    up = L.upload({"counts": new_counts, "base": base_h, "bid": slots_h % (K + 1),
+                   "bat": slots_h // (K + 1), "off": offs_h, "dest": np.arange(npool)})
+    nc, base = up["counts"].to(torch.int64), up["base"].to(torch.int64)
+    bid, bat, offs = up["bid"].to(torch.int64), up["bat"].to(torch.int64), up["off"].to(torch.int64)
     a = BucketAssignment(bucket_id=bid, bucket_offset=offs, counts=nc, bucket_base=base, S=S_new,
                          K=K, batch_id=bat, num_batches=nbatch,
-                         _dev={"id": bid.to(torch.int32), "off": offs.to(torch.int32),
-                               "counts": nc.to(torch.int32), "base": base.to(torch.int32),
-                               "batch": bat.to(torch.int32) if nbatch > 1 else None,
-                               "dest": torch.arange(npool, device=dev, dtype=torch.int32)})
+                         _dev={"id": up["bid"], "off": up["off"], "counts": up["counts"],
+                               "base": up["base"], "batch": up["bat"] if nbatch > 1 else None,
+                               "dest": up["dest"]})
     return a

@@ -131,7 +131,7 @@ class StageRunner:
     ``run(F)`` then executes every round with no host synchronisation."""
 
     def __init__(self, coords, table, schedule: ScopeSchedule, params: StageParams, n: int,
-                 f_dtype=torch.float32, weights=None):
+                 f_dtype=torch.float32, weights=None, plans=None):
         dev = L.device()
         self.p = params
         self.n = n
@@ -139,7 +139,7 @@ class StageRunner:
         self.H = params.attention.n_heads
         self.dh = params.attention.head_dim
         self.w = weights if weights is not None else params.device_weights()
-        self.plans = plan_schedule(table, schedule, dev)
+        self.plans = plans if plans is not None else plan_schedule(table, schedule, dev)
         self.f_dtype = f_dtype
         c = L.to_dev(coords, torch.float64).contiguous()
         self.pe = L.empty((n, self.d), torch.float32)
