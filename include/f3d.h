@@ -149,12 +149,14 @@ int f3d_coord_bbox(const double *coords, int64_t n, double *ws, double *lo_ext, 
 /* ------------------------------------------------------ a13: stage rows
  * Fused residual + LayerNorm (+PE) (bw/stage.py:84-88, 135, 157-158):
  *   if y:   F[r] += y[r] + ybias           (F float or double, y bf16)
- *   if out: out[r] = LN(F[r]) * gain + beta (+ pe[r])   (population var, eps)
- * out_kind: 0 bf16, 1 float, 2 double. */
+ *   if out: out[r] = LN(F[r]) * gain + beta (+ PE(pe_coords[r]))  (population var)
+ * The PE term (bw/attention.py:271-288) is computed on the fly from the f64
+ * coords, normalised by lo_ext (nullable; bw/stage.py:129-132), when
+ * pe_coords is non-null (d % 6 == 0).  out_kind: 0 bf16, 1 float, 2 double. */
 int f3d_row_ln(void *F, int f_is_f64, int64_t ldf, const void *y, int64_t ldy,
-               const float *ybias, const float *gain, const float *beta, const float *pe,
-               int64_t ldpe, void *out, int out_kind, int64_t ldo, int64_t n, int d, double eps,
-               void *stream);
+               const float *ybias, const float *gain, const float *beta,
+               const double *pe_coords, const double *lo_ext, double pe_base, void *out,
+               int out_kind, int64_t ldo, int64_t n, int d, double eps, void *stream);
 /* y = 0.5 x (1 + erf(x / sqrt 2)) in float64 (bw/stage.py:91-92). */
 int f3d_gelu_f64(const double *x, int64_t n, double *y, void *stream);
 /* u = gelu(u + bias) with the exact erf form (bw/stage.py:91-96), bf16 rows. */

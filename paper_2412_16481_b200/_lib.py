@@ -48,8 +48,8 @@ SIGNATURES = {
     "f3d_positional_encoding": (_INT, [_P, _I64, _INT, _F64, _INT, _P, _I64, _P]),
     "f3d_stage_pe": (_INT, [_P, _I64, _INT, _F64, _P, _INT, _P, _I64, _P]),
     "f3d_coord_bbox": (_INT, [_P, _I64, _P, _P, _P]),
-    "f3d_row_ln": (_INT, [_P, _INT, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _INT, _I64, _I64,
-                          _INT, _F64, _P]),
+    "f3d_row_ln": (_INT, [_P, _INT, _I64, _P, _I64, _P, _P, _P, _P, _P, _F64, _P, _INT, _I64,
+                          _I64, _INT, _F64, _P]),
     "f3d_gelu_f64": (_INT, [_P, _I64, _P, _P]),
     "f3d_pool_build": (_INT, [_P, _P, _P, _P, _INT, _INT, _P, _P, _P, _P, _P, _P, _P]),
     "f3d_pool_reduce": (_INT, [_P, _INT, _I64, _INT, _P, _P, _I64, _INT, _INT, _P, _I64, _P]),

@@ -21,7 +21,7 @@ from . import _lib as L
 from .bucketing import BucketAssignment
 from .errors import ConfigError, NumericError
 
-BLOCK_M = 64   # query rows per work item (csrc/attn.cu kBM)
+BLOCK_M = 128  # query rows per work item (csrc/attn.cu kBM)
 BLOCK_N = 64   # keys per streamed tile (csrc/attn.cu kBN)
 
 

@@ -18,9 +18,9 @@
 namespace f3d {
 namespace attn {
 
-constexpr int kBM = 64;       // query rows per CTA
+constexpr int kBM = 128;      // query rows per CTA (8 warps x 16 rows)
 constexpr int kBN = 64;       // keys per tile
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 
 struct Args {
@@ -102,17 +102,19 @@ __device__ __forceinline__ int phys_row(const Args& A, int s0, int s1, int vr) {
 template <int DH, bool kVec>
 __device__ __forceinline__ void load_tile(const Args& A, const __nv_bfloat16* base, int64_t ld,
                                           int hcol, int s0, int s1, int m, int v0,
-                                          __nv_bfloat16* sm, int kRows) {
+                                          __nv_bfloat16* sm, int kRows, bool ones = false) {
     constexpr int kRowB = DH * 2;
     constexpr int kStride = kRowB + 16;
     constexpr int kChunks = kRowB / 16;
     if (kVec) {
+        // pad chunks (c >= real) are never written here: they are set once per
+        // CTA (zeros, plus the ones column of V) by init_pad
         const int real_chunks = (A.dh * 2) / 16;
-        for (int idx = threadIdx.x; idx < kRows * kChunks; idx += kThreads) {
-            const int r = idx / kChunks;
-            const int c = idx - r * kChunks;
+        for (int idx = threadIdx.x; idx < kRows * real_chunks; idx += kThreads) {
+            const int r = idx / real_chunks;
+            const int c = idx - r * real_chunks;
             const int vr = v0 + r;
-            const bool ok = vr < m && c < real_chunks;
+            const bool ok = vr < m;
             const __nv_bfloat16* src = base;
             if (ok) src = base + (int64_t)phys_row(A, s0, s1, vr) * ld + hcol + c * 8;
             cp_async16(reinterpret_cast<char*>(sm) + r * kStride + c * 16, src, ok);
@@ -122,11 +124,35 @@ __device__ __forceinline__ void load_tile(const Args& A, const __nv_bfloat16* ba
             const int r = idx / DH;
             const int c = idx - r * DH;
             const int vr = v0 + r;
-            __nv_bfloat16 val = __float2bfloat16(0.f);
+            __nv_bfloat16 val = __float2bfloat16(ones && c == A.dh ? 1.f : 0.f);
             if (vr < m && c < A.dh) val = base[(int64_t)phys_row(A, s0, s1, vr) * ld + hcol + c];
             *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(sm) + r * kStride + c * 2) =
                 val;
         }
+    }
+}
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Zero the pad columns [dh, DH) of every smem tile once per CTA and put 1.0 in
+// column dh of the V tiles: O[:, dh] then accumulates the softmax row sum in
+// the same MMA as P V (no per-score FADD).
+template <int DH>
+__device__ __forceinline__ void init_pad(unsigned char* smem, int dh, int rows_total,
+                                         int v_row0, int v_rows) {
+    constexpr int kStride = DH * 2 + 16;
+    const int c0 = (dh * 2) / 16 * 8;   // first pad column (chunk aligned)
+    if (c0 >= DH) return;
+    for (int idx = threadIdx.x; idx < rows_total * (DH - c0); idx += kThreads) {
+        const int r = idx / (DH - c0);
+        const int c = c0 + (idx - r * (DH - c0));
+        const bool one = (r >= v_row0 && r < v_row0 + v_rows && c == dh);
+        *reinterpret_cast<__nv_bfloat16*>(smem + r * kStride + c * 2) =
+            __float2bfloat16(one ? 1.f : 0.f);
     }
 }
 
@@ -149,23 +175,27 @@ __global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
     const int s0 = A.scope_seg[scope], s1 = A.scope_seg[scope + 1];
     const int m = A.scope_len[scope];
     const int hcol = h * A.dh;
+    const bool ones = A.dh < DH;          // row sums ride in V's pad column
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
+    const bool warp_live = q0 + warp * 16 < m;
 
+    if (kVec) init_pad<DH>(smem, A.dh, kBM + 4 * kBN, kBM + 2 * kBN, 2 * kBN);
     load_tile<DH, kVec>(A, A.q, A.ld_q, hcol, s0, s1, m, q0, sQ, kBM);
     const int ntiles = (m + kBN - 1) / kBN;
     load_tile<DH, kVec>(A, A.k, A.ld_k, hcol, s0, s1, m, 0, sK, kBN);
-    load_tile<DH, kVec>(A, A.v, A.ld_v, hcol, s0, s1, m, 0, sV, kBN);
+    load_tile<DH, kVec>(A, A.v, A.ld_v, hcol, s0, s1, m, 0, sV, kBN, ones);
     cp_async_commit();
 
     float o_acc[kNd][4];
 #pragma unroll
     for (int i = 0; i < kNd; ++i) o_acc[i][0] = o_acc[i][1] = o_acc[i][2] = o_acc[i][3] = 0.f;
-    float m_run[2] = {-FLT_MAX, -FLT_MAX};
-    float l_run[2] = {0.f, 0.f};
+    float m_run[2] = {-FLT_MAX, -FLT_MAX};   // raw-score units
+    float l_run[2] = {0.f, 0.f};              // only when !ones
     uint32_t qf[kKd][4];
+    const float sl2 = A.scale_log2;
 
     for (int kt = 0; kt < ntiles; ++kt) {
         const int buf = kt & 1;
@@ -178,111 +208,130 @@ __global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
             load_tile<DH, kVec>(A, A.v, A.ld_v, hcol, s0, s1, m, (kt + 1) * kBN,
                                 reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(sV) +
                                                                  nb * kBN * kStride),
-                                kBN);
+                                kBN, ones);
             cp_async_commit();
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        if (kt == 0) {
-            // Q fragments for this warp's 16 rows, kept in registers.
-            const char* qb = reinterpret_cast<const char*>(sQ) + (warp * 16) * kStride;
+        if (warp_live) {
+            if (kt == 0) {
+                // Q fragments for this warp's 16 rows, kept in registers.
+                const char* qb = reinterpret_cast<const char*>(sQ) + (warp * 16) * kStride;
 #pragma unroll
-            for (int kk = 0; kk < kKd; ++kk) {
-                const int r = lane & 15;
-                const int c = kk * 16 + (lane >> 4) * 8;
-                ldsm_x4(smem_u32(qb + r * kStride + c * 2), qf[kk][0], qf[kk][1], qf[kk][2],
-                        qf[kk][3]);
+                for (int kk = 0; kk < kKd; ++kk) {
+                    const int r = lane & 15;
+                    const int c = kk * 16 + (lane >> 4) * 8;
+                    ldsm_x4(smem_u32(qb + r * kStride + c * 2), qf[kk][0], qf[kk][1], qf[kk][2],
+                            qf[kk][3]);
+                }
             }
-        }
-        const char* kb = reinterpret_cast<const char*>(sK) + buf * kBN * kStride;
-        const char* vb = reinterpret_cast<const char*>(sV) + buf * kBN * kStride;
+            const char* kb = reinterpret_cast<const char*>(sK) + buf * kBN * kStride;
+            const char* vb = reinterpret_cast<const char*>(sV) + buf * kBN * kStride;
 
-        // S = Q K^T : 16 rows x 64 keys per warp (8 n8 blocks)
-        float s[8][4];
-#pragma unroll
-        for (int nb = 0; nb < 8; ++nb) {
-            s[nb][0] = s[nb][1] = s[nb][2] = s[nb][3] = 0.f;
-#pragma unroll
-            for (int kk = 0; kk < kKd; ++kk) {
-                uint32_t b0, b1;
-                const int r = nb * 8 + (lane & 7);
-                const int c = kk * 16 + ((lane >> 3) & 1) * 8;
-                ldsm_x2(smem_u32(kb + r * kStride + c * 2), b0, b1);
-                mma16816(s[nb], qf[kk], b0, b1);
-            }
-        }
-        // mask ragged tail / explicit mask, scale into log2 domain
-        const int kbase = kt * kBN;
-#pragma unroll
-        for (int nb = 0; nb < 8; ++nb) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int key = kbase + nb * 8 + 2 * t + (e & 1);
-                bool ok = key < m;
-                if (kMask && ok) ok = A.mask[phys_row(A, s0, s1, key)] != 0;
-                s[nb][e] = ok ? s[nb][e] * A.scale_log2 : -INFINITY;
-            }
-        }
-        // online softmax (rows g and g+8 of this warp)
-        float p_scale[2];
-#pragma unroll
-        for (int hr = 0; hr < 2; ++hr) {
-            float mx = -INFINITY;
-#pragma unroll
-            for (int nb = 0; nb < 8; ++nb) mx = fmaxf(mx, fmaxf(s[nb][2 * hr], s[nb][2 * hr + 1]));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            const float m_new = fmaxf(m_run[hr], mx);
-            const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-            p_scale[hr] = exp2f(m_run[hr] - m_use);
-            m_run[hr] = m_new;
-            float ls = 0.f;
+            // S = Q K^T : 16 rows x 64 keys per warp (8 n8 blocks), raw scores
+            float s[8][4];
 #pragma unroll
             for (int nb = 0; nb < 8; ++nb) {
-                const float p0 = exp2f(s[nb][2 * hr] - m_use);
-                const float p1 = exp2f(s[nb][2 * hr + 1] - m_use);
-                s[nb][2 * hr] = p0;
-                s[nb][2 * hr + 1] = p1;
-                ls += p0 + p1;
+                s[nb][0] = s[nb][1] = s[nb][2] = s[nb][3] = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < kKd; ++kk) {
+                    uint32_t b0, b1;
+                    const int r = nb * 8 + (lane & 7);
+                    const int c = kk * 16 + ((lane >> 3) & 1) * 8;
+                    ldsm_x2(smem_u32(kb + r * kStride + c * 2), b0, b1);
+                    mma16816(s[nb], qf[kk], b0, b1);
+                }
             }
-            l_run[hr] = l_run[hr] * p_scale[hr] + ls;
-        }
+            // masking only where it can matter: the ragged last tile, or a user mask
+            const int kbase = kt * kBN;
+            if (kMask || kt == ntiles - 1) {
 #pragma unroll
-        for (int i = 0; i < kNd; ++i) {
-            o_acc[i][0] *= p_scale[0];
-            o_acc[i][1] *= p_scale[0];
-            o_acc[i][2] *= p_scale[1];
-            o_acc[i][3] *= p_scale[1];
-        }
-        // O += P V : P (16 x 64) as A fragments straight from the S registers
+                for (int nb = 0; nb < 8; ++nb) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            uint32_t pa[4];
-            pa[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
-            pa[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
-            pa[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-            pa[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+                    for (int e = 0; e < 4; ++e) {
+                        const int key = kbase + nb * 8 + 2 * t + (e & 1);
+                        bool ok = key < m;
+                        if (kMask && ok) ok = A.mask[phys_row(A, s0, s1, key)] != 0;
+                        if (!ok) s[nb][e] = -INFINITY;
+                    }
+                }
+            }
+            // online softmax (rows g and g+8 of this warp), exp2 domain via FFMA
+            float p_scale[2];
 #pragma unroll
-            for (int nd = 0; nd < kNd; ++nd) {
-                uint32_t b0, b1;
-                const int r = kk * 16 + (lane & 15);
-                ldsm_x2_t(smem_u32(vb + r * kStride + nd * 16), b0, b1);
-                mma16816(o_acc[nd], pa, b0, b1);
+            for (int hr = 0; hr < 2; ++hr) {
+                float mx = -INFINITY;
+#pragma unroll
+                for (int nb = 0; nb < 8; ++nb) mx = fmaxf(mx, fmaxf(s[nb][2 * hr], s[nb][2 * hr + 1]));
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                const float m_new = fmaxf(m_run[hr], mx);
+                p_scale[hr] = ex2((m_run[hr] - m_new) * sl2);
+                m_run[hr] = m_new;
+                const float nms = -m_new * sl2;
+                float ls = 0.f;
+#pragma unroll
+                for (int nb = 0; nb < 8; ++nb) {
+                    const float p0 = ex2(fmaf(s[nb][2 * hr], sl2, nms));
+                    const float p1 = ex2(fmaf(s[nb][2 * hr + 1], sl2, nms));
+                    s[nb][2 * hr] = p0;
+                    s[nb][2 * hr + 1] = p1;
+                    if (!ones) ls += p0 + p1;
+                }
+                if (!ones) l_run[hr] = l_run[hr] * p_scale[hr] + ls;
+            }
+#pragma unroll
+            for (int i = 0; i < kNd; ++i) {
+                o_acc[i][0] *= p_scale[0];
+                o_acc[i][1] *= p_scale[0];
+                o_acc[i][2] *= p_scale[1];
+                o_acc[i][3] *= p_scale[1];
+            }
+            // O += P V : P (16 x 64) as A fragments straight from the S registers
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                uint32_t pa[4];
+                pa[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
+                pa[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
+                pa[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+                pa[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+                for (int nd = 0; nd < kNd; ++nd) {
+                    uint32_t b0, b1;
+                    const int r = kk * 16 + (lane & 15);
+                    ldsm_x2_t(smem_u32(vb + r * kStride + nd * 16), b0, b1);
+                    mma16816(o_acc[nd], pa, b0, b1);
+                }
             }
         }
         __syncthreads();
     }
+    if (!warp_live) return;
 
     // epilogue: normalise, write real rows of this head at their fixed rows
     float l_tot[2];
+    if (ones) {
+        // column dh of O holds the row sum: owned by quad lane (dh % 8) / 2
+        const int nd = A.dh >> 3, tq = (A.dh & 7) >> 1, e = A.dh & 1;
+        float v0 = 0.f, v1 = 0.f;
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-        float l = l_run[hr];
-        l += __shfl_xor_sync(0xffffffffu, l, 1);
-        l += __shfl_xor_sync(0xffffffffu, l, 2);
-        l_tot[hr] = l;
+        for (int i = 0; i < kNd; ++i)
+            if (i == nd) {
+                v0 = e ? o_acc[i][1] : o_acc[i][0];
+                v1 = e ? o_acc[i][3] : o_acc[i][2];
+            }
+        l_tot[0] = __shfl_sync(0xffffffffu, v0, (lane & ~3) | tq);
+        l_tot[1] = __shfl_sync(0xffffffffu, v1, (lane & ~3) | tq);
+    } else {
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+            float l = l_run[hr];
+            l += __shfl_xor_sync(0xffffffffu, l, 1);
+            l += __shfl_xor_sync(0xffffffffu, l, 2);
+            l_tot[hr] = l;
+        }
     }
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
@@ -292,7 +341,7 @@ __global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
         bool qok = true;
         if (kMask) qok = A.mask[pr] != 0;
         const bool starved = !(l_tot[hr] > 0.f);
-        if (kMask && starved && t == 0 && qok && A.starved) atomicAdd(A.starved, 1);
+        if (kMask && starved && t == 0 && A.starved) atomicAdd(A.starved, 1);
         const float inv = (starved || !qok) ? 0.f : 1.f / l_tot[hr];
 #pragma unroll
         for (int nd = 0; nd < kNd; ++nd) {

@@ -26,10 +26,11 @@ namespace f3d {
 namespace pool {
 
 constexpr int kCap = 1024;         // TILE_CAP (bw/pooling.py:22)
-constexpr int kWarpsPerCta = 4;
+constexpr int kWarpsPerCta = 2;
 constexpr int kThreads = 32 * kWarpsPerCta;
 
 struct WarpSmem {
+    double sc[kCap][3];     // per sub id: seed coordinates (step-3 distances)
     uint16_t cnt[kCap];     // per key running count
     int16_t idk[kCap];      // key -> sub id
     int16_t sizes[kCap];    // per sub id
@@ -75,7 +76,8 @@ __device__ __forceinline__ int warp_argmin(double d, int id) {
 }
 
 __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
-    __shared__ WarpSmem smem_all[kWarpsPerCta];
+    extern __shared__ __align__(16) unsigned char pool_smem[];
+    WarpSmem* smem_all = reinterpret_cast<WarpSmem*>(pool_smem);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x * kWarpsPerCta + warp;
@@ -140,6 +142,9 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
             const int id = nalloc + __popc(fb & lt);
             S.idk[k] = (int16_t)id;
             S.seeds[id] = (int16_t)i;
+            S.sc[id][0] = C[3 * i];
+            S.sc[id][1] = C[3 * i + 1];
+            S.sc[id][2] = C[3 * i + 2];
         }
         if (v && lane == __ffs(mm) - 1) S.cnt[k] = (uint16_t)(S.cnt[k] + __popc(mm));
         nalloc += __popc(fb);
@@ -172,6 +177,9 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
                 S.sub[i] = (int16_t)id;
                 S.sizes[id] = 1;
                 S.seeds[id] = (int16_t)i;
+                S.sc[id][0] = C[3 * i];
+                S.sc[id][1] = C[3 * i + 1];
+                S.sc[id][2] = C[3 * i + 2];
             } else {
                 S.sub[i] = -2;
             }
@@ -185,12 +193,12 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     if (nqueue > 0) {
         for (int i = 0; i < m; ++i) {
             if (S.sub[i] != -2) continue;   // warp-uniform (smem broadcast)
-            const double* ci = C + 3 * i;
+            const double ci[3] = {C[3 * i], C[3 * i + 1], C[3 * i + 2]};
             double best = DBL_MAX;
             int bid = INT_MAX;
             for (int j = nalloc + lane; j < target; j += 32) {
                 if (S.sizes[j] < rho) {
-                    const double d = dist3(C + 3 * S.seeds[j], ci);
+                    const double d = dist3(S.sc[j], ci);
                     if (d < best || (d == best && j < bid)) {
                         best = d;
                         bid = j;
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
             if (!any_new) {
                 for (int j = lane; j < target; j += 32) {
                     if (S.sizes[j] < rho) {
-                        const double d = dist3(C + 3 * S.seeds[j], ci);
+                        const double d = dist3(S.sc[j], ci);
                         if (d < best || (d == best && j < bid)) {
                             best = d;
                             bid = j;
@@ -424,7 +432,14 @@ extern "C" int f3d_pool_build(const double* coords, const int32_t* tile_start,
     pool::Args A{coords, tile_start, tile_m, tile_out, ntiles, rho, sub_out, members, sizes_out,
                  seeds_out, passes_out, flags};
     const int grid = (ntiles + pool::kWarpsPerCta - 1) / pool::kWarpsPerCta;
-    pool::pool_build_kernel<<<grid, pool::kThreads, 0, st>>>(A);
+    const size_t smem = sizeof(pool::WarpSmem) * pool::kWarpsPerCta;
+    static bool attr = false;
+    if (!attr) {
+        F3D_CUDA_TRY(cudaFuncSetAttribute(pool::pool_build_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    pool::pool_build_kernel<<<grid, pool::kThreads, smem, st>>>(A);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

@@ -105,9 +105,9 @@ template <typename FT, typename OT>
 __global__ void row_ln_kernel(FT* __restrict__ F, int64_t ldf, const __nv_bfloat16* __restrict__ y,
                               int64_t ldy, const float* __restrict__ ybias,
                               const float* __restrict__ gain, const float* __restrict__ beta,
-                              const float* __restrict__ pe, int64_t ldpe,
-                              OT* __restrict__ out, int64_t ldo, int64_t n, int d,
-                              double eps) {
+                              const double* __restrict__ pec, const double* __restrict__ lo_ext,
+                              float pe_log2base, OT* __restrict__ out, int64_t ldo, int64_t n,
+                              int d, double eps) {
     using A = typename Acc<FT>::type;
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
@@ -151,15 +151,57 @@ __global__ void row_ln_kernel(FT* __restrict__ F, int64_t ldf, const __nv_bfloat
     }
     q = warp_sum(q);
     const A rstd = (A)1 / sqrt(q / (A)d + (A)eps);
+    // positional encoding of the bbox-normalised coordinate, computed on the
+    // fly (bw/attention.py:271-288; bw/stage.py:129-132): d/3 dims per axis,
+    // alternating sin/cos of x * base^(-j/npair)
+    float xn[3] = {0.f, 0.f, 0.f};
+    const int npair = d / 6, blk = 2 * npair;
+    if (pec) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            double x = pec[3 * row + a];
+            if (lo_ext) x = __ddiv_rn(__dsub_rn(x, lo_ext[a]), lo_ext[3 + a]);
+            xn[a] = (float)x;
+        }
+    }
 #pragma unroll
     for (int j = 0; j < kMaxPerLane; ++j) {
         if (j >= per) break;
         const int c = lane + 32 * j;
         if (c < d) {
             A o = (v[j] - mean) * rstd * (A)gain[c] + (A)beta[c];
-            if (pe) o += (A)pe[row * ldpe + c];
+            if (pec) {
+                const int a = c / blk, k = c - a * blk, jj = k >> 1;
+                const float ang = xn[a] * exp2f(-(float)jj / (float)npair * pe_log2base);
+                float sv, cv;
+                sincosf(ang, &sv, &cv);
+                o += (A)((k & 1) ? cv : sv);
+            }
             store_out(out + row * ldo + c, (double)o);
         }
+    }
+}
+
+__device__ __forceinline__ float gelu_f(float x) {
+    return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+
+// 16-byte vector form: 8 bf16 per thread (dh % 8 == 0).
+__global__ void bias_gelu8_kernel(uint4* __restrict__ u, int64_t n8, int dh8,
+                                  const float4* __restrict__ b) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n8;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int c8 = (int)(t % dh8);
+        uint4 w = u[t];
+        const float4 b0 = b[2 * c8], b1 = b[2 * c8 + 1];
+        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 f = __bfloat1622float2(h[q]);
+            h[q] = __floats2bfloat162_rn(gelu_f(f.x + bb[2 * q]), gelu_f(f.y + bb[2 * q + 1]));
+        }
+        u[t] = w;
     }
 }
 
@@ -227,37 +269,41 @@ extern "C" int f3d_stage_pe(const double* coords, int64_t n, int d, double base,
 template <typename FT>
 static void launch_row_ln(unsigned g, cudaStream_t st, void* F, int64_t ldf, const void* y,
                           int64_t ldy, const float* ybias, const float* gain, const float* beta,
-                          const float* pe, int64_t ldpe, void* out, int out_kind, int64_t ldo,
-                          int64_t n, int d, double eps) {
+                          const double* pec, const double* lo_ext, float pl2, void* out,
+                          int out_kind, int64_t ldo, int64_t n, int d, double eps) {
     const __nv_bfloat16* yy = (const __nv_bfloat16*)y;
     if (out_kind == 2)
         stage::row_ln_kernel<FT, double><<<g, stage::kThreads, 0, st>>>(
-            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pe, ldpe, (double*)out, ldo, n, d, eps);
+            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pec, lo_ext, pl2, (double*)out, ldo, n, d, eps);
     else if (out_kind == 1)
         stage::row_ln_kernel<FT, float><<<g, stage::kThreads, 0, st>>>(
-            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pe, ldpe, (float*)out, ldo, n, d, eps);
+            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pec, lo_ext, pl2, (float*)out, ldo, n, d, eps);
     else
         stage::row_ln_kernel<FT, __nv_bfloat16><<<g, stage::kThreads, 0, st>>>(
-            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pe, ldpe, (__nv_bfloat16*)out, ldo, n, d,
+            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pec, lo_ext, pl2, (__nv_bfloat16*)out, ldo, n, d,
             eps);
 }
 
 extern "C" int f3d_row_ln(void* F, int f_is_f64, int64_t ldf, const void* y, int64_t ldy,
                           const float* ybias, const float* gain, const float* beta,
-                          const float* pe, int64_t ldpe, void* out, int out_kind, int64_t ldo,
-                          int64_t n, int d, double eps, void* stream) {
+                          const double* pe_coords, const double* lo_ext, double pe_base,
+                          void* out, int out_kind, int64_t ldo, int64_t n, int d, double eps,
+                          void* stream) {
     if (d < 1 || d > 32 * stage::kMaxPerLane || n < 0 || out_kind < 0 || out_kind > 2)
         return F3D_ERR_CONFIG;
+    if (pe_coords && (d % 6)) return F3D_ERR_CONFIG;
+    const float pl2 = pe_coords ? (float)log2(pe_base) : 0.f;
+    const double* pec = pe_coords;
     if (out && (!gain || !beta)) return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned g = (unsigned)((n + stage::kThreads / 32 - 1) / (stage::kThreads / 32));
     if (f_is_f64)
-        launch_row_ln<double>(g, st, F, ldf, y, ldy, ybias, gain, beta, pe, ldpe, out, out_kind,
-                              ldo, n, d, eps);
+        launch_row_ln<double>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, out,
+                              out_kind, ldo, n, d, eps);
     else
-        launch_row_ln<float>(g, st, F, ldf, y, ldy, ybias, gain, beta, pe, ldpe, out, out_kind,
-                             ldo, n, d, eps);
+        launch_row_ln<float>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, out,
+                             out_kind, ldo, n, d, eps);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
@@ -287,8 +333,14 @@ extern "C" int f3d_bias_gelu(void* u_bf16, int64_t n, int dh, const float* bias,
     if (dh < 2 || dh % 2 || n < 0) return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    stage::bias_gelu_kernel<<<grid_for(n * dh / 2, stage::kThreads), stage::kThreads, 0, st>>>(
-        (__nv_bfloat16*)u_bf16, n, dh, bias);
+    if (dh % 8 == 0 && ((uintptr_t)u_bf16 & 15) == 0 && ((uintptr_t)bias & 15) == 0) {
+        const int64_t n8 = n * dh / 8;
+        stage::bias_gelu8_kernel<<<grid_for(n8, stage::kThreads), stage::kThreads, 0, st>>>(
+            (uint4*)u_bf16, n8, dh / 8, (const float4*)bias);
+    } else {
+        stage::bias_gelu_kernel<<<grid_for(n * dh / 2, stage::kThreads), stage::kThreads, 0, st>>>(
+            (__nv_bfloat16*)u_bf16, n, dh, bias);
+    }
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

@@ -111,7 +111,7 @@ def layer_norm(x, gain, bias, eps: float = 1e-12):
     out = L.empty((n, d), torch.float64)
     g = L.to_dev(gain, torch.float32)
     b = L.to_dev(bias, torch.float32)
-    L.call("f3d_row_ln", L.ptr(t2), 1, d, None, 0, None, L.ptr(g), L.ptr(b), None, 0,
+    L.call("f3d_row_ln", L.ptr(t2), 1, d, None, 0, None, L.ptr(g), L.ptr(b), None, None, 0.0,
            L.ptr(out), 2, d, n, d, float(eps), L.stream())
     return L.out(out.reshape(shp), host)
 
@@ -141,13 +141,10 @@ class StageRunner:
         self.w = weights if weights is not None else params.device_weights()
         self.plans = plans if plans is not None else plan_schedule(table, schedule, dev)
         self.f_dtype = f_dtype
-        c = L.to_dev(coords, torch.float64).contiguous()
-        self.pe = L.empty((n, self.d), torch.float32)
+        self.coords = L.to_dev(coords, torch.float64).contiguous()
         ws = L.empty((6 * 296,), torch.float64)
         self.lo_ext = L.empty((6,), torch.float64)
-        L.call("f3d_coord_bbox", L.ptr(c), n, L.ptr(ws), L.ptr(self.lo_ext), L.stream())
-        L.call("f3d_stage_pe", L.ptr(c), n, self.d, 10000.0, L.ptr(self.lo_ext), 1,
-               L.ptr(self.pe), self.d, L.stream())
+        L.call("f3d_coord_bbox", L.ptr(self.coords), n, L.ptr(ws), L.ptr(self.lo_ext), L.stream())
         d, dhid = self.d, params.d_hidden
         self.x = L.empty((n, d), torch.bfloat16)
         self.qkv = L.empty((n, 3 * d), torch.bfloat16)
@@ -157,16 +154,17 @@ class StageRunner:
 
     def _row_ln(self, F, y, ybias, g, b, pe, out):
         L.call("f3d_row_ln", L.ptr(F), int(F.dtype == torch.float64), F.stride(0), L.ptr(y),
-               0 if y is None else y.stride(0), L.ptr(ybias), L.ptr(g), L.ptr(b), L.ptr(pe),
-               0 if pe is None else pe.stride(0), L.ptr(out), 0,
-               0 if out is None else out.stride(0), self.n, self.d, LN_EPS, L.stream())
+               0 if y is None else y.stride(0), L.ptr(ybias), L.ptr(g), L.ptr(b),
+               L.ptr(self.coords) if pe else None, L.ptr(self.lo_ext) if pe else None, 10000.0,
+               L.ptr(out), 0, 0 if out is None else out.stride(0), self.n, self.d, LN_EPS,
+               L.stream())
 
     def run(self, F: torch.Tensor) -> torch.Tensor:
         """F: (n, d) residual stream on the device (float32/float64), updated
         in place and returned."""
         w = self.w
         q, k, v = (self.qkv[:, i * self.d:(i + 1) * self.d] for i in range(3))
-        self._row_ln(F, None, None, w["ln1_g"], w["ln1_b"], self.pe, self.x)
+        self._row_ln(F, None, None, w["ln1_g"], w["ln1_b"], True, self.x)
         R = len(self.plans)
         for t, plan in enumerate(self.plans):
             torch.addmm(w["b_qkv"], self.x, w["w_qkv"], out=self.qkv)
@@ -178,7 +176,7 @@ class StageRunner:
                    L.stream())
             torch.mm(self.u, w["w_out"], out=self.y)
             if t + 1 < R:
-                self._row_ln(F, self.y, w["b_out"], w["ln1_g"], w["ln1_b"], self.pe, self.x)
+                self._row_ln(F, self.y, w["b_out"], w["ln1_g"], w["ln1_b"], True, self.x)
             else:
                 self._row_ln(F, self.y, w["b_out"], None, None, None, None)
         return F
