@@ -122,17 +122,20 @@ int f3d_gather_rows(const void *src, const int32_t *idx, int64_t n, int64_t row_
  * bw/stage.py:141-156).  One launch covers every scope of a round: scope s is
  * the concatenation of segments [scope_seg[s], scope_seg[s+1]) with physical
  * start seg_start[j] and virtual start seg_vstart[j]; scope_len[s] = m_s.
- * work: nwork x (scope, q_start) pairs (64-row query tiles).  q/k/v are bf16
- * rows with head h at columns [h*dh, (h+1)*dh) and row strides ld_*; o is bf16
- * (out_f32 = 0) or f32 with the same layout, written at the fixed rows.
- * mask (nullable): per-row uint8 validity; masked keys are excluded, masked
- * queries give 0.  starved (nullable): count of rows with no valid key. */
+ * work: nwork x (scope, q_start) pairs (128-row query tiles, streaming
+ * kernel); scope_order: the nlive non-empty scopes, longest first, and
+ * max_len = max m_s (whole-scope-resident kernel, chosen when head dim <= 64
+ * and the scope's K/V fit in shared memory).  q/k/v are bf16 rows with head h
+ * at columns [h*dh, (h+1)*dh) and row strides ld_*; o is bf16 (out_f32 = 0)
+ * or f32 with the same layout, written at the fixed rows.  mask (nullable):
+ * per-row uint8 validity; masked keys are excluded, masked queries give 0.
+ * starved (nullable): count of rows with no valid key. */
 int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_q,
                         int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
                         int dh, const int32_t *scope_seg, const int32_t *seg_start,
                         const int32_t *seg_vstart, const int32_t *scope_len,
-                        const int32_t *work, int nwork, const uint8_t *mask, int32_t *starved,
-                        void *stream);
+                        const int32_t *work, int nwork, const int32_t *scope_order, int nlive,
+                        int max_len, const uint8_t *mask, int32_t *starved, void *stream);
 
 /* ---------------------------------------------- a12: positional encoding
  * bw/attention.py:271-288 (d % 6 == 0).  out_f64: 1 -> double, 0 -> float. */

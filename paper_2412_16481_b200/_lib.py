@@ -44,7 +44,7 @@ SIGNATURES = {
     "f3d_scatter_rows": (_INT, [_P, _P, _I64, _I64, _P, _P]),
     "f3d_gather_rows": (_INT, [_P, _P, _I64, _I64, _P, _P]),
     "f3d_bswin_attention": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _INT, _INT, _INT, _P,
-                                   _P, _P, _P, _P, _INT, _P, _P, _P]),
+                                   _P, _P, _P, _P, _INT, _P, _INT, _INT, _P, _P, _P]),
     "f3d_positional_encoding": (_INT, [_P, _I64, _INT, _F64, _INT, _P, _I64, _P]),
     "f3d_stage_pe": (_INT, [_P, _I64, _INT, _F64, _P, _INT, _P, _I64, _P]),
     "f3d_coord_bbox": (_INT, [_P, _I64, _P, _P, _P]),

@@ -175,6 +175,7 @@ def plan_arrays(starts, lens, members):
     nseg = np.bincount(sc_of[new_seg], minlength=ns) if len(sc_of) else np.zeros(ns, np.int64)
     scope_seg = np.r_[0, np.cumsum(nseg)]
     order = np.argsort(-scope_len, kind="stable")
+    live = order[scope_len[order] > 0]
     nt = -(-scope_len[order] // BLOCK_M)
     wscope = np.repeat(order, nt)
     wfirst = np.repeat(np.cumsum(nt) - nt, nt)
@@ -182,7 +183,7 @@ def plan_arrays(starts, lens, members):
     work = np.stack([wscope, wq], 1) if len(wscope) else np.zeros((0, 2), np.int64)
     i32 = lambda x: np.ascontiguousarray(x, dtype=np.int32)
     return {"scope_seg": i32(scope_seg), "seg_start": i32(seg_start), "seg_vstart": i32(seg_vstart),
-            "scope_len": i32(scope_len), "work": i32(work)}
+            "scope_len": i32(scope_len), "work": i32(work), "scope_order": i32(live)}
 
 
 def schedule_members(schedule: "ScopeSchedule", t: int):
@@ -217,6 +218,8 @@ class RoundPlan:
         self.host = arrays
         lens = arrays["scope_len"].astype(np.int64)
         self.nwork = int(arrays["work"].shape[0])
+        self.nlive = int(arrays["scope_order"].shape[0])
+        self.max_len = int(lens.max()) if len(lens) else 0
         self.flops_per_head = int((lens.astype(np.float64) ** 2).sum())   # sum m^2
         up = uploaded if uploaded is not None else L.upload(arrays)
         self.scope_seg = up["scope_seg"]
@@ -224,6 +227,7 @@ class RoundPlan:
         self.seg_vstart = up["seg_vstart"]
         self.scope_len = up["scope_len"]
         self.work = up["work"]
+        self.scope_order = up["scope_order"]
 
     @classmethod
     def from_ranges(cls, scope_ranges, dev=None):
@@ -260,8 +264,8 @@ def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, star
     L.call("f3d_bswin_attention", L.ptr(q), L.ptr(k), L.ptr(v), q.stride(0), k.stride(0),
            v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads, dh,
            L.ptr(plan.scope_seg), L.ptr(plan.seg_start), L.ptr(plan.seg_vstart),
-           L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork, L.ptr(mask), L.ptr(starved),
-           L.stream())
+           L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork, L.ptr(plan.scope_order),
+           plan.nlive, plan.max_len, L.ptr(mask), L.ptr(starved), L.stream())
 
 
 def _check_finite(name, t):

@@ -11,6 +11,7 @@
 // softmax in exp2 domain (FlashAttention-2 structure, 4 warps x 16 rows).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cfloat>
 
 #include "f3d_common.cuh"
@@ -41,6 +42,9 @@ struct Args {
     int nwork;
     const uint8_t* mask;       // optional per-row validity (1 = present)
     int32_t* starved;          // optional counter of query rows with no valid key
+    const int32_t* scope_order;  // non-empty scopes, longest first (resident kernel)
+    int nlive;                 // number of non-empty scopes
+    int qsplit;                // CTAs per (scope, head) in the resident kernel
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -156,161 +160,100 @@ __device__ __forceinline__ void init_pad(unsigned char* smem, int dh, int rows_t
     }
 }
 
-template <int DH, bool kVec, bool kMask, typename OutT>
-__global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
-    constexpr int kRowB = DH * 2;
-    constexpr int kStride = kRowB + 16;   // odd number of 16 B chunks: conflict-free ldmatrix
-    constexpr int kNd = DH / 8;           // n8 blocks over the head dim
-    constexpr int kKd = DH / 16;          // k16 steps over the head dim
-    extern __shared__ __align__(16) unsigned char smem[];
-    __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem);
-    __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem + kBM * kStride);
-    __nv_bfloat16* sV = reinterpret_cast<__nv_bfloat16*>(smem + (kBM + 2 * kBN) * kStride);
+// One warp, one 64-key tile: S = Q K^T (raw), mask (tail / user mask), online
+// softmax in the exp2 domain (FFMA-folded scale), O += P V with P taken from
+// the S registers.  kb/vb point at the tile's 64 K / V rows in smem.
+template <int DH, bool kMask>
+__device__ __forceinline__ void warp_tile(const Args& A, const char* kb, const char* vb, int kbase,
+                                          int m, bool tail, int s0, int s1,
+                                          const uint32_t (&qf)[DH / 16][4],
+                                          float (&o_acc)[DH / 8][4], float (&m_run)[2],
+                                          float (&l_run)[2], bool ones, float sl2) {
+    constexpr int kStride = DH * 2 + 16;
+    constexpr int kNd = DH / 8;
+    constexpr int kKd = DH / 16;
+    const int lane = threadIdx.x & 31;
+    const int t = lane & 3;
+    float s[8][4];
+#pragma unroll
+    for (int nb = 0; nb < 8; ++nb) {
+        s[nb][0] = s[nb][1] = s[nb][2] = s[nb][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < kKd; ++kk) {
+            uint32_t b0, b1;
+            const int r = nb * 8 + (lane & 7);
+            const int c = kk * 16 + ((lane >> 3) & 1) * 8;
+            ldsm_x2(smem_u32(kb + r * kStride + c * 2), b0, b1);
+            mma16816(s[nb], qf[kk], b0, b1);
+        }
+    }
+    if (kMask || tail) {
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int key = kbase + nb * 8 + 2 * t + (e & 1);
+                bool ok = key < m;
+                if (kMask && ok) ok = A.mask[phys_row(A, s0, s1, key)] != 0;
+                if (!ok) s[nb][e] = -INFINITY;
+            }
+        }
+    }
+    float p_scale[2];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) mx = fmaxf(mx, fmaxf(s[nb][2 * hr], s[nb][2 * hr + 1]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run[hr], mx);
+        p_scale[hr] = ex2((m_run[hr] - m_new) * sl2);
+        m_run[hr] = m_new;
+        const float nms = -m_new * sl2;
+        float ls = 0.f;
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) {
+            const float p0 = ex2(fmaf(s[nb][2 * hr], sl2, nms));
+            const float p1 = ex2(fmaf(s[nb][2 * hr + 1], sl2, nms));
+            s[nb][2 * hr] = p0;
+            s[nb][2 * hr + 1] = p1;
+            if (!ones) ls += p0 + p1;
+        }
+        if (!ones) l_run[hr] = l_run[hr] * p_scale[hr] + ls;
+    }
+#pragma unroll
+    for (int i = 0; i < kNd; ++i) {
+        o_acc[i][0] *= p_scale[0];
+        o_acc[i][1] *= p_scale[0];
+        o_acc[i][2] *= p_scale[1];
+        o_acc[i][3] *= p_scale[1];
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        uint32_t pa[4];
+        pa[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
+        pa[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
+        pa[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+        pa[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+        for (int nd = 0; nd < kNd; ++nd) {
+            uint32_t b0, b1;
+            const int r = kk * 16 + (lane & 15);
+            ldsm_x2_t(smem_u32(vb + r * kStride + nd * 16), b0, b1);
+            mma16816(o_acc[nd], pa, b0, b1);
+        }
+    }
+}
 
-    const int wi = blockIdx.x;
-    if (wi >= A.nwork) return;
-    const int h = blockIdx.y;
-    const int scope = A.work[2 * wi];
-    const int q0 = A.work[2 * wi + 1];
-    const int s0 = A.scope_seg[scope], s1 = A.scope_seg[scope + 1];
-    const int m = A.scope_len[scope];
-    const int hcol = h * A.dh;
-    const bool ones = A.dh < DH;          // row sums ride in V's pad column
-
-    const int warp = threadIdx.x >> 5;
+// Normalise and write this warp's 16 query rows (virtual rows q0w..q0w+15).
+template <int DH, bool kMask, typename OutT>
+__device__ __forceinline__ void warp_epilogue(const Args& A, int q0w, int m, int s0, int s1,
+                                              int hcol, float (&o_acc)[DH / 8][4],
+                                              const float (&l_run)[2], bool ones) {
+    constexpr int kNd = DH / 8;
     const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    const bool warp_live = q0 + warp * 16 < m;
-
-    if (kVec) init_pad<DH>(smem, A.dh, kBM + 4 * kBN, kBM + 2 * kBN, 2 * kBN);
-    load_tile<DH, kVec>(A, A.q, A.ld_q, hcol, s0, s1, m, q0, sQ, kBM);
-    const int ntiles = (m + kBN - 1) / kBN;
-    load_tile<DH, kVec>(A, A.k, A.ld_k, hcol, s0, s1, m, 0, sK, kBN);
-    load_tile<DH, kVec>(A, A.v, A.ld_v, hcol, s0, s1, m, 0, sV, kBN, ones);
-    cp_async_commit();
-
-    float o_acc[kNd][4];
-#pragma unroll
-    for (int i = 0; i < kNd; ++i) o_acc[i][0] = o_acc[i][1] = o_acc[i][2] = o_acc[i][3] = 0.f;
-    float m_run[2] = {-FLT_MAX, -FLT_MAX};   // raw-score units
-    float l_run[2] = {0.f, 0.f};              // only when !ones
-    uint32_t qf[kKd][4];
-    const float sl2 = A.scale_log2;
-
-    for (int kt = 0; kt < ntiles; ++kt) {
-        const int buf = kt & 1;
-        if (kt + 1 < ntiles) {
-            const int nb = buf ^ 1;
-            load_tile<DH, kVec>(A, A.k, A.ld_k, hcol, s0, s1, m, (kt + 1) * kBN,
-                                reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(sK) +
-                                                                 nb * kBN * kStride),
-                                kBN);
-            load_tile<DH, kVec>(A, A.v, A.ld_v, hcol, s0, s1, m, (kt + 1) * kBN,
-                                reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(sV) +
-                                                                 nb * kBN * kStride),
-                                kBN, ones);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        if (warp_live) {
-            if (kt == 0) {
-                // Q fragments for this warp's 16 rows, kept in registers.
-                const char* qb = reinterpret_cast<const char*>(sQ) + (warp * 16) * kStride;
-#pragma unroll
-                for (int kk = 0; kk < kKd; ++kk) {
-                    const int r = lane & 15;
-                    const int c = kk * 16 + (lane >> 4) * 8;
-                    ldsm_x4(smem_u32(qb + r * kStride + c * 2), qf[kk][0], qf[kk][1], qf[kk][2],
-                            qf[kk][3]);
-                }
-            }
-            const char* kb = reinterpret_cast<const char*>(sK) + buf * kBN * kStride;
-            const char* vb = reinterpret_cast<const char*>(sV) + buf * kBN * kStride;
-
-            // S = Q K^T : 16 rows x 64 keys per warp (8 n8 blocks), raw scores
-            float s[8][4];
-#pragma unroll
-            for (int nb = 0; nb < 8; ++nb) {
-                s[nb][0] = s[nb][1] = s[nb][2] = s[nb][3] = 0.f;
-#pragma unroll
-                for (int kk = 0; kk < kKd; ++kk) {
-                    uint32_t b0, b1;
-                    const int r = nb * 8 + (lane & 7);
-                    const int c = kk * 16 + ((lane >> 3) & 1) * 8;
-                    ldsm_x2(smem_u32(kb + r * kStride + c * 2), b0, b1);
-                    mma16816(s[nb], qf[kk], b0, b1);
-                }
-            }
-            // masking only where it can matter: the ragged last tile, or a user mask
-            const int kbase = kt * kBN;
-            if (kMask || kt == ntiles - 1) {
-#pragma unroll
-                for (int nb = 0; nb < 8; ++nb) {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int key = kbase + nb * 8 + 2 * t + (e & 1);
-                        bool ok = key < m;
-                        if (kMask && ok) ok = A.mask[phys_row(A, s0, s1, key)] != 0;
-                        if (!ok) s[nb][e] = -INFINITY;
-                    }
-                }
-            }
-            // online softmax (rows g and g+8 of this warp), exp2 domain via FFMA
-            float p_scale[2];
-#pragma unroll
-            for (int hr = 0; hr < 2; ++hr) {
-                float mx = -INFINITY;
-#pragma unroll
-                for (int nb = 0; nb < 8; ++nb) mx = fmaxf(mx, fmaxf(s[nb][2 * hr], s[nb][2 * hr + 1]));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-                const float m_new = fmaxf(m_run[hr], mx);
-                p_scale[hr] = ex2((m_run[hr] - m_new) * sl2);
-                m_run[hr] = m_new;
-                const float nms = -m_new * sl2;
-                float ls = 0.f;
-#pragma unroll
-                for (int nb = 0; nb < 8; ++nb) {
-                    const float p0 = ex2(fmaf(s[nb][2 * hr], sl2, nms));
-                    const float p1 = ex2(fmaf(s[nb][2 * hr + 1], sl2, nms));
-                    s[nb][2 * hr] = p0;
-                    s[nb][2 * hr + 1] = p1;
-                    if (!ones) ls += p0 + p1;
-                }
-                if (!ones) l_run[hr] = l_run[hr] * p_scale[hr] + ls;
-            }
-#pragma unroll
-            for (int i = 0; i < kNd; ++i) {
-                o_acc[i][0] *= p_scale[0];
-                o_acc[i][1] *= p_scale[0];
-                o_acc[i][2] *= p_scale[1];
-                o_acc[i][3] *= p_scale[1];
-            }
-            // O += P V : P (16 x 64) as A fragments straight from the S registers
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                uint32_t pa[4];
-                pa[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
-                pa[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
-                pa[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-                pa[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
-#pragma unroll
-                for (int nd = 0; nd < kNd; ++nd) {
-                    uint32_t b0, b1;
-                    const int r = kk * 16 + (lane & 15);
-                    ldsm_x2_t(smem_u32(vb + r * kStride + nd * 16), b0, b1);
-                    mma16816(o_acc[nd], pa, b0, b1);
-                }
-            }
-        }
-        __syncthreads();
-    }
-    if (!warp_live) return;
-
-    // epilogue: normalise, write real rows of this head at their fixed rows
     float l_tot[2];
     if (ones) {
         // column dh of O holds the row sum: owned by quad lane (dh % 8) / 2
@@ -335,7 +278,7 @@ __global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
     }
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
-        const int vr = q0 + warp * 16 + g + 8 * hr;
+        const int vr = q0w + g + 8 * hr;
         if (vr >= m) continue;
         const int pr = phys_row(A, s0, s1, vr);
         bool qok = true;
@@ -348,7 +291,8 @@ __global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
             const int c = nd * 8 + 2 * t;
             const float a0 = o_acc[nd][2 * hr] * inv, a1 = o_acc[nd][2 * hr + 1] * inv;
             if (sizeof(OutT) == 2) {
-                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+                __nv_bfloat16* o =
+                    reinterpret_cast<__nv_bfloat16*>(A.o) + (int64_t)pr * A.ld_o + hcol;
                 if (c + 1 < A.dh) {
                     *reinterpret_cast<__nv_bfloat162*>(o + c) = __floats2bfloat162_rn(a0, a1);
                 } else if (c < A.dh) {
@@ -360,6 +304,189 @@ __global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
                 if (c + 1 < A.dh) o[c + 1] = a1;
             }
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Streaming kernel: work item = (scope, 128-row query tile, head); K/V tiles of
+// 64 rows double-buffered through smem with cp.async.  Any scope length.
+template <int DH, bool kVec, bool kMask, typename OutT>
+__global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
+    constexpr int kStride = DH * 2 + 16;   // odd number of 16 B chunks: conflict-free ldmatrix
+    constexpr int kNd = DH / 8;
+    constexpr int kKd = DH / 16;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem);
+    __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem + kBM * kStride);
+    __nv_bfloat16* sV = reinterpret_cast<__nv_bfloat16*>(smem + (kBM + 2 * kBN) * kStride);
+
+    const int wi = blockIdx.x;
+    if (wi >= A.nwork) return;
+    const int h = blockIdx.y;
+    const int scope = A.work[2 * wi];
+    const int q0 = A.work[2 * wi + 1];
+    const int s0 = A.scope_seg[scope], s1 = A.scope_seg[scope + 1];
+    const int m = A.scope_len[scope];
+    const int hcol = h * A.dh;
+    const bool ones = A.dh < DH;          // row sums ride in V's pad column
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const bool warp_live = q0 + warp * 16 < m;
+
+    if (kVec) init_pad<DH>(smem, A.dh, kBM + 4 * kBN, kBM + 2 * kBN, 2 * kBN);
+    load_tile<DH, kVec>(A, A.q, A.ld_q, hcol, s0, s1, m, q0, sQ, kBM);
+    const int ntiles = (m + kBN - 1) / kBN;
+    load_tile<DH, kVec>(A, A.k, A.ld_k, hcol, s0, s1, m, 0, sK, kBN);
+    load_tile<DH, kVec>(A, A.v, A.ld_v, hcol, s0, s1, m, 0, sV, kBN, ones);
+    cp_async_commit();
+
+    float o_acc[kNd][4];
+#pragma unroll
+    for (int i = 0; i < kNd; ++i) o_acc[i][0] = o_acc[i][1] = o_acc[i][2] = o_acc[i][3] = 0.f;
+    float m_run[2] = {-FLT_MAX, -FLT_MAX};
+    float l_run[2] = {0.f, 0.f};
+    uint32_t qf[kKd][4];
+
+    for (int kt = 0; kt < ntiles; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < ntiles) {
+            const int nb = buf ^ 1;
+            load_tile<DH, kVec>(A, A.k, A.ld_k, hcol, s0, s1, m, (kt + 1) * kBN,
+                                reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(sK) +
+                                                                 nb * kBN * kStride),
+                                kBN);
+            load_tile<DH, kVec>(A, A.v, A.ld_v, hcol, s0, s1, m, (kt + 1) * kBN,
+                                reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(sV) +
+                                                                 nb * kBN * kStride),
+                                kBN, ones);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        if (warp_live) {
+            if (kt == 0) {
+                const char* qb = reinterpret_cast<const char*>(sQ) + (warp * 16) * kStride;
+#pragma unroll
+                for (int kk = 0; kk < kKd; ++kk) {
+                    const int r = lane & 15;
+                    const int c = kk * 16 + (lane >> 4) * 8;
+                    ldsm_x4(smem_u32(qb + r * kStride + c * 2), qf[kk][0], qf[kk][1], qf[kk][2],
+                            qf[kk][3]);
+                }
+            }
+            warp_tile<DH, kMask>(A, reinterpret_cast<const char*>(sK) + buf * kBN * kStride,
+                                 reinterpret_cast<const char*>(sV) + buf * kBN * kStride,
+                                 kt * kBN, m, kt == ntiles - 1, s0, s1, qf, o_acc, m_run, l_run,
+                                 ones, A.scale_log2);
+        }
+        __syncthreads();
+    }
+    if (!warp_live) return;
+    warp_epilogue<DH, kMask, OutT>(A, q0 + warp * 16, m, s0, s1, hcol, o_acc, l_run, ones);
+}
+
+// ---------------------------------------------------------------------------
+// Resident kernel (small head dims, scopes <= max rows): one CTA per (scope,
+// head, q-part) loads the scope's whole K and V once into smem, then every
+// warp walks its own 16-row query blocks over all keys with no block barrier
+// in the loop — warps run independently, so latency hides across warps.
+constexpr int kResWarps = 16;
+constexpr int kResThreads = kResWarps * 32;
+
+template <int DH, typename OutT>
+__global__ void __launch_bounds__(kResThreads, 1) bswin_attn_resident_kernel(const Args A) {
+    constexpr int kStride = DH * 2 + 16;
+    constexpr int kNd = DH / 8;
+    constexpr int kKd = DH / 16;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int item = blockIdx.x / A.qsplit;
+    const int qpart = blockIdx.x - item * A.qsplit;
+    if (item >= A.nlive) return;
+    const int h = blockIdx.y;
+    const int scope = A.scope_order[item];
+    const int s0 = A.scope_seg[scope], s1 = A.scope_seg[scope + 1];
+    const int m = A.scope_len[scope];
+    const int mpad = (m + kBN - 1) / kBN * kBN;
+    const int hcol = h * A.dh;
+    const bool ones = A.dh < DH;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    unsigned char* sK = smem;
+    unsigned char* sV = smem + (size_t)mpad * kStride;
+    unsigned char* sQ = smem + (size_t)2 * mpad * kStride + warp * 16 * kStride;
+
+    // pad columns: zeros (K, V, Q) and the ones column of V
+    {
+        const int c0 = (A.dh * 2) / 16 * 8;
+        if (c0 < DH) {
+            const int rows = 2 * mpad;
+            for (int idx = threadIdx.x; idx < rows * (DH - c0); idx += kResThreads) {
+                const int r = idx / (DH - c0);
+                const int c = c0 + (idx - r * (DH - c0));
+                *reinterpret_cast<__nv_bfloat16*>(smem + (size_t)r * kStride + c * 2) =
+                    __float2bfloat16((r >= mpad && c == A.dh) ? 1.f : 0.f);
+            }
+            for (int idx = lane; idx < 16 * (DH - c0); idx += 32) {
+                const int r = idx / (DH - c0);
+                const int c = c0 + (idx - r * (DH - c0));
+                *reinterpret_cast<__nv_bfloat16*>(sQ + r * kStride + c * 2) = __float2bfloat16(0.f);
+            }
+        }
+    }
+    // K and V of the whole scope, once
+    const int real_chunks = (A.dh * 2) / 16;
+    for (int idx = threadIdx.x; idx < mpad * real_chunks; idx += kResThreads) {
+        const int r = idx / real_chunks;
+        const int c = idx - r * real_chunks;
+        const bool ok = r < m;
+        int64_t off = 0;
+        if (ok) off = (int64_t)phys_row(A, s0, s1, r);
+        cp_async16(sK + (size_t)r * kStride + c * 16, ok ? A.k + off * A.ld_k + hcol + c * 8 : A.k, ok);
+        cp_async16(sV + (size_t)r * kStride + c * 16, ok ? A.v + off * A.ld_v + hcol + c * 8 : A.v, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+
+    const int nqb = (m + 15) / 16;
+    const int ntiles = mpad / kBN;
+    for (int qb = warp * A.qsplit + qpart; qb < nqb; qb += kResWarps * A.qsplit) {
+        const int q0w = qb * 16;
+        // stage this warp's 16 query rows, then ldmatrix into registers
+        for (int idx = lane; idx < 16 * real_chunks; idx += 32) {
+            const int r = idx / real_chunks;
+            const int c = idx - r * real_chunks;
+            const bool ok = q0w + r < m;
+            const __nv_bfloat16* src = A.q;
+            if (ok) src = A.q + (int64_t)phys_row(A, s0, s1, q0w + r) * A.ld_q + hcol + c * 8;
+            cp_async16(sQ + r * kStride + c * 16, src, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        uint32_t qf[kKd][4];
+#pragma unroll
+        for (int kk = 0; kk < kKd; ++kk) {
+            const int r = lane & 15;
+            const int c = kk * 16 + (lane >> 4) * 8;
+            ldsm_x4(smem_u32(sQ + r * kStride + c * 2), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+        }
+        __syncwarp();
+        float o_acc[kNd][4];
+#pragma unroll
+        for (int i = 0; i < kNd; ++i) o_acc[i][0] = o_acc[i][1] = o_acc[i][2] = o_acc[i][3] = 0.f;
+        float m_run[2] = {-FLT_MAX, -FLT_MAX};
+        float l_run[2] = {0.f, 0.f};
+        for (int kt = 0; kt < ntiles; ++kt)
+            warp_tile<DH, false>(A, reinterpret_cast<const char*>(sK) + (size_t)kt * kBN * kStride,
+                                 reinterpret_cast<const char*>(sV) + (size_t)kt * kBN * kStride,
+                                 kt * kBN, m, kt == ntiles - 1, s0, s1, qf, o_acc, m_run, l_run,
+                                 ones, A.scale_log2);
+        warp_epilogue<DH, false, OutT>(A, q0w, m, s0, s1, hcol, o_acc, l_run, ones);
     }
 }
 
@@ -377,6 +504,29 @@ int launch_t(const Args& A, int H, cudaStream_t st) {
         }
     }
     kern<<<dim3(A.nwork, H), kThreads, smem, st>>>(A);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+template <int DH, typename OutT>
+int launch_resident(Args A, int H, int max_len, cudaStream_t st) {
+    constexpr int kStride = DH * 2 + 16;
+    const int mpad = (max_len + kBN - 1) / kBN * kBN;
+    const size_t smem = ((size_t)2 * mpad + 16 * kResWarps) * kStride;
+    auto kern = bswin_attn_resident_kernel<DH, OutT>;
+    static size_t done = 0;
+    if (smem > 48 * 1024 && smem > done) {
+        F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        done = smem;
+    }
+    // enough CTAs for ~4 waves of one CTA per SM
+    const int want = 4 * f3d_num_sms();
+    int qs = (want + A.nlive * H - 1) / (A.nlive * H);
+    const int nqb = (max_len + 15) / 16;
+    qs = std::max(1, std::min(qs, std::max(1, nqb / kResWarps)));
+    A.qsplit = qs;
+    kern<<<dim3(A.nlive * qs, H), kResThreads, smem, st>>>(A);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
@@ -405,6 +555,7 @@ extern "C" int f3d_bswin_attention(const void* q, const void* k, const void* v, 
                                    int out_f32, int H, int dh, const int32_t* scope_seg,
                                    const int32_t* seg_start, const int32_t* seg_vstart,
                                    const int32_t* scope_len, const int32_t* work, int nwork,
+                                   const int32_t* scope_order, int nlive, int max_len,
                                    const uint8_t* mask, int32_t* starved, void* stream) {
     if (H < 1 || dh < 1 || dh > 128 || nwork < 0) return F3D_ERR_CONFIG;
     if (nwork == 0) return F3D_OK;
@@ -427,11 +578,30 @@ extern "C" int f3d_bswin_attention(const void* q, const void* k, const void* v, 
     A.nwork = nwork;
     A.mask = mask;
     A.starved = starved;
+    A.scope_order = scope_order;
+    A.nlive = nlive;
+    A.qsplit = 1;
     const bool vec = ((dh * 2) % 16 == 0) && (ld_q % 8 == 0) && (ld_k % 8 == 0) &&
                      (ld_v % 8 == 0) && (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v) % 16 == 0);
     const bool msk = mask != nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     const int dp = (dh + 15) / 16 * 16;
+    // resident path: whole-scope K/V in smem (<= ~200 KB), small head dims
+    const size_t res_smem = ((size_t)2 * ((max_len + 63) / 64 * 64) + 16 * attn::kResWarps) *
+                            (dp * 2 + 16);
+    if (vec && !msk && scope_order && nlive > 0 && dp <= 64 && res_smem <= 200 * 1024) {
+        switch (dp) {
+            case 16: return out_f32 ? attn::launch_resident<16, float>(A, H, max_len, st)
+                                    : attn::launch_resident<16, __nv_bfloat16>(A, H, max_len, st);
+            case 32: return out_f32 ? attn::launch_resident<32, float>(A, H, max_len, st)
+                                    : attn::launch_resident<32, __nv_bfloat16>(A, H, max_len, st);
+            case 48: return out_f32 ? attn::launch_resident<48, float>(A, H, max_len, st)
+                                    : attn::launch_resident<48, __nv_bfloat16>(A, H, max_len, st);
+            case 64: return out_f32 ? attn::launch_resident<64, float>(A, H, max_len, st)
+                                    : attn::launch_resident<64, __nv_bfloat16>(A, H, max_len, st);
+            default: break;
+        }
+    }
     switch (dp) {
         case 16: return attn::launch_dh<16>(A, H, vec, msk, out_f32, st);
         case 32: return attn::launch_dh<32>(A, H, vec, msk, out_f32, st);
