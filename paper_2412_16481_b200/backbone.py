@@ -13,6 +13,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 import torch
+from torch.profiler import record_function
 
 from . import _lib as L
 from .attention import RoundPlan, plan_arrays, round_members
@@ -108,31 +109,36 @@ class Backbone:
         trace = []
         for si, cfg in enumerate(self.stages):
             n = C.shape[0]
-            a, counts_h, sweeps = self.bucketize(C, cfg)
+            with record_function(f"stage{si}.bucketize"):
+                a, counts_h, sweeps = self.bucketize(C, cfg)
             base_h = np.zeros_like(counts_h)
             base_h[1:] = np.cumsum(counts_h[:-1])
-            dest = a._dev["dest"]
-            d = X.shape[1]
-            Xf = X.to(torch.float32).contiguous()
-            F = torch.empty((n, d), dtype=torch.float32, device=C.device)
-            Cs = torch.empty_like(C)
-            L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F), L.stream())
-            L.call("f3d_scatter_rows", L.ptr(C), L.ptr(dest), n, 24, L.ptr(Cs), L.stream())
-            table = split_table(counts_h, base_h, cfg.K, cfg.S)
-            nb = len(table[0])
-            if cfg.W > nb:
-                raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb})")
-            plans = [RoundPlan(plan_arrays(table[0], table[1],
-                                           round_members(nb, cfg.W, cfg.stride, cfg.shift, t)))
-                     for t in range(cfg.rounds)]
-            runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
-                                 weights=self._w[si], plans=plans)
-            runner.run(F)
+            with record_function(f"stage{si}.scatter"):
+                dest = a._dev["dest"]
+                d = X.shape[1]
+                Xf = X.to(torch.float32).contiguous()
+                F = torch.empty((n, d), dtype=torch.float32, device=C.device)
+                Cs = torch.empty_like(C)
+                L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F), L.stream())
+                L.call("f3d_scatter_rows", L.ptr(C), L.ptr(dest), n, 24, L.ptr(Cs), L.stream())
+            with record_function(f"stage{si}.plan"):
+                table = split_table(counts_h, base_h, cfg.K, cfg.S)
+                nb = len(table[0])
+                if cfg.W > nb:
+                    raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb})")
+                plans = [RoundPlan(plan_arrays(table[0], table[1],
+                                               round_members(nb, cfg.W, cfg.stride, cfg.shift, t)))
+                         for t in range(cfg.rounds)]
+                runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
+                                     weights=self._w[si], plans=plans)
+            with record_function(f"stage{si}.run"):
+                runner.run(F)
             if keep_trace:
                 trace.append(StageTrace(n, counts_h, a, runner.attention_flops(), sweeps))
             if cfg.pool_rho:
-                X, C, _ = pool_device(F, Cs, counts_h, base_h, cfg.K, cfg.S, 1, cfg.pool_rho,
-                                      "mean", check=False, assignment=False)
+                with record_function(f"stage{si}.pool"):
+                    X, C, _ = pool_device(F, Cs, counts_h, base_h, cfg.K, cfg.S, 1, cfg.pool_rho,
+                                          "mean", check=False, assignment=False)
             else:
                 X, C = F, Cs
         self.last_trace = trace
