@@ -120,8 +120,10 @@ int f3d_gather_rows(const void *src, const int32_t *idx, int64_t n, int64_t row_
 /* ------------------------------------------ a9-a11: bucket-swin attention
  * Replaces bw/attention.py:188-268 tiled_attention (and the per-scope loop of
  * bw/stage.py:141-156).  One launch covers every scope of a round: scope s is
- * the concatenation of segments [scope_seg[s], scope_seg[s+1]) with physical
- * start seg_start[j] and virtual start seg_vstart[j]; scope_len[s] = m_s.
+ * the concatenation of segments j in [scope_seg[s], scope_seg[s]+scope_nseg[s])
+ * with physical start seg_start[j] and virtual start seg_vstart[j];
+ * scope_len[s] = m_s.  live (nullable, device): [nwork, nlive, max_len] as
+ * written by f3d_plan_round; nwork / nlive / max_len are then upper bounds.
  * work: nwork x (scope, q_start) pairs (128-row query tiles, streaming
  * kernel); scope_order: the nlive non-empty scopes, longest first, and
  * max_len = max m_s (whole-scope-resident kernel, chosen when head dim <= 64
@@ -132,10 +134,27 @@ int f3d_gather_rows(const void *src, const int32_t *idx, int64_t n, int64_t row_
  * starved (nullable): count of rows with no valid key. */
 int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_q,
                         int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
-                        int dh, const int32_t *scope_seg, const int32_t *seg_start,
-                        const int32_t *seg_vstart, const int32_t *scope_len,
-                        const int32_t *work, int nwork, const int32_t *scope_order, int nlive,
-                        int max_len, const uint8_t *mask, int32_t *starved, void *stream);
+                        int dh, const int32_t *scope_seg, const int32_t *scope_nseg,
+                        const int32_t *seg_start, const int32_t *seg_vstart,
+                        const int32_t *scope_len, const int32_t *work, int nwork,
+                        const int32_t *scope_order, int nlive, int max_len, const int32_t *live,
+                        const uint8_t *mask, int32_t *starved, void *stream);
+
+/* Device planner for one round (bw/attention.py:84-139 over the split table
+ * of bw/bucketing.py:147-166, built from the PSH counts/base in HBM).
+ * nscopes = ceil(nb / (W*stride)) * stride; segment arrays hold nscopes*W
+ * entries (fixed stride W per scope); work holds max_work (scope, q_start)
+ * pairs; live receives [nwork, nlive, max_len].  off = (t*shift) mod W. */
+int f3d_plan_round(const int32_t *counts, const int32_t *base, int K, int S, int nb, int W,
+                   int stride, int off, int nscopes, int32_t *scope_seg, int32_t *scope_nseg,
+                   int32_t *seg_start, int32_t *seg_vstart, int32_t *scope_len,
+                   int32_t *scope_order, int32_t *work, int max_work, int32_t *live,
+                   void *stream);
+/* Device pooling tile table (bw/pooling.py:211-225): tiles of <= cap rows per
+ * slot in scatter order; totals receives [ntiles, npooled]. */
+int f3d_plan_pool(const int32_t *counts, const int32_t *base, int nslots, int cap, int rho,
+                  int32_t *tile_start, int32_t *tile_m, int32_t *tile_out, int32_t *totals,
+                  void *stream);
 
 /* ---------------------------------------------- a12: positional encoding
  * bw/attention.py:271-288 (d % 6 == 0).  out_f64: 1 -> double, 0 -> float. */

@@ -182,8 +182,9 @@ def plan_arrays(starts, lens, members):
     wq = (np.arange(len(wscope)) - wfirst) * BLOCK_M
     work = np.stack([wscope, wq], 1) if len(wscope) else np.zeros((0, 2), np.int64)
     i32 = lambda x: np.ascontiguousarray(x, dtype=np.int32)
-    return {"scope_seg": i32(scope_seg), "seg_start": i32(seg_start), "seg_vstart": i32(seg_vstart),
-            "scope_len": i32(scope_len), "work": i32(work), "scope_order": i32(live)}
+    return {"scope_seg": i32(scope_seg), "scope_nseg": i32(nseg), "seg_start": i32(seg_start),
+            "seg_vstart": i32(seg_vstart), "scope_len": i32(scope_len), "work": i32(work),
+            "scope_order": i32(live)}
 
 
 def schedule_members(schedule: "ScopeSchedule", t: int):
@@ -223,6 +224,8 @@ class RoundPlan:
         self.flops_per_head = int((lens.astype(np.float64) ** 2).sum())   # sum m^2
         up = uploaded if uploaded is not None else L.upload(arrays)
         self.scope_seg = up["scope_seg"]
+        self.scope_nseg = up["scope_nseg"]
+        self.live = None
         self.seg_start = up["seg_start"]
         self.seg_vstart = up["seg_vstart"]
         self.scope_len = up["scope_len"]
@@ -245,6 +248,39 @@ class RoundPlan:
         return cls(plan_arrays(np.array(starts + [0]), np.array(lens + [0]), M))
 
 
+class DeviceRoundPlan:
+    """Scope tables of one round built on the device by f3d_plan_round from
+    the PSH counts/base (no per-scope host work, no read-back).  nwork /
+    nlive are upper bounds for the launch grid; the kernels read the exact
+    values from ``live``."""
+
+    def __init__(self, counts_dev, base_dev, K, S, nb, W, stride, shift, t, n):
+        span = W * stride
+        ns = -(-nb // span) * stride
+        self.nlive = ns
+        self.nwork = n // BLOCK_M + ns
+        self.max_len = W * S
+        i32 = torch.int32
+        buf = L.empty((3 * ns + 2 * ns * W + ns + 2 * self.nwork + 4,), i32)
+        o = 0
+
+        def take(k):
+            nonlocal o
+            v = buf[o:o + k]
+            o += k
+            return v
+        self.scope_seg, self.scope_nseg, self.scope_len = take(ns), take(ns), take(ns)
+        self.seg_start, self.seg_vstart = take(ns * W), take(ns * W)
+        self.scope_order = take(ns)
+        self.work = take(2 * self.nwork).view(-1, 2)
+        self.live = take(4)
+        L.call("f3d_plan_round", L.ptr(counts_dev), L.ptr(base_dev), K, S, nb, W, stride,
+               (t * shift) % W, ns, L.ptr(self.scope_seg), L.ptr(self.scope_nseg),
+               L.ptr(self.seg_start), L.ptr(self.seg_vstart), L.ptr(self.scope_len),
+               L.ptr(self.scope_order), L.ptr(self.work), self.nwork, L.ptr(self.live),
+               L.stream())
+
+
 def plan_schedule(table, schedule: ScopeSchedule, dev=None):
     """One RoundPlan per round of the schedule over a (starts, lengths) table."""
     starts, lengths = _table_np(table)
@@ -263,9 +299,10 @@ def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, star
     or fp32 rows with the same head layout."""
     L.call("f3d_bswin_attention", L.ptr(q), L.ptr(k), L.ptr(v), q.stride(0), k.stride(0),
            v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads, dh,
-           L.ptr(plan.scope_seg), L.ptr(plan.seg_start), L.ptr(plan.seg_vstart),
-           L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork, L.ptr(plan.scope_order),
-           plan.nlive, plan.max_len, L.ptr(mask), L.ptr(starved), L.stream())
+           L.ptr(plan.scope_seg), L.ptr(plan.scope_nseg), L.ptr(plan.seg_start),
+           L.ptr(plan.seg_vstart), L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork,
+           L.ptr(plan.scope_order), plan.nlive, plan.max_len, L.ptr(plan.live), L.ptr(mask),
+           L.ptr(starved), L.stream())
 
 
 def _check_finite(name, t):

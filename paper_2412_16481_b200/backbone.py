@@ -16,7 +16,7 @@ import torch
 from torch.profiler import record_function
 
 from . import _lib as L
-from .attention import RoundPlan, plan_arrays, round_members
+from .attention import DeviceRoundPlan, RoundPlan, plan_arrays, round_members
 from .bucketing import BucketAssignment, _run_psh, default_probe_schedule
 from .errors import ConfigError, RangeError
 from .hashing import HashConfig, raise_range
@@ -122,13 +122,12 @@ class Backbone:
                 L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F), L.stream())
                 L.call("f3d_scatter_rows", L.ptr(C), L.ptr(dest), n, 24, L.ptr(Cs), L.stream())
             with record_function(f"stage{si}.plan"):
-                table = split_table(counts_h, base_h, cfg.K, cfg.S)
-                nb = len(table[0])
+                nb = cfg.K + -(-int(counts_h[cfg.K]) // cfg.S)
                 if cfg.W > nb:
                     raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb})")
-                plans = [RoundPlan(plan_arrays(table[0], table[1],
-                                               round_members(nb, cfg.W, cfg.stride, cfg.shift, t)))
-                         for t in range(cfg.rounds)]
+                cd, bd = a._dev["counts"], a._dev["base"]
+                plans = [DeviceRoundPlan(cd, bd, cfg.K, cfg.S, nb, cfg.W, cfg.stride, cfg.shift,
+                                         t, n) for t in range(cfg.rounds)]
                 runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
                                      weights=self._w[si], plans=plans)
             with record_function(f"stage{si}.run"):
@@ -138,7 +137,8 @@ class Backbone:
             if cfg.pool_rho:
                 with record_function(f"stage{si}.pool"):
                     X, C, _ = pool_device(F, Cs, counts_h, base_h, cfg.K, cfg.S, 1, cfg.pool_rho,
-                                          "mean", check=False, assignment=False)
+                                          "mean", check=False, assignment=False,
+                                          dev_counts=(a._dev["counts"], a._dev["base"]))
             else:
                 X, C = F, Cs
         self.last_trace = trace

@@ -34,7 +34,8 @@ struct Args {
     int dh;                    // real head dim
     float scale_log2;          // log2(e) / sqrt(dh)
     // scopes
-    const int32_t* scope_seg;  // [nscopes+1] first segment of each scope
+    const int32_t* scope_seg;  // first segment of each scope
+    const int32_t* scope_nseg; // segments per scope
     const int32_t* seg_start;  // physical start
     const int32_t* seg_vstart; // virtual start within the scope
     const int32_t* scope_len;  // m_s
@@ -45,6 +46,7 @@ struct Args {
     const int32_t* scope_order;  // non-empty scopes, longest first (resident kernel)
     int nlive;                 // number of non-empty scopes
     int qsplit;                // CTAs per (scope, head) in the resident kernel
+    const int32_t* live;       // optional device [nwork, nlive, max_len] (device planner)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -321,11 +323,11 @@ __global__ void __launch_bounds__(kThreads) bswin_attn_kernel(const Args A) {
     __nv_bfloat16* sV = reinterpret_cast<__nv_bfloat16*>(smem + (kBM + 2 * kBN) * kStride);
 
     const int wi = blockIdx.x;
-    if (wi >= A.nwork) return;
+    if (wi >= (A.live ? __ldg(A.live) : A.nwork)) return;
     const int h = blockIdx.y;
     const int scope = A.work[2 * wi];
     const int q0 = A.work[2 * wi + 1];
-    const int s0 = A.scope_seg[scope], s1 = A.scope_seg[scope + 1];
+    const int s0 = A.scope_seg[scope], s1 = s0 + A.scope_nseg[scope];
     const int m = A.scope_len[scope];
     const int hcol = h * A.dh;
     const bool ones = A.dh < DH;          // row sums ride in V's pad column
@@ -404,10 +406,10 @@ __global__ void __launch_bounds__(kResThreads, 1) bswin_attn_resident_kernel(con
     extern __shared__ __align__(16) unsigned char smem[];
     const int item = blockIdx.x / A.qsplit;
     const int qpart = blockIdx.x - item * A.qsplit;
-    if (item >= A.nlive) return;
+    if (item >= (A.live ? __ldg(A.live + 1) : A.nlive)) return;
     const int h = blockIdx.y;
     const int scope = A.scope_order[item];
-    const int s0 = A.scope_seg[scope], s1 = A.scope_seg[scope + 1];
+    const int s0 = A.scope_seg[scope], s1 = s0 + A.scope_nseg[scope];
     const int m = A.scope_len[scope];
     const int mpad = (m + kBN - 1) / kBN * kBN;
     const int hcol = h * A.dh;
@@ -553,9 +555,10 @@ using namespace f3d;
 extern "C" int f3d_bswin_attention(const void* q, const void* k, const void* v, int64_t ld_q,
                                    int64_t ld_k, int64_t ld_v, void* o, int64_t ld_o,
                                    int out_f32, int H, int dh, const int32_t* scope_seg,
-                                   const int32_t* seg_start, const int32_t* seg_vstart,
-                                   const int32_t* scope_len, const int32_t* work, int nwork,
-                                   const int32_t* scope_order, int nlive, int max_len,
+                                   const int32_t* scope_nseg, const int32_t* seg_start,
+                                   const int32_t* seg_vstart, const int32_t* scope_len,
+                                   const int32_t* work, int nwork, const int32_t* scope_order,
+                                   int nlive, int max_len, const int32_t* live,
                                    const uint8_t* mask, int32_t* starved, void* stream) {
     if (H < 1 || dh < 1 || dh > 128 || nwork < 0) return F3D_ERR_CONFIG;
     if (nwork == 0) return F3D_OK;
@@ -571,6 +574,8 @@ extern "C" int f3d_bswin_attention(const void* q, const void* k, const void* v, 
     A.dh = dh;
     A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)dh));
     A.scope_seg = scope_seg;
+    A.scope_nseg = scope_nseg;
+    A.live = live;
     A.seg_start = seg_start;
     A.seg_vstart = seg_vstart;
     A.scope_len = scope_len;

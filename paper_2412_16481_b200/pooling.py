@@ -94,6 +94,25 @@ class TilePlan:
         self.tile_out = up["tile_out"]
 
 
+class DeviceTilePlan:
+    """TilePlan built on the device by f3d_plan_pool from the PSH counts/base;
+    only the totals (tile and pooled-row counts, needed for allocation) are
+    computed on the host from the counts already read back."""
+
+    def __init__(self, counts_h, counts_dev, base_dev, rho):
+        c = np.asarray(counts_h, dtype=np.int64)
+        full, rem = c // TILE_CAP, c % TILE_CAP
+        self.ntiles = int((-(-c // TILE_CAP)).sum())
+        self.npool = int((full * (-(-TILE_CAP // rho)) + (-(-rem // rho))).sum())
+        buf = L.empty((3 * max(1, self.ntiles) + 2,), torch.int32)
+        k = max(1, self.ntiles)
+        self.tile_start, self.tile_m, self.tile_out = buf[:k], buf[k:2 * k], buf[2 * k:3 * k]
+        self.totals = buf[3 * k:]
+        L.call("f3d_plan_pool", L.ptr(counts_dev), L.ptr(base_dev), len(c), TILE_CAP, rho,
+               L.ptr(self.tile_start), L.ptr(self.tile_m), L.ptr(self.tile_out),
+               L.ptr(self.totals), L.stream())
+
+
 def _build(coords_dev, plan: TilePlan, rho: int, want_sub=False, want_seeds=False):
     n = coords_dev.shape[0]
     members = L.empty((max(1, plan.npool), rho), torch.int32)
@@ -209,10 +228,15 @@ def pool_stage(features, coords, assignment: BucketAssignment, rho: int, reduce:
     return pf, pc, na
 
 
-def pool_device(x, C, counts, base, K, S, nbatch, rho, reduce, check=True, assignment=True):
+def pool_device(x, C, counts, base, K, S, nbatch, rho, reduce, check=True, assignment=True,
+                dev_counts=None):
     """Device path of pool_stage given host counts/base; returns device
-    tensors and (optionally) a device-resident BucketAssignment."""
-    plan = TilePlan(counts, base, rho, x.device)
+    tensors and (optionally) a device-resident BucketAssignment.
+    dev_counts = (counts_dev, base_dev) builds the tile table on the device."""
+    if dev_counts is not None:
+        plan = DeviceTilePlan(counts, dev_counts[0], dev_counts[1], rho)
+    else:
+        plan = TilePlan(counts, base, rho, x.device)
     members, sizes, _, _, _, flags = _build(C, plan, rho)
     if check:
         _raise_flags(int(flags.item()))
@@ -220,6 +244,8 @@ def pool_device(x, C, counts, base, K, S, nbatch, rho, reduce, check=True, assig
     pc = _reduce(C, members, sizes, plan.npool, rho, "mean")
     na = None
     if assignment:
+        if not hasattr(plan, "new_counts"):
+            plan = TilePlan(counts, base, rho, x.device)
         na = new_assignment(plan.new_counts, K, max(1, math.ceil(S / rho)), nbatch, x.device)
     return pf, pc, na
 

@@ -183,8 +183,16 @@ class StageRunner:
 
     def attention_flops(self) -> int:
         """Algorithmic attention FLOPs per run: sum over rounds and scopes of
-        4 * m_s^2 * d."""
-        return sum(4 * p.flops_per_head * self.d for p in self.plans)
+        4 * m_s^2 * d; device plans are read back here
+        (bench bookkeeping only, outside the timed region)."""
+        tot = 0
+        for p in self.plans:
+            if hasattr(p, "flops_per_head"):
+                tot += p.flops_per_head
+            else:
+                ln = p.scope_len.to(torch.float64)
+                tot += int((ln * ln).sum().item())
+        return 4 * tot * self.d
 
 
 def stage_forward(features, coords, assignment: BucketAssignment, schedule: ScopeSchedule,

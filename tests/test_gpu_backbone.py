@@ -1,0 +1,94 @@
+"""GPU: device planners equal the host planners; the full backbone forward
+matches the oracle composition (layouts bit-exact, features within the stage
+tolerance)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import restated as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_2412_16481_b200 import attention as A  # noqa: E402
+from paper_2412_16481_b200.backbone import (Backbone, StageConfig,  # noqa: E402
+                                            scannet_backbone, split_table)
+from paper_2412_16481_b200.pooling import DeviceTilePlan, TilePlan  # noqa: E402
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_device_round_plan_equals_host(seed):
+    r = np.random.default_rng(seed)
+    K, S = int(r.integers(2, 400)), int(r.choice((64, 128, 512)))
+    counts = r.integers(0, S + 1, size=K + 1)
+    counts[K] = int(r.integers(0, 3 * S))
+    base = O.exclusive_scan(counts)
+    n = int(counts.sum())
+    starts, lens = split_table(counts, base, K, S)
+    nb = len(starts)
+    W = int(r.integers(1, min(6, nb) + 1))
+    stride = int(r.integers(1, 4))
+    shift = int(r.integers(0, W))
+    cd = torch.tensor(counts, dtype=torch.int32, device="cuda")
+    bd = torch.tensor(base, dtype=torch.int32, device="cuda")
+    for t in range(3):
+        dp = A.DeviceRoundPlan(cd, bd, K, S, nb, W, stride, shift, t, n)
+        hp = A.plan_arrays(starts, lens, A.round_members(nb, W, stride, shift, t))
+        live = dp.live.cpu().numpy()
+        assert live[1] == len(hp["scope_order"])
+        assert live[2] == hp["scope_len"].max()
+        ns = len(hp["scope_len"])
+        np.testing.assert_array_equal(dp.scope_len.cpu().numpy()[:ns], hp["scope_len"])
+        np.testing.assert_array_equal(dp.scope_nseg.cpu().numpy()[:ns], hp["scope_nseg"])
+        segs = dp.seg_start.cpu().numpy().reshape(-1, W)
+        vsts = dp.seg_vstart.cpu().numpy().reshape(-1, W)
+        for s in range(ns):
+            a, b = hp["scope_seg"][s], hp["scope_seg"][s] + hp["scope_nseg"][s]
+            np.testing.assert_array_equal(segs[s, :b - a], hp["seg_start"][a:b])
+            np.testing.assert_array_equal(vsts[s, :b - a], hp["seg_vstart"][a:b])
+        w = dp.work.cpu().numpy()[:live[0]]
+        assert sorted(map(tuple, w)) == sorted(map(tuple, hp["work"]))
+
+
+def test_device_tile_plan_equals_host():
+    r = np.random.default_rng(3)
+    counts = r.integers(0, 2600, size=300)
+    base = O.exclusive_scan(counts)
+    for rho in (1, 2, 3, 7):
+        cd = torch.tensor(counts, dtype=torch.int32, device="cuda")
+        bd = torch.tensor(base, dtype=torch.int32, device="cuda")
+        dp = DeviceTilePlan(counts, cd, bd, rho)
+        hp = TilePlan(counts, base, rho, "cuda")
+        assert dp.ntiles == hp.ntiles and dp.npool == hp.npool
+        for name in ("tile_start", "tile_m", "tile_out"):
+            np.testing.assert_array_equal(getattr(dp, name).cpu().numpy()[:dp.ntiles],
+                                          getattr(hp, name).cpu().numpy()[:hp.ntiles])
+        assert dp.totals.cpu().tolist() == [dp.ntiles, dp.npool]
+
+
+def test_backbone_matches_oracle_composition():
+    n = 20_000
+    coords = O.synth_cloud(11, n, "uniform-box")
+    feats = np.random.default_rng(2).normal(size=(n, 96))
+    stages = (StageConfig(K=64, S=512, S_div=4096, pool_rho=2, seed=0),
+              StageConfig(K=32, S=512, S_div=8192, pool_rho=0, seed=1))
+    bb = Backbone(stages)
+    f, c = bb.forward(torch.tensor(coords, device="cuda"),
+                      torch.tensor(feats, dtype=torch.float32, device="cuda"))
+    of, oc = O.backbone_forward(coords, feats, stages, threads=8)
+    np.testing.assert_array_equal(c.cpu().numpy(), oc)       # layouts + centroids exact
+    fr = f.cpu().numpy().astype(np.float64)
+    rel = np.linalg.norm(fr - of) / np.linalg.norm(of)
+    assert rel < 2e-2, rel
+
+
+def test_scannet_backbone_runs_and_is_deterministic():
+    import bench
+    coords, feats = bench.workload(0)
+    bb = Backbone(scannet_backbone())
+    C = torch.tensor(coords, device="cuda")
+    X = torch.tensor(feats, dtype=torch.float32, device="cuda")
+    f1, c1 = bb.forward(C, X)
+    f2, c2 = bb.forward(C, X)
+    assert torch.equal(c1, c2) and torch.equal(f1, f2)
+    assert torch.isfinite(f1).all()
