@@ -101,6 +101,32 @@ class Backbone:
                                    "batch": None, "dest": dest, "info": info})
         return a, counts_h, int(host[7 + cfg.K + 1])
 
+    def forward_host(self, coords_h, feats_h, out_h=None):
+        """End-to-end call with HOST buffers (pinned for async copies):
+        coords (n,3) float64, feats (n,d) bf16/float32.  The feature upload
+        runs on a side stream and overlaps the first PSH; the result (last
+        stage features, bf16) is copied back into ``out_h`` (allocated pinned
+        if None) and returned with the stage-2 coordinates left on device."""
+        dev = L.device()
+        main = torch.cuda.current_stream()
+        side = getattr(self, "_side", None)
+        if side is None:
+            side = self._side = torch.cuda.Stream()
+        C = coords_h.to(dev, non_blocking=True)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            X = feats_h.to(dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        self._feat_event = ev
+        f, c = self.forward(C, X)
+        fb = f.to(torch.bfloat16)
+        if out_h is None or tuple(out_h.shape) != tuple(fb.shape):
+            out_h = torch.empty(fb.shape, dtype=fb.dtype).pin_memory()
+        out_h.copy_(fb, non_blocking=True)
+        X.record_stream(main)
+        return out_h, c
+
     def forward(self, coords, feats, keep_trace=False):
         """coords (n,3) float64, feats (n,d) float32/bf16 CUDA tensors.
         Returns (features, coords) of the last stage in its scattered order."""
@@ -114,6 +140,10 @@ class Backbone:
             base_h = np.zeros_like(counts_h)
             base_h[1:] = np.cumsum(counts_h[:-1])
             with record_function(f"stage{si}.scatter"):
+                ev = getattr(self, "_feat_event", None)
+                if ev is not None:
+                    torch.cuda.current_stream().wait_event(ev)   # features uploaded
+                    self._feat_event = None
                 dest = a._dev["dest"]
                 d = X.shape[1]
                 Xf = X.to(torch.float32).contiguous()

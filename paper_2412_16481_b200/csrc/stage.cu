@@ -101,53 +101,49 @@ __device__ __forceinline__ void store_out(__nv_bfloat16* p, double v) { *p = __f
 __device__ __forceinline__ void store_out(float* p, double v) { *p = (float)v; }
 __device__ __forceinline__ void store_out(double* p, double v) { *p = v; }
 
-template <typename FT, typename OT>
-__global__ void row_ln_kernel(FT* __restrict__ F, int64_t ldf, const __nv_bfloat16* __restrict__ y,
-                              int64_t ldy, const float* __restrict__ ybias,
-                              const float* __restrict__ gain, const float* __restrict__ beta,
-                              const double* __restrict__ pec, const double* __restrict__ lo_ext,
-                              float pe_log2base, OT* __restrict__ out, int64_t ldo, int64_t n,
-                              int d, double eps) {
+template <typename FT, typename OT, int PER>
+__global__ void __launch_bounds__(kThreads) row_ln_kernel(
+    FT* __restrict__ F, int64_t ldf, const __nv_bfloat16* __restrict__ y, int64_t ldy,
+    const float* __restrict__ ybias, const float* __restrict__ gain,
+    const float* __restrict__ beta, const double* __restrict__ pec,
+    const double* __restrict__ lo_ext, float pe_log2base, OT* __restrict__ out, int64_t ldo,
+    int64_t n, int d, double eps) {
     using A = typename Acc<FT>::type;
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
     if (row >= n) return;
-    A v[kMaxPerLane];
-    const int per = (d + 31) / 32;
     FT* fr = F + row * ldf;
+    // issue every load of the row first (ILP), then reduce
+    A v[PER];
+    A yv[PER];
 #pragma unroll
-    for (int j = 0; j < kMaxPerLane; ++j) {
-        if (j >= per) break;
+    for (int j = 0; j < PER; ++j) {
         const int c = lane + 32 * j;
-        if (c < d) {
-            A x = (A)fr[c];
-            if (y) {
-                x += (A)to_f(y[row * ldy + c]) + (ybias ? (A)ybias[c] : (A)0);
-                fr[c] = (FT)x;
+        v[j] = (c < d) ? (A)fr[c] : (A)0;
+        yv[j] = (y && c < d) ? (A)to_f(y[row * ldy + c]) : (A)0;
+    }
+    if (y) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int c = lane + 32 * j;
+            if (c < d) {
+                v[j] += yv[j] + (ybias ? (A)ybias[c] : (A)0);
+                fr[c] = (FT)v[j];
             }
-            v[j] = x;
-        } else {
-            v[j] = 0;
         }
     }
     if (!out) return;
     A s = 0;
 #pragma unroll
-    for (int j = 0; j < kMaxPerLane; ++j) {
-        if (j >= per) break;
-        s += v[j];
-    }
+    for (int j = 0; j < PER; ++j) s += v[j];
     s = warp_sum(s);
     const A mean = s / (A)d;
     A q = 0;
 #pragma unroll
-    for (int j = 0; j < kMaxPerLane; ++j) {
-        if (j >= per) break;
+    for (int j = 0; j < PER; ++j) {
         const int c = lane + 32 * j;
-        if (c < d) {
-            const A t = v[j] - mean;
-            q += t * t;
-        }
+        const A t = (c < d) ? v[j] - mean : (A)0;
+        q += t * t;
     }
     q = warp_sum(q);
     const A rstd = (A)1 / sqrt(q / (A)d + (A)eps);
@@ -165,15 +161,14 @@ __global__ void row_ln_kernel(FT* __restrict__ F, int64_t ldf, const __nv_bfloat
         }
     }
 #pragma unroll
-    for (int j = 0; j < kMaxPerLane; ++j) {
-        if (j >= per) break;
+    for (int j = 0; j < PER; ++j) {
         const int c = lane + 32 * j;
         if (c < d) {
             A o = (v[j] - mean) * rstd * (A)gain[c] + (A)beta[c];
             if (pec) {
-                const int a = c / blk, k = c - a * blk, jj = k >> 1;
                 // |ang| <= ~1 for normalised coords: the fast MUFU forms are
                 // accurate to ~1e-6 absolute, far inside the bf16 output
+                const int a = c / blk, k = c - a * blk, jj = k >> 1;
                 const float ang = xn[a] * exp2f(-(float)jj / (float)npair * pe_log2base);
                 o += (A)((k & 1) ? __cosf(ang) : __sinf(ang));
             }
@@ -266,22 +261,53 @@ extern "C" int f3d_stage_pe(const double* coords, int64_t n, int d, double base,
     return F3D_OK;
 }
 
+template <typename FT, typename OT, int PER>
+static void launch_row_ln_p(unsigned g, cudaStream_t st, void* F, int64_t ldf, const void* y,
+                            int64_t ldy, const float* ybias, const float* gain, const float* beta,
+                            const double* pec, const double* lo_ext, float pl2, void* out,
+                            int64_t ldo, int64_t n, int d, double eps) {
+    stage::row_ln_kernel<FT, OT, PER><<<g, stage::kThreads, 0, st>>>(
+        (FT*)F, ldf, (const __nv_bfloat16*)y, ldy, ybias, gain, beta, pec, lo_ext, pl2, (OT*)out,
+        ldo, n, d, eps);
+}
+
+template <typename FT, typename OT>
+static void launch_row_ln_o(unsigned g, cudaStream_t st, void* F, int64_t ldf, const void* y,
+                            int64_t ldy, const float* ybias, const float* gain, const float* beta,
+                            const double* pec, const double* lo_ext, float pl2, void* out,
+                            int64_t ldo, int64_t n, int d, double eps) {
+    const int per = (d + 31) / 32;
+#define F3D_LN_CASE(P)                                                                          \
+    case P:                                                                                     \
+        launch_row_ln_p<FT, OT, P>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, \
+                                   out, ldo, n, d, eps);                                        \
+        break;
+    switch (per) {
+        F3D_LN_CASE(1) F3D_LN_CASE(2) F3D_LN_CASE(3) F3D_LN_CASE(4) F3D_LN_CASE(6)
+        F3D_LN_CASE(8) F3D_LN_CASE(12) F3D_LN_CASE(16)
+        default:
+            if (per <= 5) launch_row_ln_p<FT, OT, 6>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, out, ldo, n, d, eps);
+            else if (per <= 12) launch_row_ln_p<FT, OT, 12>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, out, ldo, n, d, eps);
+            else if (per <= 16) launch_row_ln_p<FT, OT, 16>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, out, ldo, n, d, eps);
+            else launch_row_ln_p<FT, OT, 32>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, out, ldo, n, d, eps);
+    }
+#undef F3D_LN_CASE
+}
+
 template <typename FT>
 static void launch_row_ln(unsigned g, cudaStream_t st, void* F, int64_t ldf, const void* y,
                           int64_t ldy, const float* ybias, const float* gain, const float* beta,
                           const double* pec, const double* lo_ext, float pl2, void* out,
                           int out_kind, int64_t ldo, int64_t n, int d, double eps) {
-    const __nv_bfloat16* yy = (const __nv_bfloat16*)y;
     if (out_kind == 2)
-        stage::row_ln_kernel<FT, double><<<g, stage::kThreads, 0, st>>>(
-            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pec, lo_ext, pl2, (double*)out, ldo, n, d, eps);
+        launch_row_ln_o<FT, double>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2,
+                                    out, ldo, n, d, eps);
     else if (out_kind == 1)
-        stage::row_ln_kernel<FT, float><<<g, stage::kThreads, 0, st>>>(
-            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pec, lo_ext, pl2, (float*)out, ldo, n, d, eps);
+        launch_row_ln_o<FT, float>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2,
+                                   out, ldo, n, d, eps);
     else
-        stage::row_ln_kernel<FT, __nv_bfloat16><<<g, stage::kThreads, 0, st>>>(
-            (FT*)F, ldf, yy, ldy, ybias, gain, beta, pec, lo_ext, pl2, (__nv_bfloat16*)out, ldo, n, d,
-            eps);
+        launch_row_ln_o<FT, __nv_bfloat16>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext,
+                                           pl2, out, ldo, n, d, eps);
 }
 
 extern "C" int f3d_row_ln(void* F, int f_is_f64, int64_t ldf, const void* y, int64_t ldy,
