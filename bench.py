@@ -236,6 +236,8 @@ def main():
     # ---- end to end through the public API with host buffers (e2e)
     out_rows = []
     out_h = None
+    for _ in range(args.warmup):          # pinned output buffer + side stream created here
+        out_h, _ = bb.forward_host(C_h, X_h, out_h)
     barrier()
     e2e_ms = []
     for _ in range(args.steps):
