@@ -140,6 +140,17 @@ int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_
                         const int32_t *scope_order, int nlive, int max_len, const int32_t *live,
                         const uint8_t *mask, int32_t *starved, void *stream);
 
+/* Same contract on the 5th-generation tensor cores (tcgen05.mma into TMEM,
+ * persistent warp-specialised CTAs: cp.async gather warps, one MMA-issuing
+ * thread, softmax warps reading S with tcgen05.ld).  Requires dh % 8 == 0,
+ * 16-byte aligned q/k/v and row strides that are multiples of 8; no mask. */
+int f3d_bswin_attention_tc(const void *q, const void *k, const void *v, int64_t ld_q,
+                           int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
+                           int dh, const int32_t *scope_seg, const int32_t *scope_nseg,
+                           const int32_t *seg_start, const int32_t *seg_vstart,
+                           const int32_t *scope_len, const int32_t *work, int nwork,
+                           const int32_t *live, void *stream);
+
 /* Device planner for one round (bw/attention.py:84-139 over the split table
  * of bw/bucketing.py:147-166, built from the PSH counts/base in HBM).
  * nscopes = ceil(nb / (W*stride)) * stride; segment arrays hold nscopes*W

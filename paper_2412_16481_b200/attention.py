@@ -11,6 +11,7 @@ streams.
 """
 
 import math
+import os
 import warnings
 from dataclasses import dataclass
 
@@ -293,10 +294,27 @@ def plan_schedule(table, schedule: ScopeSchedule, dev=None):
     return plans
 
 
+# "tc": tcgen05/TMEM kernel where eligible (default); "mma": mma.sync kernels
+ATTN_IMPL = os.environ.get("F3D_ATTN", "tc")
+
+
+def _tc_ok(q, k, v, dh, mask):
+    return (ATTN_IMPL == "tc" and mask is None and dh % 8 == 0 and 8 <= dh <= 128
+            and all(t.stride(0) % 8 == 0 and t.data_ptr() % 16 == 0 for t in (q, k, v)))
+
+
 def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, starved=None):
-    """Launch f3d_bswin_attention.  q/k/v: bf16 CUDA tensors whose rows hold
-    heads side by side (head h at columns h*dh..), any row stride; out: bf16
-    or fp32 rows with the same head layout."""
+    """Launch bucket-swin attention for one round.  q/k/v: bf16 CUDA tensors
+    whose rows hold heads side by side (head h at columns h*dh..), any row
+    stride; out: bf16 or fp32 rows with the same head layout.  Uses the
+    tcgen05 kernel when eligible, else the mma.sync kernels."""
+    if _tc_ok(q, k, v, dh, mask):
+        L.call("f3d_bswin_attention_tc", L.ptr(q), L.ptr(k), L.ptr(v), q.stride(0), k.stride(0),
+               v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads,
+               dh, L.ptr(plan.scope_seg), L.ptr(plan.scope_nseg), L.ptr(plan.seg_start),
+               L.ptr(plan.seg_vstart), L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork,
+               L.ptr(plan.live), L.stream())
+        return
     L.call("f3d_bswin_attention", L.ptr(q), L.ptr(k), L.ptr(v), q.stride(0), k.stride(0),
            v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads, dh,
            L.ptr(plan.scope_seg), L.ptr(plan.scope_nseg), L.ptr(plan.seg_start),

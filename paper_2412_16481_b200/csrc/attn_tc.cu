@@ -1,0 +1,444 @@
+// Bucket-swin attention on 5th-generation tensor cores (tcgen05 / TMEM).
+//
+// Same contract as csrc/attn.cu (bw/attention.py:188-268 per scope, one launch
+// per round), FlashAttention-style with the Blackwell execution model:
+//   * persistent CTAs (one per SM) walk the (query-tile, head) work list;
+//   * warps 0-3 gather Q / K / V rows of the scope straight from the fixed
+//     scattered layout with cp.async into UMMA core-matrix smem tiles (a
+//     scope is up to W physical segments, so rows are gathered, not boxed);
+//     completion is signalled on mbarriers (cp.async.mbarrier.arrive);
+//   * warp 8 (one elected thread) issues tcgen05.mma: S = Q K^T into TMEM
+//     (double-buffered), then O_j = P_j V_j into TMEM (double-buffered),
+//     tcgen05.commit -> mbarriers;
+//   * warps 4-7 (one thread per query row = TMEM lane) read S with
+//     tcgen05.ld, run the online softmax in the exp2 domain, write P (bf16)
+//     to smem for the PV MMA, and fold O_j into register accumulators.
+// Shared-memory tiles use the SWIZZLE_NONE canonical layout: element (r, c)
+// of an R x C bf16 tile lives at (r/8)*16*C + (c/8)*128 + (r%8)*16 + (c%8)*2.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cfloat>
+
+#include "f3d_common.cuh"
+#include "tc_common.cuh"
+
+namespace f3d {
+namespace attn_tc {
+
+using namespace f3d::tc;
+
+constexpr int kBM = 128;
+constexpr int kLoadWarps = 4;
+constexpr int kSoftWarps = 4;
+constexpr int kThreads = (kLoadWarps + kSoftWarps + 1) * 32;   // + 1 MMA warp
+constexpr int kNst = 3;                                          // K/V stages
+
+struct Args {
+    const __nv_bfloat16 *q, *k, *v;
+    int64_t ld_q, ld_k, ld_v;
+    void* o;
+    int64_t ld_o;
+    int out_f32;
+    int H, dh;
+    float scale_log2;
+    const int32_t *scope_seg, *scope_nseg, *seg_start, *seg_vstart, *scope_len, *work;
+    int nwork;
+    const int32_t* live;   // optional device [nwork, ...]
+};
+
+template <int DH, int BN>
+struct Cfg {
+    static constexpr int kQBytes = kBM * DH * 2;
+    static constexpr int kKVBytes = BN * DH * 2;     // one of K or V
+    static constexpr int kPBytes = kBM * BN * 2;
+    static constexpr int kOffQ = 0;
+    static constexpr int kOffKV = kOffQ + kQBytes;
+    static constexpr int kOffP = kOffKV + kNst * 2 * kKVBytes;
+    static constexpr int kOffBar = kOffP + 2 * kPBytes;
+    static constexpr int kNumBars = 2 + 2 * kNst + 8;
+    static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
+    static constexpr int kTmemS = 0;              // S buffers: [0, BN), [BN, 2BN)
+    static constexpr int kTmemPV = 2 * BN;        // PV buffers: [2BN, 2BN+DH), [.., 2BN+2DH)
+    static constexpr int kTmemCols = 512;
+    static_assert(2 * BN + 2 * DH <= 512, "TMEM budget");
+    static_assert(kSmem <= 227 * 1024, "smem budget");
+};
+
+__device__ __forceinline__ int phys_row(const Args& A, int s0, int s1, int vr) {
+    int seg = s0;
+    for (int s = s0 + 1; s < s1; ++s)
+        if (__ldg(A.seg_vstart + s) <= vr) seg = s;
+    return __ldg(A.seg_start + seg) + (vr - __ldg(A.seg_vstart + seg));
+}
+
+// byte offset of 16-byte chunk (row r, chunk c) in an R x C core-matrix tile
+template <int C>
+__device__ __forceinline__ uint32_t core_off(int r, int c) {
+    return (uint32_t)((r >> 3) * (16 * C) + c * 128 + (r & 7) * 16);
+}
+
+struct Item {
+    int scope, q0, h, m, s0, s1, nt;
+};
+
+template <int BN>
+__device__ __forceinline__ Item decode(const Args& A, int item) {
+    Item it;
+    const int wi = item / A.H;
+    it.h = item - wi * A.H;
+    it.scope = __ldg(A.work + 2 * wi);
+    it.q0 = __ldg(A.work + 2 * wi + 1);
+    it.s0 = __ldg(A.scope_seg + it.scope);
+    it.s1 = it.s0 + __ldg(A.scope_nseg + it.scope);
+    it.m = __ldg(A.scope_len + it.scope);
+    it.nt = (it.m + BN - 1) / BN;
+    return it;
+}
+
+// Gather rows [v0, v0+R) of head h (real chunks only; zero-fill past m).
+template <int DH, int R>
+__device__ __forceinline__ void gather(const Args& A, const __nv_bfloat16* base, int64_t ld,
+                                       const Item& it, int v0, uint32_t dst, int tid) {
+    const int rc = A.dh >> 3;   // real 16-byte chunks per row
+    const int hcol = it.h * A.dh;
+    for (int idx = tid; idx < R * rc; idx += kLoadWarps * 32) {
+        const int r = idx / rc;
+        const int c = idx - r * rc;
+        const int vr = v0 + r;
+        const bool ok = vr < it.m;
+        const __nv_bfloat16* src = base;
+        if (ok) src = base + (int64_t)phys_row(A, it.s0, it.s1, vr) * ld + hcol + c * 8;
+        cp_async16z(dst + core_off<DH>(r, c), src, ok);
+    }
+}
+
+template <int DH, int BN, typename OutT>
+__global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A) {
+    using C = Cfg<DH, BN>;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+    uint64_t* q_full = bars + 0;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* kv_full = bars + 2;
+    uint64_t* kv_empty = bars + 2 + kNst;
+    uint64_t* s_full = bars + 2 + 2 * kNst;      // [2]
+    uint64_t* p_full = s_full + 2;               // [2]
+    uint64_t* pv_full = s_full + 4;              // [2]
+    uint64_t* pv_empty = s_full + 6;             // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int total = (A.live ? __ldg(A.live) : A.nwork) * A.H;
+
+    // zero the operand tiles once: pad chunks (dh < DH) are never written again
+    for (int i = tid; i < C::kOffBar / 16; i += kThreads)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) {
+        mbar_init(q_full, kLoadWarps * 32);
+        mbar_init(q_empty, 1);
+        for (int s = 0; s < kNst; ++s) {
+            mbar_init(kv_full + s, kLoadWarps * 32);
+            mbar_init(kv_empty + s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(s_full + b, 1);
+            mbar_init(p_full + b, kSoftWarps * 32);
+            mbar_init(pv_full + b, 1);
+            mbar_init(pv_empty + b, kSoftWarps * 32);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(tmem_slot, C::kTmemCols);
+        tmem_relinquish();
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_base = saddr(smem);
+
+    if (warp < kLoadWarps) {
+        // ------------------------------------------------ loader warps
+        uint32_t q_use = 0, kv_it = 0;
+        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+            const Item it = decode<BN>(A, item);
+            mbar_wait(q_empty, (q_use & 1) ^ 1);
+            gather<DH, kBM>(A, A.q, A.ld_q, it, it.q0, sm_base + C::kOffQ, tid);
+            cp_async_arrive(q_full);
+            ++q_use;
+            for (int j = 0; j < it.nt; ++j, ++kv_it) {
+                const int s = kv_it % kNst;
+                const uint32_t u = kv_it / kNst;
+                mbar_wait(kv_empty + s, (u & 1) ^ 1);
+                const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
+                gather<DH, BN>(A, A.k, A.ld_k, it, j * BN, kb, tid);
+                gather<DH, BN>(A, A.v, A.ld_v, it, j * BN, kb + C::kKVBytes, tid);
+                cp_async_arrive(kv_full + s);
+            }
+        }
+    } else if (warp == kLoadWarps + kSoftWarps) {
+        // ------------------------------------------------ MMA warp
+        if (lane == 0) {
+            constexpr uint32_t idS = idesc_bf16(kBM, BN, 0, 0);
+            constexpr uint32_t idPV = idesc_bf16(kBM, DH, 0, 1);
+            uint32_t q_use = 0, kv_it = 0, t_it = 0;
+            for (int item = blockIdx.x; item < total; item += gridDim.x) {
+                const Item it = decode<BN>(A, item);
+                mbar_wait(q_full, q_use & 1);
+                fence_proxy_async();
+                tc_fence_after();
+                const uint32_t qa = sm_base + C::kOffQ;
+                auto issue_S = [&](int j) {
+                    const uint32_t kvi = kv_it + j;
+                    const int s = kvi % kNst;
+                    mbar_wait(kv_full + s, (kvi / kNst) & 1);
+                    fence_proxy_async();
+                    tc_fence_after();
+                    const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
+                    const int tb = (t_it + j) & 1;
+#pragma unroll
+                    for (int k = 0; k < DH / 16; ++k)
+                        umma_f16(tmem + C::kTmemS + tb * BN, smem_desc(qa + k * 256, 128, 16 * DH),
+                                 smem_desc(kb + k * 256, 128, 16 * DH), idS, k > 0);
+                    umma_commit(s_full + tb);
+                };
+                issue_S(0);
+                for (int j = 0; j < it.nt; ++j) {
+                    if (j + 1 < it.nt) issue_S(j + 1);
+                    const uint32_t tj = t_it + j;
+                    const int tb = tj & 1;
+                    mbar_wait(p_full + tb, (tj >> 1) & 1);          // P_j in smem, S_j consumed
+                    mbar_wait(pv_empty + tb, ((tj >> 1) & 1) ^ 1);  // PV buffer free
+                    fence_proxy_async();
+                    tc_fence_after();
+                    const uint32_t kvi = kv_it + j;
+                    const int s = kvi % kNst;
+                    const uint32_t vb = sm_base + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes;
+                    const uint32_t pb = sm_base + C::kOffP + tb * C::kPBytes;
+#pragma unroll
+                    for (int k = 0; k < BN / 16; ++k)
+                        umma_f16(tmem + C::kTmemPV + tb * DH, smem_desc(pb + k * 256, 128, 16 * BN),
+                                 smem_desc(vb + k * 32 * DH, 16 * DH, 128), idPV, k > 0);
+                    umma_commit(pv_full + tb);
+                    umma_commit(kv_empty + s);
+                }
+                umma_commit(q_empty);
+                ++q_use;
+                kv_it += it.nt;
+                t_it += it.nt;
+            }
+        }
+    } else {
+        // ------------------------------------------------ softmax warps
+        const int r = tid - kLoadWarps * 32;                       // query row = TMEM lane
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const float sl2 = A.scale_log2;
+        uint32_t t_it = 0;
+        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+            const Item it = decode<BN>(A, item);
+            float o[DH];
+#pragma unroll
+            for (int i = 0; i < DH; ++i) o[i] = 0.f;
+            float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
+            for (int j = 0; j < it.nt; ++j) {
+                const uint32_t tj = t_it + j;
+                const int tb = tj & 1;
+                mbar_wait(s_full + tb, (tj >> 1) & 1);
+                tc_fence_after();
+                const uint32_t sb = tmem + lane_base + C::kTmemS + tb * BN;
+                const int kvalid = it.m - j * BN;                  // keys < kvalid are real
+                // pass 1: row max
+                float mx = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t x[32];
+                    tmem_ld32(sb + c * 32, x);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float v = __uint_as_float(x[e]);
+                        if (c * 32 + e < kvalid) mx = fmaxf(mx, v);
+                    }
+                }
+                const float m_new = fmaxf(m_run, mx);
+                const float alpha = (m_run == -INFINITY) ? 0.f : ex2f((m_run - m_new) * sl2);
+                const float nms = -m_new * sl2;
+                // pass 2: P = exp2(s*sl2 - m*sl2) -> bf16 smem (core-matrix rows)
+                float sum = 0.f;
+                const uint32_t pb = sm_base + C::kOffP + tb * C::kPBytes;
+#pragma unroll
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t x[32];
+                    tmem_ld32(sb + c * 32, x);
+                    tmem_wait_ld();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        float p0 = ex2f(fmaf(__uint_as_float(x[e]), sl2, nms));
+                        float p1 = ex2f(fmaf(__uint_as_float(x[e + 1]), sl2, nms));
+                        if (c * 32 + e >= kvalid) p0 = 0.f;
+                        if (c * 32 + e + 1 >= kvalid) p1 = 0.f;
+                        sum += p0 + p1;
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                        pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t dst = pb + core_off<BN>(r, c * 4 + q);
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst),
+                                     "r"(pk[4 * q]), "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]),
+                                     "r"(pk[4 * q + 3])
+                                     : "memory");
+                    }
+                }
+                fence_proxy_async();
+                tc_fence_before();
+                mbar_arrive(p_full + tb);
+                l_run = l_run * alpha + sum;
+                m_run = m_new;
+                // fold the previous tile's P V into the register accumulator
+                if (j > 0) {
+                    const uint32_t tp = tj - 1;
+                    const int pbuf = tp & 1;
+                    mbar_wait(pv_full + pbuf, (tp >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t vb = tmem + lane_base + C::kTmemPV + pbuf * DH;
+#pragma unroll
+                    for (int c = 0; c < DH / 16; ++c) {
+                        uint32_t x[16];
+                        tmem_ld16(vb + c * 16, x);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(x[e]));
+                    }
+                    tc_fence_before();
+                    mbar_arrive(pv_empty + pbuf);
+                }
+                alpha_prev = alpha;
+            }
+            // last tile's P V, then normalise and write the row
+            {
+                const uint32_t tp = t_it + it.nt - 1;
+                const int pbuf = tp & 1;
+                mbar_wait(pv_full + pbuf, (tp >> 1) & 1);
+                tc_fence_after();
+                const uint32_t vb = tmem + lane_base + C::kTmemPV + pbuf * DH;
+#pragma unroll
+                for (int c = 0; c < DH / 16; ++c) {
+                    uint32_t x[16];
+                    tmem_ld16(vb + c * 16, x);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(x[e]));
+                }
+                tc_fence_before();
+                mbar_arrive(pv_empty + pbuf);
+            }
+            const int vr = it.q0 + r;
+            if (vr < it.m) {
+                const int pr = phys_row(A, it.s0, it.s1, vr);
+                const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+                const int hcol = it.h * A.dh;
+                if (sizeof(OutT) == 2) {
+                    __nv_bfloat16* out =
+                        reinterpret_cast<__nv_bfloat16*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+#pragma unroll
+                    for (int c = 0; c < DH; c += 2)
+                        if (c < A.dh)
+                            *reinterpret_cast<__nv_bfloat162*>(out + c) =
+                                __floats2bfloat162_rn(o[c] * inv, o[c + 1] * inv);
+                } else {
+                    float* out = reinterpret_cast<float*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+#pragma unroll
+                    for (int c = 0; c < DH; ++c)
+                        if (c < A.dh) out[c] = o[c] * inv;
+                }
+            }
+            t_it += it.nt;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
+}
+
+template <int DH, int BN, typename OutT>
+int launch(const Args& A, cudaStream_t st) {
+    using C = Cfg<DH, BN>;
+    auto kern = bswin_attn_tc_kernel<DH, BN, OutT>;
+    static bool attr = false;
+    if (!attr) {
+        F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          C::kSmem));
+        attr = true;
+    }
+    const int total = A.nwork * A.H;
+    const int grid = std::max(1, std::min(total, f3d_num_sms()));
+    kern<<<grid, kThreads, C::kSmem, st>>>(A);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+template <int DH>
+int launch_dh(const Args& A, cudaStream_t st) {
+    constexpr int BN = DH <= 64 ? 128 : 64;
+    return A.out_f32 ? launch<DH, BN, float>(A, st) : launch<DH, BN, __nv_bfloat16>(A, st);
+}
+
+}  // namespace attn_tc
+}  // namespace f3d
+
+using namespace f3d;
+
+extern "C" int f3d_bswin_attention_tc(const void* q, const void* k, const void* v, int64_t ld_q,
+                                      int64_t ld_k, int64_t ld_v, void* o, int64_t ld_o,
+                                      int out_f32, int H, int dh, const int32_t* scope_seg,
+                                      const int32_t* scope_nseg, const int32_t* seg_start,
+                                      const int32_t* seg_vstart, const int32_t* scope_len,
+                                      const int32_t* work, int nwork, const int32_t* live,
+                                      void* stream) {
+    if (H < 1 || dh < 8 || dh > 128 || (dh & 7) || nwork < 0) return F3D_ERR_CONFIG;
+    if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v) & 15) return F3D_ERR_CONFIG;
+    if ((ld_q | ld_k | ld_v) & 7) return F3D_ERR_CONFIG;
+    if (nwork == 0) return F3D_OK;
+    attn_tc::Args A;
+    A.q = (const __nv_bfloat16*)q;
+    A.k = (const __nv_bfloat16*)k;
+    A.v = (const __nv_bfloat16*)v;
+    A.ld_q = ld_q;
+    A.ld_k = ld_k;
+    A.ld_v = ld_v;
+    A.o = o;
+    A.ld_o = ld_o;
+    A.out_f32 = out_f32;
+    A.H = H;
+    A.dh = dh;
+    A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)dh));
+    A.scope_seg = scope_seg;
+    A.scope_nseg = scope_nseg;
+    A.seg_start = seg_start;
+    A.seg_vstart = seg_vstart;
+    A.scope_len = scope_len;
+    A.work = work;
+    A.nwork = nwork;
+    A.live = live;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch ((dh + 15) / 16 * 16) {
+        case 16: return attn_tc::launch_dh<16>(A, st);
+        case 32: return attn_tc::launch_dh<32>(A, st);
+        case 48: return attn_tc::launch_dh<48>(A, st);
+        case 64: return attn_tc::launch_dh<64>(A, st);
+        case 80: return attn_tc::launch_dh<80>(A, st);
+        case 96: return attn_tc::launch_dh<96>(A, st);
+        case 112: return attn_tc::launch_dh<112>(A, st);
+        case 128: return attn_tc::launch_dh<128>(A, st);
+        default: return F3D_ERR_CONFIG;
+    }
+}
