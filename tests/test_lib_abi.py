@@ -42,3 +42,9 @@ def test_config_errors_need_no_gpu():
     assert lib.f3d_scatter_rows(None, None, ctypes.c_int64(4), ctypes.c_int64(6), None, None) == 1
     lib.f3d_psh_workspace_size.restype = ctypes.c_size_t
     assert lib.f3d_psh_workspace_size(ctypes.c_int64(1000), 1, 40) > 0
+
+
+def test_launch_table_is_consistent():
+    from paper_2412_16481_b200 import _lib
+    assert set(_lib.KERNELS_PER_CALL) <= set(_lib.SIGNATURES)
+    assert all(isinstance(v, int) and v >= 0 for v in _lib.KERNELS_PER_CALL.values())
