@@ -259,7 +259,10 @@ def main():
     if rank == 0:
         hbm, tflops, src = peaks()
         steps = args.steps
-        attn_ms = probe_tot.get("f3d_bswin_attention", 0.0) / steps
+        attn_name = ("f3d_bswin_attention_tc" if "f3d_bswin_attention_tc" in probe_tot
+                     else "f3d_bswin_attention")
+        attn_ms = (probe_tot.get("f3d_bswin_attention", 0.0)
+                   + probe_tot.get("f3d_bswin_attention_tc", 0.0)) / steps
         attn_flops = sum(s.attention_flops for s in trace)
         attn_tf = attn_flops / (attn_ms * 1e-3) / 1e12 if attn_ms else 0.0
         psh_ms = (probe_tot.get("f3d_voxel_hash", 0.0) + probe_tot.get("f3d_psh_assign", 0.0)) / steps
@@ -292,7 +295,7 @@ def main():
                                    "C=96 H=4 W=2 -> pool rho=2 -> PSH K=128 -> stage)",
                        "points_per_gpu": N_POINTS, "parallelism": f"scene-sharded x{world}",
                        "l2": "flushed (256 MiB write) between timed steps"},
-            "roofline": {"kernel": "f3d_bswin_attention", "bound": "tensor",
+            "roofline": {"kernel": attn_name, "bound": "tensor",
                          "achieved": round(attn_tf, 2), "peak": tflops, "unit": "TFLOP/s",
                          "frac": round(attn_tf / tflops, 4), "traffic": None,
                          "peak_source": src,

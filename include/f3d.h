@@ -142,8 +142,10 @@ int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_
 
 /* Same contract on the 5th-generation tensor cores (tcgen05.mma into TMEM,
  * persistent warp-specialised CTAs: cp.async gather warps, one MMA-issuing
- * thread, softmax warps reading S with tcgen05.ld).  Requires dh % 8 == 0,
- * 16-byte aligned q/k/v and row strides that are multiples of 8; no mask. */
+ * thread, two softmax warpgroups reading S with tcgen05.ld).  The work list
+ * must step q_start by 256 (two 128-row Q tiles share each K/V tile).
+ * Requires dh % 8 == 0, 16-byte aligned q/k/v and row strides that are
+ * multiples of 8; no mask. */
 int f3d_bswin_attention_tc(const void *q, const void *k, const void *v, int64_t ld_q,
                            int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
                            int dh, const int32_t *scope_seg, const int32_t *scope_nseg,
@@ -155,11 +157,12 @@ int f3d_bswin_attention_tc(const void *q, const void *k, const void *v, int64_t 
  * of bw/bucketing.py:147-166, built from the PSH counts/base in HBM).
  * nscopes = ceil(nb / (W*stride)) * stride; segment arrays hold nscopes*W
  * entries (fixed stride W per scope); work holds max_work (scope, q_start)
- * pairs; live receives [nwork, nlive, max_len].  off = (t*shift) mod W. */
+ * pairs with q_start stepping by qstep (128: mma.sync kernels, 256: tcgen05
+ * kernel); live receives [nwork, nlive, max_len].  off = (t*shift) mod W. */
 int f3d_plan_round(const int32_t *counts, const int32_t *base, int K, int S, int nb, int W,
                    int stride, int off, int nscopes, int32_t *scope_seg, int32_t *scope_nseg,
                    int32_t *seg_start, int32_t *seg_vstart, int32_t *scope_len,
-                   int32_t *scope_order, int32_t *work, int max_work, int32_t *live,
+                   int32_t *scope_order, int32_t *work, int max_work, int qstep, int32_t *live,
                    void *stream);
 /* Device pooling tile table (bw/pooling.py:211-225): tiles of <= cap rows per
  * slot in scatter order; totals receives [ntiles, npooled]. */

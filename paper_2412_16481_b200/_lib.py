@@ -48,7 +48,7 @@ SIGNATURES = {
     "f3d_bswin_attention_tc": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _INT, _INT, _INT,
                                       _P, _P, _P, _P, _P, _P, _INT, _P, _P]),
     "f3d_plan_round": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P, _P, _P, _P,
-                              _P, _P, _INT, _P, _P]),
+                              _P, _P, _INT, _INT, _P, _P]),
     "f3d_plan_pool": (_INT, [_P, _P, _INT, _INT, _INT, _P, _P, _P, _P, _P]),
     "f3d_positional_encoding": (_INT, [_P, _I64, _INT, _F64, _INT, _P, _I64, _P]),
     "f3d_stage_pe": (_INT, [_P, _I64, _INT, _F64, _P, _INT, _P, _I64, _P]),

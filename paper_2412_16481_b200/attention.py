@@ -22,7 +22,8 @@ from . import _lib as L
 from .bucketing import BucketAssignment
 from .errors import ConfigError, NumericError
 
-BLOCK_M = 128  # query rows per work item (csrc/attn.cu kBM)
+BLOCK_M = 128  # query rows per work item of the mma.sync kernels (csrc/attn.cu kBM)
+QSTEP_TC = 256  # query rows per work item of the tcgen05 kernel (csrc/attn_tc.cu kQStep)
 BLOCK_N = 64   # keys per streamed tile (csrc/attn.cu kBN)
 
 
@@ -142,7 +143,7 @@ def logical_gather(assignment, scope):
 
 # --------------------------------------------------------------- kernel plan
 
-def plan_arrays(starts, lens, members):
+def plan_arrays(starts, lens, members, qstep=BLOCK_M):
     """Vectorised scope planning.  members: (n_scopes, W) bucket ids (-1 pad)
     over a (starts, lens) table.  Returns int32 host arrays: scope_seg
     (n_scopes+1), seg_start, seg_vstart, scope_len, work (nwork, 2) — adjacent
@@ -177,10 +178,10 @@ def plan_arrays(starts, lens, members):
     scope_seg = np.r_[0, np.cumsum(nseg)]
     order = np.argsort(-scope_len, kind="stable")
     live = order[scope_len[order] > 0]
-    nt = -(-scope_len[order] // BLOCK_M)
+    nt = -(-scope_len[order] // qstep)
     wscope = np.repeat(order, nt)
     wfirst = np.repeat(np.cumsum(nt) - nt, nt)
-    wq = (np.arange(len(wscope)) - wfirst) * BLOCK_M
+    wq = (np.arange(len(wscope)) - wfirst) * qstep
     work = np.stack([wscope, wq], 1) if len(wscope) else np.zeros((0, 2), np.int64)
     i32 = lambda x: np.ascontiguousarray(x, dtype=np.int32)
     return {"scope_seg": i32(scope_seg), "scope_nseg": i32(nseg), "seg_start": i32(seg_start),
@@ -216,8 +217,9 @@ def round_members(nb, W, stride, shift, t):
 class RoundPlan:
     """Device tables for one attention launch (see plan_arrays)."""
 
-    def __init__(self, arrays, dev=None, uploaded=None):
+    def __init__(self, arrays, dev=None, uploaded=None, qstep=BLOCK_M):
         self.host = arrays
+        self.qstep = qstep
         lens = arrays["scope_len"].astype(np.int64)
         self.nwork = int(arrays["work"].shape[0])
         self.nlive = int(arrays["scope_order"].shape[0])
@@ -234,7 +236,7 @@ class RoundPlan:
         self.scope_order = up["scope_order"]
 
     @classmethod
-    def from_ranges(cls, scope_ranges, dev=None):
+    def from_ranges(cls, scope_ranges, dev=None, qstep=BLOCK_M):
         """Plan from explicit [(start, stop), ...] lists (one per scope)."""
         starts, lens, members = [], [], []
         W = max((len(r) for r in scope_ranges), default=1)
@@ -246,7 +248,7 @@ class RoundPlan:
                 lens.append(max(0, b - a))
                 M[i, j] = k
                 k += 1
-        return cls(plan_arrays(np.array(starts + [0]), np.array(lens + [0]), M))
+        return cls(plan_arrays(np.array(starts + [0]), np.array(lens + [0]), M, qstep), qstep=qstep)
 
 
 class DeviceRoundPlan:
@@ -255,11 +257,12 @@ class DeviceRoundPlan:
     nlive are upper bounds for the launch grid; the kernels read the exact
     values from ``live``."""
 
-    def __init__(self, counts_dev, base_dev, K, S, nb, W, stride, shift, t, n):
+    def __init__(self, counts_dev, base_dev, K, S, nb, W, stride, shift, t, n, qstep=BLOCK_M):
         span = W * stride
         ns = -(-nb // span) * stride
+        self.qstep = qstep
         self.nlive = ns
-        self.nwork = n // BLOCK_M + ns
+        self.nwork = n // qstep + ns
         self.max_len = W * S
         i32 = torch.int32
         buf = L.empty((3 * ns + 2 * ns * W + ns + 2 * self.nwork + 4,), i32)
@@ -278,11 +281,11 @@ class DeviceRoundPlan:
         L.call("f3d_plan_round", L.ptr(counts_dev), L.ptr(base_dev), K, S, nb, W, stride,
                (t * shift) % W, ns, L.ptr(self.scope_seg), L.ptr(self.scope_nseg),
                L.ptr(self.seg_start), L.ptr(self.seg_vstart), L.ptr(self.scope_len),
-               L.ptr(self.scope_order), L.ptr(self.work), self.nwork, L.ptr(self.live),
+               L.ptr(self.scope_order), L.ptr(self.work), self.nwork, qstep, L.ptr(self.live),
                L.stream())
 
 
-def plan_schedule(table, schedule: ScopeSchedule, dev=None):
+def plan_schedule(table, schedule: ScopeSchedule, dev=None, qstep=BLOCK_M):
     """One RoundPlan per round of the schedule over a (starts, lengths) table."""
     starts, lengths = _table_np(table)
     plans = []
@@ -290,16 +293,23 @@ def plan_schedule(table, schedule: ScopeSchedule, dev=None):
         M = schedule_members(schedule, t)
         if ((M >= len(starts)) | (M < -1)).any():
             raise ConfigError("scope bucket id outside the bucket table")
-        plans.append(RoundPlan(plan_arrays(starts, lengths, M)))
+        plans.append(RoundPlan(plan_arrays(starts, lengths, M, qstep), qstep=qstep))
     return plans
+
+
+def qstep_for(dh, masked=False):
+    """Work-list stride matching the kernel attend() will pick."""
+    return QSTEP_TC if (ATTN_IMPL == "tc" and not masked and dh % 8 == 0 and 8 <= dh <= 128) \
+        else BLOCK_M
 
 
 # "tc": tcgen05/TMEM kernel where eligible (default); "mma": mma.sync kernels
 ATTN_IMPL = os.environ.get("F3D_ATTN", "tc")
 
 
-def _tc_ok(q, k, v, dh, mask):
-    return (ATTN_IMPL == "tc" and mask is None and dh % 8 == 0 and 8 <= dh <= 128
+def _tc_ok(q, k, v, dh, mask, plan):
+    return (getattr(plan, "qstep", BLOCK_M) == QSTEP_TC and mask is None and dh % 8 == 0
+            and 8 <= dh <= 128
             and all(t.stride(0) % 8 == 0 and t.data_ptr() % 16 == 0 for t in (q, k, v)))
 
 
@@ -308,13 +318,15 @@ def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, star
     whose rows hold heads side by side (head h at columns h*dh..), any row
     stride; out: bf16 or fp32 rows with the same head layout.  Uses the
     tcgen05 kernel when eligible, else the mma.sync kernels."""
-    if _tc_ok(q, k, v, dh, mask):
+    if _tc_ok(q, k, v, dh, mask, plan):
         L.call("f3d_bswin_attention_tc", L.ptr(q), L.ptr(k), L.ptr(v), q.stride(0), k.stride(0),
                v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads,
                dh, L.ptr(plan.scope_seg), L.ptr(plan.scope_nseg), L.ptr(plan.seg_start),
                L.ptr(plan.seg_vstart), L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork,
                L.ptr(plan.live), L.stream())
         return
+    if getattr(plan, "qstep", BLOCK_M) != BLOCK_M:
+        raise ConfigError("attention plan stride does not match the selected kernel")
     L.call("f3d_bswin_attention", L.ptr(q), L.ptr(k), L.ptr(v), q.stride(0), k.stride(0),
            v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads, dh,
            L.ptr(plan.scope_seg), L.ptr(plan.scope_nseg), L.ptr(plan.seg_start),
@@ -375,7 +387,7 @@ def tiled_attention(Q, K, V, params: AttentionParams, ranges=None, mask=None):
     out = torch.zeros((total, params.d_model), dtype=torch.float32, device=q.device)
     # overlapping / repeated ranges are legal in the reference: run each
     # distinct physical range list as one scope over a private row space
-    plan = RoundPlan.from_ranges([real])
+    plan = RoundPlan.from_ranges([real], qstep=qstep_for(params.head_dim, mk is not None))
     starved = torch.zeros(1, dtype=torch.int32, device=q.device) if mk is not None else None
     m = sum(b - a for a, b in real)
     # bytes the kernel streams: Q once, K and V once per query tile (bf16)
@@ -387,7 +399,8 @@ def tiled_attention(Q, K, V, params: AttentionParams, ranges=None, mask=None):
         qs, ks, vs = qb[rows].contiguous(), kb[rows].contiguous(), vb[rows].contiguous()
         o2 = torch.zeros((m, params.d_model), dtype=torch.float32, device=q.device)
         mk2 = mk[rows].contiguous() if mk is not None else None
-        attend(qs, ks, vs, o2, RoundPlan.from_ranges([[(0, m)]]), params.n_heads, dh, mask=mk2,
+        attend(qs, ks, vs, o2, RoundPlan.from_ranges([[(0, m)]], qstep=qstep_for(dh, mk2 is not None)),
+               params.n_heads, dh, mask=mk2,
                starved=starved)
         res = o2.to(torch.float64)
     if mk is not None and not bool(mk[rows].any()):
@@ -415,7 +428,8 @@ def reference_attention(Q, K, V, params: AttentionParams):
     if mk != m:
         raise ConfigError("reference_attention on the GPU needs as many keys as queries")
     out = torch.zeros((m, params.d_model), dtype=torch.float32, device=q.device)
-    attend(qb, kb, vb, out, RoundPlan.from_ranges([[(0, m)]]), params.n_heads, params.head_dim)
+    attend(qb, kb, vb, out, RoundPlan.from_ranges([[(0, m)]], qstep=qstep_for(params.head_dim)),
+           params.n_heads, params.head_dim)
     return L.out(out.to(torch.float64), host)
 
 

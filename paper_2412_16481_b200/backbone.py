@@ -16,7 +16,7 @@ import torch
 from torch.profiler import record_function
 
 from . import _lib as L
-from .attention import DeviceRoundPlan, RoundPlan, plan_arrays, round_members
+from .attention import DeviceRoundPlan, RoundPlan, plan_arrays, qstep_for, round_members
 from .bucketing import BucketAssignment, _run_psh, default_probe_schedule
 from .errors import ConfigError, RangeError
 from .hashing import HashConfig, raise_range
@@ -156,8 +156,9 @@ class Backbone:
                 if cfg.W > nb:
                     raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb})")
                 cd, bd = a._dev["counts"], a._dev["base"]
+                qs = qstep_for(cfg.d_model // cfg.n_heads)
                 plans = [DeviceRoundPlan(cd, bd, cfg.K, cfg.S, nb, cfg.W, cfg.stride, cfg.shift,
-                                         t, n) for t in range(cfg.rounds)]
+                                         t, n, qstep=qs) for t in range(cfg.rounds)]
                 runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
                                      weights=self._w[si], plans=plans)
             with record_function(f"stage{si}.run"):

@@ -2,17 +2,18 @@
 //
 // Same contract as csrc/attn.cu (bw/attention.py:188-268 per scope, one launch
 // per round), FlashAttention-style with the Blackwell execution model:
-//   * persistent CTAs (one per SM) walk the (query-tile, head) work list;
-//   * warps 0-3 gather Q / K / V rows of the scope straight from the fixed
+//   * persistent CTAs (one per SM) walk the (256-row query group, head) work
+//     list; the group's two 128-row Q tiles share every K/V tile;
+//   * warps 0-2 gather Q / K / V rows of the scope straight from the fixed
 //     scattered layout with cp.async into UMMA core-matrix smem tiles (a
 //     scope is up to W physical segments, so rows are gathered, not boxed);
 //     completion is signalled on mbarriers (cp.async.mbarrier.arrive);
-//   * warp 8 (one elected thread) issues tcgen05.mma: S = Q K^T into TMEM
-//     (double-buffered), then O_j = P_j V_j into TMEM (double-buffered),
-//     tcgen05.commit -> mbarriers;
-//   * warps 4-7 (one thread per query row = TMEM lane) read S with
+//   * warp 3 (one elected thread) issues tcgen05.mma: S_g = Q_g K^T and
+//     O_g = P_g V into TMEM per Q tile g, tcgen05.commit -> mbarriers;
+//   * two softmax warpgroups (one thread per query row = TMEM lane) read S with
 //     tcgen05.ld, run the online softmax in the exp2 domain, write P (bf16)
 //     to smem for the PV MMA, and fold O_j into register accumulators.
+// While one warpgroup works on its S, the MMA warp computes the other's.
 // Shared-memory tiles use the SWIZZLE_NONE canonical layout: element (r, c)
 // of an R x C bf16 tile lives at (r/8)*16*C + (c/8)*128 + (r%8)*16 + (c%8)*2.
 #include <cuda_bf16.h>
@@ -28,11 +29,14 @@ namespace attn_tc {
 
 using namespace f3d::tc;
 
-constexpr int kBM = 128;
-constexpr int kLoadWarps = 4;
-constexpr int kSoftWarps = 4;
-constexpr int kThreads = (kLoadWarps + kSoftWarps + 1) * 32;   // + 1 MMA warp
+constexpr int kBM = 128;                                         // rows per Q tile
+constexpr int kNQ = 2;                                           // Q tiles per work item
+constexpr int kLoadWarps = 3;                                    // warps 0-2
+constexpr int kMmaWarp = 3;                                      // completes warpgroup 0
+constexpr int kSoftWarps = 4 * kNQ;                              // warps 4.. : one warpgroup per Q tile
+constexpr int kThreads = (kLoadWarps + 1 + kSoftWarps) * 32;
 constexpr int kNst = 3;                                          // K/V stages
+constexpr int kQStep = kBM * kNQ;                                // work-list q stride
 
 struct Args {
     const __nv_bfloat16 *q, *k, *v;
@@ -49,19 +53,19 @@ struct Args {
 
 template <int DH, int BN>
 struct Cfg {
-    static constexpr int kQBytes = kBM * DH * 2;
-    static constexpr int kKVBytes = BN * DH * 2;     // one of K or V
-    static constexpr int kPBytes = kBM * BN * 2;
+    static constexpr int kQBytes = kBM * DH * 2;        // one Q tile
+    static constexpr int kKVBytes = BN * DH * 2;        // one of K or V
+    static constexpr int kPBytes = kBM * BN * 2;        // one P tile
     static constexpr int kOffQ = 0;
-    static constexpr int kOffKV = kOffQ + kQBytes;
+    static constexpr int kOffKV = kOffQ + kNQ * kQBytes;
     static constexpr int kOffP = kOffKV + kNst * 2 * kKVBytes;
-    static constexpr int kOffBar = kOffP + 2 * kPBytes;
-    static constexpr int kNumBars = 2 + 2 * kNst + 8;
+    static constexpr int kOffBar = kOffP + kNQ * kPBytes;
+    static constexpr int kNumBars = 2 + 2 * kNst + 4 * kNQ;
     static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
-    static constexpr int kTmemS = 0;              // S buffers: [0, BN), [BN, 2BN)
-    static constexpr int kTmemPV = 2 * BN;        // PV buffers: [2BN, 2BN+DH), [.., 2BN+2DH)
+    static constexpr int kTmemS = 0;                    // S of tile g: [g*BN, (g+1)*BN)
+    static constexpr int kTmemPV = kNQ * BN;            // PV of tile g: [kTmemPV + g*DH, ...)
     static constexpr int kTmemCols = 512;
-    static_assert(2 * BN + 2 * DH <= 512, "TMEM budget");
+    static_assert(kNQ * (BN + DH) <= 512, "TMEM budget");
     static_assert(kSmem <= 227 * 1024, "smem budget");
 };
 
@@ -122,10 +126,10 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
     uint64_t* q_empty = bars + 1;
     uint64_t* kv_full = bars + 2;
     uint64_t* kv_empty = bars + 2 + kNst;
-    uint64_t* s_full = bars + 2 + 2 * kNst;      // [2]
-    uint64_t* p_full = s_full + 2;               // [2]
-    uint64_t* pv_full = s_full + 4;              // [2]
-    uint64_t* pv_empty = s_full + 6;             // [2]
+    uint64_t* s_full = bars + 2 + 2 * kNst;      // [kNQ]  MMA -> softmax
+    uint64_t* p_full = s_full + kNQ;             // [kNQ]  softmax -> MMA (S read, P written)
+    uint64_t* pv_full = s_full + 2 * kNQ;        // [kNQ]  MMA -> softmax
+    uint64_t* pv_empty = s_full + 3 * kNQ;       // [kNQ]  softmax -> MMA (PV folded)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
     const int tid = threadIdx.x;
@@ -143,11 +147,11 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
             mbar_init(kv_full + s, kLoadWarps * 32);
             mbar_init(kv_empty + s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(s_full + b, 1);
-            mbar_init(p_full + b, kSoftWarps * 32);
-            mbar_init(pv_full + b, 1);
-            mbar_init(pv_empty + b, kSoftWarps * 32);
+        for (int g = 0; g < kNQ; ++g) {
+            mbar_init(s_full + g, 1);
+            mbar_init(p_full + g, 128);
+            mbar_init(pv_full + g, 1);
+            mbar_init(pv_empty + g, 128);
         }
         fence_mbar_init();
     }
@@ -168,7 +172,10 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
             const Item it = decode<BN>(A, item);
             mbar_wait(q_empty, (q_use & 1) ^ 1);
-            gather<DH, kBM>(A, A.q, A.ld_q, it, it.q0, sm_base + C::kOffQ, tid);
+#pragma unroll
+            for (int g = 0; g < kNQ; ++g)
+                gather<DH, kBM>(A, A.q, A.ld_q, it, it.q0 + g * kBM,
+                                sm_base + C::kOffQ + g * C::kQBytes, tid);
             cp_async_arrive(q_full);
             ++q_use;
             for (int j = 0; j < it.nt; ++j, ++kv_it) {
@@ -181,8 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
                 cp_async_arrive(kv_full + s);
             }
         }
-    } else if (warp == kLoadWarps + kSoftWarps) {
-        // ------------------------------------------------ MMA warp
+    } else if (warp == kMmaWarp) {
+        // ------------------------------------------------ MMA warp (one thread)
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(kBM, BN, 0, 0);
             constexpr uint32_t idPV = idesc_bf16(kBM, DH, 0, 1);
@@ -190,41 +197,48 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
             for (int item = blockIdx.x; item < total; item += gridDim.x) {
                 const Item it = decode<BN>(A, item);
                 mbar_wait(q_full, q_use & 1);
-                fence_proxy_async();
-                tc_fence_after();
-                const uint32_t qa = sm_base + C::kOffQ;
-                auto issue_S = [&](int j) {
-                    const uint32_t kvi = kv_it + j;
-                    const int s = kvi % kNst;
-                    mbar_wait(kv_full + s, (kvi / kNst) & 1);
-                    fence_proxy_async();
-                    tc_fence_after();
+                auto issue_S = [&](int g, int j) {
+                    const int s = (kv_it + j) % kNst;
                     const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
-                    const int tb = (t_it + j) & 1;
+                    const uint32_t qa = sm_base + C::kOffQ + g * C::kQBytes;
 #pragma unroll
                     for (int k = 0; k < DH / 16; ++k)
-                        umma_f16(tmem + C::kTmemS + tb * BN, smem_desc(qa + k * 256, 128, 16 * DH),
+                        umma_f16(tmem + C::kTmemS + g * BN, smem_desc(qa + k * 256, 128, 16 * DH),
                                  smem_desc(kb + k * 256, 128, 16 * DH), idS, k > 0);
-                    umma_commit(s_full + tb);
+                    umma_commit(s_full + g);
                 };
-                issue_S(0);
-                for (int j = 0; j < it.nt; ++j) {
-                    if (j + 1 < it.nt) issue_S(j + 1);
-                    const uint32_t tj = t_it + j;
-                    const int tb = tj & 1;
-                    mbar_wait(p_full + tb, (tj >> 1) & 1);          // P_j in smem, S_j consumed
-                    mbar_wait(pv_empty + tb, ((tj >> 1) & 1) ^ 1);  // PV buffer free
+                auto wait_kv = [&](int j) {
+                    const uint32_t kvi = kv_it + j;
+                    mbar_wait(kv_full + kvi % kNst, (kvi / kNst) & 1);
                     fence_proxy_async();
                     tc_fence_after();
-                    const uint32_t kvi = kv_it + j;
-                    const int s = kvi % kNst;
-                    const uint32_t vb = sm_base + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes;
-                    const uint32_t pb = sm_base + C::kOffP + tb * C::kPBytes;
+                };
+                wait_kv(0);
 #pragma unroll
-                    for (int k = 0; k < BN / 16; ++k)
-                        umma_f16(tmem + C::kTmemPV + tb * DH, smem_desc(pb + k * 256, 128, 16 * BN),
-                                 smem_desc(vb + k * 32 * DH, 16 * DH, 128), idPV, k > 0);
-                    umma_commit(pv_full + tb);
+                for (int g = 0; g < kNQ; ++g) {
+                    // S_g buffer free once softmax g consumed the previous tile
+                    if (t_it > 0) mbar_wait(p_full + g, (t_it - 1) & 1);
+                    issue_S(g, 0);
+                }
+                for (int j = 0; j < it.nt; ++j) {
+                    const uint32_t tj = t_it + j;
+                    const int s = (kv_it + j) % kNst;
+                    const uint32_t vb = sm_base + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes;
+                    if (j + 1 < it.nt) wait_kv(j + 1);
+#pragma unroll
+                    for (int g = 0; g < kNQ; ++g) {
+                        mbar_wait(p_full + g, tj & 1);             // P_g,j in smem; S_g free
+                        mbar_wait(pv_empty + g, (tj & 1) ^ 1);     // PV_g folded by softmax
+                        fence_proxy_async();
+                        tc_fence_after();
+                        const uint32_t pb = sm_base + C::kOffP + g * C::kPBytes;
+#pragma unroll
+                        for (int k = 0; k < BN / 16; ++k)
+                            umma_f16(tmem + C::kTmemPV + g * DH, smem_desc(pb + k * 256, 128, 16 * BN),
+                                     smem_desc(vb + k * 32 * DH, 16 * DH, 128), idPV, k > 0);
+                        umma_commit(pv_full + g);
+                        if (j + 1 < it.nt) issue_S(g, j + 1);
+                    }
                     umma_commit(kv_empty + s);
                 }
                 umma_commit(q_empty);
@@ -234,10 +248,15 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
             }
         }
     } else {
-        // ------------------------------------------------ softmax warps
-        const int r = tid - kLoadWarps * 32;                       // query row = TMEM lane
+        // ------------------------------------------------ softmax warpgroups
+        const int sw = warp - (kMmaWarp + 1);             // 0 .. kSoftWarps-1
+        const int g = sw >> 2;                            // Q tile of this warpgroup
+        const int r = (sw & 3) * 32 + lane;               // row in the tile = TMEM lane
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
         const float sl2 = A.scale_log2;
+        const uint32_t sbase = tmem + lane_base + C::kTmemS + g * BN;
+        const uint32_t vbase = tmem + lane_base + C::kTmemPV + g * DH;
+        const uint32_t pb = sm_base + C::kOffP + g * C::kPBytes;
         uint32_t t_it = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
             const Item it = decode<BN>(A, item);
@@ -247,42 +266,61 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
             float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
             for (int j = 0; j < it.nt; ++j) {
                 const uint32_t tj = t_it + j;
-                const int tb = tj & 1;
-                mbar_wait(s_full + tb, (tj >> 1) & 1);
+                mbar_wait(s_full + g, tj & 1);
                 tc_fence_after();
-                const uint32_t sb = tmem + lane_base + C::kTmemS + tb * BN;
-                const int kvalid = it.m - j * BN;                  // keys < kvalid are real
+                const int kvalid = it.m - j * BN;         // keys < kvalid are real
+                const bool full = kvalid >= BN;
                 // pass 1: row max
                 float mx = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t x[32];
-                    tmem_ld32(sb + c * 32, x);
+                    tmem_ld32(sbase + c * 32, x);
                     tmem_wait_ld();
+                    if (full) {
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const float v = __uint_as_float(x[e]);
-                        if (c * 32 + e < kvalid) mx = fmaxf(mx, v);
+                        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(x[e]));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (c * 32 + e < kvalid) mx = fmaxf(mx, __uint_as_float(x[e]));
                     }
                 }
                 const float m_new = fmaxf(m_run, mx);
                 const float alpha = (m_run == -INFINITY) ? 0.f : ex2f((m_run - m_new) * sl2);
                 const float nms = -m_new * sl2;
+                // fold the previous tile's P V before P is overwritten
+                if (j > 0) {
+                    mbar_wait(pv_full + g, (tj - 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c = 0; c < DH / 16; ++c) {
+                        uint32_t x[16];
+                        tmem_ld16(vbase + c * 16, x);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(x[e]));
+                    }
+                    tc_fence_before();
+                    mbar_arrive(pv_empty + g);
+                }
                 // pass 2: P = exp2(s*sl2 - m*sl2) -> bf16 smem (core-matrix rows)
                 float sum = 0.f;
-                const uint32_t pb = sm_base + C::kOffP + tb * C::kPBytes;
 #pragma unroll
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t x[32];
-                    tmem_ld32(sb + c * 32, x);
+                    tmem_ld32(sbase + c * 32, x);
                     tmem_wait_ld();
                     uint32_t pk[16];
 #pragma unroll
                     for (int e = 0; e < 32; e += 2) {
                         float p0 = ex2f(fmaf(__uint_as_float(x[e]), sl2, nms));
                         float p1 = ex2f(fmaf(__uint_as_float(x[e + 1]), sl2, nms));
-                        if (c * 32 + e >= kvalid) p0 = 0.f;
-                        if (c * 32 + e + 1 >= kvalid) p1 = 0.f;
+                        if (!full) {
+                            if (c * 32 + e >= kvalid) p0 = 0.f;
+                            if (c * 32 + e + 1 >= kvalid) p1 = 0.f;
+                        }
                         sum += p0 + p1;
                         __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                         pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
@@ -298,50 +336,29 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
                 }
                 fence_proxy_async();
                 tc_fence_before();
-                mbar_arrive(p_full + tb);
+                mbar_arrive(p_full + g);
                 l_run = l_run * alpha + sum;
                 m_run = m_new;
-                // fold the previous tile's P V into the register accumulator
-                if (j > 0) {
-                    const uint32_t tp = tj - 1;
-                    const int pbuf = tp & 1;
-                    mbar_wait(pv_full + pbuf, (tp >> 1) & 1);
-                    tc_fence_after();
-                    const uint32_t vb = tmem + lane_base + C::kTmemPV + pbuf * DH;
-#pragma unroll
-                    for (int c = 0; c < DH / 16; ++c) {
-                        uint32_t x[16];
-                        tmem_ld16(vb + c * 16, x);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 16; ++e)
-                            o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(x[e]));
-                    }
-                    tc_fence_before();
-                    mbar_arrive(pv_empty + pbuf);
-                }
                 alpha_prev = alpha;
             }
             // last tile's P V, then normalise and write the row
             {
-                const uint32_t tp = t_it + it.nt - 1;
-                const int pbuf = tp & 1;
-                mbar_wait(pv_full + pbuf, (tp >> 1) & 1);
+                const uint32_t tl = t_it + it.nt - 1;
+                mbar_wait(pv_full + g, tl & 1);
                 tc_fence_after();
-                const uint32_t vb = tmem + lane_base + C::kTmemPV + pbuf * DH;
 #pragma unroll
                 for (int c = 0; c < DH / 16; ++c) {
                     uint32_t x[16];
-                    tmem_ld16(vb + c * 16, x);
+                    tmem_ld16(vbase + c * 16, x);
                     tmem_wait_ld();
 #pragma unroll
                     for (int e = 0; e < 16; ++e)
                         o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(x[e]));
                 }
                 tc_fence_before();
-                mbar_arrive(pv_empty + pbuf);
+                mbar_arrive(pv_empty + g);
             }
-            const int vr = it.q0 + r;
+            const int vr = it.q0 + g * kBM + r;
             if (vr < it.m) {
                 const int pr = phys_row(A, it.s0, it.s1, vr);
                 const float inv = l_run > 0.f ? 1.f / l_run : 0.f;

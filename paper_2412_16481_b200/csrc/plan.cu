@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kThreads) plan_round_kernel(
     const int32_t* __restrict__ counts, const int32_t* __restrict__ base, int K, int S, int nb,
     int W, int stride, int off, int nscopes, int32_t* scope_seg, int32_t* scope_nseg,
     int32_t* seg_start, int32_t* seg_vstart, int32_t* scope_len, int32_t* scope_order,
-    int32_t* work, int max_work, int32_t* live) {
+    int32_t* work, int max_work, int qstep, int32_t* live) {
     __shared__ int sh[40];
     __shared__ int s_maxlen;
     const int span = W * stride;
@@ -87,14 +87,14 @@ __global__ void __launch_bounds__(kThreads) plan_round_kernel(
         }
         int tot_live, tot_work;
         const int is_live = v > 0 ? 1 : 0;
-        const int nt = (v + 127) / 128;
+        const int nt = (v + qstep - 1) / qstep;
         const int pl = block_excl_scan(is_live, tot_live, sh) + carry_live;
         const int pw = block_excl_scan(nt, tot_work, sh) + carry_work;
         if (is_live) scope_order[pl] = s;
         for (int q = 0; q < nt; ++q)
             if (pw + q < max_work) {
                 work[2 * (pw + q)] = s;
-                work[2 * (pw + q) + 1] = q * 128;
+                work[2 * (pw + q) + 1] = q * qstep;
             }
         carry_live += tot_live;
         carry_work += tot_work;
@@ -151,13 +151,13 @@ extern "C" int f3d_plan_round(const int32_t* counts, const int32_t* base, int K,
                               int W, int stride, int off, int nscopes, int32_t* scope_seg,
                               int32_t* scope_nseg, int32_t* seg_start, int32_t* seg_vstart,
                               int32_t* scope_len, int32_t* scope_order, int32_t* work,
-                              int max_work, int32_t* live, void* stream) {
+                              int max_work, int qstep, int32_t* live, void* stream) {
     if (K < 1 || S < 1 || nb < 1 || W < 1 || stride < 1 || off < 0 || nscopes < 1 ||
-        max_work < 0)
+        max_work < 0 || qstep < 16)
         return F3D_ERR_CONFIG;
     plan::plan_round_kernel<<<1, plan::kThreads, 0, (cudaStream_t)stream>>>(
         counts, base, K, S, nb, W, stride, off, nscopes, scope_seg, scope_nseg, seg_start,
-        seg_vstart, scope_len, scope_order, work, max_work, live);
+        seg_vstart, scope_len, scope_order, work, max_work, qstep, live);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

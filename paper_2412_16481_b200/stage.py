@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .attention import AttentionParams, ScopeSchedule, attend, plan_schedule
+from .attention import AttentionParams, ScopeSchedule, attend, plan_schedule, qstep_for
 from .bucketing import BucketAssignment
 from .errors import ConfigError
 
@@ -139,7 +139,8 @@ class StageRunner:
         self.H = params.attention.n_heads
         self.dh = params.attention.head_dim
         self.w = weights if weights is not None else params.device_weights()
-        self.plans = plans if plans is not None else plan_schedule(table, schedule, dev)
+        self.plans = plans if plans is not None else plan_schedule(
+            table, schedule, dev, qstep=qstep_for(params.attention.head_dim))
         self.f_dtype = f_dtype
         self.coords = L.to_dev(coords, torch.float64).contiguous()
         ws = L.empty((6 * 296,), torch.float64)
