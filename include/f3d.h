@@ -142,8 +142,9 @@ int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_
 
 /* Same contract on the 5th-generation tensor cores (tcgen05.mma into TMEM,
  * persistent warp-specialised CTAs: cp.async gather warps, one MMA-issuing
- * thread, two softmax warpgroups reading S with tcgen05.ld).  The work list
- * must step q_start by 256 (two 128-row Q tiles share each K/V tile).
+ * thread, softmax warpgroups reading S with tcgen05.ld).  The work list
+ * must step q_start by f3d_attention_tc_qstep(dh) (NQ 128-row Q tiles share
+ * each K/V tile; NQ = 3 / 2 / 1 for head dims <= 32 / 64 / 128).
  * Requires dh % 8 == 0, 16-byte aligned q/k/v and row strides that are
  * multiples of 8; no mask. */
 int f3d_bswin_attention_tc(const void *q, const void *k, const void *v, int64_t ld_q,
@@ -152,6 +153,8 @@ int f3d_bswin_attention_tc(const void *q, const void *k, const void *v, int64_t 
                            const int32_t *seg_start, const int32_t *seg_vstart,
                            const int32_t *scope_len, const int32_t *work, int nwork,
                            const int32_t *live, void *stream);
+
+int f3d_attention_tc_qstep(int dh);
 
 /* Device planner for one round (bw/attention.py:84-139 over the split table
  * of bw/bucketing.py:147-166, built from the PSH counts/base in HBM).

@@ -23,7 +23,9 @@ from .bucketing import BucketAssignment
 from .errors import ConfigError, NumericError
 
 BLOCK_M = 128  # query rows per work item of the mma.sync kernels (csrc/attn.cu kBM)
-QSTEP_TC = 256  # query rows per work item of the tcgen05 kernel (csrc/attn_tc.cu kQStep)
+def qstep_tc(dh):
+    """Query rows per work item of the tcgen05 kernel (csrc/attn_tc.cu)."""
+    return L.load().f3d_attention_tc_qstep(dh)
 BLOCK_N = 64   # keys per streamed tile (csrc/attn.cu kBN)
 
 
@@ -299,7 +301,7 @@ def plan_schedule(table, schedule: ScopeSchedule, dev=None, qstep=BLOCK_M):
 
 def qstep_for(dh, masked=False):
     """Work-list stride matching the kernel attend() will pick."""
-    return QSTEP_TC if (ATTN_IMPL == "tc" and not masked and dh % 8 == 0 and 8 <= dh <= 128) \
+    return qstep_tc(dh) if (ATTN_IMPL == "tc" and not masked and dh % 8 == 0 and 8 <= dh <= 128) \
         else BLOCK_M
 
 
@@ -308,8 +310,8 @@ ATTN_IMPL = os.environ.get("F3D_ATTN", "tc")
 
 
 def _tc_ok(q, k, v, dh, mask, plan):
-    return (getattr(plan, "qstep", BLOCK_M) == QSTEP_TC and mask is None and dh % 8 == 0
-            and 8 <= dh <= 128
+    return (mask is None and dh % 8 == 0 and 8 <= dh <= 128
+            and getattr(plan, "qstep", BLOCK_M) == qstep_tc(dh)
             and all(t.stride(0) % 8 == 0 and t.data_ptr() % 16 == 0 for t in (q, k, v)))
 
 

@@ -2,18 +2,19 @@
 //
 // Same contract as csrc/attn.cu (bw/attention.py:188-268 per scope, one launch
 // per round), FlashAttention-style with the Blackwell execution model:
-//   * persistent CTAs (one per SM) walk the (256-row query group, head) work
-//     list; the group's two 128-row Q tiles share every K/V tile;
+//   * persistent CTAs (one per SM) walk the (query group, head) work list; a
+//     group is NQ 128-row Q tiles (NQ = 3/2/1 for dh <= 32/64/128) that
+//     share every 64-key K/V tile;
 //   * warps 0-2 gather Q / K / V rows of the scope straight from the fixed
 //     scattered layout with cp.async into UMMA core-matrix smem tiles (a
 //     scope is up to W physical segments, so rows are gathered, not boxed);
 //     completion is signalled on mbarriers (cp.async.mbarrier.arrive);
 //   * warp 3 (one elected thread) issues tcgen05.mma: S_g = Q_g K^T and
 //     O_g = P_g V into TMEM per Q tile g, tcgen05.commit -> mbarriers;
-//   * two softmax warpgroups (one thread per query row = TMEM lane) read S with
-//     tcgen05.ld, run the online softmax in the exp2 domain, write P (bf16)
-//     to smem for the PV MMA, and fold O_j into register accumulators.
-// While one warpgroup works on its S, the MMA warp computes the other's.
+//   * NQ softmax warpgroups (one thread per query row = TMEM lane) copy their
+//     S row out of TMEM (freeing it for the next tile's MMA at once), run the
+//     online softmax in the exp2 domain, write P (bf16) to smem for the PV
+//     MMA, and fold O_j into register accumulators.
 // Shared-memory tiles use the SWIZZLE_NONE canonical layout: element (r, c)
 // of an R x C bf16 tile lives at (r/8)*16*C + (c/8)*128 + (r%8)*16 + (c%8)*2.
 #include <cuda_bf16.h>
@@ -29,14 +30,22 @@ namespace attn_tc {
 
 using namespace f3d::tc;
 
-constexpr int kBM = 128;                                         // rows per Q tile
-constexpr int kNQ = 2;                                           // Q tiles per work item
-constexpr int kLoadWarps = 3;                                    // warps 0-2
-constexpr int kMmaWarp = 3;                                      // completes warpgroup 0
-constexpr int kSoftWarps = 4 * kNQ;                              // warps 4.. : one warpgroup per Q tile
-constexpr int kThreads = (kLoadWarps + 1 + kSoftWarps) * 32;
-constexpr int kNst = 3;                                          // K/V stages
-constexpr int kQStep = kBM * kNQ;                                // work-list q stride
+constexpr int kBM = 128;          // rows per Q tile (TMEM lanes)
+constexpr int kBN = 64;           // keys per K/V tile
+constexpr int kLoadWarps = 3;     // warps 0-2
+constexpr int kMmaWarp = 3;       // completes warpgroup 0
+constexpr int kNst = 3;           // K/V stages
+
+// Q tiles per work item (one softmax warpgroup each): as many as registers
+// allow (the softmax thread keeps its 64-key S row and DH-wide O row live).
+template <int DH>
+__host__ __device__ constexpr int nq_for() {
+    return DH <= 32 ? 3 : (DH <= 64 ? 2 : 1);
+}
+template <int DH>
+__host__ __device__ constexpr int threads_for() {
+    return (4 + 4 * nq_for<DH>()) * 32;
+}
 
 struct Args {
     const __nv_bfloat16 *q, *k, *v;
@@ -51,21 +60,22 @@ struct Args {
     const int32_t* live;   // optional device [nwork, ...]
 };
 
-template <int DH, int BN>
+template <int DH>
 struct Cfg {
+    static constexpr int NQ = nq_for<DH>();
     static constexpr int kQBytes = kBM * DH * 2;        // one Q tile
-    static constexpr int kKVBytes = BN * DH * 2;        // one of K or V
-    static constexpr int kPBytes = kBM * BN * 2;        // one P tile
+    static constexpr int kKVBytes = kBN * DH * 2;       // one of K or V
+    static constexpr int kPBytes = kBM * kBN * 2;       // one P tile
     static constexpr int kOffQ = 0;
-    static constexpr int kOffKV = kOffQ + kNQ * kQBytes;
+    static constexpr int kOffKV = kOffQ + NQ * kQBytes;
     static constexpr int kOffP = kOffKV + kNst * 2 * kKVBytes;
-    static constexpr int kOffBar = kOffP + kNQ * kPBytes;
-    static constexpr int kNumBars = 2 + 2 * kNst + 4 * kNQ;
+    static constexpr int kOffBar = kOffP + NQ * kPBytes;
+    static constexpr int kNumBars = 2 + 2 * kNst + 5 * NQ;
     static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
-    static constexpr int kTmemS = 0;                    // S of tile g: [g*BN, (g+1)*BN)
-    static constexpr int kTmemPV = kNQ * BN;            // PV of tile g: [kTmemPV + g*DH, ...)
-    static constexpr int kTmemCols = 512;
-    static_assert(kNQ * (BN + DH) <= 512, "TMEM budget");
+    static constexpr int kTmemS = 0;                    // S of tile g: [g*kBN, (g+1)*kBN)
+    static constexpr int kTmemPV = NQ * kBN;            // PV of tile g: [kTmemPV + g*DH, ...)
+    static constexpr int kTmemCols = NQ * (kBN + DH) <= 256 ? 256 : 512;
+    static_assert(NQ * (kBN + DH) <= 512, "TMEM budget");
     static_assert(kSmem <= 227 * 1024, "smem budget");
 };
 
@@ -83,10 +93,10 @@ __device__ __forceinline__ uint32_t core_off(int r, int c) {
 }
 
 struct Item {
-    int scope, q0, h, m, s0, s1, nt;
+    int scope, q0, h, m, s0, s1, nt, nq;   // nq: Q tiles of this item holding real rows
 };
 
-template <int BN>
+template <int NQ>
 __device__ __forceinline__ Item decode(const Args& A, int item) {
     Item it;
     const int wi = item / A.H;
@@ -96,7 +106,8 @@ __device__ __forceinline__ Item decode(const Args& A, int item) {
     it.s0 = __ldg(A.scope_seg + it.scope);
     it.s1 = it.s0 + __ldg(A.scope_nseg + it.scope);
     it.m = __ldg(A.scope_len + it.scope);
-    it.nt = (it.m + BN - 1) / BN;
+    it.nt = (it.m + kBN - 1) / kBN;
+    it.nq = min(NQ, (it.m - it.q0 + kBM - 1) / kBM);
     return it;
 }
 
@@ -117,19 +128,22 @@ __device__ __forceinline__ void gather(const Args& A, const __nv_bfloat16* base,
     }
 }
 
-template <int DH, int BN, typename OutT>
-__global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A) {
-    using C = Cfg<DH, BN>;
+template <int DH, typename OutT>
+__global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(const Args A) {
+    using C = Cfg<DH>;
+    constexpr int NQ = C::NQ;
+    constexpr int kThreads = threads_for<DH>();
     extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
     uint64_t* q_full = bars + 0;
     uint64_t* q_empty = bars + 1;
     uint64_t* kv_full = bars + 2;
     uint64_t* kv_empty = bars + 2 + kNst;
-    uint64_t* s_full = bars + 2 + 2 * kNst;      // [kNQ]  MMA -> softmax
-    uint64_t* p_full = s_full + kNQ;             // [kNQ]  softmax -> MMA (S read, P written)
-    uint64_t* pv_full = s_full + 2 * kNQ;        // [kNQ]  MMA -> softmax
-    uint64_t* pv_empty = s_full + 3 * kNQ;       // [kNQ]  softmax -> MMA (PV folded)
+    uint64_t* s_full = bars + 2 + 2 * kNst;      // [NQ] MMA -> softmax: S_g ready
+    uint64_t* s_free = s_full + NQ;              // [NQ] softmax -> MMA: S_g copied to registers
+    uint64_t* p_full = s_full + 2 * NQ;          // [NQ] softmax -> MMA: P_g in smem
+    uint64_t* pv_full = s_full + 3 * NQ;         // [NQ] MMA -> softmax: P_g V ready
+    uint64_t* pv_empty = s_full + 4 * NQ;        // [NQ] softmax -> MMA: P_g V folded
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
     const int tid = threadIdx.x;
@@ -147,8 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
             mbar_init(kv_full + s, kLoadWarps * 32);
             mbar_init(kv_empty + s, 1);
         }
-        for (int g = 0; g < kNQ; ++g) {
+        for (int g = 0; g < NQ; ++g) {
             mbar_init(s_full + g, 1);
+            mbar_init(s_free + g, 128);
             mbar_init(p_full + g, 128);
             mbar_init(pv_full + g, 1);
             mbar_init(pv_empty + g, 128);
@@ -170,10 +185,9 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
         // ------------------------------------------------ loader warps
         uint32_t q_use = 0, kv_it = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode<BN>(A, item);
+            const Item it = decode<NQ>(A, item);
             mbar_wait(q_empty, (q_use & 1) ^ 1);
-#pragma unroll
-            for (int g = 0; g < kNQ; ++g)
+            for (int g = 0; g < it.nq; ++g)
                 gather<DH, kBM>(A, A.q, A.ld_q, it, it.q0 + g * kBM,
                                 sm_base + C::kOffQ + g * C::kQBytes, tid);
             cp_async_arrive(q_full);
@@ -183,19 +197,22 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
                 const uint32_t u = kv_it / kNst;
                 mbar_wait(kv_empty + s, (u & 1) ^ 1);
                 const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
-                gather<DH, BN>(A, A.k, A.ld_k, it, j * BN, kb, tid);
-                gather<DH, BN>(A, A.v, A.ld_v, it, j * BN, kb + C::kKVBytes, tid);
+                gather<DH, kBN>(A, A.k, A.ld_k, it, j * kBN, kb, tid);
+                gather<DH, kBN>(A, A.v, A.ld_v, it, j * kBN, kb + C::kKVBytes, tid);
                 cp_async_arrive(kv_full + s);
             }
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA warp (one thread)
         if (lane == 0) {
-            constexpr uint32_t idS = idesc_bf16(kBM, BN, 0, 0);
+            constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
             constexpr uint32_t idPV = idesc_bf16(kBM, DH, 0, 1);
-            uint32_t q_use = 0, kv_it = 0, t_it = 0;
+            uint32_t q_use = 0, kv_it = 0;
+            uint32_t tg[NQ];                     // tiles processed by group g so far
+#pragma unroll
+            for (int g = 0; g < NQ; ++g) tg[g] = 0;
             for (int item = blockIdx.x; item < total; item += gridDim.x) {
-                const Item it = decode<BN>(A, item);
+                const Item it = decode<NQ>(A, item);
                 mbar_wait(q_full, q_use & 1);
                 auto issue_S = [&](int g, int j) {
                     const int s = (kv_it + j) % kNst;
@@ -203,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
                     const uint32_t qa = sm_base + C::kOffQ + g * C::kQBytes;
 #pragma unroll
                     for (int k = 0; k < DH / 16; ++k)
-                        umma_f16(tmem + C::kTmemS + g * BN, smem_desc(qa + k * 256, 128, 16 * DH),
+                        umma_f16(tmem + C::kTmemS + g * kBN, smem_desc(qa + k * 256, 128, 16 * DH),
                                  smem_desc(kb + k * 256, 128, 16 * DH), idS, k > 0);
                     umma_commit(s_full + g);
                 };
@@ -214,128 +231,121 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
                     tc_fence_after();
                 };
                 wait_kv(0);
-#pragma unroll
-                for (int g = 0; g < kNQ; ++g) {
-                    // S_g buffer free once softmax g consumed the previous tile
-                    if (t_it > 0) mbar_wait(p_full + g, (t_it - 1) & 1);
+                for (int g = 0; g < it.nq; ++g) {
+                    if (tg[g] > 0) mbar_wait(s_free + g, (tg[g] - 1) & 1);   // S_g copied out
                     issue_S(g, 0);
                 }
                 for (int j = 0; j < it.nt; ++j) {
-                    const uint32_t tj = t_it + j;
                     const int s = (kv_it + j) % kNst;
                     const uint32_t vb = sm_base + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes;
-                    if (j + 1 < it.nt) wait_kv(j + 1);
-#pragma unroll
-                    for (int g = 0; g < kNQ; ++g) {
-                        mbar_wait(p_full + g, tj & 1);             // P_g,j in smem; S_g free
-                        mbar_wait(pv_empty + g, (tj & 1) ^ 1);     // PV_g folded by softmax
+                    if (j + 1 < it.nt) {
+                        wait_kv(j + 1);
+                        for (int g = 0; g < it.nq; ++g) {
+                            mbar_wait(s_free + g, (tg[g] + j) & 1);          // S_g,j in registers
+                            tc_fence_after();
+                            issue_S(g, j + 1);
+                        }
+                    }
+                    for (int g = 0; g < it.nq; ++g) {
+                        const uint32_t t = tg[g] + j;
+                        mbar_wait(p_full + g, t & 1);                      // P_g,j in smem
+                        mbar_wait(pv_empty + g, (t & 1) ^ 1);              // previous P V folded
                         fence_proxy_async();
                         tc_fence_after();
                         const uint32_t pb = sm_base + C::kOffP + g * C::kPBytes;
 #pragma unroll
-                        for (int k = 0; k < BN / 16; ++k)
-                            umma_f16(tmem + C::kTmemPV + g * DH, smem_desc(pb + k * 256, 128, 16 * BN),
+                        for (int k = 0; k < kBN / 16; ++k)
+                            umma_f16(tmem + C::kTmemPV + g * DH,
+                                     smem_desc(pb + k * 256, 128, 16 * kBN),
                                      smem_desc(vb + k * 32 * DH, 16 * DH, 128), idPV, k > 0);
                         umma_commit(pv_full + g);
-                        if (j + 1 < it.nt) issue_S(g, j + 1);
                     }
                     umma_commit(kv_empty + s);
                 }
                 umma_commit(q_empty);
                 ++q_use;
                 kv_it += it.nt;
-                t_it += it.nt;
+                for (int g = 0; g < it.nq; ++g) tg[g] += it.nt;
             }
         }
     } else {
         // ------------------------------------------------ softmax warpgroups
-        const int sw = warp - (kMmaWarp + 1);             // 0 .. kSoftWarps-1
+        const int sw = warp - (kMmaWarp + 1);             // 0 .. 4*NQ-1
         const int g = sw >> 2;                            // Q tile of this warpgroup
         const int r = (sw & 3) * 32 + lane;               // row in the tile = TMEM lane
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
         const float sl2 = A.scale_log2;
-        const uint32_t sbase = tmem + lane_base + C::kTmemS + g * BN;
+        const uint32_t sbase = tmem + lane_base + C::kTmemS + g * kBN;
         const uint32_t vbase = tmem + lane_base + C::kTmemPV + g * DH;
         const uint32_t pb = sm_base + C::kOffP + g * C::kPBytes;
-        uint32_t t_it = 0;
+        uint32_t tg = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode<BN>(A, item);
+            const Item it = decode<NQ>(A, item);
+            if (g >= it.nq) continue;                     // this Q tile is past the scope
             float o[DH];
 #pragma unroll
             for (int i = 0; i < DH; ++i) o[i] = 0.f;
             float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
             for (int j = 0; j < it.nt; ++j) {
-                const uint32_t tj = t_it + j;
-                mbar_wait(s_full + g, tj & 1);
+                const uint32_t t = tg + j;
+                mbar_wait(s_full + g, t & 1);
                 tc_fence_after();
-                const int kvalid = it.m - j * BN;         // keys < kvalid are real
-                const bool full = kvalid >= BN;
-                // pass 1: row max
+                uint32_t x[kBN];
+                {
+                    uint32_t (&x0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[0]);
+                    uint32_t (&x1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[32]);
+                    tmem_ld32(sbase, x0);
+                    tmem_ld32(sbase + 32, x1);
+                    tmem_wait_ld();
+                }
+                tc_fence_before();
+                mbar_arrive(s_free + g);                  // MMA may overwrite S_g now
+                const int kvalid = it.m - j * kBN;        // keys < kvalid are real
+                if (kvalid < kBN) {
+#pragma unroll
+                    for (int e = 0; e < kBN; ++e)
+                        if (e >= kvalid) x[e] = __float_as_uint(-INFINITY);
+                }
                 float mx = -INFINITY;
 #pragma unroll
-                for (int c = 0; c < BN / 32; ++c) {
-                    uint32_t x[32];
-                    tmem_ld32(sbase + c * 32, x);
-                    tmem_wait_ld();
-                    if (full) {
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(x[e]));
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            if (c * 32 + e < kvalid) mx = fmaxf(mx, __uint_as_float(x[e]));
-                    }
-                }
+                for (int e = 0; e < kBN; ++e) mx = fmaxf(mx, __uint_as_float(x[e]));
                 const float m_new = fmaxf(m_run, mx);
                 const float alpha = (m_run == -INFINITY) ? 0.f : ex2f((m_run - m_new) * sl2);
                 const float nms = -m_new * sl2;
-                // fold the previous tile's P V before P is overwritten
+                // fold the previous tile's P V before P_g is overwritten
                 if (j > 0) {
-                    mbar_wait(pv_full + g, (tj - 1) & 1);
+                    mbar_wait(pv_full + g, (t - 1) & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int c = 0; c < DH / 16; ++c) {
-                        uint32_t x[16];
-                        tmem_ld16(vbase + c * 16, x);
+                        uint32_t y[16];
+                        tmem_ld16(vbase + c * 16, y);
                         tmem_wait_ld();
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
-                            o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(x[e]));
+                            o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(y[e]));
                     }
                     tc_fence_before();
                     mbar_arrive(pv_empty + g);
                 }
-                // pass 2: P = exp2(s*sl2 - m*sl2) -> bf16 smem (core-matrix rows)
+                // P = exp2(s*sl2 - m*sl2) -> bf16 smem (core-matrix rows)
                 float sum = 0.f;
 #pragma unroll
-                for (int c = 0; c < BN / 32; ++c) {
-                    uint32_t x[32];
-                    tmem_ld32(sbase + c * 32, x);
-                    tmem_wait_ld();
-                    uint32_t pk[16];
+                for (int c = 0; c < kBN / 8; ++c) {
+                    uint32_t pk[4];
 #pragma unroll
-                    for (int e = 0; e < 32; e += 2) {
-                        float p0 = ex2f(fmaf(__uint_as_float(x[e]), sl2, nms));
-                        float p1 = ex2f(fmaf(__uint_as_float(x[e + 1]), sl2, nms));
-                        if (!full) {
-                            if (c * 32 + e >= kvalid) p0 = 0.f;
-                            if (c * 32 + e + 1 >= kvalid) p1 = 0.f;
-                        }
+                    for (int e = 0; e < 8; e += 2) {
+                        const float p0 = ex2f(fmaf(__uint_as_float(x[c * 8 + e]), sl2, nms));
+                        const float p1 = ex2f(fmaf(__uint_as_float(x[c * 8 + e + 1]), sl2, nms));
                         sum += p0 + p1;
                         __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                         pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                     }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t dst = pb + core_off<BN>(r, c * 4 + q);
-                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst),
-                                     "r"(pk[4 * q]), "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]),
-                                     "r"(pk[4 * q + 3])
-                                     : "memory");
-                    }
+                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(pb + core_off<kBN>(r, c)),
+                                 "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
+                                 : "memory");
                 }
                 fence_proxy_async();
-                tc_fence_before();
                 mbar_arrive(p_full + g);
                 l_run = l_run * alpha + sum;
                 m_run = m_new;
@@ -343,17 +353,16 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
             }
             // last tile's P V, then normalise and write the row
             {
-                const uint32_t tl = t_it + it.nt - 1;
-                mbar_wait(pv_full + g, tl & 1);
+                mbar_wait(pv_full + g, (tg + it.nt - 1) & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < DH / 16; ++c) {
-                    uint32_t x[16];
-                    tmem_ld16(vbase + c * 16, x);
+                    uint32_t y[16];
+                    tmem_ld16(vbase + c * 16, y);
                     tmem_wait_ld();
 #pragma unroll
                     for (int e = 0; e < 16; ++e)
-                        o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(x[e]));
+                        o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(y[e]));
                 }
                 tc_fence_before();
                 mbar_arrive(pv_empty + g);
@@ -378,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
                         if (c < A.dh) out[c] = o[c] * inv;
                 }
             }
-            t_it += it.nt;
+            tg += it.nt;
         }
     }
     tc_fence_before();
@@ -386,10 +395,10 @@ __global__ void __launch_bounds__(kThreads, 1) bswin_attn_tc_kernel(const Args A
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
 }
 
-template <int DH, int BN, typename OutT>
+template <int DH, typename OutT>
 int launch(const Args& A, cudaStream_t st) {
-    using C = Cfg<DH, BN>;
-    auto kern = bswin_attn_tc_kernel<DH, BN, OutT>;
+    using C = Cfg<DH>;
+    auto kern = bswin_attn_tc_kernel<DH, OutT>;
     static bool attr = false;
     if (!attr) {
         F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -398,21 +407,26 @@ int launch(const Args& A, cudaStream_t st) {
     }
     const int total = A.nwork * A.H;
     const int grid = std::max(1, std::min(total, f3d_num_sms()));
-    kern<<<grid, kThreads, C::kSmem, st>>>(A);
+    kern<<<grid, threads_for<DH>(), C::kSmem, st>>>(A);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
 
 template <int DH>
 int launch_dh(const Args& A, cudaStream_t st) {
-    constexpr int BN = DH <= 64 ? 128 : 64;
-    return A.out_f32 ? launch<DH, BN, float>(A, st) : launch<DH, BN, __nv_bfloat16>(A, st);
+    return A.out_f32 ? launch<DH, float>(A, st) : launch<DH, __nv_bfloat16>(A, st);
 }
 
 }  // namespace attn_tc
 }  // namespace f3d
 
 using namespace f3d;
+
+extern "C" int f3d_attention_tc_qstep(int dh) {
+    const int dp = (dh + 15) / 16 * 16;
+    const int nq = dp <= 32 ? 3 : (dp <= 64 ? 2 : 1);
+    return nq * f3d::attn_tc::kBM;
+}
 
 extern "C" int f3d_bswin_attention_tc(const void* q, const void* k, const void* v, int64_t ld_q,
                                       int64_t ld_k, int64_t ld_v, void* o, int64_t ld_o,
