@@ -66,16 +66,16 @@ struct Cfg {
     static constexpr int kQBytes = kBM * DH * 2;        // one Q tile
     static constexpr int kKVBytes = kBN * DH * 2;       // one of K or V
     static constexpr int kPBytes = kBM * kBN * 2;       // one P tile
-    static constexpr int kOffQ = 0;
-    static constexpr int kOffKV = kOffQ + NQ * kQBytes;
+    static constexpr int kOffQ = 0;                     // 2 buffers x NQ Q tiles
+    static constexpr int kOffKV = kOffQ + 2 * NQ * kQBytes;
     static constexpr int kOffP = kOffKV + kNst * 2 * kKVBytes;
     static constexpr int kOffBar = kOffP + NQ * kPBytes;
-    static constexpr int kNumBars = 2 + 2 * kNst + 5 * NQ;
+    static constexpr int kNumBars = 4 + 2 * kNst + 4 * NQ;
     static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
-    static constexpr int kTmemS = 0;                    // S of tile g: [g*kBN, (g+1)*kBN)
-    static constexpr int kTmemPV = NQ * kBN;            // PV of tile g: [kTmemPV + g*DH, ...)
-    static constexpr int kTmemCols = NQ * (kBN + DH) <= 256 ? 256 : 512;
-    static_assert(NQ * (kBN + DH) <= 512, "TMEM budget");
+    static constexpr int kTmemS = 0;                    // S of tile g, buffer b: (2g+b)*kBN
+    static constexpr int kTmemPV = 2 * NQ * kBN;        // PV of tile g: kTmemPV + g*DH
+    static constexpr int kTmemCols = NQ * (2 * kBN + DH) <= 256 ? 256 : 512;
+    static_assert(NQ * (2 * kBN + DH) <= 512, "TMEM budget");
     static_assert(kSmem <= 227 * 1024, "smem budget");
 };
 
@@ -135,15 +135,15 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
     constexpr int kThreads = threads_for<DH>();
     extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-    uint64_t* q_full = bars + 0;
-    uint64_t* q_empty = bars + 1;
-    uint64_t* kv_full = bars + 2;
-    uint64_t* kv_empty = bars + 2 + kNst;
-    uint64_t* s_full = bars + 2 + 2 * kNst;      // [NQ] MMA -> softmax: S_g ready
-    uint64_t* s_free = s_full + NQ;              // [NQ] softmax -> MMA: S_g copied to registers
-    uint64_t* p_full = s_full + 2 * NQ;          // [NQ] softmax -> MMA: P_g in smem
-    uint64_t* pv_full = s_full + 3 * NQ;         // [NQ] MMA -> softmax: P_g V ready
-    uint64_t* pv_empty = s_full + 4 * NQ;        // [NQ] softmax -> MMA: P_g V folded
+    // every barrier below completes at most one phase ahead of its waiter
+    uint64_t* q_full = bars + 0;                 // [2] loaders -> MMA (Q buffer filled)
+    uint64_t* q_empty = bars + 2;                // [2] MMA -> loaders (Q buffer consumed)
+    uint64_t* kv_full = bars + 4;                // [kNst]
+    uint64_t* kv_empty = bars + 4 + kNst;        // [kNst]
+    uint64_t* s_full = bars + 4 + 2 * kNst;      // [NQ][2] MMA -> softmax (S_g in buffer b)
+    uint64_t* p_full = s_full + 2 * NQ;          // [NQ] softmax -> MMA (P_g written, S read,
+                                                 //      previous P_g V folded)
+    uint64_t* pv_full = s_full + 3 * NQ;         // [NQ] MMA -> softmax (P_g V ready)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
     const int tid = threadIdx.x;
@@ -155,18 +155,19 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
     for (int i = tid; i < C::kOffBar / 16; i += kThreads)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
-        mbar_init(q_full, kLoadWarps * 32);
-        mbar_init(q_empty, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(q_full + b, kLoadWarps * 32);
+            mbar_init(q_empty + b, 1);
+        }
         for (int s = 0; s < kNst; ++s) {
             mbar_init(kv_full + s, kLoadWarps * 32);
             mbar_init(kv_empty + s, 1);
         }
         for (int g = 0; g < NQ; ++g) {
-            mbar_init(s_full + g, 1);
-            mbar_init(s_free + g, 128);
+            mbar_init(s_full + 2 * g, 1);
+            mbar_init(s_full + 2 * g + 1, 1);
             mbar_init(p_full + g, 128);
             mbar_init(pv_full + g, 1);
-            mbar_init(pv_empty + g, 128);
         }
         fence_mbar_init();
     }
@@ -186,11 +187,12 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         uint32_t q_use = 0, kv_it = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
             const Item it = decode<NQ>(A, item);
-            mbar_wait(q_empty, (q_use & 1) ^ 1);
+            const int qb = q_use & 1;
+            mbar_wait(q_empty + qb, ((q_use >> 1) & 1) ^ 1);
             for (int g = 0; g < it.nq; ++g)
                 gather<DH, kBM>(A, A.q, A.ld_q, it, it.q0 + g * kBM,
-                                sm_base + C::kOffQ + g * C::kQBytes, tid);
-            cp_async_arrive(q_full);
+                                sm_base + C::kOffQ + (qb * NQ + g) * C::kQBytes, tid);
+            cp_async_arrive(q_full + qb);
             ++q_use;
             for (int j = 0; j < it.nt; ++j, ++kv_it) {
                 const int s = kv_it % kNst;
@@ -213,44 +215,39 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             for (int g = 0; g < NQ; ++g) tg[g] = 0;
             for (int item = blockIdx.x; item < total; item += gridDim.x) {
                 const Item it = decode<NQ>(A, item);
-                mbar_wait(q_full, q_use & 1);
+                const int qb = q_use & 1;
+                mbar_wait(q_full + qb, (q_use >> 1) & 1);
+                // S_g,j -> TMEM buffer (tg[g]+j)&1.  Reusing that buffer needs
+                // softmax g done with S_g,j-2: implied by p_full_g,j-2, waited
+                // before PV_g,j-2 was issued.
                 auto issue_S = [&](int g, int j) {
                     const int s = (kv_it + j) % kNst;
+                    const int b = (tg[g] + j) & 1;
                     const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
-                    const uint32_t qa = sm_base + C::kOffQ + g * C::kQBytes;
+                    const uint32_t qa = sm_base + C::kOffQ + (qb * NQ + g) * C::kQBytes;
 #pragma unroll
                     for (int k = 0; k < DH / 16; ++k)
-                        umma_f16(tmem + C::kTmemS + g * kBN, smem_desc(qa + k * 256, 128, 16 * DH),
+                        umma_f16(tmem + C::kTmemS + (2 * g + b) * kBN,
+                                 smem_desc(qa + k * 256, 128, 16 * DH),
                                  smem_desc(kb + k * 256, 128, 16 * DH), idS, k > 0);
-                    umma_commit(s_full + g);
+                    umma_commit(s_full + 2 * g + b);
                 };
                 auto wait_kv = [&](int j) {
                     const uint32_t kvi = kv_it + j;
                     mbar_wait(kv_full + kvi % kNst, (kvi / kNst) & 1);
-                    fence_proxy_async();
                     tc_fence_after();
                 };
                 wait_kv(0);
-                for (int g = 0; g < it.nq; ++g) {
-                    if (tg[g] > 0) mbar_wait(s_free + g, (tg[g] - 1) & 1);   // S_g copied out
-                    issue_S(g, 0);
-                }
+                for (int g = 0; g < it.nq; ++g) issue_S(g, 0);
                 for (int j = 0; j < it.nt; ++j) {
                     const int s = (kv_it + j) % kNst;
                     const uint32_t vb = sm_base + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes;
                     if (j + 1 < it.nt) {
                         wait_kv(j + 1);
-                        for (int g = 0; g < it.nq; ++g) {
-                            mbar_wait(s_free + g, (tg[g] + j) & 1);          // S_g,j in registers
-                            tc_fence_after();
-                            issue_S(g, j + 1);
-                        }
+                        for (int g = 0; g < it.nq; ++g) issue_S(g, j + 1);
                     }
                     for (int g = 0; g < it.nq; ++g) {
-                        const uint32_t t = tg[g] + j;
-                        mbar_wait(p_full + g, t & 1);                      // P_g,j in smem
-                        mbar_wait(pv_empty + g, (t & 1) ^ 1);              // previous P V folded
-                        fence_proxy_async();
+                        mbar_wait(p_full + g, (tg[g] + j) & 1);           // P_g,j in smem
                         tc_fence_after();
                         const uint32_t pb = sm_base + C::kOffP + g * C::kPBytes;
 #pragma unroll
@@ -262,7 +259,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                     }
                     umma_commit(kv_empty + s);
                 }
-                umma_commit(q_empty);
+                umma_commit(q_empty + qb);
                 ++q_use;
                 kv_it += it.nt;
                 for (int g = 0; g < it.nq; ++g) tg[g] += it.nt;
@@ -275,7 +272,6 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         const int r = (sw & 3) * 32 + lane;               // row in the tile = TMEM lane
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
         const float sl2 = A.scale_log2;
-        const uint32_t sbase = tmem + lane_base + C::kTmemS + g * kBN;
         const uint32_t vbase = tmem + lane_base + C::kTmemPV + g * DH;
         const uint32_t pb = sm_base + C::kOffP + g * C::kPBytes;
         uint32_t tg = 0;
@@ -288,18 +284,18 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
             for (int j = 0; j < it.nt; ++j) {
                 const uint32_t t = tg + j;
-                mbar_wait(s_full + g, t & 1);
+                const int b = t & 1;
+                mbar_wait(s_full + 2 * g + b, (t >> 1) & 1);
                 tc_fence_after();
                 uint32_t x[kBN];
                 {
+                    const uint32_t sb = tmem + lane_base + C::kTmemS + (2 * g + b) * kBN;
                     uint32_t (&x0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[0]);
                     uint32_t (&x1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[32]);
-                    tmem_ld32(sbase, x0);
-                    tmem_ld32(sbase + 32, x1);
+                    tmem_ld32(sb, x0);
+                    tmem_ld32(sb + 32, x1);
                     tmem_wait_ld();
                 }
-                tc_fence_before();
-                mbar_arrive(s_free + g);                  // MMA may overwrite S_g now
                 const int kvalid = it.m - j * kBN;        // keys < kvalid are real
                 if (kvalid < kBN) {
 #pragma unroll
@@ -312,7 +308,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 const float m_new = fmaxf(m_run, mx);
                 const float alpha = (m_run == -INFINITY) ? 0.f : ex2f((m_run - m_new) * sl2);
                 const float nms = -m_new * sl2;
-                // fold the previous tile's P V before P_g is overwritten
+                // fold the previous tile's P V (this also frees P_g for overwrite)
                 if (j > 0) {
                     mbar_wait(pv_full + g, (t - 1) & 1);
                     tc_fence_after();
@@ -325,8 +321,6 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                         for (int e = 0; e < 16; ++e)
                             o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(y[e]));
                     }
-                    tc_fence_before();
-                    mbar_arrive(pv_empty + g);
                 }
                 // P = exp2(s*sl2 - m*sl2) -> bf16 smem (core-matrix rows)
                 float sum = 0.f;
@@ -346,6 +340,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                                  : "memory");
                 }
                 fence_proxy_async();
+                tc_fence_before();
                 mbar_arrive(p_full + g);
                 l_run = l_run * alpha + sum;
                 m_run = m_new;
@@ -364,8 +359,6 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                     for (int e = 0; e < 16; ++e)
                         o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(y[e]));
                 }
-                tc_fence_before();
-                mbar_arrive(pv_empty + g);
             }
             const int vr = it.q0 + g * kBM + r;
             if (vr < it.m) {
