@@ -22,7 +22,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -52,44 +51,47 @@ def workload(rank):
 
 
 class Clocks:
-    """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
+    """Clock / throttle sampling during the timed region (B200_PROFILING.md
+    recipe): ONE `nvidia-smi -lms` process is started before the region and
+    stopped after it, so no process is forked while steps are being timed."""
 
-    def __init__(self, index):
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index, period_ms=50):
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
+        self._p = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-
-        def run():
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.1)
-
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", f"-lms={self.period_ms}"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)           # first sample lands before the timed region
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(2 * self.period_ms / 1e3)
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except Exception:
+            self._p.kill()
+            out, _ = self._p.communicate()
+        self.rows = [[x.strip() for x in ln.split(",")] for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
@@ -199,10 +201,19 @@ def main():
 
     for _ in range(args.warmup):
         bb.forward(C_d, X_d)
-    bb.forward(C_d, X_d, keep_trace=True)
+    f_eager, _ = bb.forward(C_d, X_d, keep_trace=True)
     trace = bb.last_trace
 
-    # ---- device-resident throughput (value): per-step events, L2 flushed between steps
+    # ---- device-resident throughput (value): the forward captured as CUDA
+    # graphs (no host work inside a step), inputs resident in HBM, per-step
+    # events, L2 flushed between steps
+    bb.capture(N_POINTS, torch.bfloat16)
+    bb.graph_coords.copy_(C_d)
+    bb.graph_feats.copy_(X_d.to(torch.bfloat16))
+    for _ in range(args.warmup):
+        bb.replay()
+    n_out = bb.check_graph()
+    graph_ok = bool(torch.equal(bb._graphs["X"][:n_out], bb.forward(C_d, X_d.to(torch.bfloat16))[0]))
     barrier()
     step_ms = []
     with Clocks(local) as clk:
@@ -211,10 +222,11 @@ def main():
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record()
-            bb.forward(C_d, X_d)
+            bb.replay()
             s1.record()
             torch.cuda.synchronize()
             step_ms.append(s0.elapsed_time(s1))
+    bb.check_graph()
     barrier()
     ms = sum(step_ms) / len(step_ms)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -235,9 +247,8 @@ def main():
 
     # ---- end to end through the public API with host buffers (e2e)
     out_rows = []
-    out_h = None
     for _ in range(args.warmup):          # pinned output buffer + side stream created here
-        out_h, _ = bb.forward_host(C_h, X_h, out_h)
+        bb.forward_host(C_h, X_h)
     barrier()
     e2e_ms = []
     for _ in range(args.steps):
@@ -245,8 +256,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        out_h, _ = bb.forward_host(C_h, X_h, out_h)
-        res = out_h
+        res, _ = bb.forward_host(C_h, X_h)
         e1.record()
         torch.cuda.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
@@ -319,6 +329,7 @@ def main():
             "own_kernels_ms_per_step": round(mine_ms, 4),
             "psh_sweeps": [s.sweeps for s in trace],
             "gpu_launches": launches // steps,
+            "graph_matches_eager": graph_ok,
             "e2e": {"value": total_pts / (e2e_ms_max / 1e3), "unit": "points/s",
                     "h2d_bytes_per_step": int(C_h.numel() * 8 + X_h.numel() * 2),
                     "d2h_bytes_per_step": int(out_rows[-1] * D_MODEL * 2),

@@ -15,7 +15,12 @@
  *   - int status: F3D_OK or an F3D_ERR_* code that the Python layer maps onto
  *     the reference exception classes (bw/errors.py:9-30).  Data-dependent
  *     errors (range, integrity) are reported through small device-side
- *     status arrays that the caller reads after the stream drains.
+ *     status arrays that the caller reads after the stream drains;
+ *   - arguments named n_dev / ntiles_dev / npool_dev (nullable) hold a row
+ *     count in device memory: the launch is sized for the host capacity and
+ *     processes min(capacity, *count) rows, so a pipeline whose sizes are
+ *     data dependent (pooled rows) runs with no host read-back and can be
+ *     captured in a CUDA graph.
  */
 #ifndef F3D_H_
 #define F3D_H_
@@ -71,11 +76,12 @@ int f3d_morton_encode(const int64_t *vox, int64_t n, int bits, int64_t *codes_ou
 
 /* ---------------------------------------------- a1-a3 fused (pipeline path)
  * coords -> voxelize -> per-batch min remap -> range stats -> home hash, in
- * two passes over the points.  ws: nbatch*3 int64.  Outputs as above. */
+ * two passes over the points.  ws: nbatch*3 int64.  Outputs as above.
+ * n_dev (nullable, single batch only): device point count <= n. */
 int f3d_voxel_hash(const double *coords, const int32_t *batch, int64_t n, int32_t nbatch,
                    const double *origin3_host, double voxel_size, int kind, int32_t K,
                    int64_t S_div, int bits, int32_t *vox32_out, int32_t *home_out,
-                   int64_t *stats_out, int64_t *ws, void *stream);
+                   int64_t *stats_out, int64_t *ws, const int32_t *n_dev, void *stream);
 
 /* ------------------------------------------------------ a5-a7: PSH assign
  * Replaces bw/bucketing.py:275-320 assign_buckets (and :323-382
@@ -87,13 +93,15 @@ int f3d_voxel_hash(const double *coords, const int32_t *batch, int64_t n, int32_
  * dest = base[batch*(K+1)+id] + offset (bw/bucketing.py:100-101).
  * probe_offsets_host: P x 3 int8 offsets (bw/bucketing.py:51-66), already cut
  * to min(max_probes, len).  info_out (device, 4 x int32): [sweeps,
- * used_sequential_fallback, batch_error, reserved]. */
+ * used_sequential_fallback, batch_error, reserved].  n_dev (nullable, single
+ * batch only): device point count <= n; points past it are not touched. */
 size_t f3d_psh_workspace_size(int64_t n, int32_t nbatch, int32_t K);
 int f3d_psh_assign(const int32_t *vox32, const int32_t *home, const int32_t *batch, int64_t n,
                    int32_t nbatch, int32_t K, int32_t S, int kind, int64_t S_div, int bits,
                    int strict, const int8_t *probe_offsets_host, int32_t P, int32_t max_sweeps,
                    int32_t *bucket_id, int32_t *bucket_offset, int32_t *counts, int32_t *base,
-                   int32_t *dest, int32_t *info_out, void *ws, size_t ws_bytes, void *stream);
+                   int32_t *dest, int32_t *info_out, void *ws, size_t ws_bytes,
+                   const int32_t *n_dev, void *stream);
 
 /* ------------------------------------------------- a7: validate()
  * Replaces BucketAssignment.validate (bw/bucketing.py:116-145).
@@ -112,9 +120,9 @@ int f3d_validate_assignment(const int32_t *bucket_id, const int32_t *bucket_offs
  * inverse out = scattered[perm] (pkg/tests/test_stage.py:165).  row_bytes
  * must be a multiple of 4; rows are moved with 16-byte vectors when aligned. */
 int f3d_scatter_rows(const void *src, const int32_t *dest, int64_t n, int64_t row_bytes,
-                     void *dst, void *stream);
+                     void *dst, const int32_t *n_dev, void *stream);
 int f3d_gather_rows(const void *src, const int32_t *idx, int64_t n, int64_t row_bytes,
-                    void *dst, void *stream);
+                    void *dst, const int32_t *n_dev, void *stream);
 
 
 /* ------------------------------------------ a9-a11: bucket-swin attention
@@ -158,11 +166,14 @@ int f3d_attention_tc_qstep(int dh);
 
 /* Device planner for one round (bw/attention.py:84-139 over the split table
  * of bw/bucketing.py:147-166, built from the PSH counts/base in HBM).
- * nscopes = ceil(nb / (W*stride)) * stride; segment arrays hold nscopes*W
- * entries (fixed stride W per scope); work holds max_work (scope, q_start)
- * pairs with q_start stepping by qstep (128: mma.sync kernels, 256: tcgen05
- * kernel); live receives [nwork, nlive, max_len].  off = (t*shift) mod W. */
-int f3d_plan_round(const int32_t *counts, const int32_t *base, int K, int S, int nb, int W,
+ * The table size nb = K + ceil(counts[K] / S) is read on the device; nb_cap
+ * is the host's upper bound and nscopes = ceil(nb_cap / (W*stride)) * stride;
+ * segment arrays hold nscopes*W entries (fixed stride W per scope); work
+ * holds max_work (scope, q_start) pairs with q_start stepping by qstep
+ * (f3d_attention_tc_qstep for the tcgen05 kernel); live receives [nwork,
+ * nlive, max_len, status] with status bits 1 (window_w > nb, ConfigError),
+ * 2 (nb > nb_cap), 4 (work list truncated).  off = (t*shift) mod W. */
+int f3d_plan_round(const int32_t *counts, const int32_t *base, int K, int S, int nb_cap, int W,
                    int stride, int off, int nscopes, int32_t *scope_seg, int32_t *scope_nseg,
                    int32_t *seg_start, int32_t *seg_vstart, int32_t *scope_len,
                    int32_t *scope_order, int32_t *work, int max_work, int qstep, int32_t *live,
@@ -183,7 +194,8 @@ int f3d_stage_pe(const double *coords, int64_t n, int d, double base, const doub
                  int out_kind, void *out, int64_t ld, void *stream);
 /* Per-axis bbox: lo_ext[0..2] = min, lo_ext[3..5] = max - min (0 -> 1).
  * ws: 6 * 296 doubles. */
-int f3d_coord_bbox(const double *coords, int64_t n, double *ws, double *lo_ext, void *stream);
+int f3d_coord_bbox(const double *coords, int64_t n, double *ws, double *lo_ext,
+                   const int32_t *n_dev, void *stream);
 
 /* ------------------------------------------------------ a13: stage rows
  * Fused residual + LayerNorm (+PE) (bw/stage.py:84-88, 135, 157-158):
@@ -210,17 +222,20 @@ int f3d_bias_gelu(void *u_bf16, int64_t n, int dh, const float *bias, void *stre
  * padded); sub_out (nullable) gets each row's tile-local sub-bucket id.
  * flags (device int32) collects integrity failures (1 allocation short,
  * 2 no candidate, 4 over rho, 8 empty, 16 >1 under-filled, 32 bad id).
- * rho <= 64. */
+ * rho <= 64.  ntiles_dev (nullable): device tile count <= ntiles (e.g. the
+ * totals[0] written by f3d_plan_pool). */
 int f3d_pool_build(const double *coords, const int32_t *tile_start, const int32_t *tile_m,
                    const int32_t *tile_out, int ntiles, int rho, int32_t *sub_out,
                    int32_t *members, int32_t *sizes_out, int32_t *seeds_out,
-                   int32_t *passes_out, int32_t *flags, void *stream);
+                   int32_t *passes_out, int32_t *flags, const int32_t *ntiles_dev,
+                   void *stream);
 /* Replaces bw/pooling.py:166-184 pool_features: out[j] = reduce over
  * members of x (sequential in index order; mean = sum / size).
- * dtype: 0 bf16, 1 float, 2 double.  op: 0 sum, 1 mean, 2 min, 3 max. */
+ * dtype: 0 bf16, 1 float, 2 double.  op: 0 sum, 1 mean, 2 min, 3 max.
+ * npool_dev (nullable): device pooled-row count <= npool (totals[1]). */
 int f3d_pool_reduce(const void *x, int dtype, int64_t ldx, int d, const int32_t *members,
                     const int32_t *sizes, int64_t npool, int rho, int op, void *out,
-                    int64_t ldo, void *stream);
+                    int64_t ldo, const int32_t *npool_dev, void *stream);
 
 #ifdef __cplusplus
 }

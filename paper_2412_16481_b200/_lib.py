@@ -35,14 +35,14 @@ SIGNATURES = {
     "f3d_hash_bucket": (_INT, [_P, _I64, _INT, _I32, _I64, _INT, _P, _P, _P, _P]),
     "f3d_morton_encode": (_INT, [_P, _I64, _INT, _P, _P, _P]),
     "f3d_voxel_hash": (_INT, [_P, _P, _I64, _I32, _P, _F64, _INT, _I32, _I64, _INT, _P, _P, _P,
-                              _P, _P]),
+                              _P, _P, _P]),
     "f3d_psh_workspace_size": (_SZ, [_I64, _I32, _I32]),
     "f3d_psh_assign": (_INT, [_P, _P, _P, _I64, _I32, _I32, _I32, _INT, _I64, _INT, _INT, _P,
-                              _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+                              _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P]),
     "f3d_validate_workspace_size": (_SZ, [_I64, _I64]),
     "f3d_validate_assignment": (_INT, [_P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P]),
-    "f3d_scatter_rows": (_INT, [_P, _P, _I64, _I64, _P, _P]),
-    "f3d_gather_rows": (_INT, [_P, _P, _I64, _I64, _P, _P]),
+    "f3d_scatter_rows": (_INT, [_P, _P, _I64, _I64, _P, _P, _P]),
+    "f3d_gather_rows": (_INT, [_P, _P, _I64, _I64, _P, _P, _P]),
     "f3d_bswin_attention": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _INT, _INT, _INT, _P,
                                    _P, _P, _P, _P, _P, _INT, _P, _INT, _INT, _P, _P, _P, _P]),
     "f3d_bswin_attention_tc": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _INT, _INT, _INT,
@@ -53,12 +53,12 @@ SIGNATURES = {
     "f3d_plan_pool": (_INT, [_P, _P, _INT, _INT, _INT, _P, _P, _P, _P, _P]),
     "f3d_positional_encoding": (_INT, [_P, _I64, _INT, _F64, _INT, _P, _I64, _P]),
     "f3d_stage_pe": (_INT, [_P, _I64, _INT, _F64, _P, _INT, _P, _I64, _P]),
-    "f3d_coord_bbox": (_INT, [_P, _I64, _P, _P, _P]),
+    "f3d_coord_bbox": (_INT, [_P, _I64, _P, _P, _P, _P]),
     "f3d_row_ln": (_INT, [_P, _INT, _I64, _P, _I64, _P, _P, _P, _P, _P, _F64, _P, _INT, _I64,
                           _I64, _INT, _F64, _P]),
     "f3d_gelu_f64": (_INT, [_P, _I64, _P, _P]),
-    "f3d_pool_build": (_INT, [_P, _P, _P, _P, _INT, _INT, _P, _P, _P, _P, _P, _P, _P]),
-    "f3d_pool_reduce": (_INT, [_P, _INT, _I64, _INT, _P, _P, _I64, _INT, _INT, _P, _I64, _P]),
+    "f3d_pool_build": (_INT, [_P, _P, _P, _P, _INT, _INT, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "f3d_pool_reduce": (_INT, [_P, _INT, _I64, _INT, _P, _P, _I64, _INT, _INT, _P, _I64, _P, _P]),
     "f3d_bias_gelu": (_INT, [_P, _I64, _INT, _P, _P]),
 }
 

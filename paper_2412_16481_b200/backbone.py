@@ -4,23 +4,30 @@
     per stage:  voxelize -> remap -> PSH -> scatter -> stage_forward (R rounds)
     between:    pool_stage(rho, mean), then re-bucket the pooled f64 centroids
 
-Every step runs in libf3d kernels on device-resident tensors; the host only
-reads the bucket counts once per stage (the attention plan and the pooled row
-count depend on them, exactly as the reference needs ``bucket_table``).
+Every step runs in libf3d kernels on device-resident tensors and the whole
+forward is enqueued without a single host read-back: data-dependent sizes
+(the recycle chunk count, the number of pooled rows) stay on the device, and
+each launch is sized for a host-known capacity and reads the true count
+(``n_dev`` in include/f3d.h).  Error words (voxel range statistics, PSH
+batch errors, planner and pooling flags) are collected on the device and
+checked once, after the stream drains, so ``forward`` costs one sync and
+``capture`` turns the whole forward into two CUDA graphs (stage-0 bucketing
+on the coordinates alone, then everything else), replayed by
+``forward_graph`` / ``forward_host``.
 """
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 from torch.profiler import record_function
 
 from . import _lib as L
-from .attention import DeviceRoundPlan, RoundPlan, plan_arrays, qstep_for, round_members
+from .attention import DeviceRoundPlan, qstep_for
 from .bucketing import BucketAssignment, _run_psh, default_probe_schedule
-from .errors import ConfigError, RangeError
+from .errors import ConfigError
 from .hashing import HashConfig, raise_range
-from .pooling import pool_device
+from .pooling import TILE_CAP, _FLAG_MSGS, _build, _reduce
 from .stage import StageRunner, init_params
 
 
@@ -66,6 +73,21 @@ def split_table(counts, base, K, S):
     return starts.astype(np.int64), lens.astype(np.int64)
 
 
+def pool_capacity(n_cap: int, nslots: int, rho: int):
+    """Upper bounds for the device pooling plan (bw/pooling.py:211-225):
+    sum_c ceil(c/1024) < n/1024 + nslots tiles, and sum_tiles ceil(m/rho)
+    <= ceil(n/rho) + tiles pooled rows."""
+    ntiles = nslots + n_cap // TILE_CAP + 1
+    return ntiles, -(-n_cap // rho) + ntiles
+
+
+class _StageRun:
+    """Device state of one enqueued stage (kept alive for the graph)."""
+
+    def __init__(self, si, cfg, n_cap, n_dev):
+        self.si, self.cfg, self.n_cap, self.n_dev = si, cfg, n_cap, n_dev
+
+
 class Backbone:
     """Device-resident backbone forward.  Parameters are drawn with the
     reference's init_params (bit-identical host RNG) and uploaded once."""
@@ -78,10 +100,13 @@ class Backbone:
             raise ConfigError("the reference pool preserves width: all stages share d_model")
         self._w = [p.device_weights() for p in self.params]
         self.last_trace = []
+        self._graphs = None
 
-    def bucketize(self, coords, cfg: StageConfig):
-        """f3d_voxel_hash + f3d_psh_assign on (n,3) f64 device coords."""
-        n = coords.shape[0]
+    # ------------------------------------------------------------ pieces
+    def bucketize(self, coords, cfg: StageConfig, n_cap=None, n_dev=None):
+        """f3d_voxel_hash + f3d_psh_assign on (n,3) f64 device coords; no
+        read-back.  Returns (assignment, stats int64[7], info int32[4])."""
+        n = coords.shape[0] if n_cap is None else n_cap
         hc = HashConfig(cfg.kind, K=cfg.K, S_div=cfg.S_div)
         vox32 = L.empty((n, 3), torch.int32)
         home = L.empty((n,), torch.int32)
@@ -90,90 +115,252 @@ class Backbone:
         org = (L._F64 * 3)(0.0, 0.0, 0.0)
         L.call("f3d_voxel_hash", L.ptr(coords), None, n, 1, org, float(cfg.voxel), hc.kind_code,
                cfg.K, cfg.S_div, hc.bits_per_axis, L.ptr(vox32), L.ptr(home), L.ptr(stats),
-               L.ptr(ws), L.stream())
+               L.ptr(ws), L.ptr(n_dev), L.stream())
         ids, offs, counts, base, dest, info = _run_psh(vox32, home, None, 1, n, hc, cfg.S,
-                                                       default_probe_schedule())
-        host = torch.cat([stats, counts.to(torch.int64), info.to(torch.int64)]).cpu().numpy()
-        raise_range(host[:7], hc.bits_per_axis)
-        counts_h = host[7:7 + cfg.K + 1]
+                                                       default_probe_schedule(), n_dev=n_dev)
         a = BucketAssignment(ids, offs, counts, base, cfg.S, cfg.K,
                              _dev={"id": ids, "off": offs, "counts": counts, "base": base,
                                    "batch": None, "dest": dest, "info": info})
-        return a, counts_h, int(host[7 + cfg.K + 1])
+        return a, stats, info
+
+    def _stage_body(self, r: _StageRun, C, X):
+        """Scatter -> R rounds -> (pool) for one stage whose bucketing is in
+        r.asg.  Returns the next stage's (X, C, n_cap, n_dev)."""
+        cfg, si, n, n_dev = r.cfg, r.si, r.n_cap, r.n_dev
+        a = r.asg
+        with record_function(f"stage{si}.scatter"):
+            dest = a._dev["dest"]
+            d = X.shape[1]
+            Xf = X if X.dtype == torch.float32 else X.to(torch.float32)
+            Xf = Xf.contiguous()
+            F = torch.empty((n, d), dtype=torch.float32, device=C.device)
+            Cs = torch.empty((n, 3), dtype=torch.float64, device=C.device)
+            L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F), L.ptr(n_dev),
+                   L.stream())
+            L.call("f3d_scatter_rows", L.ptr(C), L.ptr(dest), n, 24, L.ptr(Cs), L.ptr(n_dev),
+                   L.stream())
+        with record_function(f"stage{si}.plan"):
+            nb_cap = cfg.K + -(-n // cfg.S)
+            if cfg.W > nb_cap:
+                raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb_cap})")
+            cd, bd = a._dev["counts"], a._dev["base"]
+            qs = qstep_for(cfg.d_model // cfg.n_heads)
+            r.plans = [DeviceRoundPlan(cd, bd, cfg.K, cfg.S, nb_cap, cfg.W, cfg.stride, cfg.shift,
+                                       t, n, qstep=qs) for t in range(cfg.rounds)]
+            r.runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
+                                   weights=self._w[si], plans=r.plans, n_dev=n_dev)
+        with record_function(f"stage{si}.run"):
+            r.runner.run(F)
+        r.F, r.Cs = F, Cs
+        if not cfg.pool_rho:
+            return F, Cs, n, n_dev
+        with record_function(f"stage{si}.pool"):
+            rho = cfg.pool_rho
+            nslots = cfg.K + 1
+            nt_cap, np_cap = pool_capacity(n, nslots, rho)
+            buf = L.empty((3 * nt_cap + 2,), torch.int32)
+            tstart, tm, tout = buf[:nt_cap], buf[nt_cap:2 * nt_cap], buf[2 * nt_cap:3 * nt_cap]
+            totals = buf[3 * nt_cap:]
+            L.call("f3d_plan_pool", L.ptr(cd), L.ptr(bd), nslots, TILE_CAP, rho, L.ptr(tstart),
+                   L.ptr(tm), L.ptr(tout), L.ptr(totals), L.stream())
+            plan = _CapPlan(tstart, tm, tout, nt_cap, np_cap)
+            members, sizes, _, _, _, flags = _build(Cs, plan, rho, ntiles_dev=totals[0:1])
+            r.pool_flags = flags
+            r.pool_totals = totals
+            Xn = _reduce(F, members, sizes, np_cap, rho, "mean", npool_dev=totals[1:2])
+            Cn = _reduce(Cs, members, sizes, np_cap, rho, "mean", npool_dev=totals[1:2])
+        return Xn, Cn, np_cap, totals[1:2]
+
+    def _enqueue_bucketize0(self, C):
+        cfg = self.stages[0]
+        r = _StageRun(0, cfg, C.shape[0], None)
+        with record_function("stage0.bucketize"):
+            r.asg, r.stats, r.info = self.bucketize(C, cfg)
+        return r
+
+    def _enqueue_rest(self, r0: _StageRun, C, X):
+        """Everything after stage-0 bucketing; returns (X, C, n_dev, runs)."""
+        runs = [r0]
+        X, C, n_cap, n_dev = self._stage_body(r0, C, X)
+        for si in range(1, len(self.stages)):
+            cfg = self.stages[si]
+            r = _StageRun(si, cfg, n_cap, n_dev)
+            with record_function(f"stage{si}.bucketize"):
+                r.asg, r.stats, r.info = self.bucketize(C, cfg, n_cap, n_dev)
+            runs.append(r)
+            X, C, n_cap, n_dev = self._stage_body(r, C, X)
+        return X, C, n_dev, runs
+
+    # ------------------------------------------------------------ checks
+    @staticmethod
+    def _status_vector(runs, n_dev):
+        """One int64 device vector holding every error word and the final
+        row count, so the host reads it with a single copy."""
+        parts = []
+        for r in runs:
+            parts.append(r.stats)
+            parts.append(r.info.to(torch.int64))
+            parts.append(torch.stack([p.live[3] for p in r.plans]).to(torch.int64))
+            parts.append(r.pool_flags.to(torch.int64) if hasattr(r, "pool_flags")
+                         else torch.zeros(1, dtype=torch.int64, device=r.stats.device))
+        parts.append(n_dev.to(torch.int64) if n_dev is not None
+                     else torch.full((1,), runs[-1].n_cap, dtype=torch.int64,
+                                     device=runs[-1].stats.device))
+        return torch.cat(parts)
+
+    def _check(self, status_h, runs):
+        """Raise the reference exceptions from the status words (same
+        conditions and messages as bw/hashing.py:60-75, bw/attention.py:104,
+        bw/pooling.py validate); returns the final row count."""
+        o = 0
+        for r in runs:
+            cfg = r.cfg
+            stats, info = status_h[o:o + 7], status_h[o + 7:o + 11]
+            o += 11
+            live3 = status_h[o:o + cfg.rounds]
+            o += cfg.rounds
+            pflags = int(status_h[o])
+            o += 1
+            raise_range(stats, HashConfig(cfg.kind, K=cfg.K, S_div=cfg.S_div).bits_per_axis)
+            if info[2]:
+                raise ConfigError(f"PSH input error (code {int(info[2])})")
+            if (live3 & 1).any():
+                raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets")
+            if (live3 & 6).any():
+                raise RuntimeError("attention planner capacity exceeded (internal error)")
+            for bit, msg in _FLAG_MSGS:
+                if pflags & bit:
+                    from .errors import IntegrityError
+                    raise IntegrityError(msg)
+        return int(status_h[o])
+
+    def _trace(self, runs):
+        trace = []
+        for r in runs:
+            counts_h = r.asg._dev["counts"].cpu().numpy().astype(np.int64)
+            n = int(counts_h.sum())
+            trace.append(StageTrace(n, counts_h, r.asg, r.runner.attention_flops(),
+                                    int(r.info[0].item())))
+        return trace
+
+    # ------------------------------------------------------------ eager
+    def forward(self, coords, feats, keep_trace=False):
+        """coords (n,3) float64, feats (n,d) float32/bf16 CUDA tensors.
+        Returns (features, coords) of the last stage in its scattered order.
+        The whole forward is enqueued first; the host then reads one status
+        vector (one sync) and raises if any stage flagged an error."""
+        C = coords.to(torch.float64).contiguous()
+        ev = getattr(self, "_feat_event", None)
+        r0 = self._enqueue_bucketize0(C)
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)   # features uploaded (side stream)
+            self._feat_event = None
+        X, Cn, n_dev, runs = self._enqueue_rest(r0, C, feats)
+        status = self._status_vector(runs, n_dev).cpu().numpy()
+        n_out = self._check(status, runs)
+        self.last_trace = self._trace(runs) if keep_trace else []
+        return X[:n_out], Cn[:n_out]
+
+    # ------------------------------------------------------------ graphs
+    def capture(self, n, feat_dtype=torch.bfloat16):
+        """Capture the forward for n-point inputs into two CUDA graphs:
+        g0 = stage-0 bucketing (reads only the coordinates) and g1 = the
+        rest.  Inputs are the static buffers ``graph_coords`` (n,3) f64 and
+        ``graph_feats`` (n,d); replay with ``forward_graph``."""
+        dev = L.device()
+        d = self.stages[0].d_model
+        self.graph_coords = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.graph_feats = torch.zeros((n, d), dtype=feat_dtype, device=dev)
+        # a real scene to warm up (grid attributes, cuBLAS handles/workspaces)
+        rng = np.random.default_rng(0)
+        self.graph_coords.copy_(torch.from_numpy(rng.random((n, 3))))
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                r0 = self._enqueue_bucketize0(self.graph_coords)
+                self._enqueue_rest(r0, self.graph_coords, self.graph_feats)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        pool = torch.cuda.graph_pool_handle()
+        g0, g1 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g0, pool=pool):
+            r0 = self._enqueue_bucketize0(self.graph_coords)
+        with torch.cuda.graph(g1, pool=pool):
+            X, Cn, n_dev, runs = self._enqueue_rest(r0, self.graph_coords, self.graph_feats)
+            status = self._status_vector(runs, n_dev)
+            out_bf16 = X.to(torch.bfloat16)
+        self._graphs = {"n": n, "g0": g0, "g1": g1, "X": X, "C": Cn, "runs": runs,
+                        "status": status, "out_bf16": out_bf16, "side": torch.cuda.Stream()}
+        self._status_host = torch.empty(status.shape, dtype=torch.int64).pin_memory()
+        return self._graphs
+
+    def replay(self):
+        """Replay both graphs on the current stream (inputs already in
+        graph_coords / graph_feats); no host synchronisation."""
+        g = self._graphs
+        g["g0"].replay()
+        g["g1"].replay()
+
+    def check_graph(self):
+        """Read the status words of the last replay (one sync); returns the
+        final row count."""
+        g = self._graphs
+        self._status_host.copy_(g["status"])
+        return self._check(self._status_host.numpy(), g["runs"])
+
+    def forward_graph(self, coords, feats):
+        """Graph-replayed forward on device inputs of the captured size."""
+        g = self._graphs
+        if g is None or coords.shape[0] != g["n"]:
+            self.capture(coords.shape[0], feats.dtype)
+            g = self._graphs
+        self.graph_coords.copy_(coords)
+        self.graph_feats.copy_(feats)
+        self.replay()
+        n_out = self.check_graph()
+        return g["X"][:n_out], g["C"][:n_out]
 
     def forward_host(self, coords_h, feats_h, out_h=None):
         """End-to-end call with HOST buffers (pinned for async copies):
-        coords (n,3) float64, feats (n,d) bf16/float32.  The feature upload
-        runs on a side stream and overlaps the first PSH; the result (last
-        stage features, bf16) is copied back into ``out_h`` (allocated pinned
-        if None) and returned with the stage-2 coordinates left on device."""
-        dev = L.device()
+        coords (n,3) float64, feats (n,d) bf16.  Coordinates are uploaded and
+        stage-0 bucketing (graph g0) starts at once; the feature upload runs
+        on a side stream under it; graph g1 then runs the rest and the last
+        stage's features (bf16, capacity rows) are copied back into the
+        pinned ``out_h`` (a buffer kept with the graphs when None).  One sync (the status read) per call.  Returns
+        (out_h[:n_out], n_out)."""
+        n = coords_h.shape[0]
+        g = self._graphs
+        if g is None or g["n"] != n or self.graph_feats.dtype != feats_h.dtype:
+            g = self.capture(n, feats_h.dtype)
         main = torch.cuda.current_stream()
-        side = getattr(self, "_side", None)
-        if side is None:
-            side = self._side = torch.cuda.Stream()
-        C = coords_h.to(dev, non_blocking=True)
+        side = g["side"]
+        self.graph_coords.copy_(coords_h, non_blocking=True)
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            X = feats_h.to(dev, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(side)
-        self._feat_event = ev
-        f, c = self.forward(C, X)
-        fb = f.to(torch.bfloat16)
-        if out_h is None or tuple(out_h.shape) != tuple(fb.shape):
-            out_h = torch.empty(fb.shape, dtype=fb.dtype).pin_memory()
-        out_h.copy_(fb, non_blocking=True)
-        X.record_stream(main)
-        return out_h, c
+            self.graph_feats.copy_(feats_h, non_blocking=True)
+        g["g0"].replay()
+        main.wait_stream(side)
+        g["g1"].replay()
+        ob = g["out_bf16"]
+        if out_h is None or tuple(out_h.shape) != tuple(ob.shape):
+            out_h = g.get("out_h")
+            if out_h is None:
+                out_h = g["out_h"] = torch.empty(ob.shape, dtype=ob.dtype).pin_memory()
+        out_h.copy_(ob, non_blocking=True)
+        self._status_host.copy_(g["status"], non_blocking=True)
+        main.synchronize()
+        n_out = self._check(self._status_host.numpy(), g["runs"])
+        return out_h[:n_out], n_out
 
-    def forward(self, coords, feats, keep_trace=False):
-        """coords (n,3) float64, feats (n,d) float32/bf16 CUDA tensors.
-        Returns (features, coords) of the last stage in its scattered order."""
-        C = coords.to(torch.float64).contiguous()
-        X = feats
-        trace = []
-        for si, cfg in enumerate(self.stages):
-            n = C.shape[0]
-            with record_function(f"stage{si}.bucketize"):
-                a, counts_h, sweeps = self.bucketize(C, cfg)
-            base_h = np.zeros_like(counts_h)
-            base_h[1:] = np.cumsum(counts_h[:-1])
-            with record_function(f"stage{si}.scatter"):
-                ev = getattr(self, "_feat_event", None)
-                if ev is not None:
-                    torch.cuda.current_stream().wait_event(ev)   # features uploaded
-                    self._feat_event = None
-                dest = a._dev["dest"]
-                d = X.shape[1]
-                Xf = X.to(torch.float32).contiguous()
-                F = torch.empty((n, d), dtype=torch.float32, device=C.device)
-                Cs = torch.empty_like(C)
-                L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F), L.stream())
-                L.call("f3d_scatter_rows", L.ptr(C), L.ptr(dest), n, 24, L.ptr(Cs), L.stream())
-            with record_function(f"stage{si}.plan"):
-                nb = cfg.K + -(-int(counts_h[cfg.K]) // cfg.S)
-                if cfg.W > nb:
-                    raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb})")
-                cd, bd = a._dev["counts"], a._dev["base"]
-                qs = qstep_for(cfg.d_model // cfg.n_heads)
-                plans = [DeviceRoundPlan(cd, bd, cfg.K, cfg.S, nb, cfg.W, cfg.stride, cfg.shift,
-                                         t, n, qstep=qs) for t in range(cfg.rounds)]
-                runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
-                                     weights=self._w[si], plans=plans)
-            with record_function(f"stage{si}.run"):
-                runner.run(F)
-            if keep_trace:
-                trace.append(StageTrace(n, counts_h, a, runner.attention_flops(), sweeps))
-            if cfg.pool_rho:
-                with record_function(f"stage{si}.pool"):
-                    X, C, _ = pool_device(F, Cs, counts_h, base_h, cfg.K, cfg.S, 1, cfg.pool_rho,
-                                          "mean", check=False, assignment=False,
-                                          dev_counts=(a._dev["counts"], a._dev["base"]))
-            else:
-                X, C = F, Cs
-        self.last_trace = trace
-        return X, C
+
+class _CapPlan:
+    """Pool tile table sized for capacity; the device totals hold the
+    true tile / pooled-row counts."""
+
+    def __init__(self, tile_start, tile_m, tile_out, ntiles, npool):
+        self.tile_start, self.tile_m, self.tile_out = tile_start, tile_m, tile_out
+        self.ntiles, self.npool = ntiles, npool
 
 
 def backbone_forward(coords, feats, stages=None):

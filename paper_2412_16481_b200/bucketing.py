@@ -287,8 +287,9 @@ def _prepare(voxels, batch_id, cfg: HashConfig, S: int):
 
 
 def _run_psh(vox32, home, b32, nb, n, cfg: HashConfig, S: int, probes: ProbeSchedule,
-             max_sweeps: int = DEFAULT_MAX_SWEEPS):
-    """Launch f3d_psh_assign; returns int32 device (id, off, counts, base, dest, info)."""
+             max_sweeps: int = DEFAULT_MAX_SWEEPS, n_dev=None):
+    """Launch f3d_psh_assign; returns int32 device (id, off, counts, base, dest, info).
+    n_dev: optional device point count <= n (sync-free pipelines)."""
     table, P = probes.device_table()
     W = cfg.K + 1
     ids = L.empty((n,), torch.int32)
@@ -302,7 +303,7 @@ def _run_psh(vox32, home, b32, nb, n, cfg: HashConfig, S: int, probes: ProbeSche
     L.call("f3d_psh_assign", L.ptr(vox32), L.ptr(home), L.ptr(b32), n, nb, cfg.K, S,
            cfg.kind_code, cfg.S_div, cfg.bits_per_axis, int(cfg.div_overflow == "error"),
            table.ctypes.data_as(L._P), P, max_sweeps, L.ptr(ids), L.ptr(offs), L.ptr(counts),
-           L.ptr(base), L.ptr(dest), L.ptr(info), L.ptr(ws), ws_bytes, L.stream())
+           L.ptr(base), L.ptr(dest), L.ptr(info), L.ptr(ws), ws_bytes, L.ptr(n_dev), L.stream())
     return ids, offs, counts, base, dest, info
 
 
@@ -386,7 +387,8 @@ def scatter(features, assignment: BucketAssignment):
     out = torch.empty_like(f)
     rb = _row_bytes(f)
     if f.shape[0] and rb % 4 == 0:
-        L.call("f3d_scatter_rows", L.ptr(f), L.ptr(dest), f.shape[0], rb, L.ptr(out), L.stream())
+        L.call("f3d_scatter_rows", L.ptr(f), L.ptr(dest), f.shape[0], rb, L.ptr(out), None,
+               L.stream())
     elif f.shape[0]:
         raise ConfigError("row size must be a multiple of 4 bytes on the GPU")
     perm = dest.to(torch.int64)
@@ -402,5 +404,6 @@ def gather(scattered, assignment: BucketAssignment):
     out = torch.empty_like(f)
     rb = _row_bytes(f)
     if f.shape[0]:
-        L.call("f3d_gather_rows", L.ptr(f), L.ptr(dest), f.shape[0], rb, L.ptr(out), L.stream())
+        L.call("f3d_gather_rows", L.ptr(f), L.ptr(dest), f.shape[0], rb, L.ptr(out), None,
+               L.stream())
     return L.out(out, host)

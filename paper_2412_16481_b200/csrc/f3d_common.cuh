@@ -110,4 +110,12 @@ __device__ __forceinline__ T warp_sum(T v) {
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 __device__ __forceinline__ int cdiv_dev(int a, int b) { return (a + b - 1) / b; }
 
+// Row count of a launch sized for capacity n: min(n, *n_dev) when the count
+// lives on the device (sync-free / graph-captured pipelines), else n.
+__device__ __forceinline__ int64_t dyn_n(int64_t n, const int32_t* n_dev) {
+    if (n_dev == nullptr) return n;
+    const int64_t d = *n_dev;
+    return d < n ? (d < 0 ? 0 : d) : n;
+}
+
 }  // namespace f3d

@@ -161,10 +161,11 @@ __global__ void morton_kernel(const int64_t* __restrict__ vox, int64_t n, int bi
 
 // Fused pass 1: voxelize + per-batch axis minimum (voxels are not stored).
 __global__ void fused_min_kernel(const double* __restrict__ coords,
-                                 const int32_t* __restrict__ batch, int64_t n, int nbatch,
-                                 Origin org, double vs, int64_t* ws_min) {
+                                 const int32_t* __restrict__ batch, int64_t n,
+                                 const int32_t* n_dev, int nbatch, Origin org, double vs,
+                                 int64_t* ws_min) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool ok = i < n;
+    const bool ok = i < dyn_n(n, n_dev);
     long long v[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
     int b = 0;
     if (ok) {
@@ -180,12 +181,13 @@ __global__ void fused_min_kernel(const double* __restrict__ coords,
 
 // Fused pass 2: re-voxelize, remap by the batch minimum, range stats, hash.
 __global__ void fused_hash_kernel(const double* __restrict__ coords,
-                                  const int32_t* __restrict__ batch, int64_t n, int nbatch,
-                                  Origin org, double vs, const int64_t* __restrict__ ws_min,
-                                  HashArgs ha, int32_t* __restrict__ home,
-                                  int32_t* __restrict__ vox32, int64_t* stats) {
+                                  const int32_t* __restrict__ batch, int64_t n,
+                                  const int32_t* n_dev, int nbatch, Origin org, double vs,
+                                  const int64_t* __restrict__ ws_min, HashArgs ha,
+                                  int32_t* __restrict__ home, int32_t* __restrict__ vox32,
+                                  int64_t* stats) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = i < n;
+    const bool valid = i < dyn_n(n, n_dev);
     long long v[3] = {0, 0, 0};
     if (valid) {
         int b = (batch && nbatch > 1) ? batch[i] : 0;
@@ -260,18 +262,20 @@ extern "C" int f3d_voxel_hash(const double* coords, const int32_t* batch, int64_
                               int32_t nbatch, const double* origin3_host, double voxel_size,
                               int kind, int32_t K, int64_t S_div, int bits, int32_t* vox32_out,
                               int32_t* home_out, int64_t* stats_out, int64_t* ws,
-                              void* stream) {
+                              const int32_t* n_dev, void* stream) {
     if (n < 0 || nbatch < 1 || !(voxel_size > 0) || bad_hash_cfg(kind, K, S_div, bits))
         return F3D_ERR_CONFIG;
+    if (n_dev && nbatch > 1) return F3D_ERR_CONFIG;
     cudaStream_t st = (cudaStream_t)stream;
     Origin o{{origin3_host[0], origin3_host[1], origin3_host[2]}};
     init_stats_kernel<<<nblk(3 * nbatch + 7), kThreads, 0, st>>>(stats_out, ws, 3 * nbatch);
     if (n > 0) {
-        fused_min_kernel<<<nblk(n), kThreads, 0, st>>>(coords, batch, n, nbatch, o, voxel_size,
-                                                        ws);
+        fused_min_kernel<<<nblk(n), kThreads, 0, st>>>(coords, batch, n, n_dev, nbatch, o,
+                                                        voxel_size, ws);
         HashArgs ha{HashParams{kind, K, S_div, bits, 0}, 1};
-        fused_hash_kernel<<<nblk(n), kThreads, 0, st>>>(coords, batch, n, nbatch, o, voxel_size,
-                                                         ws, ha, home_out, vox32_out, stats_out);
+        fused_hash_kernel<<<nblk(n), kThreads, 0, st>>>(coords, batch, n, n_dev, nbatch, o,
+                                                         voxel_size, ws, ha, home_out, vox32_out,
+                                                         stats_out);
     }
     F3D_LAUNCH_CHECK();
     return F3D_OK;

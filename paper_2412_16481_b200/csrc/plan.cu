@@ -37,7 +37,7 @@ __device__ int block_excl_scan(int v, int& total, int* sh /* >= 33 ints */) {
 }
 
 __global__ void __launch_bounds__(kThreads) plan_round_kernel(
-    const int32_t* __restrict__ counts, const int32_t* __restrict__ base, int K, int S, int nb,
+    const int32_t* __restrict__ counts, const int32_t* __restrict__ base, int K, int S, int nb_cap,
     int W, int stride, int off, int nscopes, int32_t* scope_seg, int32_t* scope_nseg,
     int32_t* seg_start, int32_t* seg_vstart, int32_t* scope_len, int32_t* scope_order,
     int32_t* work, int max_work, int qstep, int32_t* live) {
@@ -46,6 +46,9 @@ __global__ void __launch_bounds__(kThreads) plan_round_kernel(
     const int span = W * stride;
     const int r = counts[K];
     const int rb = base[K];
+    // table size from the device counts: K buckets + ceil(r/S) recycle chunks
+    // (bw/bucketing.py:147-166); nb_cap (host bound) sized the scope arrays
+    const int nb = K + (r + S - 1) / S;
     if (threadIdx.x == 0) s_maxlen = 0;
     __syncthreads();
     int carry_live = 0, carry_work = 0;
@@ -104,6 +107,9 @@ __global__ void __launch_bounds__(kThreads) plan_round_kernel(
         live[0] = min(carry_work, max_work);
         live[1] = carry_live;
         live[2] = s_maxlen;
+        // 1: window_w exceeds num_buckets (bw/attention.py:104); 2: table
+        // larger than the capacity the host planned for; 4: work list cut
+        live[3] = (W > nb ? 1 : 0) | (nb > nb_cap ? 2 : 0) | (carry_work > max_work ? 4 : 0);
     }
 }
 
@@ -147,16 +153,16 @@ __global__ void __launch_bounds__(kThreads) plan_pool_kernel(
 
 using namespace f3d;
 
-extern "C" int f3d_plan_round(const int32_t* counts, const int32_t* base, int K, int S, int nb,
+extern "C" int f3d_plan_round(const int32_t* counts, const int32_t* base, int K, int S, int nb_cap,
                               int W, int stride, int off, int nscopes, int32_t* scope_seg,
                               int32_t* scope_nseg, int32_t* seg_start, int32_t* seg_vstart,
                               int32_t* scope_len, int32_t* scope_order, int32_t* work,
                               int max_work, int qstep, int32_t* live, void* stream) {
-    if (K < 1 || S < 1 || nb < 1 || W < 1 || stride < 1 || off < 0 || nscopes < 1 ||
+    if (K < 1 || S < 1 || nb_cap < 1 || W < 1 || stride < 1 || off < 0 || nscopes < 1 ||
         max_work < 0 || qstep < 16)
         return F3D_ERR_CONFIG;
     plan::plan_round_kernel<<<1, plan::kThreads, 0, (cudaStream_t)stream>>>(
-        counts, base, K, S, nb, W, stride, off, nscopes, scope_seg, scope_nseg, seg_start,
+        counts, base, K, S, nb_cap, W, stride, off, nscopes, scope_seg, scope_nseg, seg_start,
         seg_vstart, scope_len, scope_order, work, max_work, qstep, live);
     F3D_LAUNCH_CHECK();
     return F3D_OK;

@@ -45,6 +45,7 @@ struct Args {
     const int32_t* tile_m;      // rows in tile t
     const int32_t* tile_out;    // first pooled row of tile t
     int ntiles;
+    const int32_t* ntiles_dev;  // nullable: device tile count (<= ntiles)
     int rho;
     int32_t* sub_out;           // (N) tile-local sub id per row (nullable)
     int32_t* members;           // (npool, rho) global row ids, -1 padded
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x * kWarpsPerCta + warp;
-    if (t >= A.ntiles) return;
+    if (t >= dyn_n(A.ntiles, A.ntiles_dev)) return;
     WarpSmem& S = smem_all[warp];
     const int r0 = A.tile_start[t];
     const int m = A.tile_m[t];
@@ -373,10 +374,11 @@ __device__ __forceinline__ void st_f(double* p, double v) { *p = v; }
 template <typename T>
 __global__ void pool_reduce_kernel(const T* __restrict__ x, int64_t ldx, int d,
                                    const int32_t* __restrict__ members,
-                                   const int32_t* __restrict__ sizes, int64_t npool, int rho,
-                                   int op, T* __restrict__ out, int64_t ldo) {
+                                   const int32_t* __restrict__ sizes, int64_t npool,
+                                   const int32_t* npool_dev, int rho, int op,
+                                   T* __restrict__ out, int64_t ldo) {
     using A = typename RAcc<T>::type;
-    const int64_t tot = npool * d;
+    const int64_t tot = dyn_n(npool, npool_dev) * d;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = t / d;
@@ -424,12 +426,12 @@ extern "C" int f3d_pool_build(const double* coords, const int32_t* tile_start,
                               const int32_t* tile_m, const int32_t* tile_out, int ntiles, int rho,
                               int32_t* sub_out, int32_t* members, int32_t* sizes_out,
                               int32_t* seeds_out, int32_t* passes_out, int32_t* flags,
-                              void* stream) {
+                              const int32_t* ntiles_dev, void* stream) {
     if (rho < 1 || rho > 64 || ntiles < 0) return F3D_ERR_CONFIG;
     cudaStream_t st = (cudaStream_t)stream;
     F3D_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
     if (ntiles == 0) return F3D_OK;
-    pool::Args A{coords, tile_start, tile_m, tile_out, ntiles, rho, sub_out, members, sizes_out,
+    pool::Args A{coords, tile_start, tile_m, tile_out, ntiles, ntiles_dev, rho, sub_out, members, sizes_out,
                  seeds_out, passes_out, flags};
     const int grid = (ntiles + pool::kWarpsPerCta - 1) / pool::kWarpsPerCta;
     const size_t smem = sizeof(pool::WarpSmem) * pool::kWarpsPerCta;
@@ -446,7 +448,8 @@ extern "C" int f3d_pool_build(const double* coords, const int32_t* tile_start,
 
 extern "C" int f3d_pool_reduce(const void* x, int dtype, int64_t ldx, int d,
                                const int32_t* members, const int32_t* sizes, int64_t npool,
-                               int rho, int op, void* out, int64_t ldo, void* stream) {
+                               int rho, int op, void* out, int64_t ldo, const int32_t* npool_dev,
+                               void* stream) {
     if (d < 1 || rho < 1 || op < 0 || op > 3 || npool < 0) return F3D_ERR_CONFIG;
     if (npool == 0) return F3D_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -455,13 +458,13 @@ extern "C" int f3d_pool_reduce(const void* x, int dtype, int64_t ldx, int d,
     if (g > (int64_t)f3d_num_sms() * 32) g = (int64_t)f3d_num_sms() * 32;
     if (dtype == 2)
         pool::pool_reduce_kernel<double><<<(unsigned)g, 256, 0, st>>>(
-            (const double*)x, ldx, d, members, sizes, npool, rho, op, (double*)out, ldo);
+            (const double*)x, ldx, d, members, sizes, npool, npool_dev, rho, op, (double*)out, ldo);
     else if (dtype == 1)
         pool::pool_reduce_kernel<float><<<(unsigned)g, 256, 0, st>>>(
-            (const float*)x, ldx, d, members, sizes, npool, rho, op, (float*)out, ldo);
+            (const float*)x, ldx, d, members, sizes, npool, npool_dev, rho, op, (float*)out, ldo);
     else if (dtype == 0)
         pool::pool_reduce_kernel<__nv_bfloat16><<<(unsigned)g, 256, 0, st>>>(
-            (const __nv_bfloat16*)x, ldx, d, members, sizes, npool, rho, op,
+            (const __nv_bfloat16*)x, ldx, d, members, sizes, npool, npool_dev, rho, op,
             (__nv_bfloat16*)out, ldo);
     else
         return F3D_ERR_CONFIG;

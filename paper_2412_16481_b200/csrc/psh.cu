@@ -47,6 +47,7 @@ struct Params {
     const int32_t* home;   // (n)
     const int32_t* batch;  // (n) or null
     int n, nbatch, K, S, P, max_sweeps;
+    const int32_t* n_dev;  // nullable: device point count (<= n), single batch only
     HashParams hp;
     int vmax;
     int8_t probe[kMaxProbes * 3];
@@ -187,7 +188,7 @@ struct TileInfo {
     int p0, p1, b;
 };
 
-__device__ __forceinline__ TileInfo tile_info(const Params& P_, bool multi, int t) {
+__device__ __forceinline__ TileInfo tile_info(const Params& P_, bool multi, int t, int n) {
     TileInfo ti;
     if (multi) {
         ti.p0 = __ldcg(P_.tile_p0 + t);
@@ -195,7 +196,7 @@ __device__ __forceinline__ TileInfo tile_info(const Params& P_, bool multi, int 
         ti.p1 = min(ti.p0 + kTile, __ldcg(P_.bstart + ti.b + 1));
     } else {
         ti.p0 = t * kTile;
-        ti.p1 = min(ti.p0 + kTile, P_.n);
+        ti.p1 = min(ti.p0 + kTile, n);
         ti.b = 0;
     }
     return ti;
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const bool multi = P_.nbatch > 1;
+    const int n = (int)dyn_n(P_.n, P_.n_dev);
     const int K = P_.K;
     const int W = K + 1;
     const int nbins = multi ? max(W, P_.nbatch) : W;
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
         grid.sync();
         ntiles = __ldcg(P_.btile + B);
     } else {
-        ntiles = cdiv_dev(P_.n, kTile);
+        ntiles = cdiv_dev(n, kTile);
     }
 
     // ------------------------------------------------------------ sweeps
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
         // Phase A: decide + per-tile histogram
         int changed = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const TileInfo ti = tile_info(P_, multi, t);
+            const TileInfo ti = tile_info(P_, multi, t, n);
             zero_hist(sh, hwords);
             __syncthreads();
             int key[kPerLane];
@@ -418,7 +420,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
         grid.sync();
         // Phase C: in-tile stable ranks -> offsets; S-th taker -> T
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const TileInfo ti = tile_info(P_, multi, t);
+            const TileInfo ti = tile_info(P_, multi, t, n);
             zero_hist(sh, hwords);
             __syncthreads();
             int key[kPerLane];
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
             int32_t* ctr = reinterpret_cast<int32_t*>(sh);
             for (int b = 0; b < P_.nbatch; ++b) {
                 const int pb0 = multi ? __ldcg(P_.bstart + b) : 0;
-                const int pb1 = multi ? __ldcg(P_.bstart + b + 1) : P_.n;
+                const int pb1 = multi ? __ldcg(P_.bstart + b + 1) : n;
                 sequential_batch(P_, b, pb0, pb1, ctr, probe);
             }
         }
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     }
     grid.sync();
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const TileInfo ti = tile_info(P_, multi, t);
+        const TileInfo ti = tile_info(P_, multi, t, n);
         const int32_t* bb = P_.base + (int64_t)ti.b * W;
         for (int p = ti.p0 + tid; p < ti.p1; p += kThreads) {
             const int i = multi ? __ldcg(P_.orig + p) : p;
@@ -553,6 +555,7 @@ extern "C" size_t f3d_psh_workspace_size(int64_t n, int32_t nbatch, int32_t K) {
 // histogram limit: the reference loop verbatim, counters in global memory.
 __global__ void psh_sequential_kernel(psh::Params P_) {
     const int W = P_.K + 1;
+    P_.n = (int)dyn_n(P_.n, P_.n_dev);
     for (int s = 0; s < P_.nbatch * W; ++s) P_.counts[s] = 0;
     for (int i = 0; i < P_.n; ++i) {
         const int b = P_.batch ? P_.batch[i] : 0;
@@ -595,11 +598,12 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
                               const int8_t* probe_offsets_host, int32_t P, int32_t max_sweeps,
                               int32_t* bucket_id, int32_t* bucket_offset, int32_t* counts,
                               int32_t* base, int32_t* dest, int32_t* info_out, void* ws,
-                              size_t ws_bytes, void* stream) {
+                              size_t ws_bytes, const int32_t* n_dev, void* stream) {
     if (n <= 0) return F3D_ERR_EMPTY;
     if (n >= INT_MAX / 2 || K < 1 || S < 1 || nbatch < 1 || P < 0 || P > psh::kMaxProbes ||
         bits < 1 || bits > 21 || S_div < 1 || kind < 0 || kind > 3)
         return F3D_ERR_CONFIG;
+    if (n_dev && nbatch > 1) return F3D_ERR_CONFIG;
     if (max_sweeps < 1) max_sweeps = 1;
     if (max_sweeps > psh::kMaxSweepsCap) max_sweeps = psh::kMaxSweepsCap;
     const psh::WsLayout L = psh::layout(n, nbatch, K, max_sweeps);
@@ -612,6 +616,7 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
     p.home = home;
     p.batch = nbatch > 1 ? batch : nullptr;
     p.n = (int)n;
+    p.n_dev = n_dev;
     p.nbatch = nbatch;
     p.K = K;
     p.S = S;

@@ -13,9 +13,10 @@ constexpr int kThreads = 256;
 // contiguously so both the read and the write side are coalesced per row.
 template <typename V, bool kScatter>
 __global__ void move_rows_kernel(const V* __restrict__ src, const int32_t* __restrict__ idx,
-                                 int64_t n, int64_t vec_per_row, V* __restrict__ dst) {
+                                 int64_t n, const int32_t* n_dev, int64_t vec_per_row,
+                                 V* __restrict__ dst) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t tot = n * vec_per_row;
+    const int64_t tot = dyn_n(n, n_dev) * vec_per_row;
     if (t >= tot) return;
     const int64_t r = t / vec_per_row;
     const int64_t k = t - r * vec_per_row;
@@ -25,8 +26,8 @@ __global__ void move_rows_kernel(const V* __restrict__ src, const int32_t* __res
 }
 
 template <bool kScatter>
-int move_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst,
-              cudaStream_t st) {
+int move_rows(const void* src, const int32_t* idx, int64_t n, const int32_t* n_dev,
+              int64_t row_bytes, void* dst, cudaStream_t st) {
     if (n < 0 || row_bytes <= 0 || (row_bytes & 3)) return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
     const bool v16 = ((row_bytes & 15) == 0) && ((uintptr_t)src & 15) == 0 &&
@@ -35,12 +36,12 @@ int move_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
         const int64_t vpr = row_bytes / 16;
         const int64_t tot = n * vpr;
         move_rows_kernel<int4, kScatter><<<(unsigned)((tot + kThreads - 1) / kThreads), kThreads,
-                                           0, st>>>((const int4*)src, idx, n, vpr, (int4*)dst);
+                                           0, st>>>((const int4*)src, idx, n, n_dev, vpr, (int4*)dst);
     } else {
         const int64_t vpr = row_bytes / 4;
         const int64_t tot = n * vpr;
         move_rows_kernel<int, kScatter><<<(unsigned)((tot + kThreads - 1) / kThreads), kThreads, 0,
-                                          st>>>((const int*)src, idx, n, vpr, (int*)dst);
+                                          st>>>((const int*)src, idx, n, n_dev, vpr, (int*)dst);
     }
     F3D_LAUNCH_CHECK();
     return F3D_OK;
@@ -131,13 +132,13 @@ __global__ void validate_seen_kernel(const int32_t* __restrict__ seen, int64_t n
 using namespace f3d;
 
 extern "C" int f3d_scatter_rows(const void* src, const int32_t* dest, int64_t n,
-                                int64_t row_bytes, void* dst, void* stream) {
-    return rows::move_rows<true>(src, dest, n, row_bytes, dst, (cudaStream_t)stream);
+                                int64_t row_bytes, void* dst, const int32_t* n_dev, void* stream) {
+    return rows::move_rows<true>(src, dest, n, n_dev, row_bytes, dst, (cudaStream_t)stream);
 }
 
 extern "C" int f3d_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
-                               void* dst, void* stream) {
-    return rows::move_rows<false>(src, idx, n, row_bytes, dst, (cudaStream_t)stream);
+                               void* dst, const int32_t* n_dev, void* stream) {
+    return rows::move_rows<false>(src, idx, n, n_dev, row_bytes, dst, (cudaStream_t)stream);
 }
 
 extern "C" size_t f3d_validate_workspace_size(int64_t n, int64_t nslots) {

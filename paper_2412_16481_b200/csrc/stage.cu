@@ -17,7 +17,9 @@ constexpr int kMaxPerLane = 32;   // d <= 1024
 
 // ---------------------------------------------------------------- bbox
 
-__global__ void bbox_partial_kernel(const double* __restrict__ c, int64_t n, double* part) {
+__global__ void bbox_partial_kernel(const double* __restrict__ c, int64_t n,
+                                    const int32_t* n_dev, double* part) {
+    n = dyn_n(n, n_dev);
     __shared__ double s[6][kThreads / 32];
     double mn[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, mx[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -228,11 +230,11 @@ static inline unsigned grid_for(int64_t work, int threads) {
 }
 
 extern "C" int f3d_coord_bbox(const double* coords, int64_t n, double* ws, double* lo_ext,
-                              void* stream) {
+                              const int32_t* n_dev, void* stream) {
     if (n < 1) return F3D_ERR_EMPTY;
     cudaStream_t st = (cudaStream_t)stream;
     const int parts = (int)std::min<int64_t>((n + 1023) / 1024, 296);
-    stage::bbox_partial_kernel<<<parts, stage::kThreads, 0, st>>>(coords, n, ws);
+    stage::bbox_partial_kernel<<<parts, stage::kThreads, 0, st>>>(coords, n, n_dev, ws);
     stage::bbox_final_kernel<<<1, 32, 0, st>>>(ws, parts, lo_ext);
     F3D_LAUNCH_CHECK();
     return F3D_OK;

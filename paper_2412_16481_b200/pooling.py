@@ -113,7 +113,8 @@ class DeviceTilePlan:
                L.ptr(self.totals), L.stream())
 
 
-def _build(coords_dev, plan: TilePlan, rho: int, want_sub=False, want_seeds=False):
+def _build(coords_dev, plan: TilePlan, rho: int, want_sub=False, want_seeds=False,
+           ntiles_dev=None):
     n = coords_dev.shape[0]
     members = L.empty((max(1, plan.npool), rho), torch.int32)
     sizes = L.empty((max(1, plan.npool),), torch.int32)
@@ -123,11 +124,11 @@ def _build(coords_dev, plan: TilePlan, rho: int, want_sub=False, want_seeds=Fals
     flags = L.empty((1,), torch.int32)
     L.call("f3d_pool_build", L.ptr(coords_dev), L.ptr(plan.tile_start), L.ptr(plan.tile_m),
            L.ptr(plan.tile_out), plan.ntiles, rho, L.ptr(sub), L.ptr(members), L.ptr(sizes),
-           L.ptr(seeds), L.ptr(passes), L.ptr(flags), L.stream())
+           L.ptr(seeds), L.ptr(passes), L.ptr(flags), L.ptr(ntiles_dev), L.stream())
     return members, sizes, seeds, sub, passes, flags
 
 
-def _reduce(x, members, sizes, npool, rho, reduce):
+def _reduce(x, members, sizes, npool, rho, reduce, npool_dev=None, out=None):
     if x.dtype == torch.float64:
         dt = 2
     elif x.dtype == torch.float32:
@@ -138,9 +139,11 @@ def _reduce(x, members, sizes, npool, rho, reduce):
         x = x.to(torch.float64)
         dt = 2
     x = x.contiguous()
-    out = torch.empty((npool, x.shape[1]), dtype=x.dtype, device=x.device)
+    if out is None:
+        out = torch.empty((npool, x.shape[1]), dtype=x.dtype, device=x.device)
     L.call("f3d_pool_reduce", L.ptr(x), dt, x.stride(0), x.shape[1], L.ptr(members),
-           L.ptr(sizes), npool, rho, _OP[reduce], L.ptr(out), out.stride(0), L.stream())
+           L.ptr(sizes), npool, rho, _OP[reduce], L.ptr(out), out.stride(0), L.ptr(npool_dev),
+           L.stream())
     return out
 
 

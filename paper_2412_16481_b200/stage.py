@@ -131,7 +131,7 @@ class StageRunner:
     ``run(F)`` then executes every round with no host synchronisation."""
 
     def __init__(self, coords, table, schedule: ScopeSchedule, params: StageParams, n: int,
-                 f_dtype=torch.float32, weights=None, plans=None):
+                 f_dtype=torch.float32, weights=None, plans=None, n_dev=None):
         dev = L.device()
         self.p = params
         self.n = n
@@ -145,7 +145,8 @@ class StageRunner:
         self.coords = L.to_dev(coords, torch.float64).contiguous()
         ws = L.empty((6 * 296,), torch.float64)
         self.lo_ext = L.empty((6,), torch.float64)
-        L.call("f3d_coord_bbox", L.ptr(self.coords), n, L.ptr(ws), L.ptr(self.lo_ext), L.stream())
+        L.call("f3d_coord_bbox", L.ptr(self.coords), n, L.ptr(ws), L.ptr(self.lo_ext),
+               L.ptr(n_dev), L.stream())
         d, dhid = self.d, params.d_hidden
         self.x = L.empty((n, d), torch.bfloat16)
         self.qkv = L.empty((n, 3 * d), torch.bfloat16)

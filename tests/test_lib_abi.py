@@ -39,7 +39,8 @@ def test_ctypes_table_covers_header():
 def test_config_errors_need_no_gpu():
     """Argument validation happens before any CUDA call."""
     lib = ctypes.CDLL(LIB)
-    assert lib.f3d_scatter_rows(None, None, ctypes.c_int64(4), ctypes.c_int64(6), None, None) == 1
+    assert lib.f3d_scatter_rows(None, None, ctypes.c_int64(4), ctypes.c_int64(6), None, None,
+                                None) == 1
     lib.f3d_psh_workspace_size.restype = ctypes.c_size_t
     assert lib.f3d_psh_workspace_size(ctypes.c_int64(1000), 1, 40) > 0
 
