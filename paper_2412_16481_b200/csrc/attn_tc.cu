@@ -3,18 +3,23 @@
 // Same contract as csrc/attn.cu (bw/attention.py:188-268 per scope, one launch
 // per round), FlashAttention-style with the Blackwell execution model:
 //   * persistent CTAs (one per SM) walk the (query group, head) work list; a
-//     group is NQ 128-row Q tiles (NQ = 3/2/1 for dh <= 32/64/128) that
+//     group is NQ 128-row Q tiles (NQ = 3 for head dims <= 32, else 2) that
 //     share every 64-key K/V tile;
 //   * warps 0-2 gather Q / K / V rows of the scope straight from the fixed
 //     scattered layout with cp.async into UMMA core-matrix smem tiles (a
 //     scope is up to W physical segments, so rows are gathered, not boxed);
-//     completion is signalled on mbarriers (cp.async.mbarrier.arrive);
-//   * warp 3 (one elected thread) issues tcgen05.mma: S_g = Q_g K^T and
-//     O_g = P_g V into TMEM per Q tile g, tcgen05.commit -> mbarriers;
-//   * NQ softmax warpgroups (one thread per query row = TMEM lane) copy their
-//     S row out of TMEM (freeing it for the next tile's MMA at once), run the
-//     online softmax in the exp2 domain, write P (bf16) to smem for the PV
-//     MMA, and fold O_j into register accumulators.
+//     one thread per row, completion signalled on mbarriers;
+//   * warp 3 (one thread) issues tcgen05.mma: S_g = Q_g K^T into one of two
+//     TMEM S buffers per Q tile, then O_g += P_g V with P_g read from TMEM
+//     (the softmax writes it over S_g) and O_g accumulated in TMEM across all
+//     key tiles; tcgen05.commit -> mbarriers;
+//   * NQ softmax warpgroups (thread = query row = TMEM lane) read S with
+//     tcgen05.ld, run the online softmax in the exp2 domain, and store P as
+//     bf16 back into TMEM.  The running max is only moved (and O rescaled in
+//     TMEM) when a row's max grows by more than 2^8, so almost every tile is
+//     ld S -> max -> exp -> st P with no O traffic.  When the head dim is
+//     padded (dh < DH) a ones column in V makes the PV MMA produce the row
+//     sums, so the softmax does no per-score add.
 // Shared-memory tiles use the SWIZZLE_NONE canonical layout: element (r, c)
 // of an R x C bf16 tile lives at (r/8)*16*C + (c/8)*128 + (r%8)*16 + (c%8)*2.
 #include <cuda_bf16.h>
@@ -34,13 +39,11 @@ constexpr int kBM = 128;          // rows per Q tile (TMEM lanes)
 constexpr int kBN = 64;           // keys per K/V tile
 constexpr int kLoadWarps = 3;     // warps 0-2
 constexpr int kMmaWarp = 3;       // completes warpgroup 0
-constexpr int kNst = 3;           // K/V stages
+constexpr float kRescale = 8.f;   // move the running max only when it grows by > 2^8
 
-// Q tiles per work item (one softmax warpgroup each): as many as registers
-// allow (the softmax thread keeps its 64-key S row and DH-wide O row live).
 template <int DH>
 __host__ __device__ constexpr int nq_for() {
-    return DH <= 32 ? 3 : (DH <= 64 ? 2 : 1);
+    return DH <= 32 ? 3 : 2;
 }
 template <int DH>
 __host__ __device__ constexpr int threads_for() {
@@ -65,17 +68,21 @@ struct Cfg {
     static constexpr int NQ = nq_for<DH>();
     static constexpr int kQBytes = kBM * DH * 2;        // one Q tile
     static constexpr int kKVBytes = kBN * DH * 2;       // one of K or V
-    static constexpr int kPBytes = kBM * kBN * 2;       // one P tile
-    static constexpr int kOffQ = 0;                     // 2 buffers x NQ Q tiles
-    static constexpr int kOffKV = kOffQ + 2 * NQ * kQBytes;
-    static constexpr int kOffP = kOffKV + kNst * 2 * kKVBytes;
-    static constexpr int kOffBar = kOffP + NQ * kPBytes;
-    static constexpr int kNumBars = 4 + 2 * kNst + 4 * NQ;
+    static constexpr int kBudget = 227 * 1024 - 512;
+    // K/V depth first (>= 4 stages), then a second Q buffer if it still fits
+    static constexpr int NQB = (2 * NQ * kQBytes + 4 * 2 * kKVBytes <= kBudget) ? 2 : 1;
+    static constexpr int kNstFit = (kBudget - NQB * NQ * kQBytes) / (2 * kKVBytes);
+    static constexpr int kNst = kNstFit > 6 ? 6 : kNstFit;
+    static constexpr int kOffQ = 0;
+    static constexpr int kOffKV = kOffQ + NQB * NQ * kQBytes;
+    static constexpr int kOffBar = kOffKV + kNst * 2 * kKVBytes;
+    static constexpr int kNumBars = 2 * NQB + 2 * kNst + 5 * NQ;
     static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
-    static constexpr int kTmemS = 0;                    // S of tile g, buffer b: (2g+b)*kBN
-    static constexpr int kTmemPV = 2 * NQ * kBN;        // PV of tile g: kTmemPV + g*DH
+    static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (2g+b)*kBN
+    static constexpr int kTmemO = 2 * NQ * kBN;         // O of tile g: kTmemO + g*DH
     static constexpr int kTmemCols = NQ * (2 * kBN + DH) <= 256 ? 256 : 512;
     static_assert(NQ * (2 * kBN + DH) <= 512, "TMEM budget");
+    static_assert(kNst >= 2, "K/V pipeline depth");
     static_assert(kSmem <= 227 * 1024, "smem budget");
 };
 
@@ -111,51 +118,57 @@ __device__ __forceinline__ Item decode(const Args& A, int item) {
     return it;
 }
 
-// Gather rows [v0, v0+R) of head h (real chunks only; zero-fill past m).
-template <int DH, int R>
-__device__ __forceinline__ void gather(const Args& A, const __nv_bfloat16* base, int64_t ld,
-                                       const Item& it, int v0, uint32_t dst, int tid) {
-    const int rc = A.dh >> 3;   // real 16-byte chunks per row
-    const int hcol = it.h * A.dh;
-    for (int idx = tid; idx < R * rc; idx += kLoadWarps * 32) {
-        const int r = idx / rc;
-        const int c = idx - r * rc;
-        const int vr = v0 + r;
-        const bool ok = vr < it.m;
-        const __nv_bfloat16* src = base;
-        if (ok) src = base + (int64_t)phys_row(A, it.s0, it.s1, vr) * ld + hcol + c * 8;
-        cp_async16z(dst + core_off<DH>(r, c), src, ok);
-    }
+// One row of head h (real 16-byte chunks only; zero-filled past m).
+template <int DH>
+__device__ __forceinline__ void gather_row(const Args& A, const __nv_bfloat16* base, int64_t ld,
+                                           const Item& it, int vr, uint32_t dst_row, int r) {
+    const int rc = A.dh >> 3;
+    const bool ok = vr < it.m;
+    const __nv_bfloat16* src = base;
+    if (ok) src = base + (int64_t)phys_row(A, it.s0, it.s1, vr) * ld + it.h * A.dh;
+    for (int c = 0; c < rc; ++c) cp_async16z(dst_row + core_off<DH>(r, c), src + c * 8, ok);
 }
 
 template <int DH, typename OutT>
 __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(const Args A) {
     using C = Cfg<DH>;
     constexpr int NQ = C::NQ;
+    constexpr int NQB = C::NQB;
+    constexpr int kNst = C::kNst;
     constexpr int kThreads = threads_for<DH>();
     extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
     // every barrier below completes at most one phase ahead of its waiter
-    uint64_t* q_full = bars + 0;                 // [2] loaders -> MMA (Q buffer filled)
-    uint64_t* q_empty = bars + 2;                // [2] MMA -> loaders (Q buffer consumed)
-    uint64_t* kv_full = bars + 4;                // [kNst]
-    uint64_t* kv_empty = bars + 4 + kNst;        // [kNst]
-    uint64_t* s_full = bars + 4 + 2 * kNst;      // [NQ][2] MMA -> softmax (S_g in buffer b)
-    uint64_t* p_full = s_full + 2 * NQ;          // [NQ] softmax -> MMA (P_g written, S read,
-                                                 //      previous P_g V folded)
-    uint64_t* pv_full = s_full + 3 * NQ;         // [NQ] MMA -> softmax (P_g V ready)
+    uint64_t* q_full = bars;                     // [NQB] loaders -> MMA
+    uint64_t* q_empty = q_full + NQB;            // [NQB] MMA -> loaders
+    uint64_t* kv_full = q_empty + NQB;           // [kNst]
+    uint64_t* kv_empty = kv_full + kNst;         // [kNst]
+    uint64_t* s_full = kv_empty + kNst;          // [NQ][2] MMA -> softmax (S_g in buffer b)
+    uint64_t* p_full = s_full + 2 * NQ;          // [NQ] softmax -> MMA (P_g in TMEM, O rescaled)
+    uint64_t* pv_done = p_full + NQ;             // [NQ] MMA -> softmax (O_g += P_g V done)
+    uint64_t* o_free = pv_done + NQ;             // [NQ] softmax -> MMA (O_g read out)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const int total = (A.live ? __ldg(A.live) : A.nwork) * A.H;
+    const bool ones = A.dh < DH;                 // V column dh = 1 -> O column dh = row sum
 
     // zero the operand tiles once: pad chunks (dh < DH) are never written again
     for (int i = tid; i < C::kOffBar / 16; i += kThreads)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (ones) {
+        const __nv_bfloat16 one = __float2bfloat16(1.f);
+        for (int i = tid; i < kNst * kBN; i += kThreads) {
+            const int s = i / kBN, r = i - s * kBN;
+            *reinterpret_cast<__nv_bfloat16*>(smem + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes +
+                                              core_off<DH>(r, A.dh >> 3) + (A.dh & 7) * 2) = one;
+        }
+    }
     if (tid == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NQB; ++b) {
             mbar_init(q_full + b, kLoadWarps * 32);
             mbar_init(q_empty + b, 1);
         }
@@ -167,7 +180,8 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             mbar_init(s_full + 2 * g, 1);
             mbar_init(s_full + 2 * g + 1, 1);
             mbar_init(p_full + g, 128);
-            mbar_init(pv_full + g, 1);
+            mbar_init(pv_done + g, 1);
+            mbar_init(o_free + g, 128);
         }
         fence_mbar_init();
     }
@@ -187,11 +201,13 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         uint32_t q_use = 0, kv_it = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
             const Item it = decode<NQ>(A, item);
-            const int qb = q_use & 1;
-            mbar_wait(q_empty + qb, ((q_use >> 1) & 1) ^ 1);
-            for (int g = 0; g < it.nq; ++g)
-                gather<DH, kBM>(A, A.q, A.ld_q, it, it.q0 + g * kBM,
-                                sm_base + C::kOffQ + (qb * NQ + g) * C::kQBytes, tid);
+            const int qb = q_use % NQB;
+            mbar_wait(q_empty + qb, ((q_use / NQB) & 1) ^ 1);
+            const uint32_t qdst = sm_base + C::kOffQ + qb * NQ * C::kQBytes;
+            for (int i = tid; i < it.nq * kBM; i += kLoadWarps * 32) {
+                const int g = i >> 7, r = i & (kBM - 1);
+                gather_row<DH>(A, A.q, A.ld_q, it, it.q0 + i, qdst + g * C::kQBytes, r);
+            }
             cp_async_arrive(q_full + qb);
             ++q_use;
             for (int j = 0; j < it.nt; ++j, ++kv_it) {
@@ -199,8 +215,11 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 const uint32_t u = kv_it / kNst;
                 mbar_wait(kv_empty + s, (u & 1) ^ 1);
                 const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
-                gather<DH, kBN>(A, A.k, A.ld_k, it, j * kBN, kb, tid);
-                gather<DH, kBN>(A, A.v, A.ld_v, it, j * kBN, kb + C::kKVBytes, tid);
+                for (int i = tid; i < 2 * kBN; i += kLoadWarps * 32) {
+                    const int isv = i >> 6, r = i & (kBN - 1);
+                    gather_row<DH>(A, isv ? A.v : A.k, isv ? A.ld_v : A.ld_k, it, j * kBN + r,
+                                   kb + isv * C::kKVBytes, r);
+                }
                 cp_async_arrive(kv_full + s);
             }
         }
@@ -210,21 +229,21 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
             constexpr uint32_t idPV = idesc_bf16(kBM, DH, 0, 1);
             uint32_t q_use = 0, kv_it = 0;
-            uint32_t tg[NQ];                     // tiles processed by group g so far
+            uint32_t tg[NQ], ig[NQ];             // tiles / items processed by group g so far
 #pragma unroll
-            for (int g = 0; g < NQ; ++g) tg[g] = 0;
+            for (int g = 0; g < NQ; ++g) tg[g] = ig[g] = 0;
             for (int item = blockIdx.x; item < total; item += gridDim.x) {
                 const Item it = decode<NQ>(A, item);
-                const int qb = q_use & 1;
-                mbar_wait(q_full + qb, (q_use >> 1) & 1);
-                // S_g,j -> TMEM buffer (tg[g]+j)&1.  Reusing that buffer needs
-                // softmax g done with S_g,j-2: implied by p_full_g,j-2, waited
-                // before PV_g,j-2 was issued.
+                const int qb = q_use % NQB;
+                mbar_wait(q_full + qb, (q_use / NQB) & 1);
+                const uint32_t qa0 = sm_base + C::kOffQ + qb * NQ * C::kQBytes;
+                // S_g,j -> TMEM buffer (tg[g]+j)&1, which last held P_g,j-2:
+                // PV_g,j-2 was issued before (tcgen05.mma executes in order).
                 auto issue_S = [&](int g, int j) {
                     const int s = (kv_it + j) % kNst;
                     const int b = (tg[g] + j) & 1;
                     const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
-                    const uint32_t qa = sm_base + C::kOffQ + (qb * NQ + g) * C::kQBytes;
+                    const uint32_t qa = qa0 + g * C::kQBytes;
 #pragma unroll
                     for (int k = 0; k < DH / 16; ++k)
                         umma_f16(tmem + C::kTmemS + (2 * g + b) * kBN,
@@ -239,30 +258,39 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 };
                 wait_kv(0);
                 for (int g = 0; g < it.nq; ++g) issue_S(g, 0);
+                if (it.nt > 1) {
+                    wait_kv(1);
+                    for (int g = 0; g < it.nq; ++g) issue_S(g, 1);
+                }
+                if (it.nt <= 2) umma_commit(q_empty + qb);
                 for (int j = 0; j < it.nt; ++j) {
                     const int s = (kv_it + j) % kNst;
                     const uint32_t vb = sm_base + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes;
-                    if (j + 1 < it.nt) {
-                        wait_kv(j + 1);
-                        for (int g = 0; g < it.nq; ++g) issue_S(g, j + 1);
-                    }
                     for (int g = 0; g < it.nq; ++g) {
-                        mbar_wait(p_full + g, (tg[g] + j) & 1);           // P_g,j in smem
+                        if (j == 0 && ig[g] > 0) mbar_wait(o_free + g, (ig[g] - 1) & 1);
+                        mbar_wait(p_full + g, (tg[g] + j) & 1);   // P_g,j in TMEM
                         tc_fence_after();
-                        const uint32_t pb = sm_base + C::kOffP + g * C::kPBytes;
+                        const uint32_t pa = tmem + C::kTmemS + (2 * g + ((tg[g] + j) & 1)) * kBN;
 #pragma unroll
                         for (int k = 0; k < kBN / 16; ++k)
-                            umma_f16(tmem + C::kTmemPV + g * DH,
-                                     smem_desc(pb + k * 256, 128, 16 * kBN),
-                                     smem_desc(vb + k * 32 * DH, 16 * DH, 128), idPV, k > 0);
-                        umma_commit(pv_full + g);
+                            umma_f16_ts(tmem + C::kTmemO + g * DH, pa + k * 8,
+                                        smem_desc(vb + k * 32 * DH, 16 * DH, 128), idPV,
+                                        (j > 0 || k > 0) ? 1u : 0u);
+                        umma_commit(pv_done + g);
+                        if (j + 2 < it.nt) {
+                            if (g == 0) wait_kv(j + 2);   // after PV_0,j is on its way
+                            issue_S(g, j + 2);
+                        }
                     }
                     umma_commit(kv_empty + s);
+                    if (j + 3 == it.nt) umma_commit(q_empty + qb);   // last S just issued
                 }
-                umma_commit(q_empty + qb);
                 ++q_use;
                 kv_it += it.nt;
-                for (int g = 0; g < it.nq; ++g) tg[g] += it.nt;
+                for (int g = 0; g < it.nq; ++g) {
+                    tg[g] += it.nt;
+                    ++ig[g];
+                }
             }
         }
     } else {
@@ -272,24 +300,20 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         const int r = (sw & 3) * 32 + lane;               // row in the tile = TMEM lane
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
         const float sl2 = A.scale_log2;
-        const uint32_t vbase = tmem + lane_base + C::kTmemPV + g * DH;
-        const uint32_t pb = sm_base + C::kOffP + g * C::kPBytes;
+        const uint32_t obase = tmem + lane_base + C::kTmemO + g * DH;
         uint32_t tg = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
             const Item it = decode<NQ>(A, item);
             if (g >= it.nq) continue;                     // this Q tile is past the scope
-            float o[DH];
-#pragma unroll
-            for (int i = 0; i < DH; ++i) o[i] = 0.f;
-            float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
+            float ms = -INFINITY, l = 0.f;                // running max (scaled, log2), sum
             for (int j = 0; j < it.nt; ++j) {
                 const uint32_t t = tg + j;
                 const int b = t & 1;
+                const uint32_t sb = tmem + lane_base + C::kTmemS + (2 * g + b) * kBN;
                 mbar_wait(s_full + 2 * g + b, (t >> 1) & 1);
                 tc_fence_after();
                 uint32_t x[kBN];
                 {
-                    const uint32_t sb = tmem + lane_base + C::kTmemS + (2 * g + b) * kBN;
                     uint32_t (&x0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[0]);
                     uint32_t (&x1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[32]);
                     tmem_ld32(sb, x0);
@@ -305,81 +329,96 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 float mx = -INFINITY;
 #pragma unroll
                 for (int e = 0; e < kBN; ++e) mx = fmaxf(mx, __uint_as_float(x[e]));
-                const float m_new = fmaxf(m_run, mx);
-                const float alpha = (m_run == -INFINITY) ? 0.f : ex2f((m_run - m_new) * sl2);
-                const float nms = -m_new * sl2;
-                // fold the previous tile's P V (this also frees P_g for overwrite)
-                if (j > 0) {
-                    mbar_wait(pv_full + g, (t - 1) & 1);
-                    tc_fence_after();
+                const float mxs = mx * sl2;
+                // pv_done is consumed once per tile, in order (a parity wait
+                // is only exact when its barrier is at most one phase ahead):
+                // PV_g,j-1 here if O must be rescaled, else before p_full_g,j.
+                bool pv_waited = j == 0;
+                if (j == 0) {
+                    ms = mxs;
+                } else {
+                    const bool need = mxs > ms + kRescale;
+                    if (__any_sync(0xffffffffu, need)) {
+                        // O_g must hold P_g,j-1 V before it is rescaled in place
+                        mbar_wait(pv_done + g, (t - 1) & 1);
+                        tc_fence_after();
+                        pv_waited = true;
+                        const float alpha = need ? ex2f(ms - mxs) : 1.f;
+                        if (need) {
+                            ms = mxs;
+                            l *= alpha;
+                        }
 #pragma unroll
-                    for (int c = 0; c < DH / 16; ++c) {
-                        uint32_t y[16];
-                        tmem_ld16(vbase + c * 16, y);
-                        tmem_wait_ld();
+                        for (int c = 0; c < DH / 16; ++c) {
+                            uint32_t y[16];
+                            tmem_ld16(obase + c * 16, y);
+                            tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 16; ++e)
-                            o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(y[e]));
+                            for (int e = 0; e < 16; ++e)
+                                y[e] = __float_as_uint(__uint_as_float(y[e]) * alpha);
+                            tmem_st16(obase + c * 16, y);
+                        }
                     }
                 }
-                // P = exp2(s*sl2 - m*sl2) -> bf16 smem (core-matrix rows)
+                // P = exp2(s*sl2 - ms) (<= 2^8) -> bf16 pairs over the S columns
+                const float nms = -ms;
+                uint32_t pk[kBN / 2];
                 float sum = 0.f;
 #pragma unroll
-                for (int c = 0; c < kBN / 8; ++c) {
-                    uint32_t pk[4];
-#pragma unroll
-                    for (int e = 0; e < 8; e += 2) {
-                        const float p0 = ex2f(fmaf(__uint_as_float(x[c * 8 + e]), sl2, nms));
-                        const float p1 = ex2f(fmaf(__uint_as_float(x[c * 8 + e + 1]), sl2, nms));
-                        sum += p0 + p1;
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                        pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
-                    }
-                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(pb + core_off<kBN>(r, c)),
-                                 "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
-                                 : "memory");
+                for (int e = 0; e < kBN; e += 2) {
+                    const float p0 = ex2f(fmaf(__uint_as_float(x[e]), sl2, nms));
+                    const float p1 = ex2f(fmaf(__uint_as_float(x[e + 1]), sl2, nms));
+                    if (!ones) sum += p0 + p1;
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                    pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
-                fence_proxy_async();
+                l += sum;
+                tmem_st32(sb, pk);
+                tmem_wait_st();
+                if (!pv_waited) mbar_wait(pv_done + g, (t - 1) & 1);
                 tc_fence_before();
                 mbar_arrive(p_full + g);
-                l_run = l_run * alpha + sum;
-                m_run = m_new;
-                alpha_prev = alpha;
             }
-            // last tile's P V, then normalise and write the row
-            {
-                mbar_wait(pv_full + g, (tg + it.nt - 1) & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < DH / 16; ++c) {
-                    uint32_t y[16];
-                    tmem_ld16(vbase + c * 16, y);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 16; ++e)
-                        o[c * 16 + e] = fmaf(o[c * 16 + e], alpha_prev, __uint_as_float(y[e]));
-                }
+            // O_g complete: normalise and write the row
+            mbar_wait(pv_done + g, (tg + it.nt - 1) & 1);
+            tc_fence_after();
+            float lsum = l;
+            if (ones) {
+                uint32_t y[16];
+                tmem_ld16(obase + (A.dh & ~15), y);
+                tmem_wait_ld();
+                lsum = __uint_as_float(y[A.dh & 15]);
             }
+            const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
             const int vr = it.q0 + g * kBM + r;
-            if (vr < it.m) {
-                const int pr = phys_row(A, it.s0, it.s1, vr);
-                const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-                const int hcol = it.h * A.dh;
-                if (sizeof(OutT) == 2) {
-                    __nv_bfloat16* out =
-                        reinterpret_cast<__nv_bfloat16*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+            const bool live_row = vr < it.m;
+            const int pr = live_row ? phys_row(A, it.s0, it.s1, vr) : 0;
+            const int hcol = it.h * A.dh;
 #pragma unroll
-                    for (int c = 0; c < DH; c += 2)
-                        if (c < A.dh)
-                            *reinterpret_cast<__nv_bfloat162*>(out + c) =
-                                __floats2bfloat162_rn(o[c] * inv, o[c + 1] * inv);
-                } else {
-                    float* out = reinterpret_cast<float*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+            for (int c = 0; c < DH / 16; ++c) {
+                uint32_t y[16];
+                tmem_ld16(obase + c * 16, y);
+                tmem_wait_ld();
+                if (live_row) {
+                    if (sizeof(OutT) == 2) {
+                        __nv_bfloat16* out =
+                            reinterpret_cast<__nv_bfloat16*>(A.o) + (int64_t)pr * A.ld_o + hcol;
 #pragma unroll
-                    for (int c = 0; c < DH; ++c)
-                        if (c < A.dh) out[c] = o[c] * inv;
+                        for (int e = 0; e < 16; e += 2)
+                            if (c * 16 + e < A.dh)
+                                *reinterpret_cast<__nv_bfloat162*>(out + c * 16 + e) =
+                                    __floats2bfloat162_rn(__uint_as_float(y[e]) * inv,
+                                                          __uint_as_float(y[e + 1]) * inv);
+                    } else {
+                        float* out = reinterpret_cast<float*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if (c * 16 + e < A.dh) out[c * 16 + e] = __uint_as_float(y[e]) * inv;
+                    }
                 }
             }
+            tc_fence_before();
+            mbar_arrive(o_free + g);
             tg += it.nt;
         }
     }
@@ -417,7 +456,7 @@ using namespace f3d;
 
 extern "C" int f3d_attention_tc_qstep(int dh) {
     const int dp = (dh + 15) / 16 * 16;
-    const int nq = dp <= 32 ? 3 : (dp <= 64 ? 2 : 1);
+    const int nq = dp <= 32 ? 3 : 2;
     return nq * f3d::attn_tc::kBM;
 }
 

@@ -195,3 +195,22 @@ def test_layer_norm_and_gelu_f64():
     g, b = r.normal(size=24), r.normal(size=24)
     np.testing.assert_allclose(F.layer_norm(x, g, b), O.layer_norm(x, g, b), rtol=1e-6, atol=1e-6)
     np.testing.assert_allclose(F.gelu(x), O.gelu(x), rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("d,H", [(96, 4), (512, 4), (64, 4)])
+def test_attention_growing_max_rescales(d, H):
+    """Logits that grow along the key order move every row's running max
+    tile after tile (the kernel rescales O in TMEM only when the max grows
+    by more than 2^8), over a 3000-row two-segment scope."""
+    r = np.random.default_rng(d + H)
+    m = 3000
+    N = m + 64
+    Q = r.normal(size=(N, d))
+    Q[:, :] = np.abs(Q) * 0.5
+    K = np.abs(r.normal(size=(N, d))) * np.linspace(0.0, 3.0, N)[:, None]
+    V = r.normal(size=(N, d))
+    ranges = [(0, 1700), (1764, 1764 + m - 1700)]
+    out = F.tiled_attention(Q, K, V, F.AttentionParams(d, H), ranges=ranges)
+    ref = O.attention_ranges(Q, K, V, H, ranges)
+    assert np.isfinite(out).all()
+    assert rel(out, ref) < 3e-2, rel(out, ref)

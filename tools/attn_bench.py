@@ -44,7 +44,8 @@ def main():
     torch.cuda.set_device(0)
     C = torch.tensor(synth_cloud(7, n, "uniform-box"), device="cuda")
     bb = Backbone.__new__(Backbone)
-    asg, counts_h, sweeps = Backbone.bucketize(bb, C, cfg)
+    asg, _, _ = Backbone.bucketize(bb, C, cfg)
+    counts_h = asg._dev["counts"].cpu().numpy()
     nb = cfg.K + -(-int(counts_h[cfg.K]) // cfg.S)
     dh = d // a.heads
     plan = DeviceRoundPlan(asg._dev["counts"], asg._dev["base"], cfg.K, cfg.S, nb, cfg.W,
