@@ -17,7 +17,8 @@ from .errors import (ConfigError, EmptyInputError, IntegrityError, NumericError,
                      RangeError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libf3d.so")
+# F3D_LIB_PATH: developer override (A/B builds of the same sources under tools/)
+LIB_PATH = os.environ.get("F3D_LIB_PATH") or os.path.join(_HERE, "libf3d.so")
 
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32

@@ -30,6 +30,10 @@
 #include "f3d_common.cuh"
 #include "tc_common.cuh"
 
+#ifndef F3D_EXPERIMENT
+#define F3D_EXPERIMENT 0   // developer A/B knob (tools/): 1 no K/V/Q loads, 2 no exp
+#endif
+
 namespace f3d {
 namespace attn_tc {
 
@@ -76,7 +80,7 @@ struct Cfg {
     static constexpr int kOffQ = 0;
     static constexpr int kOffKV = kOffQ + NQB * NQ * kQBytes;
     static constexpr int kOffBar = kOffKV + kNst * 2 * kKVBytes;
-    static constexpr int kNumBars = 2 * NQB + 2 * kNst + 5 * NQ;
+    static constexpr int kNumBars = 2 * NQB + 2 * kNst + 7 * NQ;
     static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
     static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (2g+b)*kBN
     static constexpr int kTmemO = 2 * NQ * kBN;         // O of tile g: kTmemO + g*DH
@@ -126,6 +130,9 @@ __device__ __forceinline__ void gather_row(const Args& A, const __nv_bfloat16* b
     const bool ok = vr < it.m;
     const __nv_bfloat16* src = base;
     if (ok) src = base + (int64_t)phys_row(A, it.s0, it.s1, vr) * ld + it.h * A.dh;
+#if F3D_EXPERIMENT == 1
+    return;
+#endif
     for (int c = 0; c < rc; ++c) cp_async16z(dst_row + core_off<DH>(r, c), src + c * 8, ok);
 }
 
@@ -144,9 +151,15 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
     uint64_t* kv_full = q_empty + NQB;           // [kNst]
     uint64_t* kv_empty = kv_full + kNst;         // [kNst]
     uint64_t* s_full = kv_empty + kNst;          // [NQ][2] MMA -> softmax (S_g in buffer b)
-    uint64_t* p_full = s_full + 2 * NQ;          // [NQ] softmax -> MMA (P_g in TMEM, O rescaled)
-    uint64_t* pv_done = p_full + NQ;             // [NQ] MMA -> softmax (O_g += P_g V done)
-    uint64_t* o_free = pv_done + NQ;             // [NQ] softmax -> MMA (O_g read out)
+    // [NQ][2] softmax -> MMA: P_g,t in TMEM buffer t&1 (O rescaled).  Per
+    // buffer, because the softmax may finish tile t+1 before the MMA thread
+    // has consumed tile t (S_g,t and S_g,t+1 are both in flight).
+    uint64_t* p_full = s_full + 2 * NQ;
+    // [NQ][2] MMA -> softmax: O_g += P_g,t V done, on buffer t&1.  A waiter
+    // for PV_g,t has already seen S_g,t (or S_g,t+1) complete, which was
+    // issued after PV_g,t-2: so the barrier is never a phase behind either.
+    uint64_t* pv_done = p_full + 2 * NQ;
+    uint64_t* o_free = pv_done + 2 * NQ;         // [NQ] softmax -> MMA (O_g read out)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
     const int tid = threadIdx.x;
@@ -179,8 +192,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         for (int g = 0; g < NQ; ++g) {
             mbar_init(s_full + 2 * g, 1);
             mbar_init(s_full + 2 * g + 1, 1);
-            mbar_init(p_full + g, 128);
-            mbar_init(pv_done + g, 1);
+            mbar_init(p_full + 2 * g, 128);
+            mbar_init(p_full + 2 * g + 1, 128);
+            mbar_init(pv_done + 2 * g, 1);
+            mbar_init(pv_done + 2 * g + 1, 1);
             mbar_init(o_free + g, 128);
         }
         fence_mbar_init();
@@ -268,7 +283,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                     const uint32_t vb = sm_base + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes;
                     for (int g = 0; g < it.nq; ++g) {
                         if (j == 0 && ig[g] > 0) mbar_wait(o_free + g, (ig[g] - 1) & 1);
-                        mbar_wait(p_full + g, (tg[g] + j) & 1);   // P_g,j in TMEM
+                        {
+                            const uint32_t t = tg[g] + j;     // P_g,j in TMEM
+                            mbar_wait(p_full + 2 * g + (t & 1), (t >> 1) & 1);
+                        }
                         tc_fence_after();
                         const uint32_t pa = tmem + C::kTmemS + (2 * g + ((tg[g] + j) & 1)) * kBN;
 #pragma unroll
@@ -276,7 +294,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                             umma_f16_ts(tmem + C::kTmemO + g * DH, pa + k * 8,
                                         smem_desc(vb + k * 32 * DH, 16 * DH, 128), idPV,
                                         (j > 0 || k > 0) ? 1u : 0u);
-                        umma_commit(pv_done + g);
+                        umma_commit(pv_done + 2 * g + ((tg[g] + j) & 1));
                         if (j + 2 < it.nt) {
                             if (g == 0) wait_kv(j + 2);   // after PV_0,j is on its way
                             issue_S(g, j + 2);
@@ -330,19 +348,14 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
 #pragma unroll
                 for (int e = 0; e < kBN; ++e) mx = fmaxf(mx, __uint_as_float(x[e]));
                 const float mxs = mx * sl2;
-                // pv_done is consumed once per tile, in order (a parity wait
-                // is only exact when its barrier is at most one phase ahead):
-                // PV_g,j-1 here if O must be rescaled, else before p_full_g,j.
-                bool pv_waited = j == 0;
                 if (j == 0) {
                     ms = mxs;
                 } else {
                     const bool need = mxs > ms + kRescale;
                     if (__any_sync(0xffffffffu, need)) {
                         // O_g must hold P_g,j-1 V before it is rescaled in place
-                        mbar_wait(pv_done + g, (t - 1) & 1);
+                        mbar_wait(pv_done + 2 * g + ((t - 1) & 1), ((t - 1) >> 1) & 1);
                         tc_fence_after();
-                        pv_waited = true;
                         const float alpha = need ? ex2f(ms - mxs) : 1.f;
                         if (need) {
                             ms = mxs;
@@ -366,8 +379,13 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 float sum = 0.f;
 #pragma unroll
                 for (int e = 0; e < kBN; e += 2) {
+#if F3D_EXPERIMENT == 2
+                    const float p0 = fmaf(__uint_as_float(x[e]), sl2, nms);
+                    const float p1 = fmaf(__uint_as_float(x[e + 1]), sl2, nms);
+#else
                     const float p0 = ex2f(fmaf(__uint_as_float(x[e]), sl2, nms));
                     const float p1 = ex2f(fmaf(__uint_as_float(x[e + 1]), sl2, nms));
+#endif
                     if (!ones) sum += p0 + p1;
                     __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                     pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
@@ -375,12 +393,14 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 l += sum;
                 tmem_st32(sb, pk);
                 tmem_wait_st();
-                if (!pv_waited) mbar_wait(pv_done + g, (t - 1) & 1);
                 tc_fence_before();
-                mbar_arrive(p_full + g);
+                mbar_arrive(p_full + 2 * g + b);
             }
             // O_g complete: normalise and write the row
-            mbar_wait(pv_done + g, (tg + it.nt - 1) & 1);
+            {
+                const uint32_t tl = tg + it.nt - 1;
+                mbar_wait(pv_done + 2 * g + (tl & 1), (tl >> 1) & 1);
+            }
             tc_fence_after();
             float lsum = l;
             if (ones) {
