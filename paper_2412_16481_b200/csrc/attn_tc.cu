@@ -31,7 +31,18 @@
 #include "tc_common.cuh"
 
 #ifndef F3D_EXPERIMENT
-#define F3D_EXPERIMENT 0   // developer A/B knob (tools/): 1 no K/V/Q loads, 2 no exp
+#define F3D_EXPERIMENT 0   // developer A/B knob (tools/): 1 no K/V/Q loads, 2 no exp,
+#endif                     // 3 per-role wait-cycle counters (f3d_attn_prof)
+#if F3D_EXPERIMENT == 3
+__device__ unsigned long long g_attn_prof[16];
+#define PROF_WAIT(slot, call)                                            \
+    do {                                                                 \
+        const long long _t0 = clock64();                                 \
+        call;                                                            \
+        if ((threadIdx.x & 31) == 0) prof[slot] += clock64() - _t0;      \
+    } while (0)
+#else
+#define PROF_WAIT(slot, call) call
 #endif
 
 namespace f3d {
@@ -45,9 +56,19 @@ constexpr int kLoadWarps = 3;     // warps 0-2
 constexpr int kMmaWarp = 3;       // completes warpgroup 0
 constexpr float kRescale = 8.f;   // move the running max only when it grows by > 2^8
 
+#ifndef F3D_SMALL_NQ3
+#define F3D_SMALL_NQ3 0    // developer A/B knob: 3 Q tiles x 2 S buffers for head dims <= 32
+#endif
+// Q tiles per work item and TMEM S/P buffers per Q tile: NQ * (NSB*kBN + DH)
+// TMEM columns; a third S buffer lets the softmax run two tiles ahead of the
+// MMA round trip (PV_j, then S_j+NSB into the freed buffer).
 template <int DH>
 __host__ __device__ constexpr int nq_for() {
-    return DH <= 32 ? 3 : 2;
+    return (F3D_SMALL_NQ3 && DH <= 32) ? 3 : 2;
+}
+template <int DH>
+__host__ __device__ constexpr int nsb_for() {
+    return nq_for<DH>() * (3 * 64 + DH) <= 512 ? 3 : 2;
 }
 template <int DH>
 __host__ __device__ constexpr int threads_for() {
@@ -70,6 +91,7 @@ struct Args {
 template <int DH>
 struct Cfg {
     static constexpr int NQ = nq_for<DH>();
+    static constexpr int NSB = nsb_for<DH>();
     static constexpr int kQBytes = kBM * DH * 2;        // one Q tile
     static constexpr int kKVBytes = kBN * DH * 2;       // one of K or V
     static constexpr int kBudget = 227 * 1024 - 512;
@@ -80,12 +102,12 @@ struct Cfg {
     static constexpr int kOffQ = 0;
     static constexpr int kOffKV = kOffQ + NQB * NQ * kQBytes;
     static constexpr int kOffBar = kOffKV + kNst * 2 * kKVBytes;
-    static constexpr int kNumBars = 2 * NQB + 2 * kNst + 7 * NQ;
+    static constexpr int kNumBars = 2 * NQB + 2 * kNst + (3 * NSB + 1) * NQ;
     static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
-    static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (2g+b)*kBN
-    static constexpr int kTmemO = 2 * NQ * kBN;         // O of tile g: kTmemO + g*DH
-    static constexpr int kTmemCols = NQ * (2 * kBN + DH) <= 256 ? 256 : 512;
-    static_assert(NQ * (2 * kBN + DH) <= 512, "TMEM budget");
+    static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (NSB*g+b)*kBN
+    static constexpr int kTmemO = NSB * NQ * kBN;       // O of tile g: kTmemO + g*DH
+    static constexpr int kTmemCols = NQ * (NSB * kBN + DH) <= 256 ? 256 : 512;
+    static_assert(NQ * (NSB * kBN + DH) <= 512, "TMEM budget");
     static_assert(kNst >= 2, "K/V pipeline depth");
     static_assert(kSmem <= 227 * 1024, "smem budget");
 };
@@ -141,6 +163,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
     using C = Cfg<DH>;
     constexpr int NQ = C::NQ;
     constexpr int NQB = C::NQB;
+    constexpr int NSB = C::NSB;
     constexpr int kNst = C::kNst;
     constexpr int kThreads = threads_for<DH>();
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -150,16 +173,16 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
     uint64_t* q_empty = q_full + NQB;            // [NQB] MMA -> loaders
     uint64_t* kv_full = q_empty + NQB;           // [kNst]
     uint64_t* kv_empty = kv_full + kNst;         // [kNst]
-    uint64_t* s_full = kv_empty + kNst;          // [NQ][2] MMA -> softmax (S_g in buffer b)
-    // [NQ][2] softmax -> MMA: P_g,t in TMEM buffer t&1 (O rescaled).  Per
-    // buffer, because the softmax may finish tile t+1 before the MMA thread
-    // has consumed tile t (S_g,t and S_g,t+1 are both in flight).
-    uint64_t* p_full = s_full + 2 * NQ;
-    // [NQ][2] MMA -> softmax: O_g += P_g,t V done, on buffer t&1.  A waiter
-    // for PV_g,t has already seen S_g,t (or S_g,t+1) complete, which was
-    // issued after PV_g,t-2: so the barrier is never a phase behind either.
-    uint64_t* pv_done = p_full + 2 * NQ;
-    uint64_t* o_free = pv_done + 2 * NQ;         // [NQ] softmax -> MMA (O_g read out)
+    uint64_t* s_full = kv_empty + kNst;          // [NQ][NSB] MMA -> softmax (S_g in buffer b)
+    // [NQ][NSB] softmax -> MMA: P_g,t in TMEM buffer t%NSB (O rescaled).  Per
+    // buffer, because the softmax may finish tiles t+1.. before the MMA
+    // thread has consumed tile t (S_g,t .. S_g,t+NSB-1 are all in flight).
+    uint64_t* p_full = s_full + NSB * NQ;
+    // [NQ][NSB] MMA -> softmax: O_g += P_g,t V done, on buffer t%NSB.  A
+    // waiter for PV_g,t has already seen S_g,t+1 complete, which was issued
+    // after PV_g,t+1-NSB: so the barrier is never a phase behind either.
+    uint64_t* pv_done = p_full + NSB * NQ;
+    uint64_t* o_free = pv_done + NSB * NQ;       // [NQ] softmax -> MMA (O_g read out)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
     const int tid = threadIdx.x;
@@ -167,6 +190,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
     const int lane = tid & 31;
     const int total = (A.live ? __ldg(A.live) : A.nwork) * A.H;
     const bool ones = A.dh < DH;                 // V column dh = 1 -> O column dh = row sum
+#if F3D_EXPERIMENT == 3
+    unsigned long long prof[16] = {0};
+    const long long t_start = clock64();
+#endif
 
     // zero the operand tiles once: pad chunks (dh < DH) are never written again
     for (int i = tid; i < C::kOffBar / 16; i += kThreads)
@@ -190,12 +217,11 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             mbar_init(kv_empty + s, 1);
         }
         for (int g = 0; g < NQ; ++g) {
-            mbar_init(s_full + 2 * g, 1);
-            mbar_init(s_full + 2 * g + 1, 1);
-            mbar_init(p_full + 2 * g, 128);
-            mbar_init(p_full + 2 * g + 1, 128);
-            mbar_init(pv_done + 2 * g, 1);
-            mbar_init(pv_done + 2 * g + 1, 1);
+            for (int b = 0; b < NSB; ++b) {
+                mbar_init(s_full + NSB * g + b, 1);
+                mbar_init(p_full + NSB * g + b, 128);
+                mbar_init(pv_done + NSB * g + b, 1);
+            }
             mbar_init(o_free + g, 128);
         }
         fence_mbar_init();
@@ -217,7 +243,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
             const Item it = decode<NQ>(A, item);
             const int qb = q_use % NQB;
-            mbar_wait(q_empty + qb, ((q_use / NQB) & 1) ^ 1);
+            PROF_WAIT(10, mbar_wait(q_empty + qb, ((q_use / NQB) & 1) ^ 1));
             const uint32_t qdst = sm_base + C::kOffQ + qb * NQ * C::kQBytes;
             for (int i = tid; i < it.nq * kBM; i += kLoadWarps * 32) {
                 const int g = i >> 7, r = i & (kBM - 1);
@@ -228,7 +254,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             for (int j = 0; j < it.nt; ++j, ++kv_it) {
                 const int s = kv_it % kNst;
                 const uint32_t u = kv_it / kNst;
-                mbar_wait(kv_empty + s, (u & 1) ^ 1);
+                PROF_WAIT(9, mbar_wait(kv_empty + s, (u & 1) ^ 1));
                 const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
                 for (int i = tid; i < 2 * kBN; i += kLoadWarps * 32) {
                     const int isv = i >> 6, r = i & (kBN - 1);
@@ -239,77 +265,97 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             }
         }
     } else if (warp == kMmaWarp) {
-        // ------------------------------------------------ MMA warp (one thread)
-        if (lane == 0) {
-            constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
-            constexpr uint32_t idPV = idesc_bf16(kBM, DH, 0, 1);
-            uint32_t q_use = 0, kv_it = 0;
-            uint32_t tg[NQ], ig[NQ];             // tiles / items processed by group g so far
+        // ------------------------------------------------ MMA warp
+        // The whole warp walks the schedule (warp-uniform control flow and
+        // waits); one elected lane issues every tcgen05.mma / commit.  Descriptors are
+        // built once: per tile only the 14-bit start-address field moves
+        // (addresses < 2^18, so adding (bytes >> 4) never carries out).
+        constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
+        constexpr uint32_t idPV = idesc_bf16(kBM, DH, 0, 1);
+        const uint64_t dQ = smem_desc(sm_base + C::kOffQ, 128, 16 * DH);
+        const uint64_t dK = smem_desc(sm_base + C::kOffKV, 128, 16 * DH);
+        const uint64_t dV = smem_desc(sm_base + C::kOffKV + C::kKVBytes, 16 * DH, 128);
+        constexpr uint32_t kStageD = (2 * C::kKVBytes) >> 4;   // descriptor step per K/V stage
+        constexpr uint32_t kQD = C::kQBytes >> 4;              // per Q tile
+        uint32_t q_use = 0, kv_it = 0;
+        uint32_t tg[NQ], ig[NQ];             // tiles / items processed by group g so far
 #pragma unroll
-            for (int g = 0; g < NQ; ++g) tg[g] = ig[g] = 0;
-            for (int item = blockIdx.x; item < total; item += gridDim.x) {
-                const Item it = decode<NQ>(A, item);
-                const int qb = q_use % NQB;
-                mbar_wait(q_full + qb, (q_use / NQB) & 1);
-                const uint32_t qa0 = sm_base + C::kOffQ + qb * NQ * C::kQBytes;
-                // S_g,j -> TMEM buffer (tg[g]+j)&1, which last held P_g,j-2:
-                // PV_g,j-2 was issued before (tcgen05.mma executes in order).
-                auto issue_S = [&](int g, int j) {
-                    const int s = (kv_it + j) % kNst;
-                    const int b = (tg[g] + j) & 1;
-                    const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
-                    const uint32_t qa = qa0 + g * C::kQBytes;
+        for (int g = 0; g < NQ; ++g) tg[g] = ig[g] = 0;
+        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+            const Item it = decode<NQ>(A, item);
+            const int qb = q_use % NQB;
+            PROF_WAIT(4, mbar_wait(q_full + qb, (q_use / NQB) & 1));
+            const uint64_t dq = dQ + (uint64_t)(qb * NQ * kQD);
+            // S_g,j -> TMEM buffer (tg[g]+j)%NSB, which last held P_g,j-NSB:
+            // PV_g,j-NSB was issued before (tcgen05.mma executes in order).
+            auto issue_S = [&](int g, int j) {
+                const uint32_t s = (kv_it + j) % kNst;
+                const uint32_t b = (tg[g] + j) % NSB;
+                const uint64_t dk = dK + (uint64_t)(s * kStageD);
+                const uint64_t dqg = dq + (uint64_t)(g * kQD);
+                const uint32_t d = tmem + C::kTmemS + (NSB * g + b) * kBN;
+                if (elect_one()) {
 #pragma unroll
                     for (int k = 0; k < DH / 16; ++k)
-                        umma_f16(tmem + C::kTmemS + (2 * g + b) * kBN,
-                                 smem_desc(qa + k * 256, 128, 16 * DH),
-                                 smem_desc(kb + k * 256, 128, 16 * DH), idS, k > 0);
-                    umma_commit(s_full + 2 * g + b);
-                };
-                auto wait_kv = [&](int j) {
-                    const uint32_t kvi = kv_it + j;
-                    mbar_wait(kv_full + kvi % kNst, (kvi / kNst) & 1);
-                    tc_fence_after();
-                };
-                wait_kv(0);
-                for (int g = 0; g < it.nq; ++g) issue_S(g, 0);
-                if (it.nt > 1) {
-                    wait_kv(1);
-                    for (int g = 0; g < it.nq; ++g) issue_S(g, 1);
+                        umma_f16(d, dqg + (uint64_t)(16 * k), dk + (uint64_t)(16 * k), idS, k > 0);
+                    umma_commit(s_full + NSB * g + b);
                 }
-                if (it.nt <= 2) umma_commit(q_empty + qb);
-                for (int j = 0; j < it.nt; ++j) {
-                    const int s = (kv_it + j) % kNst;
-                    const uint32_t vb = sm_base + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes;
-                    for (int g = 0; g < it.nq; ++g) {
-                        if (j == 0 && ig[g] > 0) mbar_wait(o_free + g, (ig[g] - 1) & 1);
-                        {
-                            const uint32_t t = tg[g] + j;     // P_g,j in TMEM
-                            mbar_wait(p_full + 2 * g + (t & 1), (t >> 1) & 1);
-                        }
-                        tc_fence_after();
-                        const uint32_t pa = tmem + C::kTmemS + (2 * g + ((tg[g] + j) & 1)) * kBN;
+                __syncwarp();
+            };
+            auto wait_kv = [&](int j) {
+                const uint32_t kvi = kv_it + j;
+                PROF_WAIT(5, mbar_wait(kv_full + kvi % kNst, (kvi / kNst) & 1));
+                tc_fence_after();
+            };
+            for (int j = 0; j < NSB && j < it.nt; ++j) {
+                wait_kv(j);
+#pragma unroll
+                for (int g = 0; g < NQ; ++g)
+                    if (g < it.nq) issue_S(g, j);
+            }
+            if (it.nt <= NSB) {
+                if (elect_one()) umma_commit(q_empty + qb);
+                __syncwarp();
+            }
+            for (int j = 0; j < it.nt; ++j) {
+                const uint32_t s = (kv_it + j) % kNst;
+                const uint64_t dv = dV + (uint64_t)(s * kStageD);
+#pragma unroll
+                for (int g = 0; g < NQ; ++g) {
+                    if (g >= it.nq) break;
+                    if (j == 0 && ig[g] > 0) PROF_WAIT(7, mbar_wait(o_free + g, (ig[g] - 1) & 1));
+                    const uint32_t t = tg[g] + j;     // P_g,j in TMEM buffer t % NSB
+                    PROF_WAIT(6, mbar_wait(p_full + NSB * g + t % NSB, (t / NSB) & 1));
+                    tc_fence_after();
+                    const uint32_t pa = tmem + C::kTmemS + (NSB * g + t % NSB) * kBN;
+                    const uint32_t od = tmem + C::kTmemO + g * DH;
+                    if (elect_one()) {
 #pragma unroll
                         for (int k = 0; k < kBN / 16; ++k)
-                            umma_f16_ts(tmem + C::kTmemO + g * DH, pa + k * 8,
-                                        smem_desc(vb + k * 32 * DH, 16 * DH, 128), idPV,
+                            umma_f16_ts(od, pa + k * 8, dv + (uint64_t)(2 * DH * k), idPV,
                                         (j > 0 || k > 0) ? 1u : 0u);
-                        umma_commit(pv_done + 2 * g + ((tg[g] + j) & 1));
-                        if (j + 2 < it.nt) {
-                            if (g == 0) wait_kv(j + 2);   // after PV_0,j is on its way
-                            issue_S(g, j + 2);
-                        }
+                        umma_commit(pv_done + NSB * g + t % NSB);
                     }
-                    umma_commit(kv_empty + s);
-                    if (j + 3 == it.nt) umma_commit(q_empty + qb);   // last S just issued
+                    __syncwarp();
+                    if (j + NSB < it.nt) {
+                        if (g == 0) wait_kv(j + NSB);   // after PV_0,j is on its way
+                        issue_S(g, j + NSB);
+                    }
                 }
-                ++q_use;
-                kv_it += it.nt;
-                for (int g = 0; g < it.nq; ++g) {
+                if (elect_one()) {
+                    umma_commit(kv_empty + s);
+                    if (j + NSB + 1 == it.nt) umma_commit(q_empty + qb);   // last S just issued
+                }
+                __syncwarp();
+            }
+            ++q_use;
+            kv_it += it.nt;
+#pragma unroll
+            for (int g = 0; g < NQ; ++g)
+                if (g < it.nq) {
                     tg[g] += it.nt;
                     ++ig[g];
                 }
-            }
         }
     } else {
         // ------------------------------------------------ softmax warpgroups
@@ -326,9 +372,12 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             float ms = -INFINITY, l = 0.f;                // running max (scaled, log2), sum
             for (int j = 0; j < it.nt; ++j) {
                 const uint32_t t = tg + j;
-                const int b = t & 1;
-                const uint32_t sb = tmem + lane_base + C::kTmemS + (2 * g + b) * kBN;
-                mbar_wait(s_full + 2 * g + b, (t >> 1) & 1);
+                const int b = t % NSB;
+                const uint32_t sb = tmem + lane_base + C::kTmemS + (NSB * g + b) * kBN;
+                PROF_WAIT(1, mbar_wait(s_full + NSB * g + b, (t / NSB) & 1));
+#if F3D_EXPERIMENT == 3
+                if (lane == 0) prof[12] += 1;
+#endif
                 tc_fence_after();
                 uint32_t x[kBN];
                 {
@@ -354,7 +403,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                     const bool need = mxs > ms + kRescale;
                     if (__any_sync(0xffffffffu, need)) {
                         // O_g must hold P_g,j-1 V before it is rescaled in place
-                        mbar_wait(pv_done + 2 * g + ((t - 1) & 1), ((t - 1) >> 1) & 1);
+                        PROF_WAIT(2, mbar_wait(pv_done + NSB * g + (t - 1) % NSB, ((t - 1) / NSB) & 1));
+#if F3D_EXPERIMENT == 3
+                        if (lane == 0) prof[13] += 1;
+#endif
                         tc_fence_after();
                         const float alpha = need ? ex2f(ms - mxs) : 1.f;
                         if (need) {
@@ -394,12 +446,12 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 tmem_st32(sb, pk);
                 tmem_wait_st();
                 tc_fence_before();
-                mbar_arrive(p_full + 2 * g + b);
+                mbar_arrive(p_full + NSB * g + b);
             }
             // O_g complete: normalise and write the row
             {
                 const uint32_t tl = tg + it.nt - 1;
-                mbar_wait(pv_done + 2 * g + (tl & 1), (tl >> 1) & 1);
+                PROF_WAIT(3, mbar_wait(pv_done + NSB * g + tl % NSB, (tl / NSB) & 1));
             }
             tc_fence_after();
             float lsum = l;
@@ -442,6 +494,14 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             tg += it.nt;
         }
     }
+#if F3D_EXPERIMENT == 3
+    if (lane == 0) {
+        const int role = warp < kLoadWarps ? 11 : (warp == kMmaWarp ? 8 : 0);
+        prof[role] += clock64() - t_start;
+        for (int i = 0; i < 16; ++i)
+            if (prof[i]) atomicAdd(&g_attn_prof[i], prof[i]);
+    }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
@@ -474,9 +534,20 @@ int launch_dh(const Args& A, cudaStream_t st) {
 
 using namespace f3d;
 
+#if F3D_EXPERIMENT == 3
+extern "C" int f3d_attn_prof(unsigned long long* out16_host, int reset) {
+    cudaMemcpyFromSymbol(out16_host, g_attn_prof, sizeof(g_attn_prof));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_attn_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
 extern "C" int f3d_attention_tc_qstep(int dh) {
     const int dp = (dh + 15) / 16 * 16;
-    const int nq = dp <= 32 ? 3 : 2;
+    const int nq = (F3D_SMALL_NQ3 && dp <= 32) ? 3 : 2;
     return nq * f3d::attn_tc::kBM;
 }
 
