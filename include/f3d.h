@@ -149,18 +149,19 @@ int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_
                         const uint8_t *mask, int32_t *starved, void *stream);
 
 /* Same contract on the 5th-generation tensor cores (tcgen05.mma into TMEM,
- * persistent warp-specialised CTAs: cp.async gather warps, one MMA-issuing
- * thread, softmax warpgroups reading S with tcgen05.ld).  The work list
- * must step q_start by f3d_attention_tc_qstep(dh) (NQ 128-row Q tiles share
- * each K/V tile; NQ = 3 / 2 / 1 for head dims <= 32 / 64 / 128).
- * Requires dh % 8 == 0, 16-byte aligned q/k/v and row strides that are
- * multiples of 8; no mask. */
+ * persistent warp-specialised CTAs: TMA loads of in-segment tiles with a
+ * cp.async row gather for tiles straddling segments, one elected MMA-issuing
+ * lane, softmax warpgroups reading S / writing P with tcgen05.ld / st).  The
+ * work list must step q_start by f3d_attention_tc_qstep(dh) (two 128-row Q
+ * tiles share each K/V tile).  n_rows: rows of q/k/v (bounds of the TMA
+ * tensor maps; 0 disables TMA).  Requires dh % 8 == 0, dh <= 128, 16-byte
+ * aligned q/k/v and row strides that are multiples of 8; no mask. */
 int f3d_bswin_attention_tc(const void *q, const void *k, const void *v, int64_t ld_q,
                            int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
                            int dh, const int32_t *scope_seg, const int32_t *scope_nseg,
                            const int32_t *seg_start, const int32_t *seg_vstart,
                            const int32_t *scope_len, const int32_t *work, int nwork,
-                           const int32_t *live, void *stream);
+                           const int32_t *live, int64_t n_rows, void *stream);
 
 int f3d_attention_tc_qstep(int dh);
 

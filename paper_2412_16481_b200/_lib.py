@@ -47,7 +47,7 @@ SIGNATURES = {
     "f3d_bswin_attention": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _INT, _INT, _INT, _P,
                                    _P, _P, _P, _P, _P, _INT, _P, _INT, _INT, _P, _P, _P, _P]),
     "f3d_bswin_attention_tc": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _INT, _INT, _INT,
-                                      _P, _P, _P, _P, _P, _P, _INT, _P, _P]),
+                                      _P, _P, _P, _P, _P, _P, _INT, _P, _I64, _P]),
     "f3d_attention_tc_qstep": (_INT, [_INT]),
     "f3d_plan_round": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P, _P, _P, _P,
                               _P, _P, _INT, _INT, _P, _P]),

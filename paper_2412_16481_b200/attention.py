@@ -325,7 +325,7 @@ def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, star
                v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads,
                dh, L.ptr(plan.scope_seg), L.ptr(plan.scope_nseg), L.ptr(plan.seg_start),
                L.ptr(plan.seg_vstart), L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork,
-               L.ptr(plan.live), L.stream())
+               L.ptr(plan.live), min(q.shape[0], k.shape[0], v.shape[0]), L.stream())
         return
     if getattr(plan, "qstep", BLOCK_M) != BLOCK_M:
         raise ConfigError("attention plan stride does not match the selected kernel")

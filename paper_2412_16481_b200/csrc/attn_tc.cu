@@ -1,37 +1,44 @@
-// Bucket-swin attention on 5th-generation tensor cores (tcgen05 / TMEM).
+// Bucket-swin attention on 5th-generation tensor cores (tcgen05 / TMEM / TMA).
 //
 // Same contract as csrc/attn.cu (bw/attention.py:188-268 per scope, one launch
 // per round), FlashAttention-style with the Blackwell execution model:
 //   * persistent CTAs (one per SM) walk the (query group, head) work list; a
-//     group is NQ 128-row Q tiles (NQ = 3 for head dims <= 32, else 2) that
-//     share every 64-key K/V tile;
-//   * warps 0-2 gather Q / K / V rows of the scope straight from the fixed
-//     scattered layout with cp.async into UMMA core-matrix smem tiles (a
-//     scope is up to W physical segments, so rows are gathered, not boxed);
-//     one thread per row, completion signalled on mbarriers;
-//   * warp 3 (one thread) issues tcgen05.mma: S_g = Q_g K^T into one of two
-//     TMEM S buffers per Q tile, then O_g += P_g V with P_g read from TMEM
-//     (the softmax writes it over S_g) and O_g accumulated in TMEM across all
-//     key tiles; tcgen05.commit -> mbarriers;
+//     group is NQ = 2 128-row Q tiles that share every 64-key K/V tile;
+//   * loads: a scope is the concatenation of up to W physical row segments of
+//     the fixed scattered layout (adjacent buckets are merged, so most scopes
+//     are one segment).  A tile whose rows lie inside one segment is fetched
+//     by TMA (one elected thread, 2-D boxes of the head's columns, swizzled
+//     straight into the UMMA operand layout); a tile that straddles two
+//     segments or runs past the scope end is gathered row by row with
+//     cp.async (zero-filled past m) by warps 0-2.  Both complete on the
+//     same mbarrier (96 cp.async arrivals + one elected arrive[.expect_tx]);
+//   * warp 3 walks the schedule and one elected lane issues tcgen05.mma:
+//     S_g = Q_g K^T into one of NSB TMEM S buffers per Q tile, then
+//     O_g += P_g V with P_g read from TMEM (the softmax writes it over S_g) and
+//     O_g accumulated in TMEM across all key tiles; tcgen05.commit ->
+//     mbarriers;
 //   * NQ softmax warpgroups (thread = query row = TMEM lane) read S with
 //     tcgen05.ld, run the online softmax in the exp2 domain, and store P as
-//     bf16 back into TMEM.  The running max is only moved (and O rescaled in
-//     TMEM) when a row's max grows by more than 2^8, so almost every tile is
-//     ld S -> max -> exp -> st P with no O traffic.  When the head dim is
+//     bf16 back into TMEM.  The running max only moves (and O is rescaled in
+//     TMEM) when a row's max grows by more than 2^8.  When the head dim is
 //     padded (dh < DH) a ones column in V makes the PV MMA produce the row
 //     sums, so the softmax does no per-score add.
-// Shared-memory tiles use the SWIZZLE_NONE canonical layout: element (r, c)
-// of an R x C bf16 tile lives at (r/8)*16*C + (c/8)*128 + (r%8)*16 + (c%8)*2.
+// Operand tiles use the UMMA swizzled layouts (SW = 2*min(DH,64) bytes per
+// row): Q and K K-major, V MN-major; a 128-wide head is two 64-column blocks.
+// Element (r, c) of an R-row tile: block b = c / BW, byte o = r*SW + (c%BW)*2,
+// o ^= ((o >> 7) & (SW/16 - 1)) << 4, at b*R*SW + o (Swizzle<log2(SW/16),4,3>).
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cfloat>
+#include <cstring>
 
 #include "f3d_common.cuh"
 #include "tc_common.cuh"
 
 #ifndef F3D_EXPERIMENT
-#define F3D_EXPERIMENT 0   // developer A/B knob (tools/): 1 no K/V/Q loads, 2 no exp,
+#define F3D_EXPERIMENT 0   // developer A/B knob (tools/): 1 no loads, 2 no exp,
 #endif                     // 3 per-role wait-cycle counters (f3d_attn_prof)
 #if F3D_EXPERIMENT == 3
 __device__ unsigned long long g_attn_prof[16];
@@ -52,28 +59,48 @@ using namespace f3d::tc;
 
 constexpr int kBM = 128;          // rows per Q tile (TMEM lanes)
 constexpr int kBN = 64;           // keys per K/V tile
+constexpr int kNQ = 2;            // Q tiles per work item
 constexpr int kLoadWarps = 3;     // warps 0-2
+constexpr int kLoadThreads = kLoadWarps * 32;
 constexpr int kMmaWarp = 3;       // completes warpgroup 0
+constexpr int kThreads = (4 + 4 * kNQ) * 32;
 constexpr float kRescale = 8.f;   // move the running max only when it grows by > 2^8
+constexpr int kMaps = 6;          // TMA maps: {q, k, v} x {first block, second block}
 
-#ifndef F3D_SMALL_NQ3
-#define F3D_SMALL_NQ3 0    // developer A/B knob: 3 Q tiles x 2 S buffers for head dims <= 32
-#endif
-// Q tiles per work item and TMEM S/P buffers per Q tile: NQ * (NSB*kBN + DH)
-// TMEM columns; a third S buffer lets the softmax run two tiles ahead of the
-// MMA round trip (PV_j, then S_j+NSB into the freed buffer).
-template <int DH>
-__host__ __device__ constexpr int nq_for() {
-    return (F3D_SMALL_NQ3 && DH <= 32) ? 3 : 2;
+__host__ __device__ constexpr int dh_tile(int dh) {   // padded head dim of the kernel
+    return dh <= 16 ? 16 : dh <= 32 ? 32 : dh <= 64 ? 64 : 128;
 }
+
+// Swizzled operand layout of a DH-wide head.
+template <int DH>
+struct Lay {
+    static constexpr int SW = DH >= 64 ? 128 : 2 * DH;  // bytes per block row (= swizzle span)
+    static constexpr int BW = SW / 2;                   // elements per block row
+    static constexpr int NBLK = DH / BW;
+    static constexpr int XM = SW / 16 - 1;              // swizzle xor mask (16-byte chunks)
+    static constexpr uint32_t LT = SW == 128 ? 2u : (SW == 64 ? 4u : 6u);   // UMMA layout type
+    // byte offset of 16-byte chunk c of row r in an R-row tile
+    template <int R>
+    static __device__ __forceinline__ uint32_t off(int r, int c) {
+        const int b = c / (BW / 8), cc = c - b * (BW / 8);
+        uint32_t o = (uint32_t)(r * SW + cc * 16);
+        o ^= ((o >> 7) & XM) << 4;
+        return (uint32_t)(b * R * SW) + o;
+    }
+};
+
+__device__ __forceinline__ uint64_t sw_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t lt) {
+    return smem_desc(addr, lbo, sbo) | ((uint64_t)lt << 61);
+}
+
 template <int DH>
 __host__ __device__ constexpr int nsb_for() {
-    return nq_for<DH>() * (3 * 64 + DH) <= 512 ? 3 : 2;
+    return kNQ * (3 * kBN + DH) <= 512 ? 3 : 2;
 }
-template <int DH>
-__host__ __device__ constexpr int threads_for() {
-    return (4 + 4 * nq_for<DH>()) * 32;
-}
+
+struct Maps {
+    CUtensorMap m[kMaps];
+};
 
 struct Args {
     const __nv_bfloat16 *q, *k, *v;
@@ -86,15 +113,16 @@ struct Args {
     const int32_t *scope_seg, *scope_nseg, *seg_start, *seg_vstart, *scope_len, *work;
     int nwork;
     const int32_t* live;   // optional device [nwork, ...]
+    int use_tma;
 };
 
 template <int DH>
 struct Cfg {
-    static constexpr int NQ = nq_for<DH>();
+    static constexpr int NQ = kNQ;
     static constexpr int NSB = nsb_for<DH>();
     static constexpr int kQBytes = kBM * DH * 2;        // one Q tile
     static constexpr int kKVBytes = kBN * DH * 2;       // one of K or V
-    static constexpr int kBudget = 227 * 1024 - 512;
+    static constexpr int kBudget = 227 * 1024 - 1024 - 512;
     // K/V depth first (>= 4 stages), then a second Q buffer if it still fits
     static constexpr int NQB = (2 * NQ * kQBytes + 4 * 2 * kKVBytes <= kBudget) ? 2 : 1;
     static constexpr int kNstFit = (kBudget - NQB * NQ * kQBytes) / (2 * kKVBytes);
@@ -103,7 +131,7 @@ struct Cfg {
     static constexpr int kOffKV = kOffQ + NQB * NQ * kQBytes;
     static constexpr int kOffBar = kOffKV + kNst * 2 * kKVBytes;
     static constexpr int kNumBars = 2 * NQB + 2 * kNst + (3 * NSB + 1) * NQ;
-    static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
+    static constexpr int kSmem = kOffBar + kNumBars * 8 + 16 + 1024;   // + 1 KB alignment slack
     static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (NSB*g+b)*kBN
     static constexpr int kTmemO = NSB * NQ * kBN;       // O of tile g: kTmemO + g*DH
     static constexpr int kTmemCols = NQ * (NSB * kBN + DH) <= 256 ? 256 : 512;
@@ -119,17 +147,10 @@ __device__ __forceinline__ int phys_row(const Args& A, int s0, int s1, int vr) {
     return __ldg(A.seg_start + seg) + (vr - __ldg(A.seg_vstart + seg));
 }
 
-// byte offset of 16-byte chunk (row r, chunk c) in an R x C core-matrix tile
-template <int C>
-__device__ __forceinline__ uint32_t core_off(int r, int c) {
-    return (uint32_t)((r >> 3) * (16 * C) + c * 128 + (r & 7) * 16);
-}
-
 struct Item {
     int scope, q0, h, m, s0, s1, nt, nq;   // nq: Q tiles of this item holding real rows
 };
 
-template <int NQ>
 __device__ __forceinline__ Item decode(const Args& A, int item) {
     Item it;
     const int wi = item / A.H;
@@ -140,33 +161,83 @@ __device__ __forceinline__ Item decode(const Args& A, int item) {
     it.s1 = it.s0 + __ldg(A.scope_nseg + it.scope);
     it.m = __ldg(A.scope_len + it.scope);
     it.nt = (it.m + kBN - 1) / kBN;
-    it.nq = min(NQ, (it.m - it.q0 + kBM - 1) / kBM);
+    it.nq = min(kNQ, (it.m - it.q0 + kBM - 1) / kBM);
     return it;
 }
 
-// One row of head h (real 16-byte chunks only; zero-filled past m).
-template <int DH>
-__device__ __forceinline__ void gather_row(const Args& A, const __nv_bfloat16* base, int64_t ld,
-                                           const Item& it, int vr, uint32_t dst_row, int r) {
-    const int rc = A.dh >> 3;
-    const bool ok = vr < it.m;
-    const __nv_bfloat16* src = base;
-    if (ok) src = base + (int64_t)phys_row(A, it.s0, it.s1, vr) * ld + it.h * A.dh;
+// First physical row of [v0, v0 + R) if those virtual rows lie inside one
+// segment (so inside the scope, all real): the tile can be one TMA box.
+__device__ __forceinline__ int tile_run(const Args& A, const Item& it, int v0, int R) {
+    int seg = it.s0;
+    for (int s = it.s0 + 1; s < it.s1; ++s)
+        if (__ldg(A.seg_vstart + s) <= v0) seg = s;
+    const int vs = __ldg(A.seg_vstart + seg);
+    const int ve = seg + 1 < it.s1 ? __ldg(A.seg_vstart + seg + 1) : it.m;
+    return v0 + R <= ve ? __ldg(A.seg_start + seg) + (v0 - vs) : -1;
+}
+
+// cp.async fallback: rows [v0, v0+R) of head h, one row per loader thread,
+// real 16-byte chunks only, zero-filled past m.
+template <int DH, int R>
+__device__ __forceinline__ void gather_rows(const Args& A, const __nv_bfloat16* base, int64_t ld,
+                                            const Item& it, int v0, uint32_t dst, int tid) {
 #if F3D_EXPERIMENT == 1
     return;
 #endif
-    for (int c = 0; c < rc; ++c) cp_async16z(dst_row + core_off<DH>(r, c), src + c * 8, ok);
+    const int rc = A.dh >> 3;
+    for (int r = tid; r < R; r += kLoadThreads) {
+        const int vr = v0 + r;
+        const bool ok = vr < it.m;
+        const __nv_bfloat16* src = base;
+        if (ok) src = base + (int64_t)phys_row(A, it.s0, it.s1, vr) * ld + it.h * A.dh;
+        for (int c = 0; c < rc; ++c)
+            cp_async16z(dst + Lay<DH>::template off<R>(r, c), src + c * 8, ok);
+    }
+}
+
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(saddr(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// TMA of rows [p0, p0 + R) of head h (map pair mp: q=0, k=2, v=4) into a
+// tile of R rows: one box of 64 rows per column block and 64-row slab.
+template <int DH, int R>
+__device__ __forceinline__ void tma_rows(const Maps& M, int mp, const Args& A, int h, int p0,
+                                         uint32_t dst, uint64_t* bar) {
+    using L = Lay<DH>;
+    const int c0 = h * A.dh;
+#pragma unroll
+    for (int b = 0; b < L::NBLK; ++b) {
+        if (b * L::BW >= A.dh) break;
+#pragma unroll
+        for (int s = 0; s < R / 64; ++s)
+            tma_2d(dst + b * R * L::SW + s * 64 * L::SW, &M.m[mp + b], bar, c0 + b * L::BW,
+                   p0 + s * 64);
+    }
 }
 
 template <int DH, typename OutT>
-__global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(const Args A) {
+__global__ void __launch_bounds__(kThreads, 1)
+    bswin_attn_tc_kernel(const Args A, const __grid_constant__ Maps M) {
     using C = Cfg<DH>;
+    using L = Lay<DH>;
     constexpr int NQ = C::NQ;
     constexpr int NQB = C::NQB;
     constexpr int NSB = C::NSB;
     constexpr int kNst = C::kNst;
-    constexpr int kThreads = threads_for<DH>();
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ unsigned char smem_raw[];
+    // swizzled tiles need 1024-byte aligned bases
+    unsigned char* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
     // every barrier below completes at most one phase ahead of its waiter
     uint64_t* q_full = bars;                     // [NQB] loaders -> MMA
@@ -204,16 +275,17 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         for (int i = tid; i < kNst * kBN; i += kThreads) {
             const int s = i / kBN, r = i - s * kBN;
             *reinterpret_cast<__nv_bfloat16*>(smem + C::kOffKV + s * 2 * C::kKVBytes + C::kKVBytes +
-                                              core_off<DH>(r, A.dh >> 3) + (A.dh & 7) * 2) = one;
+                                              L::template off<kBN>(r, A.dh >> 3) + (A.dh & 7) * 2) =
+                one;
         }
     }
     if (tid == 0) {
         for (int b = 0; b < NQB; ++b) {
-            mbar_init(q_full + b, kLoadWarps * 32);
+            mbar_init(q_full + b, kLoadThreads + 1);
             mbar_init(q_empty + b, 1);
         }
         for (int s = 0; s < kNst; ++s) {
-            mbar_init(kv_full + s, kLoadWarps * 32);
+            mbar_init(kv_full + s, kLoadThreads + 1);
             mbar_init(kv_empty + s, 1);
         }
         for (int g = 0; g < NQ; ++g) {
@@ -225,6 +297,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
             mbar_init(o_free + g, 128);
         }
         fence_mbar_init();
+        if (A.use_tma)
+            for (int i = 0; i < kMaps; ++i)
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&M.m[i]))
+                             : "memory");
     }
     if (warp == 0) {
         tmem_alloc(tmem_slot, C::kTmemCols);
@@ -241,40 +317,75 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         // ------------------------------------------------ loader warps
         uint32_t q_use = 0, kv_it = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode<NQ>(A, item);
+            const Item it = decode(A, item);
             const int qb = q_use % NQB;
             PROF_WAIT(10, mbar_wait(q_empty + qb, ((q_use / NQB) & 1) ^ 1));
             const uint32_t qdst = sm_base + C::kOffQ + qb * NQ * C::kQBytes;
-            for (int i = tid; i < it.nq * kBM; i += kLoadWarps * 32) {
-                const int g = i >> 7, r = i & (kBM - 1);
-                gather_row<DH>(A, A.q, A.ld_q, it, it.q0 + i, qdst + g * C::kQBytes, r);
+            {
+                int run[NQ];
+                uint32_t bytes = 0;
+#pragma unroll
+                for (int g = 0; g < NQ; ++g) {
+                    run[g] = -1;
+                    if (g < it.nq) {
+                        run[g] = A.use_tma ? tile_run(A, it, it.q0 + g * kBM, kBM) : -1;
+                        if (run[g] < 0)
+                            gather_rows<DH, kBM>(A, A.q, A.ld_q, it, it.q0 + g * kBM,
+                                                 qdst + g * C::kQBytes, tid);
+                        else
+                            bytes += kBM * A.dh * 2;
+                    }
+                }
+                cp_async_arrive(q_full + qb);
+                if (tid == 0) {
+                    if (bytes) {
+                        mbar_arrive_expect(q_full + qb, bytes);
+#pragma unroll
+                        for (int g = 0; g < NQ; ++g)
+                            if (run[g] >= 0)
+                                tma_rows<DH, kBM>(M, 0, A, it.h, run[g], qdst + g * C::kQBytes,
+                                                  q_full + qb);
+                    } else {
+                        mbar_arrive(q_full + qb);
+                    }
+                }
             }
-            cp_async_arrive(q_full + qb);
             ++q_use;
             for (int j = 0; j < it.nt; ++j, ++kv_it) {
                 const int s = kv_it % kNst;
                 const uint32_t u = kv_it / kNst;
                 PROF_WAIT(9, mbar_wait(kv_empty + s, (u & 1) ^ 1));
                 const uint32_t kb = sm_base + C::kOffKV + s * 2 * C::kKVBytes;
-                for (int i = tid; i < 2 * kBN; i += kLoadWarps * 32) {
-                    const int isv = i >> 6, r = i & (kBN - 1);
-                    gather_row<DH>(A, isv ? A.v : A.k, isv ? A.ld_v : A.ld_k, it, j * kBN + r,
-                                   kb + isv * C::kKVBytes, r);
+                const int run = A.use_tma ? tile_run(A, it, j * kBN, kBN) : -1;
+                if (run < 0) {
+                    gather_rows<DH, kBN>(A, A.k, A.ld_k, it, j * kBN, kb, tid);
+                    gather_rows<DH, kBN>(A, A.v, A.ld_v, it, j * kBN, kb + C::kKVBytes, tid);
                 }
                 cp_async_arrive(kv_full + s);
+                if (tid == 0) {
+                    if (run >= 0) {
+                        mbar_arrive_expect(kv_full + s, 2 * kBN * A.dh * 2);
+                        tma_rows<DH, kBN>(M, 2, A, it.h, run, kb, kv_full + s);
+                        tma_rows<DH, kBN>(M, 4, A, it.h, run, kb + C::kKVBytes, kv_full + s);
+                    } else {
+                        mbar_arrive(kv_full + s);
+                    }
+                }
             }
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA warp
         // The whole warp walks the schedule (warp-uniform control flow and
-        // waits); one elected lane issues every tcgen05.mma / commit.  Descriptors are
-        // built once: per tile only the 14-bit start-address field moves
-        // (addresses < 2^18, so adding (bytes >> 4) never carries out).
+        // waits); one elected lane issues every tcgen05.mma / commit.
+        // Descriptors are built once: per tile only the 14-bit start-address
+        // field moves (addresses < 2^18, so adding (bytes >> 4) never carries).
         constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
         constexpr uint32_t idPV = idesc_bf16(kBM, DH, 0, 1);
-        const uint64_t dQ = smem_desc(sm_base + C::kOffQ, 128, 16 * DH);
-        const uint64_t dK = smem_desc(sm_base + C::kOffKV, 128, 16 * DH);
-        const uint64_t dV = smem_desc(sm_base + C::kOffKV + C::kKVBytes, 16 * DH, 128);
+        // K-major Q / K: rows of SW bytes, 8-row groups SBO = 8*SW apart
+        const uint64_t dQ = sw_desc(sm_base + C::kOffQ, 16, 8 * L::SW, L::LT);
+        const uint64_t dK = sw_desc(sm_base + C::kOffKV, 16, 8 * L::SW, L::LT);
+        // MN-major V: LBO = column-block stride, SBO = 8-key group stride
+        const uint64_t dV = sw_desc(sm_base + C::kOffKV + C::kKVBytes, kBN * L::SW, 8 * L::SW, L::LT);
         constexpr uint32_t kStageD = (2 * C::kKVBytes) >> 4;   // descriptor step per K/V stage
         constexpr uint32_t kQD = C::kQBytes >> 4;              // per Q tile
         uint32_t q_use = 0, kv_it = 0;
@@ -282,9 +393,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
 #pragma unroll
         for (int g = 0; g < NQ; ++g) tg[g] = ig[g] = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode<NQ>(A, item);
+            const Item it = decode(A, item);
             const int qb = q_use % NQB;
             PROF_WAIT(4, mbar_wait(q_full + qb, (q_use / NQB) & 1));
+            tc_fence_after();
             const uint64_t dq = dQ + (uint64_t)(qb * NQ * kQD);
             // S_g,j -> TMEM buffer (tg[g]+j)%NSB, which last held P_g,j-NSB:
             // PV_g,j-NSB was issued before (tcgen05.mma executes in order).
@@ -296,8 +408,13 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 const uint32_t d = tmem + C::kTmemS + (NSB * g + b) * kBN;
                 if (elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < DH / 16; ++k)
-                        umma_f16(d, dqg + (uint64_t)(16 * k), dk + (uint64_t)(16 * k), idS, k > 0);
+                    for (int k = 0; k < DH / 16; ++k) {
+                        // K-step k: column block k*16/BW, 32-byte step inside the swizzled row
+                        constexpr int kPerBlk = L::BW / 16;
+                        const uint32_t oq = (uint32_t)(((k / kPerBlk) * kBM * L::SW + (k % kPerBlk) * 32) >> 4);
+                        const uint32_t ok = (uint32_t)(((k / kPerBlk) * kBN * L::SW + (k % kPerBlk) * 32) >> 4);
+                        umma_f16(d, dqg + oq, dk + ok, idS, k > 0);
+                    }
                     umma_commit(s_full + NSB * g + b);
                 }
                 __syncwarp();
@@ -331,8 +448,8 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                     const uint32_t od = tmem + C::kTmemO + g * DH;
                     if (elect_one()) {
 #pragma unroll
-                        for (int k = 0; k < kBN / 16; ++k)
-                            umma_f16_ts(od, pa + k * 8, dv + (uint64_t)(2 * DH * k), idPV,
+                        for (int k = 0; k < kBN / 16; ++k)   // 16 keys = two 8-key groups
+                            umma_f16_ts(od, pa + k * 8, dv + (uint64_t)((16 * L::SW * k) >> 4), idPV,
                                         (j > 0 || k > 0) ? 1u : 0u);
                         umma_commit(pv_done + NSB * g + t % NSB);
                     }
@@ -367,7 +484,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
         const uint32_t obase = tmem + lane_base + C::kTmemO + g * DH;
         uint32_t tg = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode<NQ>(A, item);
+            const Item it = decode(A, item);
             if (g >= it.nq) continue;                     // this Q tile is past the scope
             float ms = -INFINITY, l = 0.f;                // running max (scaled, log2), sum
             for (int j = 0; j < it.nt; ++j) {
@@ -375,9 +492,6 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                 const int b = t % NSB;
                 const uint32_t sb = tmem + lane_base + C::kTmemS + (NSB * g + b) * kBN;
                 PROF_WAIT(1, mbar_wait(s_full + NSB * g + b, (t / NSB) & 1));
-#if F3D_EXPERIMENT == 3
-                if (lane == 0) prof[12] += 1;
-#endif
                 tc_fence_after();
                 uint32_t x[kBN];
                 {
@@ -393,10 +507,13 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                     for (int e = 0; e < kBN; ++e)
                         if (e >= kvalid) x[e] = __float_as_uint(-INFINITY);
                 }
-                float mx = -INFINITY;
+                float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-                for (int e = 0; e < kBN; ++e) mx = fmaxf(mx, __uint_as_float(x[e]));
-                const float mxs = mx * sl2;
+                for (int e = 0; e < kBN; e += 2) {
+                    mx0 = fmaxf(mx0, __uint_as_float(x[e]));
+                    mx1 = fmaxf(mx1, __uint_as_float(x[e + 1]));
+                }
+                const float mxs = fmaxf(mx0, mx1) * sl2;
                 if (j == 0) {
                     ms = mxs;
                 } else {
@@ -404,9 +521,6 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
                     if (__any_sync(0xffffffffu, need)) {
                         // O_g must hold P_g,j-1 V before it is rescaled in place
                         PROF_WAIT(2, mbar_wait(pv_done + NSB * g + (t - 1) % NSB, ((t - 1) / NSB) & 1));
-#if F3D_EXPERIMENT == 3
-                        if (lane == 0) prof[13] += 1;
-#endif
                         tc_fence_after();
                         const float alpha = need ? ex2f(ms - mxs) : 1.f;
                         if (need) {
@@ -507,9 +621,48 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1) bswin_attn_tc_kernel(con
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
 }
 
+// ------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                             CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeFn)p;
+    }
+    return fn;
+}
+
+// 2-D map over rows [0, n) x columns [0, ncols) of a bf16 matrix with row
+// stride ld; box = {bw columns, 64 rows}, swizzled like Lay<DH>.
+static bool make_map(CUtensorMap* m, const void* base, int64_t ld, int64_t ncols, int64_t n,
+                     int bw, int sw_bytes) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)ncols, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {(cuuint32_t)bw, 64};
+    cuuint32_t es[2] = {1, 1};
+    const CUtensorMapSwizzle sw = sw_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : sw_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                   : CU_TENSOR_MAP_SWIZZLE_32B;
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int DH, typename OutT>
-int launch(const Args& A, cudaStream_t st) {
+int launch(Args A, int64_t n_rows, cudaStream_t st) {
     using C = Cfg<DH>;
+    using LY = Lay<DH>;
     auto kern = bswin_attn_tc_kernel<DH, OutT>;
     static bool attr = false;
     if (!attr) {
@@ -517,16 +670,30 @@ int launch(const Args& A, cudaStream_t st) {
                                           C::kSmem));
         attr = true;
     }
+    Maps M;
+    memset(&M, 0, sizeof(M));
+    // TMA boxes cover the head's own columns: blocks of BW, the last one
+    // possibly narrower (dh < DH); pad columns of the tiles stay zero
+    const int64_t ncols = (int64_t)A.H * A.dh;
+    A.use_tma = n_rows > 0 ? 1 : 0;
+    const void* bases[3] = {A.q, A.k, A.v};
+    const int64_t lds[3] = {A.ld_q, A.ld_k, A.ld_v};
+    for (int t = 0; t < 3 && A.use_tma; ++t)
+        for (int b = 0; b < 2; ++b) {
+            const int w = std::min(LY::BW, A.dh - b * LY::BW);
+            if (w <= 0) continue;
+            if (!make_map(&M.m[2 * t + b], bases[t], lds[t], ncols, n_rows, w, LY::SW)) A.use_tma = 0;
+        }
     const int total = A.nwork * A.H;
     const int grid = std::max(1, std::min(total, f3d_num_sms()));
-    kern<<<grid, threads_for<DH>(), C::kSmem, st>>>(A);
+    kern<<<grid, kThreads, C::kSmem, st>>>(A, M);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
 
 template <int DH>
-int launch_dh(const Args& A, cudaStream_t st) {
-    return A.out_f32 ? launch<DH, float>(A, st) : launch<DH, __nv_bfloat16>(A, st);
+int launch_dh(const Args& A, int64_t n_rows, cudaStream_t st) {
+    return A.out_f32 ? launch<DH, float>(A, n_rows, st) : launch<DH, __nv_bfloat16>(A, n_rows, st);
 }
 
 }  // namespace attn_tc
@@ -546,9 +713,8 @@ extern "C" int f3d_attn_prof(unsigned long long* out16_host, int reset) {
 #endif
 
 extern "C" int f3d_attention_tc_qstep(int dh) {
-    const int dp = (dh + 15) / 16 * 16;
-    const int nq = (F3D_SMALL_NQ3 && dp <= 32) ? 3 : 2;
-    return nq * f3d::attn_tc::kBM;
+    (void)dh;
+    return f3d::attn_tc::kNQ * f3d::attn_tc::kBM;
 }
 
 extern "C" int f3d_bswin_attention_tc(const void* q, const void* k, const void* v, int64_t ld_q,
@@ -557,8 +723,8 @@ extern "C" int f3d_bswin_attention_tc(const void* q, const void* k, const void* 
                                       const int32_t* scope_nseg, const int32_t* seg_start,
                                       const int32_t* seg_vstart, const int32_t* scope_len,
                                       const int32_t* work, int nwork, const int32_t* live,
-                                      void* stream) {
-    if (H < 1 || dh < 8 || dh > 128 || (dh & 7) || nwork < 0) return F3D_ERR_CONFIG;
+                                      int64_t n_rows, void* stream) {
+    if (H < 1 || dh < 8 || dh > 128 || (dh & 7) || nwork < 0 || n_rows < 0) return F3D_ERR_CONFIG;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v) & 15) return F3D_ERR_CONFIG;
     if ((ld_q | ld_k | ld_v) & 7) return F3D_ERR_CONFIG;
     if (nwork == 0) return F3D_OK;
@@ -583,16 +749,13 @@ extern "C" int f3d_bswin_attention_tc(const void* q, const void* k, const void* 
     A.work = work;
     A.nwork = nwork;
     A.live = live;
+    A.use_tma = 0;
     cudaStream_t st = (cudaStream_t)stream;
-    switch ((dh + 15) / 16 * 16) {
-        case 16: return attn_tc::launch_dh<16>(A, st);
-        case 32: return attn_tc::launch_dh<32>(A, st);
-        case 48: return attn_tc::launch_dh<48>(A, st);
-        case 64: return attn_tc::launch_dh<64>(A, st);
-        case 80: return attn_tc::launch_dh<80>(A, st);
-        case 96: return attn_tc::launch_dh<96>(A, st);
-        case 112: return attn_tc::launch_dh<112>(A, st);
-        case 128: return attn_tc::launch_dh<128>(A, st);
+    switch (attn_tc::dh_tile(dh)) {
+        case 16: return attn_tc::launch_dh<16>(A, n_rows, st);
+        case 32: return attn_tc::launch_dh<32>(A, n_rows, st);
+        case 64: return attn_tc::launch_dh<64>(A, n_rows, st);
+        case 128: return attn_tc::launch_dh<128>(A, n_rows, st);
         default: return F3D_ERR_CONFIG;
     }
 }
