@@ -44,8 +44,8 @@ def peaks():
 
 
 def workload(rank):
-    from oracle.restated import synth_cloud   # input generation only (same PCG64 draws)
-    coords = synth_cloud(7 + rank, N_POINTS, "uniform-box")
+    from paper_2412_16481_b200.geometry import synth_cloud   # bw/geometry.py:183-212 draws
+    coords = synth_cloud(7 + rank, N_POINTS, "uniform-box").coords
     feats = np.random.default_rng(1 + rank).normal(size=(N_POINTS, D_MODEL))
     return coords, feats
 
@@ -156,6 +156,56 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------- GPU leg
+
+def wide_attention_roofline(tflops_peak, iters=5):
+    """Config D attention (BASELINE.json configs[3]): the
+    1M-point synth_cloud(7) scene at voxel 1/128, PSH K=1280 S=1024
+    S_div=1639, W=4 (scopes up to 4096 rows), C=512, H=4 (dh=128); random
+    bf16 Q/K/V rows in the scattered layout, both rounds of the schedule.
+    Algorithmic FLOPs = sum over scopes of 4 m^2 C; each launch reads
+    ~3 GB of Q/K/V (> L2), so no flush is needed between launches."""
+    import torch
+    from paper_2412_16481_b200.attention import DeviceRoundPlan, attend, qstep_for
+    from paper_2412_16481_b200.backbone import Backbone, StageConfig
+    from paper_2412_16481_b200.geometry import synth_cloud
+    n, d, H = 1_000_000, 512, 4
+    cfg = StageConfig(voxel=1 / 128, K=1280, S=1024, S_div=1639, W=4, d_model=d, n_heads=H)
+    C = torch.tensor(synth_cloud(7, n, "uniform-box").coords, device="cuda")
+    asg, _, _ = Backbone.bucketize(Backbone.__new__(Backbone), C, cfg)
+    nb_cap = cfg.K + -(-n // cfg.S)
+    plans = [DeviceRoundPlan(asg._dev["counts"], asg._dev["base"], cfg.K, cfg.S, nb_cap, cfg.W,
+                             cfg.stride, cfg.shift, t, n, qstep=qstep_for(d // H)) for t in range(2)]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    qkv = torch.randn((n, 3 * d), device="cuda", generator=g).to(torch.bfloat16)
+    q, k, v = (qkv[:, i * d:(i + 1) * d] for i in range(3))
+    out = torch.empty((n, d), device="cuda", dtype=torch.bfloat16)
+    flops = 0.0
+    for p in plans:
+        ln = p.scope_len.to(torch.float64)
+        flops += 4.0 * float((ln * ln).sum().item()) * d
+    for p in plans:
+        attend(q, k, v, out, p, H, d // H)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for p in plans:
+            attend(q, k, v, out, p, H, d // H)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    best = statistics.median(ms)
+    tf = flops / (best * 1e-3) / 1e12
+    del qkv, out
+    torch.cuda.empty_cache()
+    return {"kernel": "f3d_bswin_attention_tc", "bound": "tensor", "achieved": round(tf, 1),
+            "peak": tflops_peak, "unit": "TFLOP/s", "frac": round(tf / tflops_peak, 4),
+            "traffic": None, "workload": "config D: 1M points, K=1280 S=1024 W=4, C=512 H=4 "
+                                         "(dh=128), 2 rounds, bf16 operands, fp32 accumulate",
+            "flops_per_step": flops, "ms_per_step": round(best, 3),
+            "launches_per_step": len(plans)}
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -338,6 +388,7 @@ def main():
                     "ms_per_step": e2e_ms_max},
             "clocks": clk.summary(),
         }
+        line["roofline_wide"] = wide_attention_roofline(tflops)
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(coords, feats)
         print(json.dumps(line), flush=True)

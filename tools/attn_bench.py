@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
-from oracle.restated import synth_cloud  # noqa: E402  (input generation only)
+from paper_2412_16481_b200.geometry import synth_cloud  # noqa: E402
 from paper_2412_16481_b200.attention import DeviceRoundPlan, attend, qstep_for  # noqa: E402
 from paper_2412_16481_b200.backbone import Backbone, StageConfig  # noqa: E402
 
@@ -42,7 +42,7 @@ def main():
     d = a.d or cfg.d_model
     n = spec["n"]
     torch.cuda.set_device(0)
-    C = torch.tensor(synth_cloud(7, n, "uniform-box"), device="cuda")
+    C = torch.tensor(synth_cloud(7, n, "uniform-box").coords, device="cuda")
     bb = Backbone.__new__(Backbone)
     asg, _, _ = Backbone.bucketize(bb, C, cfg)
     counts_h = asg._dev["counts"].cpu().numpy()

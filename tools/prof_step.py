@@ -1,6 +1,7 @@
-"""One profiled backbone forward (config B) for ncu:
+"""One profiled config-B backbone step for ncu, replayed from the captured
+CUDA graphs exactly as bench.py times it:
     ncu --profile-from-start off ... python tools/prof_step.py
-Warm-up steps run outside the cudaProfilerStart/Stop window."""
+Capture and warm-up run outside the cudaProfilerStart/Stop window."""
 import os
 import sys
 
@@ -15,14 +16,17 @@ from paper_2412_16481_b200.backbone import Backbone  # noqa: E402
 steps = int(os.environ.get("PROF_STEPS", "1"))
 coords, feats = bench.workload(0)
 C = torch.tensor(coords, device="cuda")
-X = torch.tensor(feats, dtype=torch.float32, device="cuda")
+X = torch.tensor(feats, dtype=torch.bfloat16, device="cuda")
 bb = Backbone()
+bb.capture(C.shape[0], torch.bfloat16)
+bb.graph_coords.copy_(C)
+bb.graph_feats.copy_(X)
 for _ in range(3):
-    bb.forward(C, X)
+    bb.replay()
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
 for _ in range(steps):
-    bb.forward(C, X)
+    bb.replay()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("profiled", steps, "step(s)")
+print("profiled", steps, "step(s); rows out", bb.check_graph())
