@@ -52,14 +52,22 @@ __global__ void bbox_partial_kernel(const double* __restrict__ c, int64_t n,
 }
 
 // lo[3], ext[3] with ext == 0 -> 1 (bw/stage.py:129-131)
+// one warp per axis: lanes stride over the partial results (min / max are
+// exact in any order)
 __global__ void bbox_final_kernel(const double* part, int nparts, double* lo_ext) {
-    if (threadIdx.x >= 3) return;
-    const int a = threadIdx.x;
+    const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (a >= 3) return;
     double mn = DBL_MAX, mx = -DBL_MAX;
-    for (int j = 0; j < nparts; ++j) {
+    for (int j = lane; j < nparts; j += 32) {
         mn = fmin(mn, part[6 * j + a]);
         mx = fmax(mx, part[6 * j + 3 + a]);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane) return;
     double e = __dsub_rn(mx, mn);
     if (e == 0.0) e = 1.0;
     lo_ext[a] = mn;
@@ -183,12 +191,14 @@ __device__ __forceinline__ float gelu_f(float x) {
     return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
 }
 
-// 16-byte vector form: 8 bf16 per thread (dh % 8 == 0).
-__global__ void bias_gelu8_kernel(uint4* __restrict__ u, int64_t n8, int dh8,
+// 16-byte vector form: 8 bf16 per thread (dh % 8 == 0).  IT = uint32_t when
+// the element count allows it (a 64-bit modulo per vector costs more than the
+// GELU itself).
+template <typename IT>
+__global__ void bias_gelu8_kernel(uint4* __restrict__ u, IT n8, int dh8,
                                   const float4* __restrict__ b) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n8;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int c8 = (int)(t % dh8);
+    for (IT t = (IT)blockIdx.x * blockDim.x + threadIdx.x; t < n8; t += (IT)gridDim.x * blockDim.x) {
+        const int c8 = (int)(t % (IT)dh8);
         uint4 w = u[t];
         const float4 b0 = b[2 * c8], b1 = b[2 * c8 + 1];
         const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
@@ -235,7 +245,7 @@ extern "C" int f3d_coord_bbox(const double* coords, int64_t n, double* ws, doubl
     cudaStream_t st = (cudaStream_t)stream;
     const int parts = (int)std::min<int64_t>((n + 1023) / 1024, 296);
     stage::bbox_partial_kernel<<<parts, stage::kThreads, 0, st>>>(coords, n, n_dev, ws);
-    stage::bbox_final_kernel<<<1, 32, 0, st>>>(ws, parts, lo_ext);
+    stage::bbox_final_kernel<<<1, 96, 0, st>>>(ws, parts, lo_ext);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
@@ -261,6 +271,152 @@ extern "C" int f3d_stage_pe(const double* coords, int64_t n, int d, double base,
                                                                (float*)out, ld);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
+}
+
+namespace f3d {
+namespace stage {
+
+// Vector form of row_ln for the pipeline's common case: fp32 residual rows,
+// bf16 y / out, d % 4 == 0, d <= 128.  Lane q owns columns [4q, 4q+4) (one
+// 16-byte F load, one 8-byte y load); each warp carries RPW rows at once so
+// every load of all of them is in flight before the first reduction.
+template <int RPW, bool HAS_Y, bool HAS_OUT, bool HAS_PE>
+__global__ void __launch_bounds__(kThreads) row_ln_vec_kernel(
+    float* __restrict__ F, int64_t ldf, const __nv_bfloat16* __restrict__ y, int64_t ldy,
+    const float* __restrict__ ybias, const float* __restrict__ gain,
+    const float* __restrict__ beta, const double* __restrict__ pec,
+    const double* __restrict__ lo_ext, float pl2, __nv_bfloat16* __restrict__ out, int64_t ldo,
+    int64_t n, int d, float eps) {
+    const int lane = threadIdx.x & 31;
+    const bool act = lane < (d >> 2);
+    const int64_t row0 = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * RPW;
+    const int c0 = 4 * lane;
+    float4 v[RPW];
+    uint2 yy[RPW];
+    double pc[RPW][3];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int64_t row = row0 + i;
+        const bool ok = act && row < n;
+        v[i] = ok ? *reinterpret_cast<const float4*>(F + row * ldf + c0) : make_float4(0, 0, 0, 0);
+        if (HAS_Y) yy[i] = ok ? *reinterpret_cast<const uint2*>(y + row * ldy + c0) : make_uint2(0, 0);
+        if (HAS_PE && HAS_OUT) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) pc[i][a] = (row < n) ? pec[3 * row + a] : 0.0;
+        }
+    }
+    if (HAS_Y) {
+        const float4 yb = (ybias && act) ? *reinterpret_cast<const float4*>(ybias + c0)
+                                         : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&yy[i]);
+            const float2 y01 = __bfloat1622float2(h[0]), y23 = __bfloat1622float2(h[1]);
+            v[i].x += y01.x + yb.x;
+            v[i].y += y01.y + yb.y;
+            v[i].z += y23.x + yb.z;
+            v[i].w += y23.y + yb.w;
+            const int64_t row = row0 + i;
+            if (act && row < n) *reinterpret_cast<float4*>(F + row * ldf + c0) = v[i];
+        }
+    }
+    if (!HAS_OUT) return;
+    float s[RPW], q[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) s[i] = (v[i].x + v[i].y) + (v[i].z + v[i].w);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+    const float inv_d = 1.f / (float)d;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const float m = s[i] * inv_d;
+        const float a = act ? v[i].x - m : 0.f, b = act ? v[i].y - m : 0.f;
+        const float c = act ? v[i].z - m : 0.f, e = act ? v[i].w - m : 0.f;
+        q[i] = (a * a + b * b) + (c * c + e * e);
+        s[i] = m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
+    if (!act) return;
+    const float4 gg = *reinterpret_cast<const float4*>(gain + c0);
+    const float4 bb = *reinterpret_cast<const float4*>(beta + c0);
+    // PE: columns (c0, c0+1) and (c0+2, c0+3) are (sin, cos) pairs (d % 6 == 0,
+    // so blk = d/3 is even); bw/attention.py:271-288 on the bbox-normalised
+    // coordinate (bw/stage.py:129-132)
+    const int npair = d / 6, blk = 2 * npair;
+    int pa[2], pj[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int c = c0 + 2 * p;
+        pa[p] = c / blk;
+        pj[p] = (c - pa[p] * blk) >> 1;
+    }
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int64_t row = row0 + i;
+        if (row >= n) break;
+        const float rstd = rsqrtf(q[i] * inv_d + eps);
+        const float m = s[i];
+        float o0 = (v[i].x - m) * rstd * gg.x + bb.x;
+        float o1 = (v[i].y - m) * rstd * gg.y + bb.y;
+        float o2 = (v[i].z - m) * rstd * gg.z + bb.z;
+        float o3 = (v[i].w - m) * rstd * gg.w + bb.w;
+        if (HAS_PE) {
+            float sn[2], cs[2];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                double x = pc[i][pa[p]];
+                if (lo_ext) x = __ddiv_rn(__dsub_rn(x, lo_ext[pa[p]]), lo_ext[3 + pa[p]]);
+                const float ang = (float)x * exp2f(-(float)pj[p] / (float)npair * pl2);
+                __sincosf(ang, &sn[p], &cs[p]);
+            }
+            o0 += sn[0];
+            o1 += cs[0];
+            o2 += sn[1];
+            o3 += cs[1];
+        }
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(o0, o1), h1 = __floats2bfloat162_rn(o2, o3);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(out + row * ldo + c0) = w;
+    }
+}
+
+}  // namespace stage
+}  // namespace f3d
+
+// returns false when the vector form does not apply
+static bool launch_row_ln_vec(cudaStream_t st, void* F, int64_t ldf, const void* y, int64_t ldy,
+                              const float* ybias, const float* gain, const float* beta,
+                              const double* pec, const double* lo_ext, float pl2, void* out,
+                              int64_t ldo, int64_t n, int d, double eps) {
+    auto al = [](const void* p, int a) { return ((uintptr_t)p % a) == 0; };
+    if (d % 4 || d > 128 || ldf % 4 || !al(F, 16)) return false;
+    if (y && (ldy % 4 || !al(y, 8) || (ybias && !al(ybias, 16)))) return false;
+    if (out && (ldo % 4 || !al(out, 8) || !al(gain, 16) || !al(beta, 16))) return false;
+    constexpr int RPW = 2;
+    const unsigned g = (unsigned)((n + RPW * 8 - 1) / (RPW * 8));
+    using BF = __nv_bfloat16;
+    float* Ff = (float*)F;
+    const BF* yb = (const BF*)y;
+    BF* ob = (BF*)out;
+    const float fe = (float)eps;
+#define F3D_LNV(HY, HO, HP)                                                                       \
+    stage::row_ln_vec_kernel<RPW, HY, HO, HP><<<g, stage::kThreads, 0, st>>>(                     \
+        Ff, ldf, yb, ldy, ybias, gain, beta, pec, lo_ext, pl2, ob, ldo, n, d, fe)
+    if (y && out && pec) F3D_LNV(true, true, true);
+    else if (y && out) F3D_LNV(true, true, false);
+    else if (y) F3D_LNV(true, false, false);
+    else if (out && pec) F3D_LNV(false, true, true);
+    else if (out) F3D_LNV(false, true, false);
+    else return true;
+#undef F3D_LNV
+    return true;
 }
 
 template <typename FT, typename OT, int PER>
@@ -325,6 +481,12 @@ extern "C" int f3d_row_ln(void* F, int f_is_f64, int64_t ldf, const void* y, int
     if (out && (!gain || !beta)) return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (!f_is_f64 && (out_kind == 0 || !out) &&
+        launch_row_ln_vec(st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, out, ldo, n, d,
+                          eps)) {
+        F3D_LAUNCH_CHECK();
+        return F3D_OK;
+    }
     const unsigned g = (unsigned)((n + stage::kThreads / 32 - 1) / (stage::kThreads / 32));
     if (f_is_f64)
         launch_row_ln<double>(g, st, F, ldf, y, ldy, ybias, gain, beta, pec, lo_ext, pl2, out,
@@ -363,8 +525,14 @@ extern "C" int f3d_bias_gelu(void* u_bf16, int64_t n, int dh, const float* bias,
     cudaStream_t st = (cudaStream_t)stream;
     if (dh % 8 == 0 && ((uintptr_t)u_bf16 & 15) == 0 && ((uintptr_t)bias & 15) == 0) {
         const int64_t n8 = n * dh / 8;
-        stage::bias_gelu8_kernel<<<grid_for(n8, stage::kThreads), stage::kThreads, 0, st>>>(
-            (uint4*)u_bf16, n8, dh / 8, (const float4*)bias);
+        if (n8 < (int64_t)1 << 31)
+            stage::bias_gelu8_kernel<uint32_t><<<grid_for(n8, stage::kThreads), stage::kThreads, 0,
+                                                 st>>>((uint4*)u_bf16, (uint32_t)n8, dh / 8,
+                                                       (const float4*)bias);
+        else
+            stage::bias_gelu8_kernel<int64_t><<<grid_for(n8, stage::kThreads), stage::kThreads, 0,
+                                                st>>>((uint4*)u_bf16, n8, dh / 8,
+                                                      (const float4*)bias);
     } else {
         stage::bias_gelu_kernel<<<grid_for(n * dh / 2, stage::kThreads), stage::kThreads, 0, st>>>(
             (__nv_bfloat16*)u_bf16, n, dh, bias);
