@@ -41,7 +41,9 @@
 #define F3D_EXPERIMENT 0   // developer A/B knob (tools/): 1 no loads, 2 no exp,
 #endif                     // 3 per-role wait-cycle counters (f3d_attn_prof)
 #if F3D_EXPERIMENT == 3
-__device__ unsigned long long g_attn_prof[16];
+__device__ unsigned long long g_attn_prof[24];
+#define PROF_MARK(var) const long long var = clock64()
+#define PROF_ADD(slot, a, b) if ((threadIdx.x & 31) == 0) prof[slot] += (b) - (a)
 #define PROF_WAIT(slot, call)                                            \
     do {                                                                 \
         const long long _t0 = clock64();                                 \
@@ -50,6 +52,8 @@ __device__ unsigned long long g_attn_prof[16];
     } while (0)
 #else
 #define PROF_WAIT(slot, call) call
+#define PROF_MARK(var)
+#define PROF_ADD(slot, a, b)
 #endif
 
 namespace f3d {
@@ -66,6 +70,27 @@ constexpr int kMmaWarp = 3;       // completes warpgroup 0
 constexpr int kThreads = (4 + 4 * kNQ) * 32;
 constexpr float kRescale = 8.f;   // move the running max only when it grows by > 2^8
 constexpr int kMaps = 6;          // TMA maps: {q, k, v} x {first block, second block}
+// 1 pair in poly_every<DH>() uses ex2_poly (0: none).  Measured (config B
+// dh=24: 2 % faster with 1 in 4; config D dh=128: 7 % slower): the softmax is
+// issue-bound, not MUFU-bound, once dh >= 64.
+template <int DH>
+__host__ __device__ constexpr int poly_every() {
+    return DH <= 32 ? 4 : 0;
+}
+
+// 2^x on the FMA/ALU pipes for x <= 2^8 (softmax arguments): round x to
+// j = rint(x) with the 1.5*2^23 trick, 2^f for f in [-0.5, 0.5] by a cubic
+// (relative error <= 8e-4, below the bf16 rounding of P), exponent added
+// as an integer.  Arguments below -127 flush to 0 like ex2.approx.ftz.
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -127.f);
+    const float t = __fadd_rn(x, 12582912.f);
+    const float f = __fsub_rn(x, __fsub_rn(t, 12582912.f));
+    float p = fmaf(0.0555041086648216f, f, 0.2402264923172690f);
+    p = fmaf(p, f, 0.6931471805599453f);
+    p = fmaf(p, f, 1.f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 
 __host__ __device__ constexpr int dh_tile(int dh) {   // padded head dim of the kernel
     return dh <= 16 ? 16 : dh <= 32 ? 32 : dh <= 64 ? 64 : 128;
@@ -262,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int total = (A.live ? __ldg(A.live) : A.nwork) * A.H;
     const bool ones = A.dh < DH;                 // V column dh = 1 -> O column dh = row sum
 #if F3D_EXPERIMENT == 3
-    unsigned long long prof[16] = {0};
+    unsigned long long prof[24] = {0};
     const long long t_start = clock64();
 #endif
 
@@ -497,10 +522,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 {
                     uint32_t (&x0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[0]);
                     uint32_t (&x1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[32]);
+                    PROF_MARK(tl0);
                     tmem_ld32(sb, x0);
                     tmem_ld32(sb + 32, x1);
                     tmem_wait_ld();
+                    PROF_MARK(tl1);
+                    PROF_ADD(16, tl0, tl1);
                 }
+                PROF_MARK(tm0);
                 const int kvalid = it.m - j * kBN;        // keys < kvalid are real
                 if (kvalid < kBN) {
 #pragma unroll
@@ -514,6 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mx1 = fmaxf(mx1, __uint_as_float(x[e + 1]));
                 }
                 const float mxs = fmaxf(mx0, mx1) * sl2;
+                PROF_MARK(tm1);
+                PROF_ADD(17, tm0, tm1);
                 if (j == 0) {
                     ms = mxs;
                 } else {
@@ -541,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 // P = exp2(s*sl2 - ms) (<= 2^8) -> bf16 pairs over the S columns
                 const float nms = -ms;
-                uint32_t pk[kBN / 2];
+                PROF_MARK(te0);
                 float sum = 0.f;
 #pragma unroll
                 for (int e = 0; e < kBN; e += 2) {
@@ -549,18 +580,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float p0 = fmaf(__uint_as_float(x[e]), sl2, nms);
                     const float p1 = fmaf(__uint_as_float(x[e + 1]), sl2, nms);
 #else
-                    const float p0 = ex2f(fmaf(__uint_as_float(x[e]), sl2, nms));
-                    const float p1 = ex2f(fmaf(__uint_as_float(x[e + 1]), sl2, nms));
+                    // every kPolyEvery-th pair on the FMA pipe: the MUFU unit
+                    // (16 ex2/clk/SM) is the softmax roof at small head dims
+                    const float a0 = fmaf(__uint_as_float(x[e]), sl2, nms);
+                    const float a1 = fmaf(__uint_as_float(x[e + 1]), sl2, nms);
+                    constexpr int kPE = poly_every<DH>();
+                    const bool poly = kPE > 0 && ((e >> 1) % (kPE > 0 ? kPE : 1)) == kPE - 1;
+                    const float p0 = poly ? ex2_poly(a0) : ex2f(a0);
+                    const float p1 = poly ? ex2_poly(a1) : ex2f(a1);
 #endif
                     if (!ones) sum += p0 + p1;
                     __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                    pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+                    x[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);   // in place: x[e/2] consumed
                 }
                 l += sum;
-                tmem_st32(sb, pk);
+                PROF_MARK(te1);
+                PROF_ADD(18, te0, te1);
+                tmem_st32(sb, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(p_full + NSB * g + b);
+                PROF_MARK(te2);
+                PROF_ADD(19, te1, te2);
             }
             // O_g complete: normalise and write the row
             {
@@ -612,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
         const int role = warp < kLoadWarps ? 11 : (warp == kMmaWarp ? 8 : 0);
         prof[role] += clock64() - t_start;
-        for (int i = 0; i < 16; ++i)
+        for (int i = 0; i < 24; ++i)
             if (prof[i]) atomicAdd(&g_attn_prof[i], prof[i]);
     }
 #endif
@@ -702,10 +743,10 @@ int launch_dh(const Args& A, int64_t n_rows, cudaStream_t st) {
 using namespace f3d;
 
 #if F3D_EXPERIMENT == 3
-extern "C" int f3d_attn_prof(unsigned long long* out16_host, int reset) {
-    cudaMemcpyFromSymbol(out16_host, g_attn_prof, sizeof(g_attn_prof));
+extern "C" int f3d_attn_prof(unsigned long long* out24_host, int reset) {
+    cudaMemcpyFromSymbol(out24_host, g_attn_prof, sizeof(g_attn_prof));
     if (reset) {
-        unsigned long long z[16] = {0};
+        unsigned long long z[24] = {0};
         cudaMemcpyToSymbol(g_attn_prof, z, sizeof(z));
     }
     return 0;

@@ -31,6 +31,8 @@ constexpr int kThreads = 32 * kWarpsPerCta;
 
 struct WarpSmem {
     double sc[kCap][3];     // per sub id: seed coordinates (step-3 distances)
+    double cc[kCap][3];     // per row: the tile's coordinates (staged once)
+    uint16_t qrow[kCap];    // step-3 queue: queued rows in index order
     uint16_t cnt[kCap];     // per key running count
     int16_t idk[kCap];      // key -> sub id
     int16_t sizes[kCap];    // per sub id
@@ -93,9 +95,14 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
 
     // ---- bbox of the tile
     double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    for (int i = lane; i < 3 * m; i += 32) {   // coalesced; rows staged in smem
+        const double v = C[i];
+        (&S.cc[0][0])[i] = v;
+    }
+    __syncwarp();
     for (int i = lane; i < m; i += 32)
         for (int a = 0; a < 3; ++a) {
-            const double v = C[3 * i + a];
+            const double v = S.cc[i][a];
             lo[a] = fmin(lo[a], v);
             hi[a] = fmax(hi[a], v);
         }
@@ -119,7 +126,7 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     for (int i = lane; i < m; i += 32) {
         uint32_t q[3];
         for (int a = 0; a < 3; ++a) {
-            double v = __dmul_rn(__ddiv_rn(__dsub_rn(C[3 * i + a], lo[a]), ext[a]), 1024.0);
+            double v = __dmul_rn(__ddiv_rn(__dsub_rn(S.cc[i][a], lo[a]), ext[a]), 1024.0);
             v = fmin(v, 1023.0);
             q[a] = (uint32_t)(int64_t)v;   // truncation (values >= 0)
         }
@@ -143,9 +150,9 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
             const int id = nalloc + __popc(fb & lt);
             S.idk[k] = (int16_t)id;
             S.seeds[id] = (int16_t)i;
-            S.sc[id][0] = C[3 * i];
-            S.sc[id][1] = C[3 * i + 1];
-            S.sc[id][2] = C[3 * i + 2];
+            S.sc[id][0] = S.cc[i][0];
+            S.sc[id][1] = S.cc[i][1];
+            S.sc[id][2] = S.cc[i][2];
         }
         if (v && lane == __ffs(mm) - 1) S.cnt[k] = (uint16_t)(S.cnt[k] + __popc(mm));
         nalloc += __popc(fb);
@@ -178,11 +185,12 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
                 S.sub[i] = (int16_t)id;
                 S.sizes[id] = 1;
                 S.seeds[id] = (int16_t)i;
-                S.sc[id][0] = C[3 * i];
-                S.sc[id][1] = C[3 * i + 1];
-                S.sc[id][2] = C[3 * i + 2];
+                S.sc[id][0] = S.cc[i][0];
+                S.sc[id][1] = S.cc[i][1];
+                S.sc[id][2] = S.cc[i][2];
             } else {
                 S.sub[i] = -2;
+                S.qrow[r - need_new] = (uint16_t)i;   // queue keeps index order
             }
         }
         rank += __popc(ob);
@@ -192,9 +200,10 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     __syncwarp();
     // ---- step 3: queued rows join the nearest under-filled sub-bucket
     if (nqueue > 0) {
-        for (int i = 0; i < m; ++i) {
-            if (S.sub[i] != -2) continue;   // warp-uniform (smem broadcast)
-            const double ci[3] = {C[3 * i], C[3 * i + 1], C[3 * i + 2]};
+        __syncwarp();
+        for (int qi = 0; qi < nqueue; ++qi) {
+            const int i = S.qrow[qi];       // queued rows in index order (smem broadcast)
+            const double ci[3] = {S.cc[i][0], S.cc[i][1], S.cc[i][2]};
             double best = DBL_MAX;
             int bid = INT_MAX;
             for (int j = nalloc + lane; j < target; j += 32) {
@@ -282,11 +291,11 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
             int mem[64];
             double md[64];
             int nm = 0;
-            const double* cs = C + 3 * S.seeds[full_t];
+            const double* cs = S.cc[S.seeds[full_t]];
             for (int i = 0; i < m && nm < 64; ++i)
                 if (S.sub[i] == donor) {
                     mem[nm] = i;
-                    md[nm] = dist3(C + 3 * i, cs);
+                    md[nm] = dist3(S.cc[i], cs);
                     ++nm;
                 }
             // stable insertion sort by distance
