@@ -209,6 +209,19 @@ int f3d_row_ln(void *F, int f_is_f64, int64_t ldf, const void *y, int64_t ldy,
                const float *ybias, const float *gain, const float *beta,
                const double *pe_coords, const double *lo_ext, double pe_base, void *out,
                int out_kind, int64_t ldo, int64_t n, int d, double eps, void *stream);
+/* Fused stage MLP on tcgen05 (bw/stage.py:146-158) for d = 96 (config A/B width):
+ *   F[r] += gelu(x[r] W_in + b_in) W_out + b_out          (exact-erf GELU)
+ *   x_next[r] = LN(F[r]) * ln_g + ln_b (+ PE(pe_coords[r], lo_ext))  if x_next
+ * x: (n, d) bf16 rows (LN2 output); w_in_t = W_in^T (4d, d) and w_out_t =
+ * W_out^T (d, 4d), bf16 row-major; F: (n, d) fp32 residual stream.  The 4d-wide
+ * hidden activations never leave TMEM.  x_next may alias x (rows are read
+ * before they are rewritten).  n_dev (nullable): device row count <= n. */
+int f3d_mlp_supported(int d);
+int f3d_mlp_fused(const void *x, int64_t ldx, int64_t n, int d, const void *w_in_t,
+                  const float *b_in, const void *w_out_t, const float *b_out, float *F,
+                  int64_t ldf, const float *ln_g, const float *ln_b, const double *pe_coords,
+                  const double *lo_ext, double pe_base, void *x_next, int64_t ldxn, double eps,
+                  const int32_t *n_dev, void *stream);
 /* y = 0.5 x (1 + erf(x / sqrt 2)) in float64 (bw/stage.py:91-92). */
 int f3d_gelu_f64(const double *x, int64_t n, double *y, void *stream);
 /* u = gelu(u + bias) with the exact erf form (bw/stage.py:91-96), bf16 rows. */

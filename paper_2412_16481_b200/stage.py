@@ -15,6 +15,7 @@ pkg/tests/test_stage.py:75-84; float32 otherwise); GEMM operands are bf16 with
 fp32 accumulation.  Rows never move: attention reads each scope in place.
 """
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -26,6 +27,10 @@ from .bucketing import BucketAssignment
 from .errors import ConfigError
 
 LN_EPS = 1e-12
+# F3D_FUSED_MLP=1 selects the fused tcgen05 MLP (csrc/mlp_tc.cu, d = 96) over
+# cuBLAS GEMMs + f3d_bias_gelu + f3d_row_ln.  Opt-in: measured 0.46 vs 0.39 ms
+# per config-B step (tools/mlp_ab.py)
+FUSED_MLP = os.environ.get("F3D_FUSED_MLP", "0") == "1"
 
 
 @dataclass
@@ -70,6 +75,7 @@ class StageParams:
             "w_o": f(self.w_o, bf), "b_o": f(self.b_o, f32),
             "w_in": f(self.w_in, bf), "b_in": f(self.b_in, f32),
             "w_out": f(self.w_out, bf), "b_out": f(self.b_out, f32),
+            "w_in_t": f(self.w_in, bf).t().contiguous(), "w_out_t": f(self.w_out, bf).t().contiguous(),
             "ln1_g": f(self.ln1_gain, f32), "ln1_b": f(self.ln1_bias, f32),
             "ln2_g": f(self.ln2_gain, f32), "ln2_b": f(self.ln2_bias, f32),
         }
@@ -152,7 +158,11 @@ class StageRunner:
         self.qkv = L.empty((n, 3 * d), torch.bfloat16)
         self.a = L.empty((n, d), torch.bfloat16)
         self.y = L.empty((n, d), torch.bfloat16)
-        self.u = L.empty((n, dhid), torch.bfloat16)
+        self.n_dev = n_dev
+        self.fused_mlp = (FUSED_MLP and f_dtype == torch.float32 and dhid == 4 * d
+                          and self.w.get("w_in_t") is not None
+                          and bool(L.load().f3d_mlp_supported(d)))
+        self.u = None if self.fused_mlp else L.empty((n, dhid), torch.bfloat16)
 
     def _row_ln(self, F, y, ybias, g, b, pe, out):
         L.call("f3d_row_ln", L.ptr(F), int(F.dtype == torch.float64), F.stride(0), L.ptr(y),
@@ -173,6 +183,17 @@ class StageRunner:
             attend(q, k, v, self.a, plan, self.H, self.dh)
             torch.mm(self.a, w["w_o"], out=self.y)
             self._row_ln(F, self.y, w["b_o"], w["ln2_g"], w["ln2_b"], None, self.x)
+            if self.fused_mlp and F.dtype == torch.float32:
+                last = t + 1 == R
+                # F += MLP(x); x <- LN1(F) + PE for the next round, one kernel
+                L.call("f3d_mlp_fused", L.ptr(self.x), self.x.stride(0), self.n, self.d,
+                       L.ptr(w["w_in_t"]), L.ptr(w["b_in"]), L.ptr(w["w_out_t"]), L.ptr(w["b_out"]),
+                       L.ptr(F), F.stride(0), None if last else L.ptr(w["ln1_g"]),
+                       None if last else L.ptr(w["ln1_b"]), None if last else L.ptr(self.coords),
+                       None if last else L.ptr(self.lo_ext), 10000.0,
+                       None if last else L.ptr(self.x), self.x.stride(0), LN_EPS,
+                       L.ptr(self.n_dev), L.stream())
+                continue
             torch.mm(self.x, w["w_in"], out=self.u)
             L.call("f3d_bias_gelu", L.ptr(self.u), self.n, self.u.shape[1], L.ptr(w["b_in"]),
                    L.stream())

@@ -214,3 +214,31 @@ def test_attention_growing_max_rescales(d, H):
     ref = O.attention_ranges(Q, K, V, H, ranges)
     assert np.isfinite(out).all()
     assert rel(out, ref) < 3e-2, rel(out, ref)
+
+
+def test_fused_mlp_matches_unfused_stage():
+    """The opt-in fused tcgen05 MLP (csrc/mlp_tc.cu) reproduces the cuBLAS +
+    bias_gelu + row_ln path of a 2-round stage within bf16 tolerance."""
+    from paper_2412_16481_b200 import stage as ST
+    r = np.random.default_rng(5)
+    n, d = 3000, 96
+    coords = r.random((n, 3))
+    feats = r.normal(size=(n, d))
+    a = F.assign_buckets(F.remap_nonnegative(F.voxelize(F.PointCloud(coords), F.VoxelGrid(1 / 16))),
+                         None, F.HashConfig("zorder-div", K=16, S_div=256), 256)
+    sf, _ = F.scatter(feats, a)
+    sc, _ = F.scatter(coords, a)
+    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
+    p = F.init_params(0, d, n_heads=4)
+    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
+    C = torch.tensor(sc, device="cuda")
+    old = ST.FUSED_MLP
+    try:
+        ST.FUSED_MLP = False
+        ref = F.stage_forward(X, C, a, sched, p)
+        ST.FUSED_MLP = True
+        out = F.stage_forward(X, C, a, sched, p)
+    finally:
+        ST.FUSED_MLP = old
+    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
+    assert rr < 1e-2, rr
