@@ -123,6 +123,11 @@ int f3d_scatter_rows(const void *src, const int32_t *dest, int64_t n, int64_t ro
                      void *dst, const int32_t *n_dev, void *stream);
 int f3d_gather_rows(const void *src, const int32_t *idx, int64_t n, int64_t row_bytes,
                     void *dst, const int32_t *n_dev, void *stream);
+/* Scatter with a dtype change: dst (fp32, row stride ld_dst)[dest[i]] =
+ * src (bf16, row stride ld_src)[i]; d % 8 == 0, 16-byte aligned rows. */
+int f3d_scatter_rows_bf16_f32(const void *src, int64_t ld_src, const int32_t *dest, int64_t n,
+                              int d, void *dst, int64_t ld_dst, const int32_t *n_dev,
+                              void *stream);
 
 
 /* ------------------------------------------ a9-a11: bucket-swin attention
@@ -179,6 +184,14 @@ int f3d_plan_round(const int32_t *counts, const int32_t *base, int K, int S, int
                    int32_t *seg_start, int32_t *seg_vstart, int32_t *scope_len,
                    int32_t *scope_order, int32_t *work, int max_work, int qstep, int32_t *live,
                    void *stream);
+/* All rounds of a schedule in one launch: round t (block t) uses rotation
+ * (t*shift) mod W and writes its tables round_stride int32 elements after
+ * round t-1's (every output pointer is round 0's). */
+int f3d_plan_rounds(const int32_t *counts, const int32_t *base, int K, int S, int nb_cap, int W,
+                    int stride, int shift, int nrounds, int64_t round_stride, int nscopes,
+                    int32_t *scope_seg, int32_t *scope_nseg, int32_t *seg_start,
+                    int32_t *seg_vstart, int32_t *scope_len, int32_t *scope_order,
+                    int32_t *work, int max_work, int qstep, int32_t *live, void *stream);
 /* Device pooling tile table (bw/pooling.py:211-225): tiles of <= cap rows per
  * slot in scatter order; totals receives [ntiles, npooled]. */
 int f3d_plan_pool(const int32_t *counts, const int32_t *base, int nslots, int cap, int rho,

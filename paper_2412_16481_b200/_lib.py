@@ -44,6 +44,7 @@ SIGNATURES = {
     "f3d_validate_assignment": (_INT, [_P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P]),
     "f3d_scatter_rows": (_INT, [_P, _P, _I64, _I64, _P, _P, _P]),
     "f3d_gather_rows": (_INT, [_P, _P, _I64, _I64, _P, _P, _P]),
+    "f3d_scatter_rows_bf16_f32": (_INT, [_P, _I64, _P, _I64, _INT, _P, _I64, _P, _P]),
     "f3d_bswin_attention": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _INT, _INT, _INT, _P,
                                    _P, _P, _P, _P, _P, _INT, _P, _INT, _INT, _P, _P, _P, _P]),
     "f3d_bswin_attention_tc": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _INT, _INT, _INT,
@@ -51,6 +52,8 @@ SIGNATURES = {
     "f3d_attention_tc_qstep": (_INT, [_INT]),
     "f3d_plan_round": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P, _P, _P, _P,
                               _P, _P, _INT, _INT, _P, _P]),
+    "f3d_plan_rounds": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _I64, _INT, _P,
+                               _P, _P, _P, _P, _P, _P, _INT, _INT, _P, _P]),
     "f3d_plan_pool": (_INT, [_P, _P, _INT, _INT, _INT, _P, _P, _P, _P, _P]),
     "f3d_positional_encoding": (_INT, [_P, _I64, _INT, _F64, _INT, _P, _I64, _P]),
     "f3d_stage_pe": (_INT, [_P, _I64, _INT, _F64, _P, _INT, _P, _I64, _P]),
@@ -93,11 +96,11 @@ _ERRS = {1: ConfigError, 2: RangeError, 3: IntegrityError, 5: EmptyInputError, 6
 KERNELS_PER_CALL = {
     "f3d_voxelize": 1, "f3d_remap_nonnegative": 3, "f3d_hash_bucket": 2, "f3d_morton_encode": 2,
     "f3d_voxel_hash": 3, "f3d_psh_assign": 1, "f3d_validate_assignment": 3,
-    "f3d_scatter_rows": 1, "f3d_gather_rows": 1, "f3d_bswin_attention": 1,
+    "f3d_scatter_rows": 1, "f3d_gather_rows": 1, "f3d_scatter_rows_bf16_f32": 1, "f3d_bswin_attention": 1,
     "f3d_bswin_attention_tc": 1,
     "f3d_positional_encoding": 1, "f3d_stage_pe": 1, "f3d_coord_bbox": 2, "f3d_row_ln": 1,
     "f3d_gelu_f64": 1, "f3d_bias_gelu": 1, "f3d_pool_build": 1, "f3d_pool_reduce": 1,
-    "f3d_plan_round": 1, "f3d_plan_pool": 1, "f3d_mlp_fused": 1,
+    "f3d_plan_round": 1, "f3d_plan_rounds": 1, "f3d_plan_pool": 1, "f3d_mlp_fused": 1,
 }
 
 

@@ -259,7 +259,8 @@ class DeviceRoundPlan:
     nlive are upper bounds for the launch grid; the kernels read the exact
     values from ``live``."""
 
-    def __init__(self, counts_dev, base_dev, K, S, nb, W, stride, shift, t, n, qstep=BLOCK_M):
+    def __init__(self, counts_dev, base_dev, K, S, nb, W, stride, shift, t, n, qstep=BLOCK_M,
+                 _buf=None):
         span = W * stride
         ns = -(-nb // span) * stride
         self.qstep = qstep
@@ -267,7 +268,7 @@ class DeviceRoundPlan:
         self.nwork = n // qstep + ns
         self.max_len = W * S
         i32 = torch.int32
-        buf = L.empty((3 * ns + 2 * ns * W + ns + 2 * self.nwork + 4,), i32)
+        buf = _buf if _buf is not None else L.empty((self.size_for(nb, W, stride, n, qstep),), i32)
         o = 0
 
         def take(k):
@@ -280,11 +281,34 @@ class DeviceRoundPlan:
         self.scope_order = take(ns)
         self.work = take(2 * self.nwork).view(-1, 2)
         self.live = take(4)
+        if _buf is not None:
+            return                       # filled by all_rounds' single launch
         L.call("f3d_plan_round", L.ptr(counts_dev), L.ptr(base_dev), K, S, nb, W, stride,
                (t * shift) % W, ns, L.ptr(self.scope_seg), L.ptr(self.scope_nseg),
                L.ptr(self.seg_start), L.ptr(self.seg_vstart), L.ptr(self.scope_len),
                L.ptr(self.scope_order), L.ptr(self.work), self.nwork, qstep, L.ptr(self.live),
                L.stream())
+
+    @staticmethod
+    def size_for(nb, W, stride, n, qstep):
+        ns = -(-nb // (W * stride)) * stride
+        return 3 * ns + 2 * ns * W + ns + 2 * (n // qstep + ns) + 4
+
+    @classmethod
+    def all_rounds(cls, counts_dev, base_dev, K, S, nb, W, stride, shift, rounds, n, qstep=BLOCK_M):
+        """Plans of rounds 0..rounds-1 (rotation (t*shift) mod W) from one
+        f3d_plan_rounds launch; each round's tables live round_stride int32
+        apart in one buffer."""
+        per = cls.size_for(nb, W, stride, n, qstep)
+        buf = L.empty((rounds * per,), torch.int32)
+        plans = [cls(counts_dev, base_dev, K, S, nb, W, stride, shift, t, n, qstep,
+                     _buf=buf[t * per:(t + 1) * per]) for t in range(rounds)]
+        p0 = plans[0]
+        L.call("f3d_plan_rounds", L.ptr(counts_dev), L.ptr(base_dev), K, S, nb, W, stride, shift,
+               rounds, per, p0.nlive, L.ptr(p0.scope_seg), L.ptr(p0.scope_nseg),
+               L.ptr(p0.seg_start), L.ptr(p0.seg_vstart), L.ptr(p0.scope_len),
+               L.ptr(p0.scope_order), L.ptr(p0.work), p0.nwork, qstep, L.ptr(p0.live), L.stream())
+        return plans
 
 
 def plan_schedule(table, schedule: ScopeSchedule, dev=None, qstep=BLOCK_M):

@@ -131,12 +131,16 @@ class Backbone:
         with record_function(f"stage{si}.scatter"):
             dest = a._dev["dest"]
             d = X.shape[1]
-            Xf = X if X.dtype == torch.float32 else X.to(torch.float32)
-            Xf = Xf.contiguous()
             F = torch.empty((n, d), dtype=torch.float32, device=C.device)
             Cs = torch.empty((n, 3), dtype=torch.float64, device=C.device)
-            L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F), L.ptr(n_dev),
-                   L.stream())
+            if X.dtype == torch.bfloat16 and d % 8 == 0 and X.is_contiguous():
+                # bf16 upload -> fp32 residual stream in the scatter itself
+                L.call("f3d_scatter_rows_bf16_f32", L.ptr(X), X.stride(0), L.ptr(dest), n, d,
+                       L.ptr(F), F.stride(0), L.ptr(n_dev), L.stream())
+            else:
+                Xf = (X if X.dtype == torch.float32 else X.to(torch.float32)).contiguous()
+                L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F),
+                       L.ptr(n_dev), L.stream())
             L.call("f3d_scatter_rows", L.ptr(C), L.ptr(dest), n, 24, L.ptr(Cs), L.ptr(n_dev),
                    L.stream())
         with record_function(f"stage{si}.plan"):
@@ -145,8 +149,8 @@ class Backbone:
                 raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb_cap})")
             cd, bd = a._dev["counts"], a._dev["base"]
             qs = qstep_for(cfg.d_model // cfg.n_heads)
-            r.plans = [DeviceRoundPlan(cd, bd, cfg.K, cfg.S, nb_cap, cfg.W, cfg.stride, cfg.shift,
-                                       t, n, qstep=qs) for t in range(cfg.rounds)]
+            r.plans = DeviceRoundPlan.all_rounds(cd, bd, cfg.K, cfg.S, nb_cap, cfg.W, cfg.stride,
+                                                 cfg.shift, cfg.rounds, n, qstep=qs)
             r.runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
                                    weights=self._w[si], plans=r.plans, n_dev=n_dev)
         with record_function(f"stage{si}.run"):

@@ -38,9 +38,23 @@ __device__ int block_excl_scan(int v, int& total, int* sh /* >= 33 ints */) {
 
 __global__ void __launch_bounds__(kThreads) plan_round_kernel(
     const int32_t* __restrict__ counts, const int32_t* __restrict__ base, int K, int S, int nb_cap,
-    int W, int stride, int off, int nscopes, int32_t* scope_seg, int32_t* scope_nseg,
-    int32_t* seg_start, int32_t* seg_vstart, int32_t* scope_len, int32_t* scope_order,
-    int32_t* work, int max_work, int qstep, int32_t* live) {
+    int W, int stride, int off0, int off_step, int64_t round_stride, int nscopes,
+    int32_t* scope_seg, int32_t* scope_nseg, int32_t* seg_start, int32_t* seg_vstart,
+    int32_t* scope_len, int32_t* scope_order, int32_t* work, int max_work, int qstep,
+    int32_t* live) {
+    // block t plans round t: rotation off0 + t*off_step, outputs round_stride apart
+    const int off = (off0 + (int)blockIdx.x * off_step) % W;
+    {
+        const int64_t o = (int64_t)blockIdx.x * round_stride;
+        scope_seg += o;
+        scope_nseg += o;
+        seg_start += o;
+        seg_vstart += o;
+        scope_len += o;
+        scope_order += o;
+        work += o;
+        live += o;
+    }
     __shared__ int sh[40];
     __shared__ int s_maxlen;
     const int span = W * stride;
@@ -162,8 +176,24 @@ extern "C" int f3d_plan_round(const int32_t* counts, const int32_t* base, int K,
         max_work < 0 || qstep < 16)
         return F3D_ERR_CONFIG;
     plan::plan_round_kernel<<<1, plan::kThreads, 0, (cudaStream_t)stream>>>(
-        counts, base, K, S, nb_cap, W, stride, off, nscopes, scope_seg, scope_nseg, seg_start,
-        seg_vstart, scope_len, scope_order, work, max_work, qstep, live);
+        counts, base, K, S, nb_cap, W, stride, off, 0, 0, nscopes, scope_seg, scope_nseg,
+        seg_start, seg_vstart, scope_len, scope_order, work, max_work, qstep, live);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_plan_rounds(const int32_t* counts, const int32_t* base, int K, int S,
+                               int nb_cap, int W, int stride, int shift, int nrounds,
+                               int64_t round_stride, int nscopes, int32_t* scope_seg,
+                               int32_t* scope_nseg, int32_t* seg_start, int32_t* seg_vstart,
+                               int32_t* scope_len, int32_t* scope_order, int32_t* work,
+                               int max_work, int qstep, int32_t* live, void* stream) {
+    if (K < 1 || S < 1 || nb_cap < 1 || W < 1 || stride < 1 || shift < 0 || nscopes < 1 ||
+        max_work < 0 || qstep < 16 || nrounds < 1 || round_stride < 0)
+        return F3D_ERR_CONFIG;
+    plan::plan_round_kernel<<<nrounds, plan::kThreads, 0, (cudaStream_t)stream>>>(
+        counts, base, K, S, nb_cap, W, stride, 0, shift % W, round_stride, nscopes, scope_seg,
+        scope_nseg, seg_start, seg_vstart, scope_len, scope_order, work, max_work, qstep, live);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

@@ -1,5 +1,7 @@
 // Row scatter / gather (bw/bucketing.py:385-401) and assignment validation
 // (bw/bucketing.py:116-145).  HBM-bound: 16-byte vectors, one warp-row.
+#include <cuda_bf16.h>
+
 #include <climits>
 
 #include "f3d_common.cuh"
@@ -45,6 +47,25 @@ int move_rows(const void* src, const int32_t* idx, int64_t n, const int32_t* n_d
     }
     F3D_LAUNCH_CHECK();
     return F3D_OK;
+}
+
+// Scatter of bf16 rows into fp32 rows (the backbone's feature upload is bf16,
+// the residual stream fp32): one thread per 8 columns, 16-byte in, 2x16 out.
+__global__ void scatter_bf16_f32_kernel(const uint4* __restrict__ src, int64_t ld_src8,
+                                        const int32_t* __restrict__ dest, int64_t n,
+                                        const int32_t* n_dev, int d8, float4* __restrict__ dst,
+                                        int64_t ld_dst4) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= dyn_n(n, n_dev) * d8) return;
+    const int64_t r = t / d8;
+    const int k = (int)(t - r * d8);
+    const uint4 w = src[r * ld_src8 + k];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+    const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+    const float2 c = __bfloat1622float2(h[2]), e = __bfloat1622float2(h[3]);
+    float4* o = dst + (int64_t)__ldg(dest + r) * ld_dst4 + 2 * k;
+    o[0] = make_float4(a.x, a.y, b.x, b.y);
+    o[1] = make_float4(c.x, c.y, e.x, e.y);
 }
 
 // ------------------------------------------------------------- validate
@@ -134,6 +155,21 @@ using namespace f3d;
 extern "C" int f3d_scatter_rows(const void* src, const int32_t* dest, int64_t n,
                                 int64_t row_bytes, void* dst, const int32_t* n_dev, void* stream) {
     return rows::move_rows<true>(src, dest, n, n_dev, row_bytes, dst, (cudaStream_t)stream);
+}
+
+extern "C" int f3d_scatter_rows_bf16_f32(const void* src, int64_t ld_src, const int32_t* dest,
+                                         int64_t n, int d, void* dst, int64_t ld_dst,
+                                         const int32_t* n_dev, void* stream) {
+    if (n < 0 || d < 8 || (d & 7) || (ld_src & 7) || (ld_dst & 3) ||
+        (((uintptr_t)src | (uintptr_t)dst) & 15))
+        return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    const int64_t tot = n * (d / 8);
+    rows::scatter_bf16_f32_kernel<<<(unsigned)((tot + rows::kThreads - 1) / rows::kThreads),
+                                    rows::kThreads, 0, (cudaStream_t)stream>>>(
+        (const uint4*)src, ld_src / 8, dest, n, n_dev, d / 8, (float4*)dst, ld_dst / 4);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
 }
 
 extern "C" int f3d_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
