@@ -219,6 +219,8 @@ def test_attention_growing_max_rescales(d, H):
 def test_fused_mlp_matches_unfused_stage():
     """The opt-in fused tcgen05 MLP (csrc/mlp_tc.cu) reproduces the cuBLAS +
     bias_gelu + row_ln path of a 2-round stage within bf16 tolerance."""
+    import torch
+
     from paper_2412_16481_b200 import stage as ST
     r = np.random.default_rng(5)
     n, d = 3000, 96
