@@ -266,38 +266,103 @@ class Backbone:
         return X[:n_out], Cn[:n_out]
 
     # ------------------------------------------------------------ graphs
-    def capture(self, n, feat_dtype=torch.bfloat16):
-        """Capture the forward for n-point inputs into two CUDA graphs:
-        g0 = stage-0 bucketing (reads only the coordinates) and g1 = the
-        rest.  Inputs are the static buffers ``graph_coords`` (n,3) f64 and
-        ``graph_feats`` (n,d); replay with ``forward_graph``."""
+    def _capture_slot(self, n, feat_dtype):
+        """Two CUDA graphs over private static buffers: g0 = stage-0
+        bucketing (reads only the coordinates), g1 = the rest."""
         dev = L.device()
         d = self.stages[0].d_model
-        self.graph_coords = torch.zeros((n, 3), dtype=torch.float64, device=dev)
-        self.graph_feats = torch.zeros((n, d), dtype=feat_dtype, device=dev)
+        coords = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        feats = torch.zeros((n, d), dtype=feat_dtype, device=dev)
         # a real scene to warm up (grid attributes, cuBLAS handles/workspaces)
         rng = np.random.default_rng(0)
-        self.graph_coords.copy_(torch.from_numpy(rng.random((n, 3))))
+        coords.copy_(torch.from_numpy(rng.random((n, 3))))
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             for _ in range(2):
-                r0 = self._enqueue_bucketize0(self.graph_coords)
-                self._enqueue_rest(r0, self.graph_coords, self.graph_feats)
+                r0 = self._enqueue_bucketize0(coords)
+                self._enqueue_rest(r0, coords, feats)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         pool = torch.cuda.graph_pool_handle()
         g0, g1 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(g0, pool=pool):
-            r0 = self._enqueue_bucketize0(self.graph_coords)
+            r0 = self._enqueue_bucketize0(coords)
         with torch.cuda.graph(g1, pool=pool):
-            X, Cn, n_dev, runs = self._enqueue_rest(r0, self.graph_coords, self.graph_feats)
+            X, Cn, n_dev, runs = self._enqueue_rest(r0, coords, feats)
             status = self._status_vector(runs, n_dev)
             out_bf16 = X.to(torch.bfloat16)
-        self._graphs = {"n": n, "g0": g0, "g1": g1, "X": X, "C": Cn, "runs": runs,
-                        "status": status, "out_bf16": out_bf16, "side": torch.cuda.Stream()}
-        self._status_host = torch.empty(status.shape, dtype=torch.int64).pin_memory()
+        return {"n": n, "g0": g0, "g1": g1, "X": X, "C": Cn, "runs": runs, "status": status,
+                "out_bf16": out_bf16, "side": torch.cuda.Stream(), "coords": coords,
+                "feats": feats,
+                "status_h": torch.empty(status.shape, dtype=torch.int64).pin_memory(),
+                "out_h": torch.empty(out_bf16.shape, dtype=out_bf16.dtype).pin_memory()}
+
+    def capture(self, n, feat_dtype=torch.bfloat16):
+        """Capture the forward for n-point inputs into two CUDA graphs (see
+        _capture_slot).  Inputs are the static buffers ``graph_coords`` (n,3)
+        f64 and ``graph_feats`` (n,d); replay with ``forward_graph``."""
+        self._graphs = self._capture_slot(n, feat_dtype)
+        self.graph_coords = self._graphs["coords"]
+        self.graph_feats = self._graphs["feats"]
+        self._status_host = self._graphs["status_h"]
         return self._graphs
+
+    def stream_host(self, scenes, on_result=None):
+        """Pipelined end-to-end forward over a sequence of host scenes
+        ``[(coords_h (n,3) f64, feats_h (n,d) bf16), ...]`` (pinned, equal n).
+        Two graph slots alternate: step i's upload runs on an H2D stream
+        while step i-1 computes, and step i-1's read-back (last-stage bf16
+        features + status words) runs on a D2H stream under step i's compute.
+        ``on_result(i, feats_host_view, n_out)`` is called in step order once a
+        step's read-back landed (the view is reused two steps later); a step's
+        errors are raised then, before its slot is reused."""
+        n = scenes[0][0].shape[0]
+        dt = scenes[0][1].dtype
+        slots = getattr(self, "_slots", None)
+        if slots is None or slots[0]["n"] != n or slots[0]["feats"].dtype != dt:
+            slots = self._slots = [self._capture_slot(n, dt) for _ in range(2)]
+            for sl in slots:
+                for k in ("ev_in", "ev_done", "ev_out"):
+                    sl[k] = torch.cuda.Event()
+                sl["pending"] = None
+        if not hasattr(self, "_h2d"):
+            self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        compute = torch.cuda.current_stream()
+        h2d, d2h = self._h2d, self._d2h
+
+        def finish(sl):
+            i = sl["pending"]
+            if i is None:
+                return
+            sl["ev_out"].synchronize()
+            sl["pending"] = None
+            n_out = self._check(sl["status_h"].numpy(), sl["runs"])
+            if on_result is not None:
+                on_result(i, sl["out_h"][:n_out], n_out)
+
+        for i, (ch, fh) in enumerate(scenes):
+            sl = slots[i % 2]
+            finish(sl)                                   # step i-2 read back + checked
+            if i >= 2:
+                h2d.wait_event(sl["ev_done"])            # its inputs are free
+            with torch.cuda.stream(h2d):
+                sl["coords"].copy_(ch, non_blocking=True)
+                sl["feats"].copy_(fh, non_blocking=True)
+                sl["ev_in"].record(h2d)
+            compute.wait_event(sl["ev_in"])
+            sl["g0"].replay()
+            sl["g1"].replay()
+            sl["ev_done"].record(compute)
+            d2h.wait_event(sl["ev_done"])
+            with torch.cuda.stream(d2h):
+                sl["out_h"].copy_(sl["out_bf16"], non_blocking=True)
+                sl["status_h"].copy_(sl["status"], non_blocking=True)
+                sl["ev_out"].record(d2h)
+            sl["pending"] = i
+        nxt = len(scenes) % 2                             # drain in step order
+        finish(slots[nxt])
+        finish(slots[1 - nxt])
 
     def replay(self):
         """Replay both graphs on the current stream (inputs already in

@@ -117,3 +117,24 @@ def test_graph_replay_matches_eager_and_host_path():
     f_e2, c_e2 = bb.forward(C2, X)
     f_g2, c_g2 = bb.forward_graph(C2, X)
     assert torch.equal(c_e2, c_g2) and torch.equal(f_e2, f_g2)
+
+
+def test_stream_host_pipelined_matches_single_calls():
+    """Two-slot pipelined host streaming returns each scene's features in
+    order, equal to the synchronous host call, with errors checked per step."""
+    n = 20_000
+    stages = (StageConfig(K=64, S=512, S_div=4096, pool_rho=2, seed=0),
+              StageConfig(K=32, S=512, S_div=8192, pool_rho=0, seed=1))
+    bb = Backbone(stages)
+    scenes = []
+    for seed in (3, 4, 5):
+        c = torch.tensor(O.synth_cloud(seed, n, "uniform-box")).pin_memory()
+        f = torch.tensor(np.random.default_rng(seed).normal(size=(n, 96)),
+                         dtype=torch.bfloat16).pin_memory()
+        scenes.append((c, f))
+    got = {}
+    bb.stream_host(scenes, on_result=lambda i, out, n_out: got.__setitem__(i, out.clone()))
+    assert sorted(got) == [0, 1, 2]
+    for i, (c, f) in enumerate(scenes):
+        ref, n_ref = bb.forward_host(c, f)
+        assert got[i].shape[0] == n_ref and torch.equal(got[i], ref)
