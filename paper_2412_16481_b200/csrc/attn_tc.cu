@@ -536,13 +536,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int e = 0; e < kBN; ++e)
                         if (e >= kvalid) x[e] = __float_as_uint(-INFINITY);
                 }
-                float mx0 = -INFINITY, mx1 = -INFINITY;
+                // row max with 8 independent chains (short dependency depth)
+                float mx[8];
 #pragma unroll
-                for (int e = 0; e < kBN; e += 2) {
-                    mx0 = fmaxf(mx0, __uint_as_float(x[e]));
-                    mx1 = fmaxf(mx1, __uint_as_float(x[e + 1]));
-                }
-                const float mxs = fmaxf(mx0, mx1) * sl2;
+                for (int q = 0; q < 8; ++q) mx[q] = __uint_as_float(x[q]);
+#pragma unroll
+                for (int e = 8; e < kBN; e += 8)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) mx[q] = fmaxf(mx[q], __uint_as_float(x[e + q]));
+                const float mxs = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                        fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
                 PROF_MARK(tm1);
                 PROF_ADD(17, tm0, tm1);
                 if (j == 0) {
