@@ -139,6 +139,7 @@ struct Args {
     int nwork;
     const int32_t* live;   // optional device [nwork, ...]
     int use_tma;
+    int o_vec;             // output rows allow 16-byte stores
 };
 
 template <int DH>
@@ -629,21 +630,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t y[16];
                 tmem_ld16(obase + c * 16, y);
                 tmem_wait_ld();
-                if (live_row) {
-                    if (sizeof(OutT) == 2) {
-                        __nv_bfloat16* out =
-                            reinterpret_cast<__nv_bfloat16*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+                if (!live_row) continue;
+                if (sizeof(OutT) == 2) {
+                    __nv_bfloat16* out =
+                        reinterpret_cast<__nv_bfloat16*>(A.o) + (int64_t)pr * A.ld_o + hcol;
 #pragma unroll
-                        for (int e = 0; e < 16; e += 2)
-                            if (c * 16 + e < A.dh)
-                                *reinterpret_cast<__nv_bfloat162*>(out + c * 16 + e) =
-                                    __floats2bfloat162_rn(__uint_as_float(y[e]) * inv,
-                                                          __uint_as_float(y[e + 1]) * inv);
-                    } else {
-                        float* out = reinterpret_cast<float*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+                    for (int e = 0; e < 16; e += 8) {
+                        if (c * 16 + e >= A.dh) break;
+                        uint32_t w[4];
 #pragma unroll
-                        for (int e = 0; e < 16; ++e)
-                            if (c * 16 + e < A.dh) out[c * 16 + e] = __uint_as_float(y[e]) * inv;
+                        for (int q = 0; q < 4; ++q) {
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(
+                                __uint_as_float(y[e + 2 * q]) * inv, __uint_as_float(y[e + 2 * q + 1]) * inv);
+                            w[q] = *reinterpret_cast<uint32_t*>(&h2);
+                        }
+                        if (A.o_vec)   // 16-byte stores: 8 columns at a time
+                            *reinterpret_cast<uint4*>(out + c * 16 + e) = make_uint4(w[0], w[1], w[2], w[3]);
+                        else
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                *reinterpret_cast<uint32_t*>(out + c * 16 + e + 2 * q) = w[q];
+                    }
+                } else {
+                    float* out = reinterpret_cast<float*>(A.o) + (int64_t)pr * A.ld_o + hcol;
+#pragma unroll
+                    for (int e = 0; e < 16; e += 4) {
+                        if (c * 16 + e >= A.dh) break;
+                        const float4 v = make_float4(__uint_as_float(y[e]) * inv, __uint_as_float(y[e + 1]) * inv,
+                                                     __uint_as_float(y[e + 2]) * inv, __uint_as_float(y[e + 3]) * inv);
+                        if (A.o_vec)
+                            *reinterpret_cast<float4*>(out + c * 16 + e) = v;
+                        else {
+                            out[c * 16 + e] = v.x;
+                            out[c * 16 + e + 1] = v.y;
+                            out[c * 16 + e + 2] = v.z;
+                            out[c * 16 + e + 3] = v.w;
+                        }
                     }
                 }
             }
@@ -794,6 +816,10 @@ extern "C" int f3d_bswin_attention_tc(const void* q, const void* k, const void* 
     A.nwork = nwork;
     A.live = live;
     A.use_tma = 0;
+    {
+        const int esz = out_f32 ? 4 : 2;
+        A.o_vec = (((uintptr_t)o & 15) == 0 && (ld_o * esz) % 16 == 0 && (dh * esz) % 16 == 0) ? 1 : 0;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     switch (attn_tc::dh_tile(dh)) {
         case 16: return attn_tc::launch_dh<16>(A, n_rows, st);
