@@ -67,7 +67,18 @@ constexpr int kNQ = 2;            // Q tiles per work item
 constexpr int kLoadWarps = 3;     // warps 0-2
 constexpr int kLoadThreads = kLoadWarps * 32;
 constexpr int kMmaWarp = 3;       // completes warpgroup 0
-constexpr int kThreads = (4 + 4 * kNQ) * 32;
+// Softmax column split: CS warps share each 32-row lane quarter of a Q tile
+// and take kBN/CS key columns each (row max / sum exchanged through shared
+// memory) -- more warps per SM sub-partition to hide the per-tile latencies
+// of the exp-bound small-head softmax.
+template <int DH>
+__host__ __device__ constexpr int cs_for() {
+    return DH == 64 ? 2 : 1;   // measured: DH 64 451 -> 492 TFLOP/s; DH 32 (0.165 -> 0.185 ms) and DH 128 (948 -> 919) slower
+}
+template <int DH>
+__host__ __device__ constexpr int threads_for() {
+    return (4 + 4 * kNQ * cs_for<DH>()) * 32;
+}
 constexpr float kRescale = 8.f;   // move the running max only when it grows by > 2^8
 constexpr int kMaps = 6;          // TMA maps: {q, k, v} x {first block, second block}
 // 1 pair in poly_every<DH>() uses ex2_poly (0: none).  Measured (config B
@@ -148,7 +159,9 @@ struct Cfg {
     static constexpr int NSB = nsb_for<DH>();
     static constexpr int kQBytes = kBM * DH * 2;        // one Q tile
     static constexpr int kKVBytes = kBN * DH * 2;       // one of K or V
-    static constexpr int kBudget = 227 * 1024 - 1024 - 512;
+    static constexpr int CS = cs_for<DH>();
+    static constexpr int kXchg = CS > 1 ? NQ * 4 * 3 * CS * 32 * 4 : 0;   // pair exchange
+    static constexpr int kBudget = 227 * 1024 - 1024 - 512 - kXchg;
     // K/V depth first (>= 4 stages), then a second Q buffer if it still fits
     static constexpr int NQB = (2 * NQ * kQBytes + 4 * 2 * kKVBytes <= kBudget) ? 2 : 1;
     static constexpr int kNstFit = (kBudget - NQB * NQ * kQBytes) / (2 * kKVBytes);
@@ -157,7 +170,9 @@ struct Cfg {
     static constexpr int kOffKV = kOffQ + NQB * NQ * kQBytes;
     static constexpr int kOffBar = kOffKV + kNst * 2 * kKVBytes;
     static constexpr int kNumBars = 2 * NQB + 2 * kNst + (3 * NSB + 1) * NQ;
-    static constexpr int kSmem = kOffBar + kNumBars * 8 + 16 + 1024;   // + 1 KB alignment slack
+    // pair exchange: [NQ][4 quarters][2 parities][CS][32] row maxima, + row sums
+    static constexpr int kOffX = kOffBar + kNumBars * 8 + 16;
+    static constexpr int kSmem = kOffX + kXchg + 1024;   // + 1 KB alignment slack
     static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (NSB*g+b)*kBN
     static constexpr int kTmemO = NSB * NQ * kBN;       // O of tile g: kTmemO + g*DH
     static constexpr int kTmemCols = NQ * (NSB * kBN + DH) <= 256 ? 256 : 512;
@@ -253,7 +268,7 @@ __device__ __forceinline__ void tma_rows(const Maps& M, int mp, const Args& A, i
 }
 
 template <int DH, typename OutT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(threads_for<DH>(), 1)
     bswin_attn_tc_kernel(const Args A, const __grid_constant__ Maps M) {
     using C = Cfg<DH>;
     using L = Lay<DH>;
@@ -261,6 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int NQB = C::NQB;
     constexpr int NSB = C::NSB;
     constexpr int kNst = C::kNst;
+    constexpr int CS = C::CS;
+    constexpr int kThreads = threads_for<DH>();
     extern __shared__ unsigned char smem_raw[];
     // swizzled tiles need 1024-byte aligned bases
     unsigned char* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
@@ -317,10 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int g = 0; g < NQ; ++g) {
             for (int b = 0; b < NSB; ++b) {
                 mbar_init(s_full + NSB * g + b, 1);
-                mbar_init(p_full + NSB * g + b, 128);
+                mbar_init(p_full + NSB * g + b, 128 * CS);
                 mbar_init(pv_done + NSB * g + b, 1);
             }
-            mbar_init(o_free + g, 128);
+            mbar_init(o_free + g, 128 * CS);
         }
         fence_mbar_init();
         if (A.use_tma)
@@ -502,12 +519,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------------------------ softmax warpgroups
-        const int sw = warp - (kMmaWarp + 1);             // 0 .. 4*NQ-1
-        const int g = sw >> 2;                            // Q tile of this warpgroup
-        const int r = (sw & 3) * 32 + lane;               // row in the tile = TMEM lane
-        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const int sw = warp - (kMmaWarp + 1);             // 0 .. 4*NQ*CS-1
+        const int wgi = sw >> 2;
+        const int g = wgi / CS;                           // Q tile of this warpgroup
+        const int hh = wgi - g * CS;                      // column share of this warp
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;                // row in the tile = TMEM lane
+        const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
         const float sl2 = A.scale_log2;
+        constexpr int KC = kBN / CS;                      // S columns per warp
+        constexpr int OC = DH / CS;                       // O columns per warp
         const uint32_t obase = tmem + lane_base + C::kTmemO + g * DH;
+        const uint32_t ocols = obase + hh * OC;
+        // pair exchange slots (CS == 2): [g][quarter][slot 0..2][share][lane]
+        float* xg = reinterpret_cast<float*>(smem + C::kOffX) + ((g * 4 + quarter) * 3) * CS * 32;
+        const int bar_id = 1 + g * 4 + quarter;           // named barrier of the pair
+        auto pair_max = [&](float v, int slot) -> float {
+            if (CS == 1) return v;
+            xg[(slot * CS + hh) * 32 + lane] = v;
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * CS) : "memory");
+            return fmaxf(v, xg[(slot * CS + (hh ^ 1)) * 32 + lane]);
+        };
         uint32_t tg = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
             const Item it = decode(A, item);
@@ -519,22 +551,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t sb = tmem + lane_base + C::kTmemS + (NSB * g + b) * kBN;
                 PROF_WAIT(1, mbar_wait(s_full + NSB * g + b, (t / NSB) & 1));
                 tc_fence_after();
-                uint32_t x[kBN];
+                uint32_t x[KC];
                 {
-                    uint32_t (&x0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[0]);
-                    uint32_t (&x1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&x[32]);
                     PROF_MARK(tl0);
-                    tmem_ld32(sb, x0);
-                    tmem_ld32(sb + 32, x1);
+#pragma unroll
+                    for (int c = 0; c < KC; c += 32)
+                        tmem_ld32(sb + hh * KC + c, *reinterpret_cast<uint32_t(*)[32]>(&x[c]));
                     tmem_wait_ld();
                     PROF_MARK(tl1);
                     PROF_ADD(16, tl0, tl1);
                 }
                 PROF_MARK(tm0);
-                const int kvalid = it.m - j * kBN;        // keys < kvalid are real
-                if (kvalid < kBN) {
+                const int kvalid = it.m - j * kBN - hh * KC;     // my keys < kvalid are real
+                if (kvalid < KC) {
 #pragma unroll
-                    for (int e = 0; e < kBN; ++e)
+                    for (int e = 0; e < KC; ++e)
                         if (e >= kvalid) x[e] = __float_as_uint(-INFINITY);
                 }
                 // row max with 8 independent chains (short dependency depth)
@@ -542,16 +573,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 8; ++q) mx[q] = __uint_as_float(x[q]);
 #pragma unroll
-                for (int e = 8; e < kBN; e += 8)
+                for (int e = 8; e < KC; e += 8)
 #pragma unroll
                     for (int q = 0; q < 8; ++q) mx[q] = fmaxf(mx[q], __uint_as_float(x[e + q]));
-                const float mxs = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                        fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+                const float mxs = pair_max(fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))),
+                                           t & 1) * sl2;
                 PROF_MARK(tm1);
                 PROF_ADD(17, tm0, tm1);
                 if (j == 0) {
                     ms = mxs;
                 } else {
+                    // the pair computed the same row maxima: both warps take
+                    // the same branch and rescale their own O columns
                     const bool need = mxs > ms + kRescale;
                     if (__any_sync(0xffffffffu, need)) {
                         // O_g must hold P_g,j-1 V before it is rescaled in place
@@ -563,14 +597,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                             l *= alpha;
                         }
 #pragma unroll
-                        for (int c = 0; c < DH / 16; ++c) {
+                        for (int c = 0; c < OC; c += 16) {
                             uint32_t y[16];
-                            tmem_ld16(obase + c * 16, y);
+                            tmem_ld16(ocols + c, y);
                             tmem_wait_ld();
 #pragma unroll
                             for (int e = 0; e < 16; ++e)
                                 y[e] = __float_as_uint(__uint_as_float(y[e]) * alpha);
-                            tmem_st16(obase + c * 16, y);
+                            tmem_st16(ocols + c, y);
                         }
                     }
                 }
@@ -579,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 PROF_MARK(te0);
                 float sum = 0.f;
 #pragma unroll
-                for (int e = 0; e < kBN; e += 2) {
+                for (int e = 0; e < KC; e += 2) {
 #if F3D_EXPERIMENT == 2
                     const float p0 = fmaf(__uint_as_float(x[e]), sl2, nms);
                     const float p1 = fmaf(__uint_as_float(x[e + 1]), sl2, nms);
@@ -600,7 +634,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l += sum;
                 PROF_MARK(te1);
                 PROF_ADD(18, te0, te1);
-                tmem_st32(sb, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                if (KC == 64)
+                    tmem_st32(sb, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                else
+                    tmem_st16(sb + hh * (KC / 2), *reinterpret_cast<uint32_t(*)[16]>(&x[0]));
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(p_full + NSB * g + b);
@@ -619,16 +656,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld16(obase + (A.dh & ~15), y);
                 tmem_wait_ld();
                 lsum = __uint_as_float(y[A.dh & 15]);
+            } else if (CS > 1) {
+                xg[(2 * CS + hh) * 32 + lane] = l;       // slot 2: partial row sums
+                asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * CS) : "memory");
+                lsum = l + xg[(2 * CS + (hh ^ 1)) * 32 + lane];
             }
             const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
             const int vr = it.q0 + g * kBM + r;
             const bool live_row = vr < it.m;
             const int pr = live_row ? phys_row(A, it.s0, it.s1, vr) : 0;
-            const int hcol = it.h * A.dh;
+            const int hcol = it.h * A.dh + hh * OC;     // this warp's output columns
 #pragma unroll
-            for (int c = 0; c < DH / 16; ++c) {
+            for (int c = 0; c < OC / 16; ++c) {
                 uint32_t y[16];
-                tmem_ld16(obase + c * 16, y);
+                tmem_ld16(ocols + c * 16, y);
                 tmem_wait_ld();
                 if (!live_row) continue;
                 if (sizeof(OutT) == 2) {
@@ -636,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         reinterpret_cast<__nv_bfloat16*>(A.o) + (int64_t)pr * A.ld_o + hcol;
 #pragma unroll
                     for (int e = 0; e < 16; e += 8) {
-                        if (c * 16 + e >= A.dh) break;
+                        if (hh * OC + c * 16 + e >= A.dh) break;
                         uint32_t w[4];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
@@ -655,7 +696,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float* out = reinterpret_cast<float*>(A.o) + (int64_t)pr * A.ld_o + hcol;
 #pragma unroll
                     for (int e = 0; e < 16; e += 4) {
-                        if (c * 16 + e >= A.dh) break;
+                        if (hh * OC + c * 16 + e >= A.dh) break;
                         const float4 v = make_float4(__uint_as_float(y[e]) * inv, __uint_as_float(y[e + 1]) * inv,
                                                      __uint_as_float(y[e + 2]) * inv, __uint_as_float(y[e + 3]) * inv);
                         if (A.o_vec)
@@ -752,7 +793,7 @@ int launch(Args A, int64_t n_rows, cudaStream_t st) {
         }
     const int total = A.nwork * A.H;
     const int grid = std::max(1, std::min(total, f3d_num_sms()));
-    kern<<<grid, kThreads, C::kSmem, st>>>(A, M);
+    kern<<<grid, threads_for<DH>(), C::kSmem, st>>>(A, M);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
