@@ -204,24 +204,38 @@ __device__ __forceinline__ float gelu_f(float x) {
     return 0.5f * x * phi2;
 }
 
-// 16-byte vector form: 8 bf16 per thread (dh % 8 == 0).  IT = uint32_t when
-// the element count allows it (a 64-bit modulo per vector costs more than the
+// 16-byte vector form: 8 bf16 per vector (dh % 8 == 0); each thread loads
+// kU vectors before computing any (memory-level parallelism: one 16-byte load
+// in flight per thread left the kernel latency-bound).  IT = uint32_t when the
+// element count allows it (a 64-bit modulo per vector costs more than the
 // GELU itself).
 template <typename IT>
 __global__ void bias_gelu8_kernel(uint4* __restrict__ u, IT n8, int dh8,
                                   const float4* __restrict__ b) {
-    for (IT t = (IT)blockIdx.x * blockDim.x + threadIdx.x; t < n8; t += (IT)gridDim.x * blockDim.x) {
-        const int c8 = (int)(t % (IT)dh8);
-        uint4 w = u[t];
-        const float4 b0 = b[2 * c8], b1 = b[2 * c8 + 1];
-        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+    constexpr int kU = 4;
+    const IT stride = (IT)gridDim.x * blockDim.x;
+    for (IT t0 = (IT)blockIdx.x * blockDim.x + threadIdx.x; t0 < n8; t0 += stride * kU) {
+        uint4 w[kU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float2 f = __bfloat1622float2(h[q]);
-            h[q] = __floats2bfloat162_rn(gelu_f(f.x + bb[2 * q]), gelu_f(f.y + bb[2 * q + 1]));
+        for (int q = 0; q < kU; ++q) {
+            const IT t = t0 + q * stride;
+            if (t < n8) w[q] = u[t];
         }
-        u[t] = w;
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const IT t = t0 + q * stride;
+            if (t >= n8) break;
+            const int c8 = (int)(t % (IT)dh8);
+            const float4 b0 = __ldg(b + 2 * c8), b1 = __ldg(b + 2 * c8 + 1);
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w[q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                h[e] = __floats2bfloat162_rn(gelu_f(f.x + bb[2 * e]), gelu_f(f.y + bb[2 * e + 1]));
+            }
+            u[t] = w[q];
+        }
     }
 }
 
@@ -412,7 +426,7 @@ static bool launch_row_ln_vec(cudaStream_t st, void* F, int64_t ldf, const void*
     if (d % 4 || d > 128 || ldf % 4 || !al(F, 16)) return false;
     if (y && (ldy % 4 || !al(y, 8) || (ybias && !al(ybias, 16)))) return false;
     if (out && (ldo % 4 || !al(out, 8) || !al(gain, 16) || !al(beta, 16))) return false;
-    constexpr int RPW = 2;
+    constexpr int RPW = 4;
     const unsigned g = (unsigned)((n + RPW * 8 - 1) / (RPW * 8));
     using BF = __nv_bfloat16;
     float* Ff = (float*)F;
@@ -538,14 +552,13 @@ extern "C" int f3d_bias_gelu(void* u_bf16, int64_t n, int dh, const float* bias,
     cudaStream_t st = (cudaStream_t)stream;
     if (dh % 8 == 0 && ((uintptr_t)u_bf16 & 15) == 0 && ((uintptr_t)bias & 15) == 0) {
         const int64_t n8 = n * dh / 8;
+        const unsigned g = grid_for((n8 + 3) / 4, stage::kThreads);
         if (n8 < (int64_t)1 << 31)
-            stage::bias_gelu8_kernel<uint32_t><<<grid_for(n8, stage::kThreads), stage::kThreads, 0,
-                                                 st>>>((uint4*)u_bf16, (uint32_t)n8, dh / 8,
-                                                       (const float4*)bias);
+            stage::bias_gelu8_kernel<uint32_t><<<g, stage::kThreads, 0, st>>>(
+                (uint4*)u_bf16, (uint32_t)n8, dh / 8, (const float4*)bias);
         else
-            stage::bias_gelu8_kernel<int64_t><<<grid_for(n8, stage::kThreads), stage::kThreads, 0,
-                                                st>>>((uint4*)u_bf16, n8, dh / 8,
-                                                      (const float4*)bias);
+            stage::bias_gelu8_kernel<int64_t><<<g, stage::kThreads, 0, st>>>(
+                (uint4*)u_bf16, n8, dh / 8, (const float4*)bias);
     } else {
         stage::bias_gelu_kernel<<<grid_for(n * dh / 2, stage::kThreads), stage::kThreads, 0, st>>>(
             (__nv_bfloat16*)u_bf16, n, dh, bias);
