@@ -28,9 +28,65 @@ __device__ __forceinline__ void warp_min_max_atomic(long long v, long long* mn, 
         a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
         b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
     }
+    // read before the atomic: once the running extremum has settled almost no
+    // warp improves it, so the per-address atomic traffic (one L2 slice for
+    // the whole grid) collapses to a few hundred operations
     if ((threadIdx.x & 31) == 0) {
-        if (mn) atomicMin(mn, a);
-        if (mx) atomicMax(mx, b);
+        if (mn && a < *(volatile long long*)mn) atomicMin(mn, a);
+        if (mx && b > *(volatile long long*)mx) atomicMax(mx, b);
+    }
+}
+
+// Block-level aggregation of up to 8 64-bit extrema (kMin of them minima):
+// warp shuffles, then shared-memory atomics, then one filtered global atomic
+// per block and value.  Every thread of the block must call it.
+template <int N, int kMin>
+__device__ __forceinline__ void block_extrema_atomic(const long long (&v)[N], int64_t* const (&dst)[N]) {
+    __shared__ long long sh[N];
+    if (threadIdx.x < N) sh[threadIdx.x] = threadIdx.x < kMin ? LLONG_MAX : LLONG_MIN;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        long long a = v[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long b = __shfl_xor_sync(0xffffffffu, a, o);
+            a = k < kMin ? min(a, b) : max(a, b);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (k < kMin) atomicMin(&sh[k], a);
+            else atomicMax(&sh[k], a);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < N && dst[threadIdx.x]) {
+        const int k = threadIdx.x;
+        const long long a = sh[k];
+        long long* p = (long long*)dst[k];
+        if (k < kMin) {
+            if (a < *(volatile long long*)p) atomicMin(p, a);
+        } else if (a > *(volatile long long*)p) {
+            atomicMax(p, a);
+        }
+    }
+}
+
+// per-(batch, axis) minimum of one point per lane: warp-reduced when every
+// lane holds the same batch (sorted / contiguous batches), else per lane
+__device__ __forceinline__ void batch_min_atomic(const long long (&v)[3], int b, bool ok,
+                                                 int64_t* ws_min) {
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    const int b0 = __shfl_sync(0xffffffffu, b, __ffs(act | 1u) - 1);
+    const bool uniform = __all_sync(0xffffffffu, !ok || b == b0);
+    if (uniform) {
+        if (act == 0u) return;
+        for (int a = 0; a < 3; ++a)
+            warp_min_max_atomic(ok ? v[a] : LLONG_MAX, (long long*)ws_min + 3 * b0 + a, nullptr);
+    } else if (ok) {
+        for (int a = 0; a < 3; ++a) {
+            long long* p = (long long*)ws_min + 3 * b + a;
+            if (v[a] < *(volatile long long*)p) atomicMin(p, v[a]);
+        }
     }
 }
 
@@ -42,9 +98,10 @@ __global__ void init_stats_kernel(int64_t* stats, int64_t* ws_min, int nmin) {
 
 __global__ void voxelize_kernel(const double* __restrict__ coords, int64_t n, Origin org,
                                 double vs, int64_t* __restrict__ out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t tot = 3 * n;
-    if (i < tot) out[i] = vox1(coords[i], org.o[i % 3], vs);
+    const int64_t pt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one point per thread
+    if (pt >= n) return;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out[3 * pt + a] = vox1(coords[3 * pt + a], org.o[a], vs);
 }
 
 // per-(batch, axis) minimum; batch == null means one batch.
@@ -65,21 +122,21 @@ __global__ void batch_min_kernel(const int64_t* __restrict__ vox, const int32_t*
     if (!batch || nbatch == 1) {
         for (int a = 0; a < 3; ++a)
             warp_min_max_atomic(v[a], (long long*)ws_min + a, nullptr);
-    } else if (ok && b >= 0 && b < nbatch) {
-        for (int a = 0; a < 3; ++a) atomicMin((long long*)ws_min + 3 * b + a, v[a]);
+    } else {
+        batch_min_atomic(v, b, ok && b >= 0 && b < nbatch, ws_min);
     }
 }
 
 __global__ void remap_kernel(const int64_t* __restrict__ vox, const int32_t* __restrict__ batch,
                              int64_t n, int nbatch, const int64_t* __restrict__ ws_min,
                              int64_t* __restrict__ out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 3 * n) return;
-    const int64_t pt = i / 3;
-    const int a = (int)(i - 3 * pt);
+    // one thread per point (a 64-bit divide per component dominated before)
+    const int64_t pt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pt >= n) return;
     int b = (batch && nbatch > 1) ? batch[pt] : 0;
     if (b < 0 || b >= nbatch) b = 0;
-    out[i] = vox[i] - ws_min[3 * b + a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out[3 * pt + a] = vox[3 * pt + a] - ws_min[3 * b + a];
 }
 
 struct HashArgs {
@@ -113,14 +170,14 @@ __device__ __forceinline__ void hash_point(long long x, long long y, long long z
         }
     }
     if (stats) {
+        // [min x, y, z, max x, y, z, max quotient], one global atomic per block
         const long long BIGP = LLONG_MAX, BIGN = LLONG_MIN;
-        warp_min_max_atomic(valid ? x : BIGP, (long long*)stats + 0, nullptr);
-        warp_min_max_atomic(valid ? y : BIGP, (long long*)stats + 1, nullptr);
-        warp_min_max_atomic(valid ? z : BIGP, (long long*)stats + 2, nullptr);
-        warp_min_max_atomic(valid ? x : BIGN, nullptr, (long long*)stats + 3);
-        warp_min_max_atomic(valid ? y : BIGN, nullptr, (long long*)stats + 4);
-        warp_min_max_atomic(valid ? z : BIGN, nullptr, (long long*)stats + 5);
-        if (ha.want_quot) warp_min_max_atomic(valid ? q : BIGN, nullptr, (long long*)stats + 6);
+        const long long vals[7] = {valid ? x : BIGP, valid ? y : BIGP, valid ? z : BIGP,
+                                   valid ? x : BIGN, valid ? y : BIGN, valid ? z : BIGN,
+                                   valid ? q : BIGN};
+        int64_t* const dst[7] = {stats, stats + 1, stats + 2, stats + 3, stats + 4, stats + 5,
+                                 ha.want_quot ? stats + 6 : nullptr};
+        block_extrema_atomic<7, 3>(vals, dst);
     }
 }
 
@@ -173,9 +230,10 @@ __global__ void fused_min_kernel(const double* __restrict__ coords,
         if (batch) b = batch[i];
     }
     if (!batch || nbatch == 1) {
-        for (int a = 0; a < 3; ++a) warp_min_max_atomic(v[a], (long long*)ws_min + a, nullptr);
-    } else if (ok && b >= 0 && b < nbatch) {
-        for (int a = 0; a < 3; ++a) atomicMin((long long*)ws_min + 3 * b + a, v[a]);
+        int64_t* const dst[3] = {ws_min, ws_min + 1, ws_min + 2};
+        block_extrema_atomic<3, 3>(v, dst);
+    } else {
+        batch_min_atomic(v, b, ok && b >= 0 && b < nbatch, ws_min);
     }
 }
 
@@ -211,7 +269,7 @@ extern "C" int f3d_voxelize(const double* coords, int64_t n, const double* origi
     if (n < 0 || !(voxel_size > 0)) return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
     Origin o{{origin3_host[0], origin3_host[1], origin3_host[2]}};
-    voxelize_kernel<<<nblk(3 * n), kThreads, 0, (cudaStream_t)stream>>>(coords, n, o, voxel_size,
+    voxelize_kernel<<<nblk(n), kThreads, 0, (cudaStream_t)stream>>>(coords, n, o, voxel_size,
                                                                        vox_out);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
@@ -225,7 +283,7 @@ extern "C" int f3d_remap_nonnegative(const int64_t* vox, const int32_t* batch, i
     cudaStream_t st = (cudaStream_t)stream;
     init_stats_kernel<<<nblk(3 * nbatch + 7), kThreads, 0, st>>>(nullptr, ws, 3 * nbatch);
     batch_min_kernel<<<nblk(n), kThreads, 0, st>>>(vox, batch, n, nbatch, ws);
-    remap_kernel<<<nblk(3 * n), kThreads, 0, st>>>(vox, batch, n, nbatch, ws, vox_out);
+    remap_kernel<<<nblk(n), kThreads, 0, st>>>(vox, batch, n, nbatch, ws, vox_out);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
