@@ -87,13 +87,16 @@ struct Args {
 
 __device__ __forceinline__ float gelu_as(float x) {
     const float z = fabsf(x) * 0.70710678118654752f;
-    const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
+    float t;   // MUFU reciprocal / exp2 (approx): 1-2 ulp, far inside the 1.5e-7 formula error
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.f)));
     float pl = fmaf(1.061405429f, t, -1.453152027f);
     pl = fmaf(pl, t, 1.421413741f);
     pl = fmaf(pl, t, -0.284496736f);
     pl = fmaf(pl, t, 0.254829592f);
     pl *= t;
-    const float e = 1.f - pl * exp2f(-z * z * 1.4426950408889634f);
+    float ez;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ez) : "f"(-z * z * 1.4426950408889634f));
+    const float e = 1.f - pl * ez;
     return 0.5f * x * (1.f + copysignf(e, x));
 }
 
