@@ -95,11 +95,11 @@ _ERRS = {1: ConfigError, 2: RangeError, 3: IntegrityError, 5: EmptyInputError, 6
 # kernels each entry point launches (for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
     "f3d_voxelize": 1, "f3d_remap_nonnegative": 3, "f3d_hash_bucket": 2, "f3d_morton_encode": 2,
-    "f3d_voxel_hash": 3, "f3d_psh_assign": 1, "f3d_validate_assignment": 3,
+    "f3d_voxel_hash": 3, "f3d_psh_assign": 2, "f3d_validate_assignment": 5,
     "f3d_scatter_rows": 1, "f3d_gather_rows": 1, "f3d_scatter_rows_bf16_f32": 1, "f3d_bswin_attention": 1,
     "f3d_bswin_attention_tc": 1,
     "f3d_positional_encoding": 1, "f3d_stage_pe": 1, "f3d_coord_bbox": 2, "f3d_row_ln": 1,
-    "f3d_gelu_f64": 1, "f3d_bias_gelu": 1, "f3d_pool_build": 1, "f3d_pool_reduce": 1,
+    "f3d_gelu_f64": 1, "f3d_bias_gelu": 1, "f3d_pool_build": 2, "f3d_pool_reduce": 1,
     "f3d_plan_round": 1, "f3d_plan_rounds": 1, "f3d_plan_pool": 1, "f3d_mlp_fused": 1,
 }
 

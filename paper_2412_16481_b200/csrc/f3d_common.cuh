@@ -18,6 +18,10 @@
 
 void f3d_set_last_cuda_error(cudaError_t e);
 int f3d_num_sms();
+// Zero n int32 words with a kernel: a memset node in a CUDA graph may run on a
+// copy engine and then queues behind concurrent H2D/D2H traffic (measured:
+// 40 us stalls per step in the pipelined host loop).
+cudaError_t f3d_zero_i32(int32_t* p, int64_t n, cudaStream_t st);
 
 namespace f3d {
 

@@ -438,7 +438,7 @@ extern "C" int f3d_pool_build(const double* coords, const int32_t* tile_start,
                               const int32_t* ntiles_dev, void* stream) {
     if (rho < 1 || rho > 64 || ntiles < 0) return F3D_ERR_CONFIG;
     cudaStream_t st = (cudaStream_t)stream;
-    F3D_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    F3D_CUDA_TRY(f3d_zero_i32(flags, 1, st));
     if (ntiles == 0) return F3D_OK;
     pool::Args A{coords, tile_start, tile_m, tile_out, ntiles, ntiles_dev, rho, sub_out, members, sizes_out,
                  seeds_out, passes_out, flags};

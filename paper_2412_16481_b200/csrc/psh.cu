@@ -645,7 +645,7 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
     p.flags = (int32_t*)(w + L.flags);
     p.max_tiles = (int)(n / psh::kTile + nbatch + 1);
 
-    F3D_CUDA_TRY(cudaMemsetAsync(info_out, 0, 4 * sizeof(int32_t), st));
+    F3D_CUDA_TRY(f3d_zero_i32(info_out, 4, st));
     const int nbins = nbatch > 1 ? std::max(K + 1, nbatch) : K + 1;
     if (nbins > psh::kMaxBins) {
         psh_sequential_kernel<<<1, 1, 0, st>>>(p);

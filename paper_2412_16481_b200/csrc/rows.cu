@@ -189,12 +189,12 @@ extern "C" int f3d_validate_assignment(const int32_t* bucket_id, const int32_t* 
     if (n < 0 || nbatch < 1 || K < 0) return F3D_ERR_CONFIG;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t nslots = (int64_t)nbatch * (K + 1);
-    F3D_CUDA_TRY(cudaMemsetAsync(flags_out, 0, sizeof(int32_t), st));
+    F3D_CUDA_TRY(f3d_zero_i32(flags_out, 1, st));
     rows::validate_slots_kernel<<<1, rows::kThreads, 0, st>>>(counts, base, nslots, K, S, n,
                                                               flags_out);
     if (n > 0) {
         int32_t* seen = (int32_t*)ws;
-        F3D_CUDA_TRY(cudaMemsetAsync(seen, 0, sizeof(int32_t) * n, st));
+        F3D_CUDA_TRY(f3d_zero_i32(seen, n, st));
         const unsigned g = (unsigned)((n + rows::kThreads - 1) / rows::kThreads);
         rows::validate_points_kernel<<<g, rows::kThreads, 0, st>>>(
             bucket_id, bucket_offset, batch, counts, base, n, nbatch, K, seen, flags_out);
