@@ -138,3 +138,27 @@ def test_stream_host_pipelined_matches_single_calls():
     for i, (c, f) in enumerate(scenes):
         ref, n_ref = bb.forward_host(c, f)
         assert got[i].shape[0] == n_ref and torch.equal(got[i], ref)
+
+
+def test_backbone_recycle_heavy_matches_oracle():
+    """gaussian-clusters at a small K sends most points to the recycle bucket:
+    scopes mix regular buckets and S-row recycle chunks, several segments
+    each (cp.async fallback tiles); graph, eager and oracle agree."""
+    n = 12_000
+    coords = O.synth_cloud(21, n, "gaussian-clusters")
+    feats = np.random.default_rng(4).normal(size=(n, 96))
+    stages = (StageConfig(K=24, S=256, S_div=2048, W=2, stride=2, shift=1, pool_rho=2, seed=0),
+              StageConfig(K=12, S=256, S_div=4096, W=2, pool_rho=0, seed=1))
+    bb = Backbone(stages)
+    C = torch.tensor(coords, device="cuda")
+    X = torch.tensor(feats, dtype=torch.float32, device="cuda")
+    f, c = bb.forward(C, X)
+    assert bb.last_trace == [] and f.shape[0] == c.shape[0]
+    fg, cg = bb.forward_graph(C, X.to(torch.bfloat16))
+    assert torch.equal(c, cg)
+    of, oc = O.backbone_forward(coords, feats, stages, threads=8)
+    np.testing.assert_array_equal(c.cpu().numpy(), oc)
+    rel = np.linalg.norm(f.cpu().numpy().astype(np.float64) - of) / np.linalg.norm(of)
+    assert rel < 2e-2, rel
+    relg = np.linalg.norm(fg.cpu().numpy().astype(np.float64) - of) / np.linalg.norm(of)
+    assert relg < 2e-2, relg
