@@ -256,6 +256,10 @@ int f3d_pool_build(const double *coords, const int32_t *tile_start, const int32_
                    int32_t *members, int32_t *sizes_out, int32_t *seeds_out,
                    int32_t *passes_out, int32_t *flags, const int32_t *ntiles_dev,
                    void *stream);
+/* Pooling map for unpooling (no reference counterpart):
+ * parent[members[j*rho + r]] = j for r < sizes[j]. */
+int f3d_pool_parent(const int32_t *members, const int32_t *sizes, int64_t npool, int rho,
+                    int32_t *parent, const int32_t *npool_dev, void *stream);
 /* Replaces bw/pooling.py:166-184 pool_features: out[j] = reduce over
  * members of x (sequential in index order; mean = sum / size).
  * dtype: 0 bf16, 1 float, 2 double.  op: 0 sum, 1 mean, 2 min, 3 max.

@@ -19,7 +19,7 @@ from .geometry import PointCloud, VoxelGrid, synth_cloud, voxelize
 from .hashing import (HASH_KINDS, HashConfig, hash_bucket, morton_encode,
                       remap_nonnegative)
 from .pooling import (SubBucketAssignment, build_subbuckets, pool_features,
-                      pool_stage)
+                      pool_stage, pool_stage_map, unpool)
 from .stage import StageParams, gelu, init_params, layer_norm, stage_forward
 
 __version__ = "0.1.0"

@@ -480,3 +480,27 @@ extern "C" int f3d_pool_reduce(const void* x, int dtype, int64_t ldx, int d,
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
+
+// parent[members[j*rho + r]] = j for r < sizes[j]: the pooled row of every
+// scattered row, the map unpooling gathers by.
+__global__ void pool_parent_kernel(const int32_t* __restrict__ members,
+                                   const int32_t* __restrict__ sizes, int64_t npool,
+                                   const int32_t* npool_dev, int rho, int32_t* __restrict__ parent) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t j = t / rho;
+    const int r = (int)(t - j * rho);
+    if (j >= dyn_n(npool, npool_dev) || r >= sizes[j]) return;
+    const int32_t row = members[j * rho + r];
+    if (row >= 0) parent[row] = (int32_t)j;
+}
+
+extern "C" int f3d_pool_parent(const int32_t* members, const int32_t* sizes, int64_t npool,
+                               int rho, int32_t* parent, const int32_t* npool_dev, void* stream) {
+    if (npool < 0 || rho < 1 || rho > 64) return F3D_ERR_CONFIG;
+    if (npool == 0) return F3D_OK;
+    const int64_t tot = npool * rho;
+    pool_parent_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        members, sizes, npool, npool_dev, rho, parent);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}

@@ -232,7 +232,7 @@ def pool_stage(features, coords, assignment: BucketAssignment, rho: int, reduce:
 
 
 def pool_device(x, C, counts, base, K, S, nbatch, rho, reduce, check=True, assignment=True,
-                dev_counts=None):
+                dev_counts=None, want_parent=False):
     """Device path of pool_stage given host counts/base; returns device
     tensors and (optionally) a device-resident BucketAssignment.
     dev_counts = (counts_dev, base_dev) builds the tile table on the device."""
@@ -250,7 +250,61 @@ def pool_device(x, C, counts, base, K, S, nbatch, rho, reduce, check=True, assig
         if not hasattr(plan, "new_counts"):
             plan = TilePlan(counts, base, rho, x.device)
         na = new_assignment(plan.new_counts, K, max(1, math.ceil(S / rho)), nbatch, x.device)
+    if want_parent:
+        parent = L.empty((max(1, C.shape[0]),), torch.int32)
+        L.call("f3d_pool_parent", L.ptr(members), L.ptr(sizes), plan.npool, rho, L.ptr(parent),
+               None, L.stream())
+        return pf, pc, na, parent[:C.shape[0]]
     return pf, pc, na
+
+
+def pool_stage_map(features, coords, assignment: BucketAssignment, rho: int,
+                   reduce: str = "mean"):
+    """pool_stage plus the pooling map: parent[i] = pooled row of scattered
+    row i (the input of ``unpool``).  Returns
+    (pooled_features, pooled_coords, new_assignment, parent int64)."""
+    host = L.is_host(features)
+    x = features.to(L.device()) if isinstance(features, torch.Tensor) else \
+        L.to_dev(np.asarray(features, dtype=np.float64), torch.float64)
+    C = L.to_dev(coords, torch.float64).contiguous()
+    if x.shape[0] != len(assignment) or tuple(C.shape) != (x.shape[0], 3):
+        raise ConfigError("features/coords must match the assignment size")
+    if rho < 1 or rho > 64:
+        raise ConfigError(f"rho must be in [1, 64] on the GPU, got {rho}")
+    if reduce not in REDUCES:
+        raise ConfigError(f"reduce must be one of {REDUCES}, got {reduce!r}")
+    m = assignment._mirrors()
+    counts = m["counts"].cpu().numpy().astype(np.int64)
+    base = m["base"].cpu().numpy().astype(np.int64)
+    pf, pc, na, parent = pool_device(x, C, counts, base, assignment.K, assignment.S,
+                                     assignment.num_batches, rho, reduce, want_parent=True)
+    parent = parent.to(torch.int64)
+    if host:
+        return pf.cpu().numpy(), pc.cpu().numpy(), na.to_host(), parent.cpu().numpy()
+    return pf, pc, na, parent
+
+
+def unpool(pooled, parent):
+    """Unpooling of a pooled level back onto its finer rows: out[i] =
+    pooled[parent[i]] (f3d_gather_rows).  The reference has no unpooling
+    (SPEC.md:488); this is the builder-defined inverse of pool_stage's map."""
+    host = L.is_host(pooled)
+    p = pooled.to(L.device()) if isinstance(pooled, torch.Tensor) else \
+        L.to_dev(np.asarray(pooled), torch.float64)
+    if p.ndim == 1:
+        p = p[:, None]
+    p = p.contiguous()
+    idx = L.to_dev(parent, torch.int32)
+    n = idx.shape[0]
+    if n and (int(idx.min()) < 0 or int(idx.max()) >= p.shape[0]):
+        raise ConfigError("parent indices outside the pooled rows")
+    out = torch.empty((n, p.shape[1]), dtype=p.dtype, device=p.device)
+    rb = p.shape[1] * p.element_size()
+    if rb % 4:
+        raise ConfigError("row size must be a multiple of 4 bytes on the GPU")
+    if n:
+        L.call("f3d_gather_rows", L.ptr(p), L.ptr(idx), n, rb, L.ptr(out), None, L.stream())
+    return L.out(out, host)
 
 
 def new_assignment(new_counts, K, S_new, nbatch, dev) -> BucketAssignment:

@@ -98,3 +98,36 @@ def test_pool_features_matches_oracle_and_bf16_path():
     got = F.pool_features(xb, sub, "mean")
     ref = O.pool_reduce(xb.float().cpu().numpy(), np.asarray(sub.subbucket_id), np.asarray(sub.sizes), "mean")
     np.testing.assert_allclose(got.float().cpu().numpy(), ref, rtol=1e-2, atol=1e-2)
+
+
+def test_pool_stage_map_and_unpool_vs_oracle():
+    """parent[i] names the pooled row of scattered row i (tile-local sub id +
+    first pooled row of its tile, oracle-side); unpool gathers by it."""
+    coords = O.synth_cloud(9, 6000, "uniform-box")
+    vox = O.remap_nonnegative(O.voxelize(coords, (0, 0, 0), 1 / 32))
+    K, S = 24, 512
+    ids, offs, counts, base = O.psh_assign(vox, None, "zorder-div", K, S, 2048)
+    a = F.assign_buckets(vox, None, F.HashConfig("zorder-div", K=K, S_div=2048), S)
+    dest = O.dest_index(ids, offs, base, K)
+    Cs = np.empty_like(coords)
+    Cs[dest] = coords
+    feats = np.random.default_rng(2).normal(size=(6000, 8))
+    Fs = np.empty_like(feats)
+    Fs[dest] = feats
+    pf, pc, na, parent = F.pool_stage_map(Fs, Cs, a, 2, "mean")
+    of, oc, onc, _, sub_all = O.pool_stage(Fs, Cs, counts, base, K, S, 1, 2)
+    # oracle parent: pooled rows are laid out slot by slot, tile by tile
+    opar = np.empty(len(Fs), dtype=np.int64)
+    out0 = 0
+    for slot in range(K + 1):
+        st, cnt = int(base[slot]), int(counts[slot])
+        for t0 in range(0, cnt, 1024):
+            lo, hi = st + t0, st + min(t0 + 1024, cnt)
+            opar[lo:hi] = out0 + sub_all[lo:hi]
+            out0 += int(sub_all[lo:hi].max()) + 1
+    np.testing.assert_array_equal(parent, opar)
+    np.testing.assert_array_equal(pc, oc)
+    up = F.unpool(pc, parent)
+    np.testing.assert_array_equal(up, oc[opar])
+    with pytest.raises(ConfigError):
+        F.unpool(pc, np.array([len(pc)]))
