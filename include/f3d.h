@@ -159,14 +159,17 @@ int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_
  * lane, softmax warpgroups reading S / writing P with tcgen05.ld / st).  The
  * work list must step q_start by f3d_attention_tc_qstep(dh) (two 128-row Q
  * tiles share each K/V tile).  n_rows: rows of q/k/v (bounds of the TMA
- * tensor maps; 0 disables TMA).  Requires dh % 8 == 0, dh <= 128, 16-byte
- * aligned q/k/v and row strides that are multiples of 8; no mask. */
+ * tensor maps; 0 disables TMA).  lse (nullable, training): lse[row*ld_lse + h] =
+ * log2-domain logsumexp of the row's scaled scores, so P = exp2(s*scale*log2e -
+ * lse).  Requires dh % 8 == 0, dh <= 128, 16-byte aligned q/k/v and row strides
+ * that are multiples of 8; no mask. */
 int f3d_bswin_attention_tc(const void *q, const void *k, const void *v, int64_t ld_q,
                            int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
                            int dh, const int32_t *scope_seg, const int32_t *scope_nseg,
                            const int32_t *seg_start, const int32_t *seg_vstart,
                            const int32_t *scope_len, const int32_t *work, int nwork,
-                           const int32_t *live, int64_t n_rows, void *stream);
+                           const int32_t *live, int64_t n_rows, float *lse, int64_t ld_lse,
+                           void *stream);
 
 int f3d_attention_tc_qstep(int dh);
 
@@ -267,6 +270,26 @@ int f3d_pool_parent(const int32_t *members, const int32_t *sizes, int64_t npool,
 int f3d_pool_reduce(const void *x, int dtype, int64_t ldx, int d, const int32_t *members,
                     const int32_t *sizes, int64_t npool, int rho, int op, void *out,
                     int64_t ldo, const int32_t *npool_dev, void *stream);
+
+/* ------------------------------------------------ training
+ * LayerNorm backward fused with the residual add: dx = dres + rstd*(g*dy -
+ * mean(g*dy) - xhat*mean(g*dy*xhat)); dgain += sum dy*xhat, dbeta += sum dy
+ * (fp32 atomics).  x is the LN input (fp32), dy bf16 (dy_bf16=1) or fp32. */
+int f3d_ln_bwd(const float *x, int64_t ldx, const void *dy, int dy_bf16, int64_t ldy,
+               const float *gain, const float *dres, int64_t ldr, float *dx, int64_t ldd,
+               float *dgain, float *dbeta, int64_t n, int d, double eps, void *stream);
+/* du = dg * GELU'(u + bias) (exact erf form), dbias += sum du. */
+int f3d_gelu_bwd(const void *u_bf16, int64_t ldu, const float *bias, const float *dg,
+                 int64_t ldg, float *du, int64_t ldd, float *dbias, int64_t n, int h,
+                 void *stream);
+/* out[c] += sum_r x[r, c] (bias gradients). */
+int f3d_colsum(const void *x, int is_bf16, int64_t ldx, int64_t n, int d, float *out,
+               void *stream);
+/* Padded per-(scope, head) score tiles [B, M, M]: mode 0 turns S into
+ * P = exp2(S*scale_log2 - lse[b,i]) (rowv = lse), mode 1 turns dP into
+ * dS = P*(dP - D[b,i])*scale (rowv = D = rowsum(dO*O)); zero outside len[b]. */
+int f3d_softmax_bwd(float *T, const float *P, const float *rowv, const int32_t *len, int B,
+                    int M, double scale_log2, double scale, int mode, void *stream);
 
 #ifdef __cplusplus
 }

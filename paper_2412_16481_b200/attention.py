@@ -339,7 +339,8 @@ def _tc_ok(q, k, v, dh, mask, plan):
             and all(t.stride(0) % 8 == 0 and t.data_ptr() % 16 == 0 for t in (q, k, v)))
 
 
-def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, starved=None):
+def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, starved=None,
+           lse=None):
     """Launch bucket-swin attention for one round.  q/k/v: bf16 CUDA tensors
     whose rows hold heads side by side (head h at columns h*dh..), any row
     stride; out: bf16 or fp32 rows with the same head layout.  Uses the
@@ -349,8 +350,11 @@ def attend(q, k, v, out, plan: RoundPlan, n_heads: int, dh: int, mask=None, star
                v.stride(0), L.ptr(out), out.stride(0), int(out.dtype == torch.float32), n_heads,
                dh, L.ptr(plan.scope_seg), L.ptr(plan.scope_nseg), L.ptr(plan.seg_start),
                L.ptr(plan.seg_vstart), L.ptr(plan.scope_len), L.ptr(plan.work), plan.nwork,
-               L.ptr(plan.live), min(q.shape[0], k.shape[0], v.shape[0]), L.stream())
+               L.ptr(plan.live), min(q.shape[0], k.shape[0], v.shape[0]), L.ptr(lse),
+               0 if lse is None else lse.stride(0), L.stream())
         return
+    if lse is not None:
+        raise ConfigError("lse output needs the tcgen05 attention path")
     if getattr(plan, "qstep", BLOCK_M) != BLOCK_M:
         raise ConfigError("attention plan stride does not match the selected kernel")
     L.call("f3d_bswin_attention", L.ptr(q), L.ptr(k), L.ptr(v), q.stride(0), k.stride(0),

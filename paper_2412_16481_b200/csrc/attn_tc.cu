@@ -155,6 +155,8 @@ struct Args {
     const int32_t* live;   // optional device [nwork, ...]
     int use_tma;
     int o_vec;             // output rows allow 16-byte stores
+    float* lse;            // optional: per (row, head) log2-domain logsumexp (training)
+    int64_t ld_lse;
 };
 
 template <int DH>
@@ -670,6 +672,9 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
             const int vr = it.q0 + g * kBM + r;
             const bool live_row = vr < it.m;
             const int pr = live_row ? phys_row(A, it.s0, it.s1, vr) : 0;
+            // P = exp2(s * scale_log2 - lse) recomputes this row's softmax
+            if (A.lse && live_row && hh == 0)
+                A.lse[(int64_t)pr * A.ld_lse + it.h] = lsum > 0.f ? ms + __log2f(lsum) : -INFINITY;
             const int hcol = it.h * A.dh + hh * OC;     // this warp's output columns
 #pragma unroll
             for (int c = 0; c < OC / 16; ++c) {
@@ -834,7 +839,7 @@ extern "C" int f3d_bswin_attention_tc(const void* q, const void* k, const void* 
                                       const int32_t* scope_nseg, const int32_t* seg_start,
                                       const int32_t* seg_vstart, const int32_t* scope_len,
                                       const int32_t* work, int nwork, const int32_t* live,
-                                      int64_t n_rows, void* stream) {
+                                      int64_t n_rows, float* lse, int64_t ld_lse, void* stream) {
     if (H < 1 || dh < 8 || dh > 128 || (dh & 7) || nwork < 0 || n_rows < 0) return F3D_ERR_CONFIG;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v) & 15) return F3D_ERR_CONFIG;
     if ((ld_q | ld_k | ld_v) & 7) return F3D_ERR_CONFIG;
@@ -861,6 +866,8 @@ extern "C" int f3d_bswin_attention_tc(const void* q, const void* k, const void* 
     A.nwork = nwork;
     A.live = live;
     A.use_tma = 0;
+    A.lse = lse;
+    A.ld_lse = ld_lse;
     {
         const int esz = out_f32 ? 4 : 2;
         A.o_vec = (((uintptr_t)o & 15) == 0 && (ld_o * esz) % 16 == 0 && (dh * esz) % 16 == 0) ? 1 : 0;
