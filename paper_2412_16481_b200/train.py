@@ -1,0 +1,290 @@
+"""Training step of one bucket-swin stage on the GPU (SURVEY.md §8(f) #2,
+config E).  The reference has no backward pass; the
+forward is bw/stage.py:134-158 exactly as ``StageRunner.run`` executes it,
+with the activations each round's backward needs kept in HBM.
+
+Per round, in reverse (F_in -> F_mid -> F_out):
+
+    dF_out        -> db_out = colsum, dW_out = g^T dF, dg = dF W_out^T
+    f3d_gelu_bwd  -> du (and db_in),  dW_in = x2^T du,  dx2 = du W_in^T
+    f3d_ln_bwd    -> dF_mid = dF_out + LN2'(F_mid) dx2 (and dln2)
+                  -> db_o = colsum, dW_o = a^T dF_mid, da = dF_mid W_o^T
+    attention bwd -> dq, dk, dv on padded per-(scope, head) tiles:
+                     P = exp2(S*sl2 - lse) from the forward kernel's LSE
+                     (f3d_softmax_bwd mode 0), dV = P^T dO, dP = dO V^T,
+                     dS = P (dP - D) / sqrt(dh) (mode 1), dQ = dS K, dK = dS^T Q
+                  -> db_qkv = colsum, dW_qkv = x1^T dqkv, dx1 = dqkv W_qkv^T
+    f3d_ln_bwd    -> dF_in = dF_mid + LN1'(F_in) dx1 (and dln1)
+
+Weight gradients and the per-tile products are fp32 cuBLAS GEMMs (library
+GEMMs); the element-wise and row work is csrc/train.cu.  ``allreduce_grads``
+is the data-parallel exchange: one flat fp32 bucket, all_reduce(SUM)/world
+(NCCL on the GPU, gloo in the CPU tests).
+"""
+
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .attention import attend
+from .errors import ConfigError
+from .stage import LN_EPS, StageParams, StageRunner
+
+GRAD_NAMES = ("w_q", "w_k", "w_v", "w_o", "b_q", "b_k", "b_v", "b_o", "ln1_gain", "ln1_bias",
+              "ln2_gain", "ln2_bias", "w_in", "b_in", "w_out", "b_out")
+
+
+def scope_index(plan, n: int):
+    """Padded physical-row index of one round's scopes from the plan's host
+    tables: (idx (ns, M) int64 with pad value n, lens (ns,) int32), rows in
+    the scope's virtual (range) order — the order attention sees them."""
+    h = getattr(plan, "host", None)
+    if h is None:
+        raise ConfigError("training needs host-planned rounds (plan_schedule)")
+    seg, nseg = h["scope_seg"].astype(np.int64), h["scope_nseg"].astype(np.int64)
+    sst, svs = h["seg_start"].astype(np.int64), h["seg_vstart"].astype(np.int64)
+    slen = h["scope_len"].astype(np.int64)
+    live = np.flatnonzero(slen > 0)
+    ns = len(live)
+    M = int(slen.max()) if ns else 0
+    idx = np.full((ns, max(M, 1)), n, dtype=np.int64)
+    for i, s in enumerate(live):
+        a, k = seg[s], nseg[s]
+        for j in range(k):
+            v0 = svs[a + j]
+            v1 = svs[a + j + 1] if j + 1 < k else slen[s]
+            idx[i, v0:v1] = sst[a + j] + np.arange(v1 - v0)
+    return idx, slen[live].astype(np.int32)
+
+
+class _RoundIndex:
+    def __init__(self, plan, n, H, dev):
+        idx, lens = scope_index(plan, n)
+        self.ns, self.M = idx.shape
+        self.idx = torch.from_numpy(idx).to(dev)
+        self.flat = self.idx.reshape(-1)
+        self.valid = self.flat < n
+        self.rows = self.flat[self.valid]
+        self.len_bh = torch.from_numpy(np.repeat(lens, H)).to(dev)      # b = scope*H + h
+
+
+class DeviceWeights:
+    """fp32 master copies of a stage's parameters on the device plus the
+    bf16/fp32 operand dict the forward reads (StageParams.device_weights
+    layout); ``sgd`` updates the masters and re-casts in place, so trainers
+    sharing this object (one per scene) see the step with no host traffic."""
+
+    def __init__(self, params: StageParams):
+        f = lambda a: L.to_dev(a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a,
+                               torch.float32).contiguous()
+        self.master = {k: f(getattr(params, k)) for k in GRAD_NAMES}
+        self.d = params.d_model
+        self.w = params.device_weights()
+
+    def sync(self):
+        m, w, d = self.master, self.w, self.d
+        for i, k in enumerate(("w_q", "w_k", "w_v")):
+            w["w_qkv"][:, i * d:(i + 1) * d].copy_(m[k])
+        for i, k in enumerate(("b_q", "b_k", "b_v")):
+            w["b_qkv"][i * d:(i + 1) * d].copy_(m[k])
+        for k, mk in (("w_o", "w_o"), ("b_o", "b_o"), ("w_in", "w_in"), ("b_in", "b_in"),
+                      ("w_out", "w_out"), ("b_out", "b_out"), ("ln1_g", "ln1_gain"),
+                      ("ln1_b", "ln1_bias"), ("ln2_g", "ln2_gain"), ("ln2_b", "ln2_bias")):
+            w[k].copy_(m[mk])
+        w["w_in_t"].copy_(m["w_in"].t())
+        w["w_out_t"].copy_(m["w_out"].t())
+
+    def sgd(self, grads, lr: float):
+        for k in GRAD_NAMES:
+            self.master[k].add_(grads[k], alpha=-lr)
+        self.sync()
+
+
+class StageTrainer:
+    """Forward with saved activations and the backward of one stage over a
+    fixed scattered layout (host-planned rounds).  Residual stream fp32."""
+
+    def __init__(self, coords, table, schedule, params: StageParams, n: int,
+                 weights: DeviceWeights = None):
+        if params.d_model % 6:
+            raise ConfigError(f"d_model must be divisible by 6, got {params.d_model}")
+        self.p = params
+        self.n_dev = torch.tensor([n], dtype=torch.int32, device=L.device())
+        self.r = StageRunner(coords, table, schedule, params, n, torch.float32, n_dev=self.n_dev,
+                             weights=None if weights is None else weights.w)
+        self.n, self.d, self.H, self.dh = n, self.r.d, self.r.H, self.r.dh
+        self.ix = [_RoundIndex(p, n, self.H, L.device()) for p in self.r.plans]
+        self.saved = None
+
+    def refresh_weights(self):
+        """Re-cast the host parameters after a host-side update (sgd_step)."""
+        self.r.w = self.p.device_weights()
+
+    # ------------------------------------------------------------------ fwd
+    def forward(self, F: torch.Tensor) -> torch.Tensor:
+        """F (n, d) fp32 on the device, not modified; returns the stage output."""
+        r, w, n, d = self.r, self.r.w, self.n, self.d
+        if F.dtype != torch.float32 or tuple(F.shape) != (n, d):
+            raise ConfigError("training forward takes fp32 (n, d) features")
+        F = F.clone()
+        saved = []
+        y2 = None
+        for t, plan in enumerate(r.plans):
+            x1 = L.empty((n, d), torch.bfloat16)
+            if t == 0:
+                r._row_ln(F, None, None, w["ln1_g"], w["ln1_b"], True, x1)
+            else:
+                r._row_ln(F, y2, w["b_out"], w["ln1_g"], w["ln1_b"], True, x1)
+            F_in = F.clone()
+            qkv = torch.addmm(w["b_qkv"], x1, w["w_qkv"])
+            q, k, v = (qkv[:, i * d:(i + 1) * d] for i in range(3))
+            a = L.empty((n, d), torch.bfloat16)
+            lse = L.empty((n, self.H), torch.float32)
+            attend(q, k, v, a, plan, self.H, self.dh, lse=lse)
+            y = torch.mm(a, w["w_o"])
+            x2 = L.empty((n, d), torch.bfloat16)
+            r._row_ln(F, y, w["b_o"], w["ln2_g"], w["ln2_b"], None, x2)
+            F_mid = F.clone()
+            u = torch.mm(x2, w["w_in"])
+            g = u.clone()
+            L.call("f3d_bias_gelu", L.ptr(g), n, g.shape[1], L.ptr(w["b_in"]), L.stream())
+            y2 = torch.mm(g, w["w_out"])
+            saved.append(dict(F_in=F_in, x1=x1, qkv=qkv, a=a, lse=lse, F_mid=F_mid, x2=x2, u=u,
+                              g=g))
+        if y2 is not None:
+            r._row_ln(F, y2, w["b_out"], None, None, None, None)
+        self.saved = saved
+        return F
+
+    # ------------------------------------------------------------------ bwd
+    def _attn_bwd(self, ix: _RoundIndex, qkv, a, lse, da):
+        """dq|dk|dv (n, 3d) fp32 from the saved bf16 q/k/v/out and the LSE."""
+        n, d, H, dh = self.n, self.d, self.H, self.dh
+        ns, M, B = ix.ns, ix.M, ix.ns * H
+
+        def tiles(x):               # (n, d) rows -> (B, M, dh) fp32, zero pad row
+            xp = torch.cat([x.float(), x.new_zeros((1, d), dtype=torch.float32)])
+            return xp[ix.idx].view(ns, M, H, dh).permute(0, 2, 1, 3).reshape(B, M, dh)
+
+        Q, K, V = (tiles(qkv[:, i * d:(i + 1) * d]) for i in range(3))
+        O, dO = tiles(a), tiles(da)
+        lse_p = torch.cat([lse, lse.new_zeros((1, H))])[ix.idx]          # (ns, M, H)
+        lse_b = lse_p.permute(0, 2, 1).reshape(B, M).contiguous()
+        Dv = (dO * O).sum(-1).contiguous()
+        sl2 = 1.4426950408889634 / math.sqrt(dh)
+        P = torch.bmm(Q, K.transpose(1, 2))
+        L.call("f3d_softmax_bwd", L.ptr(P), None, L.ptr(lse_b), L.ptr(ix.len_bh), B, M, sl2, 0.0,
+               0, L.stream())
+        dV = torch.bmm(P.transpose(1, 2), dO)
+        dS = torch.bmm(dO, V.transpose(1, 2))
+        L.call("f3d_softmax_bwd", L.ptr(dS), L.ptr(P), L.ptr(Dv), L.ptr(ix.len_bh), B, M, sl2,
+               1.0 / math.sqrt(dh), 1, L.stream())
+        dQ = torch.bmm(dS, K)
+        dK = torch.bmm(dS.transpose(1, 2), Q)
+        out = torch.zeros((n, 3 * d), dtype=torch.float32, device=qkv.device)
+        for i, t in enumerate((dQ, dK, dV)):
+            rows = t.view(ns, H, M, dh).permute(0, 2, 1, 3).reshape(ns * M, d)[ix.valid]
+            out[:, i * d:(i + 1) * d].index_copy_(0, ix.rows, rows)
+        return out
+
+    def _ln_bwd(self, x, dy, gain, dres, dgain, dbeta):
+        dx = torch.empty_like(x)
+        L.call("f3d_ln_bwd", L.ptr(x), x.stride(0), L.ptr(dy), int(dy.dtype == torch.bfloat16),
+               dy.stride(0), L.ptr(gain), L.ptr(dres), dres.stride(0), L.ptr(dx), dx.stride(0),
+               L.ptr(dgain), L.ptr(dbeta), self.n, self.d, LN_EPS, L.stream())
+        return dx
+
+    def _colsum(self, x, out):
+        L.call("f3d_colsum", L.ptr(x), int(x.dtype == torch.bfloat16), x.stride(0), x.shape[0],
+               x.shape[1], L.ptr(out), L.stream())
+
+    def backward(self, dF: torch.Tensor):
+        """dF: gradient of the loss w.r.t. the stage output (n, d) fp32.
+        Returns (dF_in, grads) with grads keyed by GRAD_NAMES (fp32, device)."""
+        if self.saved is None:
+            raise ConfigError("backward() needs a preceding forward()")
+        w, n, d = self.r.w, self.n, self.d
+        dev = dF.device
+        z = lambda *s: torch.zeros(s, dtype=torch.float32, device=dev)
+        dhid = self.p.d_hidden
+        G = dict(w_qkv=z(d, 3 * d), b_qkv=z(3 * d), w_o=z(d, d), b_o=z(d), ln1_gain=z(d),
+                 ln1_bias=z(d), ln2_gain=z(d), ln2_bias=z(d), w_in=z(d, dhid), b_in=z(dhid),
+                 w_out=z(dhid, d), b_out=z(d))
+        wf = {k: w[k].float() for k in ("w_qkv", "w_o", "w_in", "w_out")}
+        dF = dF.contiguous().float()
+        for t in reversed(range(len(self.r.plans))):
+            s = self.saved[t]
+            self._colsum(dF, G["b_out"])
+            G["w_out"].addmm_(s["g"].float().t(), dF)
+            dg = torch.mm(dF, wf["w_out"].t())
+            du = torch.empty_like(dg)
+            L.call("f3d_gelu_bwd", L.ptr(s["u"]), s["u"].stride(0), L.ptr(w["b_in"]), L.ptr(dg),
+                   dg.stride(0), L.ptr(du), du.stride(0), L.ptr(G["b_in"]), n, dhid, L.stream())
+            G["w_in"].addmm_(s["x2"].float().t(), du)
+            dx2 = torch.mm(du, wf["w_in"].t())
+            dF = self._ln_bwd(s["F_mid"], dx2, w["ln2_g"], dF, G["ln2_gain"], G["ln2_bias"])
+            self._colsum(dF, G["b_o"])
+            G["w_o"].addmm_(s["a"].float().t(), dF)
+            da = torch.mm(dF, wf["w_o"].t())
+            dqkv = self._attn_bwd(self.ix[t], s["qkv"], s["a"], s["lse"], da)
+            self._colsum(dqkv, G["b_qkv"])
+            G["w_qkv"].addmm_(s["x1"].float().t(), dqkv)
+            dx1 = torch.mm(dqkv, wf["w_qkv"].t())
+            dF = self._ln_bwd(s["F_in"], dx1, w["ln1_g"], dF, G["ln1_gain"], G["ln1_bias"])
+        self.saved = None
+        grads = {"w_q": G["w_qkv"][:, :d], "w_k": G["w_qkv"][:, d:2 * d],
+                 "w_v": G["w_qkv"][:, 2 * d:], "b_q": G["b_qkv"][:d], "b_k": G["b_qkv"][d:2 * d],
+                 "b_v": G["b_qkv"][2 * d:]}
+        for k in ("w_o", "b_o", "ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias", "w_in", "b_in",
+                  "w_out", "b_out"):
+            grads[k] = G[k]
+        return dF, grads
+
+
+def accumulate_grads(acc, grads):
+    """acc += grads (per-scene gradients of one rank's batch); acc None -> copy."""
+    if acc is None:
+        return {k: grads[k].clone() for k in GRAD_NAMES}
+    for k in GRAD_NAMES:
+        acc[k].add_(grads[k])
+    return acc
+
+
+def flatten_grads(grads):
+    """One contiguous fp32 bucket in GRAD_NAMES order (the all-reduce message)."""
+    return torch.cat([grads[k].reshape(-1).float() for k in GRAD_NAMES])
+
+
+def unflatten_grads(flat, like):
+    out, o = {}, 0
+    for k in GRAD_NAMES:
+        m = like[k].numel()
+        out[k] = flat[o:o + m].view(like[k].shape)
+        o += m
+    return out
+
+
+def allreduce_grads(grads, group=None):
+    """Data-parallel gradient average: all_reduce(SUM) of one flat bucket,
+    divided by the world size.  No-op without a process
+    group."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return grads
+    flat = flatten_grads(grads)
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    flat /= dist.get_world_size(group)
+    return unflatten_grads(flat, grads)
+
+
+def sgd_step(params: StageParams, grads, lr: float):
+    """In-place SGD on the host-side parameter arrays (or fp32 tensors)."""
+    for k in GRAD_NAMES:
+        cur = getattr(params, k)
+        g = grads[k].detach()
+        if isinstance(cur, torch.Tensor):
+            cur.sub_(lr * g.to(cur.device, cur.dtype))
+        else:
+            cur -= lr * g.double().cpu().numpy()
