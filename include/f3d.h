@@ -285,11 +285,13 @@ int f3d_gelu_bwd(const void *u_bf16, int64_t ldu, const float *bias, const float
 /* out[c] += sum_r x[r, c] (bias gradients). */
 int f3d_colsum(const void *x, int is_bf16, int64_t ldx, int64_t n, int d, float *out,
                void *stream);
-/* Padded per-(scope, head) score tiles [B, M, M]: mode 0 turns S into
- * P = exp2(S*scale_log2 - lse[b,i]) (rowv = lse), mode 1 turns dP into
- * dS = P*(dP - D[b,i])*scale (rowv = D = rowsum(dO*O)); zero outside len[b]. */
-int f3d_softmax_bwd(float *T, const float *P, const float *rowv, const int32_t *len, int B,
-                    int M, double scale_log2, double scale, int mode, void *stream);
+/* Padded per-(scope, head) score tiles [B, M, M] (M % 8 == 0): T is the fp32
+ * GEMM output, out the bf16 operand of the next GEMM.  mode 0: out = P =
+ * exp2(T*scale_log2 - rowv[b,i]) (rowv = lse); mode 1 (T = dP, P = the mode-0
+ * bf16 output): out = dS = P*(dP - rowv[b,i])*scale (rowv = D = rowsum(dO*O)).
+ * Zero outside len[b] rows/keys. */
+int f3d_softmax_bwd(const float *T, const void *P, const float *rowv, const int32_t *len, int B,
+                    int M, double scale_log2, double scale, int mode, void *out, void *stream);
 
 #ifdef __cplusplus
 }

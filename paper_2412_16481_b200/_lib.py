@@ -69,7 +69,7 @@ SIGNATURES = {
                           _P]),
     "f3d_gelu_bwd": (_INT, [_P, _I64, _P, _P, _I64, _P, _I64, _P, _I64, _INT, _P]),
     "f3d_colsum": (_INT, [_P, _INT, _I64, _I64, _INT, _P, _P]),
-    "f3d_softmax_bwd": (_INT, [_P, _P, _P, _P, _INT, _INT, _F64, _F64, _INT, _P]),
+    "f3d_softmax_bwd": (_INT, [_P, _P, _P, _P, _INT, _INT, _F64, _F64, _INT, _P, _P]),
     "f3d_mlp_supported": (_INT, [_INT]),
     "f3d_mlp_fused": (_INT, [_P, _I64, _I64, _INT, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _F64,
                              _P, _I64, _F64, _P, _P]),

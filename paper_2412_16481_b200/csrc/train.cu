@@ -4,7 +4,8 @@
 //   * GELU backward with the bias gradient (erf form, fp32);
 //   * column sums (bias gradients) with block partials + fp32 atomics;
 //   * the softmax part of the attention backward on padded per-(scope, head)
-//     score tiles: P = exp2(S*sl2 - lse) and dS = P (dP - D) * scale, in place.
+//     score tiles: P = exp2(S*sl2 - lse) and dS = P (dP - D) * scale, fp32 GEMM
+//     outputs in, bf16 GEMM operands out.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -120,25 +121,57 @@ __global__ void __launch_bounds__(kThreads) colsum_kernel(const void* __restrict
 }
 
 // Padded score tiles [B, M, M] (row-major, B = scopes x heads); len[b] real
-// rows/keys.  mode 0: S -> P = exp2(S*sl2 - lse[b,i]) (0 outside len);
-// mode 1: dP -> dS = P (dP - D[b,i]) * scale.
+// rows/keys.  T: fp32 GEMM output, out: bf16 operand of the next GEMM.
+// mode 0: out = P = exp2(T*sl2 - lse[b,i]);  mode 1 (T = dP, P = mode-0 out):
+// out = dS = P (dP - D[b,i]) * scale.  Zero outside len.  Eight elements per
+// thread (M % 8 == 0): 32 B fp32 loads, 16 B bf16 stores.
 __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(
-    float* __restrict__ T, const float* __restrict__ P, const float* __restrict__ rowv,
-    const int32_t* __restrict__ len, int B, int M, float sl2, float scale, int mode) {
-    const int64_t tot = (int64_t)B * M * M;
-    for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < tot;
+    const float* __restrict__ T, const __nv_bfloat16* __restrict__ P,
+    const float* __restrict__ rowv, const int32_t* __restrict__ len, int B, int M, float sl2,
+    float scale, int mode, __nv_bfloat16* __restrict__ out) {
+    const int64_t tot8 = (int64_t)B * M * M / 8;
+    const int M8 = M / 8;
+    for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < tot8;
          t += (int64_t)gridDim.x * kThreads) {
-        const int64_t bi = t / M;            // (b, i)
-        const int j = (int)(t - bi * M);
+        const int64_t bi = t / M8;           // (b, i)
+        const int j0 = (int)(t - bi * M8) * 8;
         const int b = (int)(bi / M);
         const int i = (int)(bi - (int64_t)b * M);
         const int m = len[b];
-        if (i >= m || j >= m) {
-            T[t] = 0.f;
-            continue;
+        uint4 o = make_uint4(0, 0, 0, 0);
+        if (i < m && j0 < m) {
+            const float4 a = reinterpret_cast<const float4*>(T)[2 * t];
+            const float4 c = reinterpret_cast<const float4*>(T)[2 * t + 1];
+            float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+            const float r = rowv[bi];
+            float p[8];
+            if (mode == 1) {
+                const uint4 pp = reinterpret_cast<const uint4*>(P)[t];
+                const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pp);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(ph[e]);
+                    p[2 * e] = f.x;
+                    p[2 * e + 1] = f.y;
+                }
+            }
+            __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float x0, x1;
+                if (mode == 0) {
+                    x0 = exp2f(fmaf(v[2 * e], sl2, -r));
+                    x1 = exp2f(fmaf(v[2 * e + 1], sl2, -r));
+                } else {
+                    x0 = p[2 * e] * (v[2 * e] - r) * scale;
+                    x1 = p[2 * e + 1] * (v[2 * e + 1] - r) * scale;
+                }
+                if (j0 + 2 * e >= m) x0 = 0.f;
+                if (j0 + 2 * e + 1 >= m) x1 = 0.f;
+                oh[e] = __floats2bfloat162_rn(x0, x1);
+            }
         }
-        if (mode == 0) T[t] = exp2f(T[t] * sl2 - rowv[bi]);
-        else T[t] = P[t] * (T[t] - rowv[bi]) * scale;
+        reinterpret_cast<uint4*>(out)[t] = o;
     }
 }
 
@@ -190,14 +223,16 @@ extern "C" int f3d_colsum(const void* x, int is_bf16, int64_t ldx, int64_t n, in
     return F3D_OK;
 }
 
-extern "C" int f3d_softmax_bwd(float* T, const float* P, const float* rowv, const int32_t* len,
-                               int B, int M, double scale_log2, double scale, int mode,
-                               void* stream) {
-    if (B < 0 || M < 1 || mode < 0 || mode > 1) return F3D_ERR_CONFIG;
+extern "C" int f3d_softmax_bwd(const float* T, const void* P, const float* rowv,
+                               const int32_t* len, int B, int M, double scale_log2, double scale,
+                               int mode, void* out, void* stream) {
+    if (B < 0 || M < 8 || M % 8 || mode < 0 || mode > 1 || (mode == 1 && !P))
+        return F3D_ERR_CONFIG;
     if (B == 0) return F3D_OK;
-    train::softmax_bwd_kernel<<<grid_cap((int64_t)B * M * M, train::kThreads, 32),
+    train::softmax_bwd_kernel<<<grid_cap((int64_t)B * M * M / 8, train::kThreads, 16),
                                 train::kThreads, 0, (cudaStream_t)stream>>>(
-        T, P, rowv, len, B, M, (float)scale_log2, (float)scale, mode);
+        T, (const __nv_bfloat16*)P, rowv, len, B, M, (float)scale_log2, (float)scale, mode,
+        (__nv_bfloat16*)out);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

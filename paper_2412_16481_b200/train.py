@@ -16,8 +16,10 @@ Per round, in reverse (F_in -> F_mid -> F_out):
                   -> db_qkv = colsum, dW_qkv = x1^T dqkv, dx1 = dqkv W_qkv^T
     f3d_ln_bwd    -> dF_in = dF_mid + LN1'(F_in) dx1 (and dln1)
 
-Weight gradients and the per-tile products are fp32 cuBLAS GEMMs (library
-GEMMs); the element-wise and row work is csrc/train.cu.  ``allreduce_grads``
+Weight gradients and the per-tile products are bf16 tensor-core cuBLAS GEMMs
+with fp32 outputs (library GEMMs; activation gradients are rounded to bf16 as
+GEMM operands, the residual-stream gradient stays fp32); the element-wise and
+row work is csrc/train.cu.  ``allreduce_grads``
 is the data-parallel exchange: one flat fp32 bucket, all_reduce(SUM)/world
 (NCCL on the GPU, gloo in the CPU tests).
 """
@@ -39,7 +41,8 @@ GRAD_NAMES = ("w_q", "w_k", "w_v", "w_o", "b_q", "b_k", "b_v", "b_o", "ln1_gain"
 
 def scope_index(plan, n: int):
     """Padded physical-row index of one round's scopes from the plan's host
-    tables: (idx (ns, M) int64 with pad value n, lens (ns,) int32), rows in
+    tables: (idx (ns, M) int64 with pad value n, M the longest scope rounded
+    up to 16, lens (ns,) int32), rows in
     the scope's virtual (range) order — the order attention sees them."""
     h = getattr(plan, "host", None)
     if h is None:
@@ -49,8 +52,8 @@ def scope_index(plan, n: int):
     slen = h["scope_len"].astype(np.int64)
     live = np.flatnonzero(slen > 0)
     ns = len(live)
-    M = int(slen.max()) if ns else 0
-    idx = np.full((ns, max(M, 1)), n, dtype=np.int64)
+    M = -(-int(slen.max()) // 16) * 16 if ns else 16          # GEMM / 16 B vector friendly
+    idx = np.full((ns, M), n, dtype=np.int64)
     for i, s in enumerate(live):
         a, k = seg[s], nseg[s]
         for j in range(k):
@@ -161,30 +164,40 @@ class StageTrainer:
 
     # ------------------------------------------------------------------ bwd
     def _attn_bwd(self, ix: _RoundIndex, qkv, a, lse, da):
-        """dq|dk|dv (n, 3d) fp32 from the saved bf16 q/k/v/out and the LSE."""
+        """dq|dk|dv (n, 3d) fp32 from the saved bf16 q/k/v/out, the LSE and
+        da (fp32).  bf16 tensor-core GEMMs with fp32 outputs; P and dS are
+        rounded to bf16 as GEMM operands (as the forward kernel rounds P)."""
         n, d, H, dh = self.n, self.d, self.H, self.dh
         ns, M, B = ix.ns, ix.M, ix.ns * H
+        bf = torch.bfloat16
 
-        def tiles(x):               # (n, d) rows -> (B, M, dh) fp32, zero pad row
-            xp = torch.cat([x.float(), x.new_zeros((1, d), dtype=torch.float32)])
+        def tiles(x):               # (n, d) bf16 rows -> (B, M, dh), zero pad row
+            xp = torch.cat([x, x.new_zeros((1, d))])
             return xp[ix.idx].view(ns, M, H, dh).permute(0, 2, 1, 3).reshape(B, M, dh)
 
+        def row_tiles(r):           # (n, H) fp32 -> (B, M)
+            rp = torch.cat([r, r.new_zeros((1, H))])[ix.idx]
+            return rp.permute(0, 2, 1).reshape(B, M).contiguous()
+
         Q, K, V = (tiles(qkv[:, i * d:(i + 1) * d]) for i in range(3))
-        O, dO = tiles(a), tiles(da)
-        lse_p = torch.cat([lse, lse.new_zeros((1, H))])[ix.idx]          # (ns, M, H)
-        lse_b = lse_p.permute(0, 2, 1).reshape(B, M).contiguous()
-        Dv = (dO * O).sum(-1).contiguous()
+        dO = tiles(da.to(bf))
+        Dv = row_tiles((da.view(n, H, dh) * a.view(n, H, dh).float()).sum(-1))
+        lse_b = row_tiles(lse)
         sl2 = 1.4426950408889634 / math.sqrt(dh)
-        P = torch.bmm(Q, K.transpose(1, 2))
-        L.call("f3d_softmax_bwd", L.ptr(P), None, L.ptr(lse_b), L.ptr(ix.len_bh), B, M, sl2, 0.0,
-               0, L.stream())
-        dV = torch.bmm(P.transpose(1, 2), dO)
-        dS = torch.bmm(dO, V.transpose(1, 2))
-        L.call("f3d_softmax_bwd", L.ptr(dS), L.ptr(P), L.ptr(Dv), L.ptr(ix.len_bh), B, M, sl2,
-               1.0 / math.sqrt(dh), 1, L.stream())
-        dQ = torch.bmm(dS, K)
-        dK = torch.bmm(dS.transpose(1, 2), Q)
-        out = torch.zeros((n, 3 * d), dtype=torch.float32, device=qkv.device)
+        S = torch.bmm(Q, K.transpose(1, 2), out_dtype=torch.float32)
+        P = torch.empty((B, M, M), dtype=bf, device=qkv.device)
+        L.call("f3d_softmax_bwd", L.ptr(S), None, L.ptr(lse_b), L.ptr(ix.len_bh), B, M, sl2, 0.0,
+               0, L.ptr(P), L.stream())
+        del S
+        dV = torch.bmm(P.transpose(1, 2), dO, out_dtype=torch.float32)
+        dP = torch.bmm(dO, V.transpose(1, 2), out_dtype=torch.float32)
+        dS = torch.empty_like(P)
+        L.call("f3d_softmax_bwd", L.ptr(dP), L.ptr(P), L.ptr(Dv), L.ptr(ix.len_bh), B, M, sl2,
+               1.0 / math.sqrt(dh), 1, L.ptr(dS), L.stream())
+        del dP, P
+        dQ = torch.bmm(dS, K, out_dtype=torch.float32)
+        dK = torch.bmm(dS.transpose(1, 2), Q, out_dtype=torch.float32)
+        out = torch.empty((n, 3 * d), dtype=torch.float32, device=qkv.device)
         for i, t in enumerate((dQ, dK, dV)):
             rows = t.view(ns, H, M, dh).permute(0, 2, 1, 3).reshape(ns * M, d)[ix.valid]
             out[:, i * d:(i + 1) * d].index_copy_(0, ix.rows, rows)
@@ -213,26 +226,31 @@ class StageTrainer:
         G = dict(w_qkv=z(d, 3 * d), b_qkv=z(3 * d), w_o=z(d, d), b_o=z(d), ln1_gain=z(d),
                  ln1_bias=z(d), ln2_gain=z(d), ln2_bias=z(d), w_in=z(d, dhid), b_in=z(dhid),
                  w_out=z(dhid, d), b_out=z(d))
-        wf = {k: w[k].float() for k in ("w_qkv", "w_o", "w_in", "w_out")}
+        bf = torch.bfloat16
+        mm = lambda x, y: torch.mm(x, y, out_dtype=torch.float32)   # bf16 TC, fp32 out
         dF = dF.contiguous().float()
         for t in reversed(range(len(self.r.plans))):
             s = self.saved[t]
+            dFb = dF.to(bf)
             self._colsum(dF, G["b_out"])
-            G["w_out"].addmm_(s["g"].float().t(), dF)
-            dg = torch.mm(dF, wf["w_out"].t())
+            G["w_out"] += mm(s["g"].t(), dFb)
+            dg = mm(dFb, w["w_out"].t())
             du = torch.empty_like(dg)
             L.call("f3d_gelu_bwd", L.ptr(s["u"]), s["u"].stride(0), L.ptr(w["b_in"]), L.ptr(dg),
                    dg.stride(0), L.ptr(du), du.stride(0), L.ptr(G["b_in"]), n, dhid, L.stream())
-            G["w_in"].addmm_(s["x2"].float().t(), du)
-            dx2 = torch.mm(du, wf["w_in"].t())
+            dub = du.to(bf)
+            G["w_in"] += mm(s["x2"].t(), dub)
+            dx2 = mm(dub, w["w_in"].t())
             dF = self._ln_bwd(s["F_mid"], dx2, w["ln2_g"], dF, G["ln2_gain"], G["ln2_bias"])
+            dFb = dF.to(bf)
             self._colsum(dF, G["b_o"])
-            G["w_o"].addmm_(s["a"].float().t(), dF)
-            da = torch.mm(dF, wf["w_o"].t())
+            G["w_o"] += mm(s["a"].t(), dFb)
+            da = mm(dFb, w["w_o"].t())
             dqkv = self._attn_bwd(self.ix[t], s["qkv"], s["a"], s["lse"], da)
             self._colsum(dqkv, G["b_qkv"])
-            G["w_qkv"].addmm_(s["x1"].float().t(), dqkv)
-            dx1 = torch.mm(dqkv, wf["w_qkv"].t())
+            dqb = dqkv.to(bf)
+            G["w_qkv"] += mm(s["x1"].t(), dqb)
+            dx1 = mm(dqb, w["w_qkv"].t())
             dF = self._ln_bwd(s["F_in"], dx1, w["ln1_g"], dF, G["ln1_gain"], G["ln1_bias"])
         self.saved = None
         grads = {"w_q": G["w_qkv"][:, :d], "w_k": G["w_qkv"][:, d:2 * d],

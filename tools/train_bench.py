@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--points", type=int, default=100_000)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--profile", action="store_true", help="print the top kernels of one step")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -73,6 +74,13 @@ def main():
 
     for _ in range(a.warmup):
         step()
+    if a.profile and rank == 0:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=30, max_name_column_width=70))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier(device_ids=[local])
