@@ -207,6 +207,22 @@ def wide_attention_roofline(tflops_peak, iters=5):
             "launches_per_step": len(plans)}
 
 
+def _ncu_traffic():
+    """DRAM bytes per attention launch from the committed ncu --set full capture
+    (profiles/r1_attn_ncu_traffic.json: dram__bytes_read.sum + write.sum of the
+    four launches of one graph-replayed step) next to the algorithmic bytes."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                     "r1_attn_ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            t = json.load(fh)
+        return {"traffic": t["traffic_bytes_per_launch"],
+                "traffic_algorithmic": t["algorithmic_bytes_per_launch"],
+                "traffic_source": "profiles/r1_attn_ncu_traffic.json (ncu --set full, per launch)"}
+    except (OSError, KeyError, ValueError):
+        return {"traffic": None}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -382,7 +398,7 @@ def main():
                        "l2": "flushed (256 MiB write) between timed steps"},
             "roofline": {"kernel": attn_name, "bound": "tensor",
                          "achieved": round(attn_tf, 2), "peak": tflops, "unit": "TFLOP/s",
-                         "frac": round(attn_tf / tflops, 4), "traffic": None,
+                         "frac": round(attn_tf / tflops, 4), **_ncu_traffic(),
                          "peak_source": src,
                          "flops_per_step": attn_flops, "ms_per_step": round(attn_ms, 4),
                          "note": "dh=24 (padded 32): exp/MUFU-bound, see DESIGN.md"},
