@@ -88,9 +88,49 @@ constexpr int kMaps = 6;          // TMA maps: {q, k, v} x {first block, second 
 // 1 pair in poly_every<DH>() uses ex2_poly (0: none).  Measured (config B
 // dh=24: 2 % faster with 1 in 4; config D dh=128: 7 % slower): the softmax is
 // issue-bound, not MUFU-bound, once dh >= 64.
+#ifndef F3D_POLY_SMALL
+#define F3D_POLY_SMALL 4
+#endif
+#ifndef F3D_POLY_MID
+#define F3D_POLY_MID 0
+#endif
+#ifndef F3D_POLY_LARGE
+#define F3D_POLY_LARGE 0
+#endif
 template <int DH>
 __host__ __device__ constexpr int poly_every() {
-    return DH <= 32 ? 4 : 0;
+    return DH <= 32 ? F3D_POLY_SMALL : DH <= 64 ? F3D_POLY_MID : F3D_POLY_LARGE;
+}
+
+// Packed fp32 pairs (sm_100 FFMA2/FADD2/FMUL2: two lanes' worth of fp32 math
+// per issue slot; the softmax is issue-bound once the MUFU share is offloaded).
+__device__ __forceinline__ uint64_t f2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
 }
 
 // 2^x on the FMA/ALU pipes for x <= 2^8 (softmax arguments): round x to
@@ -105,6 +145,25 @@ __device__ __forceinline__ float ex2_poly(float x) {
     p = fmaf(p, f, 0.6931471805599453f);
     p = fmaf(p, f, 1.f);
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// ex2_poly on a packed pair: the rounding trick and the cubic run as f32x2.
+__device__ __forceinline__ void ex2_poly2(uint64_t a, float& p0, float& p1) {
+    float x0, x1;
+    f2_split(a, x0, x1);
+    const uint64_t x = f2(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+    const uint64_t C = f2(12582912.f, 12582912.f);
+    const uint64_t t = fadd2(x, C);
+    const uint64_t f = fsub2(x, fsub2(t, C));
+    uint64_t p = ffma2(f2(0.0555041086648216f, 0.0555041086648216f), f,
+                       f2(0.2402264923172690f, 0.2402264923172690f));
+    p = ffma2(p, f, f2(0.6931471805599453f, 0.6931471805599453f));
+    p = ffma2(p, f, f2(1.f, 1.f));
+    float q0, q1, t0, t1;
+    f2_split(p, q0, q1);
+    f2_split(t, t0, t1);
+    p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+    p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
 }
 
 __host__ __device__ constexpr int dh_tile(int dh) {   // padded head dim of the kernel
@@ -608,15 +667,22 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
                             uint32_t y[16];
                             tmem_ld16(ocols + c, y);
                             tmem_wait_ld();
+                            const uint64_t al2 = f2(alpha, alpha);
 #pragma unroll
-                            for (int e = 0; e < 16; ++e)
-                                y[e] = __float_as_uint(__uint_as_float(y[e]) * alpha);
+                            for (int e = 0; e < 16; e += 2) {
+                                float u0, u1;
+                                f2_split(fmul2(f2(__uint_as_float(y[e]), __uint_as_float(y[e + 1])), al2),
+                                         u0, u1);
+                                y[e] = __float_as_uint(u0);
+                                y[e + 1] = __float_as_uint(u1);
+                            }
                             tmem_st16(ocols + c, y);
                         }
                     }
                 }
                 // P = exp2(s*sl2 - ms) (<= 2^8) -> bf16 pairs over the S columns
                 const float nms = -ms;
+                const uint64_t sl2x2 = f2(sl2, sl2), nms2 = f2(nms, nms);
                 PROF_MARK(te0);
                 float sum = 0.f;
 #pragma unroll
@@ -627,12 +693,19 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
 #else
                     // every kPolyEvery-th pair on the FMA pipe: the MUFU unit
                     // (16 ex2/clk/SM) is the softmax roof at small head dims
-                    const float a0 = fmaf(__uint_as_float(x[e]), sl2, nms);
-                    const float a1 = fmaf(__uint_as_float(x[e + 1]), sl2, nms);
+                    const uint64_t a2 =
+                        ffma2(f2(__uint_as_float(x[e]), __uint_as_float(x[e + 1])), sl2x2, nms2);
                     constexpr int kPE = poly_every<DH>();
                     const bool poly = kPE > 0 && ((e >> 1) % (kPE > 0 ? kPE : 1)) == kPE - 1;
-                    const float p0 = poly ? ex2_poly(a0) : ex2f(a0);
-                    const float p1 = poly ? ex2_poly(a1) : ex2f(a1);
+                    float p0, p1;
+                    if (poly) {
+                        ex2_poly2(a2, p0, p1);
+                    } else {
+                        float a0, a1;
+                        f2_split(a2, a0, a1);
+                        p0 = ex2f(a0);
+                        p1 = ex2f(a1);
+                    }
 #endif
                     if (!ones) sum += p0 + p1;
                     __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
