@@ -39,6 +39,7 @@ struct WarpSmem {
     int16_t seeds[kCap];    // per sub id: tile-local seed row
     int16_t sub[kCap];      // per row: sub id (-1 overflow, -2 queued)
     uint16_t key[kCap];     // per row
+    int16_t elig[kCap];     // step 3: eligible ids of the current pass, ascending
 };
 
 struct Args {
@@ -62,6 +63,26 @@ __device__ __forceinline__ double dist3(const double* a, const double* b) {
     const double dy = __dsub_rn(a[1], b[1]);
     const double dz = __dsub_rn(a[2], b[2]);
     return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+}
+
+// (dx^2 + dy^2) + dz^2 with the reference's roundings (no contraction):
+// dist3 = sqrt(dist2), and sqrt is monotone, so comparisons can use dist2
+// except when two squared distances are close enough to share a sqrt.
+__device__ __forceinline__ double dist2(const double* a, const double* b) {
+    const double dx = __dsub_rn(a[0], b[0]);
+    const double dy = __dsub_rn(a[1], b[1]);
+    const double dz = __dsub_rn(a[2], b[2]);
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// Is (sqrt(d2), j) lexicographically below (sqrt(b2), bj)?  Squared values
+// more than 2^-45 apart (relative) have sqrt values > 2 ulp apart, so the
+// order of d2 decides; near-ties fall back to the rounded sqrt and the id.
+__device__ __forceinline__ bool closer(double d2, int j, double b2, int bj) {
+    if (d2 < __dmul_rn(b2, 1.0 - 0x1p-45)) return true;
+    if (d2 > __dmul_rn(b2, 1.0 + 0x1p-45)) return false;
+    const double s = __dsqrt_rn(d2), bs = __dsqrt_rn(b2);
+    return s < bs || (s == bs && j < bj);
 }
 
 // lexicographic (d, id) minimum across the warp; returns the winning id
@@ -198,48 +219,71 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     nqueue = max(0, novf - need_new);
     if (novf < need_new && lane == 0) atomicOr(A.flags, 1);   // allocation fell short
     __syncwarp();
-    // ---- step 3: queued rows join the nearest under-filled sub-bucket
-    if (nqueue > 0) {
+    // ---- step 3: queued rows join the nearest under-filled sub-bucket.
+    // Speculative batches of 32 queued rows, one per lane: every lane finds
+    // its row's nearest eligible id against the sizes at the start of the
+    // pass, then the choices are committed in index order while each chosen
+    // id is still under-filled.  Eligibility only shrinks during step 3, so a
+    // choice whose id is still eligible at commit time is exactly the
+    // sequential answer (the minimum over a superset that lies in the
+    // subset); the first stale choice ends the pass and the rest of the batch
+    // is re-speculated against the updated sizes (each pass commits >= 1 row).
+    for (int q0 = 0; q0 < nqueue;) {
+        // eligible ids of this pass: under-filled new ids, else any under-filled
+        int ne = 0;
+        for (int j0 = nalloc; j0 < target; j0 += 32) {
+            const int jj = j0 + lane;
+            const bool e = jj < target && S.sizes[jj] < rho;
+            const unsigned b = __ballot_sync(0xffffffffu, e);
+            if (e) S.elig[ne + __popc(b & lt)] = (int16_t)jj;
+            ne += __popc(b);
+        }
+        if (ne == 0) {
+            for (int j0 = 0; j0 < target; j0 += 32) {
+                const int jj = j0 + lane;
+                const bool e = jj < target && S.sizes[jj] < rho;
+                const unsigned b = __ballot_sync(0xffffffffu, e);
+                if (e) S.elig[ne + __popc(b & lt)] = (int16_t)jj;
+                ne += __popc(b);
+            }
+        }
         __syncwarp();
-        for (int qi = 0; qi < nqueue; ++qi) {
-            const int i = S.qrow[qi];       // queued rows in index order (smem broadcast)
+        if (ne == 0) {                       // nothing under-filled: allocation broke
+            if (lane == 0) atomicOr(A.flags, 2);
+            break;
+        }
+        const int nb = min(32, nqueue - q0);
+        int choice = INT_MAX;
+        if (lane < nb) {
+            const int i = S.qrow[q0 + lane];
             const double ci[3] = {S.cc[i][0], S.cc[i][1], S.cc[i][2]};
-            double best = DBL_MAX;
-            int bid = INT_MAX;
-            for (int j = nalloc + lane; j < target; j += 32) {
-                if (S.sizes[j] < rho) {
-                    const double d = dist3(S.sc[j], ci);
-                    if (d < best || (d == best && j < bid)) {
-                        best = d;
-                        bid = j;
-                    }
+            double bd2 = DBL_MAX;
+            for (int e = 0; e < ne; ++e) {      // ascending ids: strict '<' keeps the lowest
+                const int jj = S.elig[e];
+                const double d2 = dist2(S.sc[jj], ci);
+                if (closer(d2, jj, bd2, choice)) {
+                    bd2 = d2;
+                    choice = jj;
                 }
             }
-            bool any_new = __any_sync(0xffffffffu, bid != INT_MAX);
-            if (!any_new) {
-                for (int j = lane; j < target; j += 32) {
-                    if (S.sizes[j] < rho) {
-                        const double d = dist3(S.sc[j], ci);
-                        if (d < best || (d == best && j < bid)) {
-                            best = d;
-                            bid = j;
-                        }
-                    }
-                }
+        }
+        int done = 0;
+        for (; done < nb; ++done) {          // commit in index order while valid
+            const int jj = __shfl_sync(0xffffffffu, choice, done);
+            if (jj == INT_MAX) {             // no finite distance (non-finite coords)
+                if (lane == 0) atomicOr(A.flags, 2);
+                done = nqueue;
+                break;
             }
-            const int j = warp_argmin(best, bid);
+            if (S.sizes[jj] >= rho) break;   // stale: re-speculate from here
             __syncwarp();
             if (lane == 0) {
-                if (j == INT_MAX) {
-                    atomicOr(A.flags, 2);
-                } else {
-                    S.sub[i] = (int16_t)j;
-                    S.sizes[j] = (int16_t)(S.sizes[j] + 1);
-                }
+                S.sub[S.qrow[q0 + done]] = (int16_t)jj;
+                S.sizes[jj] = (int16_t)(S.sizes[jj] + 1);
             }
             __syncwarp();
-            if (j == INT_MAX) break;
         }
+        q0 += done;
     }
     // ---- repair: at most one under-filled sub-bucket may remain
     for (int guard = 0; guard < kCap; ++guard) {

@@ -27,7 +27,7 @@ def test_subbuckets_golden():
 
 def test_subbuckets_random_vs_oracle():
     r = np.random.default_rng(31)
-    for i in range(150):
+    for i in range(200):
         m = int(r.integers(1, 1025))
         rho = int(r.choice((1, 2, 3, 4, 7, 8, 16)))
         scale = float(r.choice((1e-3, 1.0, 50.0)))
@@ -37,6 +37,8 @@ def test_subbuckets_random_vs_oracle():
             c[: m // 2] = piles[r.integers(0, len(piles), size=m // 2)]
         if i % 5 == 2:
             c[:, 1] = 0.25   # a degenerate axis (extent 0)
+        if i % 7 == 3:       # lattice: many exactly / nearly equal step-3 distances
+            c = r.integers(0, 6, size=(m, 3)) * 0.1 * scale
         sub = F.build_subbuckets(c, rho)
         osub, osizes, oseeds = O.subbuckets(c, rho)
         np.testing.assert_array_equal(sub.subbucket_id, osub, err_msg=f"case {i}")
