@@ -102,36 +102,6 @@ __host__ __device__ constexpr int poly_every() {
     return DH <= 32 ? F3D_POLY_SMALL : DH <= 64 ? F3D_POLY_MID : F3D_POLY_LARGE;
 }
 
-// Packed fp32 pairs (sm_100 FFMA2/FADD2/FMUL2: two lanes' worth of fp32 math
-// per issue slot; the softmax is issue-bound once the MUFU share is offloaded).
-__device__ __forceinline__ uint64_t f2(float a, float b) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void f2_split(uint64_t v, float& a, float& b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
 
 // 2^x on the FMA/ALU pipes for x <= 2^8 (softmax arguments): round x to
 // j = rint(x) with the 1.5*2^23 trick, 2^f for f in [-0.5, 0.5] by a cubic

@@ -207,6 +207,34 @@ __device__ __forceinline__ float gelu_f(float x) {
     return 0.5f * x * phi2;
 }
 
+// gelu_f on a packed pair: the same operations in the same order, with the
+// FMA/FMUL work issued as f32x2 (the bias-GELU pass is issue-bound).
+__device__ __forceinline__ float2 gelu2(float x0, float x1) {
+    const uint64_t x = f2(x0, x1);
+    const uint64_t z = fmul2(f2(fabsf(x0), fabsf(x1)), f2(0.70710678118654752f, 0.70710678118654752f));
+    float d0, d1, t0, t1;
+    f2_split(ffma2(f2(0.3275911f, 0.3275911f), z, f2(1.f, 1.f)), d0, d1);
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t0) : "f"(d0));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t1) : "f"(d1));
+    const uint64_t t = f2(t0, t1);
+    // pn = -(a1 t + ... + a5 t^5)
+    uint64_t pn = ffma2(f2(-1.061405429f, -1.061405429f), t, f2(1.453152027f, 1.453152027f));
+    pn = ffma2(pn, t, f2(-1.421413741f, -1.421413741f));
+    pn = ffma2(pn, t, f2(0.284496736f, 0.284496736f));
+    pn = ffma2(pn, t, f2(-0.254829592f, -0.254829592f));
+    pn = fmul2(pn, t);
+    float a0, a1, e0, e1;
+    f2_split(fmul2(fmul2(z, z), f2(-1.4426950408889634f, -1.4426950408889634f)), a0, a1);
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(a0));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(a1));
+    float r0, r1;   // erf(|x|/sqrt2) = 1 - pl * e^{-z^2}
+    f2_split(ffma2(pn, f2(e0, e1), f2(1.f, 1.f)), r0, r1);
+    const uint64_t phi2 = fadd2(f2(1.f, 1.f), f2(copysignf(r0, x0), copysignf(r1, x1)));
+    float o0, o1;
+    f2_split(fmul2(fmul2(f2(0.5f, 0.5f), x), phi2), o0, o1);
+    return make_float2(o0, o1);
+}
+
 // 16-byte vector form: 8 bf16 per vector (dh % 8 == 0); each thread loads
 // kU vectors before computing any (memory-level parallelism: one 16-byte load
 // in flight per thread left the kernel latency-bound).  IT = uint32_t when the
@@ -234,8 +262,10 @@ __global__ void bias_gelu8_kernel(uint4* __restrict__ u, IT n8, int dh8,
             __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w[q]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h[e]);
-                h[e] = __floats2bfloat162_rn(gelu_f(f.x + bb[2 * e]), gelu_f(f.y + bb[2 * e + 1]));
+                float2 f = __bfloat1622float2(h[e]);
+                f2_split(fadd2(f2(f.x, f.y), f2(bb[2 * e], bb[2 * e + 1])), f.x, f.y);
+                const float2 g = gelu2(f.x, f.y);
+                h[e] = __floats2bfloat162_rn(g.x, g.y);
             }
             u[t] = w[q];
         }
@@ -378,12 +408,19 @@ __global__ void __launch_bounds__(kThreads) row_ln_vec_kernel(
     // so blk = d/3 is even); bw/attention.py:271-288 on the bbox-normalised
     // coordinate (bw/stage.py:129-132)
     const int npair = d / 6, blk = 2 * npair;
-    int pa[2], pj[2];
+    // per lane: the axis and frequency of its two pairs, the axis offset and
+    // reciprocal extent (fp32 angles: the normalised coordinate is in [0, 1])
+    int pa[2];
+    float fq[2], pinv[2];
+    double plo[2];
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
         const int c = c0 + 2 * p;
         pa[p] = c / blk;
-        pj[p] = (c - pa[p] * blk) >> 1;
+        const int pj = (c - pa[p] * blk) >> 1;
+        fq[p] = exp2f(-(float)pj / (float)npair * pl2);
+        plo[p] = lo_ext ? lo_ext[pa[p]] : 0.0;
+        pinv[p] = lo_ext ? (float)(1.0 / lo_ext[3 + pa[p]]) : 1.f;
     }
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
@@ -399,10 +436,8 @@ __global__ void __launch_bounds__(kThreads) row_ln_vec_kernel(
             float sn[2], cs[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                double x = pc[i][pa[p]];
-                if (lo_ext) x = __ddiv_rn(__dsub_rn(x, lo_ext[pa[p]]), lo_ext[3 + pa[p]]);
-                const float ang = (float)x * exp2f(-(float)pj[p] / (float)npair * pl2);
-                __sincosf(ang, &sn[p], &cs[p]);
+                const float xn = (float)__dsub_rn(pc[i][pa[p]], plo[p]) * pinv[p];
+                __sincosf(xn * fq[p], &sn[p], &cs[p]);
             }
             o0 += sn[0];
             o1 += cs[0];
