@@ -288,8 +288,9 @@ int f3d_colsum(const void *x, int is_bf16, int64_t ldx, int64_t n, int d, float 
 /* Padded per-(scope, head) score tiles [B, M, M] (M % 8 == 0): T is the fp32
  * GEMM output, out the bf16 operand of the next GEMM.  mode 0: out = P =
  * exp2(T*scale_log2 - rowv[b,i]) (rowv = lse); mode 1 (T = dP, P = the mode-0
- * bf16 output): out = dS = P*(dP - rowv[b,i])*scale (rowv = D = rowsum(dO*O)).
- * Zero outside len[b] rows/keys. */
+ * bf16 output): out = dS = P*(dP - rowv[b,i])*scale (rowv = D = rowsum(dO*O)), or
+ * with rowv = NULL, D = sum_j P*dP computed per row in the kernel (the consistent,
+ * cancellation-safe form).  Zero outside len[b] rows/keys. */
 int f3d_softmax_bwd(const float *T, const void *P, const float *rowv, const int32_t *len, int B,
                     int M, double scale_log2, double scale, int mode, void *out, void *stream);
 

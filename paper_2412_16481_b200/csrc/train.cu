@@ -24,9 +24,12 @@ __device__ __forceinline__ float ld_any(const void* p, int is_bf16, int64_t i) {
                    : reinterpret_cast<const float*>(p)[i];
 }
 
-// One warp per row.  x: LN input (fp32), dy: gradient of the LN output
-// (bf16 or fp32), dres: residual gradient (nullable).  dx = dres + rstd *
-// (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)); dgain += dy*xhat, dbeta += dy.
+// One warp per row, PER columns per lane (c = lane + 32 j).  x: LN input
+// (fp32), dy: gradient of the LN output (bf16 or fp32), dres: residual
+// gradient (nullable).  dx = dres + rstd * (g*dy - mean(g*dy) - xhat *
+// mean(g*dy*xhat)); dgain += dy*xhat, dbeta += dy, accumulated per lane in
+// registers over all rows of the warp and reduced once per block.
+template <int PER>
 __global__ void __launch_bounds__(kThreads) ln_bwd_kernel(
     const float* __restrict__ x, int64_t ldx, const void* __restrict__ dy, int dy_bf16,
     int64_t ldy, const float* __restrict__ gain, const float* __restrict__ dres, int64_t ldr,
@@ -37,22 +40,29 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_kernel(
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int warps = kThreads / 32;
+    float g[PER], adg[PER], adb[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int c = lane + 32 * j;
+        g[j] = c < d ? gain[c] : 0.f;
+        adg[j] = adb[j] = 0.f;
+    }
     for (int64_t row = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); row < n;
          row += (int64_t)gridDim.x * warps) {
-        float xv[kMaxPer], gy[kMaxPer], yv[kMaxPer];
+        float xv[PER], gy[PER], yv[PER];
         float s = 0.f;
 #pragma unroll
-        for (int j = 0; j < kMaxPer; ++j) {
+        for (int j = 0; j < PER; ++j) {
             const int c = lane + 32 * j;
             xv[j] = c < d ? x[row * ldx + c] : 0.f;
             yv[j] = c < d ? ld_any(dy, dy_bf16, row * ldy + c) : 0.f;
-            gy[j] = c < d ? yv[j] * gain[c] : 0.f;
+            gy[j] = yv[j] * g[j];
             s += xv[j];
         }
         const float mean = warp_sum(s) / d;
         float q = 0.f;
 #pragma unroll
-        for (int j = 0; j < kMaxPer; ++j) {
+        for (int j = 0; j < PER; ++j) {
             const int c = lane + 32 * j;
             const float t = c < d ? xv[j] - mean : 0.f;
             q += t * t;
@@ -60,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_kernel(
         const float rstd = rsqrtf(warp_sum(q) / d + eps);
         float a = 0.f, b = 0.f;
 #pragma unroll
-        for (int j = 0; j < kMaxPer; ++j) {
+        for (int j = 0; j < PER; ++j) {
             xv[j] = (xv[j] - mean) * rstd;            // xhat
             a += gy[j];
             b += gy[j] * xv[j];
@@ -68,14 +78,22 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_kernel(
         a = warp_sum(a) / d;
         b = warp_sum(b) / d;
 #pragma unroll
-        for (int j = 0; j < kMaxPer; ++j) {
+        for (int j = 0; j < PER; ++j) {
             const int c = lane + 32 * j;
             if (c >= d) continue;
             float v = rstd * (gy[j] - a - xv[j] * b);
             if (dres) v += dres[row * ldr + c];
             dx[row * ldd + c] = v;
-            atomicAdd(&s_dg[c], yv[j] * xv[j]);
-            atomicAdd(&s_db[c], yv[j]);
+            adg[j] = fmaf(yv[j], xv[j], adg[j]);
+            adb[j] += yv[j];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int c = lane + 32 * j;
+        if (c < d) {
+            atomicAdd(&s_dg[c], adg[j]);
+            atomicAdd(&s_db[c], adb[j]);
         }
     }
     __syncthreads();
@@ -85,28 +103,47 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_kernel(
     }
 }
 
-// du = dg * GELU'(u + b), GELU'(z) = Phi(z) + z phi(z); dbias += du (columns).
+// Phi(z) = 0.5 (1 + erf(z / sqrt2)) with the forward's Abramowitz-Stegun
+// 7.1.26 erf (|err| <= 1.5e-7); phi(z) = exp(-z^2/2) / sqrt(2 pi).
+__device__ __forceinline__ float gelu_grad(float z) {
+    const float a = fabsf(z) * 0.70710678118654752f;
+    const float t = __frcp_rn(fmaf(0.3275911f, a, 1.f));
+    float pl = fmaf(1.061405429f, t, -1.453152027f);
+    pl = fmaf(pl, t, 1.421413741f);
+    pl = fmaf(pl, t, -0.284496736f);
+    pl = fmaf(pl, t, 0.254829592f);
+    const float ez = __expf(-a * a);                 // = exp(-z^2/2)
+    const float erf_a = 1.f - pl * t * ez;
+    const float Phi = 0.5f * (1.f + copysignf(erf_a, z));
+    return Phi + z * (0.3989422804014327f * ez);
+}
+
+// du = dg * GELU'(u + b); dbias += du.  Blocks stride over rows; thread t
+// owns the column pairs t, t + blockDim, ... (coalesced bf16x2 / float2 row
+// accesses, bias partials in shared memory without atomics).  h even.
 __global__ void __launch_bounds__(kThreads) gelu_bwd_kernel(
     const __nv_bfloat16* __restrict__ u, int64_t ldu, const float* __restrict__ bias,
     const float* __restrict__ dg, int64_t ldg, float* __restrict__ du, int64_t ldd,
     float* __restrict__ dbias, int64_t n, int h) {
     extern __shared__ float s_db[];
-    for (int c = threadIdx.x; c < h; c += kThreads) s_db[c] = 0.f;
-    __syncthreads();
-    const int64_t tot = n * h;
-    for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < tot;
-         t += (int64_t)gridDim.x * kThreads) {
-        const int64_t r = t / h;
-        const int c = (int)(t - r * h);
-        const float z = __bfloat162float(u[r * ldu + c]) + bias[c];
-        const float phi = 0.3989422804014327f * __expf(-0.5f * z * z);
-        const float Phi = 0.5f * (1.f + erff(z * 0.70710678118654752f));
-        const float v = dg[r * ldg + c] * (Phi + z * phi);
-        du[r * ldd + c] = v;
-        atomicAdd(&s_db[c], v);
+    const int h2 = h / 2;
+    for (int c = threadIdx.x; c < h2; c += blockDim.x) s_db[2 * c] = s_db[2 * c + 1] = 0.f;
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        for (int c = threadIdx.x; c < h2; c += blockDim.x) {
+            const float2 uu = __bfloat1622float2(
+                reinterpret_cast<const __nv_bfloat162*>(u + r * ldu)[c]);
+            const float2 bb = reinterpret_cast<const float2*>(bias)[c];
+            const float2 gg = reinterpret_cast<const float2*>(dg + r * ldg)[c];
+            float2 v;
+            v.x = gg.x * gelu_grad(uu.x + bb.x);
+            v.y = gg.y * gelu_grad(uu.y + bb.y);
+            reinterpret_cast<float2*>(du + r * ldd)[c] = v;
+            s_db[2 * c] += v.x;
+            s_db[2 * c + 1] += v.y;
+        }
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < h; c += kThreads) atomicAdd(dbias + c, s_db[c]);
+    for (int c = threadIdx.x; c < h; c += blockDim.x) atomicAdd(dbias + c, s_db[c]);
 }
 
 // out[c] += sum_r x[r, c]  (x bf16 or fp32)
@@ -175,6 +212,62 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(
     }
 }
 
+// mode 1 with D computed in-kernel: one warp per (b, i) row, D = sum_j P dP
+// over the same bf16 P the product uses (so sum_j dS = 0 in this arithmetic:
+// the stable choice when dP - D cancels), then dS = P (dP - D) * scale.
+__global__ void __launch_bounds__(kThreads) softmax_bwd_rows_kernel(
+    const float* __restrict__ T, const __nv_bfloat16* __restrict__ P,
+    const int32_t* __restrict__ len, int B, int M, float scale, __nv_bfloat16* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = (int64_t)B * M;
+    for (int64_t bi = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; bi < rows;
+         bi += ((int64_t)gridDim.x * kThreads) >> 5) {
+        const int b = (int)(bi / M);
+        const int i = (int)(bi - (int64_t)b * M);
+        const int m = len[b];
+        const float* tr = T + bi * M;
+        const __nv_bfloat16* pr = P + bi * M;
+        uint4* orow = reinterpret_cast<uint4*>(out + bi * M);
+        float acc = 0.f;
+        if (i < m) {
+            for (int j0 = lane * 8; j0 < m; j0 += 256) {
+                const uint4 pp = *reinterpret_cast<const uint4*>(pr + j0);
+                const float4 a = *reinterpret_cast<const float4*>(tr + j0);
+                const float4 c = *reinterpret_cast<const float4*>(tr + j0 + 4);
+                const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+                const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pp);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(ph[e]);
+                    if (j0 + 2 * e < m) acc = fmaf(f.x, v[2 * e], acc);
+                    if (j0 + 2 * e + 1 < m) acc = fmaf(f.y, v[2 * e + 1], acc);
+                }
+            }
+        }
+        const float D = warp_sum(acc);
+        for (int j0 = lane * 8; j0 < M; j0 += 256) {
+            uint4 o = make_uint4(0, 0, 0, 0);
+            if (i < m && j0 < m) {
+                const uint4 pp = *reinterpret_cast<const uint4*>(pr + j0);
+                const float4 a = *reinterpret_cast<const float4*>(tr + j0);
+                const float4 c = *reinterpret_cast<const float4*>(tr + j0 + 4);
+                const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+                const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pp);
+                __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(ph[e]);
+                    float x0 = f.x * (v[2 * e] - D) * scale, x1 = f.y * (v[2 * e + 1] - D) * scale;
+                    if (j0 + 2 * e >= m) x0 = 0.f;
+                    if (j0 + 2 * e + 1 >= m) x1 = 0.f;
+                    oh[e] = __floats2bfloat162_rn(x0, x1);
+                }
+            }
+            orow[j0 / 8] = o;
+        }
+    }
+}
+
 }  // namespace train
 }  // namespace f3d
 
@@ -193,9 +286,20 @@ extern "C" int f3d_ln_bwd(const float* x, int64_t ldx, const void* dy, int dy_bf
                           void* stream) {
     if (n < 0 || d < 1 || d > 32 * train::kMaxPer) return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
-    train::ln_bwd_kernel<<<grid_cap(n * 32, train::kThreads), train::kThreads, 0,
-                           (cudaStream_t)stream>>>(x, ldx, dy, dy_bf16, ldy, gain, dres, ldr, dx,
-                                                   ldd, dgain, dbeta, n, d, (float)eps);
+    const int per = (d + 31) / 32;
+    const unsigned grid = grid_cap(n * 32, train::kThreads, 4);
+    cudaStream_t st = (cudaStream_t)stream;
+#define F3D_LNB(P)                                                                             \
+    train::ln_bwd_kernel<P><<<grid, train::kThreads, 0, st>>>(x, ldx, dy, dy_bf16, ldy, gain,  \
+                                                              dres, ldr, dx, ldd, dgain, dbeta, \
+                                                              n, d, (float)eps)
+    if (per <= 1) F3D_LNB(1);
+    else if (per <= 2) F3D_LNB(2);
+    else if (per <= 3) F3D_LNB(3);
+    else if (per <= 4) F3D_LNB(4);
+    else if (per <= 8) F3D_LNB(8);
+    else F3D_LNB(16);
+#undef F3D_LNB
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
@@ -203,9 +307,12 @@ extern "C" int f3d_ln_bwd(const float* x, int64_t ldx, const void* dy, int dy_bf
 extern "C" int f3d_gelu_bwd(const void* u_bf16, int64_t ldu, const float* bias, const float* dg,
                             int64_t ldg, float* du, int64_t ldd, float* dbias, int64_t n, int h,
                             void* stream) {
-    if (n < 0 || h < 1 || h > 8192) return F3D_ERR_CONFIG;
+    if (n < 0 || h < 2 || h % 2 || h > 8192 || ldu % 2 || ldg % 2 || ldd % 2)
+        return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
-    train::gelu_bwd_kernel<<<grid_cap(n * h, train::kThreads), train::kThreads, h * sizeof(float),
+    // one column pair per thread when h/2 <= 256 (h = 384: 192 threads)
+    const int threads = std::min(train::kThreads, ((h / 2 + 31) / 32) * 32);
+    train::gelu_bwd_kernel<<<grid_cap(n, 1, 8), threads, h * sizeof(float),
                              (cudaStream_t)stream>>>((const __nv_bfloat16*)u_bf16, ldu, bias, dg,
                                                      ldg, du, ldd, dbias, n, h);
     F3D_LAUNCH_CHECK();
@@ -229,6 +336,13 @@ extern "C" int f3d_softmax_bwd(const float* T, const void* P, const float* rowv,
     if (B < 0 || M < 8 || M % 8 || mode < 0 || mode > 1 || (mode == 1 && !P))
         return F3D_ERR_CONFIG;
     if (B == 0) return F3D_OK;
+    if (mode == 1 && !rowv) {
+        train::softmax_bwd_rows_kernel<<<grid_cap((int64_t)B * M * 32, train::kThreads, 16),
+                                         train::kThreads, 0, (cudaStream_t)stream>>>(
+            T, (const __nv_bfloat16*)P, len, B, M, (float)scale, (__nv_bfloat16*)out);
+        F3D_LAUNCH_CHECK();
+        return F3D_OK;
+    }
     train::softmax_bwd_kernel<<<grid_cap((int64_t)B * M * M / 8, train::kThreads, 16),
                                 train::kThreads, 0, (cudaStream_t)stream>>>(
         T, (const __nv_bfloat16*)P, rowv, len, B, M, (float)scale_log2, (float)scale, mode,

@@ -12,7 +12,8 @@ Per round, in reverse (F_in -> F_mid -> F_out):
     attention bwd -> dq, dk, dv on padded per-(scope, head) tiles:
                      P = exp2(S*sl2 - lse) from the forward kernel's LSE
                      (f3d_softmax_bwd mode 0), dV = P^T dO, dP = dO V^T,
-                     dS = P (dP - D) / sqrt(dh) (mode 1), dQ = dS K, dK = dS^T Q
+                     dS = P (dP - D) / sqrt(dh) with D = sum_j P dP per row
+                     (mode 1), dQ = dS K, dK = dS^T Q
                   -> db_qkv = colsum, dW_qkv = x1^T dqkv, dx1 = dqkv W_qkv^T
     f3d_ln_bwd    -> dF_in = dF_mid + LN1'(F_in) dx1 (and dln1)
 
@@ -64,13 +65,28 @@ def scope_index(plan, n: int):
 
 
 class _RoundIndex:
+    """Per-(scope, head) gather/scatter indices of one round over the
+    (n*H, dh) head-row view: bh[b*M + i] = row(scope b//H, i)*H + b%H.  Pad
+    entries (i >= len) point at row 0 — their scores are zeroed by
+    f3d_softmax_bwd, so they never reach a gradient — and are dropped on the
+    scatter back."""
+
     def __init__(self, plan, n, H, dev):
         idx, lens = scope_index(plan, n)
         self.ns, self.M = idx.shape
-        self.idx = torch.from_numpy(idx).to(dev)
-        self.flat = self.idx.reshape(-1)
-        self.valid = self.flat < n
-        self.rows = self.flat[self.valid]
+        valid = idx < n
+        idx = np.where(valid, idx, 0)
+        bh = (idx[:, None, :] * H + np.arange(H)[None, :, None]).reshape(-1)
+        vbh = np.broadcast_to(valid[:, None, :], (self.ns, H, self.M)).reshape(-1)
+        self.bh = torch.from_numpy(bh).to(dev)
+        self.bh32 = self.bh.to(torch.int32)
+        if int(vbh.sum()) != n * H:
+            raise ConfigError("the round's scopes do not cover every row exactly once")
+        # scatter targets into the (n, 3, H, dh) = (n, 3d) dq|dk|dv layout;
+        # pads land on the dummy head row n*3H
+        r, h = bh // H, bh % H
+        self.dest = [torch.from_numpy(np.where(vbh, r * 3 * H + i * H + h, n * 3 * H)
+                                      .astype(np.int32)).to(dev) for i in range(3)]
         self.len_bh = torch.from_numpy(np.repeat(lens, H)).to(dev)      # b = scope*H + h
 
 
@@ -171,18 +187,16 @@ class StageTrainer:
         ns, M, B = ix.ns, ix.M, ix.ns * H
         bf = torch.bfloat16
 
-        def tiles(x):               # (n, d) bf16 rows -> (B, M, dh), zero pad row
-            xp = torch.cat([x, x.new_zeros((1, d))])
-            return xp[ix.idx].view(ns, M, H, dh).permute(0, 2, 1, 3).reshape(B, M, dh)
+        def gather(src):            # src (n*H, w) head rows -> (B*M, w), f3d_gather_rows
+            t = torch.empty((B * M, src.shape[1]), dtype=src.dtype, device=src.device)
+            L.call("f3d_gather_rows", L.ptr(src), L.ptr(ix.bh32), B * M,
+                   src.shape[1] * src.element_size(), L.ptr(t), None, L.stream())
+            return t
 
-        def row_tiles(r):           # (n, H) fp32 -> (B, M)
-            rp = torch.cat([r, r.new_zeros((1, H))])[ix.idx]
-            return rp.permute(0, 2, 1).reshape(B, M).contiguous()
-
-        Q, K, V = (tiles(qkv[:, i * d:(i + 1) * d]) for i in range(3))
-        dO = tiles(da.to(bf))
-        Dv = row_tiles((da.view(n, H, dh) * a.view(n, H, dh).float()).sum(-1))
-        lse_b = row_tiles(lse)
+        Q, K, V = (gather(qkv[:, i * d:(i + 1) * d].contiguous().view(n * H, dh)).view(B, M, dh)
+                   for i in range(3))
+        dO = gather(da.to(bf).view(n * H, dh)).view(B, M, dh)
+        lse_b = gather(lse.reshape(n * H, 1)).view(B, M)
         sl2 = 1.4426950408889634 / math.sqrt(dh)
         S = torch.bmm(Q, K.transpose(1, 2), out_dtype=torch.float32)
         P = torch.empty((B, M, M), dtype=bf, device=qkv.device)
@@ -192,15 +206,17 @@ class StageTrainer:
         dV = torch.bmm(P.transpose(1, 2), dO, out_dtype=torch.float32)
         dP = torch.bmm(dO, V.transpose(1, 2), out_dtype=torch.float32)
         dS = torch.empty_like(P)
-        L.call("f3d_softmax_bwd", L.ptr(dP), L.ptr(P), L.ptr(Dv), L.ptr(ix.len_bh), B, M, sl2,
+        # D = sum_j P dP per row inside the kernel (same bf16 P as dS uses)
+        L.call("f3d_softmax_bwd", L.ptr(dP), L.ptr(P), None, L.ptr(ix.len_bh), B, M, sl2,
                1.0 / math.sqrt(dh), 1, L.ptr(dS), L.stream())
         del dP, P
         dQ = torch.bmm(dS, K, out_dtype=torch.float32)
         dK = torch.bmm(dS.transpose(1, 2), Q, out_dtype=torch.float32)
-        out = torch.empty((n, 3 * d), dtype=torch.float32, device=qkv.device)
+        out = torch.empty((n * 3 * H + 1, dh), dtype=torch.float32, device=qkv.device)
         for i, t in enumerate((dQ, dK, dV)):
-            rows = t.view(ns, H, M, dh).permute(0, 2, 1, 3).reshape(ns * M, d)[ix.valid]
-            out[:, i * d:(i + 1) * d].index_copy_(0, ix.rows, rows)
+            L.call("f3d_scatter_rows", L.ptr(t), L.ptr(ix.dest[i]), B * M, dh * 4, L.ptr(out),
+                   None, L.stream())
+        out = out[:n * 3 * H].view(n, 3 * d)
         return out
 
     def _ln_bwd(self, x, dy, gain, dres, dgain, dbeta):
@@ -306,3 +322,90 @@ def sgd_step(params: StageParams, grads, lr: float):
             cur.sub_(lr * g.to(cur.device, cur.dtype))
         else:
             cur -= lr * g.double().cpu().numpy()
+
+
+class BackboneTrainer:
+    """Training step of the multi-stage backbone (config E uses the B recipe:
+    stage 0 -> mean pool (rho) -> re-bucketed stage 1 ...).
+    The layout of every stage depends on the coordinates only, so the PSH
+    bucketing, scatter maps, pooling partition and scope plans are built once
+    per scene here (exactly as Backbone.forward builds them); forward/backward
+    then run the stage trainers with the pooling as a fixed linear map:
+
+        pool:    X_{s+1}[p] = mean_{i: parent[i] = p} F_s[i]   (f3d_pool_reduce,
+                 members in index order as in the inference path)
+        unpool:  dF_s[i] = dX_{s+1}[parent[i]] / size[parent[i]]
+
+    ``stages`` are backbone.StageConfig; ``weights`` one DeviceWeights per stage."""
+
+    def __init__(self, coords, stages, params, weights=None):
+        from .backbone import Backbone
+        from .pooling import TilePlan, _build
+        from .attention import build_schedule
+        dev = L.device()
+        self.stages = tuple(stages)
+        self.params = list(params)
+        self.weights = list(weights) if weights is not None else [DeviceWeights(p) for p in params]
+        C = L.to_dev(coords, torch.float64).contiguous()
+        bb = Backbone(self.stages)
+        self.levels = []
+        for si, cfg in enumerate(self.stages):
+            n = C.shape[0]
+            asg, _, _ = bb.bucketize(C, cfg)
+            dest = asg._dev["dest"].to(torch.int64)
+            table = asg.bucket_table(split_recycle=True)
+            sched = build_schedule(len(table[0]), cfg.W, cfg.stride, cfg.shift, cfg.rounds)
+            Cs = torch.empty_like(C)
+            Cs[dest] = C
+            lvl = {"n": n, "dest": dest, "table": table, "schedule": sched, "coords": Cs,
+                   "trainer": StageTrainer(Cs, table, sched, self.params[si], n,
+                                           weights=self.weights[si])}
+            if cfg.pool_rho:
+                m = asg._mirrors()
+                counts = m["counts"].cpu().numpy().astype(np.int64)
+                base = m["base"].cpu().numpy().astype(np.int64)
+                plan = TilePlan(counts, base, cfg.pool_rho, dev)
+                members, sizes, _, _, _, flags = _build(Cs, plan, cfg.pool_rho)
+                if int(flags.item()):
+                    raise ConfigError(f"pooling partition failed (flags {int(flags.item())})")
+                parent = L.empty((max(1, n),), torch.int32)
+                L.call("f3d_pool_parent", L.ptr(members), L.ptr(sizes), plan.npool,
+                       cfg.pool_rho, L.ptr(parent), None, L.stream())
+                parent = parent[:n].to(torch.int64)
+                lvl.update(members=members, sizes=sizes, npool=plan.npool, rho=cfg.pool_rho,
+                           parent=parent,
+                           inv_size=(1.0 / sizes[:plan.npool].to(torch.float32))[parent, None])
+                C = self._pool(Cs, lvl)                    # centroids feed the next stage
+            self.levels.append(lvl)
+
+    @staticmethod
+    def _pool(x, lvl):
+        from .pooling import _reduce
+        return _reduce(x, lvl["members"], lvl["sizes"], lvl["npool"], lvl["rho"], "mean")
+
+    def forward(self, X: torch.Tensor) -> torch.Tensor:
+        """X: (n0, d) fp32 features in the caller's (unscattered) row order.
+        Returns the last stage's output rows in that stage's scattered order."""
+        for lvl in self.levels:
+            Xs = torch.empty_like(X)
+            Xs[lvl["dest"]] = X
+            out = lvl["trainer"].forward(Xs)
+            X = self._pool(out, lvl) if "parent" in lvl else out
+        return X
+
+    def backward(self, dout: torch.Tensor):
+        """dout: gradient w.r.t. forward()'s output.  Returns (dX in the
+        caller's row order, [grads of stage 0, grads of stage 1, ...])."""
+        grads = [None] * len(self.levels)
+        d = dout
+        for si in reversed(range(len(self.levels))):
+            lvl = self.levels[si]
+            if "parent" in lvl:                            # through the mean pool
+                d = d[lvl["parent"]] * lvl["inv_size"]
+            d, grads[si] = lvl["trainer"].backward(d)
+            d = d[lvl["dest"]]                             # back through the scatter
+        return d, grads
+
+    def sgd(self, grads, lr: float):
+        for w, g in zip(self.weights, grads):
+            w.sgd(g, lr)

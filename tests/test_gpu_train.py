@@ -113,3 +113,71 @@ def test_device_weights_sync_matches_host_cast():
     dw.sync()
     for k, v in ref.items():
         assert torch.equal(dw.w[k], v), k
+
+
+# ----------------------------------------------------------- two-stage backbone
+
+def _backbone_instance(n=4000, d=48, H=2):
+    from paper_2412_16481_b200.backbone import StageConfig
+    stages = (StageConfig(K=40, S=128, S_div=6554, W=2, d_model=d, n_heads=H, pool_rho=2, seed=0),
+              StageConfig(K=20, S=128, S_div=13108, W=2, d_model=d, n_heads=H, pool_rho=0, seed=1))
+    coords = O.synth_cloud(11, n, "uniform-box")
+    feats = np.random.default_rng(2).normal(size=(n, d))
+    params = [F.init_params(s.seed, d, n_heads=H) for s in stages]
+    return stages, coords, feats, params
+
+
+def test_backbone_trainer_forward_matches_inference():
+    from paper_2412_16481_b200.backbone import Backbone
+    from paper_2412_16481_b200.train import BackboneTrainer
+    stages, coords, feats, params = _backbone_instance()
+    C = torch.tensor(coords, device="cuda")
+    X = torch.tensor(feats, dtype=torch.float32, device="cuda")
+    out = BackboneTrainer(C, stages, params).forward(X)
+    ref, _ = Backbone(stages).forward(C, X)
+    assert out.shape == ref.shape
+    assert rel(out.cpu().numpy(), ref.float().cpu().numpy()) < 1e-5
+
+
+def test_backbone_gradients_vs_autograd():
+    """Two stages with the mean pool between them: gradients of every stage's
+    parameters and of the input features against float64 autograd of the
+    torch restatement run on the same layout (PSH / pooling partitions are
+    integer maps already pinned bit-exact by the PSH and pooling tests)."""
+    from paper_2412_16481_b200.train import BackboneTrainer
+    stages, coords, feats, params = _backbone_instance()
+    C = torch.tensor(coords, device="cuda")
+    X = torch.tensor(feats, dtype=torch.float32, device="cuda")
+    bt = BackboneTrainer(C, stages, params)
+    out = bt.forward(X)
+    dout = np.random.default_rng(4).normal(size=tuple(out.shape))
+    dx, grads = bt.backward(torch.tensor(dout, dtype=torch.float32, device="cuda"))
+
+    H = stages[0].n_heads
+    Xt = torch.tensor(feats, requires_grad=True)
+    tps, h = [], Xt
+    for lvl, p in zip(bt.levels, params):
+        tp = T.params_to_torch({k: getattr(p, k) for k in T.PARAM_NAMES})
+        tps.append(tp)
+        dest = lvl["dest"].cpu().numpy()
+        hs = h[np.argsort(dest)]                        # scatter: row i -> dest[i]
+        rows = T.scope_rows(lvl["table"], lvl["schedule"].rounds)
+        o = T.stage_forward(hs, lvl["coords"].cpu().numpy(), rows, tp, H)
+        if "parent" in lvl:
+            par = torch.as_tensor(lvl["parent"].cpu().numpy())
+            cnt = torch.bincount(par, minlength=lvl["npool"]).to(torch.float64)
+            h = torch.zeros((lvl["npool"], o.shape[1]), dtype=torch.float64).index_add(0, par, o)
+            h = h / cnt[:, None]
+        else:
+            h = o
+    assert rel(out.cpu().numpy(), h.detach().numpy()) < STAGE_TOL
+    (h * torch.tensor(dout)).sum().backward()
+    errs = {"input": rel(dx.cpu().numpy(), Xt.grad.numpy())}
+    for si, (g, tp) in enumerate(zip(grads, tps)):
+        for k in GRAD_NAMES:
+            if k == "b_k":
+                continue
+            errs[f"s{si}.{k}"] = rel(g[k].cpu().numpy(), tp[k].grad.numpy())
+    print(errs)
+    bad = {k: v for k, v in errs.items() if not v < TRAIN_TOL}
+    assert not bad, errs

@@ -1,16 +1,19 @@
-"""Training-step throughput of one bucket-swin stage (SURVEY.md §8(d) config E:
-B recipe scenes, 64 x 100K over 8 GPUs = 8 scenes per GPU).
+"""Training-step throughput (B recipe scenes, 64 x 100K
+over 8 GPUs = 8 scenes per GPU) of the 2-stage config-B backbone
+(stage 0 -> mean pool rho=2 -> re-bucketed stage 1), or of stage 0 alone
+with --stage0-only.
 
     python tools/train_bench.py [--scenes 8] [--steps 3]
     torchrun --nproc-per-node N tools/train_bench.py   # scenes per rank fixed (weak)
 
-Per rank: scenes synth_cloud(7 + 64*rank/8 + s, 100K) bucketed on the GPU with
-the config-B stage-0 recipe (voxel 1/64, K=256 S=512 S_div=1024, W=2, 2 rounds,
-C=96 H=4), scattered once (setup, untimed).  One timed step = for every scene
-forward with saved activations + loss 0.5*mean(out^2) + backward, gradients
-summed over the scenes, one flat NCCL all_reduce(SUM)/world, SGD on the
-device fp32 masters with the bf16 operands re-cast in place.  CUDA-event time,
-max over ranks.
+Per rank: scenes synth_cloud(7 + 8*rank + s, 100K) with the config-B recipe
+(stage 0: voxel 1/64, K=256 S=512 S_div=1024, W=2, 2 rounds, C=96 H=4, pool
+rho=2; stage 1: K=128 S=512 S_div=2048); per-scene layouts (PSH, scatter maps,
+pooling partition, scope plans) are built once (setup, untimed).  One timed
+step = for every scene forward with saved activations + loss 0.5*mean(out^2) +
+backward, gradients summed over the scenes, one flat NCCL all_reduce(SUM)/world
+per stage, SGD on the device fp32 masters with the bf16 operands re-cast in
+place.  CUDA-event time, max over ranks.
 """
 import argparse
 import json
@@ -24,9 +27,9 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_2412_16481_b200 as F  # noqa: E402
-from paper_2412_16481_b200.backbone import Backbone, StageConfig  # noqa: E402
-from paper_2412_16481_b200.train import (DeviceWeights, StageTrainer, accumulate_grads,  # noqa: E402
-                                         allreduce_grads)
+from paper_2412_16481_b200.backbone import StageConfig, scannet_backbone  # noqa: E402
+from paper_2412_16481_b200.train import (BackboneTrainer, DeviceWeights,  # noqa: E402
+                                         accumulate_grads, allreduce_grads)
 
 
 def main():
@@ -36,6 +39,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--profile", action="store_true", help="print the top kernels of one step")
+    ap.add_argument("--stage0-only", action="store_true")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -43,33 +47,30 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = StageConfig(K=256, S=512, S_div=1024, W=2, d_model=96, pool_rho=0)
-    bb = Backbone((cfg,))
-    p = F.init_params(0, 96, n_heads=4)
-    wts = DeviceWeights(p)
+    if a.stage0_only:
+        stages = (StageConfig(K=256, S=512, S_div=1024, W=2, d_model=96, pool_rho=0),)
+    else:
+        stages = scannet_backbone()
+    params = [F.init_params(s.seed, s.d_model, n_heads=s.n_heads) for s in stages]
+    wts = [DeviceWeights(p) for p in params]
     trainers, feats = [], []
     for s in range(a.scenes):
         seed = 7 + rank * a.scenes + s
         C = torch.tensor(F.synth_cloud(seed, a.points, "uniform-box").coords, device="cuda")
-        asg, _, _ = bb.bucketize(C, cfg)
-        table = asg.bucket_table(split_recycle=True)
-        sched = F.build_schedule(len(table[0]), cfg.W, cfg.stride, cfg.shift, cfg.rounds)
         X = torch.tensor(np.random.default_rng(seed).normal(size=(a.points, 96)),
                          dtype=torch.float32, device="cuda")
-        Xs = F.scatter(X, asg)[0].contiguous()
-        Cs = F.scatter(C, asg)[0].contiguous()
-        trainers.append(StageTrainer(Cs, table, sched, p, a.points, weights=wts))
-        feats.append(Xs)
+        trainers.append(BackboneTrainer(C, stages, params, weights=wts))
+        feats.append(X)
 
     def step():
-        acc, loss = None, 0.0
+        acc, loss = [None] * len(stages), 0.0
         for tr, X in zip(trainers, feats):
             out = tr.forward(X)
             loss = loss + 0.5 * (out * out).mean()
-            _, g = tr.backward(out / out.numel())
-            acc = accumulate_grads(acc, g)
-        acc = allreduce_grads(acc)
-        wts.sgd(acc, 1e-3)
+            _, gs = tr.backward(out / out.numel())
+            acc = [accumulate_grads(x, g) for x, g in zip(acc, gs)]
+        for w, g in zip(wts, acc):
+            w.sgd(allreduce_grads(g), 1e-3)
         return loss
 
     for _ in range(a.warmup):
@@ -94,7 +95,9 @@ def main():
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     if rank == 0:
         pts = a.scenes * a.points * world
-        print(json.dumps({"workload": "config E (stage-0 of the B recipe), fwd+bwd+allreduce+SGD",
+        print(json.dumps({"workload": ("config E, stage 0 only" if a.stage0_only else
+                                       "config E, 2-stage B-recipe backbone") +
+                                      ": fwd+bwd+allreduce+SGD",
                           "n_gpus": world, "scenes_per_gpu": a.scenes, "points_per_scene": a.points,
                           "ms_per_step": round(float(ms.item()), 3),
                           "train_points_per_s": pts / (float(ms.item()) * 1e-3),
