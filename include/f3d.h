@@ -271,6 +271,15 @@ int f3d_pool_reduce(const void *x, int dtype, int64_t ldx, int d, const int32_t 
                     const int32_t *sizes, int64_t npool, int rho, int op, void *out,
                     int64_t ldo, const int32_t *npool_dev, void *stream);
 
+/* u = GELU(x W_in + b_in) as bf16 rows (n x 4d): tcgen05 GEMM with the
+ * bias + exact-erf GELU epilogue read from TMEM (replaces a library GEMM +
+ * f3d_bias_gelu; bw/stage.py:153-156).  w_in_t = W_in^T (4d x d, row-major
+ * bf16).  d in {64, 96} (f3d_gemm_gelu_supported).  n_dev (nullable): device
+ * row count <= n (graph capture with a capacity n). */
+int f3d_gemm_gelu_supported(int d);
+int f3d_gemm_gelu(const void *x, int64_t ldx, int64_t n, int d, const void *w_in_t,
+                  const float *b_in, void *u, int64_t ldu, const int32_t *n_dev, void *stream);
+
 /* ------------------------------------------------ training
  * LayerNorm backward fused with the residual add: dx = dres + rstd*(g*dy -
  * mean(g*dy) - xhat*mean(g*dy*xhat)); dgain += sum dy*xhat, dbeta += sum dy

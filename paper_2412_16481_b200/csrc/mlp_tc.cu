@@ -405,6 +405,224 @@ int launch(const Args& A, cudaStream_t st) {
     return F3D_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// u = GELU(x W_in + b_in) -> bf16 rows (the MLP's first half, bw/stage.py:91-92,
+// 153-156), replacing cuBLAS GEMM + f3d_bias_gelu: the fp32 products never
+// leave TMEM and u is written once.  One persistent CTA per SM:
+//   * warp 0 loads x tiles (cp.async, 3 buffers); warp 1 (elected lane)
+//     issues D[:, q*QP, +QP) = X W_in^T[q*QP, +QP)^T for the four column
+//     quarters q into TMEM (4 x QP = 4d <= 512 columns);
+//   * warpgroups 1-4 own one quarter each: tcgen05.ld 32 columns (the next
+//     chunk's load in flight while the current one is processed), + b_in,
+//     packed-pair GELU, bf16, 16-byte stores of the row; the quarter's TMEM is
+//     released after its last load, so the next tile's MMA overlaps the tail.
+namespace gg {
+#ifndef F3D_GG_PARTS
+#define F3D_GG_PARTS 4
+#endif
+constexpr int kQ = F3D_GG_PARTS;               // column parts = epilogue warpgroups
+constexpr int kThreads = (1 + kQ) * 128;
+constexpr int kNX = 2;                         // x tile buffers
+
+template <int D>
+struct Cfg {
+    static constexpr int H = 4 * D;
+    static constexpr int QP = H / kQ;          // = D columns per quarter
+    static constexpr int kWBytes = H * D * 2;
+    static constexpr int kXBytes = kBM * D * 2;
+    static constexpr int kOffW = 0;
+    static constexpr int kOffX = kOffW + kWBytes;
+    // per-part output staging: 128 rows x QP bf16, row stride padded by 16 B
+    // (conflict-free 16-byte row writes), copied out with coalesced stores
+    static constexpr int kStStride = QP * 2 + 16;
+    static constexpr int kOffSt = kOffX + kNX * kXBytes;
+    static constexpr int kOffBias = kOffSt + kQ * kBM * kStStride;
+    static constexpr int kOffBar = kOffBias + H * 4;
+    static constexpr int kNumBars = 2 * kNX + 2 * kQ;   // x_full, x_empty, d_full, d_empty
+    static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
+    static_assert(QP % 16 == 0 && QP * kQ == H && QP <= 256 && H <= 512,
+                  "parts: 16-column chunks, MMA N");
+    static_assert(kSmem <= 227 * 1024, "smem budget");
+};
+
+struct Args {
+    const __nv_bfloat16* x;
+    int64_t ldx;
+    int64_t n;
+    const int32_t* n_dev;
+    const __nv_bfloat16* w_in_t;    // (4d, d) = W_in^T
+    const float* b_in;
+    __nv_bfloat16* u;               // (n, 4d) out
+    int64_t ldu;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) gemm_gelu_kernel(const Args A) {
+    using C = Cfg<D>;
+    constexpr int H = C::H, QP = C::QP;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+    uint64_t* x_full = bars;
+    uint64_t* x_empty = bars + kNX;
+    uint64_t* d_full = bars + 2 * kNX;
+    uint64_t* d_empty = d_full + kQ;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+    float* s_b = reinterpret_cast<float*>(smem + C::kOffBias);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t n = dyn_n(A.n, A.n_dev);
+    const int ntiles = (int)((n + kBM - 1) / kBM);
+
+    for (int i = tid; i < H * (D / 8); i += kThreads) {
+        const int r = i / (D / 8), c = i - r * (D / 8);
+        *reinterpret_cast<uint4*>(smem + C::kOffW + core_off<D>(r, c)) =
+            __ldg(reinterpret_cast<const uint4*>(A.w_in_t + (int64_t)r * D) + c);
+    }
+    for (int i = tid; i < H; i += kThreads) s_b[i] = A.b_in[i];
+    if (tid == 0) {
+        for (int b = 0; b < kNX; ++b) {
+            mbar_init(x_full + b, 32);
+            mbar_init(x_empty + b, 1);
+        }
+        for (int q = 0; q < kQ; ++q) {
+            mbar_init(d_full + q, 1);
+            mbar_init(d_empty + q, 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_base = saddr(smem);
+
+    if (warp == 0) {
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int b = it % kNX;
+            mbar_wait(x_empty + b, ((it / kNX) & 1) ^ 1);
+            const uint32_t dst = sm_base + C::kOffX + b * C::kXBytes;
+            const int64_t r0 = (int64_t)tile * kBM;
+            for (int i = lane; i < kBM * (D / 8); i += 32) {
+                const int r = i / (D / 8), c = i - r * (D / 8);
+                const bool ok = r0 + r < n;
+                const __nv_bfloat16* src = ok ? A.x + (r0 + r) * A.ldx + c * 8 : A.x;
+                cp_async16z(dst + core_off<D>(r, c), src, ok);
+            }
+            cp_async_arrive(x_full + b);
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id = idesc_bf16(kBM, QP, 0, 0);
+        const uint64_t dW = smem_desc(sm_base + C::kOffW, 128, 16 * D);
+        const uint64_t dX = smem_desc(sm_base + C::kOffX, 128, 16 * D);
+        constexpr uint32_t kXD = C::kXBytes >> 4;
+        constexpr uint32_t kQD = ((QP / 8) * 16 * D) >> 4;   // W_in^T rows [q*QP, ...)
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int b = it % kNX;
+            mbar_wait(x_full + b, (it / kNX) & 1);
+            tc_fence_after();
+            const uint64_t dx = dX + (uint64_t)(b * kXD);
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                if (it > 0) mbar_wait(d_empty + q, (it - 1) & 1);   // quarter q of tile it-1 read
+                tc_fence_after();
+                if (elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < D / 16; ++k)
+                        umma_f16(tmem + q * QP, dx + (uint64_t)(16 * k),
+                                 dW + (uint64_t)(q * kQD + 16 * k), id, k > 0);
+                    umma_commit(d_full + q);
+                }
+                __syncwarp();
+            }
+            if (elect_one()) umma_commit(x_empty + b);
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        const int q = (warp >> 2) - 1;                      // column quarter of this WG
+        const int r = (warp & 3) * 32 + lane;               // row in tile = TMEM lane
+        const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t c0 = tmem + lb + q * QP;
+        const float* bq = s_b + q * QP;
+        unsigned char* stage = smem + C::kOffSt + q * kBM * C::kStStride;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            mbar_wait(d_full + q, it & 1);
+            tc_fence_after();
+            const int64_t r0 = (int64_t)tile * kBM;
+            unsigned char* strow = stage + r * C::kStStride;
+            constexpr int CW = 16;                          // columns per TMEM load
+            uint32_t v[CW], nv[CW];
+            tmem_ld16(c0, v);
+            tmem_wait_ld();
+#pragma unroll 1
+            for (int cc = 0; cc < QP; cc += CW) {
+                const bool more = cc + CW < QP;
+                if (more) tmem_ld16(c0 + cc + CW, nv);      // next chunk in flight
+                else {
+                    tc_fence_before();
+                    mbar_arrive(d_empty + q);               // part fully read
+                }
+                uint32_t pk[CW / 2];
+#pragma unroll
+                for (int e = 0; e < CW; e += 2) {
+                    const float2 bb = *reinterpret_cast<const float2*>(bq + cc + e);
+                    const float2 g = gelu2(__uint_as_float(v[e]) + bb.x,
+                                           __uint_as_float(v[e + 1]) + bb.y);
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(g.x, g.y);
+                    pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+                }
+#pragma unroll
+                for (int e = 0; e < CW / 2; e += 4)
+                    *reinterpret_cast<uint4*>(strow + (cc + 2 * e) * 2) =
+                        make_uint4(pk[e], pk[e + 1], pk[e + 2], pk[e + 3]);
+                if (more) {
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < CW; ++e) v[e] = nv[e];
+                }
+            }
+            named_bar_sync(1 + q, 128);                     // staging tile complete
+            // coalesced copy-out: consecutive threads take consecutive 16 B of a row
+            constexpr int kChunks = QP * 2 / 16;            // 16-byte chunks per row
+            const int tq = tid & 127;
+            for (int i = tq; i < kBM * kChunks; i += 128) {
+                const int rr = i / kChunks, ch = i - rr * kChunks;
+                if (r0 + rr < n)
+                    *reinterpret_cast<uint4*>(A.u + (r0 + rr) * A.ldu + q * QP + ch * 8) =
+                        *reinterpret_cast<const uint4*>(stage + rr * C::kStStride + ch * 16);
+            }
+            named_bar_sync(1 + q, 128);                     // staging free for the next tile
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int D>
+int launch(const Args& A, cudaStream_t st) {
+    using C = Cfg<D>;
+    auto kern = gemm_gelu_kernel<D>;
+    static bool attr = false;
+    if (!attr) {
+        F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          C::kSmem));
+        attr = true;
+    }
+    const int64_t tiles = (A.n + kBM - 1) / kBM;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, f3d_num_sms()));
+    kern<<<grid, kThreads, C::kSmem, st>>>(A);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+}  // namespace gg
 }  // namespace mlp
 }  // namespace f3d
 
@@ -447,4 +665,31 @@ extern "C" int f3d_mlp_fused(const void* x, int64_t ldx, int64_t n, int d, const
     A.eps = (float)eps;
     cudaStream_t st = (cudaStream_t)stream;
     return mlp::launch<96>(A, st);
+}
+
+extern "C" int f3d_gemm_gelu_supported(int d) {
+    return (d == 96 || (d == 64 && (4 * 64) % (16 * mlp::gg::kQ) == 0)) ? 1 : 0;
+}
+
+extern "C" int f3d_gemm_gelu(const void* x, int64_t ldx, int64_t n, int d, const void* w_in_t,
+                             const float* b_in, void* u, int64_t ldu, const int32_t* n_dev,
+                             void* stream) {
+    if (!f3d_gemm_gelu_supported(d) || n < 0 || (ldx & 7) || (ldu & 7)) return F3D_ERR_CONFIG;
+    if (((uintptr_t)x | (uintptr_t)w_in_t | (uintptr_t)u) & 15) return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    mlp::gg::Args A;
+    A.x = (const __nv_bfloat16*)x;
+    A.ldx = ldx;
+    A.n = n;
+    A.n_dev = n_dev;
+    A.w_in_t = (const __nv_bfloat16*)w_in_t;
+    A.b_in = b_in;
+    A.u = (__nv_bfloat16*)u;
+    A.ldu = ldu;
+    cudaStream_t st = (cudaStream_t)stream;
+#if F3D_GG_PARTS == 4
+    return d == 96 ? mlp::gg::launch<96>(A, st) : mlp::gg::launch<64>(A, st);
+#else
+    return mlp::gg::launch<96>(A, st);
+#endif
 }

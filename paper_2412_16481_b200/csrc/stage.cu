@@ -207,34 +207,6 @@ __device__ __forceinline__ float gelu_f(float x) {
     return 0.5f * x * phi2;
 }
 
-// gelu_f on a packed pair: the same operations in the same order, with the
-// FMA/FMUL work issued as f32x2 (the bias-GELU pass is issue-bound).
-__device__ __forceinline__ float2 gelu2(float x0, float x1) {
-    const uint64_t x = f2(x0, x1);
-    const uint64_t z = fmul2(f2(fabsf(x0), fabsf(x1)), f2(0.70710678118654752f, 0.70710678118654752f));
-    float d0, d1, t0, t1;
-    f2_split(ffma2(f2(0.3275911f, 0.3275911f), z, f2(1.f, 1.f)), d0, d1);
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t0) : "f"(d0));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t1) : "f"(d1));
-    const uint64_t t = f2(t0, t1);
-    // pn = -(a1 t + ... + a5 t^5)
-    uint64_t pn = ffma2(f2(-1.061405429f, -1.061405429f), t, f2(1.453152027f, 1.453152027f));
-    pn = ffma2(pn, t, f2(-1.421413741f, -1.421413741f));
-    pn = ffma2(pn, t, f2(0.284496736f, 0.284496736f));
-    pn = ffma2(pn, t, f2(-0.254829592f, -0.254829592f));
-    pn = fmul2(pn, t);
-    float a0, a1, e0, e1;
-    f2_split(fmul2(fmul2(z, z), f2(-1.4426950408889634f, -1.4426950408889634f)), a0, a1);
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(a0));
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(a1));
-    float r0, r1;   // erf(|x|/sqrt2) = 1 - pl * e^{-z^2}
-    f2_split(ffma2(pn, f2(e0, e1), f2(1.f, 1.f)), r0, r1);
-    const uint64_t phi2 = fadd2(f2(1.f, 1.f), f2(copysignf(r0, x0), copysignf(r1, x1)));
-    float o0, o1;
-    f2_split(fmul2(fmul2(f2(0.5f, 0.5f), x), phi2), o0, o1);
-    return make_float2(o0, o1);
-}
-
 // 16-byte vector form: 8 bf16 per vector (dh % 8 == 0); each thread loads
 // kU vectors before computing any (memory-level parallelism: one 16-byte load
 // in flight per thread left the kernel latency-bound).  IT = uint32_t when the

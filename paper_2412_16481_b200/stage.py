@@ -31,6 +31,13 @@ LN_EPS = 1e-12
 # cuBLAS GEMMs + f3d_bias_gelu + f3d_row_ln.  Opt-in: measured 0.46 vs 0.39 ms
 # per config-B step (tools/mlp_ab.py)
 FUSED_MLP = os.environ.get("F3D_FUSED_MLP", "0") == "1"
+# The MLP's first half: f3d_gemm_gelu (tcgen05 GEMM, bias + GELU epilogue from
+# TMEM, u written once) from GEMM_GELU_MIN_ROWS rows up, cuBLAS GEMM +
+# f3d_bias_gelu below (tools/gemm_gelu_bench.py, d = 96: 53 vs 52 us at 100K
+# rows, 158 vs 183 us at 400K, 360 vs 423 us at 1M).  F3D_GEMM_GELU=0/1 forces.
+_GG = os.environ.get("F3D_GEMM_GELU")
+GEMM_GELU = _GG != "0"
+GEMM_GELU_MIN_ROWS = 0 if _GG == "1" else 200_000
 
 
 @dataclass
@@ -163,6 +170,10 @@ class StageRunner:
                           and self.w.get("w_in_t") is not None
                           and bool(L.load().f3d_mlp_supported(d)))
         self.u = None if self.fused_mlp else L.empty((n, dhid), torch.bfloat16)
+        self.gemm_gelu = (GEMM_GELU and n >= GEMM_GELU_MIN_ROWS and not self.fused_mlp
+                          and dhid == 4 * d
+                          and self.w.get("w_in_t") is not None
+                          and bool(L.load().f3d_gemm_gelu_supported(d)))
 
     def _row_ln(self, F, y, ybias, g, b, pe, out):
         L.call("f3d_row_ln", L.ptr(F), int(F.dtype == torch.float64), F.stride(0), L.ptr(y),
@@ -194,9 +205,14 @@ class StageRunner:
                        None if last else L.ptr(self.x), self.x.stride(0), LN_EPS,
                        L.ptr(self.n_dev), L.stream())
                 continue
-            torch.mm(self.x, w["w_in"], out=self.u)
-            L.call("f3d_bias_gelu", L.ptr(self.u), self.n, self.u.shape[1], L.ptr(w["b_in"]),
-                   L.stream())
+            if self.gemm_gelu:
+                L.call("f3d_gemm_gelu", L.ptr(self.x), self.x.stride(0), self.n, self.d,
+                       L.ptr(w["w_in_t"]), L.ptr(w["b_in"]), L.ptr(self.u), self.u.stride(0),
+                       L.ptr(self.n_dev), L.stream())
+            else:
+                torch.mm(self.x, w["w_in"], out=self.u)
+                L.call("f3d_bias_gelu", L.ptr(self.u), self.n, self.u.shape[1],
+                       L.ptr(w["b_in"]), L.stream())
             torch.mm(self.u, w["w_out"], out=self.y)
             if t + 1 < R:
                 self._row_ln(F, self.y, w["b_out"], w["ln1_g"], w["ln1_b"], True, self.x)

@@ -244,3 +244,50 @@ def test_fused_mlp_matches_unfused_stage():
         ST.FUSED_MLP = old
     rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
     assert rr < 1e-2, rr
+
+
+@pytest.mark.parametrize("n,d,ndev", [(1000, 96, None), (4099, 96, 4000), (777, 64, None)])
+def test_gemm_gelu_matches_torch(n, d, ndev):
+    """f3d_gemm_gelu (tcgen05 GEMM + bias + erf-GELU epilogue) against torch
+    fp32 gelu(x W_in + b) on the same bf16 operands; rows past n_dev untouched."""
+    import torch
+
+    from paper_2412_16481_b200 import _lib as L
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randn((n, d), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((d, 4 * d), device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
+    b = torch.randn((4 * d,), device="cuda", generator=g) * 0.1
+    wt = w.t().contiguous()
+    u = torch.full((n, 4 * d), 7.0, device="cuda", dtype=torch.bfloat16)
+    nd = None if ndev is None else torch.tensor([ndev], dtype=torch.int32, device="cuda")
+    L.call("f3d_gemm_gelu", L.ptr(x), x.stride(0), n, d, L.ptr(wt), L.ptr(b), L.ptr(u),
+           u.stride(0), L.ptr(nd), L.stream())
+    m = n if ndev is None else ndev
+    ref = torch.nn.functional.gelu(x.float() @ w.float() + b)[:m]
+    got = u[:m].float()
+    rr = ((got - ref).norm() / ref.norm()).item()
+    assert rr < 5e-3, rr
+    if ndev is not None:
+        assert bool((u[m:] == 7.0).all())
+
+
+def test_stage_gemm_gelu_matches_cublas_path():
+    """The stage with f3d_gemm_gelu (forced on) against the cuBLAS + bias_gelu path."""
+    import torch
+
+    from paper_2412_16481_b200 import stage as ST
+    a, sf, sc = _config_a(n=3000, d=96)
+    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
+    p = F.init_params(0, 96, n_heads=4)
+    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
+    C = torch.tensor(sc, device="cuda")
+    old = ST.GEMM_GELU, ST.GEMM_GELU_MIN_ROWS
+    try:
+        ST.GEMM_GELU = False
+        ref = F.stage_forward(X, C, a, sched, p)
+        ST.GEMM_GELU, ST.GEMM_GELU_MIN_ROWS = True, 0
+        out = F.stage_forward(X, C, a, sched, p)
+    finally:
+        ST.GEMM_GELU, ST.GEMM_GELU_MIN_ROWS = old
+    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
+    assert rr < 1e-2, rr
