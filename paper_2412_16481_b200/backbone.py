@@ -199,28 +199,33 @@ class Backbone:
     @staticmethod
     def _status_vector(runs, n_dev):
         """One int64 device vector holding every error word and the final
-        row count, so the host reads it with a single copy."""
-        parts = []
+        row count, so the host reads it with a single copy.  Layout: the
+        7 int64 hash stats of every stage, then per stage the int32 words
+        [PSH info (4), planner status of each round, pool flags], then the
+        row count.  Built with three launches (int32 cat, widen, cat)."""
+        dev = runs[0].stats.device
+        w32 = []
         for r in runs:
-            parts.append(r.stats)
-            parts.append(r.info.to(torch.int64))
-            parts.append(torch.stack([p.live[3] for p in r.plans]).to(torch.int64))
-            parts.append(r.pool_flags.to(torch.int64) if hasattr(r, "pool_flags")
-                         else torch.zeros(1, dtype=torch.int64, device=r.stats.device))
-        parts.append(n_dev.to(torch.int64) if n_dev is not None
-                     else torch.full((1,), runs[-1].n_cap, dtype=torch.int64,
-                                     device=runs[-1].stats.device))
-        return torch.cat(parts)
+            w32.append(r.info)
+            p0 = r.plans[0]
+            per = (r.plans[1].live.storage_offset() - p0.live.storage_offset()
+                   if len(r.plans) > 1 else 1)
+            w32.append(p0.live.as_strided((len(r.plans),), (per,), p0.live.storage_offset() + 3))
+            w32.append(r.pool_flags if hasattr(r, "pool_flags")
+                       else torch.zeros(1, dtype=torch.int32, device=dev))
+        w32.append(n_dev if n_dev is not None
+                   else torch.full((1,), runs[-1].n_cap, dtype=torch.int32, device=dev))
+        return torch.cat([r.stats for r in runs] + [torch.cat(w32).to(torch.int64)])
 
     def _check(self, status_h, runs):
         """Raise the reference exceptions from the status words (same
         conditions and messages as bw/hashing.py:60-75, bw/attention.py:104,
         bw/pooling.py validate); returns the final row count."""
-        o = 0
-        for r in runs:
+        o = 7 * len(runs)
+        for si, r in enumerate(runs):
             cfg = r.cfg
-            stats, info = status_h[o:o + 7], status_h[o + 7:o + 11]
-            o += 11
+            stats, info = status_h[7 * si:7 * si + 7], status_h[o:o + 4]
+            o += 4
             live3 = status_h[o:o + cfg.rounds]
             o += cfg.rounds
             pflags = int(status_h[o])

@@ -62,7 +62,12 @@ namespace attn_tc {
 using namespace f3d::tc;
 
 constexpr int kBM = 128;          // rows per Q tile (TMEM lanes)
-constexpr int kBN = 64;           // keys per K/V tile
+#ifndef F3D_BN_SMALL
+#define F3D_BN_SMALL 64    // keys per K/V tile for head dims <= 32
+#endif
+// keys per K/V tile (S tile columns)
+template <int DH>
+__host__ __device__ constexpr int bn_for() { return DH <= 32 ? F3D_BN_SMALL : 64; }
 #ifndef F3D_NQ_SMALL
 #define F3D_NQ_SMALL 3     // Q tiles per work item for head dims <= 32 (measured: 3 > 2 by 1-4 %)
 #endif
@@ -164,7 +169,7 @@ __device__ __forceinline__ uint64_t sw_desc(uint32_t addr, uint32_t lbo, uint32_
 
 template <int DH>
 __host__ __device__ constexpr int nsb_for() {
-    return nq_for_dh(DH) * (3 * kBN + DH) <= 512 ? 3 : 2;
+    return nq_for_dh(DH) * (3 * bn_for<DH>() + DH) <= 512 ? 3 : 2;
 }
 
 struct Maps {
@@ -190,6 +195,7 @@ struct Args {
 
 template <int DH>
 struct Cfg {
+    static constexpr int kBN = bn_for<DH>();
     static constexpr int NQ = nq_for_dh(DH);
     static constexpr int NSB = nsb_for<DH>();
     static constexpr int kQBytes = kBM * DH * 2;        // one Q tile
@@ -227,7 +233,7 @@ struct Item {
     int scope, q0, h, m, s0, s1, nt, nq;   // nq: Q tiles of this item holding real rows
 };
 
-template <int NQ>
+template <int NQ, int kBN>
 __device__ __forceinline__ Item decode(const Args& A, int item) {
     Item it;
     const int wi = item / A.H;
@@ -288,18 +294,19 @@ __device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes
 
 // TMA of rows [p0, p0 + R) of head h (map pair mp: q=0, k=2, v=4) into a
 // tile of R rows: one box of 64 rows per column block and 64-row slab.
-template <int DH, int R>
+template <int DH, int R, int BOX>
 __device__ __forceinline__ void tma_rows(const Maps& M, int mp, const Args& A, int h, int p0,
                                          uint32_t dst, uint64_t* bar) {
     using L = Lay<DH>;
+    static_assert(R % BOX == 0, "tile rows in whole boxes");
     const int c0 = h * A.dh;
 #pragma unroll
     for (int b = 0; b < L::NBLK; ++b) {
         if (b * L::BW >= A.dh) break;
 #pragma unroll
-        for (int s = 0; s < R / 64; ++s)
-            tma_2d(dst + b * R * L::SW + s * 64 * L::SW, &M.m[mp + b], bar, c0 + b * L::BW,
-                   p0 + s * 64);
+        for (int s = 0; s < R / BOX; ++s)
+            tma_2d(dst + b * R * L::SW + s * BOX * L::SW, &M.m[mp + b], bar, c0 + b * L::BW,
+                   p0 + s * BOX);
     }
 }
 
@@ -313,6 +320,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
     constexpr int NSB = C::NSB;
     constexpr int kNst = C::kNst;
     constexpr int CS = C::CS;
+    constexpr int kBN = C::kBN;
     constexpr int kThreads = threads_for<DH>();
     extern __shared__ unsigned char smem_raw[];
     // swizzled tiles need 1024-byte aligned bases
@@ -396,7 +404,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
         // ------------------------------------------------ loader warps
         uint32_t q_use = 0, kv_it = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode<NQ>(A, item);
+            const Item it = decode<NQ, kBN>(A, item);
             const int qb = q_use % NQB;
             PROF_WAIT(10, mbar_wait(q_empty + qb, ((q_use / NQB) & 1) ^ 1));
             const uint32_t qdst = sm_base + C::kOffQ + qb * NQ * C::kQBytes;
@@ -422,7 +430,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
 #pragma unroll
                         for (int g = 0; g < NQ; ++g)
                             if (run[g] >= 0)
-                                tma_rows<DH, kBM>(M, 0, A, it.h, run[g], qdst + g * C::kQBytes,
+                                tma_rows<DH, kBM, 64>(M, 0, A, it.h, run[g], qdst + g * C::kQBytes,
                                                   q_full + qb);
                     } else {
                         mbar_arrive(q_full + qb);
@@ -444,8 +452,8 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
                 if (tid == 0) {
                     if (run >= 0) {
                         mbar_arrive_expect(kv_full + s, 2 * kBN * A.dh * 2);
-                        tma_rows<DH, kBN>(M, 2, A, it.h, run, kb, kv_full + s);
-                        tma_rows<DH, kBN>(M, 4, A, it.h, run, kb + C::kKVBytes, kv_full + s);
+                        tma_rows<DH, kBN, kBN>(M, 2, A, it.h, run, kb, kv_full + s);
+                        tma_rows<DH, kBN, kBN>(M, 4, A, it.h, run, kb + C::kKVBytes, kv_full + s);
                     } else {
                         mbar_arrive(kv_full + s);
                     }
@@ -472,7 +480,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
 #pragma unroll
         for (int g = 0; g < NQ; ++g) tg[g] = ig[g] = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode<NQ>(A, item);
+            const Item it = decode<NQ, kBN>(A, item);
             const int qb = q_use % NQB;
             PROF_WAIT(4, mbar_wait(q_full + qb, (q_use / NQB) & 1));
             tc_fence_after();
@@ -578,7 +586,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
         };
         uint32_t tg = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const Item it = decode<NQ>(A, item);
+            const Item it = decode<NQ, kBN>(A, item);
             if (g >= it.nq) continue;                     // this Q tile is past the scope
             float ms = -INFINITY, l = 0.f;                // running max (scaled, log2), sum
             for (int j = 0; j < it.nt; ++j) {
@@ -591,8 +599,11 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
                 {
                     PROF_MARK(tl0);
 #pragma unroll
-                    for (int c = 0; c < KC; c += 32)
+                    for (int c = 0; c + 32 <= KC; c += 32)
                         tmem_ld32(sb + hh * KC + c, *reinterpret_cast<uint32_t(*)[32]>(&x[c]));
+                    if (KC % 32 == 16)
+                        tmem_ld16(sb + hh * KC + (KC & ~31),
+                                  *reinterpret_cast<uint32_t(*)[16]>(&x[KC & ~31]));
                     tmem_wait_ld();
                     PROF_MARK(tl1);
                     PROF_ADD(16, tl0, tl1);
@@ -686,7 +697,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
                 PROF_ADD(18, te0, te1);
                 if (KC == 64)
                     tmem_st32(sb, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
-                else
+                else if (KC == 48) {
+                    tmem_st16(sb, *reinterpret_cast<uint32_t(*)[16]>(&x[0]));
+                    tmem_st8(sb + 16, *reinterpret_cast<uint32_t(*)[8]>(&x[16]));
+                } else
                     tmem_st16(sb + hh * (KC / 2), *reinterpret_cast<uint32_t(*)[16]>(&x[0]));
                 tmem_wait_st();
                 tc_fence_before();
@@ -804,12 +818,12 @@ static EncodeFn encode_fn() {
 // 2-D map over rows [0, n) x columns [0, ncols) of a bf16 matrix with row
 // stride ld; box = {bw columns, 64 rows}, swizzled like Lay<DH>.
 static bool make_map(CUtensorMap* m, const void* base, int64_t ld, int64_t ncols, int64_t n,
-                     int bw, int sw_bytes) {
+                     int bw, int sw_bytes, int box_rows) {
     EncodeFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)ncols, (cuuint64_t)n};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    cuuint32_t box[2] = {(cuuint32_t)bw, 64};
+    cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     const CUtensorMapSwizzle sw = sw_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : sw_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
@@ -842,7 +856,9 @@ int launch(Args A, int64_t n_rows, cudaStream_t st) {
         for (int b = 0; b < 2; ++b) {
             const int w = std::min(LY::BW, A.dh - b * LY::BW);
             if (w <= 0) continue;
-            if (!make_map(&M.m[2 * t + b], bases[t], lds[t], ncols, n_rows, w, LY::SW)) A.use_tma = 0;
+            if (!make_map(&M.m[2 * t + b], bases[t], lds[t], ncols, n_rows, w, LY::SW,
+                          t == 0 ? 64 : C::kBN))
+                A.use_tma = 0;
         }
     const int total = A.nwork * A.H;
     const int grid = std::max(1, std::min(total, f3d_num_sms()));
