@@ -470,6 +470,67 @@ __global__ void pool_reduce_kernel(const T* __restrict__ x, int64_t ldx, int d,
     }
 }
 
+// fp32 rows with d % 4 == 0: one thread per (pooled row, 4 columns), float4
+// loads/stores, 32-bit index math; per column the same operations in the same
+// order as pool_reduce_kernel (so the same bits).
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4_min(float4 a, float4 b) {
+    return make_float4(b.x < a.x ? b.x : a.x, b.y < a.y ? b.y : a.y, b.z < a.z ? b.z : a.z,
+                       b.w < a.w ? b.w : a.w);
+}
+__device__ __forceinline__ float4 f4_max(float4 a, float4 b) {
+    return make_float4(b.x > a.x ? b.x : a.x, b.y > a.y ? b.y : a.y, b.z > a.z ? b.z : a.z,
+                       b.w > a.w ? b.w : a.w);
+}
+
+__global__ void pool_reduce4_kernel(const float* __restrict__ x, int64_t ldx, int d4,
+                                    const int32_t* __restrict__ members,
+                                    const int32_t* __restrict__ sizes, int npool,
+                                    const int32_t* npool_dev, int rho, int op,
+                                    float* __restrict__ out, int64_t ldo) {
+    const int np = (int)dyn_n(npool, npool_dev);
+    const uint32_t tot = (uint32_t)np * (uint32_t)d4;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+        const uint32_t j = t / (uint32_t)d4;
+        const int c = 4 * (int)(t - j * (uint32_t)d4);
+        const int32_t* mem = members + (int64_t)j * rho;
+        const int sz = sizes[j];
+        auto X = [&](int r) -> float4 {
+            return __ldg(reinterpret_cast<const float4*>(x + (int64_t)mem[r] * ldx + c));
+        };
+        float4 acc = X(0);
+        if (op == R_MIN || op == R_MAX) {
+            for (int r = 1; r < sz; ++r) acc = op == R_MIN ? f4_min(acc, X(r)) : f4_max(acc, X(r));
+        } else if (sz > 1) {
+            const int nr = sz - 1;
+            float4 res;
+            if (nr < 8) {
+                res = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int r = 1; r <= nr; ++r) res = f4_add(res, X(r));
+            } else {
+                float4 a8[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) a8[q] = X(1 + q);
+                const int full = nr - nr % 8;
+                for (int i = 8; i < full; i += 8)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) a8[q] = f4_add(a8[q], X(1 + i + q));
+                res = f4_add(f4_add(f4_add(a8[0], a8[1]), f4_add(a8[2], a8[3])),
+                             f4_add(f4_add(a8[4], a8[5]), f4_add(a8[6], a8[7])));
+                for (int i = full; i < nr; ++i) res = f4_add(res, X(1 + i));
+            }
+            acc = f4_add(acc, res);
+        }
+        if (op == R_MEAN) {
+            const float fs = (float)sz;
+            acc = make_float4(acc.x / fs, acc.y / fs, acc.z / fs, acc.w / fs);
+        }
+        *reinterpret_cast<float4*>(out + (int64_t)j * ldo + c) = acc;
+    }
+}
+
 }  // namespace pool
 }  // namespace f3d
 
@@ -512,7 +573,14 @@ extern "C" int f3d_pool_reduce(const void* x, int dtype, int64_t ldx, int d,
     if (dtype == 2)
         pool::pool_reduce_kernel<double><<<(unsigned)g, 256, 0, st>>>(
             (const double*)x, ldx, d, members, sizes, npool, npool_dev, rho, op, (double*)out, ldo);
-    else if (dtype == 1)
+    else if (dtype == 1 && d % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0 &&
+             (((uintptr_t)x | (uintptr_t)out) & 15) == 0 && npool * (d / 4) < ((int64_t)1 << 31)) {
+        int64_t g4 = (npool * (d / 4) + 255) / 256;
+        if (g4 > (int64_t)f3d_num_sms() * 32) g4 = (int64_t)f3d_num_sms() * 32;
+        pool::pool_reduce4_kernel<<<(unsigned)g4, 256, 0, st>>>(
+            (const float*)x, ldx, d / 4, members, sizes, (int)npool, npool_dev, rho, op, (float*)out,
+            ldo);
+    } else if (dtype == 1)
         pool::pool_reduce_kernel<float><<<(unsigned)g, 256, 0, st>>>(
             (const float*)x, ldx, d, members, sizes, npool, npool_dev, rho, op, (float*)out, ldo);
     else if (dtype == 0)

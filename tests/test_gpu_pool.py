@@ -133,3 +133,32 @@ def test_pool_stage_map_and_unpool_vs_oracle():
     np.testing.assert_array_equal(up, oc[opar])
     with pytest.raises(ConfigError):
         F.unpool(pc, np.array([len(pc)]))
+
+
+@pytest.mark.parametrize("rho", [2, 8, 11, 64])
+@pytest.mark.parametrize("reduce", ["sum", "mean", "min", "max"])
+def test_pool_features_fp32_vector_path_bit_exact(rho, reduce):
+    """fp32 rows with d % 4 == 0 take the float4 reduce kernel; per column it
+    must reproduce numpy's float32 add.reduceat order (and min/max/mean) bit
+    for bit."""
+    import torch
+    r = np.random.default_rng(rho)
+    m = 1000
+    c = r.uniform(size=(m, 3))
+    x = r.normal(size=(m, 96)).astype(np.float32)
+    sub = F.build_subbuckets(c, rho)
+    got = F.pool_features(torch.tensor(x, device="cuda"), sub, reduce).cpu().numpy()
+    sid, sizes = np.asarray(sub.subbucket_id), np.asarray(sub.sizes)
+    order = np.argsort(sid, kind="stable")
+    bounds = np.r_[0, np.cumsum(sizes)[:-1]]
+    g = x[order]
+    if reduce in ("sum", "mean"):
+        ref = np.add.reduceat(g, bounds, axis=0)
+        if reduce == "mean":
+            ref = ref / sizes[:, None].astype(np.float32)
+    elif reduce == "min":
+        ref = np.minimum.reduceat(g, bounds, axis=0)
+    else:
+        ref = np.maximum.reduceat(g, bounds, axis=0)
+    assert got.dtype == np.float32
+    np.testing.assert_array_equal(got, ref.astype(np.float32))
