@@ -280,6 +280,16 @@ int f3d_gemm_gelu_supported(int d);
 int f3d_gemm_gelu(const void *x, int64_t ldx, int64_t n, int d, const void *w_in_t,
                   const float *b_in, void *u, int64_t ldu, const int32_t *n_dev, void *stream);
 
+/* F += x W + bias (x: n x k bf16, w_t = W^T: d x k bf16), then, when ln_g is
+ * given, x_next = LayerNorm(F) * ln_g + ln_b (+ PE of pe_coords when given) in
+ * bf16: the projection GEMM and f3d_row_ln of the stage in one tcgen05 kernel
+ * (bw/stage.py:146-158).  (d, k) in {(96, 96), (96, 384)} (f3d_gemm_ln_supported). */
+int f3d_gemm_ln_supported(int d, int k);
+int f3d_gemm_ln(const void *x, int64_t ldx, int64_t n, int d, int k, const void *w_t,
+                const float *bias, float *F, int64_t ldf, const float *ln_g, const float *ln_b,
+                const double *pe_coords, const double *lo_ext, double pe_base, void *x_next,
+                int64_t ldxn, double eps, const int32_t *n_dev, void *stream);
+
 /* ------------------------------------------------ training
  * LayerNorm backward fused with the residual add: dx = dres + rstd*(g*dy -
  * mean(g*dy) - xhat*mean(g*dy*xhat)); dgain += sum dy*xhat, dbeta += sum dy

@@ -623,6 +623,320 @@ int launch(const Args& A, cudaStream_t st) {
     return F3D_OK;
 }
 }  // namespace gg
+
+// ---------------------------------------------------------------------------
+// Projection + residual + LayerNorm: F += X W + bias (X: n x K bf16, W: K x D),
+// then x_next = LN(F) * g + b (+ PE) in bf16 -- the cuBLAS GEMM + f3d_row_ln
+// pair of the stage (O projection -> LN2, bw/stage.py:146-152; MLP output ->
+// LN1 + PE of the next round, :153-158) in one pass: the fp32 products go
+// TMEM -> bf16 smem tile (the unfused path's bf16 GEMM output) -> row
+// epilogue with lanes over columns (coalesced F / x_next), the arithmetic of
+// row_ln_vec_kernel.
+//   * warp 0 streams X in 96-column K chunks (cp.async, kNC-deep ring), W^T
+//     stays in smem; warp 1 (elected lane) accumulates each tile into one of
+//     two TMEM buffers (D columns each);
+//   * two epilogue warpgroups copy a tile's accumulator rows to the smem y
+//     tile (releasing the TMEM buffer), then run the row epilogue.
+namespace gl {
+constexpr int kKC = 96;                        // K columns per streamed chunk
+constexpr int kNC = 4;                         // chunk ring depth
+constexpr int kEW = 8;                         // epilogue warps (2 warpgroups)
+constexpr int kThreads = 128 + kEW * 32;
+
+template <int D, int K>
+struct Cfg {
+    static constexpr int kChunks = K / kKC;
+    static constexpr int kWBytes = D * K * 2;                 // W^T: D rows x K cols
+    static constexpr int kCBytes = kBM * kKC * 2;             // one X chunk
+    static constexpr int kYStride = 2 * D + 16;
+    static constexpr int kOffW = 0;
+    static constexpr int kOffC = kOffW + kWBytes;
+    static constexpr int kOffY = kOffC + kNC * kCBytes;
+    static constexpr int kOffBias = kOffY + kBM * kYStride;
+    static constexpr int kOffBar = kOffBias + D * 4;
+    static constexpr int kNumBars = 2 * kNC + 4;              // c_full, c_empty, d_full[2], d_empty[2]
+    static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
+    static_assert(K % kKC == 0 && D % 32 == 0 && D <= 128, "shapes");
+    static_assert(kSmem <= 227 * 1024, "smem budget");
+};
+
+struct Args {
+    const __nv_bfloat16* x;
+    int64_t ldx;
+    int64_t n;
+    const int32_t* n_dev;
+    const __nv_bfloat16* w_t;       // (D, K) row-major = W^T
+    const float* bias;              // (D)
+    float* F;
+    int64_t ldf;
+    const float* ln_g;              // nullable: residual only
+    const float* ln_b;
+    const double* pec;              // nullable: no PE
+    const double* lo_ext;
+    float pl2;
+    __nv_bfloat16* x_next;
+    int64_t ldxn;
+    float eps;
+};
+
+// rows [r0, r0 + 128): warp w of kEW takes 8-row blocks; lane q owns columns
+// [4q, 4q + 4) (q < D/4) -- f3d_row_ln's vector arithmetic and PE.
+template <int D>
+__device__ __forceinline__ void row_epi(const Args& A, const unsigned char* ytile,
+                                        const float* s_bias, int64_t r0, int64_t n, int w,
+                                        int lane) {
+    constexpr int kYStride = 2 * D + 16;
+    const bool act = lane < D / 4;
+    const int c0 = 4 * lane;
+    const float4 bo = act ? *reinterpret_cast<const float4*>(s_bias + c0) : make_float4(0, 0, 0, 0);
+    float4 gg = make_float4(0, 0, 0, 0), bb = gg;
+    if (A.ln_g && act) {
+        gg = __ldg(reinterpret_cast<const float4*>(A.ln_g + c0));
+        bb = __ldg(reinterpret_cast<const float4*>(A.ln_b + c0));
+    }
+    constexpr int npair = D / 6, blk = 2 * npair;
+    int pa[2];
+    float fq[2], pinv[2];
+    double plo[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int c = c0 + 2 * p;
+        pa[p] = c / blk;
+        const int pj = (c - pa[p] * blk) >> 1;
+        fq[p] = exp2f(-(float)pj / (float)npair * A.pl2);
+        plo[p] = (A.pec && A.lo_ext) ? A.lo_ext[pa[p]] : 0.0;
+        pinv[p] = (A.pec && A.lo_ext) ? (float)(1.0 / A.lo_ext[3 + pa[p]]) : 1.f;
+    }
+    constexpr int RB = 8;
+#pragma unroll 1
+    for (int rb = w * RB; rb < kBM; rb += kEW * RB) {
+        float4 v[RB];
+        double pc[RB][3];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            const int64_t row = r0 + rb + i;
+            const bool ok = act && row < n;
+            v[i] = ok ? *reinterpret_cast<const float4*>(A.F + row * A.ldf + c0) : make_float4(0, 0, 0, 0);
+            if (A.pec && A.ln_g)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) pc[i][a] = row < n ? A.pec[3 * row + a] : 0.0;
+        }
+        float s[RB], q[RB];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            const int64_t row = r0 + rb + i;
+            if (act) {
+                const uint2 yy = *reinterpret_cast<const uint2*>(ytile + (rb + i) * kYStride + c0 * 2);
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&yy);
+                const float2 y01 = __bfloat1622float2(h[0]), y23 = __bfloat1622float2(h[1]);
+                v[i].x += y01.x + bo.x;
+                v[i].y += y01.y + bo.y;
+                v[i].z += y23.x + bo.z;
+                v[i].w += y23.y + bo.w;
+                if (row < n) *reinterpret_cast<float4*>(A.F + row * A.ldf + c0) = v[i];
+            }
+            s[i] = (v[i].x + v[i].y) + (v[i].z + v[i].w);
+        }
+        if (!A.ln_g) continue;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < RB; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+        const float inv_d = 1.f / (float)D;
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            const float m = s[i] * inv_d;
+            const float a = act ? v[i].x - m : 0.f, b = act ? v[i].y - m : 0.f;
+            const float c = act ? v[i].z - m : 0.f, e = act ? v[i].w - m : 0.f;
+            q[i] = (a * a + b * b) + (c * c + e * e);
+            s[i] = m;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < RB; ++i) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
+        if (!act) continue;
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            const int64_t row = r0 + rb + i;
+            if (row >= n) break;
+            const float rstd = rsqrtf(q[i] * inv_d + A.eps);
+            const float m = s[i];
+            float o0 = (v[i].x - m) * rstd * gg.x + bb.x;
+            float o1 = (v[i].y - m) * rstd * gg.y + bb.y;
+            float o2 = (v[i].z - m) * rstd * gg.z + bb.z;
+            float o3 = (v[i].w - m) * rstd * gg.w + bb.w;
+            if (A.pec) {
+                float sn[2], cs[2];
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    // select the axis without dynamic register-array indexing
+                    const double cv = pa[p] == 0 ? pc[i][0] : (pa[p] == 1 ? pc[i][1] : pc[i][2]);
+                    const float xn = (float)__dsub_rn(cv, plo[p]) * pinv[p];
+                    __sincosf(xn * fq[p], &sn[p], &cs[p]);
+                }
+                o0 += sn[0];
+                o1 += cs[0];
+                o2 += sn[1];
+                o3 += cs[1];
+            }
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(o0, o1), h1 = __floats2bfloat162_rn(o2, o3);
+            uint2 wv;
+            wv.x = *reinterpret_cast<uint32_t*>(&h0);
+            wv.y = *reinterpret_cast<uint32_t*>(&h1);
+            *reinterpret_cast<uint2*>(A.x_next + row * A.ldxn + c0) = wv;
+        }
+    }
+}
+
+template <int D, int K>
+__global__ void __launch_bounds__(kThreads, 1) gemm_ln_kernel(const Args A) {
+    using C = Cfg<D, K>;
+    constexpr int NCH = C::kChunks;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+    uint64_t* c_full = bars;
+    uint64_t* c_empty = bars + kNC;
+    uint64_t* d_full = bars + 2 * kNC;
+    uint64_t* d_empty = d_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+    float* s_bias = reinterpret_cast<float*>(smem + C::kOffBias);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t n = dyn_n(A.n, A.n_dev);
+    const int ntiles = (int)((n + kBM - 1) / kBM);
+
+    for (int i = tid; i < D * (K / 8); i += kThreads) {
+        const int r = i / (K / 8), c = i - r * (K / 8);
+        *reinterpret_cast<uint4*>(smem + C::kOffW + core_off<K>(r, c)) =
+            __ldg(reinterpret_cast<const uint4*>(A.w_t + (int64_t)r * K) + c);
+    }
+    for (int i = tid; i < D; i += kThreads) s_bias[i] = A.bias[i];
+    if (tid == 0) {
+        for (int b = 0; b < kNC; ++b) {
+            mbar_init(c_full + b, 32);
+            mbar_init(c_empty + b, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(d_full + b, 1);
+            mbar_init(d_empty + b, kEW * 32);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(tmem_slot, 256);
+        tmem_relinquish();
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_base = saddr(smem);
+
+    if (warp == 0) {
+        int ci = 0;                                          // chunk counter
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t r0 = (int64_t)tile * kBM;
+            for (int kc = 0; kc < NCH; ++kc, ++ci) {
+                const int b = ci % kNC;
+                mbar_wait(c_empty + b, ((ci / kNC) & 1) ^ 1);
+                const uint32_t dst = sm_base + C::kOffC + b * C::kCBytes;
+                for (int i = lane; i < kBM * (kKC / 8); i += 32) {
+                    const int r = i / (kKC / 8), c = i - r * (kKC / 8);
+                    const bool ok = r0 + r < n;
+                    const __nv_bfloat16* src = ok ? A.x + (r0 + r) * A.ldx + kc * kKC + c * 8 : A.x;
+                    cp_async16z(dst + core_off<kKC>(r, c), src, ok);
+                }
+                cp_async_arrive(c_full + b);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id = idesc_bf16(kBM, D, 0, 0);
+        const uint64_t dW = smem_desc(sm_base + C::kOffW, 128, 16 * K);
+        const uint64_t dC = smem_desc(sm_base + C::kOffC, 128, 16 * kKC);
+        constexpr uint32_t kCD = C::kCBytes >> 4;
+        int ci = 0, it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int db = it & 1;
+            if (it >= 2) mbar_wait(d_empty + db, ((it >> 1) - 1) & 1);   // buffer read out
+            tc_fence_after();
+            for (int kc = 0; kc < NCH; ++kc, ++ci) {
+                const int b = ci % kNC;
+                mbar_wait(c_full + b, (ci / kNC) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t dc = dC + (uint64_t)(b * kCD);
+#pragma unroll
+                    for (int k = 0; k < kKC / 16; ++k)
+                        umma_f16(tmem + db * D, dc + (uint64_t)(16 * k),
+                                 dW + (uint64_t)(16 * (kc * (kKC / 16) + k)), id,
+                                 (kc > 0 || k > 0) ? 1u : 0u);
+                    umma_commit(c_empty + b);
+                    if (kc == NCH - 1) umma_commit(d_full + db);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4) {
+        const int e = warp - 4;                              // 0 .. kEW-1
+        const int r = (warp & 3) * 32 + lane;                // TMEM lane = tile row
+        const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+        const int half = e >> 2;                             // column half of the copy
+        unsigned char* yrow = smem + C::kOffY + r * C::kYStride;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int db = it & 1;
+            mbar_wait(d_full + db, (it >> 1) & 1);
+            tc_fence_after();
+            named_bar_sync(5, kEW * 32);                     // previous tile's y reads done
+#pragma unroll
+            for (int c = half * (D / 2); c < (half + 1) * (D / 2); c += 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem + lb + db * D + c, v);
+                tmem_wait_ld();
+                uint4 w0, w1;
+                uint32_t* p0 = reinterpret_cast<uint32_t*>(&w0);
+                uint32_t* p1 = reinterpret_cast<uint32_t*>(&w1);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * q]),
+                                                             __uint_as_float(v[2 * q + 1]));
+                    p0[q] = *reinterpret_cast<uint32_t*>(&h);
+                    h = __floats2bfloat162_rn(__uint_as_float(v[8 + 2 * q]),
+                                              __uint_as_float(v[9 + 2 * q]));
+                    p1[q] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                *reinterpret_cast<uint4*>(yrow + c * 2) = w0;
+                *reinterpret_cast<uint4*>(yrow + c * 2 + 16) = w1;
+            }
+            tc_fence_before();
+            mbar_arrive(d_empty + db);                       // TMEM buffer free
+            named_bar_sync(5, kEW * 32);                     // y tile complete
+            row_epi<D>(A, smem + C::kOffY, s_bias, (int64_t)tile * kBM, n, e, lane);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+template <int D, int K>
+int launch(const Args& A, cudaStream_t st) {
+    using C = Cfg<D, K>;
+    auto kern = gemm_ln_kernel<D, K>;
+    static bool attr = false;
+    if (!attr) {
+        F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          C::kSmem));
+        attr = true;
+    }
+    const int64_t tiles = (A.n + kBM - 1) / kBM;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, f3d_num_sms()));
+    kern<<<grid, kThreads, C::kSmem, st>>>(A);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+}  // namespace gl
 }  // namespace mlp
 }  // namespace f3d
 
@@ -692,4 +1006,39 @@ extern "C" int f3d_gemm_gelu(const void* x, int64_t ldx, int64_t n, int d, const
 #else
     return mlp::gg::launch<96>(A, st);
 #endif
+}
+
+extern "C" int f3d_gemm_ln_supported(int d, int k) { return (d == 96 && (k == 96 || k == 384)) ? 1 : 0; }
+
+extern "C" int f3d_gemm_ln(const void* x, int64_t ldx, int64_t n, int d, int k, const void* w_t,
+                           const float* bias, float* F, int64_t ldf, const float* ln_g,
+                           const float* ln_b, const double* pe_coords, const double* lo_ext,
+                           double pe_base, void* x_next, int64_t ldxn, double eps,
+                           const int32_t* n_dev, void* stream) {
+    if (!f3d_gemm_ln_supported(d, k) || n < 0 || (ldx & 7) || (ldf & 3) || (x_next && (ldxn & 7)))
+        return F3D_ERR_CONFIG;
+    if ((ln_g != nullptr) != (x_next != nullptr) || (ln_g && !ln_b)) return F3D_ERR_CONFIG;
+    if (pe_coords && (!ln_g || d % 6)) return F3D_ERR_CONFIG;
+    if (((uintptr_t)x | (uintptr_t)w_t | (uintptr_t)F | (uintptr_t)x_next | (uintptr_t)bias) & 15)
+        return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    mlp::gl::Args A;
+    A.x = (const __nv_bfloat16*)x;
+    A.ldx = ldx;
+    A.n = n;
+    A.n_dev = n_dev;
+    A.w_t = (const __nv_bfloat16*)w_t;
+    A.bias = bias;
+    A.F = F;
+    A.ldf = ldf;
+    A.ln_g = ln_g;
+    A.ln_b = ln_b;
+    A.pec = pe_coords;
+    A.lo_ext = lo_ext;
+    A.pl2 = pe_coords ? (float)log2(pe_base) : 0.f;
+    A.x_next = (__nv_bfloat16*)x_next;
+    A.ldxn = ldxn;
+    A.eps = (float)eps;
+    cudaStream_t st = (cudaStream_t)stream;
+    return k == 96 ? mlp::gl::launch<96, 96>(A, st) : mlp::gl::launch<96, 384>(A, st);
 }

@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(kThreads) row_ln_vec_kernel(
             float sn[2], cs[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                const float xn = (float)__dsub_rn(pc[i][pa[p]], plo[p]) * pinv[p];
+                // select the axis without dynamic register-array indexing
+                const double cv = pa[p] == 0 ? pc[i][0] : (pa[p] == 1 ? pc[i][1] : pc[i][2]);
+                const float xn = (float)__dsub_rn(cv, plo[p]) * pinv[p];
                 __sincosf(xn * fq[p], &sn[p], &cs[p]);
             }
             o0 += sn[0];

@@ -35,6 +35,11 @@ FUSED_MLP = os.environ.get("F3D_FUSED_MLP", "0") == "1"
 # TMEM, u written once) from GEMM_GELU_MIN_ROWS rows up, cuBLAS GEMM +
 # f3d_bias_gelu below (tools/gemm_gelu_bench.py, d = 96: 53 vs 52 us at 100K
 # rows, 158 vs 183 us at 400K, 360 vs 423 us at 1M).  F3D_GEMM_GELU=0/1 forces.
+# F3D_GEMM_LN=1 selects f3d_gemm_ln (projection + residual + LayerNorm (+PE) in
+# one tcgen05 kernel) over cuBLAS GEMMs + f3d_row_ln.  Opt-in: measured 1.37 vs
+# 1.22 ms per config-B step -- one CTA per SM leaves the row epilogue with too
+# few loads in flight
+GEMM_LN = os.environ.get("F3D_GEMM_LN", "0") == "1"
 _GG = os.environ.get("F3D_GEMM_GELU")
 GEMM_GELU = _GG != "0"
 GEMM_GELU_MIN_ROWS = 0 if _GG == "1" else 200_000
@@ -83,6 +88,7 @@ class StageParams:
             "w_in": f(self.w_in, bf), "b_in": f(self.b_in, f32),
             "w_out": f(self.w_out, bf), "b_out": f(self.b_out, f32),
             "w_in_t": f(self.w_in, bf).t().contiguous(), "w_out_t": f(self.w_out, bf).t().contiguous(),
+            "w_o_t": f(self.w_o, bf).t().contiguous(),
             "ln1_g": f(self.ln1_gain, f32), "ln1_b": f(self.ln1_bias, f32),
             "ln2_g": f(self.ln2_gain, f32), "ln2_b": f(self.ln2_bias, f32),
         }
@@ -170,6 +176,11 @@ class StageRunner:
                           and self.w.get("w_in_t") is not None
                           and bool(L.load().f3d_mlp_supported(d)))
         self.u = None if self.fused_mlp else L.empty((n, dhid), torch.bfloat16)
+        lib = L.load()
+        self.gemm_ln = (GEMM_LN and not self.fused_mlp and dhid == 4 * d
+                        and self.w.get("w_o_t") is not None
+                        and bool(lib.f3d_gemm_ln_supported(d, d))
+                        and bool(lib.f3d_gemm_ln_supported(d, dhid)))
         self.gemm_gelu = (GEMM_GELU and n >= GEMM_GELU_MIN_ROWS and not self.fused_mlp
                           and dhid == 4 * d
                           and self.w.get("w_in_t") is not None
@@ -182,6 +193,12 @@ class StageRunner:
                L.ptr(out), 0, 0 if out is None else out.stride(0), self.n, self.d, LN_EPS,
                L.stream())
 
+    def _gemm_ln(self, X, k, w_t, bias, F, g, b, pe, out):
+        L.call("f3d_gemm_ln", L.ptr(X), X.stride(0), self.n, self.d, k, L.ptr(w_t), L.ptr(bias),
+               L.ptr(F), F.stride(0), L.ptr(g), L.ptr(b), L.ptr(self.coords) if pe else None,
+               L.ptr(self.lo_ext) if pe else None, 10000.0, L.ptr(out),
+               0 if out is None else out.stride(0), LN_EPS, L.ptr(self.n_dev), L.stream())
+
     def run(self, F: torch.Tensor) -> torch.Tensor:
         """F: (n, d) residual stream on the device (float32/float64), updated
         in place and returned."""
@@ -192,8 +209,12 @@ class StageRunner:
         for t, plan in enumerate(self.plans):
             torch.addmm(w["b_qkv"], self.x, w["w_qkv"], out=self.qkv)
             attend(q, k, v, self.a, plan, self.H, self.dh)
-            torch.mm(self.a, w["w_o"], out=self.y)
-            self._row_ln(F, self.y, w["b_o"], w["ln2_g"], w["ln2_b"], None, self.x)
+            if self.gemm_ln and F.dtype == torch.float32:
+                self._gemm_ln(self.a, self.d, w["w_o_t"], w["b_o"], F, w["ln2_g"], w["ln2_b"],
+                              False, self.x)
+            else:
+                torch.mm(self.a, w["w_o"], out=self.y)
+                self._row_ln(F, self.y, w["b_o"], w["ln2_g"], w["ln2_b"], None, self.x)
             if self.fused_mlp and F.dtype == torch.float32:
                 last = t + 1 == R
                 # F += MLP(x); x <- LN1(F) + PE for the next round, one kernel
@@ -213,6 +234,12 @@ class StageRunner:
                 torch.mm(self.x, w["w_in"], out=self.u)
                 L.call("f3d_bias_gelu", L.ptr(self.u), self.n, self.u.shape[1],
                        L.ptr(w["b_in"]), L.stream())
+            if self.gemm_ln and F.dtype == torch.float32:
+                last = t + 1 == R
+                self._gemm_ln(self.u, self.u.shape[1], w["w_out_t"], w["b_out"], F,
+                              None if last else w["ln1_g"], None if last else w["ln1_b"],
+                              not last, None if last else self.x)
+                continue
             torch.mm(self.u, w["w_out"], out=self.y)
             if t + 1 < R:
                 self._row_ln(F, self.y, w["b_out"], w["ln1_g"], w["ln1_b"], True, self.x)

@@ -115,6 +115,7 @@ class DeviceWeights:
             w[k].copy_(m[mk])
         w["w_in_t"].copy_(m["w_in"].t())
         w["w_out_t"].copy_(m["w_out"].t())
+        w["w_o_t"].copy_(m["w_o"].t())
 
     def sgd(self, grads, lr: float):
         for k in GRAD_NAMES:

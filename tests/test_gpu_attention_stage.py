@@ -291,3 +291,69 @@ def test_stage_gemm_gelu_matches_cublas_path():
         ST.GEMM_GELU, ST.GEMM_GELU_MIN_ROWS = old
     rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
     assert rr < 1e-2, rr
+
+
+@pytest.mark.parametrize("k,ln,pe,ndev", [(96, True, False, None), (384, True, True, 2900),
+                                          (384, False, False, None), (96, True, True, None)])
+def test_gemm_ln_matches_torch(k, ln, pe, ndev):
+    """f3d_gemm_ln: F += x W + b, x_next = LN(F) g + b (+PE) against torch on
+    the same bf16 operands (y rounded to bf16 as the unfused GEMM output)."""
+    import torch
+
+    from paper_2412_16481_b200 import _lib as L
+    n, d = 3001, 96
+    g = torch.Generator(device="cuda").manual_seed(k + n)
+    x = torch.randn((n, k), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((k, d), device="cuda", generator=g) / k ** 0.5).to(torch.bfloat16)
+    bias = torch.randn((d,), device="cuda", generator=g) * 0.1
+    F0 = torch.randn((n, d), device="cuda", generator=g)
+    lg = 1 + 0.1 * torch.randn((d,), device="cuda", generator=g)
+    lb = 0.1 * torch.randn((d,), device="cuda", generator=g)
+    coords = torch.rand((n, 3), device="cuda", dtype=torch.float64, generator=g)
+    lo_ext = torch.tensor([0, 0, 0, 1, 1, 1], device="cuda", dtype=torch.float64)
+    Fg = F0.clone()
+    xn = torch.full((n, d), 3.0, device="cuda", dtype=torch.bfloat16)
+    nd = None if ndev is None else torch.tensor([ndev], dtype=torch.int32, device="cuda")
+    wt = w.t().contiguous()
+    rc = L.load().f3d_gemm_ln(L.ptr(x), x.stride(0), n, d, k, L.ptr(wt), L.ptr(bias), L.ptr(Fg),
+                              Fg.stride(0), L.ptr(lg) if ln else None, L.ptr(lb) if ln else None,
+                              L.ptr(coords) if pe else None, L.ptr(lo_ext) if pe else None,
+                              __import__("ctypes").c_double(10000.0), L.ptr(xn) if ln else None,
+                              xn.stride(0), __import__("ctypes").c_double(1e-12), L.ptr(nd),
+                              L.stream())
+    assert rc == 0
+    m = n if ndev is None else ndev
+    y = (x.float() @ w.float()).to(torch.bfloat16).float()
+    Fr = F0 + (y + bias)
+    assert float(((Fg[:m] - Fr[:m]).norm() / Fr[:m].norm()).item()) < 1e-3
+    assert torch.equal(Fg[m:], F0[m:])
+    if ln:
+        xr = torch.nn.functional.layer_norm(Fr, (d,), lg, lb, eps=1e-12)
+        if pe:
+            xr = xr + torch.tensor(F.positional_encoding(coords.cpu().numpy(), d),
+                                   device="cuda", dtype=torch.float32)
+        got = xn[:m].float()
+        assert float(((got - xr[:m]).norm() / xr[:m].norm()).item()) < 1e-2
+        assert bool((xn[m:] == 3.0).all())
+
+
+def test_stage_gemm_ln_matches_cublas_path():
+    """The stage with f3d_gemm_ln (opt-in) against cuBLAS GEMMs + f3d_row_ln."""
+    import torch
+
+    from paper_2412_16481_b200 import stage as ST
+    a, sf, sc = _config_a(n=3000, d=96)
+    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
+    p = F.init_params(0, 96, n_heads=4)
+    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
+    C = torch.tensor(sc, device="cuda")
+    old = ST.GEMM_LN
+    try:
+        ST.GEMM_LN = False
+        ref = F.stage_forward(X, C, a, sched, p)
+        ST.GEMM_LN = True
+        out = F.stage_forward(X, C, a, sched, p)
+    finally:
+        ST.GEMM_LN = old
+    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
+    assert rr < 1e-2, rr
