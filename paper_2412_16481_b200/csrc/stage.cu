@@ -313,7 +313,7 @@ namespace stage {
 // 16-byte F load, one 8-byte y load); each warp carries RPW rows at once so
 // every load of all of them is in flight before the first reduction.
 template <int RPW, bool HAS_Y, bool HAS_OUT, bool HAS_PE>
-__global__ void __launch_bounds__(kThreads) row_ln_vec_kernel(
+__global__ void __launch_bounds__(kThreads, HAS_PE ? 4 : 5) row_ln_vec_kernel(
     float* __restrict__ F, int64_t ldf, const __nv_bfloat16* __restrict__ y, int64_t ldy,
     const float* __restrict__ ybias, const float* __restrict__ gain,
     const float* __restrict__ beta, const double* __restrict__ pec,
@@ -325,17 +325,12 @@ __global__ void __launch_bounds__(kThreads) row_ln_vec_kernel(
     const int c0 = 4 * lane;
     float4 v[RPW];
     uint2 yy[RPW];
-    double pc[RPW][3];
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
         const int64_t row = row0 + i;
         const bool ok = act && row < n;
         v[i] = ok ? *reinterpret_cast<const float4*>(F + row * ldf + c0) : make_float4(0, 0, 0, 0);
         if (HAS_Y) yy[i] = ok ? *reinterpret_cast<const uint2*>(y + row * ldy + c0) : make_uint2(0, 0);
-        if (HAS_PE && HAS_OUT) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) pc[i][a] = (row < n) ? pec[3 * row + a] : 0.0;
-        }
     }
     if (HAS_Y) {
         const float4 yb = (ybias && act) ? *reinterpret_cast<const float4*>(ybias + c0)
@@ -394,6 +389,17 @@ __global__ void __launch_bounds__(kThreads) row_ln_vec_kernel(
         plo[p] = lo_ext ? lo_ext[pa[p]] : 0.0;
         pinv[p] = lo_ext ? (float)(1.0 / lo_ext[3 + pa[p]]) : 1.f;
     }
+    // PE inputs: only this lane's two axes, loaded after the reductions (short
+    // live ranges: the PE variant stays at the non-PE occupancy)
+    double pcv[RPW][2];
+    if (HAS_PE) {
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int64_t row = row0 + i < n ? row0 + i : 0;
+            pcv[i][0] = pec[3 * row + pa[0]];
+            pcv[i][1] = pec[3 * row + pa[1]];
+        }
+    }
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
         const int64_t row = row0 + i;
@@ -408,9 +414,7 @@ __global__ void __launch_bounds__(kThreads) row_ln_vec_kernel(
             float sn[2], cs[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                // select the axis without dynamic register-array indexing
-                const double cv = pa[p] == 0 ? pc[i][0] : (pa[p] == 1 ? pc[i][1] : pc[i][2]);
-                const float xn = (float)__dsub_rn(cv, plo[p]) * pinv[p];
+                const float xn = (float)__dsub_rn(pcv[i][p], plo[p]) * pinv[p];
                 __sincosf(xn * fq[p], &sn[p], &cs[p]);
             }
             o0 += sn[0];
