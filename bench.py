@@ -377,6 +377,10 @@ def main():
         breakdown = {k: round(v / steps, 4) for k, v in sorted(probe_tot.items(), key=lambda kv: -kv[1])}
         mine_ms = sum(probe_tot.values()) / steps
         total_pts = N_POINTS * world
+        # the roof that binds at dh = 24: one exp2 per score on the MUFU unit
+        n_scores = attn_flops // (4 * (D_MODEL // 4))
+        exp_ach = n_scores / (attn_ms * 1e-3) / 1e12 if attn_ms else 0.0
+        exp_peak = 16 * 148 * (clk.summary().get("sm_mhz") or 1965.0) * 1e6 / 1e12
         line = {
             "metric": METRIC,
             "value": total_pts / (ms_max / 1e3),
@@ -401,7 +405,17 @@ def main():
                          "frac": round(attn_tf / tflops, 4), **_ncu_traffic(),
                          "peak_source": src,
                          "flops_per_step": attn_flops, "ms_per_step": round(attn_ms, 4),
-                         "note": "dh=24 (padded 32): exp/MUFU-bound, see DESIGN.md"},
+                         "note": "dh=24 (padded 32): exp/MUFU-bound, see roofline_exp and DESIGN.md"},
+            # the roof that actually binds at dh = 24: one exp2 per score on the
+            # MUFU unit (16/clk/SM; 3 in 4 of them there, 1 in 4 on the FMA pipe)
+            "roofline_exp": {"kernel": attn_name, "bound": "mufu", "achieved": round(exp_ach, 3),
+                             "peak": round(exp_peak, 3), "unit": "T exp/s",
+                             "frac": round(exp_ach / exp_peak, 4),
+                             "scores_per_step": n_scores,
+                             "note": "algorithmic scores (sum over scopes of m^2 x heads) / attention "
+                                     "time vs 16 MUFU ex2 per clk per SM x 148 SMs at the sampled "
+                                     "SM clock; a quarter of the exponentials run on the FMA pipe, "
+                                     "so frac can exceed the pure-MUFU share"},
             "rooflines": {
                 "psh (f3d_voxel_hash+f3d_psh_assign)": {"bound": "hbm", "achieved": round(psh_gbs, 1),
                                                         "peak": hbm, "unit": "GB/s",

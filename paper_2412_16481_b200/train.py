@@ -64,30 +64,48 @@ def scope_index(plan, n: int):
     return idx, slen[live].astype(np.int32)
 
 
-class _RoundIndex:
-    """Per-(scope, head) gather/scatter indices of one round over the
-    (n*H, dh) head-row view: bh[b*M + i] = row(scope b//H, i)*H + b%H.  Pad
-    entries (i >= len) point at row 0 — their scores are zeroed by
-    f3d_softmax_bwd, so they never reach a gradient — and are dropped on the
-    scatter back."""
+class _ScopeGroup:
+    """Scopes of similar length padded to a common M (a multiple of 16):
+    per-(scope, head) gather/scatter indices over the (n*H, dh) head-row view,
+    bh[b*M + i] = row(scope b//H, i)*H + b%H.  Pad entries (i >= len) point at
+    row 0 -- their scores are zeroed by f3d_softmax_bwd, so they never reach a
+    gradient -- and are dropped on the scatter back (dummy head row n*3H)."""
 
-    def __init__(self, plan, n, H, dev):
-        idx, lens = scope_index(plan, n)
+    def __init__(self, idx, lens, n, H, dev):
         self.ns, self.M = idx.shape
         valid = idx < n
         idx = np.where(valid, idx, 0)
         bh = (idx[:, None, :] * H + np.arange(H)[None, :, None]).reshape(-1)
         vbh = np.broadcast_to(valid[:, None, :], (self.ns, H, self.M)).reshape(-1)
-        self.bh = torch.from_numpy(bh).to(dev)
-        self.bh32 = self.bh.to(torch.int32)
-        if int(vbh.sum()) != n * H:
-            raise ConfigError("the round's scopes do not cover every row exactly once")
-        # scatter targets into the (n, 3, H, dh) = (n, 3d) dq|dk|dv layout;
-        # pads land on the dummy head row n*3H
-        r, h = bh // H, bh % H
+        self.nvalid = int(vbh.sum())
+        self.bh32 = torch.from_numpy(bh.astype(np.int32)).to(dev)
+        r, h = bh // H, bh % H        # targets in the (n, 3, H, dh) = (n, 3d) dq|dk|dv layout
         self.dest = [torch.from_numpy(np.where(vbh, r * 3 * H + i * H + h, n * 3 * H)
                                       .astype(np.int32)).to(dev) for i in range(3)]
         self.len_bh = torch.from_numpy(np.repeat(lens, H)).to(dev)      # b = scope*H + h
+
+
+class _RoundIndex:
+    """One round's scopes in length groups: sorted by length and cut where the
+    length falls below kRatio of the group's longest, so the padded M x M
+    score tiles stay close to the real m x m work (one padded batch over all
+    scopes of a config-B round wasted ~70 %)."""
+
+    kRatio = 0.8
+
+    def __init__(self, plan, n, H, dev):
+        idx, lens = scope_index(plan, n)
+        order = np.argsort(-lens, kind="stable")
+        groups, start = [], 0
+        for k in range(1, len(order) + 1):
+            if k == len(order) or lens[order[k]] < self.kRatio * lens[order[start]]:
+                sel = order[start:k]
+                M = -(-int(lens[sel[0]]) // 16) * 16
+                groups.append(_ScopeGroup(idx[sel, :M], lens[sel], n, H, dev))
+                start = k
+        self.groups = groups
+        if sum(g.nvalid for g in groups) != n * H:
+            raise ConfigError("the round's scopes do not cover every row exactly once")
 
 
 class DeviceWeights:
@@ -185,40 +203,42 @@ class StageTrainer:
         da (fp32).  bf16 tensor-core GEMMs with fp32 outputs; P and dS are
         rounded to bf16 as GEMM operands (as the forward kernel rounds P)."""
         n, d, H, dh = self.n, self.d, self.H, self.dh
-        ns, M, B = ix.ns, ix.M, ix.ns * H
         bf = torch.bfloat16
-
-        def gather(src):            # src (n*H, w) head rows -> (B*M, w), f3d_gather_rows
-            t = torch.empty((B * M, src.shape[1]), dtype=src.dtype, device=src.device)
-            L.call("f3d_gather_rows", L.ptr(src), L.ptr(ix.bh32), B * M,
-                   src.shape[1] * src.element_size(), L.ptr(t), None, L.stream())
-            return t
-
-        Q, K, V = (gather(qkv[:, i * d:(i + 1) * d].contiguous().view(n * H, dh)).view(B, M, dh)
-                   for i in range(3))
-        dO = gather(da.to(bf).view(n * H, dh)).view(B, M, dh)
-        lse_b = gather(lse.reshape(n * H, 1)).view(B, M)
+        heads = [qkv[:, i * d:(i + 1) * d].contiguous().view(n * H, dh) for i in range(3)]
+        heads.append(da.to(bf).view(n * H, dh))
+        lse_r = lse.reshape(n * H, 1)
         sl2 = 1.4426950408889634 / math.sqrt(dh)
-        S = torch.bmm(Q, K.transpose(1, 2), out_dtype=torch.float32)
-        P = torch.empty((B, M, M), dtype=bf, device=qkv.device)
-        L.call("f3d_softmax_bwd", L.ptr(S), None, L.ptr(lse_b), L.ptr(ix.len_bh), B, M, sl2, 0.0,
-               0, L.ptr(P), L.stream())
-        del S
-        dV = torch.bmm(P.transpose(1, 2), dO, out_dtype=torch.float32)
-        dP = torch.bmm(dO, V.transpose(1, 2), out_dtype=torch.float32)
-        dS = torch.empty_like(P)
-        # D = sum_j P dP per row inside the kernel (same bf16 P as dS uses)
-        L.call("f3d_softmax_bwd", L.ptr(dP), L.ptr(P), None, L.ptr(ix.len_bh), B, M, sl2,
-               1.0 / math.sqrt(dh), 1, L.ptr(dS), L.stream())
-        del dP, P
-        dQ = torch.bmm(dS, K, out_dtype=torch.float32)
-        dK = torch.bmm(dS.transpose(1, 2), Q, out_dtype=torch.float32)
         out = torch.empty((n * 3 * H + 1, dh), dtype=torch.float32, device=qkv.device)
-        for i, t in enumerate((dQ, dK, dV)):
-            L.call("f3d_scatter_rows", L.ptr(t), L.ptr(ix.dest[i]), B * M, dh * 4, L.ptr(out),
-                   None, L.stream())
-        out = out[:n * 3 * H].view(n, 3 * d)
-        return out
+        for gp in ix.groups:
+            ns, M = gp.ns, gp.M
+            B = ns * H
+
+            def gather(src):        # src (n*H, w) head rows -> (B*M, w), f3d_gather_rows
+                t = torch.empty((B * M, src.shape[1]), dtype=src.dtype, device=src.device)
+                L.call("f3d_gather_rows", L.ptr(src), L.ptr(gp.bh32), B * M,
+                       src.shape[1] * src.element_size(), L.ptr(t), None, L.stream())
+                return t
+
+            Q, K, V, dO = (gather(t).view(B, M, dh) for t in heads)
+            lse_b = gather(lse_r).view(B, M)
+            S = torch.bmm(Q, K.transpose(1, 2), out_dtype=torch.float32)
+            P = torch.empty((B, M, M), dtype=bf, device=qkv.device)
+            L.call("f3d_softmax_bwd", L.ptr(S), None, L.ptr(lse_b), L.ptr(gp.len_bh), B, M, sl2,
+                   0.0, 0, L.ptr(P), L.stream())
+            del S
+            dV = torch.bmm(P.transpose(1, 2), dO, out_dtype=torch.float32)
+            dP = torch.bmm(dO, V.transpose(1, 2), out_dtype=torch.float32)
+            dS = torch.empty_like(P)
+            # D = sum_j P dP per row inside the kernel (same bf16 P as dS uses)
+            L.call("f3d_softmax_bwd", L.ptr(dP), L.ptr(P), None, L.ptr(gp.len_bh), B, M, sl2,
+                   1.0 / math.sqrt(dh), 1, L.ptr(dS), L.stream())
+            del dP, P
+            dQ = torch.bmm(dS, K, out_dtype=torch.float32)
+            dK = torch.bmm(dS.transpose(1, 2), Q, out_dtype=torch.float32)
+            for i, t in enumerate((dQ, dK, dV)):
+                L.call("f3d_scatter_rows", L.ptr(t), L.ptr(gp.dest[i]), B * M, dh * 4,
+                       L.ptr(out), None, L.stream())
+        return out[:n * 3 * H].view(n, 3 * d)
 
     def _ln_bwd(self, x, dy, gain, dres, dgain, dbeta):
         dx = torch.empty_like(x)

@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--profile", action="store_true", help="print the top kernels of one step")
     ap.add_argument("--stage0-only", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture each scene's forward + backward as one CUDA graph")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -62,13 +64,41 @@ def main():
         trainers.append(BackboneTrainer(C, stages, params, weights=wts))
         feats.append(X)
 
+    def scene_step(tr, X):
+        out = tr.forward(X)
+        loss = 0.5 * (out * out).mean()
+        _, gs = tr.backward(out / out.numel())
+        return loss, gs
+
+    graphs = None
+    if a.graph:
+        # static per-scene graphs: inputs/weights are resident, the grads and
+        # loss are the graph's static outputs (allocations from the graph pool)
+        graphs = []
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for tr, X in zip(trainers, feats):
+                scene_step(tr, X)                       # warm-up on the side stream
+        torch.cuda.current_stream().wait_stream(side)
+        for tr, X in zip(trainers, feats):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                loss, gs = scene_step(tr, X)
+            graphs.append((g, loss, gs))
+
     def step():
         acc, loss = [None] * len(stages), 0.0
-        for tr, X in zip(trainers, feats):
-            out = tr.forward(X)
-            loss = loss + 0.5 * (out * out).mean()
-            _, gs = tr.backward(out / out.numel())
-            acc = [accumulate_grads(x, g) for x, g in zip(acc, gs)]
+        if graphs is not None:
+            for g, l, gs in graphs:
+                g.replay()
+                loss = loss + l
+                acc = [accumulate_grads(x, gg) for x, gg in zip(acc, gs)]
+        else:
+            for tr, X in zip(trainers, feats):
+                l, gs = scene_step(tr, X)
+                loss = loss + l
+                acc = [accumulate_grads(x, g) for x, g in zip(acc, gs)]
         for w, g in zip(wts, acc):
             w.sgd(allreduce_grads(g), 1e-3)
         return loss
@@ -97,7 +127,8 @@ def main():
         pts = a.scenes * a.points * world
         print(json.dumps({"workload": ("config E, stage 0 only" if a.stage0_only else
                                        "config E, 2-stage B-recipe backbone") +
-                                      ": fwd+bwd+allreduce+SGD",
+                                      ": fwd+bwd+allreduce+SGD" +
+                                      (" (CUDA graph per scene)" if a.graph else ""),
                           "n_gpus": world, "scenes_per_gpu": a.scenes, "points_per_scene": a.points,
                           "ms_per_step": round(float(ms.item()), 3),
                           "train_points_per_s": pts / (float(ms.item()) * 1e-3),
