@@ -108,21 +108,11 @@ __host__ __device__ constexpr int poly_every() {
 }
 
 
-// 2^x on the FMA/ALU pipes for x <= 2^8 (softmax arguments): round x to
+// 2^x of a packed pair on the FMA/ALU pipes for x <= 2^8 (softmax arguments): round x to
 // j = rint(x) with the 1.5*2^23 trick, 2^f for f in [-0.5, 0.5] by a cubic
 // (relative error <= 8e-4, below the bf16 rounding of P), exponent added
 // as an integer.  Arguments below -127 flush to 0 like ex2.approx.ftz.
-__device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -127.f);
-    const float t = __fadd_rn(x, 12582912.f);
-    const float f = __fsub_rn(x, __fsub_rn(t, 12582912.f));
-    float p = fmaf(0.0555041086648216f, f, 0.2402264923172690f);
-    p = fmaf(p, f, 0.6931471805599453f);
-    p = fmaf(p, f, 1.f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
-// ex2_poly on a packed pair: the rounding trick and the cubic run as f32x2.
+// The rounding trick and the cubic run as f32x2.
 __device__ __forceinline__ void ex2_poly2(uint64_t a, float& p0, float& p1) {
     float x0, x1;
     f2_split(a, x0, x1);

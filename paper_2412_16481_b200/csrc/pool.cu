@@ -85,20 +85,6 @@ __device__ __forceinline__ bool closer(double d2, int j, double b2, int bj) {
     return s < bs || (s == bs && j < bj);
 }
 
-// lexicographic (d, id) minimum across the warp; returns the winning id
-__device__ __forceinline__ int warp_argmin(double d, int id) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double d2 = __shfl_xor_sync(0xffffffffu, d, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, id, o);
-        if (d2 < d || (d2 == d && i2 < id)) {
-            d = d2;
-            id = i2;
-        }
-    }
-    return id;
-}
-
 __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     extern __shared__ __align__(16) unsigned char pool_smem[];
     WarpSmem* smem_all = reinterpret_cast<WarpSmem*>(pool_smem);
