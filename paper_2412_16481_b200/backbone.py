@@ -348,17 +348,22 @@ class Backbone:
 
         for i, (ch, fh) in enumerate(scenes):
             sl = slots[i % 2]
-            finish(sl)                                   # step i-2 read back + checked
+            # everything of step i is enqueued before the host blocks on step
+            # i-2's read-back, so the upload of step i overlaps step i-1's
+            # compute even when the PCIe copies are slower than a step
             if i >= 2:
-                h2d.wait_event(sl["ev_done"])            # its inputs are free
+                h2d.wait_event(sl["ev_done"])            # step i-2's inputs are free
             with torch.cuda.stream(h2d):
                 sl["coords"].copy_(ch, non_blocking=True)
                 sl["feats"].copy_(fh, non_blocking=True)
                 sl["ev_in"].record(h2d)
             compute.wait_event(sl["ev_in"])
+            if i >= 2:
+                compute.wait_event(sl["ev_out"])         # step i-2's outputs read out
             sl["g0"].replay()
             sl["g1"].replay()
             sl["ev_done"].record(compute)
+            finish(sl)                                   # step i-2 read back + checked
             d2h.wait_event(sl["ev_done"])
             with torch.cuda.stream(d2h):
                 sl["out_h"].copy_(sl["out_bf16"], non_blocking=True)
