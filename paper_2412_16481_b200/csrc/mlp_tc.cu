@@ -418,6 +418,9 @@ int launch(const Args& A, cudaStream_t st) {
 //     packed-pair GELU, bf16, 16-byte stores of the row; the quarter's TMEM is
 //     released after its last load, so the next tile's MMA overlaps the tail.
 namespace gg {
+#ifndef F3D_GG_NOGELU
+#define F3D_GG_NOGELU 0    // A/B only: bias epilogue without the GELU
+#endif
 #ifndef F3D_GG_PARTS
 #define F3D_GG_PARTS 4
 #endif
@@ -573,8 +576,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_gelu_kernel(const Args A) {
 #pragma unroll
                 for (int e = 0; e < CW; e += 2) {
                     const float2 bb = *reinterpret_cast<const float2*>(bq + cc + e);
+#if F3D_GG_NOGELU
+                    const float2 g = make_float2(__uint_as_float(v[e]) + bb.x,
+                                                 __uint_as_float(v[e + 1]) + bb.y);
+#else
                     const float2 g = gelu2(__uint_as_float(v[e]) + bb.x,
                                            __uint_as_float(v[e + 1]) + bb.y);
+#endif
                     __nv_bfloat162 h2 = __floats2bfloat162_rn(g.x, g.y);
                     pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
