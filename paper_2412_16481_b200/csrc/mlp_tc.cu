@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstring>
 #include <cfloat>
 
 #include "f3d_common.cuh"
@@ -460,8 +461,22 @@ struct Args {
     int64_t ldu;
 };
 
+#ifndef F3D_GG_TMA
+#define F3D_GG_TMA 1       // x tiles by TMA (SW64 K-major); 0: cp.async core-matrix tiles
+#endif
+// SW64 K-major operand: 32-column blocks of 64-byte swizzled rows (R rows per
+// block); byte offset of 16-byte chunk c of row r
+template <int R>
+__device__ __forceinline__ uint32_t sw64_off(int r, int c) {
+    const int b = c >> 2, cc = c & 3;
+    uint32_t o = (uint32_t)(r * 64 + cc * 16);
+    o ^= ((o >> 7) & 3) << 4;
+    return (uint32_t)(b * R * 64) + o;
+}
+
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) gemm_gelu_kernel(const Args A) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_gelu_kernel(const Args A,
+                                                                const __grid_constant__ CUtensorMap xmap) {
     using C = Cfg<D>;
     constexpr int H = C::H, QP = C::QP;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -478,13 +493,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_gelu_kernel(const Args A) {
 
     for (int i = tid; i < H * (D / 8); i += kThreads) {
         const int r = i / (D / 8), c = i - r * (D / 8);
-        *reinterpret_cast<uint4*>(smem + C::kOffW + core_off<D>(r, c)) =
+#if F3D_GG_TMA
+        const uint32_t wo = sw64_off<H>(r, c);
+#else
+        const uint32_t wo = core_off<D>(r, c);
+#endif
+        *reinterpret_cast<uint4*>(smem + C::kOffW + wo) =
             __ldg(reinterpret_cast<const uint4*>(A.w_in_t + (int64_t)r * D) + c);
     }
     for (int i = tid; i < H; i += kThreads) s_b[i] = A.b_in[i];
     if (tid == 0) {
         for (int b = 0; b < kNX; ++b) {
-            mbar_init(x_full + b, 32);
+            mbar_init(x_full + b, F3D_GG_TMA ? 1 : 32);
             mbar_init(x_empty + b, 1);
         }
         for (int q = 0; q < kQ; ++q) {
@@ -511,6 +531,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_gelu_kernel(const Args A) {
             mbar_wait(x_empty + b, ((it / kNX) & 1) ^ 1);
             const uint32_t dst = sm_base + C::kOffX + b * C::kXBytes;
             const int64_t r0 = (int64_t)tile * kBM;
+#if F3D_GG_TMA
+            if (lane == 0) {           // three 32-column boxes; rows past n zero-filled
+                mbar_arrive_expect(x_full + b, C::kXBytes);
+#pragma unroll
+                for (int blk = 0; blk < D / 32; ++blk)
+                    tma_2d(dst + blk * kBM * 64, &xmap, x_full + b, blk * 32, (int)r0);
+            }
+            __syncwarp();
+#else
             for (int i = lane; i < kBM * (D / 8); i += 32) {
                 const int r = i / (D / 8), c = i - r * (D / 8);
                 const bool ok = r0 + r < n;
@@ -518,13 +547,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_gelu_kernel(const Args A) {
                 cp_async16z(dst + core_off<D>(r, c), src, ok);
             }
             cp_async_arrive(x_full + b);
+#endif
         }
     } else if (warp == 1) {
         constexpr uint32_t id = idesc_bf16(kBM, QP, 0, 0);
+#if F3D_GG_TMA
+        // SW64 K-major: SBO = 8 rows x 64 B; K-step k = block k/2, +32 B inside it
+        const uint64_t dW = sw_desc(sm_base + C::kOffW, 16, 512, 4);
+        const uint64_t dX = sw_desc(sm_base + C::kOffX, 16, 512, 4);
+        constexpr uint32_t kXD = C::kXBytes >> 4;
+        constexpr uint32_t kQD = (QP * 64) >> 4;             // W_in^T rows [q*QP, ...)
+        auto xk = [](int k) { return (uint32_t)(((k >> 1) * kBM * 64 + (k & 1) * 32) >> 4); };
+        auto wk = [](int k) { return (uint32_t)(((k >> 1) * H * 64 + (k & 1) * 32) >> 4); };
+#else
         const uint64_t dW = smem_desc(sm_base + C::kOffW, 128, 16 * D);
         const uint64_t dX = smem_desc(sm_base + C::kOffX, 128, 16 * D);
         constexpr uint32_t kXD = C::kXBytes >> 4;
         constexpr uint32_t kQD = ((QP / 8) * 16 * D) >> 4;   // W_in^T rows [q*QP, ...)
+        auto xk = [](int k) { return (uint32_t)(16 * k); };
+        auto wk = [](int k) { return (uint32_t)(16 * k); };
+#endif
         int it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const int b = it % kNX;
@@ -538,8 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_gelu_kernel(const Args A) {
                 if (elect_one()) {
 #pragma unroll
                     for (int k = 0; k < D / 16; ++k)
-                        umma_f16(tmem + q * QP, dx + (uint64_t)(16 * k),
-                                 dW + (uint64_t)(q * kQD + 16 * k), id, k > 0);
+                        umma_f16(tmem + q * QP, dx + (uint64_t)xk(k),
+                                 dW + (uint64_t)(q * kQD + wk(k)), id, k > 0);
                     umma_commit(d_full + q);
                 }
                 __syncwarp();
@@ -624,9 +666,17 @@ int launch(const Args& A, cudaStream_t st) {
                                           C::kSmem));
         attr = true;
     }
+    CUtensorMap xmap;
+    memset(&xmap, 0, sizeof(xmap));
+#if F3D_GG_TMA
+    if (!make_map(&xmap, A.x, A.ldx, D, A.n, 32, 64, kBM)) {
+        f3d_set_last_cuda_error(cudaErrorNotSupported);   // no cuTensorMapEncodeTiled
+        return F3D_ERR_CUDA;
+    }
+#endif
     const int64_t tiles = (A.n + kBM - 1) / kBM;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, f3d_num_sms()));
-    kern<<<grid, kThreads, C::kSmem, st>>>(A);
+    kern<<<grid, kThreads, C::kSmem, st>>>(A, xmap);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
