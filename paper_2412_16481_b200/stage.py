@@ -31,6 +31,11 @@ LN_EPS = 1e-12
 # cuBLAS GEMMs + f3d_bias_gelu + f3d_row_ln.  Opt-in: measured 0.46 vs 0.39 ms
 # per config-B step (tools/mlp_ab.py)
 FUSED_MLP = os.environ.get("F3D_FUSED_MLP", "0") == "1"
+# F3D_GEMM_LN=1 selects f3d_gemm_ln (projection + residual + LayerNorm (+PE) in
+# one tcgen05 kernel) over cuBLAS GEMMs + f3d_row_ln.  Opt-in: measured 1.37 vs
+# 1.22 ms per config-B step -- one CTA per SM leaves the row epilogue with too
+# few loads in flight
+GEMM_LN = os.environ.get("F3D_GEMM_LN", "0") == "1"
 # The MLP's first half: f3d_gemm_gelu (TMA-fed tcgen05 GEMM, bias + GELU
 # epilogue from TMEM, u written once) instead of cuBLAS GEMM + f3d_bias_gelu
 # (tools/gemm_gelu_bench.py, d = 96: 27 vs 30 us at 50K rows, 50 vs 52 at 100K,

@@ -81,8 +81,19 @@ def test_training_forward_matches_inference_stage():
     n = sf.shape[0]
     X = torch.tensor(sf, dtype=torch.float32, device="cuda")
     out = StageTrainer(sc, table, sched, p, n).forward(X)
+    # the training forward keeps the pre-GELU activations, so it runs the
+    # cuBLAS GEMM + f3d_bias_gelu split: against the same kernels it agrees to
+    # 1e-3, against the default fused f3d_gemm_gelu stage to bf16 tolerance
+    from paper_2412_16481_b200 import stage as ST
+    old = ST.GEMM_GELU
+    try:
+        ST.GEMM_GELU = False
+        ref_split = F.stage_forward(X, sc, a, sched, p)
+    finally:
+        ST.GEMM_GELU = old
     ref = F.stage_forward(X, sc, a, sched, p)
-    assert rel(out.cpu().numpy(), ref.cpu().numpy()) < 1e-3
+    assert rel(out.cpu().numpy(), ref_split.cpu().numpy()) < 1e-3
+    assert rel(out.cpu().numpy(), ref.cpu().numpy()) < STAGE_TOL
 
 
 def test_sgd_steps_reduce_loss():
