@@ -212,8 +212,9 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     // id is still under-filled.  Eligibility only shrinks during step 3, so a
     // choice whose id is still eligible at commit time is exactly the
     // sequential answer (the minimum over a superset that lies in the
-    // subset); the first stale choice ends the pass and the rest of the batch
-    // is re-speculated against the updated sizes (each pass commits >= 1 row).
+    // subset); a stale choice is recomputed for that row alone (warp-parallel
+    // over the still-eligible ids of the pass's tier) and committing goes on;
+    // only an exhausted tier ends the pass and rebuilds the list.
     for (int q0 = 0; q0 < nqueue;) {
         // eligible ids of this pass: under-filled new ids, else any under-filled
         int ne = 0;
@@ -261,11 +262,40 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
                 done = nqueue;
                 break;
             }
-            if (S.sizes[jj] >= rho) break;   // stale: re-speculate from here
+            int pick = jj;
+            if (S.sizes[jj] >= rho) {
+                // stale: this row alone, warp-parallel over the pass's eligible
+                // ids that are still under-filled (same tier: the list only
+                // shrinks; an exhausted tier ends the pass and rebuilds it)
+                const int i = S.qrow[q0 + done];
+                const double ci[3] = {S.cc[i][0], S.cc[i][1], S.cc[i][2]};
+                double bd2 = DBL_MAX;
+                int bid = INT_MAX;
+                for (int e = lane; e < ne; e += 32) {
+                    const int j = S.elig[e];
+                    if (S.sizes[j] >= rho) continue;
+                    const double d2 = dist2(S.sc[j], ci);
+                    if (closer(d2, j, bd2, bid)) {
+                        bd2 = d2;
+                        bid = j;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double d2 = __shfl_xor_sync(0xffffffffu, bd2, o);
+                    const int j = __shfl_xor_sync(0xffffffffu, bid, o);
+                    if (j != INT_MAX && (bid == INT_MAX || closer(d2, j, bd2, bid))) {
+                        bd2 = d2;
+                        bid = j;
+                    }
+                }
+                if (bid == INT_MAX) break;   // tier exhausted: rebuild the list
+                pick = bid;
+            }
             __syncwarp();
             if (lane == 0) {
-                S.sub[S.qrow[q0 + done]] = (int16_t)jj;
-                S.sizes[jj] = (int16_t)(S.sizes[jj] + 1);
+                S.sub[S.qrow[q0 + done]] = (int16_t)pick;
+                S.sizes[pick] = (int16_t)(S.sizes[pick] + 1);
             }
             __syncwarp();
         }
