@@ -33,9 +33,18 @@ namespace psh {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kPerLane = 8;
-constexpr int kWarpSpan = 32 * kPerLane;      // 256 points per warp
-constexpr int kTile = kWarps * kWarpSpan;     // 2048 points per tile
+// Points per lane (PL) is a kernel template parameter: tiles of kWarps*32*PL
+// points.  Small scenes want small tiles (more CTAs in the latency-bound
+// sweeps: config B 100K points 53 -> 43 us with PL = 2), large ones large
+// tiles (config D 1M points 172 us with PL = 8 vs 269 with PL = 2).
+constexpr int kPerLaneSmall = 2, kPerLaneLarge = 8;
+constexpr int64_t kSmallTileMaxN = 300000;   // n below this: PL = 2
+template <int PL> struct TileC {
+    static constexpr int kPerLane = PL;
+    static constexpr int kWarpSpan = 32 * PL;
+    static constexpr int kTile = kWarps * 32 * PL;
+};
+constexpr int kTileMin = kWarps * 32 * kPerLaneSmall;   // workspace sizing (most tiles)
 constexpr int kMaxBins = 12288;               // smem histogram limit (8 * 12288 * 2 B)
 constexpr int kMaxProbes = 128;
 constexpr int kScanU = 4;
@@ -76,6 +85,7 @@ __device__ __forceinline__ void zero_hist(uint16_t* h, int words32) {
 }
 
 // Count this warp's keys into its private u16 row (keys < 0 ignored).
+template <int kPerLane>
 __device__ __forceinline__ void warp_count(const int (&key)[kPerLane], uint16_t* row) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -89,6 +99,7 @@ __device__ __forceinline__ void warp_count(const int (&key)[kPerLane], uint16_t*
 
 // Stable rank of each key within the tile, given row = exclusive prefix of
 // this warp's keys over earlier warps of the tile.
+template <int kPerLane>
 __device__ __forceinline__ void warp_rank(const int (&key)[kPerLane], uint16_t* row,
                                           int (&rank)[kPerLane]) {
     const int lane = threadIdx.x & 31;
@@ -188,6 +199,7 @@ struct TileInfo {
     int p0, p1, b;
 };
 
+template <int kTile>
 __device__ __forceinline__ TileInfo tile_info(const Params& P_, bool multi, int t, int n) {
     TileInfo ti;
     if (multi) {
@@ -230,7 +242,11 @@ __device__ void sequential_batch(const Params& P_, int b, int pb0, int pb1, int3
 
 // --------------------------------------------------------------- the kernel
 
+template <int PL>
 __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
+    constexpr int kPerLane = TileC<PL>::kPerLane;
+    constexpr int kWarpSpan = TileC<PL>::kWarpSpan;
+    constexpr int kTile = TileC<PL>::kTile;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) uint16_t sh[];
     __shared__ int8_t probe[kMaxProbes * 3];
@@ -350,7 +366,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
         // Phase A: decide + per-tile histogram
         int changed = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const TileInfo ti = tile_info(P_, multi, t, n);
+            const TileInfo ti = tile_info<kTile>(P_, multi, t, n);
             zero_hist(sh, hwords);
             __syncthreads();
             int key[kPerLane];
@@ -420,7 +436,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
         grid.sync();
         // Phase C: in-tile stable ranks -> offsets; S-th taker -> T
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const TileInfo ti = tile_info(P_, multi, t, n);
+            const TileInfo ti = tile_info<kTile>(P_, multi, t, n);
             zero_hist(sh, hwords);
             __syncthreads();
             int key[kPerLane];
@@ -499,7 +515,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     }
     grid.sync();
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const TileInfo ti = tile_info(P_, multi, t, n);
+        const TileInfo ti = tile_info<kTile>(P_, multi, t, n);
         const int32_t* bb = P_.base + (int64_t)ti.b * W;
         for (int p = ti.p0 + tid; p < ti.p1; p += kThreads) {
             const int i = multi ? __ldcg(P_.orig + p) : p;
@@ -520,7 +536,7 @@ static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static WsLayout layout(int64_t n, int32_t nbatch, int32_t K, int max_sweeps) {
     WsLayout L;
-    const int64_t max_tiles = n / kTile + nbatch + 1;
+    const int64_t max_tiles = n / kTileMin + nbatch + 1;
     const int64_t nslots = (int64_t)nbatch * (K + 1);
     const int64_t nbins = nbatch > 1 ? std::max<int64_t>(K + 1, nbatch) : (K + 1);
     size_t o = 0;
@@ -643,7 +659,10 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
     p.btile = (int32_t*)(w + L.btile);
     p.bstart = (int32_t*)(w + L.bstart);
     p.flags = (int32_t*)(w + L.flags);
-    p.max_tiles = (int)(n / psh::kTile + nbatch + 1);
+    const bool small = n < psh::kSmallTileMaxN;
+    const int tile = small ? psh::TileC<psh::kPerLaneSmall>::kTile
+                           : psh::TileC<psh::kPerLaneLarge>::kTile;
+    p.max_tiles = (int)(n / tile + nbatch + 1);
 
     F3D_CUDA_TRY(f3d_zero_i32(info_out, 4, st));
     const int nbins = nbatch > 1 ? std::max(K + 1, nbatch) : K + 1;
@@ -654,15 +673,15 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
     }
     const int stride = (nbins + 1) & ~1;
     const size_t smem = (size_t)psh::kWarps * stride * sizeof(uint16_t);
-    static int attr_smem = 0;
-    if ((int)smem > 48 * 1024 && (int)smem > attr_smem) {
-        F3D_CUDA_TRY(cudaFuncSetAttribute(psh::psh_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_smem = (int)smem;
+    auto kern = small ? psh::psh_kernel<psh::kPerLaneSmall> : psh::psh_kernel<psh::kPerLaneLarge>;
+    static int attr_smem[2] = {0, 0};
+    if ((int)smem > 48 * 1024 && (int)smem > attr_smem[small]) {
+        F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        attr_smem[small] = (int)smem;
     }
     int per_sm = 0;
-    F3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, psh::psh_kernel,
-                                                               psh::kThreads, smem));
+    F3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, psh::kThreads, smem));
     if (per_sm < 1) return F3D_ERR_CONFIG;
     const int max_tiles = p.max_tiles;
     int grid = std::min(per_sm * f3d_num_sms(), max_tiles);
@@ -671,7 +690,7 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
     grid = std::max(grid, std::min(col_ctas, per_sm * f3d_num_sms()));
     grid = std::max(grid, 1);
     void* args[] = {(void*)&p};
-    F3D_CUDA_TRY(cudaLaunchCooperativeKernel((void*)psh::psh_kernel, dim3(grid),
-                                             dim3(psh::kThreads), args, smem, st));
+    F3D_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(psh::kThreads), args,
+                                             smem, st));
     return F3D_OK;
 }
