@@ -442,7 +442,10 @@ static bool launch_row_ln_vec(cudaStream_t st, void* F, int64_t ldf, const void*
     if (d % 4 || d > 128 || ldf % 4 || !al(F, 16)) return false;
     if (y && (ldy % 4 || !al(y, 8) || (ybias && !al(ybias, 16)))) return false;
     if (out && (ldo % 4 || !al(out, 8) || !al(gain, 16) || !al(beta, 16))) return false;
-    constexpr int RPW = 4;
+#ifndef F3D_LN_RPW
+#define F3D_LN_RPW 4
+#endif
+    constexpr int RPW = F3D_LN_RPW;
     const unsigned g = (unsigned)((n + RPW * 8 - 1) / (RPW * 8));
     using BF = __nv_bfloat16;
     float* Ff = (float*)F;
