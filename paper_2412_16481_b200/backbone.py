@@ -130,27 +130,16 @@ class Backbone:
                                    "batch": None, "dest": dest, "info": info})
         return a, stats, info
 
-    def _stage_body(self, r: _StageRun, C, X):
-        """Scatter -> R rounds -> (pool) for one stage whose bucketing is in
-        r.asg.  Returns the next stage's (X, C, n_cap, n_dev)."""
+    def _stage_prologue(self, r: _StageRun, C):
+        """Coordinate-only setup of a bucketed stage: scattered coordinates,
+        the device scope plans of every round and the stage runner (buffers,
+        coordinate bounding box).  Sets r.Cs, r.plans, r.runner."""
         cfg, si, n, n_dev = r.cfg, r.si, r.n_cap, r.n_dev
         a = r.asg
-        with record_function(f"stage{si}.scatter"):
-            dest = a._dev["dest"]
-            d = X.shape[1]
-            F = torch.empty((n, d), dtype=torch.float32, device=C.device)
-            Cs = torch.empty((n, 3), dtype=torch.float64, device=C.device)
-            if X.dtype == torch.bfloat16 and d % 8 == 0 and X.is_contiguous():
-                # bf16 upload -> fp32 residual stream in the scatter itself
-                L.call("f3d_scatter_rows_bf16_f32", L.ptr(X), X.stride(0), L.ptr(dest), n, d,
-                       L.ptr(F), F.stride(0), L.ptr(n_dev), L.stream())
-            else:
-                Xf = (X if X.dtype == torch.float32 else X.to(torch.float32)).contiguous()
-                L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F),
-                       L.ptr(n_dev), L.stream())
-            L.call("f3d_scatter_rows", L.ptr(C), L.ptr(dest), n, 24, L.ptr(Cs), L.ptr(n_dev),
-                   L.stream())
         with record_function(f"stage{si}.plan"):
+            Cs = torch.empty((n, 3), dtype=torch.float64, device=C.device)
+            L.call("f3d_scatter_rows", L.ptr(C), L.ptr(a._dev["dest"]), n, 24, L.ptr(Cs),
+                   L.ptr(n_dev), L.stream())
             nb_cap = cfg.K + -(-n // cfg.S)
             if cfg.W > nb_cap:
                 raise ConfigError(f"window_w ({cfg.W}) exceeds num_buckets ({nb_cap})")
@@ -160,30 +149,66 @@ class Backbone:
                                                  cfg.shift, cfg.rounds, n, qstep=qs)
             r.runner = StageRunner(Cs, None, None, self.params[si], n, torch.float32,
                                    weights=self._w[si], plans=r.plans, n_dev=n_dev)
+            r.Cs = Cs
+
+    @staticmethod
+    def _stage_tensors(r: _StageRun):
+        """Every device tensor a prepared stage owns (for record_stream)."""
+        out = [r.Cs, r.stats, r.info] + [v for v in r.asg._dev.values()
+                                         if isinstance(v, torch.Tensor)]
+        for p in r.plans:
+            out += [v for v in vars(p).values() if isinstance(v, torch.Tensor)]
+        out += [v for v in vars(r.runner).values() if isinstance(v, torch.Tensor)]
+        return out
+
+    def _stage_body(self, r: _StageRun, C, X):
+        """Scatter -> R rounds -> (pool) for one stage whose bucketing is in
+        r.asg (and whose prologue may already be enqueued).  Returns the next
+        stage's (X, C, n_cap, n_dev)."""
+        cfg, si, n, n_dev = r.cfg, r.si, r.n_cap, r.n_dev
+        a = r.asg
+        if getattr(r, "runner", None) is None:
+            self._stage_prologue(r, C)
+        Cs = r.Cs
+        with record_function(f"stage{si}.scatter"):
+            dest = a._dev["dest"]
+            d = X.shape[1]
+            F = torch.empty((n, d), dtype=torch.float32, device=C.device)
+            if X.dtype == torch.bfloat16 and d % 8 == 0 and X.is_contiguous():
+                # bf16 upload -> fp32 residual stream in the scatter itself
+                L.call("f3d_scatter_rows_bf16_f32", L.ptr(X), X.stride(0), L.ptr(dest), n, d,
+                       L.ptr(F), F.stride(0), L.ptr(n_dev), L.stream())
+            else:
+                Xf = (X if X.dtype == torch.float32 else X.to(torch.float32)).contiguous()
+                L.call("f3d_scatter_rows", L.ptr(Xf), L.ptr(dest), n, d * 4, L.ptr(F),
+                       L.ptr(n_dev), L.stream())
         pool_ev = None
         if cfg.pool_rho and POOL_OVERLAP:
-            # the pooling partition needs only the scattered coordinates: build
-            # it on a side stream under the stage's transformer rounds
+            # the pooling partition, the pooled centroids and the whole
+            # coordinate-only prologue of the next stage (PSH bucketing,
+            # scattered coordinates, plans, runner) run on a side stream under
+            # this stage's transformer rounds
             main = torch.cuda.current_stream()
             side = self._pool_stream = getattr(self, "_pool_stream", None) or torch.cuda.Stream()
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 pool_parts = self._pool_partition(cfg, n, a, Cs)
                 keep = [t for t in pool_parts if isinstance(t, torch.Tensor)]
-                if si + 1 < len(self.stages):         # the next stage's bucketing too
+                if si + 1 < len(self.stages):
                     ncfg = self.stages[si + 1]
                     _, _, totals_, np_cap_, _, Cn_ = pool_parts
-                    r.next_bucket = self.bucketize(Cn_, ncfg, np_cap_, totals_[1:2])
-                    asg_, stats_, info_ = r.next_bucket
-                    keep += [stats_, info_] + [v for v in asg_._dev.values()
-                                               if isinstance(v, torch.Tensor)]
+                    nr = _StageRun(si + 1, ncfg, np_cap_, totals_[1:2])
+                    nr.asg, nr.stats, nr.info = self.bucketize(Cn_, ncfg, np_cap_, totals_[1:2])
+                    self._stage_prologue(nr, Cn_)
+                    keep += self._stage_tensors(nr)
+                    r.next_run = nr
                 pool_ev = torch.cuda.Event()
                 pool_ev.record(side)
             for t in keep:
                 t.record_stream(main)
         with record_function(f"stage{si}.run"):
             r.runner.run(F)
-        r.F, r.Cs = F, Cs
+        r.F = F
         if not cfg.pool_rho:
             return F, Cs, n, n_dev
         with record_function(f"stage{si}.pool"):
@@ -230,9 +255,9 @@ class Backbone:
             cfg = self.stages[si]
             r = _StageRun(si, cfg, n_cap, n_dev)
             prev = runs[-1]
-            if getattr(prev, "next_bucket", None) is not None:
-                r.asg, r.stats, r.info = prev.next_bucket     # done on the side stream
-                prev.next_bucket = None
+            if getattr(prev, "next_run", None) is not None:
+                r = prev.next_run                             # prepared on the side stream
+                prev.next_run = None
             else:
                 with record_function(f"stage{si}.bucketize"):
                     r.asg, r.stats, r.info = self.bucketize(C, cfg, n_cap, n_dev)
