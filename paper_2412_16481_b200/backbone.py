@@ -241,10 +241,13 @@ class Backbone:
         return members, sizes, totals, np_cap, flags, Cn
 
     def _enqueue_bucketize0(self, C):
+        """Stage-0 work that needs only the coordinates: PSH bucketing and the
+        stage prologue (graph g0; the feature upload overlaps it)."""
         cfg = self.stages[0]
         r = _StageRun(0, cfg, C.shape[0], None)
         with record_function("stage0.bucketize"):
             r.asg, r.stats, r.info = self.bucketize(C, cfg)
+        self._stage_prologue(r, C)
         return r
 
     def _enqueue_rest(self, r0: _StageRun, C, X):
@@ -343,7 +346,7 @@ class Backbone:
     # ------------------------------------------------------------ graphs
     def _capture_slot(self, n, feat_dtype):
         """Two CUDA graphs over private static buffers: g0 = stage-0
-        bucketing (reads only the coordinates), g1 = the rest."""
+        bucketing + prologue (reads only the coordinates), g1 = the rest."""
         dev = L.device()
         d = self.stages[0].d_model
         coords = torch.zeros((n, 3), dtype=torch.float64, device=dev)
