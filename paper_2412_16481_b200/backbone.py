@@ -401,7 +401,7 @@ class Backbone:
         if slots is None or slots[0]["n"] != n or slots[0]["feats"].dtype != dt:
             slots = self._slots = [self._capture_slot(n, dt) for _ in range(2)]
             for sl in slots:
-                for k in ("ev_in", "ev_done", "ev_out"):
+                for k in ("ev_c", "ev_in", "ev_done", "ev_out"):
                     sl[k] = torch.cuda.Event()
                 sl["pending"] = None
         if not hasattr(self, "_h2d"):
@@ -428,12 +428,14 @@ class Backbone:
                 h2d.wait_event(sl["ev_done"])            # step i-2's inputs are free
             with torch.cuda.stream(h2d):
                 sl["coords"].copy_(ch, non_blocking=True)
+                sl["ev_c"].record(h2d)                   # g0 needs the coordinates only
                 sl["feats"].copy_(fh, non_blocking=True)
                 sl["ev_in"].record(h2d)
-            compute.wait_event(sl["ev_in"])
+            compute.wait_event(sl["ev_c"])
             if i >= 2:
                 compute.wait_event(sl["ev_out"])         # step i-2's outputs read out
             sl["g0"].replay()
+            compute.wait_event(sl["ev_in"])
             sl["g1"].replay()
             sl["ev_done"].record(compute)
             finish(sl)                                   # step i-2 read back + checked
