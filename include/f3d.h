@@ -271,6 +271,17 @@ int f3d_pool_reduce(const void *x, int dtype, int64_t ldx, int d, const int32_t 
                     const int32_t *sizes, int64_t npool, int rho, int op, void *out,
                     int64_t ldo, const int32_t *npool_dev, void *stream);
 
+/* Positional encoding of (bounding-box normalised) coordinates as bf16 rows,
+ * with f3d_row_ln's fp32 arithmetic (bw/attention.py:271-288); and the
+ * vector row_ln that adds such a precomputed table instead of evaluating
+ * sin/cos (F += y + ybias when y; out = LN(F)*gain + beta + pe_tab[row]).
+ * d % 12 == 0, d <= 128. */
+int f3d_pe_table(const double *coords, const double *lo_ext, double pe_base, int64_t n, int d,
+                 void *out_bf16, int64_t ldo, void *stream);
+int f3d_row_ln_pt(float *F, int64_t ldf, const void *y, int64_t ldy, const float *ybias,
+                  const float *gain, const float *beta, const void *pe_tab, int64_t ldp, void *out,
+                  int64_t ldo, int64_t n, int d, double eps, void *stream);
+
 /* u = GELU(x W_in + b_in) as bf16 rows (n x 4d): tcgen05 GEMM with the
  * bias + exact-erf GELU epilogue read from TMEM (replaces a library GEMM +
  * f3d_bias_gelu; bw/stage.py:153-156).  w_in_t = W_in^T (4d x d, row-major

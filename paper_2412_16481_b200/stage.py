@@ -40,6 +40,11 @@ GEMM_LN = os.environ.get("F3D_GEMM_LN", "0") == "1"
 # epilogue from TMEM, u written once) instead of cuBLAS GEMM + f3d_bias_gelu
 # (tools/gemm_gelu_bench.py, d = 96: 27 vs 30 us at 50K rows, 50 vs 52 at 100K,
 # 144 vs 184 at 400K, 321 vs 422 at 1M).  F3D_GEMM_GELU=0 selects the cuBLAS path.
+# F3D_PE_TABLE=1: the positional encoding is computed once per stage into a bf16
+# table (coordinate-only, part of the overlapped prologue) and row_ln adds it.
+# Opt-in: measured 1.117 vs 1.103 ms per config-B step (the stage-0 table sits on
+# the critical path and the table reads cost about what the sin/cos saved)
+PE_TABLE = os.environ.get("F3D_PE_TABLE", "0") == "1"
 _GG = os.environ.get("F3D_GEMM_GELU")
 GEMM_GELU = _GG != "0"
 GEMM_GELU_MIN_ROWS = 0
@@ -176,6 +181,11 @@ class StageRunner:
                           and self.w.get("w_in_t") is not None
                           and bool(L.load().f3d_mlp_supported(d)))
         self.u = None if self.fused_mlp else L.empty((n, dhid), torch.bfloat16)
+        self.pe_tab = None
+        if PE_TABLE and f_dtype == torch.float32 and d % 12 == 0 and d <= 128:
+            self.pe_tab = L.empty((n, d), torch.bfloat16)
+            L.call("f3d_pe_table", L.ptr(self.coords), L.ptr(self.lo_ext), 10000.0, n, d,
+                   L.ptr(self.pe_tab), d, L.stream())
         lib = L.load()
         self.gemm_ln = (GEMM_LN and not self.fused_mlp and dhid == 4 * d
                         and self.w.get("w_o_t") is not None
@@ -187,6 +197,12 @@ class StageRunner:
                           and bool(L.load().f3d_gemm_gelu_supported(d)))
 
     def _row_ln(self, F, y, ybias, g, b, pe, out):
+        if pe and self.pe_tab is not None and F.dtype == torch.float32 and out is not None:
+            L.call("f3d_row_ln_pt", L.ptr(F), F.stride(0), L.ptr(y),
+                   0 if y is None else y.stride(0), L.ptr(ybias), L.ptr(g), L.ptr(b),
+                   L.ptr(self.pe_tab), self.pe_tab.stride(0), L.ptr(out), out.stride(0), self.n,
+                   self.d, LN_EPS, L.stream())
+            return
         L.call("f3d_row_ln", L.ptr(F), int(F.dtype == torch.float64), F.stride(0), L.ptr(y),
                0 if y is None else y.stride(0), L.ptr(ybias), L.ptr(g), L.ptr(b),
                L.ptr(self.coords) if pe else None, L.ptr(self.lo_ext) if pe else None, 10000.0,
