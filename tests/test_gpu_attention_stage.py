@@ -357,3 +357,26 @@ def test_stage_gemm_ln_matches_cublas_path():
         ST.GEMM_LN = old
     rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
     assert rr < 1e-2, rr
+
+
+def test_stage_pe_table_matches_computed_pe():
+    """The opt-in bf16 PE table path (f3d_pe_table + f3d_row_ln_pt) against the
+    default in-kernel PE (bf16 rounding of the table only)."""
+    import torch
+
+    from paper_2412_16481_b200 import stage as ST
+    a, sf, sc = _config_a(n=3000, d=96)
+    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
+    p = F.init_params(0, 96, n_heads=4)
+    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
+    C = torch.tensor(sc, device="cuda")
+    old = ST.PE_TABLE
+    try:
+        ST.PE_TABLE = False
+        ref = F.stage_forward(X, C, a, sched, p)
+        ST.PE_TABLE = True
+        out = F.stage_forward(X, C, a, sched, p)
+    finally:
+        ST.PE_TABLE = old
+    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
+    assert rr < 1e-2, rr
