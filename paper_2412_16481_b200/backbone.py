@@ -36,6 +36,13 @@ from .stage import StageRunner, init_params
 # the stage's transformer rounds (config B: 1.16 -> 1.12 ms per step for the
 # partition alone).  F3D_POOL_OVERLAP=0 keeps them on the main stream.
 POOL_OVERLAP = os.environ.get("F3D_POOL_OVERLAP", "1") == "1"
+# stream_host runs step i+1's coordinate-only graph g0 on its own stream under
+# step i's g1, gated on an external event recorded after g1's cooperative
+# stage-1 PSH (two cooperative PSH grids in flight at once corrupted results):
+# e2e 1.17 -> 1.10 ms per step.  F3D_G0_CONCURRENT=0 keeps the steps serial.
+# F3D_NEXT_PROLOGUE_SIDE=0 keeps the next stage's PSH/prologue on the main stream.
+G0_CONCURRENT = os.environ.get("F3D_G0_CONCURRENT", "1") == "1"
+NEXT_PROLOGUE_SIDE = os.environ.get("F3D_NEXT_PROLOGUE_SIDE", "1") == "1"
 
 
 @dataclass(frozen=True)
@@ -194,11 +201,16 @@ class Backbone:
             with torch.cuda.stream(side):
                 pool_parts = self._pool_partition(cfg, n, a, Cs)
                 keep = [t for t in pool_parts if isinstance(t, torch.Tensor)]
-                if si + 1 < len(self.stages):
+                if si + 1 < len(self.stages) and NEXT_PROLOGUE_SIDE:
                     ncfg = self.stages[si + 1]
                     _, _, totals_, np_cap_, _, Cn_ = pool_parts
                     nr = _StageRun(si + 1, ncfg, np_cap_, totals_[1:2])
                     nr.asg, nr.stats, nr.info = self.bucketize(Cn_, ncfg, np_cap_, totals_[1:2])
+                    # an external event (a graph event-record node when captured):
+                    # stream_host keeps the next scene's cooperative stage-0 PSH
+                    # from running while this cooperative PSH is in flight
+                    r.psh_event = torch.cuda.Event(external=True)
+                    r.psh_event.record(side)
                     self._stage_prologue(nr, Cn_)
                     keep += self._stage_tensors(nr)
                     r.next_run = nr
@@ -390,8 +402,10 @@ class Backbone:
         """Pipelined end-to-end forward over a sequence of host scenes
         ``[(coords_h (n,3) f64, feats_h (n,d) bf16), ...]`` (pinned, equal n).
         Two graph slots alternate: step i's upload runs on an H2D stream
-        while step i-1 computes, and step i-1's read-back (last-stage bf16
-        features + status words) runs on a D2H stream under step i's compute.
+        while step i-1 computes, step i's coordinate-only graph g0 runs on its
+        own stream under step i-1's g1 (after step i-1's cooperative stage-1
+        PSH), and step i-1's read-back (last-stage bf16 features + status
+        words) runs on a D2H stream under step i's compute.
         ``on_result(i, feats_host_view, n_out)`` is called in step order once a
         step's read-back landed (the view is reused two steps later); a step's
         errors are raised then, before its slot is reused."""
@@ -401,13 +415,14 @@ class Backbone:
         if slots is None or slots[0]["n"] != n or slots[0]["feats"].dtype != dt:
             slots = self._slots = [self._capture_slot(n, dt) for _ in range(2)]
             for sl in slots:
-                for k in ("ev_c", "ev_in", "ev_done", "ev_out"):
+                for k in ("ev_c", "ev_in", "ev_g0", "ev_done", "ev_out"):
                     sl[k] = torch.cuda.Event()
                 sl["pending"] = None
         if not hasattr(self, "_h2d"):
             self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+            self._g0s = torch.cuda.Stream()
         compute = torch.cuda.current_stream()
-        h2d, d2h = self._h2d, self._d2h
+        h2d, d2h, g0s = self._h2d, self._d2h, self._g0s
 
         def finish(sl):
             i = sl["pending"]
@@ -431,10 +446,25 @@ class Backbone:
                 sl["ev_c"].record(h2d)                   # g0 needs the coordinates only
                 sl["feats"].copy_(fh, non_blocking=True)
                 sl["ev_in"].record(h2d)
-            compute.wait_event(sl["ev_c"])
+            if G0_CONCURRENT:
+                # g0 (coordinate-only) on its own stream, under step i-1's g1
+                g0s.wait_event(sl["ev_c"])
+                if i >= 2:
+                    g0s.wait_event(sl["ev_done"])        # step i-2 done with the slot
+                if i >= 1:                                # not under step i-1's cooperative PSH
+                    pev = getattr(slots[(i - 1) % 2]["runs"][0], "psh_event", None)
+                    if pev is not None:
+                        g0s.wait_event(pev)
+                with torch.cuda.stream(g0s):
+                    sl["g0"].replay()
+                    sl["ev_g0"].record(g0s)
+                compute.wait_event(sl["ev_g0"])
+            else:
+                compute.wait_event(sl["ev_c"])
             if i >= 2:
                 compute.wait_event(sl["ev_out"])         # step i-2's outputs read out
-            sl["g0"].replay()
+            if not G0_CONCURRENT:
+                sl["g0"].replay()
             compute.wait_event(sl["ev_in"])
             sl["g1"].replay()
             sl["ev_done"].record(compute)

@@ -133,11 +133,13 @@ def test_stream_host_pipelined_matches_single_calls():
                          dtype=torch.bfloat16).pin_memory()
         scenes.append((c, f))
     got = {}
-    bb.stream_host(scenes, on_result=lambda i, out, n_out: got.__setitem__(i, out.clone()))
-    assert sorted(got) == [0, 1, 2]
-    for i, (c, f) in enumerate(scenes):
-        ref, n_ref = bb.forward_host(c, f)
-        assert got[i].shape[0] == n_ref and torch.equal(got[i], ref)
+    seq = scenes * 3                     # 9 steps: slot reuse + concurrent g0 under g1
+    bb.stream_host(seq, on_result=lambda i, out, n_out: got.__setitem__(i, out.clone()))
+    assert sorted(got) == list(range(len(seq)))
+    single = Backbone(stages)
+    for i, (c, f) in enumerate(seq):
+        ref, n_ref = single.forward_host(c, f)
+        assert got[i].shape[0] == n_ref and torch.equal(got[i], ref), i
 
 
 def test_backbone_recycle_heavy_matches_oracle():
