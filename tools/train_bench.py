@@ -40,8 +40,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--profile", action="store_true", help="print the top kernels of one step")
     ap.add_argument("--stage0-only", action="store_true")
-    ap.add_argument("--graph", action="store_true",
-                    help="capture each scene's forward + backward as one CUDA graph")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="eager per-scene steps instead of one CUDA graph per scene")
     a = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
