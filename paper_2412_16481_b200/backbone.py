@@ -451,10 +451,11 @@ class Backbone:
                 g0s.wait_event(sl["ev_c"])
                 if i >= 2:
                     g0s.wait_event(sl["ev_done"])        # step i-2 done with the slot
-                if i >= 1:                                # not under step i-1's cooperative PSH
-                    pev = getattr(slots[(i - 1) % 2]["runs"][0], "psh_event", None)
-                    if pev is not None:
-                        g0s.wait_event(pev)
+                if i >= 1:                                # not under step i-1's cooperative PSHs
+                    for pr in slots[(i - 1) % 2]["runs"]:
+                        pev = getattr(pr, "psh_event", None)
+                        if pev is not None:
+                            g0s.wait_event(pev)
                 with torch.cuda.stream(g0s):
                     sl["g0"].replay()
                     sl["ev_g0"].record(g0s)
