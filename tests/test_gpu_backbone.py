@@ -164,3 +164,26 @@ def test_backbone_recycle_heavy_matches_oracle():
     assert rel < 2e-2, rel
     relg = np.linalg.norm(fg.cpu().numpy().astype(np.float64) - of) / np.linalg.norm(of)
     assert relg < 2e-2, relg
+
+
+def test_stream_host_three_stage_backbone():
+    """Three stages (two pooled levels, two side-branch PSH launches per step):
+    the pipelined path with the next scene's g0 under g1 equals single calls."""
+    n = 20_000
+    stages = (StageConfig(K=64, S=512, S_div=4096, pool_rho=2, seed=0),
+              StageConfig(K=32, S=512, S_div=8192, pool_rho=2, seed=1),
+              StageConfig(K=16, S=512, S_div=16384, pool_rho=0, seed=2))
+    bb = Backbone(stages)
+    scenes = []
+    for seed in (6, 7):
+        c = torch.tensor(O.synth_cloud(seed, n, "uniform-box")).pin_memory()
+        f = torch.tensor(np.random.default_rng(seed).normal(size=(n, 96)),
+                         dtype=torch.bfloat16).pin_memory()
+        scenes.append((c, f))
+    seq = scenes * 3
+    got = {}
+    bb.stream_host(seq, on_result=lambda i, out, n_out: got.__setitem__(i, out.clone()))
+    single = Backbone(stages)
+    for i, (c, f) in enumerate(seq):
+        ref, n_ref = single.forward_host(c, f)
+        assert got[i].shape[0] == n_ref and torch.equal(got[i], ref), i
