@@ -282,6 +282,17 @@ int f3d_row_ln_pt(float *F, int64_t ldf, const void *y, int64_t ldy, const float
                   const float *gain, const float *beta, const void *pe_tab, int64_t ldp, void *out,
                   int64_t ldo, int64_t n, int d, double eps, void *stream);
 
+/* A stage's input scatter fused with its first LayerNorm + PE: row i of src
+ * (bf16, or fp32 when src_is_f32; input order) goes to F[dest[i]] (fp32) and
+ * x[dest[i]] = LN(F)*gain + beta + PE(coords[i]) (bf16) -- bit-identical to
+ * f3d_scatter_rows(_bf16_f32) followed by f3d_row_ln.  d % 12 == 0, d <= 128;
+ * n_dev (nullable): device row count <= n. */
+int f3d_scatter_ln_pe(const void *src, int src_is_f32, int64_t lds, const int32_t *dest,
+                      const double *coords, const double *lo_ext, double pe_base,
+                      const float *gain, const float *beta, float *F, int64_t ldf, void *out_bf16,
+                      int64_t ldo, int64_t n, int d, double eps, const int32_t *n_dev,
+                      void *stream);
+
 /* u = GELU(x W_in + b_in) as bf16 rows (n x 4d): tcgen05 GEMM with the
  * bias + exact-erf GELU epilogue read from TMEM (replaces a library GEMM +
  * f3d_bias_gelu; bw/stage.py:153-156).  w_in_t = W_in^T (4d x d, row-major

@@ -29,7 +29,7 @@ from .bucketing import BucketAssignment, _run_psh, default_probe_schedule
 from .errors import ConfigError
 from .hashing import HashConfig, raise_range
 from .pooling import TILE_CAP, _FLAG_MSGS, _build, _reduce
-from .stage import StageRunner, init_params
+from .stage import LN_EPS, StageRunner, init_params
 
 # The pooling partition, the pooled centroids and the next stage's PSH bucketing
 # depend on the coordinates only: by default they run on a side stream under
@@ -42,6 +42,8 @@ POOL_OVERLAP = os.environ.get("F3D_POOL_OVERLAP", "1") == "1"
 # e2e 1.17 -> 1.10 ms per step.  F3D_G0_CONCURRENT=0 keeps the steps serial.
 # F3D_NEXT_PROLOGUE_SIDE=0 keeps the next stage's PSH/prologue on the main stream.
 G0_CONCURRENT = os.environ.get("F3D_G0_CONCURRENT", "1") == "1"
+# F3D_SCATTER_LN=0: separate input scatter and first row_ln of each stage
+SCATTER_LN = os.environ.get("F3D_SCATTER_LN", "1") == "1"
 NEXT_PROLOGUE_SIDE = os.environ.get("F3D_NEXT_PROLOGUE_SIDE", "1") == "1"
 
 
@@ -177,11 +179,22 @@ class Backbone:
         if getattr(r, "runner", None) is None:
             self._stage_prologue(r, C)
         Cs = r.Cs
+        x_ready = False
         with record_function(f"stage{si}.scatter"):
             dest = a._dev["dest"]
             d = X.shape[1]
             F = torch.empty((n, d), dtype=torch.float32, device=C.device)
-            if X.dtype == torch.bfloat16 and d % 8 == 0 and X.is_contiguous():
+            rn = r.runner
+            if (SCATTER_LN and d % 12 == 0 and d <= 128 and X.is_contiguous()
+                    and X.dtype in (torch.bfloat16, torch.float32)):
+                # scatter + the stage's first LN1 + PE in one pass (bit-identical)
+                w = rn.w
+                L.call("f3d_scatter_ln_pe", L.ptr(X), int(X.dtype == torch.float32), X.stride(0),
+                       L.ptr(dest), L.ptr(C), L.ptr(rn.lo_ext), 10000.0, L.ptr(w["ln1_g"]),
+                       L.ptr(w["ln1_b"]), L.ptr(F), F.stride(0), L.ptr(rn.x), rn.x.stride(0), n,
+                       d, LN_EPS, L.ptr(n_dev), L.stream())
+                x_ready = True
+            elif X.dtype == torch.bfloat16 and d % 8 == 0 and X.is_contiguous():
                 # bf16 upload -> fp32 residual stream in the scatter itself
                 L.call("f3d_scatter_rows_bf16_f32", L.ptr(X), X.stride(0), L.ptr(dest), n, d,
                        L.ptr(F), F.stride(0), L.ptr(n_dev), L.stream())
@@ -219,7 +232,7 @@ class Backbone:
             for t in keep:
                 t.record_stream(main)
         with record_function(f"stage{si}.run"):
-            r.runner.run(F)
+            r.runner.run(F, x_ready=x_ready)
         r.F = F
         if not cfg.pool_rho:
             return F, Cs, n, n_dev

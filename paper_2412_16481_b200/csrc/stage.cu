@@ -480,6 +480,110 @@ __global__ void __launch_bounds__(kThreads) pe_table_kernel(const double* __rest
     }
 }
 
+// Scatter + first LayerNorm + PE of a stage in one pass: input row i (bf16 or
+// fp32, input order) -> F[dest[i]] (fp32) and x[dest[i]] = LN(F)*g + b + PE(C[i])
+// (bf16), with row_ln_vec_kernel's arithmetic (so bit-identical to the scatter
+// followed by f3d_row_ln), saving the re-read of F.
+template <int RPW, typename ST>
+__global__ void __launch_bounds__(kThreads, 4) scatter_ln_pe_kernel(
+    const ST* __restrict__ src, int64_t lds, const int32_t* __restrict__ dest,
+    const double* __restrict__ C, const double* __restrict__ lo_ext, float pl2,
+    const float* __restrict__ gain, const float* __restrict__ beta, float* __restrict__ F,
+    int64_t ldf, __nv_bfloat16* __restrict__ out, int64_t ldo, int64_t n,
+    const int32_t* __restrict__ n_dev, int d, float eps) {
+    const int lane = threadIdx.x & 31;
+    const bool act = lane < (d >> 2);
+    const int64_t nn = dyn_n(n, n_dev);
+    const int64_t row0 = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * RPW;
+    if (row0 >= nn) return;
+    const int c0 = 4 * lane;
+    float4 v[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int64_t row = row0 + i;
+        const bool ok = act && row < nn;
+        if (sizeof(ST) == 2) {
+            if (ok) {
+                const uint2 w = *reinterpret_cast<const uint2*>(
+                    reinterpret_cast<const __nv_bfloat16*>(src) + row * lds + c0);
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+                const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+                v[i] = make_float4(a.x, a.y, b.x, b.y);
+            } else {
+                v[i] = make_float4(0, 0, 0, 0);
+            }
+        } else {
+            v[i] = ok ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src) +
+                                                         row * lds + c0)
+                      : make_float4(0, 0, 0, 0);
+        }
+    }
+    float s[RPW], q[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) s[i] = (v[i].x + v[i].y) + (v[i].z + v[i].w);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+    const float inv_d = 1.f / (float)d;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const float m = s[i] * inv_d;
+        const float a = act ? v[i].x - m : 0.f, b = act ? v[i].y - m : 0.f;
+        const float c = act ? v[i].z - m : 0.f, e = act ? v[i].w - m : 0.f;
+        q[i] = (a * a + b * b) + (c * c + e * e);
+        s[i] = m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
+    if (!act) return;
+    const float4 gg = *reinterpret_cast<const float4*>(gain + c0);
+    const float4 bb = *reinterpret_cast<const float4*>(beta + c0);
+    const int npair = d / 6, blk = 2 * npair;
+    int pa[2];
+    float fq[2], pinv[2];
+    double plo[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int c = c0 + 2 * p;
+        pa[p] = c / blk;
+        const int pj = (c - pa[p] * blk) >> 1;
+        fq[p] = exp2f(-(float)pj / (float)npair * pl2);
+        plo[p] = lo_ext ? lo_ext[pa[p]] : 0.0;
+        pinv[p] = lo_ext ? (float)(1.0 / lo_ext[3 + pa[p]]) : 1.f;
+    }
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int64_t row = row0 + i;
+        if (row >= nn) break;
+        const int64_t dr = __ldg(dest + row);
+        *reinterpret_cast<float4*>(F + dr * ldf + c0) = v[i];
+        const float rstd = rsqrtf(q[i] * inv_d + eps);
+        const float m = s[i];
+        float o0 = (v[i].x - m) * rstd * gg.x + bb.x;
+        float o1 = (v[i].y - m) * rstd * gg.y + bb.y;
+        float o2 = (v[i].z - m) * rstd * gg.z + bb.z;
+        float o3 = (v[i].w - m) * rstd * gg.w + bb.w;
+        float sn[2], cs[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const float xn = (float)__dsub_rn(C[3 * row + pa[p]], plo[p]) * pinv[p];
+            __sincosf(xn * fq[p], &sn[p], &cs[p]);
+        }
+        o0 += sn[0];
+        o1 += cs[0];
+        o2 += sn[1];
+        o3 += cs[1];
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(o0, o1), h1 = __floats2bfloat162_rn(o2, o3);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(out + dr * ldo + c0) = w;
+    }
+}
+
 }  // namespace stage
 }  // namespace f3d
 
@@ -670,6 +774,32 @@ extern "C" int f3d_row_ln_pt(float* F, int64_t ldf, const void* y, int64_t ldy,
         stage::row_ln_vec_kernel<RPW, false, true, false, true><<<g, stage::kThreads, 0, st>>>(
             F, ldf, nullptr, 0, nullptr, gain, beta, nullptr, nullptr, 0.f, (BF*)out, ldo, n, d,
             (float)eps, (const BF*)pe_tab, ldp);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_scatter_ln_pe(const void* src, int src_is_f32, int64_t lds,
+                                 const int32_t* dest, const double* coords, const double* lo_ext,
+                                 double pe_base, const float* gain, const float* beta, float* F,
+                                 int64_t ldf, void* out_bf16, int64_t ldo, int64_t n, int d,
+                                 double eps, const int32_t* n_dev, void* stream) {
+    auto al = [](const void* p, int a) { return ((uintptr_t)p % a) == 0; };
+    if (d % 12 || d > 128 || n < 0 || ldf % 4 || ldo % 4 || lds % 4 || !al(F, 16) ||
+        !al(out_bf16, 8) || !al(gain, 16) || !al(beta, 16) || !al(src, src_is_f32 ? 16 : 8))
+        return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    constexpr int RPW = 4;
+    const unsigned g = (unsigned)((n + RPW * 8 - 1) / (RPW * 8));
+    const float pl2 = (float)log2(pe_base);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (src_is_f32)
+        stage::scatter_ln_pe_kernel<RPW, float><<<g, stage::kThreads, 0, st>>>(
+            (const float*)src, lds, dest, coords, lo_ext, pl2, gain, beta, F, ldf,
+            (__nv_bfloat16*)out_bf16, ldo, n, n_dev, d, (float)eps);
+    else
+        stage::scatter_ln_pe_kernel<RPW, __nv_bfloat16><<<g, stage::kThreads, 0, st>>>(
+            (const __nv_bfloat16*)src, lds, dest, coords, lo_ext, pl2, gain, beta, F, ldf,
+            (__nv_bfloat16*)out_bf16, ldo, n, n_dev, d, (float)eps);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

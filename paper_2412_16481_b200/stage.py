@@ -215,12 +215,14 @@ class StageRunner:
                L.ptr(self.lo_ext) if pe else None, 10000.0, L.ptr(out),
                0 if out is None else out.stride(0), LN_EPS, L.ptr(self.n_dev), L.stream())
 
-    def run(self, F: torch.Tensor) -> torch.Tensor:
+    def run(self, F: torch.Tensor, x_ready: bool = False) -> torch.Tensor:
         """F: (n, d) residual stream on the device (float32/float64), updated
-        in place and returned."""
+        in place and returned.  x_ready: self.x already holds LN1(F) + PE
+        (written by f3d_scatter_ln_pe together with F)."""
         w = self.w
         q, k, v = (self.qkv[:, i * self.d:(i + 1) * self.d] for i in range(3))
-        self._row_ln(F, None, None, w["ln1_g"], w["ln1_b"], True, self.x)
+        if not x_ready:
+            self._row_ln(F, None, None, w["ln1_g"], w["ln1_b"], True, self.x)
         R = len(self.plans)
         for t, plan in enumerate(self.plans):
             torch.addmm(w["b_qkv"], self.x, w["w_qkv"], out=self.qkv)
