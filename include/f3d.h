@@ -282,6 +282,14 @@ int f3d_row_ln_pt(float *F, int64_t ldf, const void *y, int64_t ldy, const float
                   const float *gain, const float *beta, const void *pe_tab, int64_t ldp, void *out,
                   int64_t ldo, int64_t n, int d, double eps, void *stream);
 
+/* f3d_pool_reduce of fp32 rows with the stage's pending residual folded in:
+ * each member row is x + (y + ybias) (y bf16, f3d_row_ln's arithmetic), so the
+ * last residual pass of a pooled stage is skipped.  d % 4 == 0. */
+int f3d_pool_reduce_res(const float *x, int64_t ldx, const void *y_bf16, int64_t ldy,
+                        const float *ybias, int d, const int32_t *members, const int32_t *sizes,
+                        int64_t npool, int rho, int op, float *out, int64_t ldo,
+                        const int32_t *npool_dev, void *stream);
+
 /* A stage's input scatter fused with its first LayerNorm + PE: row i of src
  * (bf16, or fp32 when src_is_f32; input order) goes to F[dest[i]] (fp32) and
  * x[dest[i]] = LN(F)*gain + beta + PE(coords[i]) (bf16) -- bit-identical to

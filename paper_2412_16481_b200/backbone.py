@@ -44,6 +44,8 @@ POOL_OVERLAP = os.environ.get("F3D_POOL_OVERLAP", "1") == "1"
 G0_CONCURRENT = os.environ.get("F3D_G0_CONCURRENT", "1") == "1"
 # F3D_SCATTER_LN=0: separate input scatter and first row_ln of each stage
 SCATTER_LN = os.environ.get("F3D_SCATTER_LN", "1") == "1"
+# F3D_POOL_RESIDUAL=0: a pooled stage's last residual as its own row pass
+POOL_RESIDUAL = os.environ.get("F3D_POOL_RESIDUAL", "1") == "1"
 NEXT_PROLOGUE_SIDE = os.environ.get("F3D_NEXT_PROLOGUE_SIDE", "1") == "1"
 
 
@@ -231,8 +233,12 @@ class Backbone:
                 pool_ev.record(side)
             for t in keep:
                 t.record_stream(main)
+        # a pooled stage's last residual (F += y + b_out) is folded into the
+        # feature pooling (f3d_pool_reduce_res) instead of its own pass over F
+        defer = (cfg.pool_rho and POOL_RESIDUAL and F.dtype == torch.float32 and d % 4 == 0
+                 and not r.runner.gemm_ln and not r.runner.fused_mlp)
         with record_function(f"stage{si}.run"):
-            r.runner.run(F, x_ready=x_ready)
+            r.runner.run(F, x_ready=x_ready, defer_last_residual=defer)
         r.F = F
         if not cfg.pool_rho:
             return F, Cs, n, n_dev
@@ -245,7 +251,14 @@ class Backbone:
                 members, sizes, totals, np_cap, flags, Cn = self._pool_partition(cfg, n, a, Cs)
             r.pool_flags = flags
             r.pool_totals = totals
-            Xn = _reduce(F, members, sizes, np_cap, rho, "mean", npool_dev=totals[1:2])
+            if defer:
+                y = r.runner.y
+                Xn = torch.empty((np_cap, d), dtype=torch.float32, device=F.device)
+                L.call("f3d_pool_reduce_res", L.ptr(F), F.stride(0), L.ptr(y), y.stride(0),
+                       L.ptr(r.runner.w["b_out"]), d, L.ptr(members), L.ptr(sizes), np_cap, rho,
+                       1, L.ptr(Xn), Xn.stride(0), L.ptr(totals[1:2]), L.stream())
+            else:
+                Xn = _reduce(F, members, sizes, np_cap, rho, "mean", npool_dev=totals[1:2])
         return Xn, Cn, np_cap, totals[1:2]
 
     def _pool_partition(self, cfg, n, a, Cs):

@@ -505,7 +505,9 @@ __global__ void pool_reduce4_kernel(const float* __restrict__ x, int64_t ldx, in
                                     const int32_t* __restrict__ members,
                                     const int32_t* __restrict__ sizes, int npool,
                                     const int32_t* npool_dev, int rho, int op,
-                                    float* __restrict__ out, int64_t ldo) {
+                                    float* __restrict__ out, int64_t ldo,
+                                    const __nv_bfloat16* __restrict__ y = nullptr,
+                                    int64_t ldy = 0, const float* __restrict__ yb = nullptr) {
     const int np = (int)dyn_n(npool, npool_dev);
     const uint32_t tot = (uint32_t)np * (uint32_t)d4;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
@@ -513,8 +515,21 @@ __global__ void pool_reduce4_kernel(const float* __restrict__ x, int64_t ldx, in
         const int c = 4 * (int)(t - j * (uint32_t)d4);
         const int32_t* mem = members + (int64_t)j * rho;
         const int sz = sizes[j];
+        const float4 b4 = (y && yb) ? __ldg(reinterpret_cast<const float4*>(yb + c))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        // y: the stage's pending residual, x + (y + b) with f3d_row_ln's ops
         auto X = [&](int r) -> float4 {
-            return __ldg(reinterpret_cast<const float4*>(x + (int64_t)mem[r] * ldx + c));
+            float4 v = __ldg(reinterpret_cast<const float4*>(x + (int64_t)mem[r] * ldx + c));
+            if (y) {
+                const uint2 w = *reinterpret_cast<const uint2*>(y + (int64_t)mem[r] * ldy + c);
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+                const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+                v.x += a.x + b4.x;
+                v.y += a.y + b4.y;
+                v.z += b.x + b4.z;
+                v.w += b.y + b4.w;
+            }
+            return v;
         };
         float4 acc = X(0);
         if (op == R_MIN || op == R_MAX) {
@@ -629,6 +644,25 @@ extern "C" int f3d_pool_parent(const int32_t* members, const int32_t* sizes, int
     const int64_t tot = npool * rho;
     pool_parent_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         members, sizes, npool, npool_dev, rho, parent);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_pool_reduce_res(const float* x, int64_t ldx, const void* y_bf16, int64_t ldy,
+                                   const float* ybias, int d, const int32_t* members,
+                                   const int32_t* sizes, int64_t npool, int rho, int op,
+                                   float* out, int64_t ldo, const int32_t* npool_dev,
+                                   void* stream) {
+    if (d < 4 || d % 4 || rho < 1 || op < 0 || op > 3 || npool < 0 || ldx % 4 || ldo % 4 ||
+        ldy % 4 || (((uintptr_t)x | (uintptr_t)out | (uintptr_t)ybias) & 15) ||
+        ((uintptr_t)y_bf16 & 7) || npool * (d / 4) >= ((int64_t)1 << 31))
+        return F3D_ERR_CONFIG;
+    if (npool == 0) return F3D_OK;
+    int64_t g4 = (npool * (d / 4) + 255) / 256;
+    if (g4 > (int64_t)f3d_num_sms() * 32) g4 = (int64_t)f3d_num_sms() * 32;
+    pool::pool_reduce4_kernel<<<(unsigned)g4, 256, 0, (cudaStream_t)stream>>>(
+        x, ldx, d / 4, members, sizes, (int)npool, npool_dev, rho, op, out, ldo,
+        (const __nv_bfloat16*)y_bf16, ldy, ybias);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

@@ -215,10 +215,13 @@ class StageRunner:
                L.ptr(self.lo_ext) if pe else None, 10000.0, L.ptr(out),
                0 if out is None else out.stride(0), LN_EPS, L.ptr(self.n_dev), L.stream())
 
-    def run(self, F: torch.Tensor, x_ready: bool = False) -> torch.Tensor:
+    def run(self, F: torch.Tensor, x_ready: bool = False,
+            defer_last_residual: bool = False) -> torch.Tensor:
         """F: (n, d) residual stream on the device (float32/float64), updated
         in place and returned.  x_ready: self.x already holds LN1(F) + PE
-        (written by f3d_scatter_ln_pe together with F)."""
+        (written by f3d_scatter_ln_pe together with F).  defer_last_residual:
+        the last round's F += y + b_out is left to the consumer (self.y holds
+        y; f3d_pool_reduce_res folds it into the pooling)."""
         w = self.w
         q, k, v = (self.qkv[:, i * self.d:(i + 1) * self.d] for i in range(3))
         if not x_ready:
@@ -261,7 +264,7 @@ class StageRunner:
             torch.mm(self.u, w["w_out"], out=self.y)
             if t + 1 < R:
                 self._row_ln(F, self.y, w["b_out"], w["ln1_g"], w["ln1_b"], True, self.x)
-            else:
+            elif not defer_last_residual:
                 self._row_ln(F, self.y, w["b_out"], None, None, None, None)
         return F
 
