@@ -282,6 +282,11 @@ int f3d_row_ln_pt(float *F, int64_t ldf, const void *y, int64_t ldy, const float
                   const float *gain, const float *beta, const void *pe_tab, int64_t ldp, void *out,
                   int64_t ldo, int64_t n, int d, double eps, void *stream);
 
+/* A stage's last residual and the bf16 copy of the result in one pass:
+ * F += y + ybias (f3d_row_ln's arithmetic), out = bf16(F).  d % 4 == 0. */
+int f3d_residual_out(float *F, int64_t ldf, const void *y_bf16, int64_t ldy, const float *ybias,
+                     void *out_bf16, int64_t ldo, int64_t n, int d, void *stream);
+
 /* f3d_pool_reduce of fp32 rows with the stage's pending residual folded in:
  * each member row is x + (y + ybias) (y bf16, f3d_row_ln's arithmetic), so the
  * last residual pass of a pooled stage is skipped.  d % 4 == 0. */

@@ -237,8 +237,13 @@ class Backbone:
         # feature pooling (f3d_pool_reduce_res) instead of its own pass over F
         defer = (cfg.pool_rho and POOL_RESIDUAL and F.dtype == torch.float32 and d % 4 == 0
                  and not r.runner.gemm_ln and not r.runner.fused_mlp)
+        r.out_bf16 = None
+        if (getattr(self, "_want_out_bf16", False) and si == len(self.stages) - 1
+                and not cfg.pool_rho and not r.runner.gemm_ln and not r.runner.fused_mlp):
+            # the graphs read the last stage back in bf16: written with its last residual
+            r.out_bf16 = torch.empty((n, d), dtype=torch.bfloat16, device=F.device)
         with record_function(f"stage{si}.run"):
-            r.runner.run(F, x_ready=x_ready, defer_last_residual=defer)
+            r.runner.run(F, x_ready=x_ready, defer_last_residual=defer, out_bf16=r.out_bf16)
         r.F = F
         if not cfg.pool_rho:
             return F, Cs, n, n_dev
@@ -405,9 +410,14 @@ class Backbone:
         with torch.cuda.graph(g0, pool=pool):
             r0 = self._enqueue_bucketize0(coords)
         with torch.cuda.graph(g1, pool=pool):
-            X, Cn, n_dev, runs = self._enqueue_rest(r0, coords, feats)
+            self._want_out_bf16 = True
+            try:
+                X, Cn, n_dev, runs = self._enqueue_rest(r0, coords, feats)
+            finally:
+                self._want_out_bf16 = False
             status = self._status_vector(runs, n_dev)
-            out_bf16 = X.to(torch.bfloat16)
+            out_bf16 = runs[-1].out_bf16 if runs[-1].out_bf16 is not None \
+                else X.to(torch.bfloat16)
         return {"n": n, "g0": g0, "g1": g1, "X": X, "C": Cn, "runs": runs, "status": status,
                 "out_bf16": out_bf16, "side": torch.cuda.Stream(), "coords": coords,
                 "feats": feats,

@@ -584,6 +584,35 @@ __global__ void __launch_bounds__(kThreads, 4) scatter_ln_pe_kernel(
     }
 }
 
+// A stage's last residual fused with the bf16 copy of the result:
+// F += y + b (f3d_row_ln's arithmetic), out = bf16(F); 4 columns per thread.
+__global__ void residual_out_kernel(float* __restrict__ F, int64_t ldf,
+                                    const __nv_bfloat16* __restrict__ y, int64_t ldy,
+                                    const float* __restrict__ yb, __nv_bfloat16* __restrict__ out,
+                                    int64_t ldo, int64_t n, int d4) {
+    const int64_t tot = n * d4;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / d4;
+        const int c = 4 * (int)(t - r * d4);
+        float4 v = *reinterpret_cast<const float4*>(F + r * ldf + c);
+        const uint2 w = *reinterpret_cast<const uint2*>(y + r * ldy + c);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+        const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+        const float4 bb = *reinterpret_cast<const float4*>(yb + c);
+        v.x += a.x + bb.x;
+        v.y += a.y + bb.y;
+        v.z += b.x + bb.z;
+        v.w += b.y + bb.w;
+        *reinterpret_cast<float4*>(F + r * ldf + c) = v;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
+        uint2 o;
+        o.x = *reinterpret_cast<uint32_t*>(&h0);
+        o.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(out + r * ldo + c) = o;
+    }
+}
+
 }  // namespace stage
 }  // namespace f3d
 
@@ -800,6 +829,21 @@ extern "C" int f3d_scatter_ln_pe(const void* src, int src_is_f32, int64_t lds,
         stage::scatter_ln_pe_kernel<RPW, __nv_bfloat16><<<g, stage::kThreads, 0, st>>>(
             (const __nv_bfloat16*)src, lds, dest, coords, lo_ext, pl2, gain, beta, F, ldf,
             (__nv_bfloat16*)out_bf16, ldo, n, n_dev, d, (float)eps);
+    F3D_LAUNCH_CHECK();
+    return F3D_OK;
+}
+
+extern "C" int f3d_residual_out(float* F, int64_t ldf, const void* y_bf16, int64_t ldy,
+                                const float* ybias, void* out_bf16, int64_t ldo, int64_t n, int d,
+                                void* stream) {
+    if (d < 4 || d % 4 || n < 0 || ldf % 4 || ldy % 4 || ldo % 4 ||
+        (((uintptr_t)F | (uintptr_t)ybias) & 15) || (((uintptr_t)y_bf16 | (uintptr_t)out_bf16) & 7))
+        return F3D_ERR_CONFIG;
+    if (n == 0) return F3D_OK;
+    const int64_t tot = n * (d / 4);
+    const unsigned g = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)f3d_num_sms() * 16);
+    stage::residual_out_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(
+        F, ldf, (const __nv_bfloat16*)y_bf16, ldy, ybias, (__nv_bfloat16*)out_bf16, ldo, n, d / 4);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

@@ -216,12 +216,14 @@ class StageRunner:
                0 if out is None else out.stride(0), LN_EPS, L.ptr(self.n_dev), L.stream())
 
     def run(self, F: torch.Tensor, x_ready: bool = False,
-            defer_last_residual: bool = False) -> torch.Tensor:
+            defer_last_residual: bool = False, out_bf16=None) -> torch.Tensor:
         """F: (n, d) residual stream on the device (float32/float64), updated
         in place and returned.  x_ready: self.x already holds LN1(F) + PE
         (written by f3d_scatter_ln_pe together with F).  defer_last_residual:
         the last round's F += y + b_out is left to the consumer (self.y holds
-        y; f3d_pool_reduce_res folds it into the pooling)."""
+        y; f3d_pool_reduce_res folds it into the pooling).  out_bf16: (n, d)
+        bf16 buffer that receives a copy of the final F (same pass as the last
+        residual, f3d_residual_out)."""
         w = self.w
         q, k, v = (self.qkv[:, i * self.d:(i + 1) * self.d] for i in range(3))
         if not x_ready:
@@ -265,7 +267,12 @@ class StageRunner:
             if t + 1 < R:
                 self._row_ln(F, self.y, w["b_out"], w["ln1_g"], w["ln1_b"], True, self.x)
             elif not defer_last_residual:
-                self._row_ln(F, self.y, w["b_out"], None, None, None, None)
+                if out_bf16 is not None and F.dtype == torch.float32:
+                    L.call("f3d_residual_out", L.ptr(F), F.stride(0), L.ptr(self.y),
+                           self.y.stride(0), L.ptr(w["b_out"]), L.ptr(out_bf16),
+                           out_bf16.stride(0), self.n, self.d, L.stream())
+                else:
+                    self._row_ln(F, self.y, w["b_out"], None, None, None, None)
         return F
 
     def attention_flops(self) -> int:
