@@ -187,3 +187,25 @@ def test_stream_host_three_stage_backbone():
     for i, (c, f) in enumerate(seq):
         ref, n_ref = single.forward_host(c, f)
         assert got[i].shape[0] == n_ref and torch.equal(got[i], ref), i
+
+
+def test_stage_boundary_fusions_are_bit_identical():
+    """f3d_scatter_ln_pe (input scatter + first LN1 + PE) and
+    f3d_pool_reduce_res (last residual folded into the pooling) reproduce the
+    unfused scatter / row_ln / pool_reduce sequence bit for bit."""
+    from paper_2412_16481_b200 import backbone as B
+    n = 30_000
+    c = torch.tensor(O.synth_cloud(21, n, "uniform-box"), device="cuda")
+    f = torch.tensor(np.random.default_rng(21).normal(size=(n, 96)), dtype=torch.bfloat16,
+                     device="cuda")
+    stages = (StageConfig(K=64, S=512, S_div=4096, pool_rho=2, seed=0),
+              StageConfig(K=32, S=512, S_div=8192, pool_rho=0, seed=1))
+    old = B.SCATTER_LN, B.POOL_RESIDUAL
+    try:
+        B.SCATTER_LN, B.POOL_RESIDUAL = True, True
+        a, ca = Backbone(stages).forward(c, f)
+        B.SCATTER_LN, B.POOL_RESIDUAL = False, False
+        b, cb = Backbone(stages).forward(c, f)
+    finally:
+        B.SCATTER_LN, B.POOL_RESIDUAL = old
+    assert torch.equal(a, b) and torch.equal(ca, cb)
