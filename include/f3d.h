@@ -275,7 +275,7 @@ int f3d_pool_reduce(const void *x, int dtype, int64_t ldx, int d, const int32_t 
  * with f3d_row_ln's fp32 arithmetic (bw/attention.py:271-288); and the
  * vector row_ln that adds such a precomputed table instead of evaluating
  * sin/cos (F += y + ybias when y; out = LN(F)*gain + beta + pe_tab[row]).
- * d % 12 == 0, d <= 128. */
+ * d % 12 == 0, d <= 128.  Alternative to f3d_row_ln's in-kernel PE (opt-in). */
 int f3d_pe_table(const double *coords, const double *lo_ext, double pe_base, int64_t n, int d,
                  void *out_bf16, int64_t ldo, void *stream);
 int f3d_row_ln_pt(float *F, int64_t ldf, const void *y, int64_t ldy, const float *ybias,
@@ -283,13 +283,15 @@ int f3d_row_ln_pt(float *F, int64_t ldf, const void *y, int64_t ldy, const float
                   int64_t ldo, int64_t n, int d, double eps, void *stream);
 
 /* A stage's last residual and the bf16 copy of the result in one pass:
- * F += y + ybias (f3d_row_ln's arithmetic), out = bf16(F).  d % 4 == 0. */
+ * F += y + ybias (f3d_row_ln's arithmetic), out = bf16(F).  d % 4 == 0.
+ * Replaces the MLP residual of the last round (bw/stage.py:156-158) + a cast. */
 int f3d_residual_out(float *F, int64_t ldf, const void *y_bf16, int64_t ldy, const float *ybias,
                      void *out_bf16, int64_t ldo, int64_t n, int d, void *stream);
 
 /* f3d_pool_reduce of fp32 rows with the stage's pending residual folded in:
  * each member row is x + (y + ybias) (y bf16, f3d_row_ln's arithmetic), so the
- * last residual pass of a pooled stage is skipped.  d % 4 == 0. */
+ * last residual pass of a pooled stage is skipped.  d % 4 == 0.
+ * Replaces bw/stage.py:156-158 (last residual) + bw/pooling.py:166-184 (reduce). */
 int f3d_pool_reduce_res(const float *x, int64_t ldx, const void *y_bf16, int64_t ldy,
                         const float *ybias, int d, const int32_t *members, const int32_t *sizes,
                         int64_t npool, int rho, int op, float *out, int64_t ldo,
@@ -299,7 +301,8 @@ int f3d_pool_reduce_res(const float *x, int64_t ldx, const void *y_bf16, int64_t
  * (bf16, or fp32 when src_is_f32; input order) goes to F[dest[i]] (fp32) and
  * x[dest[i]] = LN(F)*gain + beta + PE(coords[i]) (bf16) -- bit-identical to
  * f3d_scatter_rows(_bf16_f32) followed by f3d_row_ln.  d % 12 == 0, d <= 128;
- * n_dev (nullable): device row count <= n. */
+ * n_dev (nullable): device row count <= n.  Replaces bw/bucketing.py:385-401
+ * (scatter) + bw/stage.py:129-136 (LN1 + PE of the first round). */
 int f3d_scatter_ln_pe(const void *src, int src_is_f32, int64_t lds, const int32_t *dest,
                       const double *coords, const double *lo_ext, double pe_base,
                       const float *gain, const float *beta, float *F, int64_t ldf, void *out_bf16,
