@@ -143,7 +143,9 @@ int f3d_scatter_rows_bf16_f32(const void *src, int64_t ld_src, const int32_t *de
  * and the scope's K/V fit in shared memory).  q/k/v are bf16 rows with head h
  * at columns [h*dh, (h+1)*dh) and row strides ld_*; o is bf16 (out_f32 = 0)
  * or f32 with the same layout, written at the fixed rows.  mask (nullable):
- * per-row uint8 validity; masked keys are excluded, masked queries give 0.
+ * per-row uint8 validity; 0 = masked (excluded as key, query gives 0), 1 = present,
+ * 2 = query only (excluded as key; lets reference_attention take a key set of its
+ * own size, bw/attention.py:147-166).
  * starved (nullable): count of rows with no valid key. */
 int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_q,
                         int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
@@ -283,7 +285,7 @@ int f3d_row_ln_pt(float *F, int64_t ldf, const void *y, int64_t ldy, const float
                   int64_t ldo, int64_t n, int d, double eps, void *stream);
 
 /* A stage's last residual and the bf16 copy of the result in one pass:
- * F += y + ybias (f3d_row_ln's arithmetic), out = bf16(F).  d % 4 == 0.
+ * F += y + ybias (f3d_row_ln's arithmetic; ybias NULL = zero), out = bf16(F).  d % 4 == 0.
  * Replaces the MLP residual of the last round (bw/stage.py:156-158) + a cast. */
 int f3d_residual_out(float *F, int64_t ldf, const void *y_bf16, int64_t ldy, const float *ybias,
                      void *out_bf16, int64_t ldo, int64_t n, int d, void *stream);

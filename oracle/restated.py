@@ -498,7 +498,8 @@ def pool_stage(F, C, counts, base, K, S, nbatch, rho, reduce="mean"):
 
 # ------------------------------------------------------------------ backbone
 
-def backbone_forward(coords, feats, stages, threads=1, scope_limit=None, timings=None):
+def backbone_forward(coords, feats, stages, threads=1, scope_limit=None, timings=None,
+                     record=None):
     """Composition of the restated ops in the order of
     paper_2412_16481_b200/backbone.py (voxelize -> remap -> PSH -> scatter ->
     stage_forward -> pool_stage, per stage).  ``stages`` is a sequence of
@@ -524,10 +525,16 @@ def backbone_forward(coords, feats, stages, threads=1, scope_limit=None, timings
                            timings=st_t)
         t2 = time.perf_counter()
         if cfg.pool_rho:
-            X, C, _, _, _ = pool_stage(Xs, Cs, counts, base, cfg.K, cfg.S, 1, cfg.pool_rho, "mean")
+            X, C, pcounts, _, _ = pool_stage(Xs, Cs, counts, base, cfg.K, cfg.S, 1, cfg.pool_rho,
+                                             "mean")
         else:
-            X, C = Xs, Cs
+            X, C, pcounts = Xs, Cs, None
         t3 = time.perf_counter()
+        if record is not None:
+            # per-stage intermediates for the parity tests
+            record.append({"ids": ids, "offs": offs, "counts": counts, "base": base,
+                           "Cs": Cs, "F": Xs, "pooled_C": C if cfg.pool_rho else None,
+                           "pooled_counts": pcounts})
         if timings is not None:
             nsc = sum(len(r) for r in rounds)
             # attention time extrapolated linearly in the scope count when sampled

@@ -11,8 +11,8 @@ from .attention import (AttentionParams, CopyMeter, ScopeSchedule, build_schedul
                         copy_meter, logical_gather, lowest_period, positional_encoding,
                         reference_attention, tiled_attention)
 from .bucketing import (BucketAssignment, ProbeSchedule, assign_buckets,
-                        assign_buckets_two_stage, compute_bucket_base,
-                        default_probe_schedule, gather, scatter)
+                        assign_buckets_two_stage, claim_slot, compute_bucket_base,
+                        default_probe_schedule, gather, optimistic_race, scatter)
 from .errors import (ConfigError, EmptyInputError, IntegrityError, NumericError,
                      ParseError, RangeError)
 from .geometry import PointCloud, VoxelGrid, synth_cloud, voxelize

@@ -150,9 +150,49 @@ class Probe:
         return out
 
 
+class Recorder:
+    """Optional instrumentation used by bench.py: keeps (name, args) of every
+    entry point called while active (e.g. during a CUDA-graph capture, whose
+    buffers stay alive with the graph), so a family of launches can be
+    re-issued alone -- in its own graph, on one stream -- and timed with CUDA
+    events (``replay_calls``).  The last argument of every entry point that
+    launches work is its stream."""
+
+    active = None
+
+    def __init__(self):
+        self.calls = []
+        # every tensor handed to an entry point while recording stays alive, so
+        # no buffer of a recorded call is reused by a later allocation of the
+        # capture: any family of recorded calls can then be re-issued alone
+        self.keep = []
+
+    def __enter__(self):
+        self._prev, Recorder.active = Recorder.active, self
+        return self
+
+    def __exit__(self, *exc):
+        Recorder.active = self._prev
+
+    def launches(self):
+        return sum(KERNELS_PER_CALL.get(n, 0) for n, _ in self.calls)
+
+
+def replay_calls(calls, stream_ptr):
+    """Re-issue recorded entry-point calls with their stream replaced."""
+    lib = load()
+    for name, args in calls:
+        st = getattr(lib, name)(*args[:-1], stream_ptr)
+        if st != 0:
+            raise RuntimeError(f"replay of {name} failed (status {st})")
+
+
 def call(name, *args):
     """Invoke an f3d_* entry point and map a non-zero status to the
     reference exception classes (bw/errors.py)."""
+    rec = Recorder.active
+    if rec is not None and torch.cuda.is_current_stream_capturing():
+        rec.calls.append((name, args))
     pr = Probe.active
     if pr is not None:
         pr.launches += KERNELS_PER_CALL.get(name, 0)
@@ -186,7 +226,12 @@ def stream():
 
 
 def ptr(t):
-    return None if t is None else _P(t.data_ptr())
+    if t is None:
+        return None
+    rec = Recorder.active
+    if rec is not None:
+        rec.keep.append(t)
+    return _P(t.data_ptr())
 
 
 def is_host(x) -> bool:

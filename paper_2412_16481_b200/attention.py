@@ -455,8 +455,28 @@ def reference_attention(Q, K, V, params: AttentionParams):
     m = q.shape[0]
     qb, kb, vb = (t.to(torch.bfloat16).contiguous() for t in (q, k, v))
     mk = k.shape[0]
+    if v.shape[0] != mk or k.shape[1] != params.d_model or v.shape[1] != params.d_model:
+        raise ConfigError("K and V must share one shape (n_keys, d_model)")
     if mk != m:
-        raise ConfigError("reference_attention on the GPU needs as many keys as queries")
+        # queries and keys of different sizes (the reference einsum takes any):
+        # one scope over [Q rows; K/V rows], the Q rows marked query-only
+        # (mask 2: excluded as keys) and the K/V rows key-only (their outputs
+        # are dropped)
+        if mk == 0:
+            raise ConfigError("reference_attention needs at least one key")
+        T = m + mk
+        d = params.d_model
+        q2 = torch.zeros((T, d), dtype=torch.bfloat16, device=q.device)
+        k2 = torch.zeros_like(q2)
+        v2 = torch.zeros_like(q2)
+        q2[:m], k2[m:], v2[m:] = qb, kb, vb
+        mask = torch.ones(T, dtype=torch.uint8, device=q.device)
+        mask[:m] = 2
+        o2 = torch.zeros((T, d), dtype=torch.float32, device=q.device)
+        starved = torch.zeros(1, dtype=torch.int32, device=q.device)
+        attend(q2, k2, v2, o2, RoundPlan.from_ranges([[(0, T)]], qstep=qstep_for(params.head_dim, True)),
+               params.n_heads, params.head_dim, mask=mask, starved=starved)
+        return L.out(o2[:m].to(torch.float64), host)
     out = torch.zeros((m, params.d_model), dtype=torch.float32, device=q.device)
     attend(qb, kb, vb, out, RoundPlan.from_ranges([[(0, m)]], qstep=qstep_for(params.head_dim)),
            params.n_heads, params.head_dim)

@@ -187,7 +187,8 @@ class Backbone:
             d = X.shape[1]
             F = torch.empty((n, d), dtype=torch.float32, device=C.device)
             rn = r.runner
-            if (SCATTER_LN and d % 12 == 0 and d <= 128 and X.is_contiguous()
+            if (SCATTER_LN and rn.pe_tab is None and d % 12 == 0 and d <= 128
+                    and X.is_contiguous()
                     and X.dtype in (torch.bfloat16, torch.float32)):
                 # scatter + the stage's first LN1 + PE in one pass (bit-identical)
                 w = rn.w
@@ -235,13 +236,20 @@ class Backbone:
                 t.record_stream(main)
         # a pooled stage's last residual (F += y + b_out) is folded into the
         # feature pooling (f3d_pool_reduce_res) instead of its own pass over F
+        # (f3d_pool_reduce_res indexes pooled rows x d/4 columns in 32 bits; larger
+        # pooled capacities keep the residual in the stage and pool F itself)
+        np_cap_ = pool_capacity(n, cfg.K + 1, cfg.pool_rho)[1] if cfg.pool_rho else 0
         defer = (cfg.pool_rho and POOL_RESIDUAL and F.dtype == torch.float32 and d % 4 == 0
+                 and np_cap_ * (d // 4) < 2 ** 31
                  and not r.runner.gemm_ln and not r.runner.fused_mlp)
         r.out_bf16 = None
         if (getattr(self, "_want_out_bf16", False) and si == len(self.stages) - 1
                 and not cfg.pool_rho and not r.runner.gemm_ln and not r.runner.fused_mlp):
             # the graphs read the last stage back in bf16: written with its last residual
             r.out_bf16 = torch.empty((n, d), dtype=torch.bfloat16, device=F.device)
+        hook = getattr(self, "round_hook", None)      # test instrumentation (eager only)
+        r.runner.round_hook = (None if hook is None else
+                               (lambda t, q, k, v, a, _si=si: hook(_si, t, q, k, v, a)))
         with record_function(f"stage{si}.run"):
             r.runner.run(F, x_ready=x_ready, defer_last_residual=defer, out_bf16=r.out_bf16)
         r.F = F
@@ -307,6 +315,10 @@ class Backbone:
             else:
                 with record_function(f"stage{si}.bucketize"):
                     r.asg, r.stats, r.info = self.bucketize(C, cfg, n_cap, n_dev)
+                # every stage>=1 PSH records the event stream_host gates the next
+                # scene's stage-0 PSH on, wherever it runs (here: the main stream)
+                r.psh_event = torch.cuda.Event(external=True)
+                r.psh_event.record(torch.cuda.current_stream())
             runs.append(r)
             X, C, n_cap, n_dev = self._stage_body(r, C, X)
         return X, C, n_dev, runs
@@ -470,6 +482,21 @@ class Backbone:
             if on_result is not None:
                 on_result(i, sl["out_h"][:n_out], n_out)
 
+        def drain():
+            # a previous call that raised may have left a read-back in flight:
+            # wait for it and forget its step index before the slots are reused
+            for sl in slots:
+                if sl["pending"] is not None:
+                    sl["ev_out"].synchronize()
+                    sl["pending"] = None
+
+        drain()
+        try:
+            self._stream_steps(scenes, slots, compute, h2d, d2h, g0s, finish)
+        finally:
+            drain()
+
+    def _stream_steps(self, scenes, slots, compute, h2d, d2h, g0s, finish):
         for i, (ch, fh) in enumerate(scenes):
             sl = slots[i % 2]
             # everything of step i is enqueued before the host blocks on step
@@ -584,11 +611,30 @@ class _CapPlan:
         self.ntiles, self.npool = ntiles, npool
 
 
+_BACKBONES = {}
+
+
 def backbone_forward(coords, feats, stages=None):
-    """Public entry: host or device arrays in; the caller's array type out."""
+    """Public entry: host or device arrays in; the caller's array type out
+    (features float32, coordinates float64, last stage's scattered order).
+    One Backbone per stage configuration is kept, and its forward is captured
+    as CUDA graphs per input size and replayed (``Backbone.forward_graph``), so
+    repeated calls of one size cost one upload, one replay and one read-back."""
     host = L.is_host(coords)
-    C = L.to_dev(coords, torch.float64)
-    X = L.to_dev(feats, torch.float32) if host else feats.to(L.device())
-    bb = Backbone(stages)
-    f, c = bb.forward(C, X)
-    return L.out(f, host), L.out(c, host)
+    key = tuple(stages) if stages is not None else None
+    bb = _BACKBONES.get(key)
+    if bb is None:
+        bb = _BACKBONES[key] = Backbone(stages)
+    if host:
+        C = torch.from_numpy(np.ascontiguousarray(coords, dtype=np.float64)).to(L.device())
+        X = torch.from_numpy(np.ascontiguousarray(feats, dtype=np.float32)).to(L.device())
+    else:
+        C = coords.to(L.device(), torch.float64)
+        X = feats.to(L.device())
+        if X.dtype not in (torch.float32, torch.bfloat16):
+            X = X.to(torch.float32)
+    if C.ndim != 2 or C.shape[1] != 3 or X.ndim != 2 or X.shape[0] != C.shape[0]:
+        raise ConfigError("coords must be (N, 3) and feats (N, d) with matching N")
+    f, c = bb.forward_graph(C.contiguous(), X.contiguous())
+    # the graph's static buffers are overwritten by the next call: copy out
+    return (f.cpu().numpy(), c.cpu().numpy()) if host else (f.clone(), c.clone())

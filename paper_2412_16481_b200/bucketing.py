@@ -356,6 +356,77 @@ def assign_buckets_two_stage(voxels, batch_id, cfg: HashConfig, S: int,
     return _assign(voxels, batch_id, cfg, S, probes)
 
 
+# ------------------------------------------------- claim protocol helpers
+
+def claim_slot(counters, bucket: int, capacity: int, trace=None):
+    """Increment-then-verify claim on one counter (bw/bucketing.py:182-200):
+    the pre-increment value is the claimed offset, valid only when it was
+    below capacity; otherwise the increment is rolled back and None returned.
+    ``counters`` is the caller's host array, mutated in place like the
+    reference's; this is the single-counter protocol step the PSH kernel
+    restates in bulk (csrc/psh.cu), not a hot-path entry point."""
+    prev = int(counters[bucket])
+    counters[bucket] += 1
+    if prev < capacity:
+        if trace is not None:
+            trace.append(("claim", bucket, prev))
+        return prev
+    counters[bucket] -= 1
+    if trace is not None:
+        trace.append(("full", bucket, prev))
+    return None
+
+
+def _probe_candidates(v, cfg: HashConfig, probes: ProbeSchedule):
+    """Hashes of the clamped probe voxels of one point, computed on the GPU in
+    one launch; -1 where a strict '-div' quotient leaves [0, K)
+    (bw/_kernels.py:34-37, 52-58)."""
+    P = min(probes.max_probes, len(probes.offsets))
+    vmax = (1 << cfg.bits_per_axis) - 1
+    cand = np.clip(np.asarray(v, dtype=np.int64)[None, :3] + probes.offsets[:P], 0, vmax)
+    pts = torch.as_tensor(cand, dtype=torch.int64).to(L.device())
+    wrap = HashConfig(cfg.kind, K=cfg.K, S_div=cfg.S_div, bits_per_axis=cfg.bits_per_axis)
+    home, _, _ = hash_device(pts, wrap)
+    h = home.to(torch.int64).cpu().numpy()
+    if cfg.div_overflow == "error" and cfg.kind.endswith("-div"):
+        if cfg.kind.startswith("zorder"):
+            from .hashing import morton_encode
+            code = np.asarray(morton_encode(pts, cfg.bits_per_axis).cpu().numpy())
+        else:
+            code = cand[:, 0] ^ cand[:, 1] ^ cand[:, 2]
+        h = np.where(code // cfg.S_div >= cfg.K, -1, h)
+    return h
+
+
+def optimistic_race(i: int, v, counters, S: int, cfg: HashConfig, probes: ProbeSchedule,
+                    trace=None):
+    """Rebalance one point whose home bucket is full (bw/bucketing.py:203-239):
+    probes nearest first, each claimed with increment / validate / rollback
+    (claim_slot), else the unbounded recycle bucket K.  Returns (bucket,
+    offset) and mutates the caller's host ``counters``.  The candidate hashes
+    come from the GPU hash kernel in one launch."""
+    cands = _probe_candidates(v, cfg, probes)
+    for p, h in enumerate(cands):
+        h = int(h)
+        if h < 0:
+            if trace is not None:
+                trace.append((i, "probe", p, -1, "skipped"))
+            continue
+        if counters[h] < S:
+            off = claim_slot(counters, h, S)
+            if off is not None:
+                if trace is not None:
+                    trace.append((i, "probe", p, h, "claimed"))
+                return h, off
+        if trace is not None:
+            trace.append((i, "probe", p, h, "full"))
+    off = int(counters[cfg.K])
+    counters[cfg.K] += 1
+    if trace is not None:
+        trace.append((i, "recycle", len(cands), cfg.K, "claimed"))
+    return cfg.K, off
+
+
 # ------------------------------------------------------------ row movement
 
 def _rows(features):
@@ -381,8 +452,7 @@ def scatter(features, assignment: BucketAssignment):
     if f.shape[0] != len(assignment):
         raise ConfigError(
             f"features rows ({f.shape[0]}) != assignment size ({len(assignment)})")
-    if assignment._dev is None:
-        assignment.validate()
+    assignment.validate()          # always, as bw/bucketing.py:397
     dest = assignment.dest_device()
     out = torch.empty_like(f)
     rb = _row_bytes(f)

@@ -41,7 +41,8 @@ struct Args {
     const int32_t* scope_len;  // m_s
     const int32_t* work;       // [nwork][2] = (scope, q_start)
     int nwork;
-    const uint8_t* mask;       // optional per-row validity (1 = present)
+    const uint8_t* mask;       // optional per-row validity: 1 = present (key and query);
+                               // 2 = query only (its key/value row is excluded)
     int32_t* starved;          // optional counter of query rows with no valid key
     const int32_t* scope_order;  // non-empty scopes, longest first (resident kernel)
     int nlive;                 // number of non-empty scopes
@@ -196,7 +197,7 @@ __device__ __forceinline__ void warp_tile(const Args& A, const char* kb, const c
             for (int e = 0; e < 4; ++e) {
                 const int key = kbase + nb * 8 + 2 * t + (e & 1);
                 bool ok = key < m;
-                if (kMask && ok) ok = A.mask[phys_row(A, s0, s1, key)] != 0;
+                if (kMask && ok) ok = (A.mask[phys_row(A, s0, s1, key)] & 1) != 0;   // bit 0: key present
                 if (!ok) s[nb][e] = -INFINITY;
             }
         }

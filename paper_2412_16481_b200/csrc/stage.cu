@@ -599,7 +599,8 @@ __global__ void residual_out_kernel(float* __restrict__ F, int64_t ldf,
         const uint2 w = *reinterpret_cast<const uint2*>(y + r * ldy + c);
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
         const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
-        const float4 bb = *reinterpret_cast<const float4*>(yb + c);
+        const float4 bb = yb ? *reinterpret_cast<const float4*>(yb + c)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);   // NULL ybias = zero bias
         v.x += a.x + bb.x;
         v.y += a.y + bb.y;
         v.z += b.x + bb.z;

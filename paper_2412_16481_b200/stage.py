@@ -229,9 +229,14 @@ class StageRunner:
         if not x_ready:
             self._row_ln(F, None, None, w["ln1_g"], w["ln1_b"], True, self.x)
         R = len(self.plans)
+        hook = getattr(self, "round_hook", None)
         for t, plan in enumerate(self.plans):
             torch.addmm(w["b_qkv"], self.x, w["w_qkv"], out=self.qkv)
             attend(q, k, v, self.a, plan, self.H, self.dh)
+            if hook is not None:
+                # test instrumentation (parity on the GPU's own round input):
+                # called at enqueue time with the round's bf16 Q/K/V and output
+                hook(t, q, k, v, self.a)
             if self.gemm_ln and F.dtype == torch.float32:
                 self._gemm_ln(self.a, self.d, w["w_o_t"], w["b_o"], F, w["ln2_g"], w["ln2_b"],
                               False, self.x)

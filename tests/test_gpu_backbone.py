@@ -189,6 +189,53 @@ def test_stream_host_three_stage_backbone():
         assert got[i].shape[0] == n_ref and torch.equal(got[i], ref), i
 
 
+def test_stream_host_unpooled_intermediate_stage():
+    """An unpooled intermediate stage: the next stage's PSH runs on the main
+    stream (no side branch) and records the gating event itself, so the
+    pipelined path with the next scene's g0 under g1 still equals single calls."""
+    n = 16_000
+    stages = (StageConfig(K=64, S=512, S_div=4096, pool_rho=0, seed=0),
+              StageConfig(K=48, S=512, S_div=4096, pool_rho=2, seed=1),
+              StageConfig(K=16, S=512, S_div=16384, pool_rho=0, seed=2))
+    bb = Backbone(stages)
+    scenes = []
+    for seed in (3, 4, 5):
+        c = torch.tensor(O.synth_cloud(seed, n, "surface-shell")).pin_memory()
+        f = torch.tensor(np.random.default_rng(seed).normal(size=(n, 96)),
+                         dtype=torch.bfloat16).pin_memory()
+        scenes.append((c, f))
+    seq = scenes * 3
+    got = {}
+    bb.stream_host(seq, on_result=lambda i, out, n_out: got.__setitem__(i, out.clone()))
+    single = Backbone(stages)
+    for i, (c, f) in enumerate(seq):
+        ref, n_ref = single.forward_host(c, f)
+        assert got[i].shape[0] == n_ref and torch.equal(got[i], ref), i
+
+
+def test_stream_host_recovers_after_error():
+    """A scene that raises inside stream_host leaves no pending read-back
+    behind: the next call on the same slots returns correct results."""
+    from paper_2412_16481_b200.errors import RangeError
+    n = 8_000
+    stages = (StageConfig(K=64, S=512, S_div=4096, pool_rho=2, seed=0),
+              StageConfig(K=32, S=512, S_div=8192, pool_rho=0, seed=1))
+    bb = Backbone(stages)
+    good = torch.tensor(O.synth_cloud(9, n, "uniform-box")).pin_memory()
+    bad = (good * 1e4).pin_memory()          # voxels beyond 2^10 per axis -> RangeError
+    f = torch.tensor(np.random.default_rng(9).normal(size=(n, 96)),
+                     dtype=torch.bfloat16).pin_memory()
+    with pytest.raises(RangeError):
+        bb.stream_host([(good, f), (bad, f), (good, f)])
+    got = {}
+    bb.stream_host([(good, f)] * 3,
+                   on_result=lambda i, out, n_out: got.__setitem__(i, out.clone()))
+    ref, n_ref = Backbone(stages).forward_host(good, f)
+    assert sorted(got) == [0, 1, 2]
+    for i in range(3):
+        assert torch.equal(got[i], ref), i
+
+
 def test_stage_boundary_fusions_are_bit_identical():
     """f3d_scatter_ln_pe (input scatter + first LN1 + PE) and
     f3d_pool_reduce_res (last residual folded into the pooling) reproduce the
