@@ -103,6 +103,22 @@ int f3d_psh_assign(const int32_t *vox32, const int32_t *home, const int32_t *bat
                    int32_t *dest, int32_t *info_out, void *ws, size_t ws_bytes,
                    const int32_t *n_dev, void *stream);
 
+/* Voxelize + per-axis remap + range statistics + home hash + PSH assignment
+ * in one cooperative launch, for one batch (the backbone's per-stage
+ * bucketing): bw/geometry.py:69-72, bw/hashing.py:60-149,
+ * bw/bucketing.py:275-320 and compute_bucket_base (:169-179).  coords: n x 3
+ * float64 (device); outputs as f3d_psh_assign, plus stats_out = the 7 range
+ * words of f3d_voxel_hash (axis minima / maxima of the remapped voxels, the
+ * largest div quotient).  K + 1 <= 12288.  ws: f3d_psh_coords_workspace_size. */
+size_t f3d_psh_coords_workspace_size(int64_t n, int32_t K);
+int f3d_psh_assign_coords(const double *coords, int64_t n, const double *origin3_host,
+                          double voxel_size, int kind, int32_t K, int32_t S, int64_t S_div,
+                          int bits, int strict, const int8_t *probe_offsets_host, int32_t P,
+                          int32_t max_sweeps, int32_t *bucket_id, int32_t *bucket_offset,
+                          int32_t *counts, int32_t *base, int32_t *dest, int32_t *info_out,
+                          int64_t *stats_out, void *ws, size_t ws_bytes, const int32_t *n_dev,
+                          void *stream);
+
 /* ------------------------------------------------- a7: validate()
  * Replaces BucketAssignment.validate (bw/bucketing.py:116-145).
  * flags_out (device int32) receives a bit set: 1 counts sum != n,
@@ -310,6 +326,18 @@ int f3d_scatter_ln_pe(const void *src, int src_is_f32, int64_t lds, const int32_
                       const float *gain, const float *beta, float *F, int64_t ldf, void *out_bf16,
                       int64_t ldo, int64_t n, int d, double eps, const int32_t *n_dev,
                       void *stream);
+
+/* Stage projection GEMM on the tensor cores: y = x W (+ bias) (GELU-erf when
+ * gelu != 0) as bf16 rows, fp32 accumulation in TMEM.  x: n x K bf16 (row
+ * stride ldx), w_t = W^T (N x K row-major bf16), bias: N fp32 (nullable), y:
+ * n x N bf16 (row stride ldy).  The QKV, O-projection and MLP GEMMs of
+ * bw/stage.py:135-138, 146-158.  K % 32 == 0, N % 16 == 0, N <= 4096
+ * (f3d_gemm_supported); 16-byte aligned rows.  n_dev (nullable): device row
+ * count <= n. */
+int f3d_gemm_supported(int K, int N);
+int f3d_gemm(const void *x, int64_t ldx, int64_t n, int K, const void *w_t, int N,
+             const float *bias, int gelu, void *y, int64_t ldy, const int32_t *n_dev,
+             void *stream);
 
 /* u = GELU(x W_in + b_in) as bf16 rows (n x 4d): tcgen05 GEMM with the
  * bias + exact-erf GELU epilogue read from TMEM (replaces a library GEMM +

@@ -40,6 +40,9 @@ SIGNATURES = {
     "f3d_psh_workspace_size": (_SZ, [_I64, _I32, _I32]),
     "f3d_psh_assign": (_INT, [_P, _P, _P, _I64, _I32, _I32, _I32, _INT, _I64, _INT, _INT, _P,
                               _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P]),
+    "f3d_psh_coords_workspace_size": (_SZ, [_I64, _I32]),
+    "f3d_psh_assign_coords": (_INT, [_P, _I64, _P, _F64, _INT, _I32, _I32, _I64, _INT, _INT, _P,
+                                     _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P]),
     "f3d_validate_workspace_size": (_SZ, [_I64, _I64]),
     "f3d_validate_assignment": (_INT, [_P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P]),
     "f3d_scatter_rows": (_INT, [_P, _P, _I64, _I64, _P, _P, _P]),
@@ -73,6 +76,8 @@ SIGNATURES = {
     "f3d_pe_table": (_INT, [_P, _P, _F64, _I64, _INT, _P, _I64, _P]),
     "f3d_row_ln_pt": (_INT, [_P, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _I64, _INT, _F64,
                              _P]),
+    "f3d_gemm_supported": (_INT, [_INT, _INT]),
+    "f3d_gemm": (_INT, [_P, _I64, _I64, _INT, _P, _INT, _P, _INT, _P, _I64, _P, _P]),
     "f3d_gemm_gelu_supported": (_INT, [_INT]),
     "f3d_gemm_gelu": (_INT, [_P, _I64, _I64, _INT, _P, _P, _P, _I64, _P, _P]),
     "f3d_gemm_ln_supported": (_INT, [_INT, _INT]),
@@ -114,11 +119,11 @@ _ERRS = {1: ConfigError, 2: RangeError, 3: IntegrityError, 5: EmptyInputError, 6
 # kernels each entry point launches (for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
     "f3d_voxelize": 1, "f3d_remap_nonnegative": 3, "f3d_hash_bucket": 2, "f3d_morton_encode": 2,
-    "f3d_voxel_hash": 3, "f3d_psh_assign": 2, "f3d_validate_assignment": 5,
+    "f3d_voxel_hash": 3, "f3d_psh_assign": 2, "f3d_psh_assign_coords": 1, "f3d_validate_assignment": 5,
     "f3d_scatter_rows": 1, "f3d_gather_rows": 1, "f3d_scatter_rows_bf16_f32": 1, "f3d_bswin_attention": 1,
     "f3d_bswin_attention_tc": 1,
     "f3d_positional_encoding": 1, "f3d_stage_pe": 1, "f3d_coord_bbox": 2, "f3d_row_ln": 1,
-    "f3d_gelu_f64": 1, "f3d_bias_gelu": 1, "f3d_pool_build": 2, "f3d_pool_reduce": 1, "f3d_pool_parent": 1, "f3d_gemm_gelu": 1, "f3d_gemm_ln": 1, "f3d_pe_table": 1, "f3d_row_ln_pt": 1, "f3d_scatter_ln_pe": 1, "f3d_pool_reduce_res": 1, "f3d_residual_out": 1, "f3d_ln_bwd": 1, "f3d_gelu_bwd": 1, "f3d_colsum": 1,
+    "f3d_gelu_f64": 1, "f3d_bias_gelu": 1, "f3d_pool_build": 2, "f3d_pool_reduce": 1, "f3d_pool_parent": 1, "f3d_gemm_gelu": 1, "f3d_gemm": 1, "f3d_gemm_ln": 1, "f3d_pe_table": 1, "f3d_row_ln_pt": 1, "f3d_scatter_ln_pe": 1, "f3d_pool_reduce_res": 1, "f3d_residual_out": 1, "f3d_ln_bwd": 1, "f3d_gelu_bwd": 1, "f3d_colsum": 1,
     "f3d_softmax_bwd": 1,
     "f3d_plan_round": 1, "f3d_plan_rounds": 1, "f3d_plan_pool": 1, "f3d_mlp_fused": 1,
 }

@@ -25,7 +25,8 @@ from torch.profiler import record_function
 
 from . import _lib as L
 from .attention import DeviceRoundPlan, qstep_for
-from .bucketing import BucketAssignment, _run_psh, default_probe_schedule
+from .bucketing import (DEFAULT_MAX_SWEEPS, BucketAssignment, _run_psh,
+                        default_probe_schedule)
 from .errors import ConfigError
 from .hashing import HashConfig, raise_range
 from .pooling import TILE_CAP, _FLAG_MSGS, _build, _reduce
@@ -47,6 +48,9 @@ SCATTER_LN = os.environ.get("F3D_SCATTER_LN", "1") == "1"
 # F3D_POOL_RESIDUAL=0: a pooled stage's last residual as its own row pass
 POOL_RESIDUAL = os.environ.get("F3D_POOL_RESIDUAL", "1") == "1"
 NEXT_PROLOGUE_SIDE = os.environ.get("F3D_NEXT_PROLOGUE_SIDE", "1") == "1"
+# F3D_FUSED_PSH=0: voxel hash and PSH as separate launches (f3d_voxel_hash +
+# f3d_psh_assign) instead of the one fused cooperative launch
+FUSED_PSH = os.environ.get("F3D_FUSED_PSH", "1") == "1"
 
 
 @dataclass(frozen=True)
@@ -122,10 +126,33 @@ class Backbone:
 
     # ------------------------------------------------------------ pieces
     def bucketize(self, coords, cfg: StageConfig, n_cap=None, n_dev=None):
-        """f3d_voxel_hash + f3d_psh_assign on (n,3) f64 device coords; no
-        read-back.  Returns (assignment, stats int64[7], info int32[4])."""
+        """Voxelize + remap + hash + PSH on (n,3) f64 device coords, no
+        read-back: one fused cooperative launch (f3d_psh_assign_coords) when
+        K + 1 <= 12288, else f3d_voxel_hash + f3d_psh_assign.  Returns
+        (assignment, stats int64[7], info int32[4])."""
         n = coords.shape[0] if n_cap is None else n_cap
         hc = HashConfig(cfg.kind, K=cfg.K, S_div=cfg.S_div)
+        if FUSED_PSH and cfg.K + 1 <= 12288 and n > 0:
+            table, P = default_probe_schedule().device_table()
+            ids = L.empty((n,), torch.int32)
+            offs = L.empty((n,), torch.int32)
+            counts = L.empty((cfg.K + 1,), torch.int32)
+            base = L.empty((cfg.K + 1,), torch.int32)
+            dest = L.empty((n,), torch.int32)
+            info = L.empty((4,), torch.int32)
+            stats = L.empty((7,), torch.int64)
+            ws_bytes = L.load().f3d_psh_coords_workspace_size(n, cfg.K)
+            ws = L.empty((ws_bytes,), torch.uint8)
+            org = (L._F64 * 3)(0.0, 0.0, 0.0)
+            L.call("f3d_psh_assign_coords", L.ptr(coords), n, org, float(cfg.voxel), hc.kind_code,
+                   cfg.K, cfg.S, cfg.S_div, hc.bits_per_axis, int(hc.div_overflow == "error"),
+                   table.ctypes.data_as(L._P), P, DEFAULT_MAX_SWEEPS, L.ptr(ids), L.ptr(offs),
+                   L.ptr(counts), L.ptr(base), L.ptr(dest), L.ptr(info), L.ptr(stats), L.ptr(ws),
+                   ws_bytes, L.ptr(n_dev), L.stream())
+            a = BucketAssignment(ids, offs, counts, base, cfg.S, cfg.K,
+                                 _dev={"id": ids, "off": offs, "counts": counts, "base": base,
+                                       "batch": None, "dest": dest, "info": info})
+            return a, stats, info
         vox32 = L.empty((n, 3), torch.int32)
         home = L.empty((n,), torch.int32)
         stats = L.empty((7,), torch.int64)

@@ -75,7 +75,43 @@ struct Params {
     int32_t* bstart;   // batch -> first sorted position, nbatch + 1
     int32_t* flags;    // max_sweeps + 2 "changed" words
     int max_tiles;
+    // fused voxelize + remap + hash (f3d_psh_assign_coords; single batch):
+    // the kernel reads the float64 coordinates itself instead of vox / home
+    const double* coords;
+    double org[3];
+    double vs;
+    int64_t* stats;      // [min x,y,z, max x,y,z, max quotient] of the remapped voxels
+    long long* part;     // per-CTA partial extrema, 8 per CTA
 };
+
+// floor((c - o) / vs) with no contraction: __dsub_rn then __ddiv_rn
+// (bw/geometry.py:69-72; the same arithmetic as csrc/hash.cu)
+__device__ __forceinline__ long long vox_floor(double c, double o, double vs) {
+    return (long long)floor(__ddiv_rn(__dsub_rn(c, o), vs));
+}
+
+// Block-wide min (kMin) / max of 64-bit values into out[] (thread 0 writes).
+template <int N, int kMin>
+__device__ __forceinline__ void block_extrema(long long (&v)[N], long long* sh, long long* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long b = __shfl_xor_sync(0xffffffffu, v[k], o);
+            v[k] = k < kMin ? min(v[k], b) : max(v[k], b);
+        }
+        if (lane == 0) sh[warp * N + k] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        const int k = threadIdx.x;
+        long long a = sh[k];
+        for (int w = 1; w < kWarps; ++w) a = k < kMin ? min(a, sh[w * N + k]) : max(a, sh[w * N + k]);
+        out[k] = a;
+    }
+    __syncthreads();
+}
 
 // ---------------------------------------------------------------- helpers
 
@@ -242,7 +278,7 @@ __device__ void sequential_batch(const Params& P_, int b, int pb0, int pb1, int3
 
 // --------------------------------------------------------------- the kernel
 
-template <int PL>
+template <int PL, bool FUSED>
 __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     constexpr int kPerLane = TileC<PL>::kPerLane;
     constexpr int kWarpSpan = TileC<PL>::kWarpSpan;
@@ -270,6 +306,33 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
 
     const int gwarp = blockIdx.x * kWarps + warp;
     const int nwarps = gridDim.x * kWarps;
+
+    // ------------------------------- fused: voxelize + per-axis extrema
+    __shared__ long long s_red[kWarps * 6];
+    __shared__ long long s_gmin[3];
+    long long qmax = LLONG_MIN;          // largest div quotient seen (stats[6])
+    if constexpr (FUSED) {
+        long long v[6] = {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MIN, LLONG_MIN, LLONG_MIN};
+        for (int p = blockIdx.x * kThreads + tid; p < n; p += gridDim.x * kThreads) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const long long x = vox_floor(P_.coords[3 * (int64_t)p + a], P_.org[a], P_.vs);
+                v[a] = min(v[a], x);
+                v[3 + a] = max(v[3 + a], x);
+            }
+        }
+        block_extrema<6, 3>(v, s_red, P_.part + 8 * blockIdx.x);
+        grid.sync();
+        // every CTA reduces the partials: warp a < 3 the minimum of axis a
+        if (warp < 3) {
+            long long m = LLONG_MAX;
+            for (int b = lane; b < (int)gridDim.x; b += 32) m = min(m, __ldcg(P_.part + 8 * b + warp));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) s_gmin[warp] = m;
+        }
+        __syncthreads();
+    }
 
     int ntiles;
     // ------------------------------------------------ stable batch sort
@@ -378,7 +441,28 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
                 if (p < ti.p1) {
                     if (sweep == 0) {
                         int4 q;
-                        if (multi) {
+                        if constexpr (FUSED) {
+                            // remap (subtract the axis minimum), range check, home
+                            // hash: the arithmetic of hash.cu hash_point
+                            // (bw/hashing.py:60-149)
+                            long long c3[3];
+#pragma unroll
+                            for (int a = 0; a < 3; ++a)
+                                c3[a] = vox_floor(P_.coords[3 * (int64_t)p + a], P_.org[a], P_.vs) -
+                                        s_gmin[a];
+                            const long long lim = 1ll << P_.hp.bits;
+                            q = make_int4(0, 0, 0, 0);
+                            if (c3[0] < lim && c3[1] < lim && c3[2] < lim) {
+                                int64_t key = P_.hp.kind <= XOR_DIV ? (c3[0] ^ c3[1] ^ c3[2])
+                                                                    : morton3(c3[0], c3[1], c3[2]);
+                                if (P_.hp.kind == XOR_DIV || P_.hp.kind == ZORDER_DIV) {
+                                    key = key / P_.hp.S_div;
+                                    qmax = max(qmax, (long long)key);
+                                }
+                                q = make_int4((int)c3[0], (int)c3[1], (int)c3[2], (int)(key % P_.K));
+                            }
+                            P_.pk[p] = q;
+                        } else if (multi) {
                             q = __ldcg(P_.pk + p);
                         } else {
                             q = make_int4(P_.vox[3 * (int64_t)p], P_.vox[3 * (int64_t)p + 1],
@@ -407,6 +491,12 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
         if (sweep > 0) {
             const int any = __syncthreads_or(changed);
             if (tid == 0 && any) atomicOr(P_.flags + sweep, 1);
+        }
+        if constexpr (FUSED) {
+            if (sweep == 0) {
+                long long qv[1] = {qmax};
+                block_extrema<1, 0>(qv, s_red, P_.part + 8 * blockIdx.x + 6);
+            }
         }
         grid.sync();
         if (sweep > 0) {
@@ -484,8 +574,14 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     }
 
     // ------------------------------------------- final: base scan, dest
-    if (blockIdx.x == 0) {
-        const int nslots = P_.nbatch * W;
+    // The exclusive scan of the slot counts is small: when it fits in this
+    // CTA's shared memory every CTA computes it itself (block 0 also writes
+    // base) and goes straight on to its tiles' dest -- no grid barrier.
+    const int nslots = P_.nbatch * W;
+    const bool local_base = nslots <= hwords;            // hwords: 32-bit smem words
+    int32_t* s_base = reinterpret_cast<int32_t*>(sh);
+    if (local_base || blockIdx.x == 0) {
+        __syncthreads();                                 // sh is free (last use: the sweeps)
         __shared__ int s_part[kThreads];
         const int per = (nslots + kThreads - 1) / kThreads;
         const int a0 = min(tid * per, nslots), a1 = min(a0 + per, nslots);
@@ -505,25 +601,42 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
         __syncthreads();
         int run = s_part[tid];
         for (int i = a0; i < a1; ++i) {
-            P_.base[i] = run;
+            if (blockIdx.x == 0) P_.base[i] = run;
+            if (local_base) s_base[i] = run;
             run += __ldcg(P_.counts + i);
         }
-        if (tid == 0) {
+        if (blockIdx.x == 0 && tid == 0) {
             P_.info[INFO_SWEEPS] = sweep + 1;
             P_.info[INFO_FALLBACK] = fallback ? 1 : 0;
+            if constexpr (FUSED) {
+                // range statistics of the remapped voxels (min is 0 by construction)
+                long long mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN}, q = LLONG_MIN;
+                for (int b = 0; b < (int)gridDim.x; ++b) {
+                    for (int a = 0; a < 3; ++a) mx[a] = max(mx[a], __ldcg(P_.part + 8 * b + 3 + a));
+                    q = max(q, __ldcg(P_.part + 8 * b + 6));
+                }
+                for (int a = 0; a < 3; ++a) {
+                    P_.stats[a] = n > 0 ? 0 : LLONG_MAX;
+                    P_.stats[3 + a] = n > 0 ? mx[a] - s_gmin[a] : LLONG_MIN;
+                }
+                P_.stats[6] = q;
+                P_.info[INFO_BATCH_ERR] = 0;     // single batch, home in [0, K) by construction
+                P_.info[3] = 0;
+            }
         }
+        __syncthreads();
     }
-    grid.sync();
+    if (!local_base) grid.sync();
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const TileInfo ti = tile_info<kTile>(P_, multi, t, n);
-        const int32_t* bb = P_.base + (int64_t)ti.b * W;
+        const int32_t* bb = local_base ? s_base + ti.b * W : P_.base + (int64_t)ti.b * W;
         for (int p = ti.p0 + tid; p < ti.p1; p += kThreads) {
             const int i = multi ? __ldcg(P_.orig + p) : p;
             const int d = __ldcg(P_.D + p);
             const int o = __ldcg(P_.off + p);
             P_.bucket_id[i] = d;
             P_.bucket_offset[i] = o;
-            P_.dest[i] = __ldcg(bb + d) + o;
+            P_.dest[i] = (local_base ? bb[d] : __ldcg(bb + d)) + o;
         }
     }
 }
@@ -608,6 +721,42 @@ __global__ void psh_sequential_kernel(psh::Params P_) {
     P_.info[1] = 2;
 }
 
+namespace {
+constexpr int kMaxGrid = 4096;    // per-CTA partials reserved in the fused workspace
+
+// Launch the cooperative kernel for prepared params (p.n, p.nbatch, p.K set).
+int launch_psh(psh::Params& p, bool fused, cudaStream_t st) {
+    const int K = p.K, nbatch = p.nbatch;
+    const int nbins = nbatch > 1 ? std::max(K + 1, nbatch) : K + 1;
+    const bool small = p.n < psh::kSmallTileMaxN;
+    const int stride = (nbins + 1) & ~1;
+    const size_t smem = (size_t)psh::kWarps * stride * sizeof(uint16_t);
+    void (*kern)(const psh::Params) =
+        fused ? (small ? psh::psh_kernel<psh::kPerLaneSmall, true> : psh::psh_kernel<psh::kPerLaneLarge, true>)
+              : (small ? psh::psh_kernel<psh::kPerLaneSmall, false> : psh::psh_kernel<psh::kPerLaneLarge, false>);
+    static int attr_smem[4] = {0, 0, 0, 0};
+    int& at = attr_smem[2 * fused + small];
+    if ((int)smem > 48 * 1024 && (int)smem > at) {
+        F3D_CUDA_TRY(cudaFuncSetAttribute((const void*)kern,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        at = (int)smem;
+    }
+    int per_sm = 0;
+    F3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, psh::kThreads, smem));
+    if (per_sm < 1) return F3D_ERR_CONFIG;
+    int grid = std::min(per_sm * f3d_num_sms(), p.max_tiles);
+    // Phase B needs nbatch*(K+1) column-warps; more CTAs than tiles only help it.
+    const int col_ctas = cdiv((int64_t)nbatch * (K + 1), psh::kWarps * 2);
+    grid = std::max(grid, std::min(col_ctas, per_sm * f3d_num_sms()));
+    grid = std::max(grid, 1);
+    if (fused) grid = std::min(grid, kMaxGrid);
+    void* args[] = {(void*)&p};
+    F3D_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(psh::kThreads), args,
+                                             smem, st));
+    return F3D_OK;
+}
+}  // namespace
+
 extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const int32_t* batch,
                               int64_t n, int32_t nbatch, int32_t K, int32_t S, int kind,
                               int64_t S_div, int bits, int strict,
@@ -671,26 +820,81 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
         F3D_LAUNCH_CHECK();
         return F3D_OK;
     }
-    const int stride = (nbins + 1) & ~1;
-    const size_t smem = (size_t)psh::kWarps * stride * sizeof(uint16_t);
-    auto kern = small ? psh::psh_kernel<psh::kPerLaneSmall> : psh::psh_kernel<psh::kPerLaneLarge>;
-    static int attr_smem[2] = {0, 0};
-    if ((int)smem > 48 * 1024 && (int)smem > attr_smem[small]) {
-        F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-        attr_smem[small] = (int)smem;
-    }
-    int per_sm = 0;
-    F3D_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, psh::kThreads, smem));
-    if (per_sm < 1) return F3D_ERR_CONFIG;
-    const int max_tiles = p.max_tiles;
-    int grid = std::min(per_sm * f3d_num_sms(), max_tiles);
-    // Phase B needs nbatch*(K+1) column-warps; more CTAs than tiles only help it.
-    const int col_ctas = cdiv((int64_t)nbatch * (K + 1), psh::kWarps * 2);
-    grid = std::max(grid, std::min(col_ctas, per_sm * f3d_num_sms()));
-    grid = std::max(grid, 1);
-    void* args[] = {(void*)&p};
-    F3D_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(psh::kThreads), args,
-                                             smem, st));
-    return F3D_OK;
+    return launch_psh(p, false, st);
+}
+
+// ---------------------------------------------------------------------------
+// Voxelize + remap + range statistics + home hash + PSH in ONE cooperative
+// launch (single batch; the backbone's per-stage bucketing):
+//   bw/geometry.py:69-72 -> bw/hashing.py:128-149 -> bw/hashing.py:60-125 ->
+//   bw/bucketing.py:275-320 (+ compute_bucket_base, dest_index).
+// The coordinates are read twice (per-axis extrema, then the hash in the
+// first sweep); stats gets the 7 range words f3d_voxel_hash produces.
+static psh::WsLayout coords_layout(int64_t n, int32_t K, int max_sweeps, size_t* part_off) {
+    psh::WsLayout L = psh::layout(n, 1, K, max_sweeps);
+    *part_off = L.total;
+    L.total = psh::align256(L.total + 8 * sizeof(long long) * kMaxGrid);
+    return L;
+}
+
+extern "C" size_t f3d_psh_coords_workspace_size(int64_t n, int32_t K) {
+    size_t po;
+    return coords_layout(n, K, psh::kMaxSweepsCap, &po).total;
+}
+
+extern "C" int f3d_psh_assign_coords(const double* coords, int64_t n,
+                                     const double* origin3_host, double voxel_size, int kind,
+                                     int32_t K, int32_t S, int64_t S_div, int bits, int strict,
+                                     const int8_t* probe_offsets_host, int32_t P,
+                                     int32_t max_sweeps, int32_t* bucket_id,
+                                     int32_t* bucket_offset, int32_t* counts, int32_t* base,
+                                     int32_t* dest, int32_t* info_out, int64_t* stats_out,
+                                     void* ws, size_t ws_bytes, const int32_t* n_dev,
+                                     void* stream) {
+    if (n <= 0) return F3D_ERR_EMPTY;
+    if (n >= INT_MAX / 2 || K < 1 || S < 1 || P < 0 || P > psh::kMaxProbes || bits < 1 ||
+        bits > 21 || S_div < 1 || kind < 0 || kind > 3 || !(voxel_size > 0) ||
+        K + 1 > psh::kMaxBins)
+        return F3D_ERR_CONFIG;
+    if (max_sweeps < 1) max_sweeps = 1;
+    if (max_sweeps > psh::kMaxSweepsCap) max_sweeps = psh::kMaxSweepsCap;
+    size_t part_off;
+    const psh::WsLayout L = coords_layout(n, K, max_sweeps, &part_off);
+    if (ws_bytes < L.total) return F3D_ERR_CONFIG;
+    char* w = (char*)ws;
+    psh::Params p{};
+    p.coords = coords;
+    for (int a = 0; a < 3; ++a) p.org[a] = origin3_host[a];
+    p.vs = voxel_size;
+    p.stats = stats_out;
+    p.part = (long long*)(w + part_off);
+    p.n = (int)n;
+    p.n_dev = n_dev;
+    p.nbatch = 1;
+    p.K = K;
+    p.S = S;
+    p.P = P;
+    p.max_sweeps = max_sweeps;
+    p.hp = HashParams{kind, K, S_div, bits, strict};
+    p.vmax = (1 << bits) - 1;
+    for (int i = 0; i < 3 * P; ++i) p.probe[i] = probe_offsets_host[i];
+    p.bucket_id = bucket_id;
+    p.bucket_offset = bucket_offset;
+    p.counts = counts;
+    p.base = base;
+    p.dest = dest;
+    p.info = info_out;
+    p.pk = (int4*)(w + L.pk);
+    p.D = (int32_t*)(w + L.D);
+    p.off = (int32_t*)(w + L.off);
+    p.orig = (int32_t*)(w + L.orig);
+    p.T0 = (int32_t*)(w + L.T0);
+    p.T1 = (int32_t*)(w + L.T1);
+    p.hist = (int32_t*)(w + L.hist);
+    p.flags = (int32_t*)(w + L.flags);
+    const bool small = n < psh::kSmallTileMaxN;
+    const int tile = small ? psh::TileC<psh::kPerLaneSmall>::kTile
+                           : psh::TileC<psh::kPerLaneLarge>::kTile;
+    p.max_tiles = (int)(n / tile + 2);
+    return launch_psh(p, true, (cudaStream_t)stream);
 }

@@ -4,7 +4,7 @@ Drop-in for bw/stage.py.  Per round (bw/stage.py:134-158):
 
     x  = LN1(F) + PE(C)                 f3d_row_ln (fused with the previous
                                         round's MLP residual) -> bf16
-    QKV = x @ [Wq|Wk|Wv] + b            one bf16 GEMM (cuBLAS, library GEMM)
+    QKV = x @ [Wq|Wk|Wv] + b            one bf16 GEMM (f3d_gemm, tcgen05)
     A  = bucket-swin MHSA per scope     f3d_bswin_attention, one launch/round
     F += A @ Wo + bo ; h = LN2(F)       GEMM + f3d_row_ln (fused residual+LN)
     F += gelu(h @ Win + bin) @ Wout + bout    GEMM, f3d_bias_gelu, GEMM, row_ln
@@ -45,6 +45,10 @@ GEMM_LN = os.environ.get("F3D_GEMM_LN", "0") == "1"
 # Opt-in: measured 1.117 vs 1.103 ms per config-B step (the stage-0 table sits on
 # the critical path and the table reads cost about what the sin/cos saved)
 PE_TABLE = os.environ.get("F3D_PE_TABLE", "0") == "1"
+# The QKV, O-projection and MLP GEMMs run on f3d_gemm (csrc/gemm_tc.cu: TMA-fed
+# persistent tcgen05 GEMM, bias / GELU epilogue from TMEM).  F3D_OWN_GEMM=0
+# selects the library GEMMs (A/B measurements only).
+OWN_GEMM = os.environ.get("F3D_OWN_GEMM", "1") == "1"
 _GG = os.environ.get("F3D_GEMM_GELU")
 GEMM_GELU = _GG != "0"
 GEMM_GELU_MIN_ROWS = 0
@@ -94,6 +98,8 @@ class StageParams:
             "w_out": f(self.w_out, bf), "b_out": f(self.b_out, f32),
             "w_in_t": f(self.w_in, bf).t().contiguous(), "w_out_t": f(self.w_out, bf).t().contiguous(),
             "w_o_t": f(self.w_o, bf).t().contiguous(),
+            "w_qkv_t": torch.cat([f(self.w_q, bf), f(self.w_k, bf), f(self.w_v, bf)], 1).t().contiguous(),
+            "b_qkv32": torch.cat([f(self.b_q, f32), f(self.b_k, f32), f(self.b_v, f32)]).contiguous(),
             "ln1_g": f(self.ln1_gain, f32), "ln1_b": f(self.ln1_bias, f32),
             "ln2_g": f(self.ln2_gain, f32), "ln2_b": f(self.ln2_bias, f32),
         }
@@ -195,6 +201,13 @@ class StageRunner:
                           and dhid == 4 * d
                           and self.w.get("w_in_t") is not None
                           and bool(L.load().f3d_gemm_gelu_supported(d)))
+        self.own_gemm = (OWN_GEMM and self.w.get("w_qkv_t") is not None
+                         and all(lib.f3d_gemm_supported(k_, n_)
+                                 for k_, n_ in ((d, 3 * d), (d, d), (d, dhid), (dhid, d))))
+
+    def _gemm(self, X, K, w_t, N, bias, gelu, Y):
+        L.call("f3d_gemm", L.ptr(X), X.stride(0), self.n, K, L.ptr(w_t), N, L.ptr(bias),
+               int(gelu), L.ptr(Y), Y.stride(0), L.ptr(self.n_dev), L.stream())
 
     def _row_ln(self, F, y, ybias, g, b, pe, out):
         if pe and self.pe_tab is not None and F.dtype == torch.float32 and out is not None:
@@ -230,8 +243,13 @@ class StageRunner:
             self._row_ln(F, None, None, w["ln1_g"], w["ln1_b"], True, self.x)
         R = len(self.plans)
         hook = getattr(self, "round_hook", None)
+        d, dhid = self.d, self.p.d_hidden
+        own = self.own_gemm
         for t, plan in enumerate(self.plans):
-            torch.addmm(w["b_qkv"], self.x, w["w_qkv"], out=self.qkv)
+            if own:
+                self._gemm(self.x, d, w["w_qkv_t"], 3 * d, w["b_qkv32"], False, self.qkv)
+            else:
+                torch.addmm(w["b_qkv"], self.x, w["w_qkv"], out=self.qkv)
             attend(q, k, v, self.a, plan, self.H, self.dh)
             if hook is not None:
                 # test instrumentation (parity on the GPU's own round input):
@@ -241,7 +259,10 @@ class StageRunner:
                 self._gemm_ln(self.a, self.d, w["w_o_t"], w["b_o"], F, w["ln2_g"], w["ln2_b"],
                               False, self.x)
             else:
-                torch.mm(self.a, w["w_o"], out=self.y)
+                if own:
+                    self._gemm(self.a, d, w["w_o_t"], d, None, False, self.y)
+                else:
+                    torch.mm(self.a, w["w_o"], out=self.y)
                 self._row_ln(F, self.y, w["b_o"], w["ln2_g"], w["ln2_b"], None, self.x)
             if self.fused_mlp and F.dtype == torch.float32:
                 last = t + 1 == R
@@ -258,6 +279,8 @@ class StageRunner:
                 L.call("f3d_gemm_gelu", L.ptr(self.x), self.x.stride(0), self.n, self.d,
                        L.ptr(w["w_in_t"]), L.ptr(w["b_in"]), L.ptr(self.u), self.u.stride(0),
                        L.ptr(self.n_dev), L.stream())
+            elif own:
+                self._gemm(self.x, d, w["w_in_t"], dhid, w["b_in"], True, self.u)
             else:
                 torch.mm(self.x, w["w_in"], out=self.u)
                 L.call("f3d_bias_gelu", L.ptr(self.u), self.n, self.u.shape[1],
@@ -268,7 +291,10 @@ class StageRunner:
                               None if last else w["ln1_g"], None if last else w["ln1_b"],
                               not last, None if last else self.x)
                 continue
-            torch.mm(self.u, w["w_out"], out=self.y)
+            if own:
+                self._gemm(self.u, dhid, w["w_out_t"], d, None, False, self.y)
+            else:
+                torch.mm(self.u, w["w_out"], out=self.y)
             if t + 1 < R:
                 self._row_ln(F, self.y, w["b_out"], w["ln1_g"], w["ln1_b"], True, self.x)
             elif not defer_last_residual:

@@ -134,6 +134,9 @@ class DeviceWeights:
         w["w_in_t"].copy_(m["w_in"].t())
         w["w_out_t"].copy_(m["w_out"].t())
         w["w_o_t"].copy_(m["w_o"].t())
+        w["w_qkv_t"].copy_(w["w_qkv"].t())
+        for i, k in enumerate(("b_q", "b_k", "b_v")):
+            w["b_qkv32"][i * d:(i + 1) * d].copy_(m[k])
 
     def sgd(self, grads, lr: float):
         for k in GRAD_NAMES:
