@@ -26,11 +26,10 @@ namespace f3d {
 namespace pool {
 
 constexpr int kCap = 1024;         // TILE_CAP (bw/pooling.py:22)
-constexpr int kWarpsPerCta = 2;
+constexpr int kWarpsPerCta = 1;   // 40 KB of smem per warp: 5 tiles in flight per SM
 constexpr int kThreads = 32 * kWarpsPerCta;
 
 struct WarpSmem {
-    double sc[kCap][3];     // per sub id: seed coordinates (step-3 distances)
     double cc[kCap][3];     // per row: the tile's coordinates (staged once)
     uint16_t qrow[kCap];    // step-3 queue: queued rows in index order
     uint16_t cnt[kCap];     // per key running count
@@ -157,9 +156,6 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
             const int id = nalloc + __popc(fb & lt);
             S.idk[k] = (int16_t)id;
             S.seeds[id] = (int16_t)i;
-            S.sc[id][0] = S.cc[i][0];
-            S.sc[id][1] = S.cc[i][1];
-            S.sc[id][2] = S.cc[i][2];
         }
         if (v && lane == __ffs(mm) - 1) S.cnt[k] = (uint16_t)(S.cnt[k] + __popc(mm));
         nalloc += __popc(fb);
@@ -192,10 +188,7 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
                 S.sub[i] = (int16_t)id;
                 S.sizes[id] = 1;
                 S.seeds[id] = (int16_t)i;
-                S.sc[id][0] = S.cc[i][0];
-                S.sc[id][1] = S.cc[i][1];
-                S.sc[id][2] = S.cc[i][2];
-            } else {
+                        } else {
                 S.sub[i] = -2;
                 S.qrow[r - need_new] = (uint16_t)i;   // queue keeps index order
             }
@@ -247,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
             double bd2 = DBL_MAX;
             for (int e = 0; e < ne; ++e) {      // ascending ids: strict '<' keeps the lowest
                 const int jj = S.elig[e];
-                const double d2 = dist2(S.sc[jj], ci);
+                const double d2 = dist2(S.cc[S.seeds[jj]], ci);   // seed row's coordinates
                 if (closer(d2, jj, bd2, choice)) {
                     bd2 = d2;
                     choice = jj;
@@ -274,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
                 for (int e = lane; e < ne; e += 32) {
                     const int j = S.elig[e];
                     if (S.sizes[j] >= rho) continue;
-                    const double d2 = dist2(S.sc[j], ci);
+                    const double d2 = dist2(S.cc[S.seeds[j]], ci);
                     if (closer(d2, j, bd2, bid)) {
                         bd2 = d2;
                         bid = j;

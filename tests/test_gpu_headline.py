@@ -83,8 +83,13 @@ def _check_sampled_scopes(stages, trace, rounds, n_heads=4, per_round=64, tol=1e
         for s in pick:
             rows = np.concatenate([np.arange(starts[b], starts[b] + lens[b]) for b in scopes[s]])
             ri = torch.as_tensor(rows, device=q.device)
-            qh, kh, vh = (x[ri].double().cpu().numpy() for x in (q, k, v))
-            got = a[ri].double().cpu().numpy()
+            kh, vh = (x[ri].double().cpu().numpy() for x in (k, v))
+            # every key of the scope; up to 256 sampled query rows of it (the
+            # dense float64 oracle of a 4096-row scope is 4 x 4096^2 scores)
+            qi = rows if len(rows) <= 256 else np.sort(r.choice(rows, 256, replace=False))
+            qt = torch.as_tensor(qi, device=q.device)
+            qh = q[qt].double().cpu().numpy()
+            got = a[qt].double().cpu().numpy()
             ref = O.attention_dense(qh, kh, vh, n_heads)
             e = _rel(got, ref)
             worst = max(worst, e)

@@ -16,9 +16,9 @@ from paper_2412_16481_b200.backbone import Backbone  # noqa: E402
 steps = int(os.environ.get("PROF_STEPS", "1"))
 coords, feats = bench.workload(0)
 C = torch.tensor(coords, device="cuda")
-X = torch.tensor(feats, dtype=torch.bfloat16, device="cuda")
+X = torch.tensor(feats, dtype=torch.float32, device="cuda")     # as bench.py
 bb = Backbone()
-bb.capture(C.shape[0], torch.bfloat16)
+bb.capture(C.shape[0], torch.float32)
 bb.graph_coords.copy_(C)
 bb.graph_feats.copy_(X)
 for _ in range(3):
