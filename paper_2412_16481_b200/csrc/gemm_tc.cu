@@ -7,12 +7,12 @@
 //   * warp 0 streams X and W^T k-blocks by TMA (K-major, 128/64-byte swizzle)
 //     through an S-deep ring of shared-memory stages;
 //   * warp 1 (one elected lane) issues tcgen05.mma M=128 N=BN K=16 into one
-//     of two TMEM accumulators (2 x BN <= 512 columns), so the next tile's
-//     MMAs overlap this tile's epilogue;
-//   * two epilogue warpgroups split the tile's columns: tcgen05.ld 16 columns
-//     at a time (the next chunk's load in flight), + bias (+ packed-pair GELU),
-//     bf16, staged in shared memory (padded rows: conflict-free), released
-//     TMEM, then coalesced 16-byte stores of whole row segments.
+//     of NB TMEM accumulators (NB x BN <= 512 columns, NB <= 4);
+//   * NB epilogue warpgroups take the tiles round robin, one whole tile each
+//     (WG g drains accumulator g), so NB tiles' epilogues overlap each other
+//     and the next tiles' MMAs: tcgen05.ld 4 x 16 columns per wait, + bias
+//     (+ packed-pair GELU), bf16, staged in shared memory (padded rows:
+//     conflict-free), then coalesced 16-byte stores of whole row segments.
 // N is split into equal tiles of at most 256 columns (a multiple of 16);
 // K is a multiple of 32 (BK = 64 with 128-byte swizzle when K % 64 == 0,
 // else BK = 32 with 64-byte swizzle).  Rows past n (device count n_dev) are
@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "f3d_common.cuh"
@@ -31,47 +32,61 @@ namespace gm {
 using namespace f3d::tc;
 
 constexpr int kBM = 128;
-constexpr int kThreads = 384;      // warp 0 TMA, warp 1 MMA, warps 4-11 epilogue (2 WGs)
+constexpr int kMaxWG = 3;          // epilogue warpgroups (one tile each, round robin); 512 threads: 128 registers
+constexpr int kThreads = (1 + kMaxWG) * 128;   // warp 0 TMA, warp 1 MMA, warps 4.. epilogue
 constexpr int kMaxStages = 8;
 constexpr int kSmemLimit = 227 * 1024;
 
 struct Args {
     int64_t n;
     const int32_t* n_dev;
-    int K, N, BN, nt, S, csplit;
+    int K, N, BN, nt, S, nbuf;     // nbuf: TMEM accumulators = active epilogue WGs
     const float* bias;       // (N) fp32, nullable
     int gelu;
+    int dbg;                 // A/B only: 1 = epilogue skips its work, 2 = no copy-out
     __nv_bfloat16* y;
     int64_t ldy;
     // shared-memory layout (bytes from the 1024-aligned base)
-    int off_stage, stage_bytes, a_bytes, off_st0, off_st1, st_stride0, st_stride1, off_bias,
-        off_bar;
+    int off_stage, stage_bytes, a_bytes, off_st, st_stride, off_bias, off_bar;
+    int resident, off_w, w_bytes;   // resident: all of W^T stays in smem (loaded once)
 };
+
+// mbarrier wait expanded at the call site (so profiles attribute the spin to
+// the waiting role's source line)
+#define GM_WAIT(bar, parity)                                                   \
+    asm volatile(                                                              \
+        "{\n\t.reg .pred p;\n"                                                 \
+        "W_%=:\n\t"                                                            \
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"           \
+        "@!p bra W_%=;\n\t"                                                    \
+        "}" ::"r"(saddr(bar)), "r"((uint32_t)(parity)) : "memory")
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int BK>
+template <int BK, bool GELU, bool BIAS>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const Args A, const __grid_constant__ CUtensorMap amap,
-                const __grid_constant__ CUtensorMap bmap) {
+                const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap ymap) {
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem =
-        (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // swizzle atoms
-    const int S = A.S, BN = A.BN;
+    // 1024-byte aligned base for the swizzle atoms, derived from the shared
+    // array itself so every access below stays a shared-space (STS/LDS) one
+    unsigned char* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+    const int S = A.S, BN = A.BN, NB = A.nbuf;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + A.off_bar);
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
     uint64_t* acc_full = bars + 2 * S;
-    uint64_t* acc_empty = acc_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* acc_empty = acc_full + kMaxWG;
+    uint64_t* w_full = acc_empty + kMaxWG;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
     float* s_bias = reinterpret_cast<float*>(smem + A.off_bias);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t n = dyn_n(A.n, A.n_dev);
     const int mblocks = (int)((n + kBM - 1) / kBM);
     const int ntiles = mblocks * A.nt;
-    const int nk = A.K / BK;
+    const int nk = (A.K + BK - 1) / BK;        // a partial last k-block is zero-filled by TMA
 
     for (int i = tid; i < A.N; i += kThreads) s_bias[i] = A.bias ? A.bias[i] : 0.f;
     if (tid == 0) {
@@ -79,10 +94,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kMaxWG; ++b) {
             mbar_init(acc_full + b, 1);
-            mbar_init(acc_empty + b, 256);
+            mbar_init(acc_empty + b, 128);
         }
+        mbar_init(w_full, 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -97,17 +113,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
+        if (A.resident && lane == 0) {
+            // W^T once: box (j, ks) at off_w + (j * nk + ks) * BN * BK * 2
+            mbar_arrive_expect(w_full, A.w_bytes);
+            for (int j = 0; j < A.nt; ++j)
+                for (int ks = 0; ks < nk; ++ks)
+                    tma_2d(sbase + A.off_w + (j * nk + ks) * BN * BK * 2, &bmap, w_full, ks * BK,
+                           j * BN);
+        }
         int kc = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int m = t / A.nt, j = t - m * A.nt;
             for (int ks = 0; ks < nk; ++ks, ++kc) {
                 const int s = kc % S;
-                if (kc >= S) mbar_wait(empty + s, ((kc / S) - 1) & 1);
+                if (kc >= S) GM_WAIT(empty + s, ((kc / S) - 1) & 1);
                 if (lane == 0) {
                     const uint32_t dst = sbase + A.off_stage + s * A.stage_bytes;
                     mbar_arrive_expect(full + s, A.stage_bytes);
                     tma_2d(dst, &amap, full + s, ks * BK, m * kBM);
-                    tma_2d(dst + A.a_bytes, &bmap, full + s, ks * BK, j * BN);
+                    if (!A.resident) tma_2d(dst + A.a_bytes, &bmap, full + s, ks * BK, j * BN);
                 }
                 __syncwarp();
             }
@@ -118,19 +142,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t kSbo = BK == 64 ? 1024u : 512u;    // 8 rows x row bytes
         const uint32_t idesc = idesc_bf16(kBM, BN, 0, 0);
         int kc = 0, it = 0;
+        if (A.resident) GM_WAIT(w_full, 0);
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const int buf = it & 1;
-            if (it >= 2) mbar_wait(acc_empty + buf, ((it >> 1) - 1) & 1);
+            const int jt = t % A.nt;
+            const int buf = it % NB, use = it / NB;
+            if (use >= 1) GM_WAIT(acc_empty + buf, (use - 1) & 1);
             tc_fence_after();
             const uint32_t d = tmem + buf * BN;
             for (int ks = 0; ks < nk; ++ks, ++kc) {
                 const int s = kc % S;
-                mbar_wait(full + s, (kc / S) & 1);
+                GM_WAIT(full + s, (kc / S) & 1);
                 tc_fence_after();
                 if (elect_one()) {
                     const uint32_t a0 = sbase + A.off_stage + s * A.stage_bytes;
                     const uint64_t da = sw_desc(a0, 16, kSbo, kLt);
-                    const uint64_t db = sw_desc(a0 + A.a_bytes, 16, kSbo, kLt);
+                    const uint32_t b0 = A.resident
+                                            ? sbase + A.off_w + (jt * nk + ks) * BN * BK * 2
+                                            : a0 + A.a_bytes;
+                    const uint64_t db = sw_desc(b0, 16, kSbo, kLt);
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk)      // +32 B per K=16 step
                         umma_f16(d, da + (uint64_t)(2 * kk), db + (uint64_t)(2 * kk), idesc,
@@ -142,65 +171,119 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (elect_one()) umma_commit(acc_full + buf);
             __syncwarp();
         }
-    } else if (warp >= 4) {
+    } else if (warp >= 4 && (warp >> 2) - 1 < NB) {
         // ------------------------------------------------ epilogue
-        const int g = (warp >> 2) - 1;                         // warpgroup 0 / 1
-        const int c_lo = g == 0 ? 0 : A.csplit, c_hi = g == 0 ? A.csplit : BN;
-        const int stride = g == 0 ? A.st_stride0 : A.st_stride1;
-        unsigned char* stage = smem + (g == 0 ? A.off_st0 : A.off_st1);
-        const int r = (warp & 3) * 32 + lane;                  // tile row = TMEM lane
-        const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+        // WG g takes the tiles it = g, g + NB, ... of this CTA (TMEM buffer g)
+        // whole: tcgen05.ld 4 x 16 columns per wait, + bias (+ GELU), bf16
+        // into its padded staging tile, then coalesced row-segment stores.
+        const int g = (warp >> 2) - 1;
+        const int wq = warp & 3;
+        const int r = wq * 32 + lane;                          // tile row = TMEM lane
+        const uint32_t lb = (uint32_t)(wq * 32) << 16;
+        const int stride = A.st_stride;
+        unsigned char* stage = smem + A.off_st + g * kBM * stride;
         unsigned char* strow = stage + r * stride;
-        const int chunks = (c_hi - c_lo) / 8;                  // 16-byte chunks per row
+        const int nch = BN / 16;
+        const int cpr = BN / 8;                                // 16-byte chunks per row
+        const uint32_t inv_cpr = ((1u << 20) + cpr - 1) / cpr;  // exact i / cpr for i < 4096
         const int tq = tid & 127;
-        int it = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const uint32_t tbase = tmem + lb + g * BN;
+        int u = 0;
+        for (int t = blockIdx.x + g * gridDim.x; t < ntiles; t += NB * gridDim.x, ++u) {
             const int m = t / A.nt, j = t - m * A.nt;
-            const int buf = it & 1;
-            mbar_wait(acc_full + buf, (it >> 1) & 1);
+            GM_WAIT(acc_full + g, u & 1);
             tc_fence_after();
-            const uint32_t c0 = tmem + lb + buf * BN;
             const float* bj = s_bias + j * BN;
-            if (c_hi > c_lo) {
-                uint32_t v[16], nv[16];
-                tmem_ld16(c0 + c_lo, v);
+            if (A.dbg == 1) {
+                tc_fence_before();
+                mbar_arrive(acc_empty + g);
+                continue;
+            }
+            const int64_t r0 = (int64_t)m * kBM;
+            const bool full_tile = r0 + kBM <= n;
+            uint32_t v[4][16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)                        // first four chunks in flight
+                if (c < nch) tmem_ld16(tbase + 16 * c, v[c]);
+            if (tq == 0) bulk_wait_read0();                    // previous tile's store left smem
+            named_bar(1 + g, 128);
+            for (int c0 = 0; c0 < nch; c0 += 4) {
+                if (c0 > 0) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (c0 + c < nch) tmem_ld16(tbase + 16 * (c0 + c), v[c]);
+                }
                 tmem_wait_ld();
-#pragma unroll 1
-                for (int cc = c_lo; cc < c_hi; cc += 16) {
-                    const bool more = cc + 16 < c_hi;
-                    if (more) tmem_ld16(c0 + cc + 16, nv);     // next chunk in flight
+                if (c0 + 4 >= nch) {
+                    tc_fence_before();
+                    mbar_arrive(acc_empty + g);                // accumulator free
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (c0 + c >= nch) break;
+                    float bv[16];
+                    if (BIAS) {                                // 4 vector loads per chunk
+                        const float4* bc = reinterpret_cast<const float4*>(bj + 16 * (c0 + c));
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 b4 = bc[q];
+                            bv[4 * q] = b4.x;
+                            bv[4 * q + 1] = b4.y;
+                            bv[4 * q + 2] = b4.z;
+                            bv[4 * q + 3] = b4.w;
+                        }
+                    }
                     uint32_t pk[8];
 #pragma unroll
                     for (int e = 0; e < 16; e += 2) {
-                        float2 f = make_float2(__uint_as_float(v[e]) + bj[cc + e],
-                                               __uint_as_float(v[e + 1]) + bj[cc + e + 1]);
-                        if (A.gelu) f = gelu2(f.x, f.y);
+                        float2 f = make_float2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1]));
+                        if (BIAS) {
+                            f.x += bv[e];
+                            f.y += bv[e + 1];
+                        }
+                        if (GELU) f = gelu2(f.x, f.y);
                         __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
                         pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                     }
-                    uint4* dst = reinterpret_cast<uint4*>(strow + (cc - c_lo) * 2);
+                    uint4* dst = reinterpret_cast<uint4*>(strow + 32 * (c0 + c));
                     dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                    if (more) {
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) v[e] = nv[e];
-                    }
                 }
             }
-            tc_fence_before();
-            mbar_arrive(acc_empty + buf);                      // accumulator free
+            if (full_tile) fence_proxy_async();                // STS visible to the TMA store
             named_bar(1 + g, 128);                             // staging tile complete
-            const int64_t r0 = (int64_t)m * kBM;
-            __nv_bfloat16* yb = A.y + j * BN + c_lo;
-            for (int i = tq; i < kBM * chunks; i += 128) {
-                const int rr = i / chunks, ch = i - rr * chunks;
-                if (r0 + rr < n)
-                    *reinterpret_cast<uint4*>(yb + (r0 + rr) * A.ldy + ch * 8) =
-                        *reinterpret_cast<const uint4*>(stage + rr * stride + ch * 16);
+            if (A.dbg == 2) continue;
+            if (full_tile) {
+                // one bulk tensor store of the whole 128 x BN tile
+                if (tq == 0) {
+                    tma_store_2d(&ymap, saddr(stage), j * BN, (int)r0);
+                    bulk_commit();
+                }
+                continue;
+            }
+            // the tile holding row n: coalesced 16-byte stores of the real rows only
+            const int rows = (int)(n - r0);
+            const int total = rows * cpr;
+            __nv_bfloat16* yb = A.y + j * BN;
+            for (int i0 = tq; i0 < total; i0 += 4 * 128) {
+                uint4 val[4];
+                int rr[4], cc[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = i0 + k * 128;
+                    rr[k] = (int)(((uint32_t)i * inv_cpr) >> 20);  // i / cpr (i < 2^12, cpr <= 32)
+                    cc[k] = i - rr[k] * cpr;
+                    if (i < total)
+                        val[k] = *reinterpret_cast<const uint4*>(stage + rr[k] * stride + cc[k] * 16);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (i0 + k * 128 < total)
+                        *reinterpret_cast<uint4*>(yb + (r0 + rr[k]) * A.ldy + cc[k] * 8) = val[k];
             }
             named_bar(1 + g, 128);                             // staging free again
         }
+        if (tq == 0) bulk_wait_read0();
     }
     tc_fence_before();
     __syncthreads();
@@ -208,41 +291,57 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 struct Plan {
-    int BK, BN, nt, S, csplit;
+    int BK, BN, nt, S;
     Args a;
     size_t smem;
 };
 
 static bool plan(int K, int N, Plan& p) {
     if (K < 32 || K % 32 || N < 16 || N % 16 || N > 4096) return false;
-    p.BK = (K % 64 == 0) ? 64 : 32;
+    // BK = 64 (128-byte rows, SWIZZLE_128B) unless F3D_GEMM_BK32 asks for 32 when K % 64 != 0
+    p.BK = (K % 64 == 0 || !getenv("F3D_GEMM_BK32")) ? 64 : 32;
     int nt = (N + 255) / 256;
     while (nt <= N / 16 && (N % nt || (N / nt) % 16)) ++nt;
     if (nt > N / 16) return false;
     p.nt = nt;
     p.BN = N / nt;
-    p.csplit = std::min(p.BN, ((p.BN / 2 + 15) / 16) * 16);
     Args& a = p.a;
     a.K = K;
     a.N = N;
     a.BN = p.BN;
     a.nt = nt;
-    a.csplit = p.csplit;
     a.a_bytes = kBM * p.BK * 2;
-    a.stage_bytes = (kBM + p.BN) * p.BK * 2;
-    a.st_stride0 = p.csplit * 2 + 16;
-    a.st_stride1 = (p.BN - p.csplit) * 2 + 16;
-    const int staging = kBM * (a.st_stride0 + a.st_stride1);
-    const int fixed = 1024 /* base alignment */ + staging + ((N * 4 + 15) & ~15) + 256;
-    const int S = std::min(kMaxStages, (kSmemLimit - fixed) / a.stage_bytes);
-    if (S < 2) return false;
+    a.st_stride = 2 * p.BN;                        // dense rows: the TMA store box layout
+    const int bias_bytes = (N * 4 + 15) & ~15;
+    // W^T resident in shared memory when it is small (d <= ~128 projections):
+    // only X streams, and no tile re-reads the weights from L2
+    a.w_bytes = N * ((K + p.BK - 1) / p.BK) * p.BK * 2;
+    // measured (tools/gemm_bench.py, d = 96): resident wins for the 55 KB QKV
+    // weights (18.8 vs 20.8 us streaming), streaming for the 74 KB MLP ones
+    // (the resident copy costs pipeline stages)
+    int wmax = 64 * 1024;
+    if (const char* e = getenv("F3D_GEMM_WRES_KB")) wmax = atoi(e) * 1024;
+    a.resident = a.w_bytes <= wmax;
+    a.stage_bytes = a.resident ? a.a_bytes : (kBM + p.BN) * p.BK * 2;
+    const int wres = a.resident ? a.w_bytes : 0;
+    // as many TMEM accumulators / epilogue WGs as fit, keeping >= 3 stages (>= 2 at worst)
+    int nb = std::min(kMaxWG, 512 / p.BN);
+    if (const char* e = getenv("F3D_GEMM_NB")) nb = std::max(1, std::min(nb, atoi(e)));
+    int S = 0;
+    for (; nb >= 1; --nb) {
+        const int fixed = 1024 + wres + nb * kBM * a.st_stride + bias_bytes + 256;
+        S = std::min(kMaxStages, (kSmemLimit - fixed) / a.stage_bytes);
+        if (S >= 3 || (nb == 1 && S >= 2)) break;
+    }
+    if (nb < 1 || S < 2) return false;
+    a.nbuf = nb;
     p.S = a.S = S;
-    a.off_stage = 0;
-    a.off_st0 = S * a.stage_bytes;
-    a.off_st1 = a.off_st0 + kBM * a.st_stride0;
-    a.off_bias = a.off_st1 + kBM * a.st_stride1;
-    a.off_bar = (a.off_bias + N * 4 + 15) & ~15;
-    p.smem = (size_t)a.off_bar + (2 * S + 4) * 8 + 16 + 1024;
+    a.off_w = 0;
+    a.off_stage = wres;
+    a.off_st = a.off_stage + S * a.stage_bytes;
+    a.off_bias = a.off_st + nb * kBM * a.st_stride;
+    a.off_bar = (a.off_bias + bias_bytes + 15) & ~15;
+    p.smem = (size_t)a.off_bar + (2 * S + 2 * kMaxWG + 1) * 8 + 16 + 1024;
     return p.smem <= (size_t)kSmemLimit;
 }
 
@@ -265,12 +364,14 @@ extern "C" int f3d_gemm(const void* x, int64_t ldx, int64_t n, int K, const void
         return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    CUtensorMap amap, bmap;
+    CUtensorMap amap, bmap, ymap;
     memset(&amap, 0, sizeof(amap));
     memset(&bmap, 0, sizeof(bmap));
+    memset(&ymap, 0, sizeof(ymap));
     const int sw = p.BK * 2;
     if (!tc::make_map(&amap, x, ldx, K, n, p.BK, sw, gm::kBM) ||
-        !tc::make_map(&bmap, w_t, K, K, N, p.BK, sw, p.BN)) {
+        !tc::make_map(&bmap, w_t, K, K, N, p.BK, sw, p.BN) ||
+        !tc::make_map(&ymap, y, ldy, N, n, p.BN, 0, gm::kBM)) {
         f3d_set_last_cuda_error(cudaErrorNotSupported);
         return F3D_ERR_CUDA;
     }
@@ -279,19 +380,30 @@ extern "C" int f3d_gemm(const void* x, int64_t ldx, int64_t n, int K, const void
     a.n_dev = n_dev;
     a.bias = bias;
     a.gelu = gelu;
+    {
+        const char* e = getenv("F3D_GEMM_DBG");
+        a.dbg = e ? atoi(e) : 0;
+    }
     a.y = (__nv_bfloat16*)y;
     a.ldy = ldy;
-    auto kern = p.BK == 64 ? gm::gemm_kernel<64> : gm::gemm_kernel<32>;
-    static int attr[2] = {0, 0};
-    int& at = attr[p.BK == 64];
+    using Kern = void (*)(const gm::Args, const CUtensorMap, const CUtensorMap, const CUtensorMap);
+    static const Kern kerns[8] = {
+        gm::gemm_kernel<32, false, false>, gm::gemm_kernel<32, false, true>,
+        gm::gemm_kernel<32, true, false>,  gm::gemm_kernel<32, true, true>,
+        gm::gemm_kernel<64, false, false>, gm::gemm_kernel<64, false, true>,
+        gm::gemm_kernel<64, true, false>,  gm::gemm_kernel<64, true, true>};
+    const int ki = 4 * (p.BK == 64) + 2 * (gelu != 0) + (bias != nullptr);
+    const Kern kern = kerns[ki];
+    static int attr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int& at = attr[ki];
     if ((int)p.smem > at) {
-        F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        F3D_CUDA_TRY(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)p.smem));
         at = (int)p.smem;
     }
     const int64_t tiles = ((n + gm::kBM - 1) / gm::kBM) * p.nt;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, f3d_num_sms()));
-    kern<<<grid, gm::kThreads, p.smem, st>>>(a, amap, bmap);
+    kern<<<grid, gm::kThreads, p.smem, st>>>(a, amap, bmap, ymap);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

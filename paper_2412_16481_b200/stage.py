@@ -48,7 +48,9 @@ PE_TABLE = os.environ.get("F3D_PE_TABLE", "0") == "1"
 # The QKV, O-projection and MLP GEMMs run on f3d_gemm (csrc/gemm_tc.cu: TMA-fed
 # persistent tcgen05 GEMM, bias / GELU epilogue from TMEM).  F3D_OWN_GEMM=0
 # selects the library GEMMs (A/B measurements only).
-OWN_GEMM = os.environ.get("F3D_OWN_GEMM", "1") == "1"
+_OG = os.environ.get("F3D_OWN_GEMM", "qkv,o,in,out")
+OWN_GEMM = {k for k in ("qkv", "o", "in", "out")
+            if _OG == "1" or k in _OG.split(",")} if _OG != "0" else set()
 _GG = os.environ.get("F3D_GEMM_GELU")
 GEMM_GELU = _GG != "0"
 GEMM_GELU_MIN_ROWS = 0
@@ -201,9 +203,11 @@ class StageRunner:
                           and dhid == 4 * d
                           and self.w.get("w_in_t") is not None
                           and bool(L.load().f3d_gemm_gelu_supported(d)))
-        self.own_gemm = (OWN_GEMM and self.w.get("w_qkv_t") is not None
-                         and all(lib.f3d_gemm_supported(k_, n_)
-                                 for k_, n_ in ((d, 3 * d), (d, d), (d, dhid), (dhid, d))))
+        ok = self.w.get("w_qkv_t") is not None
+        self.own = {k for k, (k_, n_) in (("qkv", (d, 3 * d)), ("o", (d, d)), ("in", (d, dhid)),
+                                          ("out", (dhid, d)))
+                    if ok and k in OWN_GEMM and lib.f3d_gemm_supported(k_, n_)}
+        self.own_gemm = bool(self.own)
 
     def _gemm(self, X, K, w_t, N, bias, gelu, Y):
         L.call("f3d_gemm", L.ptr(X), X.stride(0), self.n, K, L.ptr(w_t), N, L.ptr(bias),
@@ -244,9 +248,9 @@ class StageRunner:
         R = len(self.plans)
         hook = getattr(self, "round_hook", None)
         d, dhid = self.d, self.p.d_hidden
-        own = self.own_gemm
+        own = self.own
         for t, plan in enumerate(self.plans):
-            if own:
+            if "qkv" in own:
                 self._gemm(self.x, d, w["w_qkv_t"], 3 * d, w["b_qkv32"], False, self.qkv)
             else:
                 torch.addmm(w["b_qkv"], self.x, w["w_qkv"], out=self.qkv)
@@ -259,7 +263,7 @@ class StageRunner:
                 self._gemm_ln(self.a, self.d, w["w_o_t"], w["b_o"], F, w["ln2_g"], w["ln2_b"],
                               False, self.x)
             else:
-                if own:
+                if "o" in own:
                     self._gemm(self.a, d, w["w_o_t"], d, None, False, self.y)
                 else:
                     torch.mm(self.a, w["w_o"], out=self.y)
@@ -275,12 +279,12 @@ class StageRunner:
                        None if last else L.ptr(self.x), self.x.stride(0), LN_EPS,
                        L.ptr(self.n_dev), L.stream())
                 continue
-            if self.gemm_gelu:
+            if "in" in own:
+                self._gemm(self.x, d, w["w_in_t"], dhid, w["b_in"], True, self.u)
+            elif self.gemm_gelu:
                 L.call("f3d_gemm_gelu", L.ptr(self.x), self.x.stride(0), self.n, self.d,
                        L.ptr(w["w_in_t"]), L.ptr(w["b_in"]), L.ptr(self.u), self.u.stride(0),
                        L.ptr(self.n_dev), L.stream())
-            elif own:
-                self._gemm(self.x, d, w["w_in_t"], dhid, w["b_in"], True, self.u)
             else:
                 torch.mm(self.x, w["w_in"], out=self.u)
                 L.call("f3d_bias_gelu", L.ptr(self.u), self.n, self.u.shape[1],
@@ -291,7 +295,7 @@ class StageRunner:
                               None if last else w["ln1_g"], None if last else w["ln1_b"],
                               not last, None if last else self.x)
                 continue
-            if own:
+            if "out" in own:
                 self._gemm(self.u, dhid, w["w_out_t"], d, None, False, self.y)
             else:
                 torch.mm(self.u, w["w_out"], out=self.y)
