@@ -342,10 +342,10 @@ class Backbone:
             else:
                 with record_function(f"stage{si}.bucketize"):
                     r.asg, r.stats, r.info = self.bucketize(C, cfg, n_cap, n_dev)
-                # every stage>=1 PSH records the event stream_host gates the next
-                # scene's stage-0 PSH on, wherever it runs (here: the main stream)
-                r.psh_event = torch.cuda.Event(external=True)
-                r.psh_event.record(torch.cuda.current_stream())
+                # this stage's cooperative PSH runs on the main stream with no
+                # gating event: stream_host then keeps the next scene's g0 after
+                # this whole step (no two cooperative PSH grids in flight)
+                r.psh_on_main = True
             runs.append(r)
             X, C, n_cap, n_dev = self._stage_body(r, C, X)
         return X, C, n_dev, runs
@@ -542,7 +542,10 @@ class Backbone:
                 if i >= 2:
                     g0s.wait_event(sl["ev_done"])        # step i-2 done with the slot
                 if i >= 1:                                # not under step i-1's cooperative PSHs
-                    for pr in slots[(i - 1) % 2]["runs"]:
+                    prev = slots[(i - 1) % 2]
+                    if any(getattr(pr, "psh_on_main", False) for pr in prev["runs"]):
+                        g0s.wait_event(prev["ev_done"])   # a PSH without an event: serial
+                    for pr in prev["runs"]:
                         pev = getattr(pr, "psh_event", None)
                         if pev is not None:
                             g0s.wait_event(pev)
