@@ -250,30 +250,86 @@ __device__ __forceinline__ TileInfo tile_info(const Params& P_, bool multi, int 
     return ti;
 }
 
-// Sequential exact path (the reference loop) for one batch, counters in smem.
-__device__ void sequential_batch(const Params& P_, int b, int pb0, int pb1, int32_t* ctr,
-                                 const int8_t* probe) {
-    const int W = P_.K + 1;
-    for (int c = 0; c < W; ++c) ctr[c] = 0;
-    for (int p = pb0; p < pb1; ++p) {
-        const int4 q = __ldcg(P_.pk + p);
-        int got = -1;
-        if (ctr[q.w] < P_.S) {
-            got = q.w;
-        } else {
-            for (int pi = 0; pi < P_.P && got < 0; ++pi) {
-                const int x = min(max(q.x + (int)probe[3 * pi + 0], 0), P_.vmax);
-                const int y = min(max(q.y + (int)probe[3 * pi + 1], 0), P_.vmax);
-                const int z = min(max(q.z + (int)probe[3 * pi + 2], 0), P_.vmax);
-                const int c = hash_bucket1(x, y, z, P_.hp);
-                if (c >= 0 && ctr[c] < P_.S) got = c;
+// Exact sequential semantics, 32 points at a time (one warp): the App. A
+// fixed point on a window.  With the counters ctr at the window start, lane i
+// takes the first candidate c with ctr[c] + #{j < i : D_j = c} < S (home,
+// then the clamped probes, strict -1 skipped), else the recycle bucket K.
+// Iterate from D = home until no lane changes: lane i is final after i + 1
+// iterations (its decision depends only on lanes j < i), so at most 33
+// iterations.  Then offset = ctr[D] + rank among the earlier lanes with the
+// same D, and ctr[c] += takers.  ctr may live in shared or global memory
+// (only this warp touches it); sD is this warp's 32-int scratch.
+// Replaces the reference's per-point loop (bw/_kernels.py:41-90) with a
+// 32-wide window; the decisions are identical (same induction as App. A).
+__device__ void warp_exact_window(const Params& P_, int32_t* ctr, const int4 q, bool active,
+                                  int* sD, const int8_t* probe, int& d_out, int& off_out) {
+    const int lane = threadIdx.x & 31;
+    const int S = P_.S;
+    int D = active ? q.w : -1;
+    for (int iter = 0; iter < 34; ++iter) {
+        sD[lane] = D;
+        __syncwarp();
+        int nd = -1;
+        if (active) {
+            // room for this lane in c given the earlier lanes' current choices
+            auto room = [&](int c) -> bool {
+                const int base = ctr[c];
+                if (base >= S) return false;                // full at the window start
+                if (base + lane < S) return true;           // < lane earlier takers fit
+                int cnt = 0;
+                for (int j = 0; j < lane; ++j) cnt += (sD[j] == c);
+                return base + cnt < S;
+            };
+            if (room(q.w)) {
+                nd = q.w;
+            } else {
+                for (int pi = 0; pi < P_.P; ++pi) {
+                    const int x = min(max(q.x + (int)probe[3 * pi + 0], 0), P_.vmax);
+                    const int y = min(max(q.y + (int)probe[3 * pi + 1], 0), P_.vmax);
+                    const int z = min(max(q.z + (int)probe[3 * pi + 2], 0), P_.vmax);
+                    const int c = hash_bucket1(x, y, z, P_.hp);
+                    if (c >= 0 && room(c)) {
+                        nd = c;
+                        break;
+                    }
+                }
+                if (nd < 0) nd = P_.K;
             }
-            if (got < 0) got = P_.K;
         }
-        P_.D[p] = got;
-        P_.off[p] = ctr[got]++;
+        const bool ch = __any_sync(0xffffffffu, nd != D);
+        __syncwarp();                                       // sD reads done
+        D = nd;
+        if (!ch) break;
     }
-    for (int c = 0; c < W; ++c) P_.counts[(int64_t)b * W + c] = ctr[c];
+    const unsigned m = __match_any_sync(0xffffffffu, D);
+    off_out = active ? ctr[D] + __popc(m & lanemask_lt()) : 0;
+    d_out = D;
+    __syncwarp();
+    if (active && lane == __ffs(m) - 1) ctr[D] += __popc(m);
+    __syncwarp();
+}
+
+// One batch of the sorted domain [pb0, pb1) by one warp, counters in ctr
+// (W ints; written to counts[b] at the end).
+__device__ void warp_exact_batch(const Params& P_, int b, int pb0, int pb1, int32_t* ctr,
+                                 int* sD, const int8_t* probe) {
+    const int lane = threadIdx.x & 31;
+    const int W = P_.K + 1;
+    for (int c = lane; c < W; c += 32) ctr[c] = 0;
+    __syncwarp();
+    for (int w0 = pb0; w0 < pb1; w0 += 32) {
+        const int p = w0 + lane;
+        const bool active = p < pb1;
+        const int4 q = active ? __ldcg(P_.pk + p) : make_int4(0, 0, 0, 0);
+        int d, o;
+        warp_exact_window(P_, ctr, q, active, sD, probe, d, o);
+        if (active) {
+            P_.D[p] = d;
+            P_.off[p] = o;
+        }
+    }
+    __syncwarp();
+    for (int c = lane; c < W; c += 32) P_.counts[(int64_t)b * W + c] = ctr[c];
 }
 
 // --------------------------------------------------------------- the kernel
@@ -561,13 +617,15 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     }
 
     if (fallback) {
-        // Exact sequential path: one thread per batch, counters in smem.
-        if (blockIdx.x == 0 && tid == 0) {
-            int32_t* ctr = reinterpret_cast<int32_t*>(sh);
-            for (int b = 0; b < P_.nbatch; ++b) {
+        // Exact path past max_sweeps: one warp per batch (warp 0 of CTAs
+        // b, b + grid, ...), 32-point windows, counters in shared memory.
+        __shared__ int sD[32];
+        if (warp == 0) {
+            int32_t* ctr = reinterpret_cast<int32_t*>(sh);   // W ints <= the histogram area
+            for (int b = blockIdx.x; b < P_.nbatch; b += gridDim.x) {
                 const int pb0 = multi ? __ldcg(P_.bstart + b) : 0;
                 const int pb1 = multi ? __ldcg(P_.bstart + b + 1) : n;
-                sequential_batch(P_, b, pb0, pb1, ctr, probe);
+                warp_exact_batch(P_, b, pb0, pb1, ctr, sD, probe);
             }
         }
         grid.sync();
@@ -680,45 +738,75 @@ extern "C" size_t f3d_psh_workspace_size(int64_t n, int32_t nbatch, int32_t K) {
     return psh::layout(n, nbatch, K, psh::kMaxSweepsCap).total;
 }
 
-// Fully sequential single-thread kernel for bucket counts beyond the smem
-// histogram limit: the reference loop verbatim, counters in global memory.
-__global__ void psh_sequential_kernel(psh::Params P_) {
+// Bucket counts beyond the shared-memory histogram limit: one warp per batch
+// over the original order (32-index windows, lanes of other batches idle),
+// counters in the batch's slice of counts (global).  Then one CTA scans the
+// slot counts and writes dest.
+__global__ void __launch_bounds__(32) psh_warp_exact_kernel(psh::Params P_) {
+    __shared__ int sD[32];
+    __shared__ int8_t probe[psh::kMaxProbes * 3];
+    const int lane = threadIdx.x;
+    const int b = blockIdx.x;
     const int W = P_.K + 1;
-    P_.n = (int)dyn_n(P_.n, P_.n_dev);
-    for (int s = 0; s < P_.nbatch * W; ++s) P_.counts[s] = 0;
-    for (int i = 0; i < P_.n; ++i) {
-        const int b = P_.batch ? P_.batch[i] : 0;
-        int32_t* ctr = P_.counts + (int64_t)b * W;
-        const int x = P_.vox[3 * (int64_t)i], y = P_.vox[3 * (int64_t)i + 1],
-                  z = P_.vox[3 * (int64_t)i + 2];
-        int got = -1;
-        const int h = P_.home[i];
-        if (ctr[h] < P_.S) {
-            got = h;
-        } else {
-            for (int pi = 0; pi < P_.P && got < 0; ++pi) {
-                const int xx = min(max(x + (int)P_.probe[3 * pi + 0], 0), P_.vmax);
-                const int yy = min(max(y + (int)P_.probe[3 * pi + 1], 0), P_.vmax);
-                const int zz = min(max(z + (int)P_.probe[3 * pi + 2], 0), P_.vmax);
-                const int c = hash_bucket1(xx, yy, zz, P_.hp);
-                if (c >= 0 && ctr[c] < P_.S) got = c;
-            }
-            if (got < 0) got = P_.K;
+    const int n = (int)dyn_n(P_.n, P_.n_dev);
+    for (int i = lane; i < P_.P * 3; i += 32) probe[i] = P_.probe[i];
+    int32_t* ctr = P_.counts + (int64_t)b * W;
+    for (int c = lane; c < W; c += 32) ctr[c] = 0;
+    __syncwarp();
+    for (int w0 = 0; w0 < n; w0 += 32) {
+        const int i = w0 + lane;
+        bool active = i < n;
+        if (active && P_.batch) {
+            const int bi = P_.batch[i];
+            if (b == 0 && (bi < 0 || bi >= P_.nbatch)) atomicOr(P_.info + psh::INFO_BATCH_ERR, 1);
+            active = bi == b;
         }
-        P_.bucket_id[i] = got;
-        P_.bucket_offset[i] = ctr[got]++;
+        if (!__any_sync(0xffffffffu, active)) continue;
+        int4 q = make_int4(0, 0, 0, 0);
+        if (active)
+            q = make_int4(P_.vox[3 * (int64_t)i], P_.vox[3 * (int64_t)i + 1],
+                          P_.vox[3 * (int64_t)i + 2], P_.home[i]);
+        int d, o;
+        psh::warp_exact_window(P_, ctr, q, active, sD, probe, d, o);
+        if (active) {
+            P_.bucket_id[i] = d;
+            P_.bucket_offset[i] = o;
+        }
     }
-    int run = 0;
-    for (int s = 0; s < P_.nbatch * W; ++s) {
-        P_.base[s] = run;
-        run += P_.counts[s];
+}
+
+__global__ void __launch_bounds__(1024) psh_exact_finish_kernel(psh::Params P_) {
+    __shared__ int s_warp[32];
+    __shared__ int s_carry;
+    const int W = P_.K + 1;
+    const int nslots = P_.nbatch * W;
+    const int n = (int)dyn_n(P_.n, P_.n_dev);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int s0 = 0; s0 < nslots; s0 += 1024) {
+        const int s = s0 + tid;
+        const int v = s < nslots ? P_.counts[s] : 0;
+        const int incl = warp_incl_scan(v);
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) s_warp[lane] = warp_incl_scan(s_warp[lane]);
+        __syncthreads();
+        const int excl = s_carry + (warp ? s_warp[warp - 1] : 0) + incl - v;
+        if (s < nslots) P_.base[s] = excl;
+        __syncthreads();
+        if (tid == 0) s_carry += s_warp[31];
+        __syncthreads();
     }
-    for (int i = 0; i < P_.n; ++i) {
+    for (int i = tid; i < n; i += 1024) {
         const int b = P_.batch ? P_.batch[i] : 0;
+        if (b < 0 || b >= P_.nbatch) continue;
         P_.dest[i] = P_.base[(int64_t)b * W + P_.bucket_id[i]] + P_.bucket_offset[i];
     }
-    P_.info[0] = 0;
-    P_.info[1] = 2;
+    if (tid == 0) {
+        P_.info[0] = 0;
+        P_.info[1] = 2;
+    }
 }
 
 namespace {
@@ -816,7 +904,9 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
     F3D_CUDA_TRY(f3d_zero_i32(info_out, 4, st));
     const int nbins = nbatch > 1 ? std::max(K + 1, nbatch) : K + 1;
     if (nbins > psh::kMaxBins) {
-        psh_sequential_kernel<<<1, 1, 0, st>>>(p);
+        psh_warp_exact_kernel<<<nbatch, 32, 0, st>>>(p);
+        F3D_LAUNCH_CHECK();
+        psh_exact_finish_kernel<<<1, 1024, 0, st>>>(p);
         F3D_LAUNCH_CHECK();
         return F3D_OK;
     }

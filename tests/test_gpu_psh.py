@@ -166,6 +166,48 @@ def test_psh_large_k_sequential_path():
     np.testing.assert_array_equal(a.bucket_offset, offs)
 
 
+def test_psh_warp_exact_fallback_is_fast_and_exact():
+    """Past max_sweeps (here 1) the exact path is one warp per batch over
+    32-point windows: a 4-batch shell-like instance
+    with heavy recycling finishes in milliseconds and equals the oracle."""
+    import time
+    import torch
+    r = np.random.default_rng(11)
+    n = 200_000
+    vox = r.integers(0, 24, size=(n, 3))          # dense: many full buckets, recycling
+    batch = np.sort(r.integers(0, 4, size=n))
+    cfg = F.HashConfig("zorder-div", K=512, S_div=64)
+    FB._assign(vox[:4000], batch[:4000] * 0, cfg, 64, None, max_sweeps=1)   # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a = FB._assign(vox, batch, cfg, 64, None, max_sweeps=1)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    assert int(a._dev["info"][1]) == 1
+    ids, offs, counts, base = O.psh_assign(vox, batch, "zorder-div", 512, 64, S_div=64)
+    np.testing.assert_array_equal(a.bucket_id, ids)
+    np.testing.assert_array_equal(a.bucket_offset, offs)
+    np.testing.assert_array_equal(a.counts, counts)
+    assert (counts.reshape(4, -1)[:, -1] > 0).all()   # recycling happened
+    assert dt < 2.0, dt
+
+
+def test_psh_large_k_multibatch_exact():
+    """K + 1 beyond the shared-memory histogram: one warp per batch over the
+    original order (unsorted batch ids), then the base / dest pass."""
+    r = np.random.default_rng(6)
+    n = 50_000
+    vox = r.integers(0, 40, size=(n, 3))
+    batch = r.integers(0, 3, size=n)
+    cfg = F.HashConfig("zorder-mod", K=20000)
+    a = F.assign_buckets(vox, batch, cfg, S=2)
+    ids, offs, counts, base = O.psh_assign(vox, batch, "zorder-mod", 20000, 2)
+    np.testing.assert_array_equal(a.bucket_id, ids)
+    np.testing.assert_array_equal(a.bucket_offset, offs)
+    np.testing.assert_array_equal(a.counts, counts)
+    np.testing.assert_array_equal(a.dest_index(), base[batch * 20001 + ids] + offs)
+
+
 def test_two_stage_equals_one_stage():
     r = np.random.default_rng(777)
     for i in range(10):
