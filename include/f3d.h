@@ -180,7 +180,9 @@ int f3d_bswin_attention(const void *q, const void *k, const void *v, int64_t ld_
  * tensor maps; 0 disables TMA).  lse (nullable, training): lse[row*ld_lse + h] =
  * log2-domain logsumexp of the row's scaled scores, so P = exp2(s*scale*log2e -
  * lse).  Requires dh % 8 == 0, dh <= 128, 16-byte aligned q/k/v and row strides
- * that are multiples of 8; no mask. */
+ * that are multiples of 8; no mask.  With live (8 words from f3d_plan_round)
+ * the CTAs take work items from the counter live[4] (dynamic balance);
+ * without it, item i goes to CTA i mod grid. */
 int f3d_bswin_attention_tc(const void *q, const void *k, const void *v, int64_t ld_q,
                            int64_t ld_k, int64_t ld_v, void *o, int64_t ld_o, int out_f32, int H,
                            int dh, const int32_t *scope_seg, const int32_t *scope_nseg,
@@ -198,8 +200,12 @@ int f3d_attention_tc_qstep(int dh);
  * segment arrays hold nscopes*W entries (fixed stride W per scope); work
  * holds max_work (scope, q_start) pairs with q_start stepping by qstep
  * (f3d_attention_tc_qstep for the tcgen05 kernel); live receives [nwork,
- * nlive, max_len, status] with status bits 1 (window_w > nb, ConfigError),
- * 2 (nb > nb_cap), 4 (work list truncated).  off = (t*shift) mod W. */
+ * nlive, max_len, status, 0, 0, -, -] (8 words) with status bits 1 (window_w >
+ * nb, ConfigError), 2 (nb > nb_cap), 4 (work list truncated); words 4-5 are
+ * the tcgen05 attention kernel's dynamic item counter and CTA-done counter
+ * (zeroed here, left zeroed by every attention launch: launches sharing one
+ * plan must be stream-ordered).  The work list holds every scope's full
+ * qstep groups first, then the partial last groups.  off = (t*shift) mod W. */
 int f3d_plan_round(const int32_t *counts, const int32_t *base, int K, int S, int nb_cap, int W,
                    int stride, int off, int nscopes, int32_t *scope_seg, int32_t *scope_nseg,
                    int32_t *seg_start, int32_t *seg_vstart, int32_t *scope_len,

@@ -280,7 +280,7 @@ class DeviceRoundPlan:
         self.seg_start, self.seg_vstart = take(ns * W), take(ns * W)
         self.scope_order = take(ns)
         self.work = take(2 * self.nwork).view(-1, 2)
-        self.live = take(4)
+        self.live = take(8)
         if _buf is not None:
             return                       # filled by all_rounds' single launch
         L.call("f3d_plan_round", L.ptr(counts_dev), L.ptr(base_dev), K, S, nb, W, stride,
@@ -292,7 +292,7 @@ class DeviceRoundPlan:
     @staticmethod
     def size_for(nb, W, stride, n, qstep):
         ns = -(-nb // (W * stride)) * stride
-        return 3 * ns + 2 * ns * W + ns + 2 * (n // qstep + ns) + 4
+        return 3 * ns + 2 * ns * W + ns + 2 * (n // qstep + ns) + 8
 
     @classmethod
     def all_rounds(cls, counts_dev, base_dev, K, S, nb, W, stride, shift, rounds, n, qstep=BLOCK_M):

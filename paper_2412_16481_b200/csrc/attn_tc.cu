@@ -73,9 +73,13 @@ __host__ __device__ constexpr int bn_for() { return DH <= 32 ? F3D_BN_SMALL : 64
 #endif
 // Q tiles per work item (one softmax warpgroup each)
 __host__ __device__ constexpr int nq_for_dh(int DH) { return DH <= 32 ? F3D_NQ_SMALL : 2; }
-constexpr int kLoadWarps = 3;     // warps 0-2
+constexpr int kLoadWarps = 1;     // warp 0
 constexpr int kLoadThreads = kLoadWarps * 32;
-constexpr int kMmaWarp = 3;       // completes warpgroup 0
+// Warps 1..NQ issue the MMAs of Q tile g = warp - 1 (one issuing thread each):
+// measured (tools/ubench/mma_ts.cu) one thread issues at most one M128 N<=64
+// tcgen05.mma per ~45 clk, two threads reach the tensor pipe's own rate --
+// one issuer for all Q tiles was the co-bottleneck at small head dims.
+constexpr int kMmaWarp = 3;       // last warp of warpgroup 0 (softmax warps follow)
 // Softmax column split: CS warps share each 32-row lane quarter of a Q tile
 // and take kBN/CS key columns each (row max / sum exchanged through shared
 // memory) -- more warps per SM sub-partition to hide the per-tile latencies
@@ -91,10 +95,11 @@ __host__ __device__ constexpr int threads_for() {
 constexpr float kRescale = 8.f;   // move the running max only when it grows by > 2^8
 constexpr int kMaps = 6;          // TMA maps: {q, k, v} x {first block, second block}
 // 1 pair in poly_every<DH>() uses ex2_poly (0: none).  Measured (config B
-// dh=24: 2 % faster with 1 in 4; config D dh=128: 7 % slower): the softmax is
-// issue-bound, not MUFU-bound, once dh >= 64.
+// dh=24, one round: 1 in 3 0.138 ms, 1 in 4 0.140, 1 in 2 0.146, none 0.154;
+// config D dh=128: 7 % slower): the softmax is issue-bound, not MUFU-bound,
+// once dh >= 64.
 #ifndef F3D_POLY_SMALL
-#define F3D_POLY_SMALL 4
+#define F3D_POLY_SMALL 3
 #endif
 #ifndef F3D_POLY_MID
 #define F3D_POLY_MID 0
@@ -154,6 +159,14 @@ struct Lay {
 };
 
 
+// Dynamic work distribution (when the plan's live words are given): warp 0
+// takes items from a global counter (live[4]) as it is about to load them and
+// hands them to the MMA / softmax warps through a ring of shared-memory slots.
+// The last CTA to finish resets the counters (live[4], live[5]) for the next
+// launch on the plan.  Measured without it (static item += gridDim.x): the
+// softmax warps of the busiest CTAs ran 15 % longer than the average.
+constexpr int kItemRing = 4;
+
 template <int DH>
 __host__ __device__ constexpr int nsb_for() {
     return nq_for_dh(DH) * (3 * bn_for<DH>() + DH) <= 512 ? 3 : 2;
@@ -197,9 +210,10 @@ struct Cfg {
     static constexpr int kOffQ = 0;
     static constexpr int kOffKV = kOffQ + NQB * NQ * kQBytes;
     static constexpr int kOffBar = kOffKV + kNst * 2 * kKVBytes;
-    static constexpr int kNumBars = 2 * NQB + 2 * kNst + (3 * NSB + 1) * NQ;
+    static constexpr int kNumBars = 2 * NQB + 2 * kNst + (3 * NSB + 1) * NQ + 2 * kItemRing;
+    // after the barriers: TMEM address word, kItemRing item slots
     // pair exchange: [NQ][4 quarters][2 parities][CS][32] row maxima, + row sums
-    static constexpr int kOffX = kOffBar + kNumBars * 8 + 16;
+    static constexpr int kOffX = kOffBar + kNumBars * 8 + 4 + 4 * kItemRing + 12;
     static constexpr int kSmem = kOffX + kXchg + 1024;   // + 1 KB alignment slack
     static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (NSB*g+b)*kBN
     static constexpr int kTmemO = NSB * NQ * kBN;       // O of tile g: kTmemO + g*DH
@@ -315,12 +329,48 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
     // after PV_g,t+1-NSB: so the barrier is never a phase behind either.
     uint64_t* pv_done = p_full + NSB * NQ;
     uint64_t* o_free = pv_done + NSB * NQ;       // [NQ] softmax -> MMA (O_g read out)
+    uint64_t* item_full = o_free + NQ;           // [kItemRing] warp 0 -> consumers
+    uint64_t* item_empty = item_full + kItemRing;   // [kItemRing] consumers -> warp 0
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+    volatile int* s_item = reinterpret_cast<volatile int*>(tmem_slot + 1);   // [kItemRing]
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const int total = (A.live ? __ldg(A.live) : A.nwork) * A.H;
+    const bool dyn = A.live != nullptr;
+    int32_t* sched = dyn ? const_cast<int32_t*>(A.live) + 4 : nullptr;   // [next item, CTAs done]
+    // consumers of each item: the NQ MMA issuers and every softmax warp
+    constexpr int kConsumers = NQ + 4 * NQ * CS;
+    // the CTA's item sequence: static round robin, or the ring filled by warp 0
+    uint32_t item_k = 0;
+    int item_static = blockIdx.x;
+    auto next_item = [&]() -> int {
+        if (!dyn) {
+            const int r = item_static;
+            item_static += gridDim.x;
+            return r < total ? r : -1;
+        }
+        const int slot = item_k % kItemRing;
+        const uint32_t ph = (item_k / kItemRing) & 1;
+        ++item_k;
+        if (warp == 0) {                       // producer
+            if (item_k > kItemRing) mbar_wait(item_empty + slot, ph ^ 1);
+            int r = 0;
+            if (lane == 0) {
+                r = atomicAdd(sched, 1);
+                if (r >= total) r = -1;
+                s_item[slot] = r;
+                mbar_arrive(item_full + slot);
+            }
+            return __shfl_sync(0xffffffffu, r, 0);
+        }
+        mbar_wait(item_full + slot, ph);
+        const int r = s_item[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(item_empty + slot);
+        return r;
+    };
     const bool ones = A.dh < DH;                 // V column dh = 1 -> O column dh = row sum
 #if F3D_EXPERIMENT == 3
     unsigned long long prof[24] = {0};
@@ -343,11 +393,11 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
     if (tid == 0) {
         for (int b = 0; b < NQB; ++b) {
             mbar_init(q_full + b, kLoadThreads + 1);
-            mbar_init(q_empty + b, 1);
+            mbar_init(q_empty + b, NQ);                  // one commit / arrive per issuer
         }
         for (int s = 0; s < kNst; ++s) {
             mbar_init(kv_full + s, kLoadThreads + 1);
-            mbar_init(kv_empty + s, 1);
+            mbar_init(kv_empty + s, NQ);
         }
         for (int g = 0; g < NQ; ++g) {
             for (int b = 0; b < NSB; ++b) {
@@ -356,6 +406,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
                 mbar_init(pv_done + NSB * g + b, 1);
             }
             mbar_init(o_free + g, 128 * CS);
+        }
+        for (int i = 0; i < kItemRing; ++i) {
+            mbar_init(item_full + i, 1);
+            mbar_init(item_empty + i, kConsumers);
         }
         fence_mbar_init();
         if (A.use_tma)
@@ -377,7 +431,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
     if (warp < kLoadWarps) {
         // ------------------------------------------------ loader warps
         uint32_t q_use = 0, kv_it = 0;
-        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        for (int item = next_item(); item >= 0; item = next_item()) {
             const Item it = decode<NQ, kBN>(A, item);
             const int qb = q_use % NQB;
             PROF_WAIT(10, mbar_wait(q_empty + qb, ((q_use / NQB) & 1) ^ 1));
@@ -434,12 +488,17 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
                 }
             }
         }
-    } else if (warp == kMmaWarp) {
-        // ------------------------------------------------ MMA warp
-        // The whole warp walks the schedule (warp-uniform control flow and
-        // waits); one elected lane issues every tcgen05.mma / commit.
+    } else if (warp <= kMmaWarp) {
+        // ------------------------------------------------ MMA issuers
+        // Warp 1 + g issues every MMA of Q tile g (warp-uniform control flow
+        // and waits; one elected lane issues every tcgen05.mma / commit).
+        // A K/V stage is released (kv_empty) once every issuer's MMAs on it
+        // completed; an issuer with no Q tile g in an item still takes part:
+        // it waits for each of the item's K/V stages to be full before
+        // arriving (so its arrival can never count toward an earlier phase).
         // Descriptors are built once: per tile only the 14-bit start-address
         // field moves (addresses < 2^18, so adding (bytes >> 4) never carries).
+        const int g = warp - 1;
         constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
         constexpr uint32_t idPV = idesc_bf16(kBM, DH, 0, 1);
         // K-major Q / K: rows of SW bytes, 8-row groups SBO = 8*SW apart
@@ -450,22 +509,37 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
         constexpr uint32_t kStageD = (2 * C::kKVBytes) >> 4;   // descriptor step per K/V stage
         constexpr uint32_t kQD = C::kQBytes >> 4;              // per Q tile
         uint32_t q_use = 0, kv_it = 0;
-        uint32_t tg[NQ], ig[NQ];             // tiles / items processed by group g so far
-#pragma unroll
-        for (int g = 0; g < NQ; ++g) tg[g] = ig[g] = 0;
-        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        uint32_t tg = 0, ig = 0;             // tiles / items of Q tile g processed so far
+        if (g < NQ) {
+        for (int item = next_item(); item >= 0; item = next_item()) {
             const Item it = decode<NQ, kBN>(A, item);
             const int qb = q_use % NQB;
             PROF_WAIT(4, mbar_wait(q_full + qb, (q_use / NQB) & 1));
             tc_fence_after();
-            const uint64_t dq = dQ + (uint64_t)(qb * NQ * kQD);
-            // S_g,j -> TMEM buffer (tg[g]+j)%NSB, which last held P_g,j-NSB:
-            // PV_g,j-NSB was issued before (tcgen05.mma executes in order).
-            auto issue_S = [&](int g, int j) {
+            auto wait_kv = [&](int j) {
+                const uint32_t kvi = kv_it + j;
+                PROF_WAIT(5, mbar_wait(kv_full + kvi % kNst, (kvi / kNst) & 1));
+                tc_fence_after();
+            };
+            if (g >= it.nq) {
+                // no Q tile g here: release the Q buffer and each K/V stage
+                if (lane == 0) mbar_arrive(q_empty + qb);
+                for (int j = 0; j < it.nt; ++j) {
+                    wait_kv(j);
+                    if (lane == 0) mbar_arrive(kv_empty + (kv_it + j) % kNst);
+                }
+                __syncwarp();
+                ++q_use;
+                kv_it += it.nt;
+                continue;
+            }
+            const uint64_t dqg = dQ + (uint64_t)(qb * NQ * kQD + g * kQD);
+            // S_g,j -> TMEM buffer (tg+j)%NSB, which last held P_g,j-NSB:
+            // PV_g,j-NSB was issued before by this thread (in-order execution).
+            auto issue_S = [&](int j) {
                 const uint32_t s = (kv_it + j) % kNst;
-                const uint32_t b = (tg[g] + j) % NSB;
+                const uint32_t b = (tg + j) % NSB;
                 const uint64_t dk = dK + (uint64_t)(s * kStageD);
-                const uint64_t dqg = dq + (uint64_t)(g * kQD);
                 const uint32_t d = tmem + C::kTmemS + (NSB * g + b) * kBN;
                 if (elect_one()) {
 #pragma unroll
@@ -480,16 +554,9 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
                 }
                 __syncwarp();
             };
-            auto wait_kv = [&](int j) {
-                const uint32_t kvi = kv_it + j;
-                PROF_WAIT(5, mbar_wait(kv_full + kvi % kNst, (kvi / kNst) & 1));
-                tc_fence_after();
-            };
             for (int j = 0; j < NSB && j < it.nt; ++j) {
                 wait_kv(j);
-#pragma unroll
-                for (int g = 0; g < NQ; ++g)
-                    if (g < it.nq) issue_S(g, j);
+                issue_S(j);
             }
             if (it.nt <= NSB) {
                 if (elect_one()) umma_commit(q_empty + qb);
@@ -498,42 +565,35 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
             for (int j = 0; j < it.nt; ++j) {
                 const uint32_t s = (kv_it + j) % kNst;
                 const uint64_t dv = dV + (uint64_t)(s * kStageD);
-#pragma unroll
-                for (int g = 0; g < NQ; ++g) {
-                    if (g >= it.nq) break;
-                    if (j == 0 && ig[g] > 0) PROF_WAIT(7, mbar_wait(o_free + g, (ig[g] - 1) & 1));
-                    const uint32_t t = tg[g] + j;     // P_g,j in TMEM buffer t % NSB
-                    PROF_WAIT(6, mbar_wait(p_full + NSB * g + t % NSB, (t / NSB) & 1));
-                    tc_fence_after();
-                    const uint32_t pa = tmem + C::kTmemS + (NSB * g + t % NSB) * kBN;
-                    const uint32_t od = tmem + C::kTmemO + g * DH;
-                    if (elect_one()) {
-#pragma unroll
-                        for (int k = 0; k < kBN / 16; ++k)   // 16 keys = two 8-key groups
-                            umma_f16_ts(od, pa + k * 8, dv + (uint64_t)((16 * L::SW * k) >> 4), idPV,
-                                        (j > 0 || k > 0) ? 1u : 0u);
-                        umma_commit(pv_done + NSB * g + t % NSB);
-                    }
-                    __syncwarp();
-                    if (j + NSB < it.nt) {
-                        if (g == 0) wait_kv(j + NSB);   // after PV_0,j is on its way
-                        issue_S(g, j + NSB);
-                    }
-                }
+                if (j == 0 && ig > 0) PROF_WAIT(7, mbar_wait(o_free + g, (ig - 1) & 1));
+                const uint32_t t = tg + j;     // P_g,j in TMEM buffer t % NSB
+                PROF_WAIT(6, mbar_wait(p_full + NSB * g + t % NSB, (t / NSB) & 1));
+                tc_fence_after();
+                const uint32_t pa = tmem + C::kTmemS + (NSB * g + t % NSB) * kBN;
+                const uint32_t od = tmem + C::kTmemO + g * DH;
                 if (elect_one()) {
-                    umma_commit(kv_empty + s);
-                    if (j + NSB + 1 == it.nt) umma_commit(q_empty + qb);   // last S just issued
+#pragma unroll
+                    for (int k = 0; k < kBN / 16; ++k)   // 16 keys = two 8-key groups
+                        umma_f16_ts(od, pa + k * 8, dv + (uint64_t)((16 * L::SW * k) >> 4), idPV,
+                                    (j > 0 || k > 0) ? 1u : 0u);
+                    umma_commit(pv_done + NSB * g + t % NSB);
+                    umma_commit(kv_empty + s);         // S_g,j and PV_g,j read stage s
                 }
                 __syncwarp();
+                if (j + NSB < it.nt) {
+                    wait_kv(j + NSB);
+                    issue_S(j + NSB);
+                    if (j + NSB + 1 == it.nt) {          // last S of the item issued
+                        if (elect_one()) umma_commit(q_empty + qb);
+                        __syncwarp();
+                    }
+                }
             }
             ++q_use;
             kv_it += it.nt;
-#pragma unroll
-            for (int g = 0; g < NQ; ++g)
-                if (g < it.nq) {
-                    tg[g] += it.nt;
-                    ++ig[g];
-                }
+            tg += it.nt;
+            ++ig;
+        }
         }
     } else {
         // ------------------------------------------------ softmax warpgroups
@@ -559,16 +619,28 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
             return fmaxf(v, xg[(slot * CS + (hh ^ 1)) * 32 + lane]);
         };
         uint32_t tg = 0;
-        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        for (int item = next_item(); item >= 0; item = next_item()) {
+            PROF_MARK(td0);
             const Item it = decode<NQ, kBN>(A, item);
             if (g >= it.nq) continue;                     // this Q tile is past the scope
+            PROF_MARK(td1);
+            PROF_ADD(20, td0, td1);
             float ms = -INFINITY, l = 0.f;                // running max (scaled, log2), sum
+            // every row of this warp is past the scope end (the scope's last
+            // Q tile): nothing to compute or store -- the warp only keeps the
+            // barrier protocol (its P / O rows are never read for output)
+            const bool dead = it.q0 + g * kBM + quarter * 32 >= it.m;
             for (int j = 0; j < it.nt; ++j) {
                 const uint32_t t = tg + j;
                 const int b = t % NSB;
                 const uint32_t sb = tmem + lane_base + C::kTmemS + (NSB * g + b) * kBN;
                 PROF_WAIT(1, mbar_wait(s_full + NSB * g + b, (t / NSB) & 1));
                 tc_fence_after();
+                if (dead) {
+                    tc_fence_before();
+                    mbar_arrive(p_full + NSB * g + b);
+                    continue;
+                }
                 uint32_t x[KC];
                 {
                     PROF_MARK(tl0);
@@ -687,7 +759,14 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
                 const uint32_t tl = tg + it.nt - 1;
                 PROF_WAIT(3, mbar_wait(pv_done + NSB * g + tl % NSB, (tl / NSB) & 1));
             }
+            PROF_MARK(tq0);
             tc_fence_after();
+            if (dead) {
+                tc_fence_before();
+                mbar_arrive(o_free + g);
+                tg += it.nt;
+                continue;
+            }
             float lsum = l;
             if (ones) {
                 uint32_t y[16];
@@ -754,7 +833,11 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
             tc_fence_before();
             mbar_arrive(o_free + g);
             tg += it.nt;
+            PROF_MARK(tq1);
+            PROF_ADD(21, tq0, tq1);
         }
+        PROF_MARK(tend);
+        PROF_ADD(22, t_start, tend);
     }
 #if F3D_EXPERIMENT == 3
     if (lane == 0) {
@@ -767,6 +850,16 @@ __global__ void __launch_bounds__(threads_for<DH>(), 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
+    if (dyn && tid == 0) {
+        // this CTA took its last item (the counter is past total): the last
+        // CTA to get here resets the scheduler words for the next launch
+        __threadfence();
+        if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+            __threadfence();
+        }
+    }
 }
 
 // ------------------------------------------------------------- host side

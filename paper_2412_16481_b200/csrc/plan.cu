@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) plan_round_kernel(
         }
         int tot_live, tot_work;
         const int is_live = v > 0 ? 1 : 0;
-        const int nt = (v + qstep - 1) / qstep;
+        const int nt = v / qstep;                    // full query groups first
         const int pl = block_excl_scan(is_live, tot_live, sh) + carry_live;
         const int pw = block_excl_scan(nt, tot_work, sh) + carry_work;
         if (is_live) scope_order[pl] = s;
@@ -116,6 +116,20 @@ __global__ void __launch_bounds__(kThreads) plan_round_kernel(
         carry_live += tot_live;
         carry_work += tot_work;
     }
+    // then every scope's partial last group (fewer query rows): with the
+    // attention kernels' dynamic item counter the smaller items come last
+    for (int s0 = 0; s0 < nscopes; s0 += kThreads) {
+        const int s = s0 + threadIdx.x;
+        const int v = s < nscopes ? scope_len[s] : 0;   // written by this thread above
+        const int part = (v % qstep) ? 1 : 0;
+        int tot_part;
+        const int pw = block_excl_scan(part, tot_part, sh) + carry_work;
+        if (part && pw < max_work) {
+            work[2 * pw] = s;
+            work[2 * pw + 1] = (v / qstep) * qstep;
+        }
+        carry_work += tot_part;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         live[0] = min(carry_work, max_work);
@@ -124,6 +138,8 @@ __global__ void __launch_bounds__(kThreads) plan_round_kernel(
         // 1: window_w exceeds num_buckets (bw/attention.py:104); 2: table
         // larger than the capacity the host planned for; 4: work list cut
         live[3] = (W > nb ? 1 : 0) | (nb > nb_cap ? 2 : 0) | (carry_work > max_work ? 4 : 0);
+        live[4] = 0;      // attention scheduler: next item, CTAs done (reset by the kernel)
+        live[5] = 0;
     }
 }
 

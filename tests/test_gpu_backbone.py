@@ -256,3 +256,34 @@ def test_stage_boundary_fusions_are_bit_identical():
     finally:
         B.SCATTER_LN, B.POOL_RESIDUAL = old
     assert torch.equal(a, b) and torch.equal(ca, cb)
+
+
+def test_attention_dynamic_scheduler_repeats_and_resets():
+    """The tcgen05 kernel takes work items from the device plan's counter
+    (live[4]); every launch leaves live[4:6] zeroed, repeated launches on one
+    plan are bit-identical, and the static schedule (no live words) agrees."""
+    from paper_2412_16481_b200.attention import attend, qstep_for
+    r = np.random.default_rng(4)
+    K, S, W, d, H = 96, 256, 2, 96, 4
+    counts = r.integers(S // 2, S + 1, size=K + 1)
+    counts[K] = 300
+    base = O.exclusive_scan(counts)
+    n = int(counts.sum())
+    starts, lens = split_table(counts, base, K, S)
+    cd = torch.tensor(counts, dtype=torch.int32, device="cuda")
+    bd = torch.tensor(base, dtype=torch.int32, device="cuda")
+    qs = qstep_for(d // H)
+    dp = A.DeviceRoundPlan(cd, bd, K, S, len(starts), W, 1, 1, 0, n, qstep=qs)
+    q, k, v = (torch.randn(n, d, device="cuda").to(torch.bfloat16) for _ in range(3))
+    outs = []
+    for _ in range(3):
+        o = torch.zeros(n, d, dtype=torch.bfloat16, device="cuda")
+        attend(q, k, v, o, dp, H, d // H)
+        outs.append(o)
+        assert dp.live.cpu().numpy()[4:6].tolist() == [0, 0]
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    hp = A.RoundPlan(A.plan_arrays(starts, lens, A.round_members(len(starts), W, 1, 1, 0), qs),
+                     qstep=qs)
+    o = torch.zeros(n, d, dtype=torch.bfloat16, device="cuda")
+    attend(q, k, v, o, hp, H, d // H)
+    assert torch.equal(o, outs[0])

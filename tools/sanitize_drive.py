@@ -17,7 +17,7 @@ from paper_2412_16481_b200.backbone import Backbone, StageConfig  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 r = np.random.default_rng(0)
-coords = F.synth_cloud(7, 4096, "uniform-box")
+coords = F.synth_cloud(7, 4096, "uniform-box").coords
 vox = F.remap_nonnegative(F.voxelize(F.PointCloud(coords), F.VoxelGrid(1 / 64)))
 cfg = F.HashConfig("zorder-div", K=40, S_div=6554)
 if which in ("all", "psh"):
