@@ -387,6 +387,25 @@ int f3d_colsum(const void *x, int is_bf16, int64_t ldx, int64_t n, int d, float 
 int f3d_softmax_bwd(const float *T, const void *P, const float *rowv, const int32_t *len, int B,
                     int M, double scale_log2, double scale, int mode, void *out, void *stream);
 
+/* Fused bucket-swin attention backward (training; the gradient of
+ * bw/attention.py:188-268 per scope, which the reference does not provide):
+ * dQ, dK, dV (fp32, head h at column h*dh, written at the fixed rows) from the
+ * forward's bf16 q/k/v, the bf16 upstream gradient dout and the forward's
+ * log2-domain row logsumexp lse (f3d_bswin_attention_tc's lse output), for the scopes
+ * of one round (the same scope tables as the forward; nscopes / max_len are
+ * upper bounds, empty scopes are skipped on the device).  Never forms an
+ * m x m tile: a query-block kernel computes D = sum_j P dP / sum_j P per
+ * (row, head) into the caller's delta buffer (rows x ld_delta fp32) and dQ,
+ * then a key-block kernel accumulates dK, dV over the scope's query blocks
+ * (bf16 mma.sync, fp32 accumulation).  Requires dh % 8 == 0, 8 <= dh <= 32. */
+int f3d_attn_bwd(const void *q, const void *k, const void *v, const void *dout, int64_t ld_q,
+                 int64_t ld_k, int64_t ld_v, int64_t ld_do, const float *lse, int64_t ld_lse,
+                 float *delta, int64_t ld_delta, float *dq, int64_t ld_dq, float *dk,
+                 int64_t ld_dk, float *dv, int64_t ld_dv, int H, int dh,
+                 const int32_t *scope_seg, const int32_t *scope_nseg, const int32_t *seg_start,
+                 const int32_t *seg_vstart, const int32_t *scope_len, int nscopes, int max_len,
+                 void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,9 +48,12 @@ SCATTER_LN = os.environ.get("F3D_SCATTER_LN", "1") == "1"
 # F3D_POOL_RESIDUAL=0: a pooled stage's last residual as its own row pass
 POOL_RESIDUAL = os.environ.get("F3D_POOL_RESIDUAL", "1") == "1"
 NEXT_PROLOGUE_SIDE = os.environ.get("F3D_NEXT_PROLOGUE_SIDE", "1") == "1"
-# F3D_FUSED_PSH=0: voxel hash and PSH as separate launches (f3d_voxel_hash +
-# f3d_psh_assign) instead of the one fused cooperative launch
-FUSED_PSH = os.environ.get("F3D_FUSED_PSH", "1") == "1"
+# F3D_FUSED_PSH=1: voxel hash + PSH as one cooperative launch
+# (f3d_psh_assign_coords) instead of f3d_voxel_hash + f3d_psh_assign.  Opt-in:
+# measured 1.087 vs 1.069 ms per config-B step (its extra grid barrier and
+# the all-CTA reduction of the per-CTA extrema cost more than the launches
+# the fusion saves)
+FUSED_PSH = os.environ.get("F3D_FUSED_PSH", "0") == "1"
 
 
 @dataclass(frozen=True)

@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     // over the still-eligible ids of the pass's tier) and committing goes on;
     // only an exhausted tier ends the pass and rebuilds the list.
     for (int q0 = 0; q0 < nqueue;) {
+        __syncwarp();                        // the previous pass's elig reads are done
         // eligible ids of this pass: under-filled new ids, else any under-filled
         int ne = 0;
         for (int j0 = nalloc; j0 < target; j0 += 32) {
@@ -339,18 +340,27 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
             }
         }
         const int need = rho - S.sizes[full_t];
+        // members of donor in index order (< rho of them), 32 rows per ballot,
+        // into the (now free) step-3 queue
+        int nm = 0;
+        for (int base = 0; base < m && nm < 64; base += 32) {
+            const int i = base + lane;
+            const bool in = i < m && S.sub[i] == donor;
+            const unsigned b = __ballot_sync(0xffffffffu, in);
+            if (in && nm + __popc(b & lt) < 64) S.qrow[nm + __popc(b & lt)] = (uint16_t)i;
+            nm += __popc(b);
+        }
+        nm = min(nm, 64);
+        __syncwarp();
         if (lane == 0) {
-            // members of donor in index order (< rho of them), stable by distance
+            // stable by distance to the fullest id's seed
             int mem[64];
             double md[64];
-            int nm = 0;
             const double* cs = S.cc[S.seeds[full_t]];
-            for (int i = 0; i < m && nm < 64; ++i)
-                if (S.sub[i] == donor) {
-                    mem[nm] = i;
-                    md[nm] = dist3(S.cc[i], cs);
-                    ++nm;
-                }
+            for (int a = 0; a < nm; ++a) {
+                mem[a] = S.qrow[a];
+                md[a] = dist3(S.cc[mem[a]], cs);
+            }
             // stable insertion sort by distance
             for (int a = 1; a < nm; ++a) {
                 const int mi = mem[a];

@@ -75,6 +75,7 @@ struct Params {
     int32_t* bstart;   // batch -> first sorted position, nbatch + 1
     int32_t* flags;    // max_sweeps + 2 "changed" words
     int max_tiles;
+    int base_in_smem;    // nbatch*(K+1) ints of dynamic smem past the histograms
     // fused voxelize + remap + hash (f3d_psh_assign_coords; single batch):
     // the kernel reads the float64 coordinates itself instead of vox / home
     const double* coords;
@@ -332,6 +333,37 @@ __device__ void warp_exact_batch(const Params& P_, int b, int pb0, int pb1, int3
     for (int c = lane; c < W; c += 32) P_.counts[(int64_t)b * W + c] = ctr[c];
 }
 
+// Exclusive scan of the nslots slot counts (block-wide): block 0 writes base
+// (when write_global), and s_base (nullable) receives a shared-memory copy.
+__device__ void slot_base(const Params& P_, int nslots, int32_t* s_base, bool write_global) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    __shared__ int s_part[kThreads];
+    __syncthreads();
+    const int per = (nslots + kThreads - 1) / kThreads;
+    const int a0 = min(tid * per, nslots), a1 = min(a0 + per, nslots);
+    int s = 0;
+    for (int i = a0; i < a1; ++i) s += __ldcg(P_.counts + i);
+    s_part[tid] = s;
+    __syncthreads();
+    if (tid < 32) {
+        int acc = 0;
+        for (int w = 0; w < kThreads / 32; ++w) {
+            const int v = s_part[w * 32 + lane];
+            const int incl = warp_incl_scan(v);
+            s_part[w * 32 + lane] = acc + incl - v;
+            acc += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncthreads();
+    int run = s_part[tid];
+    for (int i = a0; i < a1; ++i) {
+        if (write_global) P_.base[i] = run;
+        if (s_base) s_base[i] = run;
+        run += __ldcg(P_.counts + i);
+    }
+    __syncthreads();
+}
+
 // --------------------------------------------------------------- the kernel
 
 template <int PL, bool FUSED>
@@ -367,14 +399,26 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     __shared__ long long s_red[kWarps * 6];
     __shared__ long long s_gmin[3];
     long long qmax = LLONG_MIN;          // largest div quotient seen (stats[6])
+    // raw voxel coordinates of this thread's points of sweep 0, kept in
+    // registers across the extrema barrier when every CTA owns <= 1 tile
+    long long raw[kPerLane][3];
+    bool cached = false;
     if constexpr (FUSED) {
         long long v[6] = {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MIN, LLONG_MIN, LLONG_MIN};
-        for (int p = blockIdx.x * kThreads + tid; p < n; p += gridDim.x * kThreads) {
+        const int nt0 = cdiv_dev(n, kTile);
+        cached = nt0 <= (int)gridDim.x;
+        for (int t = blockIdx.x; t < nt0; t += gridDim.x) {   // the sweeps' tile mapping
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const long long x = vox_floor(P_.coords[3 * (int64_t)p + a], P_.org[a], P_.vs);
-                v[a] = min(v[a], x);
-                v[3 + a] = max(v[3 + a], x);
+            for (int j = 0; j < kPerLane; ++j) {
+                const int p = t * kTile + warp * kWarpSpan + j * 32 + lane;
+                if (p >= n) continue;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const long long x = vox_floor(P_.coords[3 * (int64_t)p + a], P_.org[a], P_.vs);
+                    raw[j][a] = x;
+                    v[a] = min(v[a], x);
+                    v[3 + a] = max(v[3 + a], x);
+                }
             }
         }
         block_extrema<6, 3>(v, s_red, P_.part + 8 * blockIdx.x);
@@ -477,6 +521,12 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     }
 
     // ------------------------------------------------------------ sweeps
+    const int nslots = P_.nbatch * W;
+    // the slot base scan in shared memory, past the histogram rows (host
+    // decides whether it fits)
+    const bool local_base = P_.base_in_smem != 0;
+    int32_t* s_base = reinterpret_cast<int32_t*>(sh + kWarps * stride);
+    bool converged0 = false;
     int32_t* Tc = P_.T0;
     int32_t* Tn = P_.T1;
     int sweep = 0;
@@ -504,7 +554,9 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
                             long long c3[3];
 #pragma unroll
                             for (int a = 0; a < 3; ++a)
-                                c3[a] = vox_floor(P_.coords[3 * (int64_t)p + a], P_.org[a], P_.vs) -
+                                c3[a] = (cached ? raw[j][a]
+                                                : vox_floor(P_.coords[3 * (int64_t)p + a], P_.org[a],
+                                                            P_.vs)) -
                                         s_gmin[a];
                             const long long lim = 1ll << P_.hp.bits;
                             q = make_int4(0, 0, 0, 0);
@@ -576,10 +628,23 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
                 if (lane == 0) {
                     P_.counts[col] = tot;
                     if (c < K && tot < P_.S) Tn[col] = INT_MAX;
+                    // sweep 0 (D = home): no bucket above S means every point
+                    // is among its home's first S takers -- D = home is the
+                    // fixed point and this sweep's offsets are final
+                    if (sweep == 0 && c < K && tot > P_.S) atomicOr(P_.flags, 1);
                 }
             }
         }
         grid.sync();
+        // sweep 0 without overflow: phase C writes the final outputs itself
+        // (base scanned locally from the counts), no further sweep or barrier
+        bool final_c = false;
+        if (sweep == 0 && local_base) {
+            if (tid == 0) s_flag = *((volatile int32_t*)P_.flags);
+            __syncthreads();
+            final_c = s_flag == 0;
+            if (final_c) slot_base(P_, nslots, s_base, blockIdx.x == 0);
+        }
         // Phase C: in-tile stable ranks -> offsets; S-th taker -> T
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const TileInfo ti = tile_info<kTile>(P_, multi, t, n);
@@ -603,11 +668,22 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
                 const int p = ti.p0 + warp * kWarpSpan + j * 32 + lane;
                 if (key[j] >= 0) {
                     const int o = __ldcg(hrow + key[j]) + rank[j];
-                    P_.off[p] = o;
-                    if (key[j] < K && o == P_.S - 1) Tn[(int64_t)ti.b * W + key[j]] = p;
+                    if (final_c) {
+                        const int i = multi ? __ldcg(P_.orig + p) : p;
+                        P_.bucket_id[i] = key[j];
+                        P_.bucket_offset[i] = o;
+                        P_.dest[i] = s_base[ti.b * W + key[j]] + o;
+                    } else {
+                        P_.off[p] = o;
+                        if (key[j] < K && o == P_.S - 1) Tn[(int64_t)ti.b * W + key[j]] = p;
+                    }
                 }
             }
             __syncthreads();
+        }
+        if (final_c) {
+            converged0 = true;
+            break;
         }
         grid.sync();
         int32_t* tmp = Tc;
@@ -635,55 +711,28 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     // The exclusive scan of the slot counts is small: when it fits in this
     // CTA's shared memory every CTA computes it itself (block 0 also writes
     // base) and goes straight on to its tiles' dest -- no grid barrier.
-    const int nslots = P_.nbatch * W;
-    const bool local_base = nslots <= hwords;            // hwords: 32-bit smem words
-    int32_t* s_base = reinterpret_cast<int32_t*>(sh);
-    if (local_base || blockIdx.x == 0) {
-        __syncthreads();                                 // sh is free (last use: the sweeps)
-        __shared__ int s_part[kThreads];
-        const int per = (nslots + kThreads - 1) / kThreads;
-        const int a0 = min(tid * per, nslots), a1 = min(a0 + per, nslots);
-        int s = 0;
-        for (int i = a0; i < a1; ++i) s += __ldcg(P_.counts + i);
-        s_part[tid] = s;
-        __syncthreads();
-        if (tid < 32) {
-            int acc = 0;
-            for (int w = 0; w < kThreads / 32; ++w) {
-                const int v = s_part[w * 32 + lane];
-                const int incl = warp_incl_scan(v);
-                s_part[w * 32 + lane] = acc + incl - v;
-                acc += __shfl_sync(0xffffffffu, incl, 31);
+    if (!converged0 && (local_base || blockIdx.x == 0))
+        slot_base(P_, nslots, local_base ? s_base : nullptr, blockIdx.x == 0);
+    if (blockIdx.x == 0 && tid == 0) {
+        P_.info[INFO_SWEEPS] = sweep + 1;
+        P_.info[INFO_FALLBACK] = fallback ? 1 : 0;
+        if constexpr (FUSED) {
+            // range statistics of the remapped voxels (min is 0 by construction)
+            long long mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN}, q = LLONG_MIN;
+            for (int b = 0; b < (int)gridDim.x; ++b) {
+                for (int a = 0; a < 3; ++a) mx[a] = max(mx[a], __ldcg(P_.part + 8 * b + 3 + a));
+                q = max(q, __ldcg(P_.part + 8 * b + 6));
             }
-        }
-        __syncthreads();
-        int run = s_part[tid];
-        for (int i = a0; i < a1; ++i) {
-            if (blockIdx.x == 0) P_.base[i] = run;
-            if (local_base) s_base[i] = run;
-            run += __ldcg(P_.counts + i);
-        }
-        if (blockIdx.x == 0 && tid == 0) {
-            P_.info[INFO_SWEEPS] = sweep + 1;
-            P_.info[INFO_FALLBACK] = fallback ? 1 : 0;
-            if constexpr (FUSED) {
-                // range statistics of the remapped voxels (min is 0 by construction)
-                long long mx[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN}, q = LLONG_MIN;
-                for (int b = 0; b < (int)gridDim.x; ++b) {
-                    for (int a = 0; a < 3; ++a) mx[a] = max(mx[a], __ldcg(P_.part + 8 * b + 3 + a));
-                    q = max(q, __ldcg(P_.part + 8 * b + 6));
-                }
-                for (int a = 0; a < 3; ++a) {
-                    P_.stats[a] = n > 0 ? 0 : LLONG_MAX;
-                    P_.stats[3 + a] = n > 0 ? mx[a] - s_gmin[a] : LLONG_MIN;
-                }
-                P_.stats[6] = q;
-                P_.info[INFO_BATCH_ERR] = 0;     // single batch, home in [0, K) by construction
-                P_.info[3] = 0;
+            for (int a = 0; a < 3; ++a) {
+                P_.stats[a] = n > 0 ? 0 : LLONG_MAX;
+                P_.stats[3 + a] = n > 0 ? mx[a] - s_gmin[a] : LLONG_MIN;
             }
+            P_.stats[6] = q;
+            P_.info[INFO_BATCH_ERR] = 0;     // single batch, home in [0, K) by construction
+            P_.info[3] = 0;
         }
-        __syncthreads();
     }
+    if (converged0) return;
     if (!local_base) grid.sync();
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const TileInfo ti = tile_info<kTile>(P_, multi, t, n);
@@ -818,7 +867,10 @@ int launch_psh(psh::Params& p, bool fused, cudaStream_t st) {
     const int nbins = nbatch > 1 ? std::max(K + 1, nbatch) : K + 1;
     const bool small = p.n < psh::kSmallTileMaxN;
     const int stride = (nbins + 1) & ~1;
-    const size_t smem = (size_t)psh::kWarps * stride * sizeof(uint16_t);
+    const size_t hist_bytes = (size_t)psh::kWarps * stride * sizeof(uint16_t);
+    const size_t base_bytes = (size_t)4 * nbatch * (K + 1);
+    p.base_in_smem = hist_bytes + base_bytes <= 200 * 1024 ? 1 : 0;
+    const size_t smem = hist_bytes + (p.base_in_smem ? base_bytes : 0);
     void (*kern)(const psh::Params) =
         fused ? (small ? psh::psh_kernel<psh::kPerLaneSmall, true> : psh::psh_kernel<psh::kPerLaneLarge, true>)
               : (small ? psh::psh_kernel<psh::kPerLaneSmall, false> : psh::psh_kernel<psh::kPerLaneLarge, false>);

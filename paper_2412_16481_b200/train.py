@@ -9,11 +9,14 @@ Per round, in reverse (F_in -> F_mid -> F_out):
     f3d_gelu_bwd  -> du (and db_in),  dW_in = x2^T du,  dx2 = du W_in^T
     f3d_ln_bwd    -> dF_mid = dF_out + LN2'(F_mid) dx2 (and dln2)
                   -> db_o = colsum, dW_o = a^T dF_mid, da = dF_mid W_o^T
-    attention bwd -> dq, dk, dv on padded per-(scope, head) tiles:
-                     P = exp2(S*sl2 - lse) from the forward kernel's LSE
-                     (f3d_softmax_bwd mode 0), dV = P^T dO, dP = dO V^T,
-                     dS = P (dP - D) / sqrt(dh) with D = sum_j P dP per row
-                     (mode 1), dQ = dS K, dK = dS^T Q
+    attention bwd -> dq, dk, dv by the fused kernels (f3d_attn_bwd, head dims
+                     8..32): P = exp2(S*sl2 - lse) recomputed from the
+                     forward kernel's LSE block by block, dS = P (dP - D)
+                     with D = sum_j P dP / sum_j P (a first pass of the
+                     query-block kernel, which then accumulates dQ); a
+                     key-block kernel accumulates dK, dV -- no m x m tile.  Other head
+                     dims: padded per-(scope, head) tiles (f3d_softmax_bwd
+                     modes 0/1 between cuBLAS bmm's, D = sum_j P dP per row)
                   -> db_qkv = colsum, dW_qkv = x1^T dqkv, dx1 = dqkv W_qkv^T
     f3d_ln_bwd    -> dF_in = dF_mid + LN1'(F_in) dx1 (and dln1)
 
@@ -26,15 +29,18 @@ is the data-parallel exchange: one flat fp32 bucket, all_reduce(SUM)/world
 """
 
 import math
+import os
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .attention import attend
+from .attention import ATTN_IMPL, attend
 from .errors import ConfigError
 from .stage import LN_EPS, StageParams, StageRunner
+
+FUSED_ATTN_BWD = os.environ.get("F3D_FUSED_ATTN_BWD", "1") == "1"
 
 GRAD_NAMES = ("w_q", "w_k", "w_v", "w_o", "b_q", "b_k", "b_v", "b_o", "ln1_gain", "ln1_bias",
               "ln2_gain", "ln2_bias", "w_in", "b_in", "w_out", "b_out")
@@ -157,7 +163,12 @@ class StageTrainer:
         self.r = StageRunner(coords, table, schedule, params, n, torch.float32, n_dev=self.n_dev,
                              weights=None if weights is None else weights.w)
         self.n, self.d, self.H, self.dh = n, self.r.d, self.r.H, self.r.dh
-        self.ix = [_RoundIndex(p, n, self.H, L.device()) for p in self.r.plans]
+        # fused attention backward (csrc/attn_bwd.cu) for head dims 8..32, else
+        # the padded-tile path (F3D_FUSED_ATTN_BWD=0 forces it; A/B and tests)
+        self.fused_bwd = (FUSED_ATTN_BWD and self.dh % 8 == 0 and 8 <= self.dh <= 32
+                          and ATTN_IMPL == "tc")
+        self.ix = None if self.fused_bwd else [_RoundIndex(p, n, self.H, L.device())
+                                               for p in self.r.plans]
         self.saved = None
 
     def refresh_weights(self):
@@ -201,6 +212,23 @@ class StageTrainer:
         return F
 
     # ------------------------------------------------------------------ bwd
+    def _attn_bwd_fused(self, plan, qkv, lse, da):
+        """dq|dk|dv (n, 3d) fp32 by the fused kernels (csrc/attn_bwd.cu): no
+        m x m tile is formed; D = sum_j P dP / sum_j P per row is computed by
+        the query-block kernel from the same recomputed P."""
+        n, d, H, dh = self.n, self.d, self.H, self.dh
+        q, k, v = (qkv[:, i * d:(i + 1) * d] for i in range(3))
+        dob = da.to(torch.bfloat16)
+        delta = L.empty((n, H), torch.float32)
+        out = L.empty((n, 3 * d), torch.float32)
+        L.call("f3d_attn_bwd", L.ptr(q), L.ptr(k), L.ptr(v), L.ptr(dob), q.stride(0), k.stride(0),
+               v.stride(0), dob.stride(0), L.ptr(lse), lse.stride(0), L.ptr(delta), H,
+               L.ptr(out), out.stride(0), L.ptr(out[:, d:]), out.stride(0), L.ptr(out[:, 2 * d:]),
+               out.stride(0), H, dh, L.ptr(plan.scope_seg), L.ptr(plan.scope_nseg),
+               L.ptr(plan.seg_start), L.ptr(plan.seg_vstart), L.ptr(plan.scope_len),
+               int(plan.scope_len.shape[0]), int(plan.max_len), L.stream())
+        return out
+
     def _attn_bwd(self, ix: _RoundIndex, qkv, a, lse, da):
         """dq|dk|dv (n, 3d) fp32 from the saved bf16 q/k/v/out, the LSE and
         da (fp32).  bf16 tensor-core GEMMs with fp32 outputs; P and dS are
@@ -286,7 +314,10 @@ class StageTrainer:
             self._colsum(dF, G["b_o"])
             G["w_o"] += mm(s["a"].t(), dFb)
             da = mm(dFb, w["w_o"].t())
-            dqkv = self._attn_bwd(self.ix[t], s["qkv"], s["a"], s["lse"], da)
+            if self.fused_bwd:
+                dqkv = self._attn_bwd_fused(self.r.plans[t], s["qkv"], s["lse"], da)
+            else:
+                dqkv = self._attn_bwd(self.ix[t], s["qkv"], s["a"], s["lse"], da)
             self._colsum(dqkv, G["b_qkv"])
             dqb = dqkv.to(bf)
             G["w_qkv"] += mm(s["x1"].t(), dqb)
