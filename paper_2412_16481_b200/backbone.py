@@ -38,9 +38,14 @@ from .stage import LN_EPS, StageRunner, init_params
 # partition alone).  F3D_POOL_OVERLAP=0 keeps them on the main stream.
 POOL_OVERLAP = os.environ.get("F3D_POOL_OVERLAP", "1") == "1"
 # stream_host runs step i+1's coordinate-only graph g0 on its own stream under
-# step i's g1, gated on an external event recorded after g1's cooperative
-# stage-1 PSH (two cooperative PSH grids in flight at once corrupted results):
-# e2e 1.17 -> 1.10 ms per step.  F3D_G0_CONCURRENT=0 keeps the steps serial.
+# step i's g1: e2e 1.17 -> 1.10 ms per step.  F3D_G0_CONCURRENT=0 keeps the
+# steps serial.  (Round 1 gated g0 behind g1's cooperative stage-1 PSH: two
+# cooperative grids in flight corrupted results.  Root cause: the
+# cooperative_groups grid barrier lives in the driver's grid workspace, which
+# the two concurrent grids shared; the PSH kernel now synchronises on a
+# counter in its own workspace and the gate is off by default, F3D_PSH_GATE=1
+# restores it -- tools/stream_gate_stress.py reproduces the corruption with
+# the old barrier and none with the new.)
 # F3D_NEXT_PROLOGUE_SIDE=0 keeps the next stage's PSH/prologue on the main stream.
 G0_CONCURRENT = os.environ.get("F3D_G0_CONCURRENT", "1") == "1"
 # F3D_SCATTER_LN=0: separate input scatter and first row_ln of each stage
@@ -54,6 +59,9 @@ NEXT_PROLOGUE_SIDE = os.environ.get("F3D_NEXT_PROLOGUE_SIDE", "1") == "1"
 # the all-CTA reduction of the per-CTA extrema cost more than the launches
 # the fusion saves)
 FUSED_PSH = os.environ.get("F3D_FUSED_PSH", "0") == "1"
+# F3D_PSH_GATE=1: hold step i+1's g0 behind step i's cooperative PSH launches
+# (the round-1 workaround; see G0_CONCURRENT)
+PSH_GATE = os.environ.get("F3D_PSH_GATE", "0") == "1"
 
 
 @dataclass(frozen=True)
@@ -253,8 +261,8 @@ class Backbone:
                     nr = _StageRun(si + 1, ncfg, np_cap_, totals_[1:2])
                     nr.asg, nr.stats, nr.info = self.bucketize(Cn_, ncfg, np_cap_, totals_[1:2])
                     # an external event (a graph event-record node when captured):
-                    # stream_host keeps the next scene's cooperative stage-0 PSH
-                    # from running while this cooperative PSH is in flight
+                    # with F3D_PSH_GATE=1 stream_host keeps the next scene's
+                    # cooperative stage-0 PSH from running while this one is in flight
                     r.psh_event = torch.cuda.Event(external=True)
                     r.psh_event.record(side)
                     self._stage_prologue(nr, Cn_)
@@ -544,7 +552,7 @@ class Backbone:
                 g0s.wait_event(sl["ev_c"])
                 if i >= 2:
                     g0s.wait_event(sl["ev_done"])        # step i-2 done with the slot
-                if i >= 1:                                # not under step i-1's cooperative PSHs
+                if i >= 1 and PSH_GATE:                   # not under step i-1's cooperative PSHs
                     prev = slots[(i - 1) % 2]
                     if any(getattr(pr, "psh_on_main", False) for pr in prev["runs"]):
                         g0s.wait_event(prev["ev_done"])   # a PSH without an event: serial

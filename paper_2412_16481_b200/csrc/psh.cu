@@ -19,14 +19,10 @@
 // stable ranks via __match_any_sync), and the final base/dest pass.  Points
 // live in tiles of 2048 (8 warps x 8 rounds x 32 lanes); per-warp u16
 // histograms of the K+1 local buckets sit in shared memory.
-#include <cooperative_groups.h>
-
 #include <algorithm>
 #include <climits>
 
 #include "f3d_common.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace f3d {
 namespace psh {
@@ -74,6 +70,7 @@ struct Params {
     int32_t* btile;    // batch -> first tile (multi), nbatch + 1
     int32_t* bstart;   // batch -> first sorted position, nbatch + 1
     int32_t* flags;    // max_sweeps + 2 "changed" words
+    unsigned* bar;     // grid barrier counter (zeroed before the launch)
     int max_tiles;
     int base_in_smem;    // nbatch*(K+1) ints of dynamic smem past the histograms
     // fused voxelize + remap + hash (f3d_psh_assign_coords; single batch):
@@ -83,6 +80,30 @@ struct Params {
     double vs;
     int64_t* stats;      // [min x,y,z, max x,y,z, max quotient] of the remapped voxels
     long long* part;     // per-CTA partial extrema, 8 per CTA
+};
+
+// Grid-wide barrier on a per-call counter in the caller's workspace (zeroed
+// before the launch; the launch is still cooperative, for co-residency).
+// cooperative_groups' grid.sync() uses the driver's grid workspace, and two
+// cooperative PSH grids in flight at once on two streams corrupted each
+// other's barriers (wrong assignments, corrupted status words) -- with a
+// private counter concurrent launches are independent
+// (tools/psh_concurrency.py, tests/test_gpu_psh.py).
+struct GridBar {
+    unsigned* ctr;
+    unsigned target;
+    __device__ __forceinline__ void sync() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            target += gridDim.x;                 // monotonic: barrier k ends at k * grid
+            unsigned old, cur;
+            asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+            do {
+                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
+            } while (cur < target);
+        }
+        __syncthreads();
+    }
 };
 
 // floor((c - o) / vs) with no contraction: __dsub_rn then __ddiv_rn
@@ -371,7 +392,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     constexpr int kPerLane = TileC<PL>::kPerLane;
     constexpr int kWarpSpan = TileC<PL>::kWarpSpan;
     constexpr int kTile = TileC<PL>::kTile;
-    cg::grid_group grid = cg::this_grid();
+    GridBar grid{P_.bar, 0u};
     extern __shared__ __align__(16) uint16_t sh[];
     __shared__ int8_t probe[kMaxProbes * 3];
     __shared__ int s_flag;
@@ -749,7 +770,7 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
 }
 
 struct WsLayout {
-    size_t pk, D, off, orig, T0, T1, hist, tile_p0, tile_b, btile, bstart, flags, total;
+    size_t pk, D, off, orig, T0, T1, hist, tile_p0, tile_b, btile, bstart, flags, bar, total;
 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -772,6 +793,7 @@ static WsLayout layout(int64_t n, int32_t nbatch, int32_t K, int max_sweeps) {
     L.btile = o;   o = align256(o + 4 * (nbatch + 1));
     L.bstart = o;  o = align256(o + 4 * (nbatch + 1));
     L.flags = o;   o = align256(o + 4 * (max_sweeps + 2));
+    L.bar = o;     o = align256(o + 4);
     L.total = o;
     return L;
 }
@@ -890,6 +912,7 @@ int launch_psh(psh::Params& p, bool fused, cudaStream_t st) {
     grid = std::max(grid, std::min(col_ctas, per_sm * f3d_num_sms()));
     grid = std::max(grid, 1);
     if (fused) grid = std::min(grid, kMaxGrid);
+    F3D_CUDA_TRY(cudaMemsetAsync(p.bar, 0, sizeof(unsigned), st));
     void* args[] = {(void*)&p};
     F3D_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(psh::kThreads), args,
                                              smem, st));
@@ -948,6 +971,7 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
     p.btile = (int32_t*)(w + L.btile);
     p.bstart = (int32_t*)(w + L.bstart);
     p.flags = (int32_t*)(w + L.flags);
+    p.bar = (unsigned*)(w + L.bar);
     const bool small = n < psh::kSmallTileMaxN;
     const int tile = small ? psh::TileC<psh::kPerLaneSmall>::kTile
                            : psh::TileC<psh::kPerLaneLarge>::kTile;
@@ -1034,6 +1058,7 @@ extern "C" int f3d_psh_assign_coords(const double* coords, int64_t n,
     p.T1 = (int32_t*)(w + L.T1);
     p.hist = (int32_t*)(w + L.hist);
     p.flags = (int32_t*)(w + L.flags);
+    p.bar = (unsigned*)(w + L.bar);
     const bool small = n < psh::kSmallTileMaxN;
     const int tile = small ? psh::TileC<psh::kPerLaneSmall>::kTile
                            : psh::TileC<psh::kPerLaneLarge>::kTile;

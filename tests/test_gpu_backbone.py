@@ -287,3 +287,47 @@ def test_attention_dynamic_scheduler_repeats_and_resets():
     o = torch.zeros(n, d, dtype=torch.bfloat16, device="cuda")
     attend(q, k, v, o, hp, H, d // H)
     assert torch.equal(o, outs[0])
+
+
+@pytest.mark.parametrize("fused_psh", [False, True])
+def test_two_backbones_on_two_streams(fused_psh):
+    """Two Backbone objects replayed concurrently on two streams (two
+    cooperative PSH grids in flight at once, every kernel family overlapping)
+    give exactly their serial results, repeatedly.  The PSH grid barrier lives
+    in each call's workspace (cooperative_groups' driver workspace was shared
+    by concurrent grids and corrupted results)."""
+    from paper_2412_16481_b200 import backbone as B
+    old = B.FUSED_PSH
+    B.FUSED_PSH = fused_psh
+    try:
+        n = 40_000
+        stages = (StageConfig(K=128, S=512, S_div=2048, pool_rho=2, seed=0),
+                  StageConfig(K=64, S=512, S_div=4096, pool_rho=0, seed=1))
+        bbs = [Backbone(stages), Backbone(stages)]
+        ins = []
+        for bb, (seed, dist) in zip(bbs, ((11, "uniform-box"), (12, "surface-shell"))):
+            C = torch.tensor(O.synth_cloud(seed, n, dist), device="cuda")
+            X = torch.tensor(np.random.default_rng(seed).normal(size=(n, 96)),
+                             dtype=torch.bfloat16, device="cuda")
+            bb.capture(n, torch.bfloat16)
+            bb.graph_coords.copy_(C)
+            bb.graph_feats.copy_(X)
+            ins.append((C, X))
+        ref = []
+        for bb in bbs:
+            bb.replay()
+            n_out = bb.check_graph()
+            ref.append((n_out, bb._graphs["X"][:n_out].clone()))
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for _ in range(12):
+            for bb, s in zip(bbs, streams):
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s):
+                    bb.replay()
+            for s in streams:
+                torch.cuda.current_stream().wait_stream(s)
+            for bb, (n_out, X) in zip(bbs, ref):
+                assert bb.check_graph() == n_out
+                assert torch.equal(bb._graphs["X"][:n_out], X)
+    finally:
+        B.FUSED_PSH = old
