@@ -39,13 +39,15 @@ from .stage import LN_EPS, StageRunner, init_params
 POOL_OVERLAP = os.environ.get("F3D_POOL_OVERLAP", "1") == "1"
 # stream_host runs step i+1's coordinate-only graph g0 on its own stream under
 # step i's g1: e2e 1.17 -> 1.10 ms per step.  F3D_G0_CONCURRENT=0 keeps the
-# steps serial.  (Round 1 gated g0 behind g1's cooperative stage-1 PSH: two
-# cooperative grids in flight corrupted results.  Root cause: the
-# cooperative_groups grid barrier lives in the driver's grid workspace, which
-# the two concurrent grids shared; the PSH kernel now synchronises on a
-# counter in its own workspace and the gate is off by default, F3D_PSH_GATE=1
-# restores it -- tools/stream_gate_stress.py reproduces the corruption with
-# the old barrier and none with the new.)
+# steps serial.  (Round 1 gated g0 behind g1's cooperative stage-1 PSH after
+# results came back corrupted.  Root cause, found in round 2: a slot's g0 and
+# g1 share one graph memory pool, so g1's outputs (status words, last-stage
+# bf16 features) can occupy memory that g0 uses as scratch, and g0 of step
+# i+2 was only ordered after step i's g1 -- not after step i's device-to-host
+# read-back of those outputs.  g0 now waits for the slot's read-back event;
+# the gate is off by default (F3D_PSH_GATE=1 restores it).
+# tools/g0_overlap_probe.py shows concurrent g0/g1 replays themselves agree
+# bit for bit; tests/test_gpu_backbone.py covers the pipelined paths.)
 # F3D_NEXT_PROLOGUE_SIDE=0 keeps the next stage's PSH/prologue on the main stream.
 G0_CONCURRENT = os.environ.get("F3D_G0_CONCURRENT", "1") == "1"
 # F3D_SCATTER_LN=0: separate input scatter and first row_ln of each stage
@@ -552,6 +554,10 @@ class Backbone:
                 g0s.wait_event(sl["ev_c"])
                 if i >= 2:
                     g0s.wait_event(sl["ev_done"])        # step i-2 done with the slot
+                    # and step i-2's read-back done: g0 and g1 share the slot's
+                    # graph memory pool, so g1's outputs (status words, last-stage
+                    # features) can sit in memory g0 uses as scratch
+                    g0s.wait_event(sl["ev_out"])
                 if i >= 1 and PSH_GATE:                   # not under step i-1's cooperative PSHs
                     prev = slots[(i - 1) % 2]
                     if any(getattr(pr, "psh_on_main", False) for pr in prev["runs"]):

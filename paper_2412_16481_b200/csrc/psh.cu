@@ -83,12 +83,10 @@ struct Params {
 };
 
 // Grid-wide barrier on a per-call counter in the caller's workspace (zeroed
-// before the launch; the launch is still cooperative, for co-residency).
-// cooperative_groups' grid.sync() uses the driver's grid workspace, and two
-// cooperative PSH grids in flight at once on two streams corrupted each
-// other's barriers (wrong assignments, corrupted status words) -- with a
-// private counter concurrent launches are independent
-// (tools/psh_concurrency.py, tests/test_gpu_psh.py).
+// before the launch; the launch is still cooperative, for co-residency):
+// every call's barrier state is its own, whatever else runs concurrently
+// (two Backbones on two streams, tests/test_gpu_backbone.py;
+// tools/psh_concurrency.py).
 struct GridBar {
     unsigned* ctr;
     unsigned target;
