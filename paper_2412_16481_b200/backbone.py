@@ -41,10 +41,11 @@ POOL_OVERLAP = os.environ.get("F3D_POOL_OVERLAP", "1") == "1"
 # step i's g1: e2e 1.17 -> 1.10 ms per step.  F3D_G0_CONCURRENT=0 keeps the
 # steps serial.  (Round 1 gated g0 behind g1's cooperative stage-1 PSH after
 # results came back corrupted.  Root cause, found in round 2: a slot's g0 and
-# g1 share one graph memory pool, so g1's outputs (status words, last-stage
-# bf16 features) can occupy memory that g0 uses as scratch, and g0 of step
+# g1 shared one graph memory pool, so g1's outputs (status words, last-stage
+# bf16 features) could occupy memory that g0 uses as scratch, and g0 of step
 # i+2 was only ordered after step i's g1 -- not after step i's device-to-host
-# read-back of those outputs.  g0 now waits for the slot's read-back event;
+# read-back of those outputs.  g0 and g1 now capture into separate pools
+# (F3D_SEPARATE_POOLS=0: one pool, g0 then waits for the slot's read-back);
 # the gate is off by default (F3D_PSH_GATE=1 restores it).
 # tools/g0_overlap_probe.py shows concurrent g0/g1 replays themselves agree
 # bit for bit; tests/test_gpu_backbone.py covers the pipelined paths.)
@@ -64,6 +65,7 @@ FUSED_PSH = os.environ.get("F3D_FUSED_PSH", "0") == "1"
 # F3D_PSH_GATE=1: hold step i+1's g0 behind step i's cooperative PSH launches
 # (the round-1 workaround; see G0_CONCURRENT)
 PSH_GATE = os.environ.get("F3D_PSH_GATE", "0") == "1"
+SEPARATE_POOLS = os.environ.get("F3D_SEPARATE_POOLS", "1") == "1"
 
 
 @dataclass(frozen=True)
@@ -457,11 +459,15 @@ class Backbone:
                 self._enqueue_rest(r0, coords, feats)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
-        pool = torch.cuda.graph_pool_handle()
+        # one memory pool per graph: g1's outputs (status words, bf16 features),
+        # still being read back by the host stream when stream_host replays the
+        # slot's next g0, must not share memory with g0's scratch
         g0, g1 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g0, pool=pool):
+        pool0 = torch.cuda.graph_pool_handle()
+        pool1 = torch.cuda.graph_pool_handle() if SEPARATE_POOLS else pool0
+        with torch.cuda.graph(g0, pool=pool0):
             r0 = self._enqueue_bucketize0(coords)
-        with torch.cuda.graph(g1, pool=pool):
+        with torch.cuda.graph(g1, pool=pool1):
             self._want_out_bf16 = True
             try:
                 X, Cn, n_dev, runs = self._enqueue_rest(r0, coords, feats)
@@ -554,10 +560,8 @@ class Backbone:
                 g0s.wait_event(sl["ev_c"])
                 if i >= 2:
                     g0s.wait_event(sl["ev_done"])        # step i-2 done with the slot
-                    # and step i-2's read-back done: g0 and g1 share the slot's
-                    # graph memory pool, so g1's outputs (status words, last-stage
-                    # features) can sit in memory g0 uses as scratch
-                    g0s.wait_event(sl["ev_out"])
+                    if not SEPARATE_POOLS:               # (round-1 layout: shared pool)
+                        g0s.wait_event(sl["ev_out"])
                 if i >= 1 and PSH_GATE:                   # not under step i-1's cooperative PSHs
                     prev = slots[(i - 1) % 2]
                     if any(getattr(pr, "psh_on_main", False) for pr in prev["runs"]):

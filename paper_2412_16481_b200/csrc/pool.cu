@@ -200,9 +200,9 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
     __syncwarp();
     // ---- step 3: queued rows join the nearest under-filled sub-bucket.
     // Speculative batches of 32 queued rows, one per lane: every lane finds
-    // its row's kTop nearest eligible ids against the sizes at the start of
-    // the pass, then the choices are committed in index order, each row
-    // taking the first of its ids still under-filled.  Eligibility only shrinks during step 3, so a
+    // its row's nearest eligible id against the sizes at the start of the
+    // pass, then the choices are committed in index order while each chosen
+    // id is still under-filled.  Eligibility only shrinks during step 3, so a
     // choice whose id is still eligible at commit time is exactly the
     // sequential answer (the minimum over a superset that lies in the
     // subset); a stale choice is recomputed for that row alone (warp-parallel
@@ -234,63 +234,33 @@ __global__ void __launch_bounds__(kThreads) pool_build_kernel(const Args A) {
             break;
         }
         const int nb = min(32, nqueue - q0);
-        // each lane: its row's kTop nearest eligible ids of the pass, in the
-        // (distance, id) order of closer().  At commit time the first of them
-        // still under-filled is the sequential answer (any other eligible id
-        // is at least as far as the kTop-th); only when all kTop went full
-        // is the row recomputed, warp-parallel.
-        constexpr int kTop = 4;
-        int cand[kTop];
-        double cd2[kTop];
-#pragma unroll
-        for (int q = 0; q < kTop; ++q) {
-            cand[q] = INT_MAX;
-            cd2[q] = DBL_MAX;
-        }
+        int choice = INT_MAX;
         if (lane < nb) {
             const int i = S.qrow[q0 + lane];
             const double ci[3] = {S.cc[i][0], S.cc[i][1], S.cc[i][2]};
+            double bd2 = DBL_MAX;
             for (int e = 0; e < ne; ++e) {      // ascending ids: strict '<' keeps the lowest
                 const int jj = S.elig[e];
                 const double d2 = dist2(S.cc[S.seeds[jj]], ci);   // seed row's coordinates
-                if (closer(d2, jj, cd2[kTop - 1], cand[kTop - 1])) {
-                    cd2[kTop - 1] = d2;
-                    cand[kTop - 1] = jj;
-#pragma unroll
-                    for (int q = kTop - 1; q > 0; --q)
-                        if (closer(cd2[q], cand[q], cd2[q - 1], cand[q - 1])) {
-                            const double td = cd2[q];
-                            cd2[q] = cd2[q - 1];
-                            cd2[q - 1] = td;
-                            const int tc = cand[q];
-                            cand[q] = cand[q - 1];
-                            cand[q - 1] = tc;
-                        }
+                if (closer(d2, jj, bd2, choice)) {
+                    bd2 = d2;
+                    choice = jj;
                 }
             }
         }
         int done = 0;
         for (; done < nb; ++done) {          // commit in index order while valid
-            int pick = INT_MAX;
-            bool any = false;
-#pragma unroll
-            for (int q = 0; q < kTop; ++q) {
-                const int c = __shfl_sync(0xffffffffu, cand[q], done);
-                if (q == 0 && c == INT_MAX) {   // no finite distance (non-finite coords)
-                    any = true;
-                    break;
-                }
-                if (pick == INT_MAX && c != INT_MAX && S.sizes[c] < rho) pick = c;
-            }
-            if (any) {
+            const int jj = __shfl_sync(0xffffffffu, choice, done);
+            if (jj == INT_MAX) {             // no finite distance (non-finite coords)
                 if (lane == 0) atomicOr(A.flags, 2);
                 done = nqueue;
                 break;
             }
-            if (pick == INT_MAX) {
-                // all kTop went full: this row alone, warp-parallel over the
-                // pass's eligible ids that are still under-filled (same tier:
-                // the list only shrinks; an exhausted tier ends the pass)
+            int pick = jj;
+            if (S.sizes[jj] >= rho) {
+                // stale: this row alone, warp-parallel over the pass's eligible
+                // ids that are still under-filled (same tier: the list only
+                // shrinks; an exhausted tier ends the pass and rebuilds it)
                 const int i = S.qrow[q0 + done];
                 const double ci[3] = {S.cc[i][0], S.cc[i][1], S.cc[i][2]};
                 double bd2 = DBL_MAX;
