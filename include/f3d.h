@@ -345,6 +345,22 @@ int f3d_gemm(const void *x, int64_t ldx, int64_t n, int K, const void *w_t, int 
              const float *bias, int gelu, void *y, int64_t ldy, const int32_t *n_dev,
              void *stream);
 
+/* The O-projection / MLP-output GEMM with the residual + LayerNorm (+PE) row
+ * pass in its epilogue (bw/stage.py:134-158: F += attn W_o + b_o, x = LN2(F);
+ * F += MLP W_out + b_out, x = LN1(F) + PE for the next round):
+ *   F[r] += x[r] W + bias   (F: n x N fp32, row stride ldf, in place)
+ *   y[r]  = (F[r] - mean) / sqrt(var + eps) * gain + beta (+ PE) as bf16
+ * gain == NULL: residual only (y unused).  pe_coords (nullable): (n,3) f64 rows
+ * and lo_ext the bbox [lo x,y,z, extent x,y,z] (as f3d_row_ln; N % 6 == 0).
+ * The fp32 residual tile is TMA-loaded into shared memory and leaves with F
+ * and y by TMA stores.  N % 32 == 0, N <= 256 (f3d_gemm_res_ln_supported). */
+int f3d_gemm_res_ln_supported(int K, int N);
+int f3d_gemm_res_ln(const void *x, int64_t ldx, int64_t n, int K, const void *w_t, int N,
+                    const float *bias, float *F, int64_t ldf, const float *gain,
+                    const float *beta, const double *pe_coords, const double *lo_ext,
+                    double pe_base, double eps, void *y, int64_t ldy, const int32_t *n_dev,
+                    void *stream);
+
 /* u = GELU(x W_in + b_in) as bf16 rows (n x 4d): tcgen05 GEMM with the
  * bias + exact-erf GELU epilogue read from TMEM (replaces a library GEMM +
  * f3d_bias_gelu; bw/stage.py:153-156).  w_in_t = W_in^T (4d x d, row-major

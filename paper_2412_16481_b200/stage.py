@@ -51,6 +51,15 @@ PE_TABLE = os.environ.get("F3D_PE_TABLE", "0") == "1"
 _OG = os.environ.get("F3D_OWN_GEMM", "qkv,o,in,out")
 OWN_GEMM = {k for k in ("qkv", "o", "in", "out")
             if _OG == "1" or k in _OG.split(",")} if _OG != "0" else set()
+# F3D_GEMM_RES_LN=1: the O projection and the MLP output GEMMs carry the
+# residual + LayerNorm (+PE) row pass in their epilogue (f3d_gemm_res_ln: the
+# fp32 residual tile TMA-loaded into shared memory, F and LN(F) leave by TMA
+# stores) instead of a separate f3d_row_ln pass.  Correct (tests) but opt-in:
+# measured 1.115 vs 1.06 ms per config-B step -- with the accumulator's
+# thread-per-row layout, two epilogue warpgroups per SM recycle their residual
+# tiles (store, reload) on the critical path of every tile, where the
+# separate full-occupancy row pass streams F at HBM speed.
+GEMM_RES_LN = os.environ.get("F3D_GEMM_RES_LN", "0") == "1"
 _GG = os.environ.get("F3D_GEMM_GELU")
 GEMM_GELU = _GG != "0"
 GEMM_GELU_MIN_ROWS = 0
@@ -208,10 +217,20 @@ class StageRunner:
                                           ("out", (dhid, d)))
                     if ok and k in OWN_GEMM and lib.f3d_gemm_supported(k_, n_)}
         self.own_gemm = bool(self.own)
+        self.res_ln = (GEMM_RES_LN and f_dtype == torch.float32 and "o" in self.own
+                       and "out" in self.own and bool(lib.f3d_gemm_res_ln_supported(d, d))
+                       and bool(lib.f3d_gemm_res_ln_supported(dhid, d)))
 
     def _gemm(self, X, K, w_t, N, bias, gelu, Y):
         L.call("f3d_gemm", L.ptr(X), X.stride(0), self.n, K, L.ptr(w_t), N, L.ptr(bias),
                int(gelu), L.ptr(Y), Y.stride(0), L.ptr(self.n_dev), L.stream())
+
+    def _gemm_res_ln(self, X, K, w_t, bias, F, g, b, pe, out):
+        L.call("f3d_gemm_res_ln", L.ptr(X), X.stride(0), self.n, K, L.ptr(w_t), self.d,
+               L.ptr(bias), L.ptr(F), F.stride(0), L.ptr(g), L.ptr(b),
+               L.ptr(self.coords) if pe else None, L.ptr(self.lo_ext) if pe else None, 10000.0,
+               LN_EPS, L.ptr(out), 0 if out is None else out.stride(0), L.ptr(self.n_dev),
+               L.stream())
 
     def _row_ln(self, F, y, ybias, g, b, pe, out):
         if pe and self.pe_tab is not None and F.dtype == torch.float32 and out is not None:
@@ -262,6 +281,10 @@ class StageRunner:
             if self.gemm_ln and F.dtype == torch.float32:
                 self._gemm_ln(self.a, self.d, w["w_o_t"], w["b_o"], F, w["ln2_g"], w["ln2_b"],
                               False, self.x)
+            elif self.res_ln and F.dtype == torch.float32:
+                # F += a W_o + b_o;  x = LN2(F)
+                self._gemm_res_ln(self.a, d, w["w_o_t"], w["b_o"], F, w["ln2_g"], w["ln2_b"],
+                                  False, self.x)
             else:
                 if "o" in own:
                     self._gemm(self.a, d, w["w_o_t"], d, None, False, self.y)
@@ -294,6 +317,11 @@ class StageRunner:
                 self._gemm_ln(self.u, self.u.shape[1], w["w_out_t"], w["b_out"], F,
                               None if last else w["ln1_g"], None if last else w["ln1_b"],
                               not last, None if last else self.x)
+                continue
+            if t + 1 < R and self.res_ln and F.dtype == torch.float32:
+                # F += g W_out + b_out;  x = LN1(F) + PE for the next round
+                self._gemm_res_ln(self.u, dhid, w["w_out_t"], w["b_out"], F, w["ln1_g"],
+                                  w["ln1_b"], True, self.x)
                 continue
             if "out" in own:
                 self._gemm(self.u, dhid, w["w_out_t"], d, None, False, self.y)

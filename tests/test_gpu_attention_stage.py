@@ -380,3 +380,79 @@ def test_stage_pe_table_matches_computed_pe():
         ST.PE_TABLE = old
     rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
     assert rr < 1e-2, rr
+
+
+@pytest.mark.parametrize("n,k,ln,pe,ndev", [(3001, 96, True, False, None),
+                                            (3001, 384, True, True, 2900),
+                                            (4096, 384, False, False, None),
+                                            (100_000, 96, True, True, 99_900),
+                                            (257, 96, True, True, None)])
+def test_gemm_res_ln_matches_torch(n, k, ln, pe, ndev):
+    """f3d_gemm_res_ln (the opt-in O-projection / MLP-output epilogue):
+    F += x W + b in place, y = LN(F) g + b (+PE) against torch fp32 on the same
+    bf16 operands; rows past the device count are never written."""
+    import ctypes
+
+    import torch
+
+    from paper_2412_16481_b200 import _lib as L
+    d = 96
+    g = torch.Generator(device="cuda").manual_seed(k + n)
+    x = torch.randn((n, k), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((k, d), device="cuda", generator=g) / k ** 0.5).to(torch.bfloat16)
+    bias = torch.randn((d,), device="cuda", generator=g) * 0.1
+    F0 = torch.randn((n, d), device="cuda", generator=g)
+    lg = 1 + 0.1 * torch.randn((d,), device="cuda", generator=g)
+    lb = 0.1 * torch.randn((d,), device="cuda", generator=g)
+    coords = torch.rand((n, 3), device="cuda", dtype=torch.float64, generator=g)
+    lo_ext = torch.tensor([0, 0, 0, 1, 1, 1], device="cuda", dtype=torch.float64)
+    Fg = F0.clone()
+    xn = torch.full((n, d), 3.0, device="cuda", dtype=torch.bfloat16)
+    nd = None if ndev is None else torch.tensor([ndev], dtype=torch.int32, device="cuda")
+    wt = w.t().contiguous()
+    assert L.load().f3d_gemm_res_ln_supported(k, d) == 1
+    rc = L.load().f3d_gemm_res_ln(L.ptr(x), x.stride(0), n, k, L.ptr(wt), d, L.ptr(bias),
+                                  L.ptr(Fg), Fg.stride(0), L.ptr(lg) if ln else None,
+                                  L.ptr(lb) if ln else None, L.ptr(coords) if pe else None,
+                                  L.ptr(lo_ext) if pe else None, ctypes.c_double(10000.0),
+                                  ctypes.c_double(1e-12), L.ptr(xn), xn.stride(0), L.ptr(nd),
+                                  L.stream())
+    assert rc == 0
+    torch.cuda.synchronize()
+    m = n if ndev is None else ndev
+    Fr = F0 + (x.float() @ w.float() + bias)
+    assert float(((Fg[:m] - Fr[:m]).norm() / Fr[:m].norm()).item()) < 1e-4
+    assert torch.equal(Fg[m:], F0[m:])
+    if ln:
+        xr = torch.nn.functional.layer_norm(Fr, (d,), lg, lb, eps=1e-12)
+        if pe:
+            xr = xr + torch.tensor(F.positional_encoding(coords.cpu().numpy(), d),
+                                   device="cuda", dtype=torch.float32)
+        got = xn[:m].float()
+        assert float(((got - xr[:m]).norm() / xr[:m].norm()).item()) < 1e-2
+    assert bool((xn[m:] == 3.0).all())
+    if not ln:
+        assert bool((xn == 3.0).all())
+
+
+def test_stage_gemm_res_ln_matches_row_ln_path():
+    """The stage with the fused residual + LN epilogue (opt-in) against the
+    GEMM + f3d_row_ln two-kernel path (default)."""
+    import torch
+
+    from paper_2412_16481_b200 import stage as ST
+    a, sf, sc = _config_a(n=3000, d=96)
+    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
+    p = F.init_params(0, 96, n_heads=4)
+    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
+    C = torch.tensor(sc, device="cuda")
+    old = ST.GEMM_RES_LN
+    try:
+        ST.GEMM_RES_LN = False
+        ref = F.stage_forward(X, C, a, sched, p)
+        ST.GEMM_RES_LN = True
+        out = F.stage_forward(X, C, a, sched, p)
+    finally:
+        ST.GEMM_RES_LN = old
+    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
+    assert rr < 1e-2, rr
