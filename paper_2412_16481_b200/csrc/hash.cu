@@ -5,6 +5,8 @@
 // bw/hashing.py:60-125   _check_range + morton_encode + hash_bucket
 #include <climits>
 
+#include <algorithm>
+
 #include "f3d_common.cuh"
 
 namespace f3d {
@@ -104,26 +106,34 @@ __global__ void voxelize_kernel(const double* __restrict__ coords, int64_t n, Or
     for (int a = 0; a < 3; ++a) out[3 * pt + a] = vox1(coords[3 * pt + a], org.o[a], vs);
 }
 
-// per-(batch, axis) minimum; batch == null means one batch.
+// per-(batch, axis) minimum; batch == null means one batch.  Grid-stride
+// (a capped grid): one block-level atomic per axis per block for one batch.
 __global__ void batch_min_kernel(const int64_t* __restrict__ vox, const int32_t* __restrict__ batch,
                                  int64_t n, int nbatch, int64_t* ws_min) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool ok = i < n;
-    long long v[3];
-    int b = 0;
-    if (ok) {
-        v[0] = vox[3 * i];
-        v[1] = vox[3 * i + 1];
-        v[2] = vox[3 * i + 2];
-        if (batch) b = batch[i];
-    } else {
-        v[0] = v[1] = v[2] = LLONG_MAX;
+    const bool single = !batch || nbatch == 1;
+    long long acc[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_it = (n + step - 1) / step * step;     // warp-uniform trip count
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_it; i += step) {
+        const bool ok = i < n;
+        long long v[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+        int b = 0;
+        if (ok) {
+            v[0] = vox[3 * i];
+            v[1] = vox[3 * i + 1];
+            v[2] = vox[3 * i + 2];
+            if (batch) b = batch[i];
+        }
+        if (single) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) acc[a] = min(acc[a], v[a]);
+        } else {
+            batch_min_atomic(v, b, ok && b >= 0 && b < nbatch, ws_min);
+        }
     }
-    if (!batch || nbatch == 1) {
-        for (int a = 0; a < 3; ++a)
-            warp_min_max_atomic(v[a], (long long*)ws_min + a, nullptr);
-    } else {
-        batch_min_atomic(v, b, ok && b >= 0 && b < nbatch, ws_min);
+    if (single) {
+        int64_t* const dst[3] = {ws_min, ws_min + 1, ws_min + 2};
+        block_extrema_atomic<3, 3>(acc, dst);
     }
 }
 
@@ -144,76 +154,77 @@ struct HashArgs {
     int want_quot;
 };
 
-__device__ __forceinline__ void hash_point(long long x, long long y, long long z, int64_t i,
-                                           const HashArgs& ha, int32_t* home, int32_t* vox32,
-                                           int64_t* stats, bool valid) {
+// Home hash of one (remapped) voxel; range statistics accumulated in acc:
+// [min x, y, z, max x, y, z, max quotient].
+__device__ __forceinline__ void hash_one(long long x, long long y, long long z, int64_t i,
+                                         const HashArgs& ha, int32_t* home, int32_t* vox32,
+                                         bool valid, long long (&acc)[7]) {
+    if (!valid) return;
     const long long lim = 1ll << ha.hp.bits;
     const bool in = x >= 0 && y >= 0 && z >= 0 && x < lim && y < lim && z < lim;
-    long long q = LLONG_MIN;
-    if (valid) {
-        int h = 0;
-        if (in) {
-            int64_t key;
-            if (ha.hp.kind <= XOR_DIV) key = x ^ y ^ z;
-            else key = morton3(x, y, z);
-            if (ha.hp.kind == XOR_DIV || ha.hp.kind == ZORDER_DIV) {
-                key = key / ha.hp.S_div;
-                q = key;
-            }
-            h = (int)(key % ha.hp.K);
+    int h = 0;
+    if (in) {
+        int64_t key;
+        if (ha.hp.kind <= XOR_DIV) key = x ^ y ^ z;
+        else key = morton3(x, y, z);
+        if (ha.hp.kind == XOR_DIV || ha.hp.kind == ZORDER_DIV) {
+            key = key / ha.hp.S_div;
+            acc[6] = max(acc[6], (long long)key);
         }
-        home[i] = h;
-        if (vox32) {
-            vox32[3 * i] = (int)x;
-            vox32[3 * i + 1] = (int)y;
-            vox32[3 * i + 2] = (int)z;
-        }
+        h = (int)(key % ha.hp.K);
     }
-    if (stats) {
-        // [min x, y, z, max x, y, z, max quotient], one global atomic per block
-        const long long BIGP = LLONG_MAX, BIGN = LLONG_MIN;
-        const long long vals[7] = {valid ? x : BIGP, valid ? y : BIGP, valid ? z : BIGP,
-                                   valid ? x : BIGN, valid ? y : BIGN, valid ? z : BIGN,
-                                   valid ? q : BIGN};
-        int64_t* const dst[7] = {stats, stats + 1, stats + 2, stats + 3, stats + 4, stats + 5,
-                                 ha.want_quot ? stats + 6 : nullptr};
-        block_extrema_atomic<7, 3>(vals, dst);
+    home[i] = h;
+    if (vox32) {
+        vox32[3 * i] = (int)x;
+        vox32[3 * i + 1] = (int)y;
+        vox32[3 * i + 2] = (int)z;
     }
+    acc[0] = min(acc[0], x);
+    acc[1] = min(acc[1], y);
+    acc[2] = min(acc[2], z);
+    acc[3] = max(acc[3], x);
+    acc[4] = max(acc[4], y);
+    acc[5] = max(acc[5], z);
 }
+
+// one global atomic per statistic per block (filtered by the current value)
+__device__ __forceinline__ void flush_stats(const long long (&acc)[7], const HashArgs& ha,
+                                            int64_t* stats) {
+    if (!stats) return;
+    int64_t* const dst[7] = {stats, stats + 1, stats + 2, stats + 3, stats + 4, stats + 5,
+                             ha.want_quot ? stats + 6 : nullptr};
+    block_extrema_atomic<7, 3>(acc, dst);
+}
+
+#define F3D_STATS_INIT {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MIN, LLONG_MIN, LLONG_MIN, LLONG_MIN}
 
 __global__ void hash_kernel(const int64_t* __restrict__ vox, int64_t n, HashArgs ha,
                             int32_t* __restrict__ home, int32_t* __restrict__ vox32,
                             int64_t* stats) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = i < n;
-    long long x = 0, y = 0, z = 0;
-    if (valid) {
-        x = vox[3 * i];
-        y = vox[3 * i + 1];
-        z = vox[3 * i + 2];
-    }
-    hash_point(x, y, z, i, ha, home, vox32, stats, valid);
+    long long acc[7] = F3D_STATS_INIT;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += step)
+        hash_one(vox[3 * i], vox[3 * i + 1], vox[3 * i + 2], i, ha, home, vox32, true, acc);
+    flush_stats(acc, ha, stats);
 }
 
 __global__ void morton_kernel(const int64_t* __restrict__ vox, int64_t n, int bits,
                               int64_t* __restrict__ codes, int64_t* stats) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = i < n;
-    long long x = 0, y = 0, z = 0;
-    if (valid) {
-        x = vox[3 * i];
-        y = vox[3 * i + 1];
-        z = vox[3 * i + 2];
-        const uint64_t m = (1ull << bits) - 1;
+    long long acc[7] = F3D_STATS_INIT;
+    const uint64_t m = (1ull << bits) - 1;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += step) {
+        const long long x = vox[3 * i], y = vox[3 * i + 1], z = vox[3 * i + 2];
         codes[i] = morton3((int64_t)(x & m), (int64_t)(y & m), (int64_t)(z & m));
+        acc[0] = min(acc[0], x);
+        acc[1] = min(acc[1], y);
+        acc[2] = min(acc[2], z);
+        acc[3] = max(acc[3], x);
+        acc[4] = max(acc[4], y);
+        acc[5] = max(acc[5], z);
     }
-    const long long BIGP = LLONG_MAX, BIGN = LLONG_MIN;
-    warp_min_max_atomic(valid ? x : BIGP, (long long*)stats + 0, nullptr);
-    warp_min_max_atomic(valid ? y : BIGP, (long long*)stats + 1, nullptr);
-    warp_min_max_atomic(valid ? z : BIGP, (long long*)stats + 2, nullptr);
-    warp_min_max_atomic(valid ? x : BIGN, nullptr, (long long*)stats + 3);
-    warp_min_max_atomic(valid ? y : BIGN, nullptr, (long long*)stats + 4);
-    warp_min_max_atomic(valid ? z : BIGN, nullptr, (long long*)stats + 5);
+    int64_t* const dst[7] = {stats, stats + 1, stats + 2, stats + 3, stats + 4, stats + 5, nullptr};
+    block_extrema_atomic<7, 3>(acc, dst);
 }
 
 // Fused pass 1: voxelize + per-batch axis minimum (voxels are not stored).
@@ -221,19 +232,29 @@ __global__ void fused_min_kernel(const double* __restrict__ coords,
                                  const int32_t* __restrict__ batch, int64_t n,
                                  const int32_t* n_dev, int nbatch, Origin org, double vs,
                                  int64_t* ws_min) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool ok = i < dyn_n(n, n_dev);
-    long long v[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
-    int b = 0;
-    if (ok) {
-        for (int a = 0; a < 3; ++a) v[a] = vox1(coords[3 * i + a], org.o[a], vs);
-        if (batch) b = batch[i];
+    const int64_t nn = dyn_n(n, n_dev);
+    const bool single = !batch || nbatch == 1;
+    long long acc[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_it = (nn + step - 1) / step * step;    // warp-uniform trip count
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_it; i += step) {
+        const bool ok = i < nn;
+        long long v[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+        int b = 0;
+        if (ok) {
+            for (int a = 0; a < 3; ++a) v[a] = vox1(coords[3 * i + a], org.o[a], vs);
+            if (batch) b = batch[i];
+        }
+        if (single) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) acc[a] = min(acc[a], v[a]);
+        } else {
+            batch_min_atomic(v, b, ok && b >= 0 && b < nbatch, ws_min);
+        }
     }
-    if (!batch || nbatch == 1) {
+    if (single) {
         int64_t* const dst[3] = {ws_min, ws_min + 1, ws_min + 2};
-        block_extrema_atomic<3, 3>(v, dst);
-    } else {
-        batch_min_atomic(v, b, ok && b >= 0 && b < nbatch, ws_min);
+        block_extrema_atomic<3, 3>(acc, dst);
     }
 }
 
@@ -244,16 +265,17 @@ __global__ void fused_hash_kernel(const double* __restrict__ coords,
                                   const int64_t* __restrict__ ws_min, HashArgs ha,
                                   int32_t* __restrict__ home, int32_t* __restrict__ vox32,
                                   int64_t* stats) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = i < dyn_n(n, n_dev);
-    long long v[3] = {0, 0, 0};
-    if (valid) {
+    const int64_t nn = dyn_n(n, n_dev);
+    long long acc[7] = F3D_STATS_INIT;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += step) {
         int b = (batch && nbatch > 1) ? batch[i] : 0;
         if (b < 0 || b >= nbatch) b = 0;
-        for (int a = 0; a < 3; ++a)
-            v[a] = vox1(coords[3 * i + a], org.o[a], vs) - ws_min[3 * b + a];
+        long long v[3];
+        for (int a = 0; a < 3; ++a) v[a] = vox1(coords[3 * i + a], org.o[a], vs) - ws_min[3 * b + a];
+        hash_one(v[0], v[1], v[2], i, ha, home, vox32, true, acc);
     }
-    hash_point(v[0], v[1], v[2], i, ha, home, vox32, stats, valid);
+    flush_stats(acc, ha, stats);
 }
 
 }  // namespace hashk
@@ -263,6 +285,10 @@ using namespace f3d;
 using namespace f3d::hashk;
 
 static inline int nblk(int64_t work) { return (int)((work + kThreads - 1) / kThreads); }
+// grid-stride kernels with per-block statistics: at most 8 blocks per SM
+static inline int nblk_capped(int64_t work) {
+    return std::max(1, std::min(nblk(work), 8 * f3d_num_sms()));
+}
 
 extern "C" int f3d_voxelize(const double* coords, int64_t n, const double* origin3_host,
                             double voxel_size, int64_t* vox_out, void* stream) {
@@ -282,7 +308,7 @@ extern "C" int f3d_remap_nonnegative(const int64_t* vox, const int32_t* batch, i
     if (n == 0) return F3D_OK;
     cudaStream_t st = (cudaStream_t)stream;
     init_stats_kernel<<<nblk(3 * nbatch + 7), kThreads, 0, st>>>(nullptr, ws, 3 * nbatch);
-    batch_min_kernel<<<nblk(n), kThreads, 0, st>>>(vox, batch, n, nbatch, ws);
+    batch_min_kernel<<<nblk_capped(n), kThreads, 0, st>>>(vox, batch, n, nbatch, ws);
     remap_kernel<<<nblk(n), kThreads, 0, st>>>(vox, batch, n, nbatch, ws, vox_out);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
@@ -300,7 +326,7 @@ extern "C" int f3d_hash_bucket(const int64_t* vox, int64_t n, int kind, int32_t 
     init_stats_kernel<<<1, 32, 0, st>>>(stats_out, nullptr, 0);
     if (n > 0) {
         HashArgs ha{HashParams{kind, K, S_div, bits, 0}, 1};
-        hash_kernel<<<nblk(n), kThreads, 0, st>>>(vox, n, ha, home_out, vox32_out, stats_out);
+        hash_kernel<<<nblk_capped(n), kThreads, 0, st>>>(vox, n, ha, home_out, vox32_out, stats_out);
     }
     F3D_LAUNCH_CHECK();
     return F3D_OK;
@@ -311,7 +337,7 @@ extern "C" int f3d_morton_encode(const int64_t* vox, int64_t n, int bits, int64_
     if (n < 0 || bits < 1 || bits > 21) return F3D_ERR_CONFIG;
     cudaStream_t st = (cudaStream_t)stream;
     init_stats_kernel<<<1, 32, 0, st>>>(stats_out, nullptr, 0);
-    if (n > 0) morton_kernel<<<nblk(n), kThreads, 0, st>>>(vox, n, bits, codes_out, stats_out);
+    if (n > 0) morton_kernel<<<nblk_capped(n), kThreads, 0, st>>>(vox, n, bits, codes_out, stats_out);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }
@@ -328,10 +354,10 @@ extern "C" int f3d_voxel_hash(const double* coords, const int32_t* batch, int64_
     Origin o{{origin3_host[0], origin3_host[1], origin3_host[2]}};
     init_stats_kernel<<<nblk(3 * nbatch + 7), kThreads, 0, st>>>(stats_out, ws, 3 * nbatch);
     if (n > 0) {
-        fused_min_kernel<<<nblk(n), kThreads, 0, st>>>(coords, batch, n, n_dev, nbatch, o,
+        fused_min_kernel<<<nblk_capped(n), kThreads, 0, st>>>(coords, batch, n, n_dev, nbatch, o,
                                                         voxel_size, ws);
         HashArgs ha{HashParams{kind, K, S_div, bits, 0}, 1};
-        fused_hash_kernel<<<nblk(n), kThreads, 0, st>>>(coords, batch, n, n_dev, nbatch, o,
+        fused_hash_kernel<<<nblk_capped(n), kThreads, 0, st>>>(coords, batch, n, n_dev, nbatch, o,
                                                          voxel_size, ws, ha, home_out, vox32_out,
                                                          stats_out);
     }
