@@ -249,19 +249,6 @@ int f3d_row_ln(void *F, int f_is_f64, int64_t ldf, const void *y, int64_t ldy,
                const float *ybias, const float *gain, const float *beta,
                const double *pe_coords, const double *lo_ext, double pe_base, void *out,
                int out_kind, int64_t ldo, int64_t n, int d, double eps, void *stream);
-/* Fused stage MLP on tcgen05 (bw/stage.py:146-158) for d = 96 (config A/B width):
- *   F[r] += gelu(x[r] W_in + b_in) W_out + b_out          (exact-erf GELU)
- *   x_next[r] = LN(F[r]) * ln_g + ln_b (+ PE(pe_coords[r], lo_ext))  if x_next
- * x: (n, d) bf16 rows (LN2 output); w_in_t = W_in^T (4d, d) and w_out_t =
- * W_out^T (d, 4d), bf16 row-major; F: (n, d) fp32 residual stream.  The 4d-wide
- * hidden activations never leave TMEM.  x_next may alias x (rows are read
- * before they are rewritten).  n_dev (nullable): device row count <= n. */
-int f3d_mlp_supported(int d);
-int f3d_mlp_fused(const void *x, int64_t ldx, int64_t n, int d, const void *w_in_t,
-                  const float *b_in, const void *w_out_t, const float *b_out, float *F,
-                  int64_t ldf, const float *ln_g, const float *ln_b, const double *pe_coords,
-                  const double *lo_ext, double pe_base, void *x_next, int64_t ldxn, double eps,
-                  const int32_t *n_dev, void *stream);
 /* y = 0.5 x (1 + erf(x / sqrt 2)) in float64 (bw/stage.py:91-92). */
 int f3d_gelu_f64(const double *x, int64_t n, double *y, void *stream);
 /* u = gelu(u + bias) with the exact erf form (bw/stage.py:91-96), bf16 rows. */
@@ -294,17 +281,6 @@ int f3d_pool_parent(const int32_t *members, const int32_t *sizes, int64_t npool,
 int f3d_pool_reduce(const void *x, int dtype, int64_t ldx, int d, const int32_t *members,
                     const int32_t *sizes, int64_t npool, int rho, int op, void *out,
                     int64_t ldo, const int32_t *npool_dev, void *stream);
-
-/* Positional encoding of (bounding-box normalised) coordinates as bf16 rows,
- * with f3d_row_ln's fp32 arithmetic (bw/attention.py:271-288); and the
- * vector row_ln that adds such a precomputed table instead of evaluating
- * sin/cos (F += y + ybias when y; out = LN(F)*gain + beta + pe_tab[row]).
- * d % 12 == 0, d <= 128.  Alternative to f3d_row_ln's in-kernel PE (opt-in). */
-int f3d_pe_table(const double *coords, const double *lo_ext, double pe_base, int64_t n, int d,
-                 void *out_bf16, int64_t ldo, void *stream);
-int f3d_row_ln_pt(float *F, int64_t ldf, const void *y, int64_t ldy, const float *ybias,
-                  const float *gain, const float *beta, const void *pe_tab, int64_t ldp, void *out,
-                  int64_t ldo, int64_t n, int d, double eps, void *stream);
 
 /* A stage's last residual and the bf16 copy of the result in one pass:
  * F += y + ybias (f3d_row_ln's arithmetic; ybias NULL = zero), out = bf16(F).  d % 4 == 0.
@@ -360,25 +336,6 @@ int f3d_gemm_res_ln(const void *x, int64_t ldx, int64_t n, int K, const void *w_
                     const float *beta, const double *pe_coords, const double *lo_ext,
                     double pe_base, double eps, void *y, int64_t ldy, const int32_t *n_dev,
                     void *stream);
-
-/* u = GELU(x W_in + b_in) as bf16 rows (n x 4d): tcgen05 GEMM with the
- * bias + exact-erf GELU epilogue read from TMEM (replaces a library GEMM +
- * f3d_bias_gelu; bw/stage.py:153-156).  w_in_t = W_in^T (4d x d, row-major
- * bf16).  d in {64, 96} (f3d_gemm_gelu_supported).  n_dev (nullable): device
- * row count <= n (graph capture with a capacity n). */
-int f3d_gemm_gelu_supported(int d);
-int f3d_gemm_gelu(const void *x, int64_t ldx, int64_t n, int d, const void *w_in_t,
-                  const float *b_in, void *u, int64_t ldu, const int32_t *n_dev, void *stream);
-
-/* F += x W + bias (x: n x k bf16, w_t = W^T: d x k bf16), then, when ln_g is
- * given, x_next = LayerNorm(F) * ln_g + ln_b (+ PE of pe_coords when given) in
- * bf16: the projection GEMM and f3d_row_ln of the stage in one tcgen05 kernel
- * (bw/stage.py:146-158).  (d, k) in {(96, 96), (96, 384)} (f3d_gemm_ln_supported). */
-int f3d_gemm_ln_supported(int d, int k);
-int f3d_gemm_ln(const void *x, int64_t ldx, int64_t n, int d, int k, const void *w_t,
-                const float *bias, float *F, int64_t ldf, const float *ln_g, const float *ln_b,
-                const double *pe_coords, const double *lo_ext, double pe_base, void *x_next,
-                int64_t ldxn, double eps, const int32_t *n_dev, void *stream);
 
 /* ------------------------------------------------ training
  * LayerNorm backward fused with the residual add: dx = dres + rstd*(g*dy -

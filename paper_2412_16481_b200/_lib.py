@@ -73,16 +73,8 @@ SIGNATURES = {
                                    _I64, _P, _P]),
     "f3d_scatter_ln_pe": (_INT, [_P, _INT, _I64, _P, _P, _P, _F64, _P, _P, _P, _I64, _P, _I64,
                                  _I64, _INT, _F64, _P, _P]),
-    "f3d_pe_table": (_INT, [_P, _P, _F64, _I64, _INT, _P, _I64, _P]),
-    "f3d_row_ln_pt": (_INT, [_P, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _I64, _INT, _F64,
-                             _P]),
     "f3d_gemm_supported": (_INT, [_INT, _INT]),
     "f3d_gemm": (_INT, [_P, _I64, _I64, _INT, _P, _INT, _P, _INT, _P, _I64, _P, _P]),
-    "f3d_gemm_gelu_supported": (_INT, [_INT]),
-    "f3d_gemm_gelu": (_INT, [_P, _I64, _I64, _INT, _P, _P, _P, _I64, _P, _P]),
-    "f3d_gemm_ln_supported": (_INT, [_INT, _INT]),
-    "f3d_gemm_ln": (_INT, [_P, _I64, _I64, _INT, _INT, _P, _P, _P, _I64, _P, _P, _P, _P, _F64, _P,
-                           _I64, _F64, _P, _P]),
     "f3d_gemm_res_ln_supported": (_INT, [_INT, _INT]),
     "f3d_gemm_res_ln": (_INT, [_P, _I64, _I64, _INT, _P, _INT, _P, _P, _I64, _P, _P, _P, _P, _F64,
                                _F64, _P, _I64, _P, _P]),
@@ -93,9 +85,6 @@ SIGNATURES = {
     "f3d_softmax_bwd": (_INT, [_P, _P, _P, _P, _INT, _INT, _F64, _F64, _INT, _P, _P]),
     "f3d_attn_bwd": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64,
                             _P, _I64, _P, _I64, _INT, _INT, _P, _P, _P, _P, _P, _INT, _INT, _P]),
-    "f3d_mlp_supported": (_INT, [_INT]),
-    "f3d_mlp_fused": (_INT, [_P, _I64, _I64, _INT, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _F64,
-                             _P, _I64, _F64, _P, _P]),
 }
 
 _lib = None
@@ -128,9 +117,9 @@ KERNELS_PER_CALL = {
     "f3d_scatter_rows": 1, "f3d_gather_rows": 1, "f3d_scatter_rows_bf16_f32": 1, "f3d_bswin_attention": 1,
     "f3d_bswin_attention_tc": 1,
     "f3d_positional_encoding": 1, "f3d_stage_pe": 1, "f3d_coord_bbox": 2, "f3d_row_ln": 1,
-    "f3d_gelu_f64": 1, "f3d_bias_gelu": 1, "f3d_pool_build": 2, "f3d_pool_reduce": 1, "f3d_pool_parent": 1, "f3d_gemm_gelu": 1, "f3d_gemm": 1, "f3d_gemm_res_ln": 1, "f3d_gemm_ln": 1, "f3d_pe_table": 1, "f3d_row_ln_pt": 1, "f3d_scatter_ln_pe": 1, "f3d_pool_reduce_res": 1, "f3d_residual_out": 1, "f3d_ln_bwd": 1, "f3d_gelu_bwd": 1, "f3d_colsum": 1,
+    "f3d_gelu_f64": 1, "f3d_bias_gelu": 1, "f3d_pool_build": 2, "f3d_pool_reduce": 1, "f3d_pool_parent": 1, "f3d_gemm": 1, "f3d_gemm_res_ln": 1, "f3d_scatter_ln_pe": 1, "f3d_pool_reduce_res": 1, "f3d_residual_out": 1, "f3d_ln_bwd": 1, "f3d_gelu_bwd": 1, "f3d_colsum": 1,
     "f3d_softmax_bwd": 1, "f3d_attn_bwd": 2,
-    "f3d_plan_round": 1, "f3d_plan_rounds": 1, "f3d_plan_pool": 1, "f3d_mlp_fused": 1,
+    "f3d_plan_round": 1, "f3d_plan_rounds": 1, "f3d_plan_pool": 1,
 }
 
 

@@ -229,7 +229,7 @@ class Backbone:
             d = X.shape[1]
             F = torch.empty((n, d), dtype=torch.float32, device=C.device)
             rn = r.runner
-            if (SCATTER_LN and rn.pe_tab is None and d % 12 == 0 and d <= 128
+            if (SCATTER_LN and d % 12 == 0 and d <= 128
                     and X.is_contiguous()
                     and X.dtype in (torch.bfloat16, torch.float32)):
                 # scatter + the stage's first LN1 + PE in one pass (bit-identical)
@@ -282,11 +282,10 @@ class Backbone:
         # pooled capacities keep the residual in the stage and pool F itself)
         np_cap_ = pool_capacity(n, cfg.K + 1, cfg.pool_rho)[1] if cfg.pool_rho else 0
         defer = (cfg.pool_rho and POOL_RESIDUAL and F.dtype == torch.float32 and d % 4 == 0
-                 and np_cap_ * (d // 4) < 2 ** 31
-                 and not r.runner.gemm_ln and not r.runner.fused_mlp)
+                 and np_cap_ * (d // 4) < 2 ** 31)
         r.out_bf16 = None
         if (getattr(self, "_want_out_bf16", False) and si == len(self.stages) - 1
-                and not cfg.pool_rho and not r.runner.gemm_ln and not r.runner.fused_mlp):
+                and not cfg.pool_rho):
             # the graphs read the last stage back in bf16: written with its last residual
             r.out_bf16 = torch.empty((n, d), dtype=torch.bfloat16, device=F.device)
         hook = getattr(self, "round_hook", None)      # test instrumentation (eager only)

@@ -313,14 +313,13 @@ namespace stage {
 // bf16 y / out, d % 4 == 0, d <= 128.  Lane q owns columns [4q, 4q+4) (one
 // 16-byte F load, one 8-byte y load); each warp carries RPW rows at once so
 // every load of all of them is in flight before the first reduction.
-template <int RPW, bool HAS_Y, bool HAS_OUT, bool HAS_PE, bool HAS_PT = false>
+template <int RPW, bool HAS_Y, bool HAS_OUT, bool HAS_PE>
 __global__ void __launch_bounds__(kThreads, HAS_PE ? 4 : 5) row_ln_vec_kernel(
     float* __restrict__ F, int64_t ldf, const __nv_bfloat16* __restrict__ y, int64_t ldy,
     const float* __restrict__ ybias, const float* __restrict__ gain,
     const float* __restrict__ beta, const double* __restrict__ pec,
     const double* __restrict__ lo_ext, float pl2, __nv_bfloat16* __restrict__ out, int64_t ldo,
-    int64_t n, int d, float eps, const __nv_bfloat16* __restrict__ pt = nullptr,
-    int64_t ldp = 0) {
+    int64_t n, int d, float eps) {
     const int lane = threadIdx.x & 31;
     const bool act = lane < (d >> 2);
     const int64_t row0 = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * RPW;
@@ -412,15 +411,6 @@ __global__ void __launch_bounds__(kThreads, HAS_PE ? 4 : 5) row_ln_vec_kernel(
         float o1 = (v[i].y - m) * rstd * gg.y + bb.y;
         float o2 = (v[i].z - m) * rstd * gg.z + bb.z;
         float o3 = (v[i].w - m) * rstd * gg.w + bb.w;
-        if (HAS_PT) {              // precomputed bf16 PE rows (f3d_pe_table)
-            const uint2 pp = *reinterpret_cast<const uint2*>(pt + row * ldp + c0);
-            const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pp);
-            const float2 p01 = __bfloat1622float2(ph[0]), p23 = __bfloat1622float2(ph[1]);
-            o0 += p01.x;
-            o1 += p01.y;
-            o2 += p23.x;
-            o3 += p23.y;
-        }
         if (HAS_PE) {
             float sn[2], cs[2];
 #pragma unroll
@@ -434,45 +424,6 @@ __global__ void __launch_bounds__(kThreads, HAS_PE ? 4 : 5) row_ln_vec_kernel(
             o3 += cs[1];
         }
         __nv_bfloat162 h0 = __floats2bfloat162_rn(o0, o1), h1 = __floats2bfloat162_rn(o2, o3);
-        uint2 w;
-        w.x = *reinterpret_cast<uint32_t*>(&h0);
-        w.y = *reinterpret_cast<uint32_t*>(&h1);
-        *reinterpret_cast<uint2*>(out + row * ldo + c0) = w;
-    }
-}
-
-// bf16 PE rows with row_ln_vec_kernel's arithmetic (lanes over 4 columns),
-// computed once per stage from the scattered coordinates.
-__global__ void __launch_bounds__(kThreads) pe_table_kernel(const double* __restrict__ pec,
-                                                            const double* __restrict__ lo_ext,
-                                                            float pl2, int64_t n, int d,
-                                                            __nv_bfloat16* __restrict__ out,
-                                                            int64_t ldo) {
-    const int lane = threadIdx.x & 31;
-    if (lane >= (d >> 2)) return;
-    const int c0 = 4 * lane;
-    const int npair = d / 6, blk = 2 * npair;
-    int pa[2];
-    float fq[2], pinv[2];
-    double plo[2];
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        const int c = c0 + 2 * p;
-        pa[p] = c / blk;
-        const int pj = (c - pa[p] * blk) >> 1;
-        fq[p] = exp2f(-(float)pj / (float)npair * pl2);
-        plo[p] = lo_ext ? lo_ext[pa[p]] : 0.0;
-        pinv[p] = lo_ext ? (float)(1.0 / lo_ext[3 + pa[p]]) : 1.f;
-    }
-    for (int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < n;
-         row += (int64_t)gridDim.x * (kThreads / 32)) {
-        float sn[2], cs[2];
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            const float xn = (float)__dsub_rn(pec[3 * row + pa[p]], plo[p]) * pinv[p];
-            __sincosf(xn * fq[p], &sn[p], &cs[p]);
-        }
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(sn[0], cs[0]), h1 = __floats2bfloat162_rn(sn[1], cs[1]);
         uint2 w;
         w.x = *reinterpret_cast<uint32_t*>(&h0);
         w.y = *reinterpret_cast<uint32_t*>(&h1);
@@ -766,44 +717,6 @@ extern "C" int f3d_bias_gelu(void* u_bf16, int64_t n, int dh, const float* bias,
         stage::bias_gelu_kernel<<<grid_for(n * dh / 2, stage::kThreads), stage::kThreads, 0, st>>>(
             (__nv_bfloat16*)u_bf16, n, dh, bias);
     }
-    F3D_LAUNCH_CHECK();
-    return F3D_OK;
-}
-
-extern "C" int f3d_pe_table(const double* coords, const double* lo_ext, double pe_base, int64_t n,
-                            int d, void* out_bf16, int64_t ldo, void* stream) {
-    if (d % 6 || d % 4 || d > 128 || n < 0 || ldo % 4 || ((uintptr_t)out_bf16 & 7))
-        return F3D_ERR_CONFIG;
-    if (n == 0) return F3D_OK;
-    const unsigned g = (unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)f3d_num_sms() * 16);
-    stage::pe_table_kernel<<<g, stage::kThreads, 0, (cudaStream_t)stream>>>(
-        coords, lo_ext, (float)log2(pe_base), n, d, (__nv_bfloat16*)out_bf16, ldo);
-    F3D_LAUNCH_CHECK();
-    return F3D_OK;
-}
-
-extern "C" int f3d_row_ln_pt(float* F, int64_t ldf, const void* y, int64_t ldy,
-                             const float* ybias, const float* gain, const float* beta,
-                             const void* pe_tab, int64_t ldp, void* out, int64_t ldo, int64_t n,
-                             int d, double eps, void* stream) {
-    auto al = [](const void* p, int a) { return ((uintptr_t)p % a) == 0; };
-    if (d % 4 || d > 128 || ldf % 4 || !al(F, 16) || !out || !gain || !beta || !pe_tab ||
-        ldo % 4 || ldp % 4 || !al(out, 8) || !al(pe_tab, 8) || !al(gain, 16) || !al(beta, 16) ||
-        (y && (ldy % 4 || !al(y, 8) || (ybias && !al(ybias, 16)))))
-        return F3D_ERR_CONFIG;
-    if (n == 0) return F3D_OK;
-    constexpr int RPW = F3D_LN_RPW;
-    const unsigned g = (unsigned)((n + RPW * 8 - 1) / (RPW * 8));
-    using BF = __nv_bfloat16;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (y)
-        stage::row_ln_vec_kernel<RPW, true, true, false, true><<<g, stage::kThreads, 0, st>>>(
-            F, ldf, (const BF*)y, ldy, ybias, gain, beta, nullptr, nullptr, 0.f, (BF*)out, ldo, n,
-            d, (float)eps, (const BF*)pe_tab, ldp);
-    else
-        stage::row_ln_vec_kernel<RPW, false, true, false, true><<<g, stage::kThreads, 0, st>>>(
-            F, ldf, nullptr, 0, nullptr, gain, beta, nullptr, nullptr, 0.f, (BF*)out, ldo, n, d,
-            (float)eps, (const BF*)pe_tab, ldp);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
 }

@@ -27,24 +27,6 @@ from .bucketing import BucketAssignment
 from .errors import ConfigError
 
 LN_EPS = 1e-12
-# F3D_FUSED_MLP=1 selects the fused tcgen05 MLP (csrc/mlp_tc.cu, d = 96) over
-# cuBLAS GEMMs + f3d_bias_gelu + f3d_row_ln.  Opt-in: measured 0.46 vs 0.39 ms
-# per config-B step (tools/mlp_ab.py)
-FUSED_MLP = os.environ.get("F3D_FUSED_MLP", "0") == "1"
-# F3D_GEMM_LN=1 selects f3d_gemm_ln (projection + residual + LayerNorm (+PE) in
-# one tcgen05 kernel) over cuBLAS GEMMs + f3d_row_ln.  Opt-in: measured 1.37 vs
-# 1.22 ms per config-B step -- one CTA per SM leaves the row epilogue with too
-# few loads in flight
-GEMM_LN = os.environ.get("F3D_GEMM_LN", "0") == "1"
-# The MLP's first half: f3d_gemm_gelu (TMA-fed tcgen05 GEMM, bias + GELU
-# epilogue from TMEM, u written once) instead of cuBLAS GEMM + f3d_bias_gelu
-# (tools/gemm_gelu_bench.py, d = 96: 27 vs 30 us at 50K rows, 50 vs 52 at 100K,
-# 144 vs 184 at 400K, 321 vs 422 at 1M).  F3D_GEMM_GELU=0 selects the cuBLAS path.
-# F3D_PE_TABLE=1: the positional encoding is computed once per stage into a bf16
-# table (coordinate-only, part of the overlapped prologue) and row_ln adds it.
-# Opt-in: measured 1.117 vs 1.103 ms per config-B step (the stage-0 table sits on
-# the critical path and the table reads cost about what the sin/cos saved)
-PE_TABLE = os.environ.get("F3D_PE_TABLE", "0") == "1"
 # The QKV, O-projection and MLP GEMMs run on f3d_gemm (csrc/gemm_tc.cu: TMA-fed
 # persistent tcgen05 GEMM, bias / GELU epilogue from TMEM).  F3D_OWN_GEMM=0
 # selects the library GEMMs (A/B measurements only).
@@ -60,9 +42,6 @@ OWN_GEMM = {k for k in ("qkv", "o", "in", "out")
 # tiles (store, reload) on the critical path of every tile, where the
 # separate full-occupancy row pass streams F at HBM speed.
 GEMM_RES_LN = os.environ.get("F3D_GEMM_RES_LN", "0") == "1"
-_GG = os.environ.get("F3D_GEMM_GELU")
-GEMM_GELU = _GG != "0"
-GEMM_GELU_MIN_ROWS = 0
 
 
 @dataclass
@@ -194,24 +173,8 @@ class StageRunner:
         self.a = L.empty((n, d), torch.bfloat16)
         self.y = L.empty((n, d), torch.bfloat16)
         self.n_dev = n_dev
-        self.fused_mlp = (FUSED_MLP and f_dtype == torch.float32 and dhid == 4 * d
-                          and self.w.get("w_in_t") is not None
-                          and bool(L.load().f3d_mlp_supported(d)))
-        self.u = None if self.fused_mlp else L.empty((n, dhid), torch.bfloat16)
-        self.pe_tab = None
-        if PE_TABLE and f_dtype == torch.float32 and d % 12 == 0 and d <= 128:
-            self.pe_tab = L.empty((n, d), torch.bfloat16)
-            L.call("f3d_pe_table", L.ptr(self.coords), L.ptr(self.lo_ext), 10000.0, n, d,
-                   L.ptr(self.pe_tab), d, L.stream())
+        self.u = L.empty((n, dhid), torch.bfloat16)
         lib = L.load()
-        self.gemm_ln = (GEMM_LN and not self.fused_mlp and dhid == 4 * d
-                        and self.w.get("w_o_t") is not None
-                        and bool(lib.f3d_gemm_ln_supported(d, d))
-                        and bool(lib.f3d_gemm_ln_supported(d, dhid)))
-        self.gemm_gelu = (GEMM_GELU and n >= GEMM_GELU_MIN_ROWS and not self.fused_mlp
-                          and dhid == 4 * d
-                          and self.w.get("w_in_t") is not None
-                          and bool(L.load().f3d_gemm_gelu_supported(d)))
         ok = self.w.get("w_qkv_t") is not None
         self.own = {k for k, (k_, n_) in (("qkv", (d, 3 * d)), ("o", (d, d)), ("in", (d, dhid)),
                                           ("out", (dhid, d)))
@@ -233,23 +196,11 @@ class StageRunner:
                L.stream())
 
     def _row_ln(self, F, y, ybias, g, b, pe, out):
-        if pe and self.pe_tab is not None and F.dtype == torch.float32 and out is not None:
-            L.call("f3d_row_ln_pt", L.ptr(F), F.stride(0), L.ptr(y),
-                   0 if y is None else y.stride(0), L.ptr(ybias), L.ptr(g), L.ptr(b),
-                   L.ptr(self.pe_tab), self.pe_tab.stride(0), L.ptr(out), out.stride(0), self.n,
-                   self.d, LN_EPS, L.stream())
-            return
         L.call("f3d_row_ln", L.ptr(F), int(F.dtype == torch.float64), F.stride(0), L.ptr(y),
                0 if y is None else y.stride(0), L.ptr(ybias), L.ptr(g), L.ptr(b),
                L.ptr(self.coords) if pe else None, L.ptr(self.lo_ext) if pe else None, 10000.0,
                L.ptr(out), 0, 0 if out is None else out.stride(0), self.n, self.d, LN_EPS,
                L.stream())
-
-    def _gemm_ln(self, X, k, w_t, bias, F, g, b, pe, out):
-        L.call("f3d_gemm_ln", L.ptr(X), X.stride(0), self.n, self.d, k, L.ptr(w_t), L.ptr(bias),
-               L.ptr(F), F.stride(0), L.ptr(g), L.ptr(b), L.ptr(self.coords) if pe else None,
-               L.ptr(self.lo_ext) if pe else None, 10000.0, L.ptr(out),
-               0 if out is None else out.stride(0), LN_EPS, L.ptr(self.n_dev), L.stream())
 
     def run(self, F: torch.Tensor, x_ready: bool = False,
             defer_last_residual: bool = False, out_bf16=None) -> torch.Tensor:
@@ -278,10 +229,7 @@ class StageRunner:
                 # test instrumentation (parity on the GPU's own round input):
                 # called at enqueue time with the round's bf16 Q/K/V and output
                 hook(t, q, k, v, self.a)
-            if self.gemm_ln and F.dtype == torch.float32:
-                self._gemm_ln(self.a, self.d, w["w_o_t"], w["b_o"], F, w["ln2_g"], w["ln2_b"],
-                              False, self.x)
-            elif self.res_ln and F.dtype == torch.float32:
+            if self.res_ln and F.dtype == torch.float32:
                 # F += a W_o + b_o;  x = LN2(F)
                 self._gemm_res_ln(self.a, d, w["w_o_t"], w["b_o"], F, w["ln2_g"], w["ln2_b"],
                                   False, self.x)
@@ -291,33 +239,12 @@ class StageRunner:
                 else:
                     torch.mm(self.a, w["w_o"], out=self.y)
                 self._row_ln(F, self.y, w["b_o"], w["ln2_g"], w["ln2_b"], None, self.x)
-            if self.fused_mlp and F.dtype == torch.float32:
-                last = t + 1 == R
-                # F += MLP(x); x <- LN1(F) + PE for the next round, one kernel
-                L.call("f3d_mlp_fused", L.ptr(self.x), self.x.stride(0), self.n, self.d,
-                       L.ptr(w["w_in_t"]), L.ptr(w["b_in"]), L.ptr(w["w_out_t"]), L.ptr(w["b_out"]),
-                       L.ptr(F), F.stride(0), None if last else L.ptr(w["ln1_g"]),
-                       None if last else L.ptr(w["ln1_b"]), None if last else L.ptr(self.coords),
-                       None if last else L.ptr(self.lo_ext), 10000.0,
-                       None if last else L.ptr(self.x), self.x.stride(0), LN_EPS,
-                       L.ptr(self.n_dev), L.stream())
-                continue
             if "in" in own:
                 self._gemm(self.x, d, w["w_in_t"], dhid, w["b_in"], True, self.u)
-            elif self.gemm_gelu:
-                L.call("f3d_gemm_gelu", L.ptr(self.x), self.x.stride(0), self.n, self.d,
-                       L.ptr(w["w_in_t"]), L.ptr(w["b_in"]), L.ptr(self.u), self.u.stride(0),
-                       L.ptr(self.n_dev), L.stream())
             else:
                 torch.mm(self.x, w["w_in"], out=self.u)
                 L.call("f3d_bias_gelu", L.ptr(self.u), self.n, self.u.shape[1],
                        L.ptr(w["b_in"]), L.stream())
-            if self.gemm_ln and F.dtype == torch.float32:
-                last = t + 1 == R
-                self._gemm_ln(self.u, self.u.shape[1], w["w_out_t"], w["b_out"], F,
-                              None if last else w["ln1_g"], None if last else w["ln1_b"],
-                              not last, None if last else self.x)
-                continue
             if t + 1 < R and self.res_ln and F.dtype == torch.float32:
                 # F += g W_out + b_out;  x = LN1(F) + PE for the next round
                 self._gemm_res_ln(self.u, dhid, w["w_out_t"], w["b_out"], F, w["ln1_g"],

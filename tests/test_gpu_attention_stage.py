@@ -216,172 +216,6 @@ def test_attention_growing_max_rescales(d, H):
     assert rel(out, ref) < 3e-2, rel(out, ref)
 
 
-def test_fused_mlp_matches_unfused_stage():
-    """The opt-in fused tcgen05 MLP (csrc/mlp_tc.cu) reproduces the cuBLAS +
-    bias_gelu + row_ln path of a 2-round stage within bf16 tolerance."""
-    import torch
-
-    from paper_2412_16481_b200 import stage as ST
-    r = np.random.default_rng(5)
-    n, d = 3000, 96
-    coords = r.random((n, 3))
-    feats = r.normal(size=(n, d))
-    a = F.assign_buckets(F.remap_nonnegative(F.voxelize(F.PointCloud(coords), F.VoxelGrid(1 / 16))),
-                         None, F.HashConfig("zorder-div", K=16, S_div=256), 256)
-    sf, _ = F.scatter(feats, a)
-    sc, _ = F.scatter(coords, a)
-    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
-    p = F.init_params(0, d, n_heads=4)
-    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
-    C = torch.tensor(sc, device="cuda")
-    old = ST.FUSED_MLP
-    try:
-        ST.FUSED_MLP = False
-        ref = F.stage_forward(X, C, a, sched, p)
-        ST.FUSED_MLP = True
-        out = F.stage_forward(X, C, a, sched, p)
-    finally:
-        ST.FUSED_MLP = old
-    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
-    assert rr < 1e-2, rr
-
-
-@pytest.mark.parametrize("n,d,ndev", [(1000, 96, None), (4099, 96, 4000), (777, 64, None)])
-def test_gemm_gelu_matches_torch(n, d, ndev):
-    """f3d_gemm_gelu (tcgen05 GEMM + bias + erf-GELU epilogue) against torch
-    fp32 gelu(x W_in + b) on the same bf16 operands; rows past n_dev untouched."""
-    import torch
-
-    from paper_2412_16481_b200 import _lib as L
-    g = torch.Generator(device="cuda").manual_seed(n)
-    x = torch.randn((n, d), device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn((d, 4 * d), device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
-    b = torch.randn((4 * d,), device="cuda", generator=g) * 0.1
-    wt = w.t().contiguous()
-    u = torch.full((n, 4 * d), 7.0, device="cuda", dtype=torch.bfloat16)
-    nd = None if ndev is None else torch.tensor([ndev], dtype=torch.int32, device="cuda")
-    L.call("f3d_gemm_gelu", L.ptr(x), x.stride(0), n, d, L.ptr(wt), L.ptr(b), L.ptr(u),
-           u.stride(0), L.ptr(nd), L.stream())
-    m = n if ndev is None else ndev
-    ref = torch.nn.functional.gelu(x.float() @ w.float() + b)[:m]
-    got = u[:m].float()
-    rr = ((got - ref).norm() / ref.norm()).item()
-    assert rr < 5e-3, rr
-    if ndev is not None:
-        assert bool((u[m:] == 7.0).all())
-
-
-def test_stage_gemm_gelu_matches_cublas_path():
-    """The stage with f3d_gemm_gelu (forced on) against the cuBLAS + bias_gelu path."""
-    import torch
-
-    from paper_2412_16481_b200 import stage as ST
-    a, sf, sc = _config_a(n=3000, d=96)
-    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
-    p = F.init_params(0, 96, n_heads=4)
-    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
-    C = torch.tensor(sc, device="cuda")
-    old = ST.GEMM_GELU, ST.GEMM_GELU_MIN_ROWS
-    try:
-        ST.GEMM_GELU = False
-        ref = F.stage_forward(X, C, a, sched, p)
-        ST.GEMM_GELU, ST.GEMM_GELU_MIN_ROWS = True, 0
-        out = F.stage_forward(X, C, a, sched, p)
-    finally:
-        ST.GEMM_GELU, ST.GEMM_GELU_MIN_ROWS = old
-    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
-    assert rr < 1e-2, rr
-
-
-@pytest.mark.parametrize("k,ln,pe,ndev", [(96, True, False, None), (384, True, True, 2900),
-                                          (384, False, False, None), (96, True, True, None)])
-def test_gemm_ln_matches_torch(k, ln, pe, ndev):
-    """f3d_gemm_ln: F += x W + b, x_next = LN(F) g + b (+PE) against torch on
-    the same bf16 operands (y rounded to bf16 as the unfused GEMM output)."""
-    import torch
-
-    from paper_2412_16481_b200 import _lib as L
-    n, d = 3001, 96
-    g = torch.Generator(device="cuda").manual_seed(k + n)
-    x = torch.randn((n, k), device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn((k, d), device="cuda", generator=g) / k ** 0.5).to(torch.bfloat16)
-    bias = torch.randn((d,), device="cuda", generator=g) * 0.1
-    F0 = torch.randn((n, d), device="cuda", generator=g)
-    lg = 1 + 0.1 * torch.randn((d,), device="cuda", generator=g)
-    lb = 0.1 * torch.randn((d,), device="cuda", generator=g)
-    coords = torch.rand((n, 3), device="cuda", dtype=torch.float64, generator=g)
-    lo_ext = torch.tensor([0, 0, 0, 1, 1, 1], device="cuda", dtype=torch.float64)
-    Fg = F0.clone()
-    xn = torch.full((n, d), 3.0, device="cuda", dtype=torch.bfloat16)
-    nd = None if ndev is None else torch.tensor([ndev], dtype=torch.int32, device="cuda")
-    wt = w.t().contiguous()
-    rc = L.load().f3d_gemm_ln(L.ptr(x), x.stride(0), n, d, k, L.ptr(wt), L.ptr(bias), L.ptr(Fg),
-                              Fg.stride(0), L.ptr(lg) if ln else None, L.ptr(lb) if ln else None,
-                              L.ptr(coords) if pe else None, L.ptr(lo_ext) if pe else None,
-                              __import__("ctypes").c_double(10000.0), L.ptr(xn) if ln else None,
-                              xn.stride(0), __import__("ctypes").c_double(1e-12), L.ptr(nd),
-                              L.stream())
-    assert rc == 0
-    m = n if ndev is None else ndev
-    y = (x.float() @ w.float()).to(torch.bfloat16).float()
-    Fr = F0 + (y + bias)
-    assert float(((Fg[:m] - Fr[:m]).norm() / Fr[:m].norm()).item()) < 1e-3
-    assert torch.equal(Fg[m:], F0[m:])
-    if ln:
-        xr = torch.nn.functional.layer_norm(Fr, (d,), lg, lb, eps=1e-12)
-        if pe:
-            xr = xr + torch.tensor(F.positional_encoding(coords.cpu().numpy(), d),
-                                   device="cuda", dtype=torch.float32)
-        got = xn[:m].float()
-        assert float(((got - xr[:m]).norm() / xr[:m].norm()).item()) < 1e-2
-        assert bool((xn[m:] == 3.0).all())
-
-
-def test_stage_gemm_ln_matches_cublas_path():
-    """The stage with f3d_gemm_ln (opt-in) against cuBLAS GEMMs + f3d_row_ln."""
-    import torch
-
-    from paper_2412_16481_b200 import stage as ST
-    a, sf, sc = _config_a(n=3000, d=96)
-    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
-    p = F.init_params(0, 96, n_heads=4)
-    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
-    C = torch.tensor(sc, device="cuda")
-    old = ST.GEMM_LN
-    try:
-        ST.GEMM_LN = False
-        ref = F.stage_forward(X, C, a, sched, p)
-        ST.GEMM_LN = True
-        out = F.stage_forward(X, C, a, sched, p)
-    finally:
-        ST.GEMM_LN = old
-    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
-    assert rr < 1e-2, rr
-
-
-def test_stage_pe_table_matches_computed_pe():
-    """The opt-in bf16 PE table path (f3d_pe_table + f3d_row_ln_pt) against the
-    default in-kernel PE (bf16 rounding of the table only)."""
-    import torch
-
-    from paper_2412_16481_b200 import stage as ST
-    a, sf, sc = _config_a(n=3000, d=96)
-    sched = F.build_schedule(len(a.bucket_table()[0]), 2, 1, 1, 2)
-    p = F.init_params(0, 96, n_heads=4)
-    X = torch.tensor(sf, dtype=torch.float32, device="cuda")
-    C = torch.tensor(sc, device="cuda")
-    old = ST.PE_TABLE
-    try:
-        ST.PE_TABLE = False
-        ref = F.stage_forward(X, C, a, sched, p)
-        ST.PE_TABLE = True
-        out = F.stage_forward(X, C, a, sched, p)
-    finally:
-        ST.PE_TABLE = old
-    rr = ((out.double() - ref.double()).norm() / ref.double().norm()).item()
-    assert rr < 1e-2, rr
-
-
 @pytest.mark.parametrize("n,k,ln,pe,ndev", [(3001, 96, True, False, None),
                                             (3001, 384, True, True, 2900),
                                             (4096, 384, False, False, None),

@@ -43,7 +43,3 @@ for name, K, N, gelu in (("qkv", d, 3 * d, 0), ("o", d, d, 0), ("mlp_in", d, 4 *
     nbytes = 2 * n * (K + N)
     print(f"{name:8s} n={n} K={K} N={N} gelu={gelu}: f3d_gemm {ours:7.1f} us "
           f"({nbytes / ours / 1e3:6.0f} GB/s)  cuBLAS mm {lib:7.1f} us", flush=True)
-    if gelu and L.load().f3d_gemm_gelu_supported(d):
-        gg = timeit(lambda: L.call("f3d_gemm_gelu", L.ptr(x), K, n, d, L.ptr(wt), L.ptr(b),
-                                   L.ptr(y), N, None, L.stream()))
-        print(f"{'':8s} f3d_gemm_gelu (d={d} special) {gg:7.1f} us")
