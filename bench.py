@@ -348,6 +348,23 @@ def family_times(calls, names, flush, reps=20):
     return statistics.median(ms), len(sel)
 
 
+def config_e(world, rank, local, scenes=8, steps=2):
+    """BASELINE configs[4]: the training step (forward + fused attention
+    backward + gradient all-reduce over the ranks + SGD) on 8 config-B scenes
+    per GPU (64 over 8 GPUs); tools/train_bench.run.  Weak scaling."""
+    from tools.train_bench import run
+    r = run(scenes=scenes, points=N_POINTS, steps=steps, warmup=1, rank=rank, world=world,
+            local=local)
+    return {"value": r["train_points_per_s"], "unit": "training points/s", "scaling": "weak",
+            "ms_per_step": r["ms_per_step"], "scenes_per_gpu": scenes, "n_gpus": world,
+            "max_mem_gb": r["max_mem_gb"],
+            "workload": ("config E: 8 ScanNet-sized scenes (100K points) per GPU through the "
+                         "2-stage backbone, forward with saved activations + backward (fused "
+                         "attention backward kernels, no m x m tiles) + one flat NCCL "
+                         "all_reduce per stage + SGD, one CUDA graph per scene; CUDA events, "
+                         "max over ranks")}
+
+
 def config_c(world, rank, local, reps=3):
     """BASELINE configs[2]: 16 x 200K-point scenes (synth_cloud 100..115),
     K=512 S=512 S_div=512 then K=256 S_div=1024, C=96; scenes split
@@ -566,13 +583,14 @@ def main():
         backbone_forward(coords, feats)
     pub_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / min(args.steps, 5))
 
-    cfg_c = None
+    cfg_c = cfg_e = None
     if not args.no_extras:
         from paper_2412_16481_b200 import backbone as BBm
         BBm._BACKBONES.clear()
         del bb
         torch.cuda.empty_cache()
         cfg_c = config_c(world, rank, local)
+        cfg_e = config_e(world, rank, local)
 
     if rank == 0:
         hbm, tflops, src = peaks()
@@ -677,6 +695,8 @@ def main():
         }
         if cfg_c is not None:
             line["config_c"] = cfg_c
+        if cfg_e is not None:
+            line["config_e"] = cfg_e
         if not args.no_extras:
             line["roofline_wide"] = wide_attention_roofline(tflops)
         if not args.no_cpu_baseline and world == 1:

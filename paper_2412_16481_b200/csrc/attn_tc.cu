@@ -88,6 +88,15 @@ template <int DH>
 __host__ __device__ constexpr int cs_for() {
     return DH == 64 ? 2 : 1;   // measured: DH 64 451 -> 492 TFLOP/s; DH 32 (0.165 -> 0.185 ms) and DH 128 (948 -> 919) slower
 }
+// Resident CTAs per SM for head dims <= 32 (A/B knob): with several small
+// CTAs (NQ = 1 each) the softmax warps of an SM sub-partition belong to
+// different, independently progressing CTAs instead of three Q tiles of one
+// item that advance in lock step.
+#ifndef F3D_CTAS_SMALL
+#define F3D_CTAS_SMALL 1
+#endif
+template <int DH>
+__host__ __device__ constexpr int ctas_per_sm() { return DH <= 32 ? F3D_CTAS_SMALL : 1; }
 template <int DH>
 __host__ __device__ constexpr int threads_for() {
     return (4 + 4 * nq_for_dh(DH) * cs_for<DH>()) * 32;
@@ -202,7 +211,7 @@ struct Cfg {
     static constexpr int kKVBytes = kBN * DH * 2;       // one of K or V
     static constexpr int CS = cs_for<DH>();
     static constexpr int kXchg = CS > 1 ? NQ * 4 * 3 * CS * 32 * 4 : 0;   // pair exchange
-    static constexpr int kBudget = 227 * 1024 - 1024 - 512 - kXchg;
+    static constexpr int kBudget = 227 * 1024 / ctas_per_sm<DH>() - 1024 - 512 - kXchg;
     // K/V depth first (>= 4 stages), then a second Q buffer if it still fits
     static constexpr int NQB = (2 * NQ * kQBytes + 4 * 2 * kKVBytes <= kBudget) ? 2 : 1;
     static constexpr int kNstFit = (kBudget - NQB * NQ * kQBytes) / (2 * kKVBytes);
@@ -217,7 +226,10 @@ struct Cfg {
     static constexpr int kSmem = kOffX + kXchg + 1024;   // + 1 KB alignment slack
     static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (NSB*g+b)*kBN
     static constexpr int kTmemO = NSB * NQ * kBN;       // O of tile g: kTmemO + g*DH
-    static constexpr int kTmemCols = NQ * (NSB * kBN + DH) <= 256 ? 256 : 512;
+    static constexpr int kTmemNeed = NQ * (NSB * kBN + DH);
+    static constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64
+                                     : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
+    static_assert(kTmemCols * ctas_per_sm<DH>() <= 512, "TMEM for the resident CTAs");
     static_assert(NQ * (NSB * kBN + DH) <= 512, "TMEM budget");
     static_assert(kNst >= 2, "K/V pipeline depth");
     static_assert(kSmem <= 227 * 1024, "smem budget");
@@ -299,7 +311,7 @@ __device__ __forceinline__ void tma_rows(const Maps& M, int mp, const Args& A, i
 }
 
 template <int DH, typename OutT>
-__global__ void __launch_bounds__(threads_for<DH>(), 1)
+__global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
     bswin_attn_tc_kernel(const Args A, const __grid_constant__ Maps M) {
     using C = Cfg<DH>;
     using L = Lay<DH>;
@@ -892,7 +904,7 @@ int launch(Args A, int64_t n_rows, cudaStream_t st) {
                 A.use_tma = 0;
         }
     const int total = A.nwork * A.H;
-    const int grid = std::max(1, std::min(total, f3d_num_sms()));
+    const int grid = std::max(1, std::min(total, f3d_num_sms() * ctas_per_sm<DH>()));
     kern<<<grid, threads_for<DH>(), C::kSmem, st>>>(A, M);
     F3D_LAUNCH_CHECK();
     return F3D_OK;
