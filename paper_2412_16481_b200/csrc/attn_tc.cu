@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
-    const int total = (A.live ? __ldg(A.live) : A.nwork) * A.H;
+    int total = 0;                               // work items (read after pdl_wait)
     const bool dyn = A.live != nullptr;
     int32_t* sched = dyn ? const_cast<int32_t*>(A.live) + 4 : nullptr;   // [next item, CTAs done]
     // consumers of each item: the NQ MMA issuers and every softmax warp
@@ -434,6 +434,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
         tmem_relinquish();
     }
     fence_proxy_async();
+    // local set-up above overlaps the previous kernel's tail under
+    // programmatic dependent launch; inputs are read from here on
+    pdl_wait();
+    total = (A.live ? __ldg(A.live) : A.nwork) * A.H;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -905,8 +909,7 @@ int launch(Args A, int64_t n_rows, cudaStream_t st) {
         }
     const int total = A.nwork * A.H;
     const int grid = std::max(1, std::min(total, f3d_num_sms() * ctas_per_sm<DH>()));
-    kern<<<grid, threads_for<DH>(), C::kSmem, st>>>(A, M);
-    F3D_LAUNCH_CHECK();
+    F3D_CUDA_TRY(f3d_launch(kern, dim3(grid), dim3(threads_for<DH>()), C::kSmem, st, A, M));
     return F3D_OK;
 }
 

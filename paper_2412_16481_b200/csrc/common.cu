@@ -1,5 +1,6 @@
 // Library-wide state: error text, device properties.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "f3d_common.cuh"
@@ -9,6 +10,15 @@ static thread_local char g_last_error[512] = "";
 void f3d_set_last_cuda_error(cudaError_t e) {
     snprintf(g_last_error, sizeof(g_last_error), "CUDA error %d: %s", (int)e,
              cudaGetErrorString(e));
+}
+
+bool f3d_pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("F3D_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
 }
 
 int f3d_num_sms() {

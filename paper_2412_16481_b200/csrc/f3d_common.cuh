@@ -22,10 +22,35 @@ int f3d_num_sms();
 // copy engine and then queues behind concurrent H2D/D2H traffic (measured:
 // 40 us stalls per step in the pipelined host loop).
 cudaError_t f3d_zero_i32(int32_t* p, int64_t n, cudaStream_t st);
+// Programmatic dependent launch (F3D_PDL, default on): the hot-path kernels
+// are launched with programmatic stream serialisation, so a kernel's CTAs are
+// scheduled (and run their prologue: barriers, TMEM, smem set-up) while the
+// previous kernel's last CTAs finish; each such kernel executes
+// f3d::pdl_wait() before its first global read of anything a predecessor
+// wrote.  (In a kernel launched without the attribute the wait is a no-op.)
+bool f3d_pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t f3d_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = f3d_pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 namespace f3d {
 
 constexpr int kWarp = 32;
+
+// wait for the grids this one programmatically depends on (griddepcontrol)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // hash kinds: hashing.py:19 HASH_KINDS order
 enum HashKind : int { XOR_MOD = 0, XOR_DIV = 1, ZORDER_MOD = 2, ZORDER_DIV = 3 };

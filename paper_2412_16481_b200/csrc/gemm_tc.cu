@@ -97,30 +97,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(f_empty + kMaxWG);
     float* s_bias = reinterpret_cast<float*>(smem + A.off_bias);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t n = dyn_n(A.n, A.n_dev);
-    const int mblocks = (int)((n + kBM - 1) / kBM);
-    const int ntiles = mblocks * A.nt;
     const int nk = (A.K + BK - 1) / BK;        // a partial last k-block is zero-filled by TMA
 
-    for (int i = tid; i < A.N; i += kThreads) s_bias[i] = A.bias ? A.bias[i] : 0.f;
     float* s_gain = reinterpret_cast<float*>(smem + A.off_gb);
     float* s_beta = s_gain + A.N;
     float* s_fq = s_beta + A.N;                // PE frequency of pair j (N/2)
     float* s_pe = s_fq + A.N / 2;              // PE: 1/ext x,y,z
-    if constexpr (LN >= 2) {
-        for (int i = tid; i < A.N; i += kThreads) {
-            s_gain[i] = A.gain[i];
-            s_beta[i] = A.beta[i];
-        }
-        if constexpr (LN == 3) {
-            const int npair = A.N / 6;
-            for (int i = tid; i < A.N / 2; i += kThreads) {
-                const int blk = 2 * npair, c = 2 * i, ax = c / blk, pj = (c - ax * blk) >> 1;
-                s_fq[i] = exp2f(-(float)pj / (float)npair * A.pl2);
-            }
-            if (tid < 3) s_pe[tid] = A.lo_ext ? (float)(1.0 / A.lo_ext[3 + tid]) : 1.f;
-        }
-    }
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
@@ -140,6 +122,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         tmem_alloc(tmem_slot, 512);
         tmem_relinquish();
+    }
+    // everything above is local set-up: with programmatic dependent launch it
+    // overlaps the previous kernel's tail; from here on inputs are read
+    pdl_wait();
+    const int64_t n = dyn_n(A.n, A.n_dev);
+    const int mblocks = (int)((n + kBM - 1) / kBM);
+    const int ntiles = mblocks * A.nt;
+    for (int i = tid; i < A.N; i += kThreads) s_bias[i] = A.bias ? A.bias[i] : 0.f;
+    if constexpr (LN >= 2) {
+        for (int i = tid; i < A.N; i += kThreads) {
+            s_gain[i] = A.gain[i];
+            s_beta[i] = A.beta[i];
+        }
+        if constexpr (LN == 3) {
+            const int npair = A.N / 6;
+            for (int i = tid; i < A.N / 2; i += kThreads) {
+                const int blk = 2 * npair, c = 2 * i, ax = c / blk, pj = (c - ax * blk) >> 1;
+                s_fq[i] = exp2f(-(float)pj / (float)npair * A.pl2);
+            }
+            if (tid < 3) s_pe[tid] = A.lo_ext ? (float)(1.0 / A.lo_ext[3 + tid]) : 1.f;
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -595,8 +598,8 @@ extern "C" int f3d_gemm(const void* x, int64_t ldx, int64_t n, int K, const void
     }
     const int64_t tiles = ((n + gm::kBM - 1) / gm::kBM) * p.nt;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, f3d_num_sms()));
-    kern<<<grid, gm::kThreads, p.smem, st>>>(a, amap, bmap, ymap, ymap);
-    F3D_LAUNCH_CHECK();
+    F3D_CUDA_TRY(f3d_launch(kern, dim3(grid), dim3(gm::kThreads), p.smem, st, a, amap, bmap, ymap,
+                            ymap));
     return F3D_OK;
 }
 
@@ -668,7 +671,7 @@ extern "C" int f3d_gemm_res_ln(const void* x, int64_t ldx, int64_t n, int K, con
     }
     const int64_t tiles = (n + gm::kBM - 1) / gm::kBM;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, f3d_num_sms()));
-    kern<<<grid, gm::kThreads, p.smem, st>>>(a, amap, bmap, ymap, fmap);
-    F3D_LAUNCH_CHECK();
+    F3D_CUDA_TRY(f3d_launch(kern, dim3(grid), dim3(gm::kThreads), p.smem, st, a, amap, bmap, ymap,
+                            fmap));
     return F3D_OK;
 }

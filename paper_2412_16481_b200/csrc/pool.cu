@@ -511,6 +511,7 @@ __global__ void pool_reduce4_kernel(const float* __restrict__ x, int64_t ldx, in
                                     float* __restrict__ out, int64_t ldo,
                                     const __nv_bfloat16* __restrict__ y = nullptr,
                                     int64_t ldy = 0, const float* __restrict__ yb = nullptr) {
+    pdl_wait();
     const int np = (int)dyn_n(npool, npool_dev);
     const uint32_t tot = (uint32_t)np * (uint32_t)d4;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
@@ -663,9 +664,9 @@ extern "C" int f3d_pool_reduce_res(const float* x, int64_t ldx, const void* y_bf
     if (npool == 0) return F3D_OK;
     int64_t g4 = (npool * (d / 4) + 255) / 256;
     if (g4 > (int64_t)f3d_num_sms() * 32) g4 = (int64_t)f3d_num_sms() * 32;
-    pool::pool_reduce4_kernel<<<(unsigned)g4, 256, 0, (cudaStream_t)stream>>>(
-        x, ldx, d / 4, members, sizes, (int)npool, npool_dev, rho, op, out, ldo,
-        (const __nv_bfloat16*)y_bf16, ldy, ybias);
-    F3D_LAUNCH_CHECK();
+    F3D_CUDA_TRY(f3d_launch(pool::pool_reduce4_kernel, dim3((unsigned)g4), dim3(256), 0,
+                            (cudaStream_t)stream, x, ldx, d / 4, members, sizes, (int)npool,
+                            npool_dev, rho, op, out, ldo, (const __nv_bfloat16*)y_bf16, ldy,
+                            ybias));
     return F3D_OK;
 }

@@ -83,7 +83,8 @@ struct Params {
 };
 
 // Grid-wide barrier on a per-call counter in the caller's workspace (zeroed
-// before the launch; the launch is still cooperative, for co-residency):
+// by a small kernel before the launch; the launch is still cooperative, for
+// co-residency):
 // every call's barrier state is its own, whatever else runs concurrently
 // (two Backbones on two streams, tests/test_gpu_backbone.py;
 // tools/psh_concurrency.py).
@@ -910,7 +911,8 @@ int launch_psh(psh::Params& p, bool fused, cudaStream_t st) {
     grid = std::max(grid, std::min(col_ctas, per_sm * f3d_num_sms()));
     grid = std::max(grid, 1);
     if (fused) grid = std::min(grid, kMaxGrid);
-    F3D_CUDA_TRY(cudaMemsetAsync(p.bar, 0, sizeof(unsigned), st));
+    // a kernel, not a memset node (which may queue behind copy-engine traffic)
+    F3D_CUDA_TRY(f3d_zero_i32((int32_t*)p.bar, 1, st));
     void* args[] = {(void*)&p};
     F3D_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(psh::kThreads), args,
                                              smem, st));

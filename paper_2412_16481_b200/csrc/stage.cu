@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, HAS_PE ? 4 : 5) row_ln_vec_kernel(
     const float* __restrict__ beta, const double* __restrict__ pec,
     const double* __restrict__ lo_ext, float pl2, __nv_bfloat16* __restrict__ out, int64_t ldo,
     int64_t n, int d, float eps) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const bool act = lane < (d >> 2);
     const int64_t row0 = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * RPW;
@@ -442,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 4) scatter_ln_pe_kernel(
     const float* __restrict__ gain, const float* __restrict__ beta, float* __restrict__ F,
     int64_t ldf, __nv_bfloat16* __restrict__ out, int64_t ldo, int64_t n,
     const int32_t* __restrict__ n_dev, int d, float eps) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const bool act = lane < (d >> 2);
     const int64_t nn = dyn_n(n, n_dev);
@@ -541,6 +543,7 @@ __global__ void residual_out_kernel(float* __restrict__ F, int64_t ldf,
                                     const __nv_bfloat16* __restrict__ y, int64_t ldy,
                                     const float* __restrict__ yb, __nv_bfloat16* __restrict__ out,
                                     int64_t ldo, int64_t n, int d4) {
+    pdl_wait();
     const int64_t tot = n * d4;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -588,8 +591,8 @@ static bool launch_row_ln_vec(cudaStream_t st, void* F, int64_t ldf, const void*
     BF* ob = (BF*)out;
     const float fe = (float)eps;
 #define F3D_LNV(HY, HO, HP)                                                                       \
-    stage::row_ln_vec_kernel<RPW, HY, HO, HP><<<g, stage::kThreads, 0, st>>>(                     \
-        Ff, ldf, yb, ldy, ybias, gain, beta, pec, lo_ext, pl2, ob, ldo, n, d, fe)
+    f3d_launch(stage::row_ln_vec_kernel<RPW, HY, HO, HP>, dim3(g), dim3(stage::kThreads), 0, st, \
+               Ff, ldf, yb, ldy, ybias, gain, beta, pec, lo_ext, pl2, ob, ldo, n, d, fe)
     if (y && out && pec) F3D_LNV(true, true, true);
     else if (y && out) F3D_LNV(true, true, false);
     else if (y) F3D_LNV(true, false, false);
@@ -736,14 +739,15 @@ extern "C" int f3d_scatter_ln_pe(const void* src, int src_is_f32, int64_t lds,
     const float pl2 = (float)log2(pe_base);
     cudaStream_t st = (cudaStream_t)stream;
     if (src_is_f32)
-        stage::scatter_ln_pe_kernel<RPW, float><<<g, stage::kThreads, 0, st>>>(
-            (const float*)src, lds, dest, coords, lo_ext, pl2, gain, beta, F, ldf,
-            (__nv_bfloat16*)out_bf16, ldo, n, n_dev, d, (float)eps);
+        F3D_CUDA_TRY(f3d_launch(stage::scatter_ln_pe_kernel<RPW, float>, dim3(g),
+                                dim3(stage::kThreads), 0, st, (const float*)src, lds, dest, coords,
+                                lo_ext, pl2, gain, beta, F, ldf, (__nv_bfloat16*)out_bf16, ldo, n,
+                                n_dev, d, (float)eps));
     else
-        stage::scatter_ln_pe_kernel<RPW, __nv_bfloat16><<<g, stage::kThreads, 0, st>>>(
-            (const __nv_bfloat16*)src, lds, dest, coords, lo_ext, pl2, gain, beta, F, ldf,
-            (__nv_bfloat16*)out_bf16, ldo, n, n_dev, d, (float)eps);
-    F3D_LAUNCH_CHECK();
+        F3D_CUDA_TRY(f3d_launch(stage::scatter_ln_pe_kernel<RPW, __nv_bfloat16>, dim3(g),
+                                dim3(stage::kThreads), 0, st, (const __nv_bfloat16*)src, lds, dest,
+                                coords, lo_ext, pl2, gain, beta, F, ldf, (__nv_bfloat16*)out_bf16,
+                                ldo, n, n_dev, d, (float)eps));
     return F3D_OK;
 }
 
@@ -756,8 +760,8 @@ extern "C" int f3d_residual_out(float* F, int64_t ldf, const void* y_bf16, int64
     if (n == 0) return F3D_OK;
     const int64_t tot = n * (d / 4);
     const unsigned g = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)f3d_num_sms() * 16);
-    stage::residual_out_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(
-        F, ldf, (const __nv_bfloat16*)y_bf16, ldy, ybias, (__nv_bfloat16*)out_bf16, ldo, n, d / 4);
-    F3D_LAUNCH_CHECK();
+    F3D_CUDA_TRY(f3d_launch(stage::residual_out_kernel, dim3(g), dim3(256), 0, (cudaStream_t)stream,
+                            F, ldf, (const __nv_bfloat16*)y_bf16, ldy, ybias,
+                            (__nv_bfloat16*)out_bf16, ldo, n, d / 4));
     return F3D_OK;
 }
