@@ -39,6 +39,7 @@ extern "C" int f3d_abi_version(void) { return 1; }
 extern "C" const char* f3d_last_error(void) { return g_last_error; }
 
 __global__ void f3d_zero_i32_kernel(int32_t* p, int64_t n) {
+    f3d::pdl_wait();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         p[i] = 0;
@@ -48,6 +49,5 @@ cudaError_t f3d_zero_i32(int32_t* p, int64_t n, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     int64_t g = (n + 255) / 256;
     if (g > 1024) g = 1024;
-    f3d_zero_i32_kernel<<<(unsigned)g, 256, 0, st>>>(p, n);
-    return cudaGetLastError();
+    return f3d_launch(f3d_zero_i32_kernel, dim3((unsigned)g), dim3(256), 0, st, p, n);
 }

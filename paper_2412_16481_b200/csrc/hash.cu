@@ -93,6 +93,7 @@ __device__ __forceinline__ void batch_min_atomic(const long long (&v)[3], int b,
 }
 
 __global__ void init_stats_kernel(int64_t* stats, int64_t* ws_min, int nmin) {
+    f3d::pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (stats && i < 7) stats[i] = (i < 3) ? LLONG_MAX : LLONG_MIN;
     if (ws_min && i < nmin) ws_min[i] = LLONG_MAX;
@@ -232,6 +233,7 @@ __global__ void fused_min_kernel(const double* __restrict__ coords,
                                  const int32_t* __restrict__ batch, int64_t n,
                                  const int32_t* n_dev, int nbatch, Origin org, double vs,
                                  int64_t* ws_min) {
+    f3d::pdl_wait();
     const int64_t nn = dyn_n(n, n_dev);
     const bool single = !batch || nbatch == 1;
     long long acc[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
@@ -265,6 +267,7 @@ __global__ void fused_hash_kernel(const double* __restrict__ coords,
                                   const int64_t* __restrict__ ws_min, HashArgs ha,
                                   int32_t* __restrict__ home, int32_t* __restrict__ vox32,
                                   int64_t* stats) {
+    f3d::pdl_wait();
     const int64_t nn = dyn_n(n, n_dev);
     long long acc[7] = F3D_STATS_INIT;
     const int64_t step = (int64_t)gridDim.x * blockDim.x;
@@ -352,14 +355,15 @@ extern "C" int f3d_voxel_hash(const double* coords, const int32_t* batch, int64_
     if (n_dev && nbatch > 1) return F3D_ERR_CONFIG;
     cudaStream_t st = (cudaStream_t)stream;
     Origin o{{origin3_host[0], origin3_host[1], origin3_host[2]}};
-    init_stats_kernel<<<nblk(3 * nbatch + 7), kThreads, 0, st>>>(stats_out, ws, 3 * nbatch);
+    F3D_CUDA_TRY(f3d_launch(init_stats_kernel, dim3(nblk(3 * nbatch + 7)), dim3(kThreads), 0, st,
+                            stats_out, ws, 3 * nbatch));
     if (n > 0) {
-        fused_min_kernel<<<nblk_capped(n), kThreads, 0, st>>>(coords, batch, n, n_dev, nbatch, o,
-                                                        voxel_size, ws);
+        F3D_CUDA_TRY(f3d_launch(fused_min_kernel, dim3(nblk_capped(n)), dim3(kThreads), 0, st,
+                                coords, batch, n, n_dev, nbatch, o, voxel_size, ws));
         HashArgs ha{HashParams{kind, K, S_div, bits, 0}, 1};
-        fused_hash_kernel<<<nblk_capped(n), kThreads, 0, st>>>(coords, batch, n, n_dev, nbatch, o,
-                                                         voxel_size, ws, ha, home_out, vox32_out,
-                                                         stats_out);
+        F3D_CUDA_TRY(f3d_launch(fused_hash_kernel, dim3(nblk_capped(n)), dim3(kThreads), 0, st,
+                                coords, batch, n, n_dev, nbatch, o, voxel_size, (const int64_t*)ws,
+                                ha, home_out, vox32_out, stats_out));
     }
     F3D_LAUNCH_CHECK();
     return F3D_OK;

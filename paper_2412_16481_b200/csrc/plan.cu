@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(kThreads) plan_round_kernel(
     int32_t* scope_seg, int32_t* scope_nseg, int32_t* seg_start, int32_t* seg_vstart,
     int32_t* scope_len, int32_t* scope_order, int32_t* work, int max_work, int qstep,
     int32_t* live) {
+    pdl_wait();
     // block t plans round t: rotation off0 + t*off_step, outputs round_stride apart
     const int off = (off0 + (int)blockIdx.x * off_step) % W;
     {
@@ -207,10 +208,10 @@ extern "C" int f3d_plan_rounds(const int32_t* counts, const int32_t* base, int K
     if (K < 1 || S < 1 || nb_cap < 1 || W < 1 || stride < 1 || shift < 0 || nscopes < 1 ||
         max_work < 0 || qstep < 16 || nrounds < 1 || round_stride < 0)
         return F3D_ERR_CONFIG;
-    plan::plan_round_kernel<<<nrounds, plan::kThreads, 0, (cudaStream_t)stream>>>(
-        counts, base, K, S, nb_cap, W, stride, 0, shift % W, round_stride, nscopes, scope_seg,
-        scope_nseg, seg_start, seg_vstart, scope_len, scope_order, work, max_work, qstep, live);
-    F3D_LAUNCH_CHECK();
+    F3D_CUDA_TRY(f3d_launch(plan::plan_round_kernel, dim3(nrounds), dim3(plan::kThreads), 0,
+                            (cudaStream_t)stream, counts, base, K, S, nb_cap, W, stride, 0,
+                            shift % W, round_stride, nscopes, scope_seg, scope_nseg, seg_start,
+                            seg_vstart, scope_len, scope_order, work, max_work, qstep, live));
     return F3D_OK;
 }
 

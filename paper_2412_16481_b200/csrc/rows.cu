@@ -17,6 +17,7 @@ template <typename V, bool kScatter>
 __global__ void move_rows_kernel(const V* __restrict__ src, const int32_t* __restrict__ idx,
                                  int64_t n, const int32_t* n_dev, int64_t vec_per_row,
                                  V* __restrict__ dst) {
+    f3d::pdl_wait();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t tot = dyn_n(n, n_dev) * vec_per_row;
     if (t >= tot) return;
@@ -37,13 +38,15 @@ int move_rows(const void* src, const int32_t* idx, int64_t n, const int32_t* n_d
     if (v16) {
         const int64_t vpr = row_bytes / 16;
         const int64_t tot = n * vpr;
-        move_rows_kernel<int4, kScatter><<<(unsigned)((tot + kThreads - 1) / kThreads), kThreads,
-                                           0, st>>>((const int4*)src, idx, n, n_dev, vpr, (int4*)dst);
+        F3D_CUDA_TRY(f3d_launch(move_rows_kernel<int4, kScatter>,
+                                dim3((unsigned)((tot + kThreads - 1) / kThreads)), dim3(kThreads), 0,
+                                st, (const int4*)src, idx, n, n_dev, vpr, (int4*)dst));
     } else {
         const int64_t vpr = row_bytes / 4;
         const int64_t tot = n * vpr;
-        move_rows_kernel<int, kScatter><<<(unsigned)((tot + kThreads - 1) / kThreads), kThreads, 0,
-                                          st>>>((const int*)src, idx, n, n_dev, vpr, (int*)dst);
+        F3D_CUDA_TRY(f3d_launch(move_rows_kernel<int, kScatter>,
+                                dim3((unsigned)((tot + kThreads - 1) / kThreads)), dim3(kThreads), 0,
+                                st, (const int*)src, idx, n, n_dev, vpr, (int*)dst));
     }
     F3D_LAUNCH_CHECK();
     return F3D_OK;

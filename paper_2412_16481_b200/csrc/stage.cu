@@ -20,6 +20,7 @@ constexpr int kMaxPerLane = 32;   // d <= 1024
 
 __global__ void bbox_partial_kernel(const double* __restrict__ c, int64_t n,
                                     const int32_t* n_dev, double* part) {
+    f3d::pdl_wait();
     n = dyn_n(n, n_dev);
     __shared__ double s[6][kThreads / 32];
     double mn[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, mx[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
@@ -56,6 +57,7 @@ __global__ void bbox_partial_kernel(const double* __restrict__ c, int64_t n,
 // one warp per axis: lanes stride over the partial results (min / max are
 // exact in any order)
 __global__ void bbox_final_kernel(const double* part, int nparts, double* lo_ext) {
+    f3d::pdl_wait();
     const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (a >= 3) return;
     double mn = DBL_MAX, mx = -DBL_MAX;
@@ -277,9 +279,10 @@ extern "C" int f3d_coord_bbox(const double* coords, int64_t n, double* ws, doubl
     if (n < 1) return F3D_ERR_EMPTY;
     cudaStream_t st = (cudaStream_t)stream;
     const int parts = (int)std::min<int64_t>((n + 1023) / 1024, 296);
-    stage::bbox_partial_kernel<<<parts, stage::kThreads, 0, st>>>(coords, n, n_dev, ws);
-    stage::bbox_final_kernel<<<1, 96, 0, st>>>(ws, parts, lo_ext);
-    F3D_LAUNCH_CHECK();
+    F3D_CUDA_TRY(f3d_launch(stage::bbox_partial_kernel, dim3(parts), dim3(stage::kThreads), 0, st,
+                            coords, n, n_dev, ws));
+    F3D_CUDA_TRY(f3d_launch(stage::bbox_final_kernel, dim3(1), dim3(96), 0, st, (const double*)ws,
+                            parts, lo_ext));
     return F3D_OK;
 }
 
