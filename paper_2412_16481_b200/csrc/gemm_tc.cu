@@ -481,12 +481,20 @@ struct Plan {
 };
 
 // ln: 0 plain; 1..3 the residual (+LN, +PE) epilogue (one column tile, N % 32 == 0)
-static bool plan(int K, int N, Plan& p, int ln = 0) {
+static bool plan(int K, int N, Plan& p, int ln = 0, bool gelu = false) {
     if (K < 32 || K % 32 || N < 16 || N % 16 || N > 4096) return false;
     if (ln && (N % 32 || N > 256)) return false;
     // BK = 64 (128-byte rows, SWIZZLE_128B) unless F3D_GEMM_BK32 asks for 32 when K % 64 != 0
     p.BK = (K % 64 == 0 || !getenv("F3D_GEMM_BK32")) ? 64 : 32;
-    int nt = (N + 255) / 256;
+    // Column tile: at most 256 wide; with the GELU epilogue at most 96 wide, so
+    // that three epilogue warpgroups (TMEM accumulators) work on separate tiles
+    // (measured, tools/gemm_bench.py, 100K x 96 -> 384: 44.7 us at 192-wide
+    // tiles with two epilogue groups, 35.3 us at 96; config-B step 1.034 ->
+    // 1.000 ms).  F3D_GEMM_BN_MAX / F3D_GEMM_BN_GELU override (A/B).
+    int bn_max = gelu ? 96 : 256;
+    if (const char* e = getenv(gelu ? "F3D_GEMM_BN_GELU" : "F3D_GEMM_BN_MAX"))
+        bn_max = std::max(16, atoi(e));
+    int nt = (N + bn_max - 1) / bn_max;
     while (nt <= N / 16 && (N % nt || (N / nt) % 16)) ++nt;
     if (nt > N / 16) return false;
     p.nt = nt;
@@ -553,7 +561,7 @@ extern "C" int f3d_gemm(const void* x, int64_t ldx, int64_t n, int K, const void
                         const float* bias, int gelu, void* y, int64_t ldy, const int32_t* n_dev,
                         void* stream) {
     gm::Plan p;
-    if (!gm::plan(K, N, p) || n < 0 || (ldx & 7) || (ldy & 7) || ldx < K || ldy < N ||
+    if (!gm::plan(K, N, p, 0, gelu != 0) || n < 0 || (ldx & 7) || (ldy & 7) || ldx < K || ldy < N ||
         (((uintptr_t)x | (uintptr_t)w_t | (uintptr_t)y) & 15))
         return F3D_ERR_CONFIG;
     if (n == 0) return F3D_OK;
