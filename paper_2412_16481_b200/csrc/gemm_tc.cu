@@ -33,7 +33,10 @@ namespace gm {
 using namespace f3d::tc;
 
 constexpr int kBM = 128;
-constexpr int kMaxWG = 3;          // epilogue warpgroups (one tile each, round robin); 512 threads: 128 registers
+#ifndef F3D_GEMM_MAXWG
+#define F3D_GEMM_MAXWG 3
+#endif
+constexpr int kMaxWG = F3D_GEMM_MAXWG;   // epilogue warpgroups (one tile each, round robin); 3: 512 threads, 128 registers
 constexpr int kThreads = (1 + kMaxWG) * 128;   // warp 0 TMA, warp 1 MMA, warps 4.. epilogue
 constexpr int kMaxStages = 8;
 constexpr int kSmemLimit = 227 * 1024;
@@ -50,6 +53,10 @@ struct Args {
     // shared-memory layout (bytes from the 1024-aligned base)
     int off_stage, stage_bytes, a_bytes, off_st, st_stride, off_bias, off_bar;
     int resident, off_w, w_bytes;   // resident: all of W^T stays in smem (loaded once)
+    // swz: the plain epilogue stages its tile as BN/32 boxes of 32 columns in the
+    // TMA 64-byte swizzle (conflict-free 16-byte shared stores; the dense
+    // 2*BN-byte rows put 16 rows on the same banks at BN = 96)
+    int swz;
     // residual + LayerNorm (+PE) epilogue (LN > 0; N == BN, N % 32 == 0):
     //   F[r] += Y[r] + bias;  y[r] = LN(F[r]) * gain + beta (+ PE(coords[r]))
     float* F;
@@ -429,9 +436,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
                         pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                     }
-                    uint4* dst = reinterpret_cast<uint4*>(strow + 32 * (c0 + c));
-                    dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                    dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    if (A.swz) {
+                        // 16-byte chunks 2cc, 2cc+1: box cc/2, chunks q0, q0+1 of the row
+                        const int cc = c0 + c, q0 = (2 * cc) & 3, sw = (r >> 1) & 3;
+                        unsigned char* brow = stage + (cc >> 1) * (kBM * 64) + r * 64;
+                        *reinterpret_cast<uint4*>(brow + ((q0 ^ sw) << 4)) =
+                            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        *reinterpret_cast<uint4*>(brow + (((q0 + 1) ^ sw) << 4)) =
+                            make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    } else {
+                        uint4* dst = reinterpret_cast<uint4*>(strow + 32 * (c0 + c));
+                        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    }
                 }
             }
             if (full_tile) fence_proxy_async();                // STS visible to the TMA store
@@ -440,7 +457,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (full_tile) {
                 // one bulk tensor store of the whole 128 x BN tile
                 if (tq == 0) {
-                    tma_store_2d(&ymap, saddr(stage), j * BN, (int)r0);
+                    if (A.swz) {
+                        for (int b = 0; b < BN / 32; ++b)
+                            tma_store_2d(&ymap, saddr(stage + b * (kBM * 64)), j * BN + b * 32,
+                                         (int)r0);
+                    } else {
+                        tma_store_2d(&ymap, saddr(stage), j * BN, (int)r0);
+                    }
                     bulk_commit();
                 }
                 continue;
@@ -458,7 +481,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     rr[k] = (int)(((uint32_t)i * inv_cpr) >> 20);  // i / cpr (i < 2^12, cpr <= 32)
                     cc[k] = i - rr[k] * cpr;
                     if (i < total)
-                        val[k] = *reinterpret_cast<const uint4*>(stage + rr[k] * stride + cc[k] * 16);
+                        val[k] = *reinterpret_cast<const uint4*>(
+                            A.swz ? stage + (cc[k] >> 2) * (kBM * 64) + rr[k] * 64 +
+                                        (((cc[k] & 3) ^ ((rr[k] >> 1) & 3)) << 4)
+                                  : stage + rr[k] * stride + cc[k] * 16);
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
@@ -507,6 +533,7 @@ static bool plan(int K, int N, Plan& p, int ln = 0, bool gelu = false) {
     a.a_bytes = kBM * p.BK * 2;
     // dense rows: the TMA store box layout (the LN epilogue stages y only with LN)
     a.st_stride = (ln == 1) ? 0 : 2 * p.BN;
+    a.swz = (ln == 0 && p.BN % 32 == 0 && !getenv("F3D_GEMM_DENSE_STAGE")) ? 1 : 0;
     const int ftile = ln ? kBM * N * 4 : 0;        // per epilogue WG: the fp32 residual tile
     const int bias_bytes = (N * 4 + 15) & ~15;
     const int gb_bytes = ln ? ((2 * N + N / 2 + 4) * 4 + 15) & ~15 : 0;
@@ -573,7 +600,8 @@ extern "C" int f3d_gemm(const void* x, int64_t ldx, int64_t n, int K, const void
     const int sw = p.BK * 2;
     if (!tc::make_map(&amap, x, ldx, K, n, p.BK, sw, gm::kBM) ||
         !tc::make_map(&bmap, w_t, K, K, N, p.BK, sw, p.BN) ||
-        !tc::make_map(&ymap, y, ldy, N, n, p.BN, 0, gm::kBM)) {
+        !(p.a.swz ? tc::make_map(&ymap, y, ldy, N, n, 32, 64, gm::kBM)
+                  : tc::make_map(&ymap, y, ldy, N, n, p.BN, 0, gm::kBM))) {
         f3d_set_last_cuda_error(cudaErrorNotSupported);
         return F3D_ERR_CUDA;
     }
