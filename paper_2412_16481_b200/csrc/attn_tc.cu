@@ -79,7 +79,9 @@ constexpr int kLoadThreads = kLoadWarps * 32;
 // measured (tools/ubench/mma_ts.cu) one thread issues at most one M128 N<=64
 // tcgen05.mma per ~45 clk, two threads reach the tensor pipe's own rate --
 // one issuer for all Q tiles was the co-bottleneck at small head dims.
-constexpr int kMmaWarp = 3;       // last warp of warpgroup 0 (softmax warps follow)
+// warps before the softmax warpgroups: the loader and the NQ issuers, at least
+// one whole warpgroup (the softmax warps' TMEM lane quarter is warp % 4)
+__host__ __device__ constexpr int pre_warps(int nq) { return nq + 1 > 4 ? nq + 1 : 4; }
 // Softmax column split: CS warps share each 32-row lane quarter of a Q tile
 // and take kBN/CS key columns each (row max / sum exchanged through shared
 // memory) -- more warps per SM sub-partition to hide the per-tile latencies
@@ -99,7 +101,7 @@ template <int DH>
 __host__ __device__ constexpr int ctas_per_sm() { return DH <= 32 ? F3D_CTAS_SMALL : 1; }
 template <int DH>
 __host__ __device__ constexpr int threads_for() {
-    return (4 + 4 * nq_for_dh(DH) * cs_for<DH>()) * 32;
+    return (pre_warps(nq_for_dh(DH)) + 4 * nq_for_dh(DH) * cs_for<DH>()) * 32;
 }
 constexpr float kRescale = 8.f;   // move the running max only when it grows by > 2^8
 constexpr int kMaps = 6;          // TMA maps: {q, k, v} x {first block, second block}
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                 }
             }
         }
-    } else if (warp <= kMmaWarp) {
+    } else if (warp < pre_warps(NQ)) {
         // ------------------------------------------------ MMA issuers
         // Warp 1 + g issues every MMA of Q tile g (warp-uniform control flow
         // and waits; one elected lane issues every tcgen05.mma / commit).
@@ -613,7 +615,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
         }
     } else {
         // ------------------------------------------------ softmax warpgroups
-        const int sw = warp - (kMmaWarp + 1);             // 0 .. 4*NQ*CS-1
+        const int sw = warp - pre_warps(NQ);               // 0 .. 4*NQ*CS-1
         const int wgi = sw >> 2;
         const int g = wgi / CS;                           // Q tile of this warpgroup
         const int hh = wgi - g * CS;                      // column share of this warp
@@ -857,7 +859,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
     }
 #if F3D_EXPERIMENT == 3
     if (lane == 0) {
-        const int role = warp < kLoadWarps ? 11 : (warp == kMmaWarp ? 8 : 0);
+        const int role = warp < kLoadWarps ? 11 : (warp < pre_warps(NQ) ? 8 : 0);
         prof[role] += clock64() - t_start;
         for (int i = 0; i < 24; ++i)
             if (prof[i]) atomicAdd(&g_attn_prof[i], prof[i]);
