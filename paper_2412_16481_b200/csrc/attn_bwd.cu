@@ -28,6 +28,10 @@ namespace attn_bwd {
 constexpr int kBR = 64;            // rows per block (keys or queries)
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
+#ifndef F3D_BWD_MINB
+#define F3D_BWD_MINB 4     // resident CTAs per SM (register cap 128): 25.7 vs 29.5 ms per
+                           // 4-scene training step at 1 (5: 26.2, spills)
+#endif
 
 struct Args {
     const __nv_bfloat16 *q, *k, *v, *dout;   // (rows, H*dh) head h at column h*dh
@@ -150,7 +154,7 @@ __device__ __forceinline__ bool decode(const Args& A, Scope& sc, int& blk) {
 
 // ------------------------------------------------------------------ dK, dV
 template <int DH>
-__global__ void __launch_bounds__(kThreads) attn_bwd_kv_kernel(const Args A) {
+__global__ void __launch_bounds__(kThreads, F3D_BWD_MINB) attn_bwd_kv_kernel(const Args A) {
     constexpr int kStride = DH * 2 + 16;
     constexpr int kTile = kBR * kStride;
     constexpr int KS = DH / 16, NT = DH / 8;
@@ -278,7 +282,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kv_kernel(const Args A) {
 // gradients amplify by cancellation) and writes it for the key kernel; pass 1
 // accumulates dQ.
 template <int DH>
-__global__ void __launch_bounds__(kThreads) attn_bwd_q_kernel(const Args A) {
+__global__ void __launch_bounds__(kThreads, F3D_BWD_MINB) attn_bwd_q_kernel(const Args A) {
     constexpr int kStride = DH * 2 + 16;
     constexpr int kTile = kBR * kStride;
     constexpr int KS = DH / 16, NT = DH / 8;
