@@ -95,8 +95,8 @@ struct GridBar {
         __syncthreads();
         if (threadIdx.x == 0) {
             target += gridDim.x;                 // monotonic: barrier k ends at k * grid
-            unsigned old, cur;
-            asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+            unsigned cur;
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
             do {
                 asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
             } while (cur < target);
@@ -228,7 +228,10 @@ __device__ int column_scan(int32_t* hist, int stride, int col, int t0, int t1) {
 __device__ __forceinline__ int decide(const int4 q, int p, const int32_t* __restrict__ T,
                                       const Params& P_, const int8_t* probe) {
     if (__ldcg(T + q.w) >= p) return q.w;
-    constexpr int kChunk = 8;
+#ifndef F3D_PSH_CHUNK
+#define F3D_PSH_CHUNK 2   // measured (config D, 1M points): 2 -> 98 us, 4 -> 118, 8 -> 115
+#endif
+    constexpr int kChunk = F3D_PSH_CHUNK;   // candidates hashed (and their T loaded) per step
     for (int p0 = 0; p0 < P_.P; p0 += kChunk) {
         int cand[kChunk];
 #pragma unroll
