@@ -82,13 +82,42 @@ __host__ __device__ __forceinline__ uint32_t spread3_10(uint32_t a) {
     return a;
 }
 
+// Division by a run-time constant d in [1, 2^31) for dividends n < 2^31:
+// q = umulhi(n, m) >> s with m = ceil(2^(31+L) / d), s = L - 1, L = ceil(log2 d)
+// (the round-up method; exact for every n < 2^31), d = 1 handled as m = 0.
+struct FastDiv {
+    uint32_t d, m, s;
+    __host__ __device__ static FastDiv make(uint32_t d) {
+        FastDiv f{d, 0u, 0u};
+        if (d > 1) {
+            uint32_t L = 0;
+            while ((1ull << L) < d) ++L;
+            f.m = (uint32_t)(((1ull << (31 + L)) + d - 1) / d);
+            f.s = L - 1;
+        }
+        return f;
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return m ? (__umulhi(n, m) >> s) : n;
+    }
+    __device__ __forceinline__ uint32_t mod(uint32_t n) const { return n - div(n) * d; }
+};
+
 struct HashParams {
     int kind;
     int K;
     int64_t S_div;
     int bits;
     int strict;
+    FastDiv fdiv, fk;   // S_div and K (set by hash_params)
 };
+
+__host__ __device__ inline HashParams hash_params(int kind, int K, int64_t S_div, int bits,
+                                                  int strict) {
+    HashParams hp{kind, K, S_div, bits, strict, FastDiv::make(1u), FastDiv::make((uint32_t)K)};
+    if (S_div < 0x7FFFFFFFll) hp.fdiv = FastDiv::make((uint32_t)S_div);
+    return hp;
+}
 
 // _kernels.py:27-38: bucket id, or -1 when strict div rejects the quotient.
 __device__ __forceinline__ int hash_bucket1(int x, int y, int z, const HashParams& hp) {
@@ -102,13 +131,13 @@ __device__ __forceinline__ int hash_bucket1(int x, int y, int z, const HashParam
     }
     if (hp.kind == XOR_DIV || hp.kind == ZORDER_DIV) {
         if (key < 0x7FFFFFFFll && hp.S_div < 0x7FFFFFFFll) {
-            key = (int64_t)((uint32_t)key / (uint32_t)hp.S_div);
+            key = (int64_t)hp.fdiv.div((uint32_t)key);
         } else {
             key = key / hp.S_div;
         }
         if (hp.strict && key >= hp.K) return -1;
     }
-    if (key < 0x7FFFFFFFll) return (int)((uint32_t)key % (uint32_t)hp.K);
+    if (key < 0x7FFFFFFFll) return (int)hp.fk.mod((uint32_t)key);
     return (int)(key % hp.K);
 }
 

@@ -169,10 +169,12 @@ __device__ __forceinline__ void hash_one(long long x, long long y, long long z, 
         if (ha.hp.kind <= XOR_DIV) key = x ^ y ^ z;
         else key = morton3(x, y, z);
         if (ha.hp.kind == XOR_DIV || ha.hp.kind == ZORDER_DIV) {
-            key = key / ha.hp.S_div;
+            key = (key < 0x7FFFFFFFll && ha.hp.S_div < 0x7FFFFFFFll)
+                      ? (int64_t)ha.hp.fdiv.div((uint32_t)key)
+                      : key / ha.hp.S_div;
             acc[6] = max(acc[6], (long long)key);
         }
-        h = (int)(key % ha.hp.K);
+        h = key < 0x7FFFFFFFll ? (int)ha.hp.fk.mod((uint32_t)key) : (int)(key % ha.hp.K);
     }
     home[i] = h;
     if (vox32) {
@@ -328,7 +330,7 @@ extern "C" int f3d_hash_bucket(const int64_t* vox, int64_t n, int kind, int32_t 
     cudaStream_t st = (cudaStream_t)stream;
     init_stats_kernel<<<1, 32, 0, st>>>(stats_out, nullptr, 0);
     if (n > 0) {
-        HashArgs ha{HashParams{kind, K, S_div, bits, 0}, 1};
+        HashArgs ha{hash_params(kind, K, S_div, bits, 0), 1};
         hash_kernel<<<nblk_capped(n), kThreads, 0, st>>>(vox, n, ha, home_out, vox32_out, stats_out);
     }
     F3D_LAUNCH_CHECK();
@@ -360,7 +362,7 @@ extern "C" int f3d_voxel_hash(const double* coords, const int32_t* batch, int64_
     if (n > 0) {
         F3D_CUDA_TRY(f3d_launch(fused_min_kernel, dim3(nblk_capped(n)), dim3(kThreads), 0, st,
                                 coords, batch, n, n_dev, nbatch, o, voxel_size, ws));
-        HashArgs ha{HashParams{kind, K, S_div, bits, 0}, 1};
+        HashArgs ha{hash_params(kind, K, S_div, bits, 0), 1};
         F3D_CUDA_TRY(f3d_launch(fused_hash_kernel, dim3(nblk_capped(n)), dim3(kThreads), 0, st,
                                 coords, batch, n, n_dev, nbatch, o, voxel_size, (const int64_t*)ws,
                                 ha, home_out, vox32_out, stats_out));

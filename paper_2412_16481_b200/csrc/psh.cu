@@ -587,10 +587,14 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
                                 int64_t key = P_.hp.kind <= XOR_DIV ? (c3[0] ^ c3[1] ^ c3[2])
                                                                     : morton3(c3[0], c3[1], c3[2]);
                                 if (P_.hp.kind == XOR_DIV || P_.hp.kind == ZORDER_DIV) {
-                                    key = key / P_.hp.S_div;
+                                    key = (key < 0x7FFFFFFFll && P_.hp.S_div < 0x7FFFFFFFll)
+                                              ? (int64_t)P_.hp.fdiv.div((uint32_t)key)
+                                              : key / P_.hp.S_div;
                                     qmax = max(qmax, (long long)key);
                                 }
-                                q = make_int4((int)c3[0], (int)c3[1], (int)c3[2], (int)(key % P_.K));
+                                const int hk = key < 0x7FFFFFFFll ? (int)P_.hp.fk.mod((uint32_t)key)
+                                                                  : (int)(key % P_.K);
+                                q = make_int4((int)c3[0], (int)c3[1], (int)c3[2], hk);
                             }
                             P_.pk[p] = q;
                         } else if (multi) {
@@ -953,7 +957,7 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
     p.S = S;
     p.P = P;
     p.max_sweeps = max_sweeps;
-    p.hp = HashParams{kind, K, S_div, bits, strict};
+    p.hp = hash_params(kind, K, S_div, bits, strict);
     p.vmax = (1 << bits) - 1;
     for (int i = 0; i < 3 * P; ++i) p.probe[i] = probe_offsets_host[i];
     p.bucket_id = bucket_id;
@@ -1044,7 +1048,7 @@ extern "C" int f3d_psh_assign_coords(const double* coords, int64_t n,
     p.S = S;
     p.P = P;
     p.max_sweeps = max_sweeps;
-    p.hp = HashParams{kind, K, S_div, bits, strict};
+    p.hp = hash_params(kind, K, S_div, bits, strict);
     p.vmax = (1 << bits) - 1;
     for (int i = 0; i < 3 * P; ++i) p.probe[i] = probe_offsets_host[i];
     p.bucket_id = bucket_id;
