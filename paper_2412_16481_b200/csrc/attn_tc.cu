@@ -312,7 +312,10 @@ __device__ __forceinline__ void tma_rows(const Maps& M, int mp, const Args& A, i
     }
 }
 
-template <int DH, typename OutT>
+// ONES: dh < DH, the row sums come from the ones column of V (a compile-time
+// flag: with a runtime one the compiler kept the per-score sum adds in the exp
+// loop and selected the result afterwards -- 2 dead FADDs per pair).
+template <int DH, typename OutT, bool ONES>
 __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
     bswin_attn_tc_kernel(const Args A, const __grid_constant__ Maps M) {
     using C = Cfg<DH>;
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
         if (lane == 0) mbar_arrive(item_empty + slot);
         return r;
     };
-    const bool ones = A.dh < DH;                 // V column dh = 1 -> O column dh = row sum
+    constexpr bool ones = ONES;                  // V column dh = 1 -> O column dh = row sum
 #if F3D_EXPERIMENT == 3
     unsigned long long prof[24] = {0};
     const long long t_start = clock64();
@@ -672,6 +675,9 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                     PROF_MARK(tl1);
                     PROF_ADD(16, tl0, tl1);
                 }
+#if F3D_EXPERIMENT == 3
+                if (lane == 0) ++prof[12];
+#endif
                 PROF_MARK(tm0);
                 const int kvalid = it.m - j * kBN - hh * KC;     // my keys < kvalid are real
                 if (kvalid < KC) {
@@ -723,6 +729,9 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                             }
                             tmem_st16(ocols + c, y);
                         }
+#if F3D_EXPERIMENT == 3
+                        if (lane == 0) ++prof[13];
+#endif
                     }
                 }
                 // P = exp2(s*sl2 - ms) (<= 2^8) -> bf16 pairs over the S columns
@@ -882,11 +891,11 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
 
 // ------------------------------------------------------------- host side
 
-template <int DH, typename OutT>
+template <int DH, typename OutT, bool ONES>
 int launch(Args A, int64_t n_rows, cudaStream_t st) {
     using C = Cfg<DH>;
     using LY = Lay<DH>;
-    auto kern = bswin_attn_tc_kernel<DH, OutT>;
+    auto kern = bswin_attn_tc_kernel<DH, OutT, ONES>;
     static bool attr = false;
     if (!attr) {
         F3D_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -917,7 +926,11 @@ int launch(Args A, int64_t n_rows, cudaStream_t st) {
 
 template <int DH>
 int launch_dh(const Args& A, int64_t n_rows, cudaStream_t st) {
-    return A.out_f32 ? launch<DH, float>(A, n_rows, st) : launch<DH, __nv_bfloat16>(A, n_rows, st);
+    if (A.dh < DH)
+        return A.out_f32 ? launch<DH, float, true>(A, n_rows, st)
+                         : launch<DH, __nv_bfloat16, true>(A, n_rows, st);
+    return A.out_f32 ? launch<DH, float, false>(A, n_rows, st)
+                     : launch<DH, __nv_bfloat16, false>(A, n_rows, st);
 }
 
 }  // namespace attn_tc
