@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--heads", type=int, default=4)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--round", type=int, default=1)
+    ap.add_argument("--stats", action="store_true")
     a = ap.parse_args()
     spec = CONFIGS[a.config]
     cfg = spec["cfg"]
@@ -73,6 +74,17 @@ def main():
            "gflop": flops / 1e9, "ms_median": med, "ms_min": ms[0],
            "tflops_median": flops / (med * 1e-3) / 1e12, "tflops_best": flops / (ms[0] * 1e-3) / 1e12,
            "mean_scope_rows": float(lens[lens > 0].mean().item())}
+    if a.stats:   # Q tiles per scope / items by live Q tiles (NQ = qstep // 128)
+        qs = qstep_for(dh)
+        L_ = plan.scope_len[plan.scope_len > 0].cpu().long()
+        tiles = (L_ + 127) // 128
+        res["tiles_hist"] = {int(t): int((tiles == t).sum()) for t in tiles.unique()}
+        nq = qs // 128
+        last = tiles - (tiles - 1) // nq * nq
+        res["items"] = int(((tiles + nq - 1) // nq).sum())
+        res["last_item_nq_hist"] = {int(t): int((last == t).sum()) for t in last.unique()}
+        res["len_pctl"] = [int(x) for x in torch.quantile(L_.double(), torch.tensor(
+            [0.0, 0.1, 0.5, 0.9, 1.0], dtype=torch.float64)).tolist()]
     print(json.dumps(res), flush=True)
 
 
