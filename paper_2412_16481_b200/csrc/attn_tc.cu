@@ -40,6 +40,12 @@
 #ifndef F3D_EXPERIMENT
 #define F3D_EXPERIMENT 0   // developer A/B knob (tools/): 1 no loads, 2 no exp,
 #endif                     // 3 per-role wait-cycle counters (f3d_attn_prof)
+#if F3D_EXPERIMENT == 4
+// per softmax warp of CTA 0: clock at S ready, exp start, exp end of its first 96 tiles
+__device__ long long g_attn_trace[16][96][3];
+// per softmax warp of CTA 0 and item: next_item returned, final pv wait start, epilogue start, end
+__device__ long long g_attn_trace2[16][16][4];
+#endif
 #if F3D_EXPERIMENT == 3
 __device__ unsigned long long g_attn_prof[24];
 #define PROF_MARK(var) const long long var = clock64()
@@ -177,6 +183,14 @@ struct Lay {
 // launch on the plan.  Measured without it (static item += gridDim.x): the
 // softmax warps of the busiest CTAs ran 15 % longer than the average.
 constexpr int kItemRing = 4;
+// Item records in shared memory, written by warp 0 when it takes an item:
+// the decoded item and its segment table, so the MMA / softmax warps never
+// chase the work list / scope / segment arrays through global memory (two to
+// four dependent L2 round trips at every item start and in the epilogue's
+// row mapping).  A slot is held until its consumers finished the item.
+constexpr int kMaxSeg = 8;                    // scopes with more segments map rows from global
+constexpr int kRecInts = 32;                  // 9 fields + 2 * kMaxSeg, padded
+enum { R_ITEM = 0, R_SCOPE, R_Q0, R_H, R_M, R_S0, R_S1, R_NT, R_NQ, R_VST, R_ST = R_VST + kMaxSeg };
 
 template <int DH>
 __host__ __device__ constexpr int nsb_for() {
@@ -213,7 +227,8 @@ struct Cfg {
     static constexpr int kKVBytes = kBN * DH * 2;       // one of K or V
     static constexpr int CS = cs_for<DH>();
     static constexpr int kXchg = CS > 1 ? NQ * 4 * 3 * CS * 32 * 4 : 0;   // pair exchange
-    static constexpr int kBudget = 227 * 1024 / ctas_per_sm<DH>() - 1024 - 512 - kXchg;
+    static constexpr int kRecBytes = kItemRing * kRecInts * 4;
+    static constexpr int kBudget = 227 * 1024 / ctas_per_sm<DH>() - 1024 - 512 - kXchg - kRecBytes;
     // K/V depth first (>= 4 stages), then a second Q buffer if it still fits
     static constexpr int NQB = (2 * NQ * kQBytes + 4 * 2 * kKVBytes <= kBudget) ? 2 : 1;
     static constexpr int kNstFit = (kBudget - NQB * NQ * kQBytes) / (2 * kKVBytes);
@@ -225,7 +240,8 @@ struct Cfg {
     // after the barriers: TMEM address word, kItemRing item slots
     // pair exchange: [NQ][4 quarters][2 parities][CS][32] row maxima, + row sums
     static constexpr int kOffX = kOffBar + kNumBars * 8 + 4 + 4 * kItemRing + 12;
-    static constexpr int kSmem = kOffX + kXchg + 1024;   // + 1 KB alignment slack
+    static constexpr int kOffRec = kOffX + kXchg;
+    static constexpr int kSmem = kOffRec + kRecBytes + 1024;   // + 1 KB alignment slack
     static constexpr int kTmemS = 0;                    // S/P of tile g, buffer b: (NSB*g+b)*kBN
     static constexpr int kTmemO = NSB * NQ * kBN;       // O of tile g: kTmemO + g*DH
     static constexpr int kTmemNeed = NQ * (NSB * kBN + DH);
@@ -261,6 +277,29 @@ __device__ __forceinline__ Item decode(const Args& A, int item) {
     it.nt = (it.m + kBN - 1) / kBN;
     it.nq = min(NQ, (it.m - it.q0 + kBM - 1) / kBM);
     return it;
+}
+
+__device__ __forceinline__ Item rec_item(const volatile int* R) {
+    Item it;
+    it.scope = R[R_SCOPE];
+    it.q0 = R[R_Q0];
+    it.h = R[R_H];
+    it.m = R[R_M];
+    it.s0 = R[R_S0];
+    it.s1 = R[R_S1];
+    it.nt = R[R_NT];
+    it.nq = R[R_NQ];
+    return it;
+}
+
+// phys_row from the item record's segment table
+__device__ __forceinline__ int phys_row_rec(const Args& A, const volatile int* R, const Item& it, int vr) {
+    const int nseg = it.s1 - it.s0;
+    if (nseg > kMaxSeg) return phys_row(A, it.s0, it.s1, vr);
+    int k = 0;
+    for (int i = 1; i < nseg; ++i)
+        if (R[R_VST + i] <= vr) k = i;
+    return R[R_ST + k] + (vr - R[R_VST + k]);
 }
 
 // First physical row of [v0, v0 + R) if those virtual rows lie inside one
@@ -349,7 +388,6 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
     uint64_t* item_full = o_free + NQ;           // [kItemRing] warp 0 -> consumers
     uint64_t* item_empty = item_full + kItemRing;   // [kItemRing] consumers -> warp 0
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
-    volatile int* s_item = reinterpret_cast<volatile int*>(tmem_slot + 1);   // [kItemRing]
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -359,34 +397,60 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
     int32_t* sched = dyn ? const_cast<int32_t*>(A.live) + 4 : nullptr;   // [next item, CTAs done]
     // consumers of each item: the NQ MMA issuers and every softmax warp
     constexpr int kConsumers = NQ + 4 * NQ * CS;
-    // the CTA's item sequence: static round robin, or the ring filled by warp 0
+    // the CTA's item sequence (static round robin, or the global counter) is
+    // taken by warp 0 and handed to the MMA / softmax warps through a ring of
+    // shared-memory item records
     uint32_t item_k = 0;
     int item_static = blockIdx.x;
-    auto next_item = [&]() -> int {
-        if (!dyn) {
-            const int r = item_static;
-            item_static += gridDim.x;
-            return r < total ? r : -1;
-        }
+    int* recs = reinterpret_cast<int*>(smem + C::kOffRec);
+    // next record slot (-1: no more items); a consumer releases its slot with
+    // release_slot once done with the item
+    auto next_slot = [&]() -> int {
         const int slot = item_k % kItemRing;
         const uint32_t ph = (item_k / kItemRing) & 1;
         ++item_k;
+        volatile int* R = recs + slot * kRecInts;
         if (warp == 0) {                       // producer
             if (item_k > kItemRing) mbar_wait(item_empty + slot, ph ^ 1);
             int r = 0;
             if (lane == 0) {
-                r = atomicAdd(sched, 1);
+                if (dyn) {
+                    r = atomicAdd(sched, 1);
+                } else {
+                    r = item_static;
+                    item_static += gridDim.x;
+                }
                 if (r >= total) r = -1;
-                s_item[slot] = r;
+                R[R_ITEM] = r;
+                if (r >= 0) {
+                    const Item it = decode<NQ, kBN>(A, r);
+                    R[R_SCOPE] = it.scope;
+                    R[R_Q0] = it.q0;
+                    R[R_H] = it.h;
+                    R[R_M] = it.m;
+                    R[R_S0] = it.s0;
+                    R[R_S1] = it.s1;
+                    R[R_NT] = it.nt;
+                    R[R_NQ] = it.nq;
+                    const int nseg = min(it.s1 - it.s0, kMaxSeg);
+                    for (int i = 0; i < nseg; ++i) {
+                        R[R_VST + i] = __ldg(A.seg_vstart + it.s0 + i);
+                        R[R_ST + i] = __ldg(A.seg_start + it.s0 + i);
+                    }
+                }
                 mbar_arrive(item_full + slot);
             }
-            return __shfl_sync(0xffffffffu, r, 0);
+            r = __shfl_sync(0xffffffffu, r, 0);
+            return r < 0 ? -1 : slot;
         }
         mbar_wait(item_full + slot, ph);
-        const int r = s_item[slot];
+        const int r = R[R_ITEM];
+        __syncwarp();
+        return r < 0 ? -1 : slot;
+    };
+    auto release_slot = [&](int slot) {
         __syncwarp();
         if (lane == 0) mbar_arrive(item_empty + slot);
-        return r;
     };
     constexpr bool ones = ONES;                  // V column dh = 1 -> O column dh = row sum
 #if F3D_EXPERIMENT == 3
@@ -452,8 +516,8 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
     if (warp < kLoadWarps) {
         // ------------------------------------------------ loader warps
         uint32_t q_use = 0, kv_it = 0;
-        for (int item = next_item(); item >= 0; item = next_item()) {
-            const Item it = decode<NQ, kBN>(A, item);
+        for (int slot = next_slot(); slot >= 0; slot = next_slot()) {
+            const Item it = rec_item(recs + slot * kRecInts);
             const int qb = q_use % NQB;
             PROF_WAIT(10, mbar_wait(q_empty + qb, ((q_use / NQB) & 1) ^ 1));
             const uint32_t qdst = sm_base + C::kOffQ + qb * NQ * C::kQBytes;
@@ -532,8 +596,8 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
         uint32_t q_use = 0, kv_it = 0;
         uint32_t tg = 0, ig = 0;             // tiles / items of Q tile g processed so far
         if (g < NQ) {
-        for (int item = next_item(); item >= 0; item = next_item()) {
-            const Item it = decode<NQ, kBN>(A, item);
+        for (int slot = next_slot(); slot >= 0; release_slot(slot), slot = next_slot()) {
+            const Item it = rec_item(recs + slot * kRecInts);
             const int qb = q_use % NQB;
             PROF_WAIT(4, mbar_wait(q_full + qb, (q_use / NQB) & 1));
             tc_fence_after();
@@ -640,9 +704,16 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
             return fmaxf(v, xg[(slot * CS + (hh ^ 1)) * 32 + lane]);
         };
         uint32_t tg = 0;
-        for (int item = next_item(); item >= 0; item = next_item()) {
+#if F3D_EXPERIMENT == 4
+        int titem = 0;
+#endif
+        for (int slot = next_slot(); slot >= 0; release_slot(slot), slot = next_slot()) {
             PROF_MARK(td0);
-            const Item it = decode<NQ, kBN>(A, item);
+#if F3D_EXPERIMENT == 4
+            if (blockIdx.x == 0 && lane == 0 && titem < 16) g_attn_trace2[warp][titem][0] = clock64();
+#endif
+            const volatile int* rec = recs + slot * kRecInts;
+            const Item it = rec_item(rec);
             if (g >= it.nq) continue;                     // this Q tile is past the scope
             PROF_MARK(td1);
             PROF_ADD(20, td0, td1);
@@ -656,6 +727,9 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                 const int b = t % NSB;
                 const uint32_t sb = tmem + lane_base + C::kTmemS + (NSB * g + b) * kBN;
                 PROF_WAIT(1, mbar_wait(s_full + NSB * g + b, (t / NSB) & 1));
+#if F3D_EXPERIMENT == 4
+                if (blockIdx.x == 0 && lane == 0 && t < 96) g_attn_trace[warp][t][0] = clock64();
+#endif
                 tc_fence_after();
                 if (dead) {
                     tc_fence_before();
@@ -738,6 +812,9 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                 const float nms = -ms;
                 const uint64_t sl2x2 = f2(sl2, sl2), nms2 = f2(nms, nms);
                 PROF_MARK(te0);
+#if F3D_EXPERIMENT == 4
+                if (blockIdx.x == 0 && lane == 0 && t < 96) g_attn_trace[warp][t][1] = clock64();
+#endif
                 float sum = 0.f;
 #pragma unroll
                 for (int e = 0; e < KC; e += 2) {
@@ -767,6 +844,9 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                 }
                 l += sum;
                 PROF_MARK(te1);
+#if F3D_EXPERIMENT == 4
+                if (blockIdx.x == 0 && lane == 0 && t < 96) g_attn_trace[warp][t][2] = clock64();
+#endif
                 PROF_ADD(18, te0, te1);
                 if (KC == 64)
                     tmem_st32(sb, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
@@ -784,7 +864,13 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
             // O_g complete: normalise and write the row
             {
                 const uint32_t tl = tg + it.nt - 1;
+#if F3D_EXPERIMENT == 4
+                if (blockIdx.x == 0 && lane == 0 && titem < 16) g_attn_trace2[warp][titem][1] = clock64();
+#endif
                 PROF_WAIT(3, mbar_wait(pv_done + NSB * g + tl % NSB, (tl / NSB) & 1));
+#if F3D_EXPERIMENT == 4
+                if (blockIdx.x == 0 && lane == 0 && titem < 16) g_attn_trace2[warp][titem][2] = clock64();
+#endif
             }
             PROF_MARK(tq0);
             tc_fence_after();
@@ -795,7 +881,17 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                 continue;
             }
             float lsum = l;
-            if (ones) {
+            // one TMEM round trip for a 32-column O row (sum column included)
+            constexpr bool kO32 = OC == 32 && CS == 1;
+            uint32_t yo[kO32 ? 32 : 1];
+            if (kO32) {
+                tmem_ld32(ocols, *reinterpret_cast<uint32_t(*)[32]>(&yo[0]));
+                tmem_wait_ld();
+                if (ones)   // dh is a multiple of 8 below 32 (selects: no indexed local copy)
+                    lsum = __uint_as_float(A.dh == 8 ? yo[8 % (kO32 ? 32 : 1)]
+                                           : A.dh == 16 ? yo[16 % (kO32 ? 32 : 1)]
+                                                        : yo[24 % (kO32 ? 32 : 1)]);
+            } else if (ones) {
                 uint32_t y[16];
                 tmem_ld16(obase + (A.dh & ~15), y);
                 tmem_wait_ld();
@@ -808,7 +904,7 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
             const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
             const int vr = it.q0 + g * kBM + r;
             const bool live_row = vr < it.m;
-            const int pr = live_row ? phys_row(A, it.s0, it.s1, vr) : 0;
+            const int pr = live_row ? phys_row_rec(A, rec, it, vr) : 0;
             // P = exp2(s * scale_log2 - lse) recomputes this row's softmax
             if (A.lse && live_row && hh == 0)
                 A.lse[(int64_t)pr * A.ld_lse + it.h] = lsum > 0.f ? ms + __log2f(lsum) : -INFINITY;
@@ -816,8 +912,13 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
 #pragma unroll
             for (int c = 0; c < OC / 16; ++c) {
                 uint32_t y[16];
-                tmem_ld16(ocols + c * 16, y);
-                tmem_wait_ld();
+                if (kO32) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) y[e] = yo[(c * 16 + e) % (kO32 ? 32 : 1)];
+                } else {
+                    tmem_ld16(ocols + c * 16, y);
+                    tmem_wait_ld();
+                }
                 if (!live_row) continue;
                 if (sizeof(OutT) == 2) {
                     __nv_bfloat16* out =
@@ -861,6 +962,10 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
             mbar_arrive(o_free + g);
             tg += it.nt;
             PROF_MARK(tq1);
+#if F3D_EXPERIMENT == 4
+            if (blockIdx.x == 0 && lane == 0 && titem < 16) g_attn_trace2[warp][titem][3] = clock64();
+            ++titem;
+#endif
             PROF_ADD(21, tq0, tq1);
         }
         PROF_MARK(tend);
@@ -938,6 +1043,12 @@ int launch_dh(const Args& A, int64_t n_rows, cudaStream_t st) {
 
 using namespace f3d;
 
+#if F3D_EXPERIMENT == 4
+extern "C" int f3d_attn_trace(long long* out_host) {
+    int e = (int)cudaMemcpyFromSymbol(out_host, g_attn_trace, sizeof(g_attn_trace));
+    return e ? e : (int)cudaMemcpyFromSymbol(out_host + 16 * 96 * 3, g_attn_trace2, sizeof(g_attn_trace2));
+}
+#endif
 #if F3D_EXPERIMENT == 3
 extern "C" int f3d_attn_prof(unsigned long long* out24_host, int reset) {
     cudaMemcpyFromSymbol(out24_host, g_attn_prof, sizeof(g_attn_prof));
