@@ -44,7 +44,7 @@
 // per softmax warp of CTA 0: clock at S ready, exp start, exp end of its first 96 tiles
 __device__ long long g_attn_trace[16][96][3];
 // per softmax warp of CTA 0 and item: next_item returned, final pv wait start, epilogue start, end
-__device__ long long g_attn_trace2[16][16][4];
+__device__ long long g_attn_trace2[16][16][8];
 #endif
 #if F3D_EXPERIMENT == 3
 __device__ unsigned long long g_attn_prof[24];
@@ -901,10 +901,17 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                 asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * CS) : "memory");
                 lsum = l + xg[(2 * CS + (hh ^ 1)) * 32 + lane];
             }
-            const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+#if F3D_EXPERIMENT == 4
+            if (blockIdx.x == 0 && lane == 0 && titem < 16) g_attn_trace2[warp][titem][4] = clock64();
+#endif
+            float inv = 0.f;                              // MUFU reciprocal (<= 1 ulp)
+            if (lsum > 0.f) asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(lsum));
             const int vr = it.q0 + g * kBM + r;
             const bool live_row = vr < it.m;
             const int pr = live_row ? phys_row_rec(A, rec, it, vr) : 0;
+#if F3D_EXPERIMENT == 4
+            if (blockIdx.x == 0 && lane == 0 && titem < 16) g_attn_trace2[warp][titem][5] = clock64();
+#endif
             // P = exp2(s * scale_log2 - lse) recomputes this row's softmax
             if (A.lse && live_row && hh == 0)
                 A.lse[(int64_t)pr * A.ld_lse + it.h] = lsum > 0.f ? ms + __log2f(lsum) : -INFINITY;
@@ -958,6 +965,9 @@ __global__ void __launch_bounds__(threads_for<DH>(), ctas_per_sm<DH>())
                     }
                 }
             }
+#if F3D_EXPERIMENT == 4
+            if (blockIdx.x == 0 && lane == 0 && titem < 16) g_attn_trace2[warp][titem][6] = clock64();
+#endif
             tc_fence_before();
             mbar_arrive(o_free + g);
             tg += it.nt;
@@ -1023,6 +1033,7 @@ int launch(Args A, int64_t n_rows, cudaStream_t st) {
                           t == 0 ? 64 : C::kBN))
                 A.use_tma = 0;
         }
+
     const int total = A.nwork * A.H;
     const int grid = std::max(1, std::min(total, f3d_num_sms() * ctas_per_sm<DH>()));
     F3D_CUDA_TRY(f3d_launch(kern, dim3(grid), dim3(threads_for<DH>()), C::kSmem, st, A, M));

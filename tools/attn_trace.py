@@ -22,11 +22,11 @@ if __name__ == "__main__":
     AB.main()
     torch.cuda.synchronize()
     lib = L.load()
-    buf = (ctypes.c_longlong * (16 * 96 * 3 + 16 * 16 * 4))()
+    buf = (ctypes.c_longlong * (16 * 96 * 3 + 16 * 16 * 8))()
     lib.f3d_attn_trace(buf)
     arr = np.array(buf, dtype=np.int64)
     tr = arr[:16 * 96 * 3].reshape(16, 96, 3)
-    it = arr[16 * 96 * 3:].reshape(16, 16, 4)
+    it = arr[16 * 96 * 3:].reshape(16, 16, 8)
     t0 = tr[4:, 0, 0][tr[4:, 0, 0] > 0].min()
     overlap, tot = 0, 0
     for q in range(4):
@@ -51,11 +51,13 @@ if __name__ == "__main__":
                         if b[0] == 0:
                             continue
                         overlap += max(0, min(a[1], b[1]) - max(a[0], b[0]))
-    print("items (warp 4, 8, 12): item start / final-PV wait start / epilogue start / end")
+    print("items (warp 4, 8, 12): item start / final-PV wait start / epilogue start / end"
+          " / O loaded / row mapped / stored")
     for w in (4, 8, 12):
         for i in range(6):
             if it[w, i, 0]:
-                print(f"  w{w} item {i}: " + " ".join(f"{v - t0:7d}" for v in it[w, i]))
+                print(f"  w{w} item {i}: " + " ".join(f"{v - t0:7d}" for v in it[w, i][[0, 1, 2, 3]]) + "  |"
+                      + " ".join(f"{v - it[w, i, 2]:6d}" for v in it[w, i][[4, 5, 6]]))
     print("exp-window overlap fraction (pairs of warps on one sub-partition): %.2f" % (overlap / max(tot, 1)))
     ex = tr[4:, :, 2] - tr[4:, :, 1]
     per = tr[4:, 1:, 0] - tr[4:, :-1, 0]
