@@ -42,10 +42,11 @@ def main(rep, out):
                       "-c 4 python tools/prof_step.py (one config-B graph-replayed step; report " + rep + ")",
            "launches": launches,
            "traffic_bytes_per_launch": int(tb),
-           "algorithmic_bytes_per_launch": 57600000,
-           "note": "algorithmic = Q/K/V in + O out, (3+1)*d*2 B per row (d=96) for the 100K-row stage-0 "
-                   "launches; traffic averaged over the step's 4 launches (stage 1 has 50K rows); O writes "
-                   "may stay in L2 during the kernel"}
+           "algorithmic_bytes_per_launch": 43200000,
+           "note": "algorithmic = Q/K/V in + O out, (3+1)*d*2 B per row (d=96): 57.6 MB for the two "
+                   "100K-row stage-0 launches, 28.8 MB for the two 50K-row stage-1 launches, averaged "
+                   "like the traffic over the step's 4 launches; O writes may stay in L2 during the "
+                   "kernel"}
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res))
