@@ -70,6 +70,26 @@ def test_attention_random_scopes_vs_oracle(d, H):
         assert rel(out, ref) < ATT_TOL, (d, H, m, rel(out, ref))
 
 
+@pytest.mark.parametrize("nseg", [8, 9, 13])
+@pytest.mark.parametrize("d,H", [(96, 4), (64, 2), (512, 4)])
+def test_attention_many_segment_scope(nseg, d, H):
+    """A scope made of many disjoint row ranges: the kernel keeps up to 8
+    segments per item in its shared-memory item record and maps rows of
+    longer scopes through the global segment arrays."""
+    r = np.random.default_rng(nseg * 31 + d)
+    lens = r.integers(1, 160, size=nseg)
+    lens[nseg // 2] = 1                      # a one-row segment
+    ranges, at = [], 5
+    for ln in lens:
+        ranges.append((at, at + int(ln)))
+        at += int(ln) + int(r.integers(1, 30))
+    N = at + 7
+    Q, K, V = (r.normal(size=(N, d)) for _ in range(3))
+    out = F.tiled_attention(Q, K, V, F.AttentionParams(d, H), ranges=ranges)
+    ref = O.attention_ranges(Q, K, V, H, ranges)
+    assert rel(out, ref) < ATT_TOL, (nseg, d, H, rel(out, ref))
+
+
 def test_attention_extreme_logits_and_errors():
     r = np.random.default_rng(0)
     Q = r.normal(size=(128, 32)) * 30
