@@ -390,7 +390,7 @@ __device__ void slot_base(const Params& P_, int nslots, int32_t* s_base, bool wr
 // --------------------------------------------------------------- the kernel
 
 template <int PL, bool FUSED>
-__global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
+__global__ void __launch_bounds__(kThreads, FUSED ? 2 : 4) psh_kernel(const Params P_) {
     constexpr int kPerLane = TileC<PL>::kPerLane;
     constexpr int kWarpSpan = TileC<PL>::kWarpSpan;
     constexpr int kTile = TileC<PL>::kTile;
@@ -554,6 +554,14 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
     int32_t* Tn = P_.T1;
     int sweep = 0;
     bool fallback = false;
+    // Sweep 0 with at most one tile per CTA: phase A ranks its keys within
+    // each warp while counting them (warp_rank instead of warp_count) and
+    // keeps keys and ranks in registers, and the per-warp rows stay in shared
+    // memory; when sweep 0 is final, phase C only turns the rows into
+    // cross-warp prefixes -- no second read of D, count and rank pass.
+    const bool one_tile = ntiles <= (int)gridDim.x;
+    // key | (in-warp rank << 16), -1 for no point (keys < 2^14, ranks < 2^11)
+    uint32_t kra[kPerLane];
     for (;;) {
         // Phase A: decide + per-tile histogram
         int changed = 0;
@@ -618,7 +626,15 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
                 }
                 key[j] = k;
             }
-            warp_count(key, myrow);
+            if (sweep == 0 && one_tile) {
+                int rank[kPerLane];
+                warp_rank(key, myrow, rank);
+#pragma unroll
+                for (int j = 0; j < kPerLane; ++j)
+                    kra[j] = key[j] < 0 ? 0xFFFFFFFFu : (uint32_t)key[j] | ((uint32_t)rank[j] << 16);
+            } else {
+                warp_count(key, myrow);
+            }
             __syncthreads();
             store_tile_hist(sh, stride, W, P_.hist + (int64_t)t * W);
             __syncthreads();
@@ -673,6 +689,29 @@ __global__ void __launch_bounds__(kThreads) psh_kernel(const Params P_) {
             if (final_c) slot_base(P_, nslots, s_base, blockIdx.x == 0);
         }
         // Phase C: in-tile stable ranks -> offsets; S-th taker -> T
+        if (final_c && one_tile) {
+            const int t = blockIdx.x;
+            if (t < ntiles) {
+                const TileInfo ti = tile_info<kTile>(P_, multi, t, n);
+                warp_prefix_rows(sh, stride, W);       // phase A's per-warp counts
+                __syncthreads();
+                const int32_t* hrow = P_.hist + (int64_t)t * W;
+#pragma unroll
+                for (int j = 0; j < kPerLane; ++j) {
+                    const int p = ti.p0 + warp * kWarpSpan + j * 32 + lane;
+                    if (kra[j] != 0xFFFFFFFFu) {
+                        const int k = (int)(kra[j] & 0xFFFFu);
+                        const int o = __ldcg(hrow + k) + myrow[k] + (int)(kra[j] >> 16);
+                        const int i = multi ? __ldcg(P_.orig + p) : p;
+                        P_.bucket_id[i] = k;
+                        P_.bucket_offset[i] = o;
+                        P_.dest[i] = s_base[ti.b * W + k] + o;
+                    }
+                }
+            }
+            converged0 = true;
+            break;
+        }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const TileInfo ti = tile_info<kTile>(P_, multi, t, n);
             zero_hist(sh, hwords);
