@@ -82,6 +82,22 @@ __host__ __device__ __forceinline__ uint32_t spread3_10(uint32_t a) {
     return a;
 }
 
+// floor(RN(RN(c - o) / vs)) -- numpy's floor((c - o) / voxel) -- with the
+// division off the common path: q = RN(x * RN(1/vs)) lies within 1.5 ulp of the
+// rounded quotient, so when q's fractional part is farther than 2^-40 (|q| + 1)
+// from 0 and 1, the rounded quotient has the same floor as q; otherwise (a
+// quotient within ~1e-12 of an integer, |q| >= 2^52, non-finite) the exact
+// IEEE division decides.  inv = __drcp_rn(vs), once per thread.
+__device__ __forceinline__ long long vox_floor_inv(double c, double o, double vs, double inv) {
+    const double x = __dsub_rn(c, o);
+    const double q = __dmul_rn(x, inv);
+    const double f = floor(q);
+    const double fr = __dsub_rn(q, f);
+    const double tol = __fma_rn(fabs(q), 0x1p-40, 0x1p-40);
+    if (fr > tol && fr < 1.0 - tol) return (long long)f;
+    return (long long)floor(__ddiv_rn(x, vs));
+}
+
 // Division by a run-time constant d in [1, 2^31) for dividends n < 2^31:
 // q = umulhi(n, m) >> s with m = ceil(2^(31+L) / d), s = L - 1, L = ceil(log2 d)
 // (the round-up method; exact for every n < 2^31), d = 1 handled as m = 0.

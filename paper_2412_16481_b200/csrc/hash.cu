@@ -18,9 +18,10 @@ struct Origin {
     double o[3];
 };
 
-// floor((c - o) / vs) with no contraction: __dsub_rn then __ddiv_rn.
-__device__ __forceinline__ long long vox1(double c, double o, double vs) {
-    return (long long)floor(__ddiv_rn(__dsub_rn(c, o), vs));
+// floor((c - o) / vs) with no contraction: __dsub_rn then the rounded
+// division (vox_floor_inv: reciprocal multiply, exact division near integers).
+__device__ __forceinline__ long long vox1(double c, double o, double vs, double inv) {
+    return vox_floor_inv(c, o, vs, inv);
 }
 
 __device__ __forceinline__ void warp_min_max_atomic(long long v, long long* mn, long long* mx) {
@@ -103,8 +104,9 @@ __global__ void voxelize_kernel(const double* __restrict__ coords, int64_t n, Or
                                 double vs, int64_t* __restrict__ out) {
     const int64_t pt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one point per thread
     if (pt >= n) return;
+    const double inv = __drcp_rn(vs);
 #pragma unroll
-    for (int a = 0; a < 3; ++a) out[3 * pt + a] = vox1(coords[3 * pt + a], org.o[a], vs);
+    for (int a = 0; a < 3; ++a) out[3 * pt + a] = vox1(coords[3 * pt + a], org.o[a], vs, inv);
 }
 
 // per-(batch, axis) minimum; batch == null means one batch.  Grid-stride
@@ -238,6 +240,7 @@ __global__ void fused_min_kernel(const double* __restrict__ coords,
     f3d::pdl_wait();
     const int64_t nn = dyn_n(n, n_dev);
     const bool single = !batch || nbatch == 1;
+    const double inv = __drcp_rn(vs);
     long long acc[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
     const int64_t step = (int64_t)gridDim.x * blockDim.x;
     const int64_t n_it = (nn + step - 1) / step * step;    // warp-uniform trip count
@@ -246,7 +249,7 @@ __global__ void fused_min_kernel(const double* __restrict__ coords,
         long long v[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
         int b = 0;
         if (ok) {
-            for (int a = 0; a < 3; ++a) v[a] = vox1(coords[3 * i + a], org.o[a], vs);
+            for (int a = 0; a < 3; ++a) v[a] = vox1(coords[3 * i + a], org.o[a], vs, inv);
             if (batch) b = batch[i];
         }
         if (single) {
@@ -272,12 +275,13 @@ __global__ void fused_hash_kernel(const double* __restrict__ coords,
     f3d::pdl_wait();
     const int64_t nn = dyn_n(n, n_dev);
     long long acc[7] = F3D_STATS_INIT;
+    const double inv = __drcp_rn(vs);
     const int64_t step = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += step) {
         int b = (batch && nbatch > 1) ? batch[i] : 0;
         if (b < 0 || b >= nbatch) b = 0;
         long long v[3];
-        for (int a = 0; a < 3; ++a) v[a] = vox1(coords[3 * i + a], org.o[a], vs) - ws_min[3 * b + a];
+        for (int a = 0; a < 3; ++a) v[a] = vox1(coords[3 * i + a], org.o[a], vs, inv) - ws_min[3 * b + a];
         hash_one(v[0], v[1], v[2], i, ha, home, vox32, true, acc);
     }
     flush_stats(acc, ha, stats);

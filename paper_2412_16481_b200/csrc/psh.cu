@@ -108,7 +108,7 @@ struct GridBar {
 // floor((c - o) / vs) with no contraction: __dsub_rn then __ddiv_rn
 // (bw/geometry.py:69-72; the same arithmetic as csrc/hash.cu)
 __device__ __forceinline__ long long vox_floor(double c, double o, double vs) {
-    return (long long)floor(__ddiv_rn(__dsub_rn(c, o), vs));
+    return vox_floor_inv(c, o, vs, __drcp_rn(vs));
 }
 
 // Block-wide min (kMin) / max of 64-bit values into out[] (thread 0 writes).

@@ -286,3 +286,45 @@ def test_device_tensors_stay_on_device():
     f = torch.randn(5000, 96, device="cuda", dtype=torch.bfloat16)
     s, perm = F.scatter(f, a)
     assert s.is_cuda and torch.equal(s[perm], f)
+
+
+def _boundary_cloud(vs, org, n=60_000, seed=0):
+    """Coordinates on and next to voxel boundaries: c = o + k*vs, and the
+    neighbouring doubles, so (c - o) / vs rounds onto or next to an integer."""
+    r = np.random.default_rng(seed)
+    k = r.integers(-3000, 3000, size=(n, 3)).astype(np.float64)
+    c = np.asarray(org)[None, :] + k * vs
+    step = r.integers(-2, 3, size=(n, 3))
+    for s in (-2, -1, 1, 2):
+        m = step == s
+        c[m] = np.nextafter(c[m], np.inf if s > 0 else -np.inf)
+        if abs(s) == 2:
+            c[m] = np.nextafter(c[m], np.inf if s > 0 else -np.inf)
+    c[::7] = r.uniform(-60, 60, size=c[::7].shape)          # plus generic points
+    return c
+
+
+@pytest.mark.parametrize("vs,org", [(1 / 128, (0.0, 0.0, 0.0)), (0.02, (0.1, -0.3, 7.25)),
+                                    (0.05, (0.0, 0.0, 0.0)), (1 / 3, (1e-3, 2.0, -5.0)),
+                                    (0.1, (-12.7, 3.3, 0.0))])
+def test_voxelize_boundaries_exact(vs, org):
+    """floor((c - o) / vs) with numpy's rounded division, exactly, where the
+    quotient lands on or next to an integer (the kernels multiply by the
+    reciprocal and fall back to the IEEE division near integers): the plain
+    voxelize and the fused voxel-hash pass (remapped voxels)."""
+    import torch
+    from paper_2412_16481_b200 import _lib as L
+    c = _boundary_cloud(vs, org, seed=int(vs * 1e4))
+    want = np.floor((c - np.asarray(org)[None, :]) / vs).astype(np.int64)
+    got = F.voxelize(F.PointCloud(c), F.VoxelGrid(vs, org))
+    np.testing.assert_array_equal(got, want)
+    n = c.shape[0]
+    cd = torch.tensor(c, device="cuda")
+    vox32 = torch.empty((n, 3), dtype=torch.int32, device="cuda")
+    home = torch.empty(n, dtype=torch.int32, device="cuda")
+    stats = torch.empty(8, dtype=torch.int64, device="cuda")
+    ws = torch.empty(8, dtype=torch.int64, device="cuda")
+    o3 = (L._F64 * 3)(*org)
+    L.call("f3d_voxel_hash", L.ptr(cd), None, n, 1, o3, float(vs), 3, 256, 1024, 21,
+           L.ptr(vox32), L.ptr(home), L.ptr(stats), L.ptr(ws), None, L.stream())
+    np.testing.assert_array_equal(vox32.cpu().numpy().astype(np.int64), want - want.min(axis=0))
