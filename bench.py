@@ -566,7 +566,7 @@ def main():
         p1.record(cs)
         torch.cuda.synchronize()
         slot = bb._slots[0]
-        d2h = int(slot["out_bf16"].numel() * 2 + slot["status"].numel() * 8)
+        d2h = int(slot["out_bf16"].numel() * 2 + slot["status"].numel() * slot["status"].element_size())
         return max_over_ranks(p0.elapsed_time(p1) / args.steps), rows_seen, d2h
 
     e2e_ms_max, rows_seen, d2h_bytes = pipelined(X_h32)

@@ -25,7 +25,7 @@ from torch.profiler import record_function
 
 from . import _lib as L
 from .attention import DeviceRoundPlan, qstep_for
-from .bucketing import (DEFAULT_MAX_SWEEPS, BucketAssignment, _run_psh,
+from .bucketing import (DEFAULT_MAX_SWEEPS, BucketAssignment, _run_psh, _zero_batch_ids,
                         default_probe_schedule)
 from .errors import ConfigError
 from .hashing import HashConfig, raise_range
@@ -165,6 +165,7 @@ class Backbone:
                    L.ptr(counts), L.ptr(base), L.ptr(dest), L.ptr(info), L.ptr(stats), L.ptr(ws),
                    ws_bytes, L.ptr(n_dev), L.stream())
             a = BucketAssignment(ids, offs, counts, base, cfg.S, cfg.K,
+                                 batch_id=_zero_batch_ids(n, ids.device),
                                  _dev={"id": ids, "off": offs, "counts": counts, "base": base,
                                        "batch": None, "dest": dest, "info": info})
             return a, stats, info
@@ -179,6 +180,7 @@ class Backbone:
         ids, offs, counts, base, dest, info = _run_psh(vox32, home, None, 1, n, hc, cfg.S,
                                                        default_probe_schedule(), n_dev=n_dev)
         a = BucketAssignment(ids, offs, counts, base, cfg.S, cfg.K,
+                             batch_id=_zero_batch_ids(n, ids.device),
                              _dev={"id": ids, "off": offs, "counts": counts, "base": base,
                                    "batch": None, "dest": dest, "info": info})
         return a, stats, info
@@ -366,14 +368,16 @@ class Backbone:
 
     # ------------------------------------------------------------ checks
     @staticmethod
-    def _status_vector(runs, n_dev):
-        """One int64 device vector holding every error word and the final
+    def _status_vector(runs, n_dev, zero1=None):
+        """One int32 device vector holding every error word and the final
         row count, so the host reads it with a single copy.  Layout: the
-        7 int64 hash stats of every stage, then per stage the int32 words
-        [PSH info (4), planner status of each round, pool flags], then the
-        row count.  Built with three launches (int32 cat, widen, cat)."""
+        7 int64 hash stats of every stage (as int32 pairs), then per stage
+        the int32 words [PSH info (4), planner status of each round, pool
+        flags], then the row count.  One concatenation kernel (zero1: a
+        preallocated int32 zero for unpooled stages, so a captured graph
+        holds no fill node)."""
         dev = runs[0].stats.device
-        w32 = []
+        w32 = [r.stats.view(torch.int32) for r in runs]
         for r in runs:
             w32.append(r.info)
             p0 = r.plans[0]
@@ -381,19 +385,22 @@ class Backbone:
                    if len(r.plans) > 1 else 1)
             w32.append(p0.live.as_strided((len(r.plans),), (per,), p0.live.storage_offset() + 3))
             w32.append(r.pool_flags if hasattr(r, "pool_flags")
+                       else zero1 if zero1 is not None
                        else torch.zeros(1, dtype=torch.int32, device=dev))
         w32.append(n_dev if n_dev is not None
                    else torch.full((1,), runs[-1].n_cap, dtype=torch.int32, device=dev))
-        return torch.cat([r.stats for r in runs] + [torch.cat(w32).to(torch.int64)])
+        return torch.cat(w32)
 
     def _check(self, status_h, runs):
         """Raise the reference exceptions from the status words (same
         conditions and messages as bw/hashing.py:60-75, bw/attention.py:104,
         bw/pooling.py validate); returns the final row count."""
-        o = 7 * len(runs)
+        nr = len(runs)
+        s64 = np.ascontiguousarray(status_h[:14 * nr]).view(np.int64)
+        o = 14 * nr
         for si, r in enumerate(runs):
             cfg = r.cfg
-            stats, info = status_h[7 * si:7 * si + 7], status_h[o:o + 4]
+            stats, info = s64[7 * si:7 * si + 7], status_h[o:o + 4]
             o += 4
             live3 = status_h[o:o + cfg.rounds]
             o += cfg.rounds
@@ -462,6 +469,7 @@ class Backbone:
         # still being read back by the host stream when stream_host replays the
         # slot's next g0, must not share memory with g0's scratch
         g0, g1 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        zero1 = torch.zeros(1, dtype=torch.int32, device=dev)   # outside the capture
         pool0 = torch.cuda.graph_pool_handle()
         pool1 = torch.cuda.graph_pool_handle() if SEPARATE_POOLS else pool0
         with torch.cuda.graph(g0, pool=pool0):
@@ -472,13 +480,14 @@ class Backbone:
                 X, Cn, n_dev, runs = self._enqueue_rest(r0, coords, feats)
             finally:
                 self._want_out_bf16 = False
-            status = self._status_vector(runs, n_dev)
+            status = self._status_vector(runs, n_dev, zero1)
             out_bf16 = runs[-1].out_bf16 if runs[-1].out_bf16 is not None \
                 else X.to(torch.bfloat16)
         return {"n": n, "g0": g0, "g1": g1, "X": X, "C": Cn, "runs": runs, "status": status,
                 "out_bf16": out_bf16, "side": torch.cuda.Stream(), "coords": coords,
                 "feats": feats,
-                "status_h": torch.empty(status.shape, dtype=torch.int64).pin_memory(),
+                "zero1": zero1,
+                "status_h": torch.empty(status.shape, dtype=status.dtype).pin_memory(),
                 "out_h": torch.empty(out_bf16.shape, dtype=out_bf16.dtype).pin_memory()}
 
     def capture(self, n, feat_dtype=torch.bfloat16):

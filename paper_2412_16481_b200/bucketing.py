@@ -27,6 +27,21 @@ DEFAULT_MAX_PROBES = 32
 DEFAULT_MAX_SWEEPS = 128
 
 
+_ZERO_BATCH = {}
+
+
+def _zero_batch_ids(n, device):
+    """Single-batch ids for the backbone's internal assignments: one cached
+    int64 zero vector per (size, device), so an assignment built inside a
+    captured graph adds no fill kernel (the backbone never writes it; public
+    assignments keep a private zeros tensor)."""
+    key = (int(n), str(device))
+    z = _ZERO_BATCH.get(key)
+    if z is None:
+        z = _ZERO_BATCH[key] = torch.zeros(int(n), dtype=torch.int64, device=device)
+    return z
+
+
 @dataclass(frozen=True)
 class ProbeSchedule:
     """Probe offsets, nearest shell first (bw/bucketing.py:28-48)."""
