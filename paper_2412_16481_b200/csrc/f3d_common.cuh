@@ -188,36 +188,21 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
     return d;
 }
 
-#ifndef F3D_GELU_NEWTON
-#define F3D_GELU_NEWTON 0
-#endif
 // GELU, exact-erf form (bw/stage.py:91-92), on a packed pair: erf via
 // Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, below the bf16 rounding of
-// the result), MUFU rcp/ex2, the FMA/FMUL work issued as f32x2.
+// the result), MUFU rcp/ex2, the FMA/FMUL work issued as f32x2.  Written as
+//   GELU(x) = 0.5 (x + |x|) + 0.5 |x| (erf(|x|/sqrt2) - 1)
+// (x erf(x/sqrt2) = |x| erf(|x|/sqrt2)): no sign transfer, and for x < 0 the
+// result is a single product (0.5 (x + |x|) = 0 exactly) instead of the
+// difference 1 - erf of two numbers near 1.
 __device__ __forceinline__ float2 gelu2(float x0, float x1) {
-    const uint64_t x = f2(x0, x1);
-    const uint64_t z = fmul2(f2(fabsf(x0), fabsf(x1)), f2(0.70710678118654752f, 0.70710678118654752f));
-#if F3D_GELU_NEWTON
-    // 1 / (1 + p z) on the FMA pipe: z clamped to 9 (erf = 1 beyond), the
-    // denominator lies in [1, 3.95]; bit-trick seed (< 12.5 % error) and
-    // three Newton steps (error < 1e-7), leaving MUFU to the exponential
-    const uint64_t zc = f2(fminf(fabsf(x0) * 0.70710678118654752f, 9.f),
-                           fminf(fabsf(x1) * 0.70710678118654752f, 9.f));
-    const uint64_t den = ffma2(f2(0.3275911f, 0.3275911f), zc, f2(1.f, 1.f));
-    float d0, d1;
-    f2_split(den, d0, d1);
-    uint64_t t = f2(__int_as_float(0x7EF311C3 - __float_as_int(d0)),
-                    __int_as_float(0x7EF311C3 - __float_as_int(d1)));
-    const uint64_t nden = f2(-d0, -d1);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) t = ffma2(t, ffma2(nden, t, f2(1.f, 1.f)), t);
-#else
+    const uint64_t ax = f2(fabsf(x0), fabsf(x1));
+    const uint64_t z = fmul2(ax, f2(0.70710678118654752f, 0.70710678118654752f));
     float d0, d1, t0, t1;
     f2_split(ffma2(f2(0.3275911f, 0.3275911f), z, f2(1.f, 1.f)), d0, d1);
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t0) : "f"(d0));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t1) : "f"(d1));
     const uint64_t t = f2(t0, t1);
-#endif
     // pn = -(a1 t + ... + a5 t^5)
     uint64_t pn = ffma2(f2(-1.061405429f, -1.061405429f), t, f2(1.453152027f, 1.453152027f));
     pn = ffma2(pn, t, f2(-1.421413741f, -1.421413741f));
@@ -228,11 +213,11 @@ __device__ __forceinline__ float2 gelu2(float x0, float x1) {
     f2_split(fmul2(fmul2(z, z), f2(-1.4426950408889634f, -1.4426950408889634f)), a0, a1);
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(a0));
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(a1));
-    float r0, r1;   // erf(|x|/sqrt2) = 1 - pl * e^{-z^2}
-    f2_split(ffma2(pn, f2(e0, e1), f2(1.f, 1.f)), r0, r1);
-    const uint64_t phi2 = fadd2(f2(1.f, 1.f), f2(copysignf(r0, x0), copysignf(r1, x1)));
+    const uint64_t rneg = fmul2(pn, f2(e0, e1));          // erf(|x|/sqrt2) - 1
+    const uint64_t h = fmul2(ax, f2(0.5f, 0.5f));
+    const uint64_t base = ffma2(f2(0.5f, 0.5f), f2(x0, x1), h);   // 0.5 (x + |x|)
     float o0, o1;
-    f2_split(fmul2(fmul2(f2(0.5f, 0.5f), x), phi2), o0, o1);
+    f2_split(ffma2(h, rneg, base), o0, o1);
     return make_float2(o0, o1);
 }
 
