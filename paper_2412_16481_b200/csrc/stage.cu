@@ -549,6 +549,174 @@ __global__ void __launch_bounds__(kThreads, 3) row_ln8_kernel(
     }
 }
 
+// ---- 8 lanes per row with the positional encoding (d == 96: the only width
+// with d % 6 == 0 and d % 32 == 0 up to 128).  Lane gl of a row group owns the
+// 16-byte chunks gl, gl + 8, gl + 16; chunk gl + 8k holds the (sin, cos) pairs
+// of axis k at frequencies 2gl and 2gl + 1.  The per-element arithmetic is
+// row_ln_vec's (angles, affine, PE add); the row statistics are ln8_stats'.
+// row_ln8pe (residual + LN1 + PE of the next round) and scatter_ln8pe (input
+// scatter + first LN1 + PE) share it, so the fused scatter stays bit-identical
+// to scatter + row_ln.
+struct Pe8 {
+    float fq[2];
+    double plo[3];
+    float pinv[3];
+};
+__device__ __forceinline__ Pe8 pe8_consts(int gl, const double* __restrict__ lo_ext, float pl2) {
+    Pe8 c;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) c.fq[p] = exp2f(-(float)(2 * gl + p) / 16.f * pl2);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        c.plo[a] = lo_ext ? lo_ext[a] : 0.0;
+        c.pinv[a] = lo_ext ? (float)(1.0 / lo_ext[3 + a]) : 1.f;
+    }
+    return c;
+}
+
+// LN(v) * gain + beta + PE(coords of the row) -> bf16 at out_row (d == 96)
+__device__ __forceinline__ void ln8pe_out(const float4 (&v)[3], float2 st, int gl,
+                                          const float* __restrict__ gain,
+                                          const float* __restrict__ beta, const Pe8& pc,
+                                          const double* __restrict__ crow,
+                                          __nv_bfloat16* __restrict__ out_row) {
+    const float m = st.x, rstd = st.y;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int c = 4 * (gl + 8 * k);
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(gain + c));
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(beta + c));
+        float o0 = (v[k].x - m) * rstd * gg.x + bb.x;
+        float o1 = (v[k].y - m) * rstd * gg.y + bb.y;
+        float o2 = (v[k].z - m) * rstd * gg.z + bb.z;
+        float o3 = (v[k].w - m) * rstd * gg.w + bb.w;
+        const float xn = (float)__dsub_rn(crow[k], pc.plo[k]) * pc.pinv[k];
+        float sn[2], cs[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) __sincosf(xn * pc.fq[p], &sn[p], &cs[p]);
+        o0 += sn[0];
+        o1 += cs[0];
+        o2 += sn[1];
+        o3 += cs[1];
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(o0, o1), h1 = __floats2bfloat162_rn(o2, o3);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(out_row + c) = w;
+    }
+}
+
+constexpr int kRB8pe = 2;   // row batches per warp of the PE kernels (8 rows per warp)
+
+template <bool HAS_Y>
+__global__ void __launch_bounds__(kThreads, 3) row_ln8pe_kernel(
+    float* __restrict__ F, int64_t ldf, const __nv_bfloat16* __restrict__ y, int64_t ldy,
+    const float* __restrict__ ybias, const float* __restrict__ gain,
+    const float* __restrict__ beta, const double* __restrict__ pec,
+    const double* __restrict__ lo_ext, float pl2, __nv_bfloat16* __restrict__ out, int64_t ldo,
+    int64_t n, float eps) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const int64_t rw = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * (4 * kRB8pe);
+    if (rw >= n) return;
+    float4 v[kRB8pe][3];
+#pragma unroll
+    for (int b = 0; b < kRB8pe; ++b) {
+        const int64_t row = rw + 4 * b + grp;
+        const bool ok = row < n;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            v[b][k] = ok ? *reinterpret_cast<const float4*>(F + row * ldf + 4 * (gl + 8 * k))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (HAS_Y) {
+        uint2 yy[kRB8pe][3];
+#pragma unroll
+        for (int b = 0; b < kRB8pe; ++b) {
+            const int64_t row = rw + 4 * b + grp;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                yy[b][k] = row < n ? *reinterpret_cast<const uint2*>(y + row * ldy + 4 * (gl + 8 * k))
+                                   : make_uint2(0, 0);
+        }
+#pragma unroll
+        for (int b = 0; b < kRB8pe; ++b) {
+            const int64_t row = rw + 4 * b + grp;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int c = 4 * (gl + 8 * k);
+                const float4 yb = ybias ? *reinterpret_cast<const float4*>(ybias + c)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&yy[b][k]);
+                const float2 y01 = __bfloat1622float2(h[0]), y23 = __bfloat1622float2(h[1]);
+                v[b][k].x += y01.x + yb.x;
+                v[b][k].y += y01.y + yb.y;
+                v[b][k].z += y23.x + yb.z;
+                v[b][k].w += y23.y + yb.w;
+                if (row < n) *reinterpret_cast<float4*>(F + row * ldf + c) = v[b][k];
+            }
+        }
+    }
+    const Pe8 pc = pe8_consts(gl, lo_ext, pl2);
+#pragma unroll
+    for (int b = 0; b < kRB8pe; ++b) {
+        const float2 st = ln8_stats<3>(v[b], 1.f / 96.f, eps);
+        const int64_t row = rw + 4 * b + grp;
+        if (row < n) ln8pe_out(v[b], st, gl, gain, beta, pc, pec + 3 * row, out + row * ldo);
+    }
+}
+
+template <typename ST>
+__global__ void __launch_bounds__(kThreads, 3) scatter_ln8pe_kernel(
+    const ST* __restrict__ src, int64_t lds, const int32_t* __restrict__ dest,
+    const double* __restrict__ C, const double* __restrict__ lo_ext, float pl2,
+    const float* __restrict__ gain, const float* __restrict__ beta, float* __restrict__ F,
+    int64_t ldf, __nv_bfloat16* __restrict__ out, int64_t ldo, int64_t n,
+    const int32_t* __restrict__ n_dev, float eps) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const int64_t nn = dyn_n(n, n_dev);
+    const int64_t rw = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * (4 * kRB8pe);
+    if (rw >= nn) return;
+    float4 v[kRB8pe][3];
+#pragma unroll
+    for (int b = 0; b < kRB8pe; ++b) {
+        const int64_t row = rw + 4 * b + grp;
+        const bool ok = row < nn;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int c = 4 * (gl + 8 * k);
+            if (sizeof(ST) == 2) {
+                if (ok) {
+                    const uint2 w = *reinterpret_cast<const uint2*>(
+                        reinterpret_cast<const __nv_bfloat16*>(src) + row * lds + c);
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+                    const float2 a = __bfloat1622float2(h[0]), bq = __bfloat1622float2(h[1]);
+                    v[b][k] = make_float4(a.x, a.y, bq.x, bq.y);
+                } else {
+                    v[b][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            } else {
+                v[b][k] = ok ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src) +
+                                                               row * lds + c)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    }
+    const Pe8 pc = pe8_consts(gl, lo_ext, pl2);
+#pragma unroll
+    for (int b = 0; b < kRB8pe; ++b) {
+        const float2 st = ln8_stats<3>(v[b], 1.f / 96.f, eps);
+        const int64_t row = rw + 4 * b + grp;
+        if (row >= nn) continue;
+        const int64_t dr = __ldg(dest + row);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            *reinterpret_cast<float4*>(F + dr * ldf + 4 * (gl + 8 * k)) = v[b][k];
+        ln8pe_out(v[b], st, gl, gain, beta, pc, C + 3 * row, out + dr * ldo);
+    }
+}
+
 // Scatter + first LayerNorm + PE of a stage in one pass: input row i (bf16 or
 // fp32, input order) -> F[dest[i]] (fp32) and x[dest[i]] = LN(F)*g + b + PE(C[i])
 // (bf16), with row_ln_vec_kernel's arithmetic (so bit-identical to the scatter
@@ -701,6 +869,21 @@ static bool launch_row_ln_vec(cudaStream_t st, void* F, int64_t ldf, const void*
     // 100K rows); the PE variants keep 32 lanes (their 8-lane form needs 118
     // registers and measured slower, 21.3 vs 18.8 us)
     static const bool ln8 = !getenv("F3D_LN8") || getenv("F3D_LN8")[0] != '0';
+    // LN1 + PE at d == 96: 8 lanes per row as well (row_ln8pe; F3D_LN8PE=0: 32 lanes)
+    static const bool ln8pe = !getenv("F3D_LN8PE") || getenv("F3D_LN8PE")[0] != '0';
+    if (ln8pe && d == 96 && pec && out) {
+        using BF = __nv_bfloat16;
+        const unsigned g8 = (unsigned)((n + 8 * 4 * stage::kRB8pe - 1) / (8 * 4 * stage::kRB8pe));
+        if (y)
+            (void)(f3d_launch(stage::row_ln8pe_kernel<true>, dim3(g8), dim3(stage::kThreads), 0,
+                                      st, (float*)F, ldf, (const BF*)y, ldy, ybias, gain, beta, pec,
+                                      lo_ext, pl2, (BF*)out, ldo, n, (float)eps));
+        else
+            (void)(f3d_launch(stage::row_ln8pe_kernel<false>, dim3(g8), dim3(stage::kThreads), 0,
+                                      st, (float*)F, ldf, (const BF*)y, ldy, ybias, gain, beta, pec,
+                                      lo_ext, pl2, (BF*)out, ldo, n, (float)eps));
+        return true;
+    }
     if (ln8 && d % 32 == 0 && d <= 128 && !pec) {
         using BF = __nv_bfloat16;
         const unsigned g8 = (unsigned)((n + 8 * 4 * stage::kRB8 - 1) / (8 * 4 * stage::kRB8));
@@ -880,6 +1063,22 @@ extern "C" int f3d_scatter_ln_pe(const void* src, int src_is_f32, int64_t lds,
     const unsigned g = (unsigned)((n + RPW * 8 - 1) / (RPW * 8));
     const float pl2 = (float)log2(pe_base);
     cudaStream_t st = (cudaStream_t)stream;
+    // d == 96: 8 lanes per row, the statistics of row_ln8pe (bit-identical to
+    // the scatter followed by f3d_row_ln); F3D_LN8PE=0: 32 lanes
+    static const bool ln8pe = !getenv("F3D_LN8PE") || getenv("F3D_LN8PE")[0] != '0';
+    if (ln8pe && d == 96) {
+        const unsigned g8 = (unsigned)((n + 8 * 4 * stage::kRB8pe - 1) / (8 * 4 * stage::kRB8pe));
+        if (src_is_f32)
+            F3D_CUDA_TRY(f3d_launch(stage::scatter_ln8pe_kernel<float>, dim3(g8), dim3(stage::kThreads),
+                                    0, st, (const float*)src, lds, dest, coords, lo_ext, pl2, gain,
+                                    beta, F, ldf, (__nv_bfloat16*)out_bf16, ldo, n, n_dev, (float)eps));
+        else
+            F3D_CUDA_TRY(f3d_launch(stage::scatter_ln8pe_kernel<__nv_bfloat16>, dim3(g8),
+                                    dim3(stage::kThreads), 0, st, (const __nv_bfloat16*)src, lds, dest,
+                                    coords, lo_ext, pl2, gain, beta, F, ldf, (__nv_bfloat16*)out_bf16,
+                                    ldo, n, n_dev, (float)eps));
+        return F3D_OK;
+    }
     if (src_is_f32)
         F3D_CUDA_TRY(f3d_launch(stage::scatter_ln_pe_kernel<RPW, float>, dim3(g),
                                 dim3(stage::kThreads), 0, st, (const float*)src, lds, dest, coords,
