@@ -45,6 +45,19 @@ __global__ void f3d_zero_i32_kernel(int32_t* p, int64_t n) {
         p[i] = 0;
 }
 
+// two small ranges in one launch (a cooperative kernel's barrier word and its
+// status words)
+__global__ void f3d_zero_i32x2_kernel(int32_t* p, int n, int32_t* q, int m) {
+    f3d::pdl_wait();
+    const int i = threadIdx.x;
+    if (i < n) p[i] = 0;
+    if (q && i < m) q[i] = 0;
+}
+
+cudaError_t f3d_zero_i32x2(int32_t* p, int n, int32_t* q, int m, cudaStream_t st) {
+    return f3d_launch(f3d_zero_i32x2_kernel, dim3(1), dim3(32), 0, st, p, n, q, m);
+}
+
 cudaError_t f3d_zero_i32(int32_t* p, int64_t n, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     int64_t g = (n + 255) / 256;

@@ -22,6 +22,7 @@ int f3d_num_sms();
 // copy engine and then queues behind concurrent H2D/D2H traffic (measured:
 // 40 us stalls per step in the pipelined host loop).
 cudaError_t f3d_zero_i32(int32_t* p, int64_t n, cudaStream_t st);
+cudaError_t f3d_zero_i32x2(int32_t* p, int n, int32_t* q, int m, cudaStream_t st);   // n, m <= 32
 // Programmatic dependent launch (F3D_PDL, default on): the hot-path kernels
 // are launched with programmatic stream serialisation, so a kernel's CTAs are
 // scheduled (and run their prologue: barriers, TMEM, smem set-up) while the

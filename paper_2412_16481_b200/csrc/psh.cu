@@ -929,7 +929,8 @@ namespace {
 constexpr int kMaxGrid = 4096;    // per-CTA partials reserved in the fused workspace
 
 // Launch the cooperative kernel for prepared params (p.n, p.nbatch, p.K set).
-int launch_psh(psh::Params& p, bool fused, cudaStream_t st) {
+// info4 (nullable): the caller's 4 status words, zeroed with the barrier word
+int launch_psh(psh::Params& p, bool fused, cudaStream_t st, int32_t* info4 = nullptr) {
     const int K = p.K, nbatch = p.nbatch;
     const int nbins = nbatch > 1 ? std::max(K + 1, nbatch) : K + 1;
     const bool small = p.n < psh::kSmallTileMaxN;
@@ -958,7 +959,7 @@ int launch_psh(psh::Params& p, bool fused, cudaStream_t st) {
     grid = std::max(grid, 1);
     if (fused) grid = std::min(grid, kMaxGrid);
     // a kernel, not a memset node (which may queue behind copy-engine traffic)
-    F3D_CUDA_TRY(f3d_zero_i32((int32_t*)p.bar, 1, st));
+    F3D_CUDA_TRY(f3d_zero_i32x2((int32_t*)p.bar, 1, info4, 4, st));
     void* args[] = {(void*)&p};
     F3D_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(psh::kThreads), args,
                                              smem, st));
@@ -1023,16 +1024,16 @@ extern "C" int f3d_psh_assign(const int32_t* vox32, const int32_t* home, const i
                            : psh::TileC<psh::kPerLaneLarge>::kTile;
     p.max_tiles = (int)(n / tile + nbatch + 1);
 
-    F3D_CUDA_TRY(f3d_zero_i32(info_out, 4, st));
     const int nbins = nbatch > 1 ? std::max(K + 1, nbatch) : K + 1;
     if (nbins > psh::kMaxBins) {
+        F3D_CUDA_TRY(f3d_zero_i32(info_out, 4, st));
         psh_warp_exact_kernel<<<nbatch, 32, 0, st>>>(p);
         F3D_LAUNCH_CHECK();
         psh_exact_finish_kernel<<<1, 1024, 0, st>>>(p);
         F3D_LAUNCH_CHECK();
         return F3D_OK;
     }
-    return launch_psh(p, false, st);
+    return launch_psh(p, false, st, info_out);
 }
 
 // ---------------------------------------------------------------------------
