@@ -198,9 +198,10 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
 // difference 1 - erf of two numbers near 1.
 __device__ __forceinline__ float2 gelu2(float x0, float x1) {
     const uint64_t ax = f2(fabsf(x0), fabsf(x1));
-    const uint64_t z = fmul2(ax, f2(0.70710678118654752f, 0.70710678118654752f));
+    // z = |x| / sqrt2 enters only as p z and z^2: both constants folded in
+    // (p / sqrt2 = 0.2316418883, log2(e) / 2)
     float d0, d1, t0, t1;
-    f2_split(ffma2(f2(0.3275911f, 0.3275911f), z, f2(1.f, 1.f)), d0, d1);
+    f2_split(ffma2(f2(0.23164188826636f, 0.23164188826636f), ax, f2(1.f, 1.f)), d0, d1);
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t0) : "f"(d0));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t1) : "f"(d1));
     const uint64_t t = f2(t0, t1);
@@ -211,7 +212,7 @@ __device__ __forceinline__ float2 gelu2(float x0, float x1) {
     pn = ffma2(pn, t, f2(-0.254829592f, -0.254829592f));
     pn = fmul2(pn, t);
     float a0, a1, e0, e1;
-    f2_split(fmul2(fmul2(z, z), f2(-1.4426950408889634f, -1.4426950408889634f)), a0, a1);
+    f2_split(fmul2(fmul2(ax, ax), f2(-0.7213475204444817f, -0.7213475204444817f)), a0, a1);
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(a0));
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(a1));
     const uint64_t rneg = fmul2(pn, f2(e0, e1));          // erf(|x|/sqrt2) - 1

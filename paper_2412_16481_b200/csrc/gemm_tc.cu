@@ -428,10 +428,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int e = 0; e < 16; e += 2) {
                         float2 f = make_float2(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1]));
-                        if (BIAS) {
-                            f.x += bv[e];
-                            f.y += bv[e + 1];
-                        }
+                        if (BIAS)   // one packed add per pair
+                            f2_split(fadd2(f2(f.x, f.y), f2(bv[e], bv[e + 1])), f.x, f.y);
                         if (GELU) f = gelu2(f.x, f.y);
                         __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
                         pk[e >> 1] = *reinterpret_cast<uint32_t*>(&h2);
